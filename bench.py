@@ -1,0 +1,338 @@
+"""Benchmark of the batched env-step hot path (BASELINE.json metric:
+agent-steps/s at 1/2/4/8 B200 vs the CPU reference; % of HBM roofline).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload smax3m|mpe|overcooked|smax2s3z|smax27m]
+  python bench.py --impl reference ...     # the reference's own CPU path, host cores
+
+A "step" is one fused VectorEnv step over the whole synthetic batch with the
+reference probe's random-legal action stream (vector_env.cpp:169-217): the
+default workload is BASELINE.json configs[1], SMAX 3m with 65536 envs per GPU
+(weak scaling).  Multi-GPU runs are launched with torchrun (one rank per GPU,
+NCCL); envs are sharded by contiguous global index with no collective in the
+step path, and one NCCL all-reduce aggregates the episode statistics.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+THREE_M = {"ally_units": ["marine"] * 3, "enemy_units": ["marine"] * 3}
+WORKLOADS = {
+    # name: (env_id, config, envs per GPU, label)
+    "smax3m": ("SMAX_5m_vs_6m", THREE_M, 65536, "SMAX 3m (3 marines vs 3, heuristic enemy), configs[1]"),
+    "mpe": ("MPE_simple_spread_v3", {}, 1024, "MPE simple_spread, configs[0]"),
+    "mpe_large": ("MPE_simple_spread_v3", {}, 1 << 22, "MPE simple_spread at 4M envs/GPU (roofline sweep)"),
+    "overcooked": ("overcooked_cramped_room_v0", {}, 262144, "Overcooked cramped_room, configs[2]"),
+    "smax2s3z": ("SMAX_2s3z", {}, 65536, "SMAX 2s3z, configs[3]"),
+    "smax27m": ("SMAX_27m_vs_30m", {}, 4096, "SMAX 27m_vs_30m, configs[3]"),
+}
+L2_FLUSH_BYTES = 256 << 20  # > 126 MB L2
+
+
+def algorithmic_bytes(env, n_envs, n_finished):
+    """Minimum bytes one fused step must move: state read +
+    write, carry (key, return, length) read + write, every output view, and
+    final_obs rows of the envs that finished.  fp64 state, f32 obs."""
+    A, D = env.num_agents(), env.obs_dim
+    fam = env.family
+    if fam == 0:    # MPE spread: agent pos/vel rw, landmark pos read (written on reset), steps
+        E = 6 if A == 3 else 6
+        state_rw = 2 * (2 * A * 8 + 2 * A * 8 + 4) + (2 * (E - A) * 8)
+        reset_extra = 2 * (E - A) * 8
+    elif fam == 1:  # SMAX: x,y,health,cooldown f64 + packed memory u32 per unit, t
+        U = len(env.config.get("ally_units", [])) + len(env.config.get("enemy_units", [])) or None
+        U = U or {"SMAX_2s3z": 10, "SMAX_27m_vs_30m": 57}.get(env.id(), A * 2)
+        state_rw = 2 * (U * (4 * 8 + 4) + 4)
+        reset_extra = 0
+    else:           # Overcooked: agents word, pots, counter bits, t
+        state_rw = 2 * (4 + 4 + 8 + 4)
+        reset_extra = 0
+    carry_rw = 2 * (16 + 8 + 4)
+    outputs = A * D * 4 + A * 8 + (A + 1) + A * env.n_info * 8 + 1 + 8 + 4 + A * 4
+    per_env = state_rw + carry_rw + outputs
+    return n_envs * per_env + n_finished * (A * D * 4 + reset_extra)
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                                       "-lms", "200"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except FileNotFoundError:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        self.p.wait()
+        self.f.flush()
+        rows = [r.split(",") for r in open(self.f.name).read().strip().splitlines() if r.strip()]
+        os.unlink(self.f.name)
+        sm = [float(r[1]) for r in rows if len(r) >= 9 and r[1].strip().replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if len(r) >= 9 and r[2].strip().replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows if len(r) >= 9 for i in range(4) if "Active" in r[5 + i]})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+def measured_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(workload):
+    """dram bytes per launch of the step kernel from the committed ncu --set full capture."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            return json.load(f).get(workload)
+    except Exception:
+        return None
+
+
+# --------------------------------------------------------------------- CPU arms
+def cpu_reference_probe(env_id, cfg, n_envs, steps, warmup, threads):
+    """The reference's VectorEnv::step + random_legal_actions (its own
+    throughput_probe loop, vector_env.cpp:214-217) on the host cores."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O
+    kind = "reference" if O.ref_available() else "port"
+    key = O.key_from_seed(0)
+    akeys = O.split(O.fold_in(key, 2), steps + warmup + 1)
+    if kind == "reference":
+        O.ref_lib().mref_set_threads(int(threads))
+        v = O.RefVenv(env_id, cfg, n_envs)
+        import ctypes as C
+        L = O.ref_lib()
+        v.reset(key)
+        act = np.zeros((n_envs, v.n_agents), np.int32)
+
+        def one(t):
+            v._chk(L.mref_random_actions(v.h, O._ptr(akeys[t], C.c_uint32), O._ptr(act, C.c_int32)))
+            v._chk(L.mref_step(v.h, O._ptr(act, C.c_int32), None, None, None, None, None, None, None, None, 0,
+                               None, None, None, None))
+        cores = int(threads)
+    else:
+        v = O.PortVenv(env_id, cfg, n_envs)
+        v.reset(key)
+
+        def one(t):
+            v.step(v.random_actions(akeys[t]))
+        cores = 1
+    for t in range(warmup):
+        one(t)
+    t0 = time.perf_counter()
+    for t in range(warmup, warmup + steps):
+        one(t)
+    sec = time.perf_counter() - t0
+    return sec, kind, cores, v.n_agents
+
+
+def cpu_sample_size(env_id, cfg):
+    """(envs, steps) of a bounded CPU sample of the workload: ~10-30 s for the
+    cpu_baseline leg; the envs cap also bounds one reference-arm step (~1 s)."""
+    return {"MPE_simple_spread_v3": (1024, 200), "SMAX_5m_vs_6m": (65536, 5), "SMAX_2s3z": (65536, 5),
+            "SMAX_27m_vs_30m": (4096, 4), "overcooked_cramped_room_v0": (65536, 5)}.get(env_id, (1024, 10))
+
+
+def run_reference_arm(args, rank, world):
+    env_id, cfg, n_per_gpu, label = WORKLOADS[args.workload]
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    n_envs = n_per_gpu * world
+    # each step is one batch step of the whole workload on the host cores
+    # unless that would not finish within a few minutes; then a bounded sample.
+    n_cpu, _ = cpu_sample_size(env_id, cfg)
+    n_cpu = min(n_envs, max(n_cpu, 1))
+    sec, kind, cores, A = cpu_reference_probe(env_id, cfg, n_cpu, args.steps, args.warmup, threads)
+    val = n_cpu * A * args.steps / sec
+    line = {"impl": "reference", "metric": "agent-steps/sec (env-steps/sec x agents)", "value": val,
+            "unit": "agent-steps/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * sec / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference random-legal action stream)",
+            "config": {"workload": label, "env_id": env_id, "env_config": cfg, "n_envs": n_cpu,
+                       "n_envs_requested": n_envs},
+            "cpu_baseline": {"value": val, "unit": "agent-steps/s", "cores": cores, "kind": kind,
+                             "sample": f"{n_cpu} envs x {args.steps} steps of {env_id} on {cores} threads"},
+            "e2e": {"value": val, "unit": "agent-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+# --------------------------------------------------------------------- GPU arm
+def run_gpu_arm(args, rank, world, local_rank):
+    import torch
+    import paper_2311_10090_b200 as m
+    from paper_2311_10090_b200 import _native
+
+    env_id, cfg, n_per_gpu, label = WORKLOADS[args.workload]
+    if args.n_envs:
+        n_per_gpu = args.n_envs
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+    env = m.make_env(env_id, cfg)
+    A = env.num_agents()
+    N = n_per_gpu * world
+    venv = m.VectorEnv(env, n_per_gpu, device=local_rank, global_offset=rank * n_per_gpu, global_n=N)
+    stream = torch.cuda.current_stream()
+    key = m.prng.key_from_seed(0)
+    akeys = m.prng.split(m.prng.fold_in(key, 2), args.steps + args.warmup + 2)  # vector_env.cpp:202
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device="cuda")
+
+    venv.reset(key)
+    for t in range(args.warmup):
+        venv.step_random(akeys[t])
+        flush.fill_(float(t))
+    torch.cuda.synchronize()
+    venv.episode_stats(clear=True)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+
+    clocks = ClockSampler() if rank == 0 else None
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    fin_counts = torch.zeros(args.steps, dtype=torch.int64, device="cuda")
+    launches0 = _native.lib().marl_launch_count()
+    for k in range(args.steps):
+        starts[k].record(stream)
+        r = venv.step_random(akeys[args.warmup + k])
+        ends[k].record(stream)
+        fin_counts[k] = r.finished.sum()
+        flush.fill_(float(k))  # L2 flush between timed steps (not timed)
+    torch.cuda.synchronize()
+    launches = _native.lib().marl_launch_count() - launches0
+    if dist:
+        dist.barrier()
+    clk = clocks.stop() if clocks else None
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    total_ms = float(sum(step_ms))
+    t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+    stats = torch.tensor(venv.episode_stats_raw(), dtype=torch.int64, device="cuda")
+    if dist:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(stats, op=dist.ReduceOp.SUM)  # the one NCCL collective per rollout
+    total_ms = float(t.item())
+    value = N * A * args.steps / (total_ms * 1e-3)
+
+    # roofline of the dominant (only) kernel: algorithmic bytes per launch / mean launch time
+    finished = fin_counts.cpu().numpy()
+    bytes_per_launch = float(np.mean([algorithmic_bytes(env, n_per_gpu, int(f)) for f in finished]))
+    mean_launch_s = float(np.mean(step_ms)) * 1e-3
+    achieved = bytes_per_launch / mean_launch_s / 1e9
+    peak, peak_src = measured_peak()
+    traffic = ncu_traffic(args.workload)
+
+    # end-to-end through the C-ABI with host buffers (pinned), copies inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        D = env.obs_dim
+        pin = lambda shape, dt: torch.empty(shape, dtype=dt, pin_memory=True).numpy()  # noqa: E731
+        host = {"obs": pin((n_per_gpu, A, D), torch.float32), "rewards": pin((n_per_gpu, A), torch.float64),
+                "dones": pin((n_per_gpu, A + 1), torch.uint8), "finished": pin((n_per_gpu,), torch.uint8),
+                "final_returns": pin((n_per_gpu,), torch.float64), "final_lengths": pin((n_per_gpu,), torch.int32)}
+        d2h = sum(a.nbytes for a in host.values())
+        e2e_steps = max(3, min(args.steps, 20))
+        venv.host_step_random(akeys[0], host)  # warm
+        if dist:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for k in range(e2e_steps):
+            venv.host_step_random(akeys[1 + k], host)
+        sec = time.perf_counter() - t0
+        ts = torch.tensor([sec], dtype=torch.float64, device="cuda")
+        if dist:
+            dist.all_reduce(ts, op=dist.ReduceOp.MAX)
+        e2e = {"value": N * A * e2e_steps / float(ts.item()), "unit": "agent-steps/s",
+               "h2d_bytes_per_step": 16, "d2h_bytes_per_step": int(d2h * world),
+               "steps": e2e_steps, "path": "marl_venv_step_random_host (C-ABI, pinned host buffers)"}
+
+    if rank != 0:
+        return
+    cpu = None
+    if world == 1 and not args.no_cpu:
+        n_cpu, k_cpu = cpu_sample_size(env_id, cfg)
+        threads = os.cpu_count() or 1
+        sec, kind, cores, _ = cpu_reference_probe(env_id, cfg, n_cpu, k_cpu, 1, threads)
+        cpu = {"value": n_cpu * A * k_cpu / sec, "unit": "agent-steps/s", "cores": cores, "kind": kind,
+               "sample": f"{n_cpu} envs x {k_cpu} steps of {env_id} ({sec:.1f} s, {cores} threads, "
+                         "reference VectorEnv::step + random_legal_actions)"}
+    line = {
+        "metric": "agent-steps/sec (env-steps/sec x agents)", "value": value, "unit": "agent-steps/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (reset from key_from_seed(0); reference random-legal action stream)",
+        "config": {"workload": label, "env_id": env_id, "env_config": cfg, "n_envs_per_gpu": n_per_gpu,
+                   "global_envs": N, "agents": A, "parallelism": f"env-sharded x{world}, no step collective",
+                   "l2": "flushed between timed steps (256 MB write, untimed)"},
+        "env_steps_per_sec": N * args.steps / (total_ms * 1e-3),
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                     "bytes_per_launch": bytes_per_launch, "mean_launch_us": mean_launch_s * 1e6,
+                     "kernel": "fused step kernel (step_random)"},
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": int(launches),
+        "clocks": clk,
+        "episode_stats": {"episodes": int(stats[0]), "mean_length": float(stats[1]) / max(int(stats[0]), 1),
+                          "mean_return": float(stats[2]) / (1 << 24) / max(int(stats[0]), 1)},
+    }
+    print(json.dumps(line))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="marl-b200", choices=["marl-b200", "reference"])
+    ap.add_argument("--workload", default="smax3m", choices=sorted(WORKLOADS))
+    ap.add_argument("--n-envs", type=int, default=0, help="override envs per GPU")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    if args.impl == "reference":
+        run_reference_arm(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl")
+    try:
+        run_gpu_arm(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,212 @@
+/* marl-b200: C-ABI of the B200-native batched multi-agent env engine.
+ *
+ * Drop-in boundary for the reference's batched hot path, marl::VectorEnv
+ * (/root/reference/proj/core/include/marl/vector_env.hpp:74-89,
+ *  /root/reference/proj/core/src/vector_env.cpp:45-129) and the env registry
+ * that feeds it (registry.hpp:16-28).  Plain pointers and sizes only; no C++
+ * or torch types cross this boundary.
+ *
+ * Data model (per handle, N local envs, A agents, D = max obs size):
+ *   the reference's per-env AgentMap<...> dictionaries (agent_map.hpp:14-65)
+ *   are flattened to fixed-width arrays in agent order:
+ *     obs, final_obs    [N][A][D] f32   (rows of smaller agents zero-padded)
+ *     rewards           [N][A]    f64
+ *     dones             [N][A+1]  u8    (per agent, then "__all__")
+ *     finished          [N]       u8    (dones["__all__"])
+ *     final_returns     [N]       f64,  final_lengths [N] i32
+ *     infos             [N][A][n_info] f64 (fields in std::map key order,
+ *                                  see marl_venv_info_name; episode_return /
+ *                                  episode_length live in final_returns /
+ *                                  final_lengths)
+ *     actions           [N][A]    i32
+ *     keys              [N][4]    u32   (k0, k1, c0, c1 of the carry key)
+ *     episode_returns   [N] f64, episode_lengths [N] i32
+ * All view pointers are DEVICE pointers owned by the handle and valid until
+ * the next call on it.  final_obs rows are written only where finished.
+ *
+ * Threading: one caller thread per handle; work is queued on the handle's
+ * CUDA stream and is asynchronous until marl_venv_sync / a *_host call.
+ *
+ * Errors: every call returns a status (the reference's exception taxonomy,
+ * errors.hpp:9-26); the message of the last failure on the calling thread is
+ * marl_last_error().  Device-side action validation (marl_venv_step) reports
+ * at the next synchronising call; the rejected batch leaves the state as it
+ * was, like the reference's ContractError from Env::validate_actions
+ * (env.cpp:7-14).
+ */
+#ifndef MARL_B200_H
+#define MARL_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum marl_status {
+  MARL_OK = 0,
+  MARL_ERR_NOT_FOUND = 1,   /* NotFoundError   (errors.hpp:9-12)  */
+  MARL_ERR_SCHEMA = 2,      /* SchemaError     (errors.hpp:14-17) */
+  MARL_ERR_CONTRACT = 3,    /* ContractError   (errors.hpp:19-22) */
+  MARL_ERR_DIVERGENCE = 4,  /* DivergenceError (errors.hpp:24-27) */
+  MARL_ERR_CUDA = 5,
+  MARL_ERR_INTERNAL = 6
+};
+
+enum marl_family { MARL_FAMILY_MPE = 0, MARL_FAMILY_SMAX = 1, MARL_FAMILY_OVERCOOKED = 2 };
+
+typedef struct marl_venv marl_venv;
+
+typedef struct {
+  int32_t family;       /* marl_family */
+  int32_t n_agents;     /* Env::num_agents (env.hpp:46) */
+  int32_t obs_dim;      /* max observation_space(agent).flat_size() */
+  int32_t n_actions;    /* max action_space(agent).n */
+  int32_t n_info;       /* f64 info fields per agent */
+  int32_t max_steps;    /* Env::max_steps (env.hpp:59) */
+  int32_t cooperative;  /* Env::cooperative (env.hpp:62) */
+  int32_t device;
+  int64_t n_envs;       /* local envs of this handle */
+  int64_t global_offset;/* global index of local env 0 */
+  int64_t global_n;     /* envs in the whole (possibly multi-GPU) batch */
+} marl_spec;
+
+typedef struct { /* device pointers, see the data model above */
+  float* obs;
+  double* rewards;
+  uint8_t* dones;
+  uint8_t* finished;
+  float* final_obs;
+  double* final_returns;
+  int32_t* final_lengths;
+  double* infos;
+  int32_t* actions;
+  uint32_t* keys;
+  double* episode_returns;
+  int32_t* episode_lengths;
+} marl_views;
+
+typedef struct { /* host destinations for *_host / download calls; NULL = skip */
+  float* obs;
+  double* rewards;
+  uint8_t* dones;
+  uint8_t* finished;
+  float* final_obs;
+  double* final_returns;
+  int32_t* final_lengths;
+  double* infos;
+  int32_t* actions;
+} marl_host_step;
+
+/* ---- registry (registry.hpp:16-28) ----------------------------------- */
+
+/* Number of env ids this engine implements; id i via marl_registered_env.
+ * Replaces registered_envs() (registry.cpp:99-106). */
+int marl_registered_count(void);
+const char* marl_registered_env(int i);
+
+/* make_env(env_id, config) alone (registry.cpp:83-97): resolve and validate
+ * the id and config and report the env's spec (n_envs fields zero) without
+ * touching a GPU.  Same errors as marl_venv_create. */
+int marl_env_describe(const char* env_id, const char* config_json, marl_spec* out);
+int marl_env_agent(const char* env_id, const char* config_json, int i, char* name, size_t cap,
+                   int32_t* obs_size, int32_t* n_actions);
+
+/* ---- lifecycle: make_env + VectorEnv ctor ------------------------------ */
+
+/* make_env(env_id, config) (registry.cpp:83-97) + VectorEnv(env, n_envs)
+ * (vector_env.cpp:45-49) on CUDA device `device`.  config_json may be NULL or
+ * "" for the defaults; unknown keys are SchemaError (config.hpp:78-83). */
+int marl_venv_create(const char* env_id, const char* config_json, int64_t n_envs, int device,
+                     marl_venv** out);
+
+/* Shard constructor for multi-GPU batches: this handle owns global envs
+ * [global_offset, global_offset + n_local) of a global_n-env batch; per-env
+ * keys derive from global indices (vector_env.cpp:52,55,171), so any sharding
+ * reproduces the single-device trajectories bit for bit. */
+int marl_venv_create_shard(const char* env_id, const char* config_json, int64_t n_local,
+                           int64_t global_offset, int64_t global_n, int device, marl_venv** out);
+
+int marl_venv_destroy(marl_venv* h);
+
+/* Queue work on an external cudaStream_t (e.g. the framework's current
+ * stream) instead of the handle's own stream. */
+int marl_venv_set_stream(marl_venv* h, void* cuda_stream);
+
+/* ---- spaces / metadata (env.hpp:43-82) --------------------------------- */
+
+int marl_venv_spec(const marl_venv* h, marl_spec* out);
+/* agents()[i], observation_space(agent).flat_size(), action_space(agent).n */
+int marl_venv_agent(const marl_venv* h, int i, char* name, size_t cap, int32_t* obs_size,
+                    int32_t* n_actions);
+int marl_venv_info_name(const marl_venv* h, int k, char* name, size_t cap);
+int marl_venv_id(const marl_venv* h, char* name, size_t cap); /* Env::id() */
+
+/* ---- hot path ----------------------------------------------------------- */
+
+/* VectorEnv::reset(key) (vector_env.cpp:51-70): reset keys split(key, N)[g],
+ * carry keys split(fold_in(key, 1), N)[g]; writes obs + carry views. */
+int marl_venv_reset(marl_venv* h, const uint32_t key[4]);
+
+/* VectorEnv::step(state, actions) (vector_env.cpp:72-129) with caller actions
+ * in DEVICE memory, [N][A] i32.  Step, team-return bookkeeping, auto-reset
+ * with the per-env child keys, all in one kernel. */
+int marl_venv_step(marl_venv* h, const int32_t* d_actions);
+
+/* One step of throughput_probe's loop (vector_env.cpp:214-217):
+ * random_legal_actions(state, step_key) (vector_env.cpp:169-187) fused into
+ * the step kernel.  The drawn actions land in views.actions. */
+int marl_venv_step_random(marl_venv* h, const uint32_t step_key[4]);
+
+/* Host-buffer variants (the end-to-end path): host actions are validated on
+ * the host exactly like Env::validate_actions, copied in, stepped, and the
+ * requested outputs copied back; returns after the copies complete. */
+int marl_venv_step_host(marl_venv* h, const int32_t* h_actions, const marl_host_step* out);
+int marl_venv_step_random_host(marl_venv* h, const uint32_t step_key[4], const marl_host_step* out);
+/* Copy the current views to host memory (synchronising). */
+int marl_venv_download(marl_venv* h, const marl_host_step* out);
+
+int marl_venv_views(marl_venv* h, marl_views* out);
+
+/* Env::legal_actions (env.hpp:71-73; smax.cpp:195-211) for the current
+ * state: d_out [N][A][n_actions] u8 (device). */
+int marl_venv_legal(marl_venv* h, uint8_t* d_out);
+/* Env::state_hash (mpe.cpp:254-269, smax.cpp:312-337, overcooked.cpp:348-364)
+ * of the current per-env states: d_out [N] u64 (device). */
+int marl_venv_state_hash(marl_venv* h, uint64_t* d_out);
+
+/* Episode statistics accumulated over finished episodes since the last
+ * clear: out[0] episodes, out[1] sum of final_lengths, out[2] sum of
+ * final_returns in 2^-24 fixed point (exact, order-independent -> identical
+ * totals for any GPU count; reduce across ranks with one integer allreduce). */
+int marl_venv_episode_stats(marl_venv* h, int64_t out[3], int clear);
+
+int marl_venv_sync(marl_venv* h);
+
+/* ---- the reference's own benchmark --------------------------------------- */
+
+/* throughput_probe(env_id, n_envs, n_steps, key, config) (vector_env.cpp:
+ * 191-222) on `device`: cold = reset + one warm-up step (action_keys[T]),
+ * warm = T steps with action_keys = split(fold_in(key, 2), T + 1), timed
+ * with CUDA events.  sps = n_envs * n_steps / seconds. */
+int marl_throughput_probe(const char* env_id, const char* config_json, int64_t n_envs,
+                          int n_steps, const uint32_t key[4], int device, double* seconds,
+                          double* cold_seconds);
+
+/* ---- keys (prng.hpp:21-57), host-side helpers ------------------------- */
+void marl_prng_key_from_seed(uint64_t seed, uint32_t out[4]);
+void marl_prng_split(const uint32_t key[4], uint64_t n, uint32_t* out /* [n][4] */);
+void marl_prng_fold_in(const uint32_t key[4], uint64_t data, uint32_t out[4]);
+uint64_t marl_prng_bits(const uint32_t key[4], uint64_t index);
+void marl_threefry2x32(uint32_t k0, uint32_t k1, uint32_t x0, uint32_t x1, uint32_t out[2]);
+
+/* ---- diagnostics ------------------------------------------------------ */
+const char* marl_last_error(void);
+uint64_t marl_launch_count(void); /* kernels launched by this library */
+const char* marl_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MARL_B200_H */

@@ -1,0 +1,100 @@
+"""ctypes binding of the C-ABI in ``include/marl_b200.h`` (libmarl_b200.so).
+
+The library is built in-tree by ``paper_2311_10090_b200/build.py`` (or
+``__graft_entry__.build()``).  There is no fallback: if the library is missing
+or cannot be loaded, every entry point raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+from .errors import raise_for_status
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libmarl_b200.so")
+
+
+class Spec(C.Structure):
+    _fields_ = [("family", C.c_int32), ("n_agents", C.c_int32), ("obs_dim", C.c_int32),
+                ("n_actions", C.c_int32), ("n_info", C.c_int32), ("max_steps", C.c_int32),
+                ("cooperative", C.c_int32), ("device", C.c_int32), ("n_envs", C.c_int64),
+                ("global_offset", C.c_int64), ("global_n", C.c_int64)]
+
+
+class Views(C.Structure):
+    _fields_ = [(n, C.c_void_p) for n in ("obs", "rewards", "dones", "finished", "final_obs",
+                                          "final_returns", "final_lengths", "infos", "actions",
+                                          "keys", "episode_returns", "episode_lengths")]
+
+
+class HostStep(C.Structure):
+    _fields_ = [(n, C.c_void_p) for n in ("obs", "rewards", "dones", "finished", "final_obs",
+                                          "final_returns", "final_lengths", "infos", "actions")]
+
+
+EXPORTS = [
+    "marl_registered_count", "marl_registered_env", "marl_env_describe", "marl_env_agent",
+    "marl_venv_create", "marl_venv_create_shard",
+    "marl_venv_destroy", "marl_venv_set_stream", "marl_venv_spec", "marl_venv_agent",
+    "marl_venv_info_name", "marl_venv_id", "marl_venv_reset", "marl_venv_step",
+    "marl_venv_step_random", "marl_venv_step_host", "marl_venv_step_random_host",
+    "marl_venv_download", "marl_venv_views", "marl_venv_legal", "marl_venv_state_hash",
+    "marl_venv_episode_stats", "marl_venv_sync", "marl_throughput_probe",
+    "marl_prng_key_from_seed", "marl_prng_split", "marl_prng_fold_in", "marl_prng_bits",
+    "marl_threefry2x32", "marl_last_error", "marl_launch_count", "marl_version",
+]
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(f"marl-b200 native library missing at {LIB_PATH}; build it with "
+                           "`python paper_2311_10090_b200/build.py` (there is no CPU fallback)")
+    L = C.CDLL(LIB_PATH)
+    vp, u32p, i32p, i64p = C.c_void_p, C.POINTER(C.c_uint32), C.POINTER(C.c_int32), C.POINTER(C.c_int64)
+    L.marl_registered_env.restype = C.c_char_p
+    L.marl_registered_env.argtypes = [C.c_int]
+    L.marl_env_describe.argtypes = [C.c_char_p, C.c_char_p, C.POINTER(Spec)]
+    L.marl_env_agent.argtypes = [C.c_char_p, C.c_char_p, C.c_int, C.c_char_p, C.c_size_t, i32p, i32p]
+    L.marl_venv_create.argtypes = [C.c_char_p, C.c_char_p, C.c_int64, C.c_int, C.POINTER(vp)]
+    L.marl_venv_create_shard.argtypes = [C.c_char_p, C.c_char_p, C.c_int64, C.c_int64, C.c_int64,
+                                         C.c_int, C.POINTER(vp)]
+    L.marl_venv_destroy.argtypes = [vp]
+    L.marl_venv_set_stream.argtypes = [vp, vp]
+    L.marl_venv_spec.argtypes = [vp, C.POINTER(Spec)]
+    L.marl_venv_agent.argtypes = [vp, C.c_int, C.c_char_p, C.c_size_t, i32p, i32p]
+    L.marl_venv_info_name.argtypes = [vp, C.c_int, C.c_char_p, C.c_size_t]
+    L.marl_venv_id.argtypes = [vp, C.c_char_p, C.c_size_t]
+    L.marl_venv_reset.argtypes = [vp, u32p]
+    L.marl_venv_step.argtypes = [vp, vp]
+    L.marl_venv_step_random.argtypes = [vp, u32p]
+    L.marl_venv_step_host.argtypes = [vp, vp, C.POINTER(HostStep)]
+    L.marl_venv_step_random_host.argtypes = [vp, u32p, C.POINTER(HostStep)]
+    L.marl_venv_download.argtypes = [vp, C.POINTER(HostStep)]
+    L.marl_venv_views.argtypes = [vp, C.POINTER(Views)]
+    L.marl_venv_legal.argtypes = [vp, vp]
+    L.marl_venv_state_hash.argtypes = [vp, vp]
+    L.marl_venv_episode_stats.argtypes = [vp, i64p, C.c_int]
+    L.marl_venv_sync.argtypes = [vp]
+    L.marl_throughput_probe.argtypes = [C.c_char_p, C.c_char_p, C.c_int64, C.c_int, u32p, C.c_int,
+                                        C.POINTER(C.c_double), C.POINTER(C.c_double)]
+    L.marl_prng_key_from_seed.argtypes = [C.c_uint64, u32p]
+    L.marl_prng_split.argtypes = [u32p, C.c_uint64, u32p]
+    L.marl_prng_fold_in.argtypes = [u32p, C.c_uint64, u32p]
+    L.marl_prng_bits.argtypes = [u32p, C.c_uint64]
+    L.marl_prng_bits.restype = C.c_uint64
+    L.marl_threefry2x32.argtypes = [C.c_uint32] * 4 + [u32p]
+    L.marl_last_error.restype = C.c_char_p
+    L.marl_launch_count.restype = C.c_uint64
+    L.marl_version.restype = C.c_char_p
+    _lib = L
+    return L
+
+
+def check(rc: int) -> None:
+    if rc:
+        raise_for_status(rc, lib().marl_last_error().decode(errors="replace"))

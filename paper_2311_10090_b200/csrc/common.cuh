@@ -1,0 +1,224 @@
+// Device-side building blocks shared by every env kernel: the reference's
+// Threefry-2x32-20 key streams, a glibc-exact hypot, and block-cooperative
+// coalesced row stores.  Compiled for sm_100a with -fmad=false so every fp64
+// expression is evaluated as written (the reference is built for baseline
+// x86-64 without FMA contraction, proj/CMakeLists.txt:7-9).
+#pragma once
+#include <cmath>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#define MARL_HD __host__ __device__ __forceinline__
+#ifdef __CUDACC__
+#define MARL_NOINLINE __noinline__
+#else
+#define MARL_NOINLINE __attribute__((noinline))
+#endif
+
+namespace marl_b200 {
+
+MARL_HD int64_t min64(int64_t a, int64_t b) { return a < b ? a : b; }
+
+// PrngKey (prng.hpp:12-17): cipher key k0,k1 + 64-bit counter base c1:c0.
+struct Key {
+  uint32_t k0, k1, c0, c1;
+};
+
+MARL_HD uint32_t rotl32(uint32_t x, int r) {
+#ifdef __CUDA_ARCH__
+  return __funnelshift_l(x, x, r);
+#else
+  return (x << r) | (x >> (32 - r));
+#endif
+}
+
+// threefry2x32, prng.cpp:93-114 (20 rounds, key injection every 4).
+MARL_HD void threefry2x32(uint32_t k0, uint32_t k1, uint32_t x0, uint32_t x1, uint32_t& y0,
+                          uint32_t& y1) {
+  const uint32_t k2 = 0x1BD11BDAu ^ k0 ^ k1;
+  x0 += k0;
+  x1 += k1;
+#define MARL_R(r) x0 += x1; x1 = rotl32(x1, r); x1 ^= x0;
+  MARL_R(13) MARL_R(15) MARL_R(26) MARL_R(6)
+  x0 += k1; x1 += k2 + 1u;
+  MARL_R(17) MARL_R(29) MARL_R(16) MARL_R(24)
+  x0 += k2; x1 += k0 + 2u;
+  MARL_R(13) MARL_R(15) MARL_R(26) MARL_R(6)
+  x0 += k0; x1 += k1 + 3u;
+  MARL_R(17) MARL_R(29) MARL_R(16) MARL_R(24)
+  x0 += k1; x1 += k2 + 4u;
+  MARL_R(13) MARL_R(15) MARL_R(26) MARL_R(6)
+  x0 += k2; x1 += k0 + 5u;
+#undef MARL_R
+  y0 = x0;
+  y1 = x1;
+}
+
+// block_at, prng.cpp:76-81: block at counter base + offset, packed (y0<<32)|y1.
+MARL_HD uint64_t block_at(const Key& k, uint64_t off) {
+  uint64_t ctr = ((uint64_t(k.c1) << 32) | k.c0) + off;
+  uint32_t y0, y1;
+  threefry2x32(k.k0, k.k1, uint32_t(ctr), uint32_t(ctr >> 32), y0, y1);
+  return (uint64_t(y0) << 32) | y1;
+}
+
+constexpr uint64_t kSplitBase = uint64_t(1) << 63;           // prng.cpp:84
+constexpr uint64_t kFoldBase = kSplitBase + (uint64_t(1) << 62);  // prng.cpp:162
+
+MARL_HD Key key_from_blocks(uint64_t a, uint64_t b) {  // prng.cpp:153-154
+  return Key{uint32_t(a >> 32), uint32_t(a), uint32_t(b), uint32_t(b >> 32)};
+}
+
+// Child i of prng::split(key, n) (prng.cpp:147-157); O(1) in i, so any shard
+// derives its own children without materialising the others.
+MARL_HD Key split_child(const Key& k, uint64_t i) {
+  return key_from_blocks(block_at(k, kSplitBase + 2 * i), block_at(k, kSplitBase + 2 * i + 1));
+}
+
+// prng.cpp:159-167
+MARL_HD Key fold_in(const Key& k, uint64_t d) {
+  return key_from_blocks(block_at(k, kFoldBase + 2 * d), block_at(k, kFoldBase + 2 * d + 1));
+}
+
+MARL_HD double to_unit(uint64_t b) { return double(b >> 11) * 0x1.0p-53; }  // prng.cpp:86-89
+
+// Element j of prng::uniform(key, n, lo, hi) (prng.cpp:169-178).
+MARL_HD double uniform_at(const Key& k, uint64_t j, double lo, double hi) {
+  double v = lo + to_unit(block_at(k, j)) * (hi - lo);
+  if (v >= hi) v = nextafter(hi, lo);
+  return v;
+}
+
+// x % n for n < 2^16 with 32-bit arithmetic only (three 32-bit remainders):
+// x = h*2^32 + l  ->  ((h % n) * 2^16 + l_hi) % n, then (* 2^16 + l_lo) % n.
+MARL_HD uint32_t mod_small(uint64_t x, uint32_t n) {
+  uint32_t r = uint32_t(x >> 32) % n;
+  r = ((r << 16) | (uint32_t(x) >> 16)) % n;
+  r = ((r << 16) | (uint32_t(x) & 0xffffu)) % n;
+  return r;
+}
+
+// glibc >= 2.35 __hypot (sysdeps/ieee754/dbl-64/e_hypot.c, the non-FMA
+// Borges "MyHypot3" correction) -- the x86-64 libm the reference links
+// (smax.cpp:495,550).  Restated from the published algorithm (Borges,
+// arXiv:1904.09481) and glibc's scaling thresholds; every operation below is
+// an explicit IEEE round-to-nearest op so nvcc cannot contract it.
+MARL_HD double hypot_kernel(double ax, double ay) {
+#ifdef __CUDA_ARCH__
+  double h = __dsqrt_rn(__dadd_rn(__dmul_rn(ax, ax), __dmul_rn(ay, ay)));
+  double t1, t2;
+  if (h <= __dmul_rn(2.0, ay)) {
+    double delta = __dsub_rn(h, ay);
+    t1 = __dmul_rn(ax, __dsub_rn(__dmul_rn(2.0, delta), ax));
+    t2 = __dmul_rn(__dsub_rn(delta, __dmul_rn(2.0, __dsub_rn(ax, ay))), delta);
+  } else {
+    double delta = __dsub_rn(h, ax);
+    t1 = __dmul_rn(__dmul_rn(2.0, delta), __dsub_rn(ax, __dmul_rn(2.0, ay)));
+    t2 = __dadd_rn(__dmul_rn(__dsub_rn(__dmul_rn(4.0, delta), ay), ay), __dmul_rn(delta, delta));
+  }
+  return __dsub_rn(h, __ddiv_rn(__dadd_rn(t1, t2), __dmul_rn(2.0, h)));
+#else
+  double h = sqrt(ax * ax + ay * ay);
+  double t1, t2;
+  if (h <= 2.0 * ay) {
+    double delta = h - ay;
+    t1 = ax * (2.0 * delta - ax);
+    t2 = (delta - 2.0 * (ax - ay)) * delta;
+  } else {
+    double delta = h - ax;
+    t1 = 2.0 * delta * (ax - 2.0 * ay);
+    t2 = (4.0 * delta - ay) * ay + delta * delta;
+  }
+  h -= (t1 + t2) / (2.0 * h);
+  return h;
+#endif
+}
+
+// Out of line on purpose: it is the rare exact path behind dist_le and the
+// separation push, and inlining it into every unrolled pair loop bloats code.
+__host__ __device__ MARL_NOINLINE inline double hypot_glibc(double x, double y) {
+  if (!std::isfinite(x) || !std::isfinite(y)) {
+    if (std::isinf(x) || std::isinf(y)) return INFINITY;
+    return x + y;
+  }
+  x = std::fabs(x);
+  y = std::fabs(y);
+  double ax = x < y ? y : x;
+  double ay = x < y ? x : y;
+  if (ax > 0x1p+511) {
+    if (ay <= ax * 0x1p-54) return ax + ay;
+    return hypot_kernel(ax * 0x1p-600, ay * 0x1p-600) / 0x1p-600;
+  }
+  if (ay < 0x1p-511) {
+    if (ax >= ay / 0x1p-54) return ax + ay;
+    return hypot_kernel(ax / 0x1p-600, ay / 0x1p-600) * 0x1p-600;
+  }
+  if (ay <= ax * 0x1p-54) return ax + ay;
+  return hypot_kernel(ax, ay);
+}
+
+// Exact evaluation of `hypot(dx, dy) <= r` (the form every SMAX range/sight
+// test takes, smax.cpp:383,497-501,613) without the hypot in the common case:
+// dx^2+dy^2 is within a few ulps of hypot^2 and glibc's hypot is within one
+// ulp, so outside a relative band of 2e-12 around r^2 the squared distance
+// decides; inside the band the glibc-exact hypot decides.  r2lo/r2hi are
+// r^2*(1 -/+ 1e-12), precomputed on the host.
+MARL_HD bool dist_le(double dx, double dy, double r, double r2lo, double r2hi) {
+  double d2 = dx * dx + dy * dy;
+  if (d2 < r2lo) return true;
+  if (d2 > r2hi) return false;
+  return hypot_glibc(dx, dy) <= r;
+}
+
+struct Thresh {  // a distance threshold and its squared decision band
+  double r, r2lo, r2hi;
+};
+
+MARL_HD Thresh make_thresh(double r) {
+  return Thresh{r, r * r * (1.0 - 1e-12), r * r * (1.0 + 1e-12)};
+}
+
+#ifdef __CUDACC__
+// Copy `bytes` from shared to global memory with the whole block: 16-byte
+// vectors when both ends are 16-byte aligned, else 4-byte words, else bytes.
+__device__ __forceinline__ void block_store(void* gdst, const void* ssrc, size_t bytes) {
+  const uintptr_t g = reinterpret_cast<uintptr_t>(gdst);
+  const uintptr_t s = reinterpret_cast<uintptr_t>(ssrc);
+  if (((g | s | bytes) & 15) == 0) {
+    const int4* src = static_cast<const int4*>(ssrc);
+    int4* dst = static_cast<int4*>(gdst);
+    for (size_t i = threadIdx.x; i < bytes / 16; i += blockDim.x) __stcs(dst + i, src[i]);
+  } else if (((g | s | bytes) & 3) == 0) {
+    const int* src = static_cast<const int*>(ssrc);
+    int* dst = static_cast<int*>(gdst);
+    for (size_t i = threadIdx.x; i < bytes / 4; i += blockDim.x) __stcs(dst + i, src[i]);
+  } else {
+    const uint8_t* src = static_cast<const uint8_t*>(ssrc);
+    uint8_t* dst = static_cast<uint8_t*>(gdst);
+    for (size_t i = threadIdx.x; i < bytes; i += blockDim.x) dst[i] = src[i];
+  }
+}
+
+// Per-block episode statistics, folded into 64-bit integer accumulators so the
+// totals are exact and order-independent (identical for any grid shape and any
+// number of GPUs): [0] finished episodes, [1] sum of lengths, [2] sum of
+// returns in 2^-24 fixed point.
+__device__ __forceinline__ void stats_add(unsigned long long* stats, bool finished, int length,
+                                          double ret) {
+  unsigned long long n = finished ? 1ull : 0ull;
+  unsigned long long L = finished ? (unsigned long long)(long long)length : 0ull;
+  unsigned long long R = finished ? (unsigned long long)__double2ll_rn(ret * 16777216.0) : 0ull;
+  for (int o = 16; o > 0; o >>= 1) {
+    n += __shfl_xor_sync(0xffffffffu, n, o);
+    L += __shfl_xor_sync(0xffffffffu, L, o);
+    R += __shfl_xor_sync(0xffffffffu, R, o);
+  }
+  if ((threadIdx.x & 31) == 0 && n) {
+    atomicAdd(stats + 0, n);
+    atomicAdd(stats + 1, L);
+    atomicAdd(stats + 2, R);
+  }
+}
+#endif
+
+}  // namespace marl_b200

@@ -1,0 +1,152 @@
+"""GPU: the VectorEnv contract (vector_env.cpp, test_vector_env.cpp) on the
+CUDA engine -- error behaviour, purity/determinism, shard invariance (the
+analogue of the 1/4/16-thread invariance test, test_vector_env.cpp:117-154),
+episode bookkeeping, and size-independent properties at full bench sizes."""
+import numpy as np
+import pytest
+
+import oracle as O
+from _util import THREE_M, gpu_outputs, probe_keys
+
+pytestmark = pytest.mark.gpu
+
+
+def _m():
+    import paper_2311_10090_b200 as m
+    return m
+
+
+def test_invalid_actions_raise_and_leave_state_untouched():
+    import torch
+    m = _m()
+    v = m.VectorEnv("SMAX_5m_vs_6m", 32, config=THREE_M)
+    _, st = v.reset(O.key_from_seed(1))
+    h0 = v.state_hash().cpu().numpy().copy()
+    bad = torch.full((32, 3), 4, dtype=torch.int32, device="cuda")
+    bad[7, 2] = 99
+    with pytest.raises(m.ContractError, match="ally_2"):
+        v.step(st, bad)
+    assert np.array_equal(v.state_hash().cpu().numpy(), h0)
+    with pytest.raises(m.ContractError):
+        v.step(st, np.full((32, 3), -1, np.int32))
+    with pytest.raises(m.ContractError):
+        v.step(st, np.zeros((31, 3), np.int32))
+    assert np.array_equal(v.state_hash().cpu().numpy(), h0)
+    # the handle recovers: a valid step works and matches the oracle
+    o = O.PortVenv("SMAX_5m_vs_6m", THREE_M, 32)
+    o.reset(O.key_from_seed(1))
+    good = np.full((32, 3), 4, np.int32)
+    r = v.step(st, good)
+    b = o.step(good)
+    assert np.array_equal(gpu_outputs(v, 3)["obs"], b["obs"])
+    with pytest.raises(m.ContractError, match="stale"):
+        v.step(st, good)
+    v.step(r.next, good)
+
+
+def test_step_before_reset_is_contract_error():
+    m = _m()
+    v = m.VectorEnv("MPE_simple_spread_v3", 4)
+    with pytest.raises(m.ContractError):
+        v.step(None, np.zeros((4, 3), np.int32))
+
+
+@pytest.mark.parametrize("env_id,cfg", [("SMAX_5m_vs_6m", THREE_M), ("overcooked_cramped_room_v0", {"max_steps": 20}),
+                                        ("MPE_simple_spread_v3", {})])
+def test_shard_invariance(env_id, cfg):
+    """Splitting the batch across handles (as across GPUs) is bit-identical."""
+    m = _m()
+    N, T = 200, 45
+    full = m.VectorEnv(env_id, N, config=cfg)
+    parts = [m.VectorEnv(env_id, 70, config=cfg, global_offset=0, global_n=N),
+             m.VectorEnv(env_id, 130, config=cfg, global_offset=70, global_n=N)]
+    key, ak = probe_keys(21, T)
+    full.reset(key)
+    for p in parts:
+        p.reset(key)
+    for t in range(T):
+        full.step_random(ak[t])
+        for p in parts:
+            p.step_random(ak[t])
+        a = gpu_outputs(full, full.env().n_info)
+        bs = [gpu_outputs(p, p.env().n_info) for p in parts]
+        for f in a:
+            assert np.array_equal(a[f], np.concatenate([b[f] for b in bs])), (t, f)
+    assert full.episode_stats_raw() == [x + y for x, y in zip(parts[0].episode_stats_raw(),
+                                                              parts[1].episode_stats_raw())]
+
+
+def test_determinism_and_bookkeeping_identity():
+    """Re-running is bit-identical; no transition lost across boundaries
+    (test_vector_env.cpp:92-115): sum of finished lengths + in-flight == steps."""
+    m = _m()
+    N, T = 4096, 150
+    runs = []
+    for _ in range(2):
+        v = m.VectorEnv("SMAX_5m_vs_6m", N, config=THREE_M)
+        key, ak = probe_keys(5, T)
+        v.reset(key)
+        done_len = 0
+        for t in range(T):
+            r = v.step_random(ak[t])
+            fin = r.finished.bool()
+            done_len += int(r.final_lengths[fin].sum())
+        in_flight = int(v.view("episode_lengths").sum())
+        assert done_len + in_flight == N * T
+        eps, lens, rets = v.episode_stats()
+        assert lens == done_len and eps > 0
+        runs.append((v.state_hash().cpu().numpy().copy(), v.keys_numpy().copy(), eps, lens, rets))
+    assert np.array_equal(runs[0][0], runs[1][0]) and np.array_equal(runs[0][1], runs[1][1])
+    assert runs[0][2:] == runs[1][2:]
+
+
+def test_full_size_overcooked_properties():
+    """C3 at full size (262144 envs): one-hot plane invariants every step and
+    the synchronised horizon (all episodes end at t = max_steps)."""
+    import torch
+    m = _m()
+    N, T, H = 262144, 40, 25
+    v = m.VectorEnv("overcooked_cramped_room_v0", N, config={"max_steps": H})
+    key, ak = probe_keys(2, T)
+    v.reset(key)
+    cells = 20
+    for t in range(T):
+        r = v.step_random(ak[t])
+        obs = r.obs.view(N, 2, 541)
+        planes = obs[:, :, :540].view(N, 2, 27, cells)
+        assert torch.all(planes[:, :, 0].sum(-1) == 1)          # self position one-hot
+        assert torch.all(planes[:, :, 2:6].sum((-1, -2)) == 1)  # exactly one facing plane set
+        assert torch.all(planes[:, :, 10:15].sum(-2).max(-1).values <= 1)
+        expect_done = (t + 1) % H == 0
+        assert bool(torch.all(r.finished == int(expect_done)))
+        clock = ((t + 1) % H) / H
+        assert torch.allclose(obs[:, :, 540], torch.full_like(obs[:, :, 540], clock))
+    torch.cuda.synchronize()
+
+
+def test_full_size_smax_properties():
+    """C2 at full size (65536 envs): rewards identical across allies, reward
+    ledger bounded, health never increases, obs entries in [-1, 1]."""
+    import torch
+    m = _m()
+    N, T = 65536, 60
+    v = m.VectorEnv("SMAX_5m_vs_6m", N, config=THREE_M)
+    key, ak = probe_keys(4, T)
+    v.reset(key)
+    for t in range(T):
+        r = v.step_random(ak[t])
+        rew = r.rewards
+        assert torch.all(rew[:, 0] == rew[:, 1]) and torch.all(rew[:, 1] == rew[:, 2])
+        assert torch.all(rew <= 1.0 + 1e-12) and torch.all(rew >= 0.0)
+        assert torch.all(r.obs.abs() <= 1.0)
+        assert torch.all(r.dones[:, 3] == r.finished)
+    eps, lens, rets = v.episode_stats()
+    assert eps > N // 2 and 5 < lens / eps < 60
+
+
+def test_throughput_probe_runs():
+    m = _m()
+    res = m.throughput_probe("MPE_simple_spread_v3", 1024, 50, O.key_from_seed(1))
+    assert res.sps > 0 and np.isfinite(res.sps) and res.cold_seconds > 0
+    assert res.csv_row().startswith("MPE_simple_spread_v3,1024,50,")
+    assert m.ThroughputResult.csv_header() == "env_id,n_envs,steps,seconds,sps"
