@@ -18,7 +18,6 @@ import json
 import os
 import subprocess
 import sys
-import tempfile
 import time
 
 import numpy as np
@@ -64,34 +63,69 @@ def algorithmic_bytes(env, n_envs, n_finished):
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+    """SM clocks and clock-event (throttle) reasons sampled DURING the timed
+    region: NVML polled every 2 ms from a side thread (the timed region of a
+    sub-millisecond step is too short for `nvidia-smi -lms`), with the
+    nvidia-smi query of B200_PROFILING.md as the fallback when NVML is absent."""
 
-    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+               0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown"}
 
-    def __init__(self):
-        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+    def __init__(self, device=0, period_s=0.002):
+        import threading
+        self.sm, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
         try:
-            self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                                       "-lms", "200"], stdout=self.f, stderr=subprocess.DEVNULL)
-        except FileNotFoundError:
-            self.p = None
+            import pynvml as N
+            N.nvmlInit()
+            self.N, self.h = N, N.nvmlDeviceGetHandleByIndex(device)
+            self.max_mhz = float(N.nvmlDeviceGetMaxClockInfo(self.h, N.NVML_CLOCK_SM))
+        except Exception:
+            self.N = None
+        self.period = period_s
+        self.t = threading.Thread(target=self._run, daemon=True)
+        self.t.start()
+
+    def _sample(self):
+        N, h = self.N, self.h
+        self.sm.append(float(N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)))
+        try:
+            mask = N.nvmlDeviceGetCurrentClocksEventReasons(h)
+        except AttributeError:
+            mask = N.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+        for bit, name in self.REASONS.items():
+            if mask & bit:
+                self.reasons.add(name)
+
+    def _run(self):
+        if self.N is None:
+            return
+        while True:
+            self._sample()
+            if self._stop.wait(self.period):
+                break
 
     def stop(self):
-        if self.p is None:
+        self._stop.set()
+        self.t.join()
+        if self.N is None:
+            return self._smi()
+        return {"sm_mhz": float(np.median(self.sm)) if self.sm else None, "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.sm), "source": "nvml, 2 ms"}
+
+    @staticmethod
+    def _smi():
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            row = subprocess.run(["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader,nounits", "-i", "0"],
+                                 capture_output=True, text=True).stdout.strip().split(",")
+        except FileNotFoundError:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.p.terminate()
-        self.p.wait()
-        self.f.flush()
-        rows = [r.split(",") for r in open(self.f.name).read().strip().splitlines() if r.strip()]
-        os.unlink(self.f.name)
-        sm = [float(r[1]) for r in rows if len(r) >= 9 and r[1].strip().replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in rows if len(r) >= 9 and r[2].strip().replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in rows if len(r) >= 9 for i in range(4) if "Active" in r[5 + i]})
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(rows)}
+        return {"sm_mhz": float(row[0]), "sm_max_mhz": float(row[1]),
+                "reasons": [n for n, v in zip(names, row[2:]) if v.strip() == "Active"], "samples": 1,
+                "source": "nvidia-smi after the timed region (NVML unavailable)"}
 
 
 def measured_peak():
@@ -185,6 +219,7 @@ def run_gpu_arm(args, rank, world, local_rank):
     import torch
     import paper_2311_10090_b200 as m
     from paper_2311_10090_b200 import _native
+    from paper_2311_10090_b200 import dist as D
 
     env_id, cfg, n_per_gpu, label = WORKLOADS[args.workload]
     if args.n_envs:
@@ -196,7 +231,7 @@ def run_gpu_arm(args, rank, world, local_rank):
     env = m.make_env(env_id, cfg)
     A = env.num_agents()
     N = n_per_gpu * world
-    venv = m.VectorEnv(env, n_per_gpu, device=local_rank, global_offset=rank * n_per_gpu, global_n=N)
+    venv = D.make_sharded(env, N, rank, world, device=local_rank)  # contiguous shard, no step collective
     stream = torch.cuda.current_stream()
     key = m.prng.key_from_seed(0)
     akeys = m.prng.split(m.prng.fold_in(key, 2), args.steps + args.warmup + 2)  # vector_env.cpp:202
@@ -212,7 +247,7 @@ def run_gpu_arm(args, rank, world, local_rank):
         dist.barrier()
     torch.cuda.synchronize()
 
-    clocks = ClockSampler() if rank == 0 else None
+    clocks = ClockSampler(local_rank) if rank == 0 else None
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     fin_counts = torch.zeros(args.steps, dtype=torch.int64, device="cuda")
@@ -230,12 +265,8 @@ def run_gpu_arm(args, rank, world, local_rank):
     clk = clocks.stop() if clocks else None
     step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
     total_ms = float(sum(step_ms))
-    t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
-    stats = torch.tensor(venv.episode_stats_raw(), dtype=torch.int64, device="cuda")
-    if dist:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        dist.all_reduce(stats, op=dist.ReduceOp.SUM)  # the one NCCL collective per rollout
-    total_ms = float(t.item())
+    total_ms = D.max_over_ranks(total_ms, device="cuda")  # device time, max over ranks
+    stats = D.all_reduce_episode_stats(venv.episode_stats_raw(), device="cuda")  # the one collective
     value = N * A * args.steps / (total_ms * 1e-3)
 
     # roofline of the dominant (only) kernel: algorithmic bytes per launch / mean launch time
@@ -263,10 +294,8 @@ def run_gpu_arm(args, rank, world, local_rank):
         for k in range(e2e_steps):
             venv.host_step_random(akeys[1 + k], host)
         sec = time.perf_counter() - t0
-        ts = torch.tensor([sec], dtype=torch.float64, device="cuda")
-        if dist:
-            dist.all_reduce(ts, op=dist.ReduceOp.MAX)
-        e2e = {"value": N * A * e2e_steps / float(ts.item()), "unit": "agent-steps/s",
+        sec = D.max_over_ranks(sec, device="cuda")
+        e2e = {"value": N * A * e2e_steps / sec, "unit": "agent-steps/s",
                "h2d_bytes_per_step": 16, "d2h_bytes_per_step": int(d2h * world),
                "steps": e2e_steps, "path": "marl_venv_step_random_host (C-ABI, pinned host buffers)"}
 
@@ -297,8 +326,7 @@ def run_gpu_arm(args, rank, world, local_rank):
         "e2e": e2e,
         "gpu_launches": int(launches),
         "clocks": clk,
-        "episode_stats": {"episodes": int(stats[0]), "mean_length": float(stats[1]) / max(int(stats[0]), 1),
-                          "mean_return": float(stats[2]) / (1 << 24) / max(int(stats[0]), 1)},
+        "episode_stats": D.summarize(stats),
     }
     print(json.dumps(line))
 
