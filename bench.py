@@ -219,7 +219,7 @@ def run_gpu_arm(args, rank, world, local_rank):
     import torch
     import paper_2311_10090_b200 as m
     from paper_2311_10090_b200 import _native
-    from paper_2311_10090_b200 import dist as D
+    from paper_2311_10090_b200 import dist as shard
 
     env_id, cfg, n_per_gpu, label = WORKLOADS[args.workload]
     if args.n_envs:
@@ -231,7 +231,7 @@ def run_gpu_arm(args, rank, world, local_rank):
     env = m.make_env(env_id, cfg)
     A = env.num_agents()
     N = n_per_gpu * world
-    venv = D.make_sharded(env, N, rank, world, device=local_rank)  # contiguous shard, no step collective
+    venv = shard.make_sharded(env, N, rank, world, device=local_rank)  # contiguous shard, no step collective
     stream = torch.cuda.current_stream()
     key = m.prng.key_from_seed(0)
     akeys = m.prng.split(m.prng.fold_in(key, 2), args.steps + args.warmup + 2)  # vector_env.cpp:202
@@ -265,8 +265,8 @@ def run_gpu_arm(args, rank, world, local_rank):
     clk = clocks.stop() if clocks else None
     step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
     total_ms = float(sum(step_ms))
-    total_ms = D.max_over_ranks(total_ms, device="cuda")  # device time, max over ranks
-    stats = D.all_reduce_episode_stats(venv.episode_stats_raw(), device="cuda")  # the one collective
+    total_ms = shard.max_over_ranks(total_ms, device="cuda")  # device time, max over ranks
+    stats = shard.all_reduce_episode_stats(venv.episode_stats_raw(), device="cuda")  # the one collective
     value = N * A * args.steps / (total_ms * 1e-3)
 
     # roofline of the dominant (only) kernel: algorithmic bytes per launch / mean launch time
@@ -294,7 +294,7 @@ def run_gpu_arm(args, rank, world, local_rank):
         for k in range(e2e_steps):
             venv.host_step_random(akeys[1 + k], host)
         sec = time.perf_counter() - t0
-        sec = D.max_over_ranks(sec, device="cuda")
+        sec = shard.max_over_ranks(sec, device="cuda")
         e2e = {"value": N * A * e2e_steps / sec, "unit": "agent-steps/s",
                "h2d_bytes_per_step": 16, "d2h_bytes_per_step": int(d2h * world),
                "steps": e2e_steps, "path": "marl_venv_step_random_host (C-ABI, pinned host buffers)"}
@@ -326,7 +326,7 @@ def run_gpu_arm(args, rank, world, local_rank):
         "e2e": e2e,
         "gpu_launches": int(launches),
         "clocks": clk,
-        "episode_stats": D.summarize(stats),
+        "episode_stats": shard.summarize(stats),
     }
     print(json.dumps(line))
 

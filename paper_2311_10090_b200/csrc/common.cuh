@@ -80,6 +80,17 @@ MARL_HD Key fold_in(const Key& k, uint64_t d) {
   return key_from_blocks(block_at(k, kFoldBase + 2 * d), block_at(k, kFoldBase + 2 * d + 1));
 }
 
+// Out-of-line variants (~70 instructions per block) for kernels that derive
+// keys at many sites: one copy keeps a large fused kernel inside the
+// instruction cache (the SMAX step kernel).
+__host__ __device__ MARL_NOINLINE inline uint64_t block_at_nl(const Key& k, uint64_t off) { return block_at(k, off); }
+__host__ __device__ MARL_NOINLINE inline Key split_child_nl(const Key& k, uint64_t i) {
+  return key_from_blocks(block_at_nl(k, kSplitBase + 2 * i), block_at_nl(k, kSplitBase + 2 * i + 1));
+}
+__host__ __device__ MARL_NOINLINE inline Key fold_in_nl(const Key& k, uint64_t d) {
+  return key_from_blocks(block_at_nl(k, kFoldBase + 2 * d), block_at_nl(k, kFoldBase + 2 * d + 1));
+}
+
 MARL_HD double to_unit(uint64_t b) { return double(b >> 11) * 0x1.0p-53; }  // prng.cpp:86-89
 
 // Element j of prng::uniform(key, n, lo, hi) (prng.cpp:169-178).

@@ -4,20 +4,37 @@
 // separation, win/draw resolution, shaped rewards, infos, auto-reset and the
 // observation rows (VectorEnv::step body, vector_env.cpp:95-127).
 //
-// Exactness: every fp64 op is the reference's, in its order (-fmad=false).
-// The reference evaluates ~250 glibc hypot() per 3m step, but almost all are
-// only compared against a threshold; those are decided from dx^2+dy^2 outside
-// a 2e-12 relative band (dist_le in common.cuh) and by a glibc-exact hypot
-// inside it, and the hypot *values* the reference uses (separation pushes,
-// nearest-target search) come from the glibc-exact kernel -- so trajectories
-// are bit-identical to the reference at a fraction of its fp64 cost.
+// Execution model: a GROUP of G lanes (G = 8/16/32, inside one warp) owns one
+// env; lane l owns units l and l+G (UPL units per lane).  The env's unit
+// state (x, y, health, cooldown, action, prev_action, fire flag) lives in
+// shared memory for the duration of the step -- every pairwise query (range,
+// sight, nearest target, damage gather, overlap) is a lane reading the
+// others' entries -- and group-scope __syncwarp / __ballot_sync / __shfl_sync
+// separate the phases and carry the ordered reductions.  Per-unit work
+// (heuristic enemy, random-legal draw, cooldown, moves, fire, damage,
+// health/max-health ratios, observation slots, spawn jitter) runs one unit per
+// lane; pair scans are spread evenly over the group's lanes.  The only
+// sequential piece is the reference's Gauss-Seidel separation pass
+// (smax.cpp:542-567), whose result depends on pair order: a parallel ballot
+// first proves the common case "no living pair can overlap" (the pass is then
+// a no-op) and only otherwise one lane replays the exact sequential pass.
 //
-// Layout: one thread owns one env; unit state is [unit][N] structure of
-// arrays in HBM; per-unit and per-type-pair constants sit in shared memory
-// (uniform-index broadcast reads).  Small fixed rosters (<= 17 units) are
-// compile-time specialisations with the whole state in registers; larger or
-// overridden rosters use the dynamic-size instantiation.
+// Exactness: every fp64 op is the reference's, in its order (-fmad=false).
+// Threshold tests on glibc hypot() are decided from dx^2+dy^2 outside a 2e-12
+// relative band and by the glibc-exact hypot inside it (dist_le, common.cuh);
+// so is the nearest-target comparison.  Hypot values that feed arithmetic
+// (separation pushes) use the glibc-exact kernel -- trajectories are
+// bit-identical to the reference.
+//
+// HBM layout: unit state is [unit][N] structure of arrays (a warp's lanes for
+// one unit read consecutive envs: full 32-byte sectors).  Observation rows of
+// a warp's envs are staged in a per-warp shared-memory tile and leave as
+// contiguous (16-byte vector when aligned) streaming stores; no block-wide
+// barrier sits on the step path, so a group stuck in a long separation
+// fixpoint delays only its own warp.
 #include <cuda_runtime.h>
+
+#include <algorithm>
 
 #include "common.cuh"
 #include "engine.h"
@@ -29,685 +46,838 @@ constexpr double kDt = 1.0 / 16.0;  // smax.cpp:17
 constexpr int kTicks = 8;           // smax.cpp:18
 constexpr double kSepTol = 1e-6;    // smax.cpp:19
 constexpr int kNorth = 0, kSouth = 1, kEast = 2, kWest = 3, kStop = 4, kAttackBase = 5;
-constexpr int kMaxU = kSmaxMaxUnits;
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+constexpr int kTypes = 6;
+constexpr int kWarpStageBytes = 8 * 1024;  // observation staging budget per warp
 
-// Per-handle constants, precomputed on the host from SmaxConfig and staged
-// into shared memory by every block.
+struct TypeStat {  // per unit type (smax.cpp:26-33), derived on the host
+  double hmax, dmg, cdmax, spdt, rad, hi;  // spdt = speed * dt, hi = map - radius
+  Thresh sight;
+};
+struct PairStat {  // per (type a, type b)
+  Thresh reach;  // range(a) + radius(a) + radius(b), smax.cpp:497-501
+  Thresh rsum;   // radius(a) + radius(b), smax.cpp:551
+  Thresh otol;   // rsum - 1e-6: the max_overlap tolerance, smax.cpp:565,576
+};
+
+// Per-handle constants, staged into shared memory by every block (~3 KB).
 struct Params {
-  int na, ne, n, A, controlled, max_steps;
+  int na, ne, n, A, controlled, max_steps, D, n_pairs;
   double map, jitter;
-  int8_t type[kMaxU];
-  double hmax[kMaxU], dmg[kMaxU], cdmax[kMaxU], spdt[kMaxU], rad[kMaxU], hi[kMaxU];
-  Thresh sight[kMaxU];
-  Thresh reach[6][6];  // range + radius (shooter type) + radius (target type), smax.cpp:499
-  Thresh rsum[6][6];   // fl(ra + rb), smax.cpp:551
-  Thresh otol[6][6];   // fl(ra + rb) - 1e-6, the max_overlap tolerance, smax.cpp:565,576
+  double sep_r2hi;  // max rsum.r2hi over the roster's type pairs: conservative overlap pre-check
+  double pad;
+  int8_t type[kSmaxMaxUnits];
+  TypeStat ts[kTypes];
+  PairStat ps[kTypes][kTypes];
+};
+static_assert(sizeof(Params) % 16 == 0, "Params is staged with 16-byte copies");
+
+// One env's unit state during a step (shared memory).
+template <int CAP>
+struct EnvSm {
+  double x[CAP], y[CAP], h[CAP], cd[CAP];
+  int act[CAP];
+  int8_t pa[CAP];
+  int8_t fire[CAP];
 };
 
-template <int NA_, int NE_>
-struct Fixed {
-  static constexpr int CAP = NA_ + NE_;
-  static constexpr int UNROLL = NA_ + NE_;  // fully unrolled: state stays in registers
-  __device__ __forceinline__ constexpr int na() const { return NA_; }
-  __device__ __forceinline__ constexpr int ne() const { return NE_; }
-  __device__ __forceinline__ constexpr int n() const { return NA_ + NE_; }
-};
-struct Dyn {
-  static constexpr int CAP = kMaxU;
-  static constexpr int UNROLL = 1;  // runtime-sized loops, state in local memory
-  int na_, ne_;
-  __device__ __forceinline__ int na() const { return na_; }
-  __device__ __forceinline__ int ne() const { return ne_; }
-  __device__ __forceinline__ int n() const { return na_ + ne_; }
-};
-
-template <class Dm>
-struct Units {  // one env's SmaxState (smax.cpp:53-61); winner is -1 between steps
-  double x[Dm::CAP], y[Dm::CAP], h[Dm::CAP], cd[Dm::CAP];
-  int pa[Dm::CAP];  // prev_action
-  int tg[Dm::CAP];  // ai_target
-  int sw[Dm::CAP];  // ai_sweep
-  int t;
-  int winner;
+// A group of G lanes of one warp.
+template <int G>
+struct Grp {
+  int gl;         // lane within the group
+  unsigned mask;  // the group's lanes within the warp
+  __device__ __forceinline__ Grp() {
+    const int lane = threadIdx.x & 31;
+    gl = lane & (G - 1);
+    mask = G == 32 ? 0xffffffffu : (((1u << G) - 1u) << (lane & ~(G - 1)));
+  }
+  __device__ __forceinline__ void sync() const { __syncwarp(mask); }
+  __device__ __forceinline__ bool any(bool p) const { return (__ballot_sync(mask, p) & mask) != 0u; }
+  __device__ __forceinline__ bool all(bool p) const { return (__ballot_sync(mask, p) & mask) == mask; }
+  __device__ __forceinline__ int count(bool p) const { return __popc(__ballot_sync(mask, p) & mask); }
+  __device__ __forceinline__ double bcast(double v, int src) const { return __shfl_sync(mask, v, src, G); }
 };
 
 __device__ __forceinline__ double dclamp(double v, double lo, double hi) {  // std::clamp
   return (v < lo) ? lo : (hi < v) ? hi : v;
 }
 
-template <class Dm>
-__device__ __forceinline__ bool in_range(const Params& P, const Units<Dm>& s, int a, int b) {
-  const Thresh& r = P.reach[P.type[a]][P.type[b]];  // smax.cpp:497-501
-  return dist_le(s.x[a] - s.x[b], s.y[a] - s.y[b], r.r, r.r2lo, r.r2hi);
+template <int CAP>
+__device__ __forceinline__ bool in_range(const Params& P, const EnvSm<CAP>& e, int a, int b) {
+  const Thresh& r = P.ps[P.type[a]][P.type[b]].reach;  // smax.cpp:497-501
+  return dist_le(e.x[a] - e.x[b], e.y[a] - e.y[b], r.r, r.r2lo, r.r2hi);
 }
 
-template <class Dm>
-__device__ __forceinline__ bool sees(const Params& P, const Units<Dm>& s, int a, int b) {
-  const Thresh& r = P.sight[a];  // center_dist(a, b) <= sight(a), smax.cpp:383,613
-  return dist_le(s.x[a] - s.x[b], s.y[a] - s.y[b], r.r, r.r2lo, r.r2hi);
+template <int CAP>
+__device__ __forceinline__ bool sees(const Params& P, const EnvSm<CAP>& e, int a, int b) {
+  const Thresh& r = P.ts[P.type[a]].sight;  // center_dist(a, b) <= sight(a), smax.cpp:383,613
+  return dist_le(e.x[a] - e.x[b], e.y[a] - e.y[b], r.r, r.r2lo, r.r2hi);
 }
 
-// separate (smax.cpp:542-567) and max_overlap (smax.cpp:569-580).
-template <class Dm>
-__device__ __forceinline__ bool overlap_within_tol(const Params& P, const Units<Dm>& s, const Dm& d) {
-#pragma unroll(Dm::UNROLL)
-  for (int a = 0; a < d.n(); ++a) {
-    if (s.h[a] <= 0.0) continue;
-#pragma unroll(Dm::UNROLL)
-    for (int b = a + 1; b < d.n(); ++b) {
-      if (s.h[b] <= 0.0) continue;
-      const Thresh& T = P.otol[P.type[a]][P.type[b]];
-      double dx = s.x[a] - s.x[b], dy = s.y[a] - s.y[b];
-      double d2 = dx * dx + dy * dy;
-      if (d2 > T.r2hi) continue;                 // surely sum - d <= tol
-      if (d2 < T.r2lo) return false;             // surely sum - d > tol
-      double sum = P.rsum[P.type[a]][P.type[b]].r;
-      if (!(sum - hypot_glibc(dx, dy) <= kSepTol)) return false;
+// ------------------------------------------------------------- pair walks
+// Pairs (a, b > a) in the reference's row-major order, dealt round-robin to
+// the G lanes: lane l visits pair indices l, l+G, l+2G, ...
+struct PairIt {
+  int a, b, n;
+  __device__ __forceinline__ PairIt(int first, int n_) : a(0), b(0), n(n_) {
+    int p = first, row = n - 1;
+    while (row > 0 && p >= row) {
+      p -= row;
+      ++a;
+      --row;
+    }
+    b = a + 1 + p;
+  }
+  __device__ __forceinline__ bool valid() const { return a < n - 1 && b < n; }
+  __device__ __forceinline__ void advance(int step) {
+    b += step;
+    while (b >= n && a < n - 1) {  // row a holds b in [a+1, n)
+      ++a;
+      b = b - n + a + 1;
     }
   }
-  return true;
+};
+
+// ---------------------------------------------------------------- separation
+__device__ __forceinline__ unsigned long long bits_above(int i) { return i >= 63 ? 0ull : ~0ull << (i + 1); }
+
+// Unit bitmask (bit u) of a per-unit predicate held by the owning lanes.
+template <int G, int UPL>
+__device__ __forceinline__ unsigned long long unit_mask(const Grp<G>& g, const bool* pred) {
+  const int base = (threadIdx.x & 31) & ~(G - 1);
+  const unsigned gbits = G == 32 ? 0xffffffffu : ((1u << G) - 1u);
+  unsigned long long m = 0;
+#pragma unroll
+  for (int j = 0; j < UPL; ++j)
+    m |= (unsigned long long)((__ballot_sync(g.mask, pred[j]) >> base) & gbits) << (G * j);
+  return m;
 }
 
-template <class Dm>
-__device__ __forceinline__ void separate(const Params& P, Units<Dm>& s, const Dm& d, bool to_fixpoint) {
-  for (int pass = 0; pass < (to_fixpoint ? 256 : 1); ++pass) {
-#pragma unroll(Dm::UNROLL)
-    for (int a = 0; a < d.n(); ++a) {
-      if (s.h[a] <= 0.0) continue;
-#pragma unroll(Dm::UNROLL)
-      for (int b = a + 1; b < d.n(); ++b) {
-        if (s.h[b] <= 0.0) continue;
-        const Thresh& R = P.rsum[P.type[a]][P.type[b]];
-        double dx = s.x[b] - s.x[a], dy = s.y[b] - s.y[a];
-        double d2 = dx * dx + dy * dy;
-        if (d2 > R.r2hi) continue;  // hypot(dx,dy) > ra+rb: overlap <= 0
-        double dd = hypot_glibc(dx, dy);
-        double overlap = R.r - dd;
-        if (overlap <= 0.0) continue;
-        double nx = 1.0, ny = 0.0;
+// One Gauss-Seidel pass of separate() (smax.cpp:542-567), exact, row-parallel.
+// The reference visits pairs (a, b>a) in row-major order and pushes each
+// overlapping pair with the positions current at that moment.  Within row a,
+// the next pair it pushes is the lowest b (after the last push) that overlaps
+// with the CURRENT positions -- nothing moves in between -- so the group tests
+// all remaining b of the row at once (one b per lane, exact hypot test), takes
+// the lowest hit by ballot, lets b's lane apply the reference push, and
+// repeats from there: rounds per row = pushes in the row + 1, and the
+// trajectory is the sequential one bit for bit.
+template <int G, int UPL, int CAP>
+__device__ __forceinline__ void separation_pass(const Params& P, EnvSm<CAP>& e, const Grp<G>& g,
+                                                unsigned long long alive) {
+  const int n = P.n;
+  for (int a = 0; a < n - 1; ++a) {
+    if (!(alive >> a & 1ull)) continue;
+    unsigned long long row = alive & bits_above(a);
+    const int ta = P.type[a];
+    while (row) {  // group-uniform
+      bool hit[UPL];
+      double hdx[UPL], hdy[UPL], hd[UPL];
+      const double xa = e.x[a], ya = e.y[a];
+#pragma unroll
+      for (int j = 0; j < UPL; ++j) {
+        const int b = g.gl + G * j;
+        hit[j] = false;
+        hdx[j] = hdy[j] = hd[j] = 0.0;
+        if (!(row >> b & 1ull)) continue;
+        const double dx = e.x[b] - xa, dy = e.y[b] - ya;
+        const Thresh& R = P.ps[ta][P.type[b]].rsum;
+        if (dx * dx + dy * dy > R.r2hi) continue;  // hypot(dx,dy) > ra+rb: overlap <= 0
+        const double dd = hypot_glibc(dx, dy);
+        hit[j] = R.r - dd > 0.0;
+        hdx[j] = dx;
+        hdy[j] = dy;
+        hd[j] = dd;
+      }
+      const unsigned long long hits = unit_mask<G, UPL>(g, hit);
+      if (!hits) break;
+      const int b = __ffsll((long long)hits) - 1;
+      if (g.gl == (b & (G - 1))) {  // b's lane applies the reference push
+        const int j = b / G;
+        double dx = hdx[0], dy = hdy[0], dd = hd[0];
+#pragma unroll
+        for (int q = 1; q < UPL; ++q)
+          if (j == q) {
+            dx = hdx[q];
+            dy = hdy[q];
+            dd = hd[q];
+          }
+        const double overlap = P.ps[ta][P.type[b]].rsum.r - dd;
+        double nx = 1.0, ny = 0.0;  // coincident centres get a fixed nudge axis
         if (dd > 1e-12) {
           nx = dx / dd;
           ny = dy / dd;
         }
-        double push = 0.5 * overlap;
-        double ra = P.rad[a], rb = P.rad[b];
-        s.x[a] = dclamp(s.x[a] - nx * push, ra, P.hi[a]);
-        s.y[a] = dclamp(s.y[a] - ny * push, ra, P.hi[a]);
-        s.x[b] = dclamp(s.x[b] + nx * push, rb, P.hi[b]);
-        s.y[b] = dclamp(s.y[b] + ny * push, rb, P.hi[b]);
+        const double push = 0.5 * overlap;
+        const TypeStat& A_ = P.ts[ta];
+        const TypeStat& B_ = P.ts[P.type[b]];
+        e.x[a] = dclamp(xa - nx * push, A_.rad, A_.hi);
+        e.y[a] = dclamp(ya - ny * push, A_.rad, A_.hi);
+        e.x[b] = dclamp(e.x[b] + nx * push, B_.rad, B_.hi);
+        e.y[b] = dclamp(e.y[b] + ny * push, B_.rad, B_.hi);
+      }
+      g.sync();
+      row &= bits_above(b);
+    }
+  }
+}
+
+// Does any living pair of this lane's share possibly overlap?  (Conservative:
+// a false "yes" only costs an exact pass that pushes nothing.)
+template <int G, int CAP>
+__device__ __forceinline__ bool lane_pairs_may_overlap(const Params& P, const EnvSm<CAP>& e, int gl) {
+  for (PairIt it(gl, P.n); it.valid(); it.advance(G)) {
+    if (e.h[it.a] <= 0.0 || e.h[it.b] <= 0.0) continue;
+    double dx = e.x[it.b] - e.x[it.a], dy = e.y[it.b] - e.y[it.a];
+    if (!(dx * dx + dy * dy > P.sep_r2hi)) return true;
+  }
+  return false;
+}
+
+// max_overlap(s) <= kSeparationTol restricted to this lane's pairs (smax.cpp:569-580).
+template <int G, int CAP>
+__device__ __forceinline__ bool lane_pairs_within_tol(const Params& P, const EnvSm<CAP>& e, int gl) {
+  for (PairIt it(gl, P.n); it.valid(); it.advance(G)) {
+    const int a = it.a, b = it.b;
+    if (e.h[a] <= 0.0 || e.h[b] <= 0.0) continue;
+    const PairStat& S = P.ps[P.type[a]][P.type[b]];
+    double dx = e.x[a] - e.x[b], dy = e.y[a] - e.y[b];
+    double d2 = dx * dx + dy * dy;
+    if (d2 > S.otol.r2hi) continue;      // surely sum - d <= tol
+    if (d2 < S.otol.r2lo) return false;  // surely sum - d > tol
+    if (!(S.rsum.r - hypot_glibc(dx, dy) <= kSepTol)) return false;
+  }
+  return true;
+}
+
+// separate(s, to_fixpoint), smax.cpp:542-567.  A pass is a no-op exactly when
+// no living pair overlaps, which the parallel pre-check proves in the common
+// case (and then max_overlap <= 0 <= tol ends the fixpoint loop as well).
+template <int G, int UPL, int CAP>
+__device__ __forceinline__ void separate(const Params& P, EnvSm<CAP>& e, const Grp<G>& g, bool fixpoint) {
+  unsigned long long alive = 0;
+  for (int pass = 0; pass < (fixpoint ? 256 : 1); ++pass) {
+    if (!g.any(lane_pairs_may_overlap<G>(P, e, g.gl))) break;
+    if (pass == 0) {  // health is constant during separation
+      bool al[UPL];
+#pragma unroll
+      for (int j = 0; j < UPL; ++j) al[j] = g.gl + G * j < P.n && e.h[g.gl + G * j] > 0.0;
+      alive = unit_mask<G, UPL>(g, al);
+    }
+    separation_pass<G, UPL>(P, e, g, alive);
+    if (!fixpoint) break;
+    if (g.all(lane_pairs_within_tol<G>(P, e, g.gl))) break;
+  }
+}
+
+// ------------------------------------------------------------- unit logic
+// uniform1(key, lo, hi) (prng.cpp:169-178) through the out-of-line block.
+__device__ __forceinline__ double uniform_at_nl(const Key& k, double lo, double hi) {
+  double v = lo + to_unit(block_at_nl(k, 0)) * (hi - lo);
+  if (v >= hi) v = nextafter(hi, lo);
+  return v;
+}
+
+// Spawn of unit u: spawn_clusters / place_jittered (smax.cpp:448-454,481-492).
+template <int CAP>
+__device__ __forceinline__ void spawn_unit(const Params& P, EnvSm<CAP>& e, int u, const Key& key) {
+  const bool ally = u < P.na;
+  const int i = ally ? u : u - P.na;
+  double bx = ally ? 0.25 * P.map - 1.5 * (i / 5) : 0.75 * P.map + 1.5 * (i / 5);
+  double by = 0.5 * P.map + 1.5 * (i % 5 - 2);
+  if (P.jitter > 0.0) {
+    bx += uniform_at_nl(fold_in_nl(key, 3000 + 2 * uint64_t(u)), -P.jitter, P.jitter);
+    by += uniform_at_nl(fold_in_nl(key, 3001 + 2 * uint64_t(u)), -P.jitter, P.jitter);
+  }
+  const TypeStat& t = P.ts[P.type[u]];
+  e.x[u] = dclamp(bx, t.rad, t.hi);
+  e.y[u] = dclamp(by, t.rad, t.hi);
+  e.h[u] = t.hmax;
+  e.cd[u] = 0.0;
+  e.pa[u] = int8_t(kStop);
+}
+
+// The pick-th legal action of unit u (smax.cpp:195-211 with legal_uniform,
+// vector_env.cpp:21-32).  Legal order: moves 0-3, stop, attacks on living
+// opponents in range; a dead unit's only legal action is stop.
+template <int CAP>
+__device__ __forceinline__ int random_legal(const Params& P, const EnvSm<CAP>& e, int u, const Key& ek) {
+  if (e.h[u] <= 0.0) return kStop;
+  const bool ally = u < P.na;
+  const int opp0 = ally ? P.na : 0, opp_n = ally ? P.ne : P.na;
+  uint64_t att = 0;
+  for (int k = 0; k < opp_n; ++k) {
+    const int o = opp0 + k;
+    if (e.h[o] > 0.0 && in_range(P, e, u, o)) att |= uint64_t(1) << k;
+  }
+  int pick = int(mod_small(block_at_nl(ek, uint64_t(u)), uint32_t(kAttackBase + __popcll(att))));
+  if (pick < kAttackBase) return pick;
+  for (pick -= kAttackBase; pick > 0; --pick) att &= att - 1;  // drop the lowest set bits
+  return kAttackBase + __ffsll((long long)att) - 1;
+}
+
+// Is hypot(dxa, dya) < hypot(dxb, dyb)?  Decided from the squared lengths
+// outside a 2e-12 relative band (both hypots are within an ulp of the true
+// lengths), by the glibc-exact hypot inside it.
+__device__ __forceinline__ bool hypot_less(double dxa, double dya, double d2a, double dxb, double dyb, double d2b) {
+  if (d2a < d2b * (1.0 - 2e-12)) return true;
+  if (d2a > d2b * (1.0 + 2e-12)) return false;
+  return hypot_glibc(dxa, dya) < hypot_glibc(dxb, dyb);
+}
+
+// heuristic_action (smax.cpp:374-419) of unit u on the pre-step state.
+template <int CAP>
+__device__ __forceinline__ int heuristic(const Params& P, const EnvSm<CAP>& e, int u, int& target, int& sweep) {
+  if (e.h[u] <= 0.0) return kStop;
+  const int team = u < P.na ? 0 : 1;
+  const int opp0 = team == 0 ? P.na : 0, opp_n = team == 0 ? P.ne : P.na;
+  if (target < 0 || target >= opp_n || !(e.h[opp0 + target] > 0.0 && sees(P, e, u, opp0 + target))) {
+    target = -1;
+    for (int k = 0; k < opp_n; ++k) {  // lowest-index opponent already in reach
+      const int o = opp0 + k;
+      if (e.h[o] > 0.0 && sees(P, e, u, o) && in_range(P, e, u, o)) {
+        target = k;
+        break;
       }
     }
-    if (!to_fixpoint || overlap_within_tol(P, s, d)) break;
-  }
-}
-
-// SmaxEnv::reset (smax.cpp:163-193) with fixed-roster cluster spawns
-// (spawn_clusters / place_jittered, smax.cpp:448-454,481-492).
-template <class Dm>
-__device__ __forceinline__ void env_reset(const Params& P, Units<Dm>& s, const Dm& d, const Key& key) {
-#pragma unroll(Dm::UNROLL)
-  for (int u = 0; u < d.n(); ++u) {
-    const bool ally = u < d.na();
-    const int i = ally ? u : u - d.na();
-    double bx = ally ? 0.25 * P.map - 1.5 * (i / 5) : 0.75 * P.map + 1.5 * (i / 5);
-    double by = 0.5 * P.map + 1.5 * (i % 5 - 2);
-    if (P.jitter > 0.0) {
-      bx += uniform_at(fold_in(key, 3000 + 2 * uint64_t(u)), 0, -P.jitter, P.jitter);
-      by += uniform_at(fold_in(key, 3001 + 2 * uint64_t(u)), 0, -P.jitter, P.jitter);
-    }
-    s.x[u] = dclamp(bx, P.rad[u], P.hi[u]);
-    s.y[u] = dclamp(by, P.rad[u], P.hi[u]);
-    s.h[u] = P.hmax[u];
-    s.cd[u] = 0.0;
-    s.pa[u] = kStop;
-    s.tg[u] = -1;
-    s.sw[u] = -1;
-  }
-  s.t = 0;
-  s.winner = -1;
-  separate(P, s, d, true);
-}
-
-// Legal-action count and the pick-th legal action (smax.cpp:195-211 with
-// legal_uniform, vector_env.cpp:21-32).  Legal order: moves 0-3, stop, then
-// attacks on living opponents in range.
-template <class Dm>
-__device__ __forceinline__ int random_legal(const Params& P, const Units<Dm>& s, const Dm& d, int u,
-                                            const Key& ek, int j) {
-  if (s.h[u] <= 0.0) return kStop;  // only stop is legal: bits % 1 == 0
-  const bool ally = u < d.na();
-  const int opp0 = ally ? d.na() : 0, opp_n = ally ? d.ne() : d.na();
-  uint64_t att = 0;  // bitmask of attackable opponents
-  int n_att = 0;
-#pragma unroll(Dm::UNROLL)
-  for (int k = 0; k < opp_n; ++k) {
-    int o = opp0 + k;
-    if (s.h[o] > 0.0 && in_range(P, s, u, o)) {
-      att |= uint64_t(1) << k;
-      ++n_att;
-    }
-  }
-  int pick = int(mod_small(block_at(ek, uint64_t(j)), uint32_t(kAttackBase + n_att)));
-  if (pick < kAttackBase) return pick;
-  pick -= kAttackBase;
-  for (int k = 0; k < 64; ++k) {
-    if (att & (uint64_t(1) << k)) {
-      if (pick == 0) return kAttackBase + k;
-      --pick;
-    }
-  }
-  return kStop;  // unreachable
-}
-
-// heuristic_action (smax.cpp:374-419) on the pre-step state.
-template <class Dm>
-__device__ __forceinline__ int heuristic(const Params& P, const Units<Dm>& s, const Dm& d, int u,
-                                         int& target, int& sweep) {
-  if (s.h[u] <= 0.0) return kStop;
-  const int team = u < d.na() ? 0 : 1;
-  const int opp0 = team == 0 ? d.na() : 0, opp_n = team == 0 ? d.ne() : d.na();
-  bool keep = false;
-  if (target >= 0 && target < opp_n) {
-#pragma unroll(Dm::UNROLL)
-    for (int k = 0; k < opp_n; ++k)
-      if (k == target) keep = s.h[opp0 + k] > 0.0 && sees(P, s, u, opp0 + k);
-  }
-  if (!keep) {
-    target = -1;
-#pragma unroll(Dm::UNROLL)
-    for (int k = 0; k < opp_n; ++k) {
-      if (target >= 0) continue;
-      int o = opp0 + k;
-      if (s.h[o] > 0.0 && sees(P, s, u, o) && in_range(P, s, u, o)) target = k;
-    }
-    if (target < 0) {
-      double best = 0.0;
-#pragma unroll(Dm::UNROLL)
+    if (target < 0) {  // otherwise the nearest visible one (first of equals)
+      double bdx = 0.0, bdy = 0.0, bd2 = 0.0;
       for (int k = 0; k < opp_n; ++k) {
-        int o = opp0 + k;
-        if (!(s.h[o] > 0.0 && sees(P, s, u, o))) continue;
-        double dd = hypot_glibc(s.x[u] - s.x[o], s.y[u] - s.y[o]);
-        if (target < 0 || dd < best) {
+        const int o = opp0 + k;
+        if (!(e.h[o] > 0.0 && sees(P, e, u, o))) continue;
+        const double dx = e.x[u] - e.x[o], dy = e.y[u] - e.y[o], d2 = dx * dx + dy * dy;
+        if (target < 0 || hypot_less(dx, dy, d2, bdx, bdy, bd2)) {
           target = k;
-          best = dd;
+          bdx = dx;
+          bdy = dy;
+          bd2 = d2;
         }
       }
     }
   }
   if (target >= 0) {
-    double xo = 0.0, yo = 0.0;
-    bool in_reach = false;
-#pragma unroll(Dm::UNROLL)
-    for (int k = 0; k < opp_n; ++k)
-      if (k == target) {
-        xo = s.x[opp0 + k];
-        yo = s.y[opp0 + k];
-        in_reach = in_range(P, s, u, opp0 + k);
-      }
-    if (in_reach) return kAttackBase + target;
-    double dx = xo - s.x[u];
-    double dy = yo - s.y[u];
+    const int o = opp0 + target;
+    if (in_range(P, e, u, o)) return kAttackBase + target;
+    double dx = e.x[o] - e.x[u];
+    double dy = e.y[o] - e.y[u];
     if (fabs(dx) >= fabs(dy)) return dx > 0 ? kEast : kWest;
     return dy > 0 ? kNorth : kSouth;
   }
   if (sweep < 0) sweep = team == 0 ? kEast : kWest;
-  if (s.x[u] <= 1.0) sweep = kEast;
-  if (s.x[u] >= P.map - 1.0) sweep = kWest;
+  if (e.x[u] <= 1.0) sweep = kEast;
+  if (e.x[u] >= P.map - 1.0) sweep = kWest;
   return sweep;
 }
 
-// simulate_tick (smax.cpp:503-537).
-template <class Dm>
-__device__ __forceinline__ void tick(const Params& P, Units<Dm>& s, const Dm& d, const int* act,
-                                     bool final_tick) {
-#pragma unroll(Dm::UNROLL)
-  for (int u = 0; u < d.n(); ++u)
-    if (s.h[u] > 0.0) {
-      double v = s.cd[u] - kDt;
-      s.cd[u] = (0.0 < v) ? v : 0.0;  // std::max(0.0, v)
+// simulate_tick (smax.cpp:503-537), one unit per lane per phase.
+template <int G, int UPL, int CAP>
+__device__ __forceinline__ void tick(const Params& P, EnvSm<CAP>& e, const Grp<G>& g, bool final_tick) {
+  // weapons recharge, then moves: each lane touches only its own units
+#pragma unroll
+  for (int j = 0; j < UPL; ++j) {
+    const int u = g.gl + G * j;
+    if (u >= P.n || e.h[u] <= 0.0) continue;
+    double v = e.cd[u] - kDt;
+    e.cd[u] = (0.0 < v) ? v : 0.0;  // std::max(0.0, v)
+    const int a = e.act[u];
+    if (a > kWest) continue;
+    const TypeStat& t = P.ts[P.type[u]];
+    const double dxs = a == kEast ? 1.0 : a == kWest ? -1.0 : 0.0;    // kDirX
+    const double dys = a == kNorth ? 1.0 : a == kSouth ? -1.0 : 0.0;  // kDirY
+    e.x[u] = dclamp(e.x[u] + t.spdt * dxs, t.rad, t.hi);
+    e.y[u] = dclamp(e.y[u] + t.spdt * dys, t.rad, t.hi);
+  }
+  g.sync();
+  // simultaneous fire against the tick-start health snapshot (health is not
+  // written until every shooter has been resolved)
+#pragma unroll
+  for (int j = 0; j < UPL; ++j) {
+    const int u = g.gl + G * j;
+    if (u >= P.n) continue;
+    bool fire = false;
+    const int a = e.act[u];
+    if (a >= kAttackBase && e.h[u] > 0.0) {
+      const int o = (u < P.na ? P.na : 0) + (a - kAttackBase);
+      fire = e.h[o] > 0.0 && !(e.cd[u] > 0.0) && in_range(P, e, u, o);
+      if (fire) e.cd[u] = P.ts[P.type[u]].cdmax;
     }
-#pragma unroll(Dm::UNROLL)
-  for (int u = 0; u < d.n(); ++u) {
-    if (s.h[u] <= 0.0 || act[u] > kWest) continue;
-    const double dxs = act[u] == kEast ? 1.0 : act[u] == kWest ? -1.0 : 0.0;  // kDirX
-    const double dys = act[u] == kNorth ? 1.0 : act[u] == kSouth ? -1.0 : 0.0;  // kDirY
-    s.x[u] = dclamp(s.x[u] + P.spdt[u] * dxs, P.rad[u], P.hi[u]);
-    s.y[u] = dclamp(s.y[u] + P.spdt[u] * dys, P.rad[u], P.hi[u]);
+    e.fire[u] = fire;
   }
-  // simultaneous fire against the tick-start health snapshot
-  double h0[Dm::CAP];
-  bool fire[Dm::CAP];
-#pragma unroll(Dm::UNROLL)
-  for (int u = 0; u < d.n(); ++u) h0[u] = s.h[u];
-#pragma unroll(Dm::UNROLL)
-  for (int u = 0; u < d.n(); ++u) {
-    fire[u] = false;
-    if (h0[u] <= 0.0 || act[u] < kAttackBase) continue;
-    const int opp0 = u < d.na() ? d.na() : 0;
-    const int o = opp0 + (act[u] - kAttackBase);
-    double ho = 0.0;
-    bool rng = false;
-#pragma unroll(Dm::UNROLL)
-    for (int q = 0; q < d.n(); ++q)
-      if (q == o) {
-        ho = h0[q];
-        if (ho > 0.0) rng = in_range(P, s, u, q);
-      }
-    if (ho <= 0.0 || !rng) continue;
-    if (s.cd[u] > 0.0) continue;
-    fire[u] = true;
-    s.cd[u] = P.cdmax[u];
-  }
-#pragma unroll(Dm::UNROLL)
-  for (int o = 0; o < d.n(); ++o) {
+  g.sync();
+  double newh[UPL];
+#pragma unroll
+  for (int j = 0; j < UPL; ++j) {
+    const int o = g.gl + G * j;
+    newh[j] = -1.0;
+    if (o >= P.n) continue;
+    // o's shooters are its opponents; `me` is o's index among THEIR opponents
+    const int opp0 = o < P.na ? P.na : 0, opp_n = o < P.na ? P.ne : P.na;
+    const int me = o < P.na ? o : o - P.na;
     double damage = 0.0;
-#pragma unroll(Dm::UNROLL)
-    for (int u = 0; u < d.n(); ++u) {
-      if (!fire[u]) continue;
-      const int opp0 = u < d.na() ? d.na() : 0;
-      if (opp0 + (act[u] - kAttackBase) == o) damage += P.dmg[u];
+    for (int k = 0; k < opp_n; ++k) {  // shooters in unit order
+      const int u = opp0 + k;
+      if (e.fire[u] && e.act[u] - kAttackBase == me) damage += P.ts[P.type[u]].dmg;
     }
     if (damage > 0.0) {
-      double v = h0[o] - damage;
-      s.h[o] = (0.0 < v) ? v : 0.0;
+      double v = e.h[o] - damage;
+      newh[j] = (0.0 < v) ? v : 0.0;
     }
   }
-  separate(P, s, d, final_tick);
+  g.sync();
+#pragma unroll
+  for (int j = 0; j < UPL; ++j)
+    if (newh[j] >= 0.0) e.h[g.gl + G * j] = newh[j];
+  g.sync();
+  separate<G, UPL>(P, e, g, final_tick);
 }
 
-template <class Dm>
-__device__ __forceinline__ double pool(const Params& P, const Units<Dm>& s, const Dm& d, int team) {
-  double total = 0.0;  // smax.cpp:365-372
-#pragma unroll(Dm::UNROLL)
-  for (int u = 0; u < d.n(); ++u) {
-    if ((u < d.na()) != (team == 0)) continue;
-    total += s.h[u] / P.hmax[u];
-    total += s.h[u] > 0.0 ? 1.0 : 0.0;
+// pool(s, 0) and pool(s, 1) (smax.cpp:365-372): the per-unit ratios are one
+// division per lane; the sums run in the reference's unit order over
+// shuffled values.
+template <int G, int UPL, int CAP>
+__device__ __forceinline__ void pools(const Params& P, const EnvSm<CAP>& e, const Grp<G>& g, double& p0, double& p1) {
+  double ratio[UPL];
+#pragma unroll
+  for (int j = 0; j < UPL; ++j) {
+    const int u = g.gl + G * j;
+    ratio[j] = u < P.n ? e.h[u] / P.ts[P.type[u]].hmax : 0.0;
   }
-  return total;
+  p0 = 0.0;
+  p1 = 0.0;
+#pragma unroll
+  for (int j = 0; j < UPL; ++j) {
+    for (int l = 0; l < G; ++l) {
+      const int u = l + G * j;
+      const double r = g.bcast(ratio[j], l);  // group-uniform loop: every lane shuffles
+      if (u >= P.n) continue;
+      const double alive = e.h[u] > 0.0 ? 1.0 : 0.0;
+      if (u < P.na) {
+        p0 += r;
+        p0 += alive;
+      } else {
+        p1 += r;
+        p1 += alive;
+      }
+    }
+  }
 }
 
-// observe (smax.cpp:601-634) for agent `me` into a row of D floats.
-template <class Dm>
-__device__ __forceinline__ void observe(const Params& P, const Units<Dm>& s, const Dm& d, int me, float* o) {
-  const int D = 10 + 17 * (d.n() - 1);
-  if (s.h[me] <= 0.0) {
-    for (int k = 0; k < D; ++k) o[k] = 0.0f;
-    return;
+// Observation slot of unit u in `me`'s row: teammates (index order, minus
+// me), then opponents (smax.cpp:628-632).
+__device__ __forceinline__ int obs_slot(const Params& P, int me, int u) {
+  const bool me_ally = me < P.na, u_ally = u < P.na;
+  if (me_ally == u_ally) {
+    const int base = me_ally ? 0 : P.na;
+    return (u - base) - (u > me ? 1 : 0);
   }
-  const double sight = P.sight[me].r;
-  int k = 0;
-  o[k++] = float(s.h[me] / P.hmax[me]);
-  o[k++] = float(s.cd[me] / P.cdmax[me]);
-  o[k++] = float(s.x[me] / P.map);
-  o[k++] = float(s.y[me] / P.map);
-#pragma unroll(Dm::UNROLL)
-  for (int q = 0; q < 6; ++q) o[k++] = q == P.type[me] ? 1.0f : 0.0f;
-  const bool me_ally = me < d.na();
-#pragma unroll(Dm::UNROLL)
-  for (int pass = 0; pass < 2; ++pass) {
-#pragma unroll(Dm::UNROLL)
-    for (int u = 0; u < d.n(); ++u) {
-      const bool same = (u < d.na()) == me_ally;
-      if (pass == 0 ? (u == me || !same) : same) continue;
-      if (!(s.h[u] > 0.0 && sees(P, s, me, u))) {
-#pragma unroll(Dm::UNROLL)
-        for (int q = 0; q < 17; ++q) o[k + q] = 0.0f;
-        k += 17;
+  const int n_team = me_ally ? P.na : P.ne;
+  return n_team - 1 + (u_ally ? u : u - P.na);
+}
+
+// This lane's part of observe(s, me) (smax.cpp:601-634) into row[D].
+template <int G, int UPL, int CAP>
+__device__ __forceinline__ void observe_part(const Params& P, const EnvSm<CAP>& e, int gl, int me, float* row) {
+  const bool me_alive = e.h[me] > 0.0;
+  const TypeStat& my = P.ts[P.type[me]];
+#pragma unroll
+  for (int j = 0; j < UPL; ++j) {
+    const int u = gl + G * j;
+    if (u >= P.n) continue;
+    if (u == me) {
+      float* o = row;
+      if (!me_alive) {
+#pragma unroll
+        for (int k = 0; k < 10; ++k) o[k] = 0.0f;
         continue;
       }
-      o[k++] = 1.0f;
-      o[k++] = float((s.x[u] - s.x[me]) / sight);
-      o[k++] = float((s.y[u] - s.y[me]) / sight);
-      o[k++] = float(s.h[u] / P.hmax[u]);
-      o[k++] = float(s.cd[u] / P.cdmax[u]);
-#pragma unroll(Dm::UNROLL)
-      for (int q = 0; q < 6; ++q) o[k++] = q == P.type[u] ? 1.0f : 0.0f;
-      const int bucket = s.pa[u] <= kStop ? s.pa[u] : kStop + 1;  // smax.cpp:589
-#pragma unroll(Dm::UNROLL)
-      for (int q = 0; q < 6; ++q) o[k++] = q == bucket ? 1.0f : 0.0f;
+      o[0] = float(e.h[me] / my.hmax);
+      o[1] = float(e.cd[me] / my.cdmax);
+      o[2] = float(e.x[me] / P.map);
+      o[3] = float(e.y[me] / P.map);
+#pragma unroll
+      for (int q = 0; q < kTypes; ++q) o[4 + q] = q == P.type[me] ? 1.0f : 0.0f;
+      continue;
     }
+    float* o = row + 10 + 17 * obs_slot(P, me, u);
+    if (!(me_alive && e.h[u] > 0.0 && sees(P, e, me, u))) {
+#pragma unroll
+      for (int q = 0; q < 17; ++q) o[q] = 0.0f;
+      continue;
+    }
+    const TypeStat& st = P.ts[P.type[u]];
+    const double sight = my.sight.r;
+    o[0] = 1.0f;
+    o[1] = float((e.x[u] - e.x[me]) / sight);
+    o[2] = float((e.y[u] - e.y[me]) / sight);
+    o[3] = float(e.h[u] / st.hmax);
+    o[4] = float(e.cd[u] / st.cdmax);
+    const int tu = P.type[u];
+#pragma unroll
+    for (int q = 0; q < kTypes; ++q) o[5 + q] = q == tu ? 1.0f : 0.0f;
+    const int bucket = e.pa[u] <= kStop ? e.pa[u] : kStop + 1;  // action_bucket, smax.cpp:589
+#pragma unroll
+    for (int q = 0; q < 6; ++q) o[11 + q] = q == bucket ? 1.0f : 0.0f;
   }
 }
 
-template <class Dm>
-__device__ __forceinline__ void load_units(Units<Dm>& s, const SmaxState& st, const Dm& d, int64_t i, int64_t n) {
-#pragma unroll(Dm::UNROLL)
-  for (int u = 0; u < d.n(); ++u) {
-    s.x[u] = st.x[u * n + i];
-    s.y[u] = st.y[u * n + i];
-    s.h[u] = st.health[u * n + i];
-    s.cd[u] = st.cooldown[u * n + i];
-    uint32_t m = st.mem[u * n + i];
-    s.pa[u] = int(m & 0xffu);
-    s.tg[u] = int(int8_t((m >> 8) & 0xffu));
-    s.sw[u] = int(int8_t((m >> 16) & 0xffu));
-  }
-  s.t = st.t[i];
-  s.winner = -1;
-}
-
-template <class Dm>
-__device__ __forceinline__ void store_units(const Units<Dm>& s, const SmaxState& st, const Dm& d, int64_t i, int64_t n) {
-#pragma unroll(Dm::UNROLL)
-  for (int u = 0; u < d.n(); ++u) {
-    st.x[u * n + i] = s.x[u];
-    st.y[u * n + i] = s.y[u];
-    st.health[u * n + i] = s.h[u];
-    st.cooldown[u * n + i] = s.cd[u];
-    st.mem[u * n + i] = uint32_t(s.pa[u] & 0xff) | (uint32_t(uint8_t(int8_t(s.tg[u]))) << 8) |
-                        (uint32_t(uint8_t(int8_t(s.sw[u]))) << 16);
-  }
-  st.t[i] = s.t;
-}
-
-// Dynamic shared memory carve-up shared by the reset and step kernels.
-struct Smem {
-  Params* P;
-  float* row;      // [T][D]
-  double* rew;     // [T][A]
-  double* inf;     // [T][A][3]
-  int32_t* act;    // [T][A]
-  uint8_t* done;   // [T][A+1]
-  uint8_t* fin;    // [T]
+// ---------------------------------------------------------- warp plumbing
+struct Plan {  // host-chosen launch shape, passed by value
+  int rb;      // agent rows staged per env per round (A when everything fits)
 };
 
-__host__ __device__ inline size_t align16(size_t b) { return (b + 15) & ~size_t(15); }
+__host__ __device__ inline size_t a16(size_t b) { return (b + 15) & ~size_t(15); }
 
-__host__ __device__ inline size_t smem_bytes(int T, int D, int A) {
-  return align16(sizeof(Params)) + align16(size_t(T) * D * 4) + align16(size_t(T) * A * 8) +
-         align16(size_t(T) * A * 24) + align16(size_t(T) * A * 4) + align16(size_t(T) * (A + 1)) +
-         align16(size_t(T));
+template <int G>
+__host__ __device__ inline size_t warp_tile_floats(int D, int rb) {
+  return (size_t(32 / G) * rb * D + 3) & ~size_t(3);
 }
 
-__device__ __forceinline__ Smem carve(uint8_t* base, int T, int D, int A) {
-  Smem m;
-  size_t off = 0;
-  m.P = reinterpret_cast<Params*>(base + off);
-  off += align16(sizeof(Params));
-  m.row = reinterpret_cast<float*>(base + off);
-  off += align16(size_t(T) * D * 4);
-  m.rew = reinterpret_cast<double*>(base + off);
-  off += align16(size_t(T) * A * 8);
-  m.inf = reinterpret_cast<double*>(base + off);
-  off += align16(size_t(T) * A * 24);
-  m.act = reinterpret_cast<int32_t*>(base + off);
-  off += align16(size_t(T) * A * 4);
-  m.done = base + off;
-  off += align16(size_t(T) * (A + 1));
-  m.fin = base + off;
-  return m;
+template <int G, int UPL>
+__host__ __device__ inline size_t smem_bytes(int D, int rb) {
+  constexpr int EPB = kThreads / G, CAP = G * UPL;
+  return a16(sizeof(Params)) + a16(EPB * sizeof(EnvSm<CAP>)) + kWarps * warp_tile_floats<G>(D, rb) * 4;
 }
 
-__device__ __forceinline__ void stage_params(Params* dst, const Params* src) {
-  const int words = int(sizeof(Params) / 4);
-  const int* s = reinterpret_cast<const int*>(src);
-  int* d = reinterpret_cast<int*>(dst);
+__device__ __forceinline__ void stage_params(Params* dst, const Params* __restrict__ src) {
+  const int words = int(sizeof(Params) / 16);
+  const int4* s = reinterpret_cast<const int4*>(src);
+  int4* d = reinterpret_cast<int4*>(dst);
+#pragma unroll 1
   for (int q = threadIdx.x; q < words; q += blockDim.x) d[q] = __ldg(s + q);
   __syncthreads();
 }
 
-// Copy agent a's rows of this block's envs from the staging tile to global
-// obs rows ([N][A][D] layout: rows of one agent are D floats at stride A*D).
-__device__ __forceinline__ void store_agent_rows(float* gobs, const float* tile, int nvalid, int D,
-                                                 int A, int a, const uint8_t* mask) {
-  for (int idx = threadIdx.x; idx < nvalid * D; idx += blockDim.x) {
-    int e = idx / D, k = idx - e * D;
-    if (mask && !mask[e]) continue;
-    __stcs(gobs + (size_t(e) * A + a) * D + k, tile[idx]);
+// Copy nfloats from shared to global with one warp: 16-byte vectors when both
+// ends are 16-byte aligned, else 4-byte words.
+__device__ __forceinline__ void warp_store(float* __restrict__ gdst, const float* src, int nfloats) {
+  const int lane = threadIdx.x & 31;
+  if (((reinterpret_cast<uintptr_t>(gdst) | reinterpret_cast<uintptr_t>(src)) & 15) == 0) {
+    const int nv = nfloats >> 2;
+    const float4* s4 = reinterpret_cast<const float4*>(src);
+    float4* d4 = reinterpret_cast<float4*>(gdst);
+#pragma unroll 1
+    for (int q = lane; q < nv; q += 32) __stcs(d4 + q, s4[q]);
+#pragma unroll 1
+    for (int q = (nv << 2) + lane; q < nfloats; q += 32) __stcs(gdst + q, src[q]);
+  } else {
+#pragma unroll 1
+    for (int q = lane; q < nfloats; q += 32) __stcs(gdst + q, src[q]);
   }
 }
 
-template <class Dm>
-struct DimsOf;
-template <int NA_, int NE_>
-struct DimsOf<Fixed<NA_, NE_>> {
-  __device__ static Fixed<NA_, NE_> make(const Params&) { return {}; }
-};
-template <>
-struct DimsOf<Dyn> {
-  __device__ static Dyn make(const Params& P) { return Dyn{P.na, P.ne}; }
+// All observation rows of the warp's envs -> gdst ([N][A][D]).  Warp-uniform
+// call; `active` says whether this lane's group builds rows, `sel` (bitmask
+// over the warp's EPW env slots) which envs are stored.
+template <int G, int UPL, int CAP>
+__device__ __noinline__ void emit_obs(const Params& P, const EnvSm<CAP>& e, const Grp<G>& g, bool active,
+                                         float* tile, float* __restrict__ gdst, int64_t w0, int wvalid, int rb,
+                                         unsigned sel) {
+  constexpr int EPW = 32 / G;
+  const int A = P.A, D = P.D;
+  const int wslot = (threadIdx.x & 31) / G;
+  for (int a0 = 0; a0 < A; a0 += rb) {
+    const int rows = min(rb, A - a0);
+    if (active)
+      for (int r = 0; r < rows; ++r) observe_part<G, UPL>(P, e, g.gl, a0 + r, tile + (size_t(wslot) * rows + r) * D);
+    __syncwarp();
+    const int run = rows * D;
+    if (rows == A && sel == (1u << EPW) - 1u) {  // the warp's rows are one contiguous run
+      warp_store(gdst + w0 * A * D, tile, wvalid * run);
+    } else {
+      for (int s = 0; s < wvalid; ++s)
+        if (sel >> s & 1u) warp_store(gdst + ((w0 + s) * A + a0) * D, tile + size_t(s) * run, run);
+    }
+    __syncwarp();
+  }
+}
+
+template <int G, int UPL, int CAP>
+__device__ __forceinline__ void load_env(const Params& P, EnvSm<CAP>& e, const SmaxState& st, int gl, int64_t i,
+                                         int64_t n, int* tg, int* sw) {
+#pragma unroll
+  for (int j = 0; j < UPL; ++j) {
+    const int u = gl + G * j;
+    tg[j] = -1;
+    sw[j] = -1;
+    if (u >= P.n) continue;
+    e.x[u] = st.x[u * n + i];
+    e.y[u] = st.y[u * n + i];
+    e.h[u] = st.health[u * n + i];
+    e.cd[u] = st.cooldown[u * n + i];
+    const uint32_t m = st.mem[u * n + i];  // prev_action | ai_target<<8 | ai_sweep<<16
+    e.pa[u] = int8_t(m & 0xffu);
+    tg[j] = int(int8_t((m >> 8) & 0xffu));
+    sw[j] = int(int8_t((m >> 16) & 0xffu));
+  }
+}
+
+template <int G, int UPL, int CAP>
+__device__ __forceinline__ void store_env(const Params& P, const EnvSm<CAP>& e, const SmaxState& st, int gl,
+                                          int64_t i, int64_t n, const int* tg, const int* sw) {
+#pragma unroll
+  for (int j = 0; j < UPL; ++j) {
+    const int u = gl + G * j;
+    if (u >= P.n) continue;
+    st.x[u * n + i] = e.x[u];
+    st.y[u * n + i] = e.y[u];
+    st.health[u * n + i] = e.h[u];
+    st.cooldown[u * n + i] = e.cd[u];
+    st.mem[u * n + i] = uint32_t(uint8_t(e.pa[u])) | (uint32_t(uint8_t(int8_t(tg[j]))) << 8) |
+                        (uint32_t(uint8_t(int8_t(sw[j]))) << 16);
+  }
+}
+
+// SmaxEnv::reset (smax.cpp:163-193): spawns (one unit per lane), separation
+// to the fixpoint, fresh heuristic memory.
+template <int G, int UPL, int CAP>
+__device__ __noinline__ void env_reset(const Params& P, EnvSm<CAP>& e, const Grp<G>& g, const Key& key, int* tg,
+                                          int* sw) {
+#pragma unroll
+  for (int j = 0; j < UPL; ++j) {
+    const int u = g.gl + G * j;
+    tg[j] = -1;
+    sw[j] = -1;
+    if (u < P.n) spawn_unit(P, e, u, key);
+  }
+  g.sync();
+  separate<G, UPL>(P, e, g, true);
+}
+
+struct Smem {
+  uint8_t* envs;
+  float* tile;  // this warp's staging tile
 };
 
-template <class Dm>
-__global__ void smax_reset_kernel(const Params* __restrict__ gP, SmaxState st, LaunchCommon lc, Key key,
-                                  Key carry_parent) {
+template <int G, int UPL>
+__device__ __forceinline__ Smem carve(uint8_t* base, int D, int rb) {
+  constexpr int EPB = kThreads / G, CAP = G * UPL;
+  Smem m;
+  m.envs = base + a16(sizeof(Params));
+  float* tiles = reinterpret_cast<float*>(m.envs + a16(EPB * sizeof(EnvSm<CAP>)));
+  m.tile = tiles + (threadIdx.x >> 5) * warp_tile_floats<G>(D, rb);
+  return m;
+}
+
+template <int G, int UPL>
+__global__ void __launch_bounds__(kThreads) smax_reset_kernel(const Params* __restrict__ gP, SmaxState st,
+                                                              LaunchCommon lc, Key key, Key carry_parent, Plan plan) {
+  constexpr int EPB = kThreads / G, EPW = 32 / G, CAP = G * UPL;
   extern __shared__ __align__(16) uint8_t smem[];
-  const int T = blockDim.x;
-  Smem m = carve(smem, T, 1, 1);  // params only; rows are staged below
-  stage_params(m.P, gP);
-  const Params& P = *m.P;
-  const Dm d = DimsOf<Dm>::make(P);
-  const int A = P.A, D = 10 + 17 * (P.n - 1);
-  float* tile = reinterpret_cast<float*>(smem + align16(sizeof(Params)));
-  const int64_t i0 = int64_t(blockIdx.x) * T, i = i0 + threadIdx.x;
-  const int nvalid = int(min64(T, lc.n - i0));
-  Units<Dm> s;
-  if (i < lc.n) {
-    const uint64_t g = uint64_t(lc.offset + i);
-    env_reset(P, s, d, split_child(key, g));
-    Key c = split_child(carry_parent, g);
-    lc.carry.keys[i] = make_uint4(c.k0, c.k1, c.c0, c.c1);
-    lc.carry.ep_return[i] = 0.0;
-    lc.carry.ep_length[i] = 0;
-    store_units(s, st, d, i, lc.n);
+  stage_params(reinterpret_cast<Params*>(smem), gP);
+  const Params& P = *reinterpret_cast<const Params*>(smem);
+  Smem m = carve<G, UPL>(smem, P.D, plan.rb);
+  const Grp<G> g;
+  const int slot = threadIdx.x / G;
+  EnvSm<CAP>& e = reinterpret_cast<EnvSm<CAP>*>(m.envs)[slot];
+  const int64_t i = int64_t(blockIdx.x) * EPB + slot;
+  const int64_t w0 = int64_t(blockIdx.x) * EPB + (threadIdx.x >> 5) * EPW;
+  const int wvalid = int(max(int64_t(0), min64(EPW, lc.n - w0)));
+  if (wvalid == 0) return;  // whole warp past the end (warp-uniform)
+  const bool live = i < lc.n;
+  int tg[UPL], sw[UPL];
+  if (live) {
+    const uint64_t gi = uint64_t(lc.offset + i);
+    env_reset<G, UPL>(P, e, g, split_child_nl(key, gi), tg, sw);  // vector_env.cpp:52,57
+    if (g.gl == 0) {
+      Key c = split_child_nl(carry_parent, gi);  // vector_env.cpp:55
+      lc.carry.keys[i] = make_uint4(c.k0, c.k1, c.c0, c.c1);
+      lc.carry.ep_return[i] = 0.0;
+      lc.carry.ep_length[i] = 0;
+      st.t[i] = 0;
+    }
+    store_env<G, UPL>(P, e, st, g.gl, i, lc.n, tg, sw);
   }
-  for (int a = 0; a < A; ++a) {
-    if (i < lc.n) observe(P, s, d, a, tile + threadIdx.x * D);
-    __syncthreads();
-    store_agent_rows(lc.v.obs + i0 * A * D, tile, nvalid, D, A, a, nullptr);
-    __syncthreads();
-  }
+  emit_obs<G, UPL>(P, e, g, live, m.tile, lc.v.obs, w0, wvalid, plan.rb, (1u << EPW) - 1u);
 }
 
-template <class Dm, bool RANDOM>
-__global__ void smax_step_kernel(const Params* __restrict__ gP, SmaxState st, LaunchCommon lc, Key step_key) {
+template <int G, int UPL, bool RANDOM>
+__global__ void __launch_bounds__(kThreads, 3) smax_step_kernel(const Params* __restrict__ gP, SmaxState st,
+                                                             LaunchCommon lc, Key step_key, Plan plan) {
+  constexpr int EPB = kThreads / G, EPW = 32 / G, CAP = G * UPL;
   extern __shared__ __align__(16) uint8_t smem[];
   if (*(volatile int*)lc.err) return;  // a pending contract error freezes the batch
-  const int T = blockDim.x;
-  // A and D are only known after the params are staged; carve with the
-  // host-side maxima passed through gridDim.y-free args below.
-  const Params* Pg = gP;
-  const int A = Pg->A, n_units = Pg->n, D = 10 + 17 * (n_units - 1);
-  Smem m = carve(smem, T, D, A);
-  stage_params(m.P, gP);
-  const Params& P = *m.P;
-  const Dm d = DimsOf<Dm>::make(P);
-  const int tid = threadIdx.x;
-  const int64_t i0 = int64_t(blockIdx.x) * T, i = i0 + tid;
-  const int nvalid = int(min64(T, lc.n - i0));
+  stage_params(reinterpret_cast<Params*>(smem), gP);
+  const Params& P = *reinterpret_cast<const Params*>(smem);
+  Smem m = carve<G, UPL>(smem, P.D, plan.rb);
+  const Grp<G> g;
+  const int slot = threadIdx.x / G;
+  EnvSm<CAP>& e = reinterpret_cast<EnvSm<CAP>*>(m.envs)[slot];
+  const int64_t i = int64_t(blockIdx.x) * EPB + slot;
+  const int64_t w0 = int64_t(blockIdx.x) * EPB + (threadIdx.x >> 5) * EPW;
+  const int wvalid = int(max(int64_t(0), min64(EPW, lc.n - w0)));
+  if (wvalid == 0) return;  // whole warp past the end (warp-uniform)
   const bool live = i < lc.n;
+  const int A = P.A;
 
-  Units<Dm> s;
+  int tg[UPL], sw[UPL];
   Key carry{0, 0, 0, 0};
   double ep_ret = 0.0;
-  int ep_len = 0;
+  int ep_len = 0, t = 0;
   bool done = false;
   if (live) {
-    uint4 kw = lc.carry.keys[i];
+    const uint4 kw = lc.carry.keys[i];
     carry = Key{kw.x, kw.y, kw.z, kw.w};
     ep_ret = lc.carry.ep_return[i];
     ep_len = lc.carry.ep_length[i];
-    load_units(s, st, d, i, lc.n);
+    t = st.t[i];
+    load_env<G, UPL>(P, e, st, g.gl, i, lc.n, tg, sw);
+    g.sync();
 
-    // ---- actions: agents (allies, plus enemies when controlled), then the
-    // built-in controller on the pre-step state (smax.cpp:225-240)
-    int act[Dm::CAP];
-#pragma unroll(Dm::UNROLL)
-    for (int u = 0; u < d.n(); ++u) act[u] = kStop;
-    if (RANDOM) {
-      Key ek = split_child(step_key, uint64_t(lc.offset + i));  // vector_env.cpp:171
-#pragma unroll(Dm::UNROLL)
-      for (int u = 0; u < (Dm::UNROLL > 1 ? Dm::CAP : A); ++u) {
-        if (u >= A) continue;
-        act[u] = random_legal(P, s, d, u, ek, u);
-        m.act[tid * A + u] = act[u];
-      }
-    } else {
-#pragma unroll(Dm::UNROLL)
-      for (int u = 0; u < (Dm::UNROLL > 1 ? Dm::CAP : A); ++u)
-        if (u < A) act[u] = lc.v.actions[i * A + u];
-    }
-    int new_tg[Dm::CAP], new_sw[Dm::CAP];
-#pragma unroll(Dm::UNROLL)
-    for (int u = 0; u < d.n(); ++u) {
-      new_tg[u] = s.tg[u];
-      new_sw[u] = s.sw[u];
-    }
-    if (!P.controlled) {
-#pragma unroll(Dm::UNROLL)
-      for (int u = 0; u < d.n(); ++u) {
-        if (u < d.na()) continue;
-        int tg = s.tg[u], sw = s.sw[u];
-        act[u] = heuristic(P, s, d, u, tg, sw);
-        new_tg[u] = tg;
-        new_sw[u] = sw;
+    // ---- actions on the pre-step state (smax.cpp:225-240): agents from the
+    // caller / the probe's random-legal stream, enemies from the heuristic
+    int act[UPL];
+    Key ek{0, 0, 0, 0};
+    if (RANDOM) ek = split_child_nl(step_key, uint64_t(lc.offset + i));  // vector_env.cpp:171
+#pragma unroll
+    for (int j = 0; j < UPL; ++j) {
+      const int u = g.gl + G * j;
+      act[j] = kStop;
+      if (u >= P.n) continue;
+      if (u < A) {
+        act[j] = RANDOM ? random_legal(P, e, u, ek) : lc.v.actions[i * A + u];
+        if (RANDOM) lc.v.actions[i * A + u] = act[j];
+      } else {
+        act[j] = heuristic(P, e, u, tg[j], sw[j]);
       }
     }
-    const double pool_prev0 = pool(P, s, d, 0), pool_prev1 = pool(P, s, d, 1);
-#pragma unroll(Dm::UNROLL)
-    for (int u = 0; u < d.n(); ++u) {
-      s.tg[u] = new_tg[u];
-      s.sw[u] = new_sw[u];
-    }
+    double pool_prev0, pool_prev1;
+    pools<G, UPL>(P, e, g, pool_prev0, pool_prev1);
+    g.sync();  // every lane has read the pre-step state
+#pragma unroll
+    for (int j = 0; j < UPL; ++j)
+      if (g.gl + G * j < P.n) e.act[g.gl + G * j] = act[j];
+    g.sync();
 
     // ---- physics (smax.cpp:242-254)
-    for (int k = 0; k < kTicks; ++k) tick(P, s, d, act, k == kTicks - 1);
-#pragma unroll(Dm::UNROLL)
-    for (int u = 0; u < d.n(); ++u) s.pa[u] = act[u];
-    s.t += 1;
+#pragma unroll 1
+    for (int k = 0; k < kTicks; ++k) tick<G, UPL>(P, e, g, k == kTicks - 1);
     int ally_alive = 0, enemy_alive = 0;
-#pragma unroll(Dm::UNROLL)
-    for (int u = 0; u < d.n(); ++u) {
-      if (s.h[u] > 0.0) {
-        if (u < d.na()) ++ally_alive;
-        else ++enemy_alive;
-      }
+#pragma unroll
+    for (int j = 0; j < UPL; ++j) {
+      const int u = g.gl + G * j;
+      const bool alive = u < P.n && e.h[u] > 0.0;
+      ally_alive += g.count(alive && u < P.na);
+      enemy_alive += g.count(alive && u >= P.na);
     }
-    if (ally_alive == 0 && enemy_alive == 0) s.winner = 2;
-    else if (enemy_alive == 0) s.winner = 0;
-    else if (ally_alive == 0) s.winner = 1;
-    else if (s.t >= P.max_steps) s.winner = 2;
-    done = s.winner != -1;
+    t += 1;
+    int winner = -1;
+    if (ally_alive == 0 && enemy_alive == 0) winner = 2;
+    else if (enemy_alive == 0) winner = 0;
+    else if (ally_alive == 0) winner = 1;
+    else if (t >= P.max_steps) winner = 2;  // timeout is a draw
+    done = winner != -1;
 
     // ---- reward_map (smax.cpp:352-363), infos and dones (smax.cpp:256-268)
-    double ally_r = 0.5 * (pool_prev1 - pool(P, s, d, 1)) / (2.0 * d.ne());
-    double enemy_r = 0.5 * (pool_prev0 - pool(P, s, d, 0)) / (2.0 * d.na());
-    if (s.winner == 0) ally_r += 0.5;
-    if (s.winner == 1) enemy_r += 0.5;
-    double sum = 0.0;
-    for (int a = 0; a < A; ++a) {
-      const int team = a < d.na() ? 0 : 1;
-      const double r = team == 0 ? ally_r : enemy_r;
-      m.rew[tid * A + a] = r;
-      sum += r;
-      double alive = 0.0;
-#pragma unroll(Dm::UNROLL)
-      for (int u = 0; u < (Dm::UNROLL > 1 ? Dm::CAP : A); ++u)
-        if (u == a) alive = s.h[u] > 0.0 ? 1.0 : 0.0;
-      m.inf[(tid * A + a) * 3 + 0] = alive;
-      m.inf[(tid * A + a) * 3 + 1] = s.winner == team ? 1.0 : 0.0;
-      m.inf[(tid * A + a) * 3 + 2] = s.winner == 2 ? 1.0 : 0.0;
-      m.done[tid * (A + 1) + a] = done;
+    double pool_next0, pool_next1;
+    pools<G, UPL>(P, e, g, pool_next0, pool_next1);
+    double ally_r = 0.5 * (pool_prev1 - pool_next1) / (2.0 * P.ne);
+    double enemy_r = 0.5 * (pool_prev0 - pool_next0) / (2.0 * P.na);
+    if (winner == 0) ally_r += 0.5;
+    if (winner == 1) enemy_r += 0.5;
+#pragma unroll
+    for (int j = 0; j < UPL; ++j) {
+      const int a = g.gl + G * j;
+      if (a >= A) continue;
+      const int team = a < P.na ? 0 : 1;
+      lc.v.rewards[i * A + a] = team == 0 ? ally_r : enemy_r;
+      double* inf = lc.v.infos + (i * A + a) * 3;
+      inf[0] = e.h[a] > 0.0 ? 1.0 : 0.0;   // alive
+      inf[1] = winner == team ? 1.0 : 0.0;  // battle_won
+      inf[2] = winner == 2 ? 1.0 : 0.0;     // draw
+      lc.v.dones[i * (A + 1) + a] = done;
     }
-    m.done[tid * (A + 1) + A] = done;
-    ep_ret = ep_ret + sum / double(A);  // vector_env.cpp:14-18,99
-    ep_len = ep_len + 1;
-    lc.v.finished[i] = done;
-    lc.v.final_returns[i] = done ? ep_ret : 0.0;
-    lc.v.final_lengths[i] = done ? ep_len : 0;
+    if (g.gl == 0) {
+      double sum = 0.0;
+#pragma unroll 1
+      for (int a = 0; a < A; ++a) sum += a < P.na ? ally_r : enemy_r;
+      ep_ret = ep_ret + sum / double(A);  // team_reward, vector_env.cpp:14-18,99
+      ep_len = ep_len + 1;
+      lc.v.dones[i * (A + 1) + A] = done;
+      lc.v.finished[i] = done;
+      lc.v.final_returns[i] = done ? ep_ret : 0.0;
+      lc.v.final_lengths[i] = done ? ep_len : 0;
+    }
+    // prev_action <- this step's actions (smax.cpp:243)
+#pragma unroll
+    for (int j = 0; j < UPL; ++j)
+      if (g.gl + G * j < P.n) e.pa[g.gl + G * j] = int8_t(e.act[g.gl + G * j]);
+    g.sync();
   }
-  m.fin[tid] = done;
-  stats_add(lc.stats, done, ep_len, ep_ret);
+  stats_add(lc.stats, done && g.gl == 0, ep_len, ep_ret);
 
   // ---- terminal observations -> final_obs, then auto-reset (vector_env.cpp:107-119)
-  if (__syncthreads_or(done)) {
-    for (int a = 0; a < A; ++a) {
-      if (done) observe(P, s, d, a, m.row + tid * D);
-      __syncthreads();
-      store_agent_rows(lc.v.final_obs + i0 * A * D, m.row, nvalid, D, A, a, m.fin);
-      __syncthreads();
-    }
+  const unsigned done_lanes = __ballot_sync(0xffffffffu, done && g.gl == 0);
+  if (done_lanes) {
+    unsigned sel = 0;
+    for (int s = 0; s < EPW; ++s) sel |= ((done_lanes >> (s * G)) & 1u) << s;
+    emit_obs<G, UPL>(P, e, g, done, m.tile, lc.v.final_obs, w0, wvalid, plan.rb, sel);
     if (done) {
-      env_reset(P, s, d, split_child(carry, 1));
+      env_reset<G, UPL>(P, e, g, split_child_nl(carry, 1), tg, sw);
       ep_ret = 0.0;
       ep_len = 0;
+      t = 0;
     }
   }
   if (live) {
-    Key nk = split_child(carry, 2);  // vector_env.cpp:126
-    lc.carry.keys[i] = make_uint4(nk.k0, nk.k1, nk.c0, nk.c1);
-    lc.carry.ep_return[i] = ep_ret;
-    lc.carry.ep_length[i] = ep_len;
-    store_units(s, st, d, i, lc.n);
-  }
-  for (int a = 0; a < A; ++a) {
-    if (live) observe(P, s, d, a, m.row + tid * D);
-    __syncthreads();
-    store_agent_rows(lc.v.obs + i0 * A * D, m.row, nvalid, D, A, a, nullptr);
-    __syncthreads();
-  }
-  block_store(lc.v.rewards + i0 * A, m.rew, size_t(nvalid) * A * sizeof(double));
-  block_store(lc.v.infos + i0 * A * 3, m.inf, size_t(nvalid) * A * 3 * sizeof(double));
-  block_store(lc.v.dones + i0 * (A + 1), m.done, size_t(nvalid) * (A + 1));
-  if (RANDOM) block_store(lc.v.actions + i0 * A, m.act, size_t(nvalid) * A * sizeof(int32_t));
-}
-
-template <class Dm>
-__global__ void smax_legal_kernel(const Params* __restrict__ gP, SmaxState st, int64_t n, int n_act,
-                                  uint8_t* out) {
-  __shared__ Params sP;
-  stage_params(&sP, gP);
-  const Dm d = DimsOf<Dm>::make(sP);
-  int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  Units<Dm> s;
-  load_units(s, st, d, i, n);
-  for (int a = 0; a < sP.A; ++a) {  // smax.cpp:195-211
-    uint8_t* row = out + (size_t(i) * sP.A + a) * n_act;
-    for (int q = 0; q < n_act; ++q) row[q] = 0;
-    row[kStop] = 1;
-    double ha = 0.0;
-#pragma unroll(Dm::UNROLL)
-    for (int u = 0; u < (Dm::UNROLL > 1 ? Dm::CAP : sP.A); ++u)
-      if (u == a) ha = s.h[u];
-    if (ha <= 0.0) continue;
-    for (int q = 0; q < kStop; ++q) row[q] = 1;
-    const int opp0 = a < d.na() ? d.na() : 0, opp_n = a < d.na() ? d.ne() : d.na();
-#pragma unroll(Dm::UNROLL)
-    for (int u = 0; u < (Dm::UNROLL > 1 ? Dm::CAP : sP.A); ++u) {
-      if (u != a) continue;
-#pragma unroll(Dm::UNROLL)
-      for (int k = 0; k < (Dm::UNROLL > 1 ? Dm::CAP : opp_n); ++k)
-        if (k < opp_n && s.h[opp0 + k] > 0.0 && in_range(sP, s, u, opp0 + k)) row[kAttackBase + k] = 1;
+    if (g.gl == 0) {
+      const Key nk = split_child_nl(carry, 2);  // vector_env.cpp:126
+      lc.carry.keys[i] = make_uint4(nk.k0, nk.k1, nk.c0, nk.c1);
+      lc.carry.ep_return[i] = ep_ret;
+      lc.carry.ep_length[i] = ep_len;
+      st.t[i] = t;
     }
+    store_env<G, UPL>(P, e, st, g.gl, i, lc.n, tg, sw);
+  }
+  emit_obs<G, UPL>(P, e, g, live, m.tile, lc.v.obs, w0, wvalid, plan.rb, (1u << EPW) - 1u);
+}
+
+// ------------------------------------------------- non-hot helper kernels
+// Env::legal_actions (smax.cpp:195-211) and state_hash (smax.cpp:312-337):
+// one thread per env straight from the HBM state.
+__device__ __forceinline__ bool g_in_range(const Params& P, const SmaxState& st, int64_t n, int64_t i, int a, int b) {
+  const Thresh& r = P.ps[P.type[a]][P.type[b]].reach;
+  return dist_le(st.x[a * n + i] - st.x[b * n + i], st.y[a * n + i] - st.y[b * n + i], r.r, r.r2lo, r.r2hi);
+}
+
+__global__ void smax_legal_kernel(const Params* __restrict__ gP, SmaxState st, int64_t n, int n_act, uint8_t* out) {
+  __shared__ __align__(16) Params sP;
+  stage_params(&sP, gP);
+  const Params& P = sP;
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  for (int a = 0; a < P.A; ++a) {
+    uint8_t* row = out + (size_t(i) * P.A + a) * n_act;
+    for (int q = 0; q < n_act; ++q) row[q] = 0;
+    row[kStop] = 1;  // dead units can only wait
+    if (st.health[a * n + i] <= 0.0) continue;
+    for (int q = 0; q < kStop; ++q) row[q] = 1;
+    const int opp0 = a < P.na ? P.na : 0, opp_n = a < P.na ? P.ne : P.na;
+    for (int k = 0; k < opp_n; ++k)
+      if (st.health[(opp0 + k) * n + i] > 0.0 && g_in_range(P, st, n, i, a, opp0 + k)) row[kAttackBase + k] = 1;
   }
 }
 
-template <class Dm>
 __global__ void smax_hash_kernel(const Params* __restrict__ gP, SmaxState st, int64_t n, uint64_t* out) {
-  __shared__ Params sP;
+  __shared__ __align__(16) Params sP;
   stage_params(&sP, gP);
-  const Dm d = DimsOf<Dm>::make(sP);
-  int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  Units<Dm> s;
-  load_units(s, st, d, i, n);
-  uint64_t h = 1469598103934665603ull;  // smax.cpp:312-337
+  uint64_t h = 1469598103934665603ull;  // FNV-1a, smax.cpp:312-337
   auto mix = [&h](uint64_t v) { h = (h ^ v) * 1099511628211ull; };
-#pragma unroll(Dm::UNROLL)
-  for (int u = 0; u < d.n(); ++u) {
-    mix(__double_as_longlong(s.x[u]));
-    mix(__double_as_longlong(s.y[u]));
-    mix(__double_as_longlong(s.h[u]));
-    mix(__double_as_longlong(s.cd[u]));
+  for (int u = 0; u < sP.n; ++u) {
+    const uint32_t m = st.mem[u * n + i];
+    mix(__double_as_longlong(st.x[u * n + i]));
+    mix(__double_as_longlong(st.y[u * n + i]));
+    mix(__double_as_longlong(st.health[u * n + i]));
+    mix(__double_as_longlong(st.cooldown[u * n + i]));
     mix(uint64_t(uint8_t(sP.type[u])));
-    mix(uint64_t(uint16_t(int16_t(s.pa[u]))));
-    mix(uint64_t(uint16_t(int16_t(s.tg[u]))));
-    mix(uint64_t(uint8_t(int8_t(s.sw[u]))));
+    mix(uint64_t(uint16_t(int16_t(int8_t(m & 0xffu)))));         // prev_action
+    mix(uint64_t(uint16_t(int16_t(int8_t((m >> 8) & 0xffu)))));  // ai_target
+    mix(uint64_t(uint8_t((m >> 16) & 0xffu)));                   // ai_sweep
   }
-  mix(uint64_t(s.t));
-  mix(uint64_t(uint8_t(int8_t(-1))));
+  mix(uint64_t(st.t[i]));
+  mix(uint64_t(uint8_t(int8_t(-1))));  // winner of a live state
   out[i] = h;
 }
 
@@ -722,54 +892,81 @@ Params make_params(const SmaxConfig& c) {
   P.A = c.na + (c.enemy_controlled ? c.ne : 0);
   P.controlled = c.enemy_controlled;
   P.max_steps = c.max_steps;
+  P.D = 10 + 17 * (P.n - 1);
+  P.n_pairs = P.n * (P.n - 1) / 2;
   P.map = c.map;
   P.jitter = c.jitter;
-  for (int u = 0; u < P.n; ++u) {
-    const double* st = c.stats[c.type[u]];
-    P.type[u] = c.type[u];
-    P.hmax[u] = st[0];
-    P.dmg[u] = st[1];
-    P.cdmax[u] = st[2];
-    P.spdt[u] = st[3] * kDt;  // st.speed * kDt, smax.cpp:514
-    P.rad[u] = st[6];
-    P.hi[u] = c.map - st[6];  // map_ - radius, smax.cpp:515
-    P.sight[u] = make_thresh(st[4]);
+  for (int u = 0; u < P.n; ++u) P.type[u] = c.type[u];
+  for (int t = 0; t < kTypes; ++t) {
+    const double* st = c.stats[t];  // health damage cooldown speed sight range radius
+    TypeStat& T = P.ts[t];
+    T.hmax = st[0];
+    T.dmg = st[1];
+    T.cdmax = st[2];
+    T.spdt = st[3] * kDt;  // st.speed * kDt, smax.cpp:514
+    T.rad = st[6];
+    T.hi = c.map - st[6];  // map_ - radius, smax.cpp:515
+    T.sight = make_thresh(st[4]);
   }
-  for (int a = 0; a < 6; ++a)
-    for (int b = 0; b < 6; ++b) {
-      P.reach[a][b] = make_thresh(c.stats[a][5] + c.stats[a][6] + c.stats[b][6]);
-      double sum = c.stats[a][6] + c.stats[b][6];
-      P.rsum[a][b] = make_thresh(sum);
-      P.rsum[a][b].r = sum;
-      P.otol[a][b] = make_thresh(sum - kSepTol);
+  for (int a = 0; a < kTypes; ++a)
+    for (int b = 0; b < kTypes; ++b) {
+      PairStat& S = P.ps[a][b];
+      S.reach = make_thresh(c.stats[a][5] + c.stats[a][6] + c.stats[b][6]);
+      const double sum = c.stats[a][6] + c.stats[b][6];
+      S.rsum = make_thresh(sum);
+      S.otol = make_thresh(sum - kSepTol);
     }
+  P.sep_r2hi = 0.0;
+  for (int a = 0; a < P.n; ++a)
+    for (int b = 0; b < P.n; ++b) P.sep_r2hi = std::max(P.sep_r2hi, P.ps[P.type[a]][P.type[b]].rsum.r2hi);
   return P;
 }
 
-struct Launch {
-  int threads;
-  size_t smem;
-};
-
-// Which compile-time roster a config maps to (0 = dynamic).
-int roster_id(const SmaxConfig& c) {
-  if (c.na == 3 && c.ne == 3) return 1;
-  if (c.na == 5 && c.ne == 5) return 2;
-  if (c.na == 5 && c.ne == 6) return 3;
-  if (c.na == 3 && c.ne == 5) return 4;
-  if (c.na == 8 && c.ne == 8) return 5;
-  if (c.na == 8 && c.ne == 9) return 6;
-  if (c.na == 6 && c.ne == 8) return 7;
-  return 0;
+// Group shape for a roster of n units: lanes per env and units per lane.
+int shape_id(const SmaxConfig& c) {
+  const int n = c.na + c.ne;
+  return n <= 8 ? 4 : n <= 16 ? 1 : n <= 32 ? 2 : 3;
 }
 
-Launch pick_launch(const SmaxConfig& c, bool fixed) {
-  const int n = c.na + c.ne, A = c.na + (c.enemy_controlled ? c.ne : 0);
-  const int D = 10 + 17 * (n - 1);
-  int T = fixed ? 128 : 64;
-  while (T > 32 && smem_bytes(T, D, A) > 200 * 1024) T /= 2;
-  return Launch{T, smem_bytes(T, D, A)};
+template <int G, int UPL>
+Plan make_plan(const SmaxConfig& c, size_t* smem) {
+  const int n = c.na + c.ne, A = c.na + (c.enemy_controlled ? c.ne : 0), D = 10 + 17 * (n - 1);
+  constexpr int EPW = 32 / G;
+  int rb = int(kWarpStageBytes / (size_t(EPW) * D * 4));
+  rb = rb < 1 ? 1 : rb > A ? A : rb;
+  *smem = smem_bytes<G, UPL>(D, rb);
+  return Plan{rb};
 }
+
+template <int G, int UPL>
+void launch_reset_g(const SmaxConfig& c, const Params* dP, const SmaxState& s, const LaunchCommon& lc, Key k, Key cp) {
+  size_t sm;
+  Plan plan = make_plan<G, UPL>(c, &sm);
+  auto fn = smax_reset_kernel<G, UPL>;
+  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+  constexpr int EPB = kThreads / G;
+  fn<<<unsigned((lc.n + EPB - 1) / EPB), kThreads, sm, lc.stream>>>(dP, s, lc, k, cp, plan);
+}
+
+template <int G, int UPL>
+void launch_step_g(const SmaxConfig& c, const Params* dP, const SmaxState& s, const LaunchCommon& lc, bool random,
+                   Key k) {
+  size_t sm;
+  Plan plan = make_plan<G, UPL>(c, &sm);
+  auto fn = random ? smax_step_kernel<G, UPL, true> : smax_step_kernel<G, UPL, false>;
+  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+  constexpr int EPB = kThreads / G;
+  fn<<<unsigned((lc.n + EPB - 1) / EPB), kThreads, sm, lc.stream>>>(dP, s, lc, k, plan);
+}
+
+#define MARL_SMAX_SHAPES(FN, ...)           \
+  switch (shape_id(c)) {                    \
+    case 0: FN<8, 1>(__VA_ARGS__); break;   \
+    case 4: FN<4, 2>(__VA_ARGS__); break;   \
+    case 1: FN<16, 1>(__VA_ARGS__); break;  \
+    case 2: FN<32, 1>(__VA_ARGS__); break;  \
+    default: FN<32, 2>(__VA_ARGS__); break; \
+  }
 
 }  // namespace
 
@@ -786,74 +983,29 @@ void smax_release(SmaxConfig& c) {
   c.dev_params = nullptr;
 }
 
-static const Params* device_params(const SmaxConfig& c, cudaStream_t) {
-  return static_cast<const Params*>(c.dev_params);
-}
-
-template <class Dm>
-static void launch_reset_t(const SmaxConfig& c, const Params* dP, const SmaxState& s, const LaunchCommon& lc,
-                           Key k, Key cp, bool fixed) {
-  Launch L = pick_launch(c, fixed);
-  auto fn = smax_reset_kernel<Dm>;
-  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(L.smem));
-  unsigned g = unsigned((lc.n + L.threads - 1) / L.threads);
-  fn<<<g, L.threads, L.smem, lc.stream>>>(dP, s, lc, k, cp);
-}
-
-template <class Dm>
-static void launch_step_t(const SmaxConfig& c, const Params* dP, const SmaxState& s, const LaunchCommon& lc,
-                          bool random, Key k, bool fixed) {
-  Launch L = pick_launch(c, fixed);
-  auto fn = random ? smax_step_kernel<Dm, true> : smax_step_kernel<Dm, false>;
-  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(L.smem));
-  unsigned g = unsigned((lc.n + L.threads - 1) / L.threads);
-  fn<<<g, L.threads, L.smem, lc.stream>>>(dP, s, lc, k);
-}
-
-#define MARL_SMAX_DISPATCH(FN, ...)                                          \
-  switch (roster_id(c)) {                                                    \
-    case 1: FN<Fixed<3, 3>>(__VA_ARGS__, true); break;                       \
-    case 2: FN<Fixed<5, 5>>(__VA_ARGS__, true); break;                       \
-    default: FN<Dyn>(__VA_ARGS__, false); break;                             \
-  }
-
 void smax_launch_reset(const SmaxConfig& c, const SmaxState& s, const LaunchCommon& lc, KeyWords key,
                        KeyWords carry_parent) {
-  const Params* dP = device_params(c, lc.stream);
-  Key k = to_key(key), cp = to_key(carry_parent);
-  MARL_SMAX_DISPATCH(launch_reset_t, c, dP, s, lc, k, cp)
+  const Params* dP = static_cast<const Params*>(c.dev_params);
+  MARL_SMAX_SHAPES(launch_reset_g, c, dP, s, lc, to_key(key), to_key(carry_parent))
   ++g_launches;
 }
 
 void smax_launch_step(const SmaxConfig& c, const SmaxState& s, const LaunchCommon& lc, bool random,
                       KeyWords step_key) {
-  const Params* dP = device_params(c, lc.stream);
-  Key k = to_key(step_key);
-  MARL_SMAX_DISPATCH(launch_step_t, c, dP, s, lc, random, k)
+  const Params* dP = static_cast<const Params*>(c.dev_params);
+  MARL_SMAX_SHAPES(launch_step_g, c, dP, s, lc, random, to_key(step_key))
   ++g_launches;
-}
-
-template <class Dm>
-static void launch_legal_t(const Params* dP, const SmaxState& s, int64_t n, int n_act, uint8_t* out,
-                           cudaStream_t st, bool) {
-  smax_legal_kernel<Dm><<<unsigned((n + 63) / 64), 64, 0, st>>>(dP, s, n, n_act, out);
-}
-template <class Dm>
-static void launch_hash_t(const Params* dP, const SmaxState& s, int64_t n, uint64_t* out, cudaStream_t st,
-                          bool) {
-  smax_hash_kernel<Dm><<<unsigned((n + 63) / 64), 64, 0, st>>>(dP, s, n, out);
 }
 
 void smax_launch_legal(const SmaxConfig& c, const SmaxState& s, int64_t n, int n_act, uint8_t* out,
                        cudaStream_t st) {
-  const Params* dP = device_params(c, st);
-  MARL_SMAX_DISPATCH(launch_legal_t, dP, s, n, n_act, out, st)
+  smax_legal_kernel<<<unsigned((n + 127) / 128), 128, 0, st>>>(static_cast<const Params*>(c.dev_params), s, n,
+                                                                n_act, out);
   ++g_launches;
 }
 
 void smax_launch_hash(const SmaxConfig& c, const SmaxState& s, int64_t n, uint64_t* out, cudaStream_t st) {
-  const Params* dP = device_params(c, st);
-  MARL_SMAX_DISPATCH(launch_hash_t, dP, s, n, out, st)
+  smax_hash_kernel<<<unsigned((n + 127) / 128), 128, 0, st>>>(static_cast<const Params*>(c.dev_params), s, n, out);
   ++g_launches;
 }
 
