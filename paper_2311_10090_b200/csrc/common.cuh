@@ -210,6 +210,32 @@ __device__ __forceinline__ void block_store(void* gdst, const void* ssrc, size_t
   }
 }
 
+// ---- TMA bulk copies (cp.async.bulk, sm_90+; the sm_100a async proxy) ----
+// shared::cta -> global, `bytes` a multiple of 16, both ends 16-byte aligned.
+// One thread issues; completion is tracked per issuing thread with bulk
+// groups.  Generic-proxy writes to the source buffer must be ordered before
+// the copy with fence_proxy_async_smem() (by the writing threads) plus a
+// barrier, the CUTLASS TMA-store-epilogue protocol.
+__device__ __forceinline__ void bulk_store_s2g(void* gdst, const void* ssrc, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst),
+               "r"(static_cast<uint32_t>(__cvta_generic_to_shared(ssrc))), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+// Wait until at most N committed groups still READ their shared source.
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+// Wait until at most N committed groups are incomplete (writes performed).
+template <int N>
+__device__ __forceinline__ void bulk_wait() {
+  asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
 // Per-block episode statistics, folded into 64-bit integer accumulators so the
 // totals are exact and order-independent (identical for any grid shape and any
 // number of GPUs): [0] finished episodes, [1] sum of lengths, [2] sum of

@@ -3,13 +3,15 @@
 // ops per env; 97% of the bytes are the 27-plane observation rows
 // (overcooked.cpp:395-427), so the kernel is organised around storing them at
 // HBM speed:
-//   * state update: one thread per env (threads 0..E-1 of the block),
-//   * observation: the block's [E][2][D] rows are filled from a static
-//     layout template in shared memory (planes 10-14 never change), patched
-//     with the ~20 dynamic cells per row, and leave as contiguous 16-byte
-//     streaming stores of the whole tile.
+//   * state update: one lane per env (a warp steps 32 envs in SIMT),
+//   * observation: the warp streams the static layout template (planes
+//     10-14 never change, the dynamic planes are zero in it) from shared
+//     memory into its envs' contiguous [32][2][D] rows with 16-byte stores,
+//     then every lane overwrites the ~20 dynamic cells of its own rows.
 // All state is integer and trajectories are bit-identical to the reference.
 #include <cuda_runtime.h>
+
+#include <algorithm>
 
 #include "common.cuh"
 #include "engine.h"
@@ -17,8 +19,7 @@
 namespace marl_b200 {
 namespace {
 
-constexpr int kE = 16;          // envs per block
-constexpr int kThreads = 128;
+constexpr int kThreads = 256;    // 8 warps, one env per lane
 constexpr int kUp = 0, kDown = 1, kLeft = 2, kRight = 3, kStay = 4, kInteract = 5;  // overcooked.cpp:16
 constexpr int kNone = 0, kOnion = 1, kPlate = 2, kSoup = 3;                         // overcooked.cpp:21
 constexpr int kPlanes = 27;
@@ -178,80 +179,96 @@ __device__ __forceinline__ bool env_step(Kitchen& s, const OcConfig& c, const Ke
 }
 
 // Dynamic cells of encode() (overcooked.cpp:395-427) for agent `me`; the
-// static planes come from the template already in the row.
+// static planes come from the template already in the row.  CLEAR writes the
+// template's 0 back into exactly the cells a patch of the same state set.
+template <bool CLEAR = false>
 __device__ __forceinline__ void patch_row(float* o, const Kitchen& s, const OcConfig& c, int me) {
   const int cells = c.h * c.w, other = 1 - me;
-  o[0 * cells + s.pos[me]] = 1.0f;
-  o[1 * cells + s.pos[other]] = 1.0f;
-  o[(2 + s.facing[me]) * cells + s.pos[me]] = 1.0f;
-  o[(6 + s.facing[other]) * cells + s.pos[other]] = 1.0f;
+  const float one = CLEAR ? 0.0f : 1.0f;
+  o[0 * cells + s.pos[me]] = one;
+  o[1 * cells + s.pos[other]] = one;
+  o[(2 + s.facing[me]) * cells + s.pos[me]] = one;
+  o[(6 + s.facing[other]) * cells + s.pos[other]] = one;
   for (int p = 0; p < c.n_pots; ++p) {
     const int cell = c.pot_cells[p];
-    o[15 * cells + cell] = float(s.onions[p]);
-    o[16 * cells + cell] = float(s.timer[p]) / float(c.cook_time);
-    if (s.onions[p] == 3 && s.timer[p] == 0) o[17 * cells + cell] = 1.0f;
+    o[15 * cells + cell] = CLEAR ? 0.0f : float(s.onions[p]);
+    o[16 * cells + cell] = CLEAR ? 0.0f : float(s.timer[p]) / float(c.cook_time);
+    if (s.onions[p] == 3 && s.timer[p] == 0) o[17 * cells + cell] = one;
   }
-  if (s.held[me] != kNone) o[(18 + s.held[me] - 1) * cells + s.pos[me]] = 1.0f;
-  if (s.held[other] != kNone) o[(21 + s.held[other] - 1) * cells + s.pos[other]] = 1.0f;
-  for (int k = 0; k < c.n_counters; ++k) {
-    const int item = counter_get(s, k);
-    if (item != kNone) o[(24 + item - 1) * cells + c.counter_cells[k]] = 1.0f;
+  if (s.held[me] != kNone) o[(18 + s.held[me] - 1) * cells + s.pos[me]] = one;
+  if (s.held[other] != kNone) o[(21 + s.held[other] - 1) * cells + s.pos[other]] = one;
+  for (int wd = 0; wd < 2; ++wd) {  // only the occupied counters: 2 bits per counter, 0 = empty
+    const uint64_t w = s.counters[wd];
+    for (uint64_t occ = (w | (w >> 1)) & 0x5555555555555555ull; occ; occ &= occ - 1) {
+      const int bit = __ffsll((long long)occ) - 1;
+      const int item = int((w >> bit) & 3u);
+      o[(24 + item - 1) * cells + c.counter_cells[wd * 32 + (bit >> 1)]] = one;
+    }
   }
-  o[kPlanes * cells] = float(s.t) / float(c.max_steps);
+  o[kPlanes * cells] = CLEAR ? 0.0f : float(s.t) / float(c.max_steps);
 }
 
-// Fill rows [r0, r1) of the tile (rows are (env, agent) pairs) from the template.
-__device__ __forceinline__ void fill_rows(float* tile, const float* templ, int D, int nrows,
-                                          const uint8_t* env_mask) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  for (int r = warp; r < nrows; r += nw) {
-    if (env_mask && !env_mask[r >> 1]) continue;
-    float* row = tile + size_t(r) * D;
-    for (int k = lane; k < D; k += 32) row[k] = templ[k];
-  }
-}
-
-struct Smem {
-  float* templ;  // [D]
-  float* tile;   // [kE][2][D]
-  double* rew;   // [kE][2]
-  double* inf;   // [kE][2][2]  deliveries, shaped_reward
-  int32_t* act;  // [kE][2]
-  uint8_t* done; // [kE][3]
-  uint8_t* fin;  // [kE]
+// ------------------------------------------------------------ row streaming
+// A warp's envs own a contiguous run of observation rows ([N][2][D] f32).
+// The static planes of every row are identical (the layout template), so the
+// warp streams the template straight from shared memory into the run with
+// 16-byte stores, then each lane overwrites the ~20 dynamic cells of its own
+// env's two rows (patch_row) after a __syncwarp (which orders the warp's
+// global stores).  Nothing is staged per env: shared memory holds only the
+// template, in four copies shifted by 0..3 floats so that any 4 consecutive
+// template floats starting at any row offset are one aligned LDS.128.
+struct Tmpl {
+  const float* s[4];  // s[r][i] = templ[(i + r) % D]
+  int D;
 };
 
-__host__ __device__ inline size_t a16(size_t b) { return (b + 15) & ~size_t(15); }
-__host__ __device__ inline size_t smem_bytes(int D) {
-  return a16(size_t(D) * 4) + a16(size_t(kE) * 2 * D * 4) + a16(kE * 2 * 8) + a16(kE * 4 * 8) +
-         a16(kE * 2 * 4) + a16(kE * 3) + a16(kE);
+__host__ __device__ inline size_t tmpl_floats(int D) { return (size_t(D) + 3 + 3) & ~size_t(3); }
+
+__device__ __forceinline__ Tmpl stage_template(float* smem, const float* __restrict__ g, int D) {
+  const size_t stride = tmpl_floats(D);
+  for (int idx = threadIdx.x; idx < 4 * int(stride); idx += blockDim.x) {
+    const int r = idx / int(stride), i = idx - r * int(stride);
+    smem[idx] = __ldg(g + (i + r) % D);
+  }
+  __syncthreads();
+  Tmpl t;
+  for (int r = 0; r < 4; ++r) t.s[r] = smem + r * stride;
+  t.D = D;
+  return t;
 }
-__device__ __forceinline__ Smem carve(uint8_t* b, int D) {
-  Smem m;
-  size_t off = 0;
-  m.templ = reinterpret_cast<float*>(b + off); off += a16(size_t(D) * 4);
-  m.tile = reinterpret_cast<float*>(b + off); off += a16(size_t(kE) * 2 * D * 4);
-  m.rew = reinterpret_cast<double*>(b + off); off += a16(kE * 2 * 8);
-  m.inf = reinterpret_cast<double*>(b + off); off += a16(kE * 4 * 8);
-  m.act = reinterpret_cast<int32_t*>(b + off); off += a16(kE * 2 * 4);
-  m.done = b + off; off += a16(kE * 3);
-  m.fin = b + off;
-  return m;
+
+// dst: start of a run of whole rows (row offset 0), nfloats = rows * D.
+__device__ __forceinline__ void stream_rows(float* __restrict__ dst, const Tmpl& t, int nfloats) {
+  const int lane = threadIdx.x & 31, D = t.D;
+  int head = int(((16 - (reinterpret_cast<uintptr_t>(dst) & 15)) & 15) >> 2);
+  head = head < nfloats ? head : nfloats;
+  if (lane < head) dst[lane] = t.s[0][lane];
+  const int nv = (nfloats - head) >> 2;
+  float4* d4 = reinterpret_cast<float4*>(dst + head);
+  int k = (head + 4 * lane) % D;  // row offset of this lane's first vector
+#pragma unroll 4
+  for (int q = lane; q < nv; q += 32) {
+    const int r = k & 3;
+    d4[q] = *reinterpret_cast<const float4*>(t.s[r] + (k - r));
+    k += 128;
+    while (k >= D) k -= D;
+  }
+  for (int q = head + 4 * nv + lane; q < nfloats; q += 32) dst[q] = t.s[0][q % D];
 }
 
 __global__ void __launch_bounds__(kThreads) oc_reset_kernel(OcConfig c, const float* __restrict__ gtempl,
                                                             OcState st, LaunchCommon lc, Key key, Key carry_parent) {
-  extern __shared__ __align__(16) uint8_t smem[];
+  extern __shared__ __align__(16) float smem[];
   const int D = kPlanes * c.h * c.w + 1;
-  Smem m = carve(smem, D);
-  for (int k = threadIdx.x; k < D; k += blockDim.x) m.templ[k] = gtempl[k];
-  const int64_t i0 = int64_t(blockIdx.x) * kE;
-  const int nvalid = int(min64(kE, lc.n - i0));
-  __syncthreads();
-  fill_rows(m.tile, m.templ, D, 2 * nvalid, nullptr);
-  __syncthreads();
-  if (threadIdx.x < nvalid) {
-    const int64_t i = i0 + threadIdx.x;
+  const Tmpl t = stage_template(smem, gtempl, D);
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = int64_t(blockIdx.x) * kThreads + (threadIdx.x & ~31);
+  if (w0 >= lc.n) return;  // warp-uniform
+  const int wvalid = int(min64(32, lc.n - w0));
+  const int64_t i = w0 + lane;
+  stream_rows(lc.v.obs + w0 * 2 * D, t, wvalid * 2 * D);
+  __syncwarp();
+  if (lane < wvalid) {
     const uint64_t g = uint64_t(lc.offset + i);
     Kitchen s;
     env_reset(s, c);
@@ -261,103 +278,139 @@ __global__ void __launch_bounds__(kThreads) oc_reset_kernel(OcConfig c, const fl
     lc.carry.ep_return[i] = 0.0;
     lc.carry.ep_length[i] = 0;
     store(s, c, st, i, lc.n);
-    for (int a = 0; a < 2; ++a) patch_row(m.tile + (size_t(threadIdx.x) * 2 + a) * D, s, c, a);
+    for (int a = 0; a < 2; ++a) patch_row(lc.v.obs + (i * 2 + a) * D, s, c, a);
   }
-  __syncthreads();
-  block_store(lc.v.obs + i0 * 2 * D, m.tile, size_t(nvalid) * 2 * D * 4);
+}
+
+// Observation rows through the async proxy: every warp owns two shared-memory
+// buffers, each holding FOUR template rows (two envs; 16*D bytes, a multiple
+// of 16 for any layout and 16-byte aligned in global memory at even envs).
+// Per pair of envs the two owning lanes patch their rows into a buffer, one
+// lane issues a single TMA bulk store (cp.async.bulk.global.shared::cta) of
+// the whole 4-row run, and when the buffer comes round again the same lanes
+// write the template's zeros back into exactly the cells they patched.  No
+// row is ever copied through registers; the TMA engine streams 8.6 KB per
+// instruction while the warp steps the next pair.
+__host__ __device__ inline size_t oc_tma_smem_floats(int D, int warps) {
+  return 4 * tmpl_floats(D) + size_t(warps) * 2 * 4 * D;
 }
 
 template <bool RANDOM>
 __global__ void __launch_bounds__(kThreads) oc_step_kernel(OcConfig c, const float* __restrict__ gtempl,
-                                                           OcState st, LaunchCommon lc, Key step_key) {
-  extern __shared__ __align__(16) uint8_t smem[];
+                                                           OcState st, LaunchCommon lc, Key step_key, int tma) {
+  extern __shared__ __align__(16) float smem[];
   if (*(volatile int*)lc.err) return;
   const int D = kPlanes * c.h * c.w + 1;
-  Smem m = carve(smem, D);
-  for (int k = threadIdx.x; k < D; k += blockDim.x) m.templ[k] = gtempl[k];
-  const int64_t i0 = int64_t(blockIdx.x) * kE;
-  const int nvalid = int(min64(kE, lc.n - i0));
-  const int tid = threadIdx.x;
-  __syncthreads();
-  fill_rows(m.tile, m.templ, D, 2 * nvalid, nullptr);
+  const Tmpl t = stage_template(smem, gtempl, D);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, warps = blockDim.x >> 5;
+  float* bufs = smem + 4 * tmpl_floats(D) + size_t(wid) * 2 * 4 * D;
+  if (tma) {  // both buffers start as four template rows
+    for (int idx = lane; idx < 2 * 4 * D; idx += 32) bufs[idx] = t.s[0][idx % D];
+    __syncwarp();
+  }
+  const int64_t nchunks = (lc.n + 31) >> 5;
+  for (int64_t chunk = int64_t(blockIdx.x) * warps + wid; chunk < nchunks; chunk += int64_t(gridDim.x) * warps) {
+    const int64_t w0 = chunk << 5;
+    const int wvalid = int(min64(32, lc.n - w0));
+    const int64_t i = w0 + lane;
+    const bool mine = lane < wvalid;
 
-  Kitchen s;
-  Key carry{0, 0, 0, 0};
-  double ep_ret = 0.0;
-  int ep_len = 0;
-  bool done = false;
-  const bool mine = tid < nvalid;
-  const int64_t i = i0 + tid;
-  if (mine) {
-    uint4 kw = lc.carry.keys[i];
-    carry = Key{kw.x, kw.y, kw.z, kw.w};
-    ep_ret = lc.carry.ep_return[i];
-    ep_len = lc.carry.ep_length[i];
-    load(s, c, st, i, lc.n);
-    int act[2];
-    if (RANDOM) {  // all six actions always legal (env.hpp:71-73)
-      Key ek = split_child(step_key, uint64_t(lc.offset + i));
-      act[0] = int(block_at(ek, 0) % 6u);
-      act[1] = int(block_at(ek, 1) % 6u);
-      m.act[tid * 2] = act[0];
-      m.act[tid * 2 + 1] = act[1];
-    } else {
-      act[0] = lc.v.actions[i * 2];
-      act[1] = lc.v.actions[i * 2 + 1];
+    Kitchen s;
+    Key carry{0, 0, 0, 0};
+    double ep_ret = 0.0;
+    int ep_len = 0;
+    bool done = false;
+    if (mine) {
+      const uint4 kw = lc.carry.keys[i];
+      carry = Key{kw.x, kw.y, kw.z, kw.w};
+      ep_ret = lc.carry.ep_return[i];
+      ep_len = lc.carry.ep_length[i];
+      load(s, c, st, i, lc.n);
+      int act[2];
+      if (RANDOM) {  // all six actions always legal (env.hpp:71-73)
+        const Key ek = split_child(step_key, uint64_t(lc.offset + i));
+        act[0] = int(block_at(ek, 0) % 6u);
+        act[1] = int(block_at(ek, 1) % 6u);
+        *reinterpret_cast<int2*>(lc.v.actions + i * 2) = make_int2(act[0], act[1]);
+      } else {
+        act[0] = lc.v.actions[i * 2];  // caller buffer: only 4-byte alignment is guaranteed
+        act[1] = lc.v.actions[i * 2 + 1];
+      }
+      double reward, shaped[2];
+      int deliveries;
+      done = env_step(s, c, split_child(carry, 0), act, reward, shaped, deliveries);
+      *reinterpret_cast<double2*>(lc.v.rewards + i * 2) = make_double2(reward, reward);
+      double2* inf = reinterpret_cast<double2*>(lc.v.infos + i * 4);  // Info keys in std::map order
+      inf[0] = make_double2(double(deliveries), shaped[0]);
+      inf[1] = make_double2(double(deliveries), shaped[1]);
+      lc.v.dones[i * 3 + 0] = done;
+      lc.v.dones[i * 3 + 1] = done;
+      lc.v.dones[i * 3 + 2] = done;
+      ep_ret = ep_ret + (reward + reward) / 2.0;  // team_reward, vector_env.cpp:14-18
+      ep_len = ep_len + 1;
+      lc.v.finished[i] = done;
+      lc.v.final_returns[i] = done ? ep_ret : 0.0;
+      lc.v.final_lengths[i] = done ? ep_len : 0;
     }
-    double reward, shaped[2];
-    int deliveries;
-    done = env_step(s, c, split_child(carry, 0), act, reward, shaped, deliveries);
-    for (int a = 0; a < 2; ++a) {
-      m.rew[tid * 2 + a] = reward;
-      m.inf[(tid * 2 + a) * 2 + 0] = double(deliveries);  // Info keys in std::map order
-      m.inf[(tid * 2 + a) * 2 + 1] = shaped[a];
-      m.done[tid * 3 + a] = done;
+    stats_add(lc.stats, done, ep_len, ep_ret);
+
+    // terminal observations of finished envs -> final_obs (rare: one env in
+    // max_steps), then auto-reset (vector_env.cpp:107-119)
+    const unsigned fin = __ballot_sync(0xffffffffu, done);
+    if (fin) {
+      for (unsigned m = fin; m; m &= m - 1) stream_rows(lc.v.final_obs + (w0 + __ffs(m) - 1) * 2 * D, t, 2 * D);
+      __syncwarp();
+      if (done) {
+        for (int a = 0; a < 2; ++a) patch_row(lc.v.final_obs + (i * 2 + a) * D, s, c, a);
+        env_reset(s, c);
+        ep_ret = 0.0;
+        ep_len = 0;
+      }
     }
-    m.done[tid * 3 + 2] = done;
-    ep_ret = ep_ret + (reward + reward) / 2.0;  // team_reward, vector_env.cpp:14-18
-    ep_len = ep_len + 1;
-    lc.v.finished[i] = done;
-    lc.v.final_returns[i] = done ? ep_ret : 0.0;
-    lc.v.final_lengths[i] = done ? ep_len : 0;
+
+    // observation rows
+    const int pairs = tma ? wvalid >> 1 : 0;
+    for (int p = 0; p < pairs; ++p) {
+      float* buf = bufs + (p & 1) * 4 * D;
+      if (p >= 2) {  // the buffer's previous store must have read it; then undo that pair's cells
+        if (lane == 0) bulk_wait_read<1>();
+        __syncwarp();
+        if ((lane >> 1) == p - 2)
+          for (int a = 0; a < 2; ++a) patch_row<true>(buf + ((lane & 1) * 2 + a) * D, s, c, a);
+        __syncwarp();
+      }
+      if ((lane >> 1) == p)
+        for (int a = 0; a < 2; ++a) patch_row(buf + ((lane & 1) * 2 + a) * D, s, c, a);
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        bulk_store_s2g(lc.v.obs + (w0 + 2 * p) * 2 * D, buf, uint32_t(16 * D));
+        bulk_commit();
+      }
+    }
+    if (pairs > 0) {  // leave both buffers as clean template rows for the next chunk
+      if (lane == 0) bulk_wait_read<0>();
+      __syncwarp();
+      if ((lane >> 1) >= pairs - 2 && (lane >> 1) < pairs)
+        for (int a = 0; a < 2; ++a) patch_row<true>(bufs + ((lane >> 1) & 1) * 4 * D + ((lane & 1) * 2 + a) * D, s, c, a);
+      __syncwarp();
+    }
+    const int direct0 = 2 * pairs;  // envs not covered by a bulk store (odd tail / no TMA)
+    if (direct0 < wvalid) {
+      stream_rows(lc.v.obs + (w0 + direct0) * 2 * D, t, (wvalid - direct0) * 2 * D);
+      __syncwarp();
+      if (mine && lane >= direct0)
+        for (int a = 0; a < 2; ++a) patch_row(lc.v.obs + (i * 2 + a) * D, s, c, a);
+    }
+    if (mine) {
+      const Key nk = split_child(carry, 2);  // vector_env.cpp:126
+      lc.carry.keys[i] = make_uint4(nk.k0, nk.k1, nk.c0, nk.c1);
+      lc.carry.ep_return[i] = ep_ret;
+      lc.carry.ep_length[i] = ep_len;
+      store(s, c, st, i, lc.n);
+    }
   }
-  if (tid < kE) m.fin[tid] = done;
-  __syncthreads();  // template rows filled
-  if (mine)
-    for (int a = 0; a < 2; ++a) patch_row(m.tile + (size_t(tid) * 2 + a) * D, s, c, a);
-  // episode stats: threads >= kE contribute nothing
-  stats_add(lc.stats, done, ep_len, ep_ret);
-  if (__syncthreads_or(done)) {
-    // terminal rows of finished envs -> final_obs, then re-render reset rows
-    for (int e = 0; e < nvalid; ++e) {
-      if (!m.fin[e]) continue;
-      float* src = m.tile + size_t(e) * 2 * D;
-      float* dst = lc.v.final_obs + (i0 + e) * 2 * D;
-      for (int k = tid; k < 2 * D; k += blockDim.x) __stcs(dst + k, src[k]);
-    }
-    __syncthreads();
-    fill_rows(m.tile, m.templ, D, 2 * nvalid, m.fin);
-    __syncthreads();
-    if (done) {
-      env_reset(s, c);
-      ep_ret = 0.0;
-      ep_len = 0;
-      for (int a = 0; a < 2; ++a) patch_row(m.tile + (size_t(tid) * 2 + a) * D, s, c, a);
-    }
-  }
-  if (mine) {
-    Key nk = split_child(carry, 2);
-    lc.carry.keys[i] = make_uint4(nk.k0, nk.k1, nk.c0, nk.c1);
-    lc.carry.ep_return[i] = ep_ret;
-    lc.carry.ep_length[i] = ep_len;
-    store(s, c, st, i, lc.n);
-  }
-  __syncthreads();
-  block_store(lc.v.obs + i0 * 2 * D, m.tile, size_t(nvalid) * 2 * D * 4);
-  block_store(lc.v.rewards + i0 * 2, m.rew, size_t(nvalid) * 2 * 8);
-  block_store(lc.v.infos + i0 * 4, m.inf, size_t(nvalid) * 4 * 8);
-  block_store(lc.v.dones + i0 * 3, m.done, size_t(nvalid) * 3);
-  if (RANDOM) block_store(lc.v.actions + i0 * 2, m.act, size_t(nvalid) * 2 * 4);
+  if (tma && lane == 0) bulk_wait<0>();  // every bulk store has landed before the CTA retires
 }
 
 __global__ void oc_hash_kernel(OcConfig c, OcState st, int64_t n, uint64_t* out) {
@@ -385,24 +438,45 @@ Key to_key(KeyWords k) { return Key{k.w[0], k.w[1], k.w[2], k.w[3]}; }
 
 }  // namespace
 
-size_t oc_smem_bytes(const OcConfig& c) { return smem_bytes(kPlanes * c.h * c.w + 1); }
+size_t oc_smem_bytes(const OcConfig& c) { return 4 * tmpl_floats(kPlanes * c.h * c.w + 1) * sizeof(float); }
 
 void oc_launch_reset_t(const OcConfig& c, const float* templ, const OcState& s, const LaunchCommon& lc,
                        KeyWords key, KeyWords carry_parent) {
   size_t sm = oc_smem_bytes(c);
   cudaFuncSetAttribute(oc_reset_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
-  unsigned g = unsigned((lc.n + kE - 1) / kE);
+  unsigned g = unsigned((lc.n + kThreads - 1) / kThreads);
   oc_reset_kernel<<<g, kThreads, sm, lc.stream>>>(c, templ, s, lc, to_key(key), to_key(carry_parent));
   ++g_launches;
 }
 
 void oc_launch_step_t(const OcConfig& c, const float* templ, const OcState& s, const LaunchCommon& lc,
                       bool random, KeyWords step_key) {
-  size_t sm = oc_smem_bytes(c);
+  const int D = kPlanes * c.h * c.w + 1;
+  // Persistent grid: as many 8-warp (or fewer, for large layouts) blocks as
+  // fit on the device; TMA row buffers when they fit in shared memory.
+  static int sms = 0, max_smem = 0;
+  if (sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  }
+  int warps = kThreads / 32, tma = 1;
+  while (warps > 1 && oc_tma_smem_floats(D, warps) * 4 > size_t(max_smem)) --warps;
+  size_t sm = oc_tma_smem_floats(D, warps) * 4;
+  if (sm > size_t(max_smem)) {  // layout too large for the buffers: plain streaming stores
+    tma = 0;
+    warps = kThreads / 32;
+    sm = oc_smem_bytes(c);
+  }
   auto fn = random ? oc_step_kernel<true> : oc_step_kernel<false>;
   cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
-  unsigned g = unsigned((lc.n + kE - 1) / kE);
-  fn<<<g, kThreads, sm, lc.stream>>>(c, templ, s, lc, to_key(step_key));
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, warps * 32, sm);
+  const int64_t chunks = (lc.n + 31) / 32;
+  const int64_t want = (chunks + warps - 1) / warps;
+  const int64_t cap = int64_t(std::max(per_sm, 1)) * sms;
+  fn<<<unsigned(std::min(want, cap)), warps * 32, sm, lc.stream>>>(c, templ, s, lc, to_key(step_key), tma);
   ++g_launches;
 }
 

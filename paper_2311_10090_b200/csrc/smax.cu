@@ -35,6 +35,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "engine.h"
@@ -925,6 +926,11 @@ Params make_params(const SmaxConfig& c) {
 // Group shape for a roster of n units: lanes per env and units per lane.
 int shape_id(const SmaxConfig& c) {
   const int n = c.na + c.ne;
+  if (const char* f = std::getenv("MARL_SMAX_SHAPE")) {  // tuning override: 0 (8x1) 1 (16x1) 2 (32x1) 3 (32x2) 4 (4x2)
+    const int v = std::atoi(f);
+    const int lanes[5] = {8, 16, 32, 32, 4}, upl[5] = {1, 1, 1, 2, 2};
+    if (v >= 0 && v < 5 && lanes[v] * upl[v] >= n) return v;
+  }
   return n <= 8 ? 4 : n <= 16 ? 1 : n <= 32 ? 2 : 3;
 }
 
