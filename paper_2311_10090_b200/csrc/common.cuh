@@ -236,6 +236,21 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
+// Block-wide store of a shared-memory tile: one TMA bulk store issued by
+// thread 0 when the tile and its destination qualify (16-byte aligned, size a
+// multiple of 16), else the cooperative vector copy.  Call from every thread
+// after the tile is complete; the caller fences and synchronises first
+// (bulk_tile_fence).  Thread 0 waits for the TMA engine to finish READING the
+// tile, so the caller must not overwrite it before the next barrier.
+__device__ __forceinline__ bool bulk_ok(const void* gdst, const void* ssrc, size_t bytes) {
+  return ((reinterpret_cast<uintptr_t>(gdst) | reinterpret_cast<uintptr_t>(ssrc) | bytes) & 15) == 0 && bytes > 0;
+}
+__device__ __forceinline__ void bulk_tile_fence() {
+  fence_proxy_async_smem();
+  __syncthreads();
+}
+__device__ __forceinline__ void tile_store(void* gdst, const void* ssrc, size_t bytes);
+
 // Per-block episode statistics, folded into 64-bit integer accumulators so the
 // totals are exact and order-independent (identical for any grid shape and any
 // number of GPUs): [0] finished episodes, [1] sum of lengths, [2] sum of
@@ -255,6 +270,20 @@ __device__ __forceinline__ void stats_add(unsigned long long* stats, bool finish
     atomicAdd(stats + 1, L);
     atomicAdd(stats + 2, R);
   }
+}
+__device__ __forceinline__ void tile_store(void* gdst, const void* ssrc, size_t bytes) {
+  if (bulk_ok(gdst, ssrc, bytes)) {
+    if (threadIdx.x == 0) {
+      bulk_store_s2g(gdst, ssrc, uint32_t(bytes));
+      bulk_commit();
+    }
+  } else {
+    block_store(gdst, ssrc, bytes);
+  }
+}
+// Thread 0: the tiles issued by tile_store have been read out of shared memory.
+__device__ __forceinline__ void tile_store_drain() {
+  if (threadIdx.x == 0) bulk_wait_read<0>();
 }
 #endif
 

@@ -75,8 +75,17 @@ struct Local {  // one env's MpeState (mpe.cpp:31-37) in registers
   int goal;
 };
 
-__device__ __forceinline__ double logaddexp0(double z) {  // mpe.cpp:39-41
-  return z > 0 ? z + log1p(exp(-z)) : log1p(exp(z));
+// log(1 + e^z) (mpe.cpp:39-41).  Contacts are soft with margin 1e-3, so for
+// all but touching agents z is hugely negative: e^z < 2^-60 makes log1p(e^z)
+// round to e^z itself (the next series term is below half an ulp), and below
+// -745 e^z is 0 -- the libm calls are skipped with the same result.
+__device__ __forceinline__ double log1p_exp_neg(double z) {  // z <= 0
+  if (z < -746.0) return 0.0;
+  const double t = exp(z);
+  return t < 0x1p-60 ? t : log1p(t);
+}
+__device__ __forceinline__ double logaddexp0(double z) {
+  return z > 0 ? z + log1p_exp_neg(-z) : log1p_exp_neg(z);
 }
 
 template <class Sc>
@@ -422,11 +431,13 @@ __global__ void __launch_bounds__(kThreads) mpe_step_kernel(MpeState st, LaunchC
     lc.carry.ep_length[i] = ep_len;
     store_state<Sc, S>(s, st, i, lc.n, done);
   }
-  __syncthreads();
-  block_store(lc.v.obs + i0 * ROW, s_obs, size_t(nvalid) * ROW * sizeof(float));
-  block_store(lc.v.rewards + i0 * A, s_rew, size_t(nvalid) * A * sizeof(double));
-  block_store(lc.v.dones + i0 * (A + 1), s_done, size_t(nvalid) * (A + 1));
-  if (RANDOM) block_store(lc.v.actions + i0 * A, s_act, size_t(nvalid) * A * sizeof(int32_t));
+  // the block's rows leave as TMA bulk stores (one instruction per tile)
+  bulk_tile_fence();
+  tile_store(lc.v.obs + i0 * ROW, s_obs, size_t(nvalid) * ROW * sizeof(float));
+  tile_store(lc.v.rewards + i0 * A, s_rew, size_t(nvalid) * A * sizeof(double));
+  tile_store(lc.v.dones + i0 * (A + 1), s_done, size_t(nvalid) * (A + 1));
+  if (RANDOM) tile_store(lc.v.actions + i0 * A, s_act, size_t(nvalid) * A * sizeof(int32_t));
+  tile_store_drain();
 }
 
 // state_hash (mpe.cpp:254-269), parity aid.
