@@ -224,14 +224,20 @@ __device__ __forceinline__ void separation_pass(const Params& P, EnvSm<CAP>& e, 
   }
 }
 
-// Does any living pair of this lane's share possibly overlap?  (Conservative:
-// a false "yes" only costs an exact pass that pushes nothing.)
+// Does any living pair of this lane's share overlap right now (the exact
+// reference test, hypot only inside the rounding band)?  If no pair overlaps
+// at the start of a pass, the pass pushes nothing -- so it is skipped.
 template <int G, int CAP>
-__device__ __forceinline__ bool lane_pairs_may_overlap(const Params& P, const EnvSm<CAP>& e, int gl) {
+__device__ __forceinline__ bool lane_pairs_overlap(const Params& P, const EnvSm<CAP>& e, int gl) {
   for (PairIt it(gl, P.n); it.valid(); it.advance(G)) {
-    if (e.h[it.a] <= 0.0 || e.h[it.b] <= 0.0) continue;
-    double dx = e.x[it.b] - e.x[it.a], dy = e.y[it.b] - e.y[it.a];
-    if (!(dx * dx + dy * dy > P.sep_r2hi)) return true;
+    const int a = it.a, b = it.b;
+    if (e.h[a] <= 0.0 || e.h[b] <= 0.0) continue;
+    const double dx = e.x[b] - e.x[a], dy = e.y[b] - e.y[a];
+    const double d2 = dx * dx + dy * dy;
+    if (d2 > P.sep_r2hi) continue;  // farther than any radius sum
+    const Thresh& R = P.ps[P.type[a]][P.type[b]].rsum;
+    if (d2 > R.r2hi) continue;
+    if (d2 < R.r2lo || R.r - hypot_glibc(dx, dy) > 0.0) return true;
   }
   return false;
 }
@@ -259,7 +265,7 @@ template <int G, int UPL, int CAP>
 __device__ __forceinline__ void separate(const Params& P, EnvSm<CAP>& e, const Grp<G>& g, bool fixpoint) {
   unsigned long long alive = 0;
   for (int pass = 0; pass < (fixpoint ? 256 : 1); ++pass) {
-    if (!g.any(lane_pairs_may_overlap<G>(P, e, g.gl))) break;
+    if (!g.any(lane_pairs_overlap<G>(P, e, g.gl))) break;
     if (pass == 0) {  // health is constant during separation
       bool al[UPL];
 #pragma unroll
@@ -729,7 +735,7 @@ __global__ void __launch_bounds__(kThreads, 3) smax_step_kernel(const Params* __
     // caller / the probe's random-legal stream, enemies from the heuristic
     int act[UPL];
     Key ek{0, 0, 0, 0};
-    if (RANDOM) ek = split_child_nl(step_key, uint64_t(lc.offset + i));  // vector_env.cpp:171
+    if (RANDOM) ek = split_child(step_key, uint64_t(lc.offset + i));  // vector_env.cpp:171
 #pragma unroll
     for (int j = 0; j < UPL; ++j) {
       const int u = g.gl + G * j;
@@ -822,7 +828,7 @@ __global__ void __launch_bounds__(kThreads, 3) smax_step_kernel(const Params* __
   }
   if (live) {
     if (g.gl == 0) {
-      const Key nk = split_child_nl(carry, 2);  // vector_env.cpp:126
+      const Key nk = split_child(carry, 2);  // vector_env.cpp:126
       lc.carry.keys[i] = make_uint4(nk.k0, nk.k1, nk.c0, nk.c1);
       lc.carry.ep_return[i] = ep_ret;
       lc.carry.ep_length[i] = ep_len;
@@ -931,7 +937,7 @@ int shape_id(const SmaxConfig& c) {
     const int lanes[5] = {8, 16, 32, 32, 4}, upl[5] = {1, 1, 1, 2, 2};
     if (v >= 0 && v < 5 && lanes[v] * upl[v] >= n) return v;
   }
-  return n <= 8 ? 4 : n <= 16 ? 1 : n <= 32 ? 2 : 3;
+  return n <= 8 ? 0 : n <= 16 ? 1 : n <= 32 ? 2 : 3;
 }
 
 template <int G, int UPL>

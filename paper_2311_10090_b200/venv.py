@@ -225,10 +225,15 @@ class VectorEnv:
 
     # ---- views
     def view(self, name: str):
-        """Zero-copy torch tensor over one engine buffer."""
-        shape, ts = self._shapes[name]
-        ptr = getattr(self._views, name)
-        return self._torch.as_tensor(_DevArray(ptr, shape, ts), device=f"cuda:{self._device}")
+        """Zero-copy torch tensor over one engine buffer (the buffers never move
+        for the life of the handle, so each view is built once)."""
+        cache = self.__dict__.setdefault("_view_cache", {})
+        t = cache.get(name)
+        if t is None:
+            shape, ts = self._shapes[name]
+            ptr = getattr(self._views, name)
+            t = cache[name] = self._torch.as_tensor(_DevArray(ptr, shape, ts), device=f"cuda:{self._device}")
+        return t
 
     def _state(self) -> BatchedState:
         return BatchedState(self, self._version, self.view("keys"), self.view("episode_returns"),
