@@ -168,6 +168,10 @@ int marl_venv_step_random_host(marl_venv* h, const uint32_t step_key[4], const m
 int marl_venv_download(marl_venv* h, const marl_host_step* out);
 
 int marl_venv_views(marl_venv* h, marl_views* out);
+/* Synchronous copy of `bytes` from a device pointer (e.g. a marl_views field)
+ * to host memory: lets C/C++ callers without the CUDA runtime read views
+ * (used by the reference-side adapter include/marl_b200_vector_env.hpp). */
+int marl_copy_device_to_host(void* dst, const void* src, size_t bytes);
 
 /* Env::legal_actions (env.hpp:71-73; smax.cpp:195-211) for the current
  * state: d_out [N][A][n_actions] u8 (device). */

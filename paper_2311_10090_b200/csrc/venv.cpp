@@ -801,6 +801,13 @@ int marl_venv_download(marl_venv* h, const marl_host_step* out) {
   });
 }
 
+int marl_copy_device_to_host(void* dst, const void* src, size_t bytes) {
+  return guarded([&] {
+    if (bytes && (!dst || !src)) raise(MARL_ERR_CONTRACT, "marl_copy_device_to_host: NULL pointer");
+    if (bytes) cuda_check(cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost), "cudaMemcpy D2H");
+  });
+}
+
 int marl_venv_views(marl_venv* h, marl_views* o) {
   return guarded([&] {
     o->obs = h->v.obs;
