@@ -188,6 +188,58 @@ int marl_venv_episode_stats(marl_venv* h, int64_t out[3], int clear);
 
 int marl_venv_sync(marl_venv* h);
 
+/* ---- IPPO rollout collection (config 5) -------------------------------
+ * The reference's Collector (proj/core/src/algo/ppo.cpp:178-374, private):
+ * per step the actor/critic feed-forward nets (ff_forward,
+ * actor_critic.hpp:49-52) over the TeamLayout rows (team.cpp:27-33), masked
+ * sampling with per-row keys fold_in(act_key, (seq_base+t)*R + r)
+ * (ppo.cpp:249-259), the env step, and the rollout buffer; then bootstrap
+ * values and GAE (ppo.cpp:285-321).  Buffers are [T][R] (R = envs x agents),
+ * device-resident, valid until the next collect. */
+typedef struct marl_rollout marl_rollout;
+
+typedef struct {
+  int32_t in_dim;           /* PpoNetSpec::in_dim: padded obs + agent one-hot (ppo.cpp:80-107) */
+  int32_t n_actions;        /* PpoNetSpec::n_actions (padded action head) */
+  int32_t width, n_layers, relu;
+  int32_t n_actor_params;   /* floats in PpoNets::pack_actor() order (nn::pack, nn.hpp:326-341) */
+  int32_t n_critic_params;
+  int32_t rows_per_env;     /* agents */
+} marl_policy_spec;
+
+typedef struct { /* device pointers, [T][R] row-major */
+  float* obs;        /* [T][R][in_dim] */
+  int32_t* actions;
+  float* rewards;
+  uint8_t* dones;
+  uint8_t* resets;
+  float* logp;
+  float* value;
+  uint8_t* legal;    /* [T][R][n_actions] */
+  float* active;
+  float* adv;
+  float* vtarg;
+  float* last_value; /* [R] */
+  int32_t T;
+  int64_t R;
+  int32_t in_dim, n_actions;
+} marl_rollout_views;
+
+/* ppo_net_spec(env, cfg, false) for fc_width/n_fc_layers/activation. */
+int marl_rollout_policy_spec(const marl_venv* h, int width, int n_layers, int relu, marl_policy_spec* out);
+/* precision 0: fp32 in the reference's accumulation order (parity path);
+ * precision 1: bf16 operands, fp32 accumulation on tcgen05 tensor cores. */
+int marl_rollout_create(marl_venv* h, int T, int width, int n_layers, int relu, int precision,
+                        marl_rollout** out);
+/* Host parameters in PpoNets::pack_actor()/pack_critic() order. */
+int marl_rollout_set_params(marl_rollout* r, const float* actor, const float* critic);
+/* Collector constructor (ppo.cpp:189-192): reset(fold_in(key,1)), act_key = fold_in(key,2). */
+int marl_rollout_begin(marl_rollout* r, const uint32_t key[4]);
+/* Collector::collect(nets, T, seq_base, shaping) (ppo.cpp:206-323) + GAE. Asynchronous. */
+int marl_rollout_collect(marl_rollout* r, int64_t seq_base, double gamma, double lambda, double shaping);
+int marl_rollout_get_views(marl_rollout* r, marl_rollout_views* out);
+int marl_rollout_destroy(marl_rollout* r);
+
 /* ---- the reference's own benchmark --------------------------------------- */
 
 /* throughput_probe(env_id, n_envs, n_steps, key, config) (vector_env.cpp:

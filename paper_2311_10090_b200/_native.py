@@ -27,6 +27,17 @@ class Views(C.Structure):
                                           "keys", "episode_returns", "episode_lengths")]
 
 
+class PolicySpec(C.Structure):
+    _fields_ = [(n, C.c_int32) for n in ("in_dim", "n_actions", "width", "n_layers", "relu",
+                                         "n_actor_params", "n_critic_params", "rows_per_env")]
+
+
+class RolloutViews(C.Structure):
+    _fields_ = [(n, C.c_void_p) for n in ("obs", "actions", "rewards", "dones", "resets", "logp", "value",
+                                          "legal", "active", "adv", "vtarg", "last_value")] + \
+               [("T", C.c_int32), ("R", C.c_int64), ("in_dim", C.c_int32), ("n_actions", C.c_int32)]
+
+
 class HostStep(C.Structure):
     _fields_ = [(n, C.c_void_p) for n in ("obs", "rewards", "dones", "finished", "final_obs",
                                           "final_returns", "final_lengths", "infos", "actions")]
@@ -42,6 +53,8 @@ EXPORTS = [
     "marl_venv_episode_stats", "marl_venv_sync", "marl_throughput_probe",
     "marl_prng_key_from_seed", "marl_prng_split", "marl_prng_fold_in", "marl_prng_bits",
     "marl_threefry2x32", "marl_last_error", "marl_launch_count", "marl_version",
+    "marl_rollout_policy_spec", "marl_rollout_create", "marl_rollout_set_params", "marl_rollout_begin",
+    "marl_rollout_collect", "marl_rollout_get_views", "marl_rollout_destroy",
 ]
 
 _lib = None
@@ -89,6 +102,13 @@ def lib() -> C.CDLL:
     L.marl_prng_bits.argtypes = [u32p, C.c_uint64]
     L.marl_prng_bits.restype = C.c_uint64
     L.marl_threefry2x32.argtypes = [C.c_uint32] * 4 + [u32p]
+    L.marl_rollout_policy_spec.argtypes = [vp, C.c_int, C.c_int, C.c_int, C.POINTER(PolicySpec)]
+    L.marl_rollout_create.argtypes = [vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(vp)]
+    L.marl_rollout_set_params.argtypes = [vp, vp, vp]
+    L.marl_rollout_begin.argtypes = [vp, u32p]
+    L.marl_rollout_collect.argtypes = [vp, C.c_int64, C.c_double, C.c_double, C.c_double]
+    L.marl_rollout_get_views.argtypes = [vp, C.POINTER(RolloutViews)]
+    L.marl_rollout_destroy.argtypes = [vp]
     L.marl_last_error.restype = C.c_char_p
     L.marl_launch_count.restype = C.c_uint64
     L.marl_version.restype = C.c_char_p

@@ -145,6 +145,69 @@ void oc_launch_step_t(const OcConfig& c, const float* templ, const OcState& s, c
 void oc_launch_hash(const OcConfig& c, const OcState& s, int64_t n, uint64_t* out,
                     cudaStream_t st);
 
+// ------------------------------------------------------ IPPO rollout (C5)
+// Collector::collect (ppo.cpp:206-323) buffers, [T][R] row-major with
+// R = envs x agents (TeamLayout rows, team.cpp:27-33).
+struct RolloutBufs {
+  float* obs;          // [T][R][in_dim] actor input (IPPO critic input is the same row)
+  int32_t* actions;    // [T][R]  (slice t doubles as the env step's [E][A] action input)
+  float* rewards;      // [T][R]
+  uint8_t* dones;      // [T][R]
+  uint8_t* resets;     // [T][R]
+  float* logp;         // [T][R]
+  float* value;        // [T][R]
+  uint8_t* legal;      // [T][R][n_act]
+  float* active;       // [T][R]
+  float* adv;          // [T][R]
+  float* vtarg;        // [T][R]
+  float* last_value;   // [R]  bootstrap values after the window (ppo.cpp:285-299)
+};
+
+// Feed-forward actor and critic (ff_forward, actor_critic.hpp:49-52) with two
+// activated torso layers: pointers into the packed fp32 parameters in
+// nn::pack order (torso w,b per layer, then head w,b; w is [out][in]).
+struct PolicyNet {
+  const float *w1, *b1, *w2, *b2, *w3, *b3;
+  const float *cw1, *cb1, *cw2, *cb2, *cw3, *cb3;
+  int in_dim, n_act, width, relu;
+};
+
+// bf16 operand images for the tcgen05 path (K-major, no swizzle, UMMA
+// canonical layout); built once per parameter upload.
+struct PolicyNetBf16 {
+  const uint16_t* a1;   // [128 x 32] : actor W1 rows 0..63, critic W1 rows 64..127, K padded to 32
+  const uint16_t* a2;   // [64 x 64]  actor W2
+  const uint16_t* c2;   // [64 x 64]  critic W2
+  const uint16_t* h3;   // [16 x 64]  actor head (rows 0..n_act-1), zero padded
+  const uint16_t* hc3;  // [16 x 64]  critic head (row 0), zero padded
+  const float* bias;    // [64 b1a | 64 b1c | 64 b2a | 64 b2c | 16 b3a | 16 b3c]
+};
+
+struct PolicyStep {
+  const float* env_obs;        // [E][A][D] current observations
+  const uint8_t* prev_finished;  // [E] or null: every row starts an episode (Collector ctor)
+  const int32_t* agent_actions;  // [A] device: per-agent action count (legal padding, team.cpp:35-42)
+  int A, D, family;
+  int64_t R, row0, R_global;   // local rows, global index of local row 0, global rows
+  uint32_t act_key[4];         // Collector act_key = fold_in(key, 2) (ppo.cpp:192)
+  int64_t step_index;          // seq_base + t
+  int t;
+  int bootstrap;               // 1: critic only -> last_value (ppo.cpp:285-299)
+  int legal_ready;             // 1: bufs.legal slice t already filled by the env's legal kernel
+};
+
+void rollout_policy_fp32(const PolicyNet& net, const PolicyStep& s, const RolloutBufs& b, cudaStream_t st);
+bool rollout_policy_bf16_supported(int in_dim, int n_act, int width);
+void rollout_policy_bf16(const PolicyNet& net, const PolicyNetBf16& nb, const PolicyStep& s, const RolloutBufs& b,
+                         cudaStream_t st);
+void rollout_pack_bf16(const PolicyNet& net, uint16_t* images, float* bias, cudaStream_t st);
+// rewards / dones of step t from the env's views (ppo.cpp:262-276)
+void rollout_record(const RolloutBufs& b, int t, int64_t R, int A, const double* env_rewards,
+                    const double* env_infos, int n_info, int shaped_idx, double shaping,
+                    const uint8_t* env_finished, cudaStream_t st);
+// GAE per row (compute_gae, actor_critic.hpp:282-299)
+void rollout_gae(const RolloutBufs& b, int T, int64_t R, float gamma, float lambda, cudaStream_t st);
+
 // ------------------------------------------------------------ common
 // Device-side Env::validate_actions (env.cpp:7-14): n_actions per agent.
 void launch_validate(const int32_t* actions, int64_t n, int A, const int32_t* n_actions_dev,

@@ -845,6 +845,247 @@ int marl_venv_legal(marl_venv* h, uint8_t* d_out) {
   });
 }
 
+// ------------------------------------------------------ IPPO rollout (C5)
+struct marl_rollout {
+  marl_venv* h = nullptr;
+  int T = 0;
+  int64_t R = 0, R_global = 0, row0 = 0;
+  int in_dim = 0, n_act = 0, width = 64, relu = 0, precision = 0;
+  int n_actor = 0, n_critic = 0, shaped_idx = -1;
+  Arena arena;
+  RolloutBufs b{};
+  float* params = nullptr;     // packed actor | critic (fp32, nn::pack order)
+  uint16_t* images = nullptr;  // bf16 UMMA operand images (tcgen05 path)
+  float* bias = nullptr;
+  int32_t* agent_actions = nullptr;
+  uint32_t act_key[4] = {0, 0, 0, 0};
+  bool has_params = false, begun = false, first = true;
+};
+
+namespace {
+
+// ppo_net_spec (ppo.cpp:80-107) over TeamLayout::from_env (team.cpp:10-25).
+void policy_dims(const Env& e, int width, int* in_dim, int* n_act, int* n_actor, int* n_critic) {
+  *in_dim = e.D + (e.A > 1 ? e.A : 0);
+  *n_act = *std::max_element(e.n_actions.begin(), e.n_actions.end());
+  *n_actor = width * *in_dim + width + width * width + width + *n_act * width + *n_act;
+  *n_critic = width * *in_dim + width + width * width + width + width + 1;
+}
+
+PolicyNet net_of(const marl_rollout* r) {
+  PolicyNet n{};
+  const int in = r->in_dim, W = r->width, NA = r->n_act;
+  n.w1 = r->params;
+  n.b1 = n.w1 + W * in;
+  n.w2 = n.b1 + W;
+  n.b2 = n.w2 + W * W;
+  n.w3 = n.b2 + W;
+  n.b3 = n.w3 + NA * W;
+  n.cw1 = n.b3 + NA;
+  n.cb1 = n.cw1 + W * in;
+  n.cw2 = n.cb1 + W;
+  n.cb2 = n.cw2 + W * W;
+  n.cw3 = n.cb2 + W;
+  n.cb3 = n.cw3 + W;
+  n.in_dim = in;
+  n.n_act = NA;
+  n.width = W;
+  n.relu = r->relu;
+  return n;
+}
+
+PolicyNetBf16 net_bf16_of(const marl_rollout* r) {
+  PolicyNetBf16 n{};
+  n.a1 = r->images;
+  n.a2 = n.a1 + 128 * 32;
+  n.c2 = n.a2 + 64 * 64;
+  n.h3 = n.c2 + 64 * 64;
+  n.hc3 = n.h3 + 16 * 64;
+  n.bias = r->bias;
+  return n;
+}
+
+void run_policy(marl_rollout* r, int t, bool bootstrap, int64_t seq_base) {
+  marl_venv* h = r->h;
+  const Env& e = *h->env;
+  PolicyStep s{};
+  s.env_obs = h->v.obs;
+  s.prev_finished = r->first ? nullptr : h->v.finished;
+  s.agent_actions = r->agent_actions;
+  s.A = e.A;
+  s.D = e.D;
+  s.family = e.family;
+  s.R = r->R;
+  s.row0 = r->row0;
+  s.R_global = r->R_global;
+  std::memcpy(s.act_key, r->act_key, 16);
+  s.step_index = seq_base + t;
+  s.t = t;
+  s.bootstrap = bootstrap ? 1 : 0;
+  s.legal_ready = (!bootstrap && e.family == MARL_FAMILY_SMAX) ? 1 : 0;
+  if (s.legal_ready)  // Env::legal_actions straight into the buffer slice (team.cpp:35-42)
+    smax_launch_legal(e.smax, h->smax, h->n, r->n_act, r->b.legal + size_t(t) * size_t(r->R) * r->n_act, h->stream);
+  if (r->precision == 1)
+    rollout_policy_bf16(net_of(r), net_bf16_of(r), s, r->b, h->stream);
+  else
+    rollout_policy_fp32(net_of(r), s, r->b, h->stream);
+  after_launch();
+}
+
+}  // namespace
+
+extern "C" {
+
+int marl_rollout_policy_spec(const marl_venv* h, int width, int n_layers, int relu, marl_policy_spec* out) {
+  return guarded([&] {
+    if (!h || !out) raise(MARL_ERR_CONTRACT, "marl_rollout_policy_spec: NULL argument");
+    if (n_layers != 2) raise(MARL_ERR_SCHEMA, "rollout: the B200 policy kernels implement n_fc_layers = 2");
+    if (width < 1 || width > 64) raise(MARL_ERR_SCHEMA, "rollout: fc_width must be in [1, 64]");
+    *out = marl_policy_spec{};
+    policy_dims(*h->env, width, &out->in_dim, &out->n_actions, &out->n_actor_params, &out->n_critic_params);
+    out->width = width;
+    out->n_layers = n_layers;
+    out->relu = relu;
+    out->rows_per_env = h->env->A;
+  });
+}
+
+int marl_rollout_create(marl_venv* h, int T, int width, int n_layers, int relu, int precision, marl_rollout** out) {
+  return guarded([&] {
+    if (!h || !out) raise(MARL_ERR_CONTRACT, "marl_rollout_create: NULL argument");
+    if (T < 1) raise(MARL_ERR_CONTRACT, "rollout: n_rollout_steps must be >= 1");
+    marl_policy_spec ps{};
+    if (marl_rollout_policy_spec(h, width, n_layers, relu, &ps) != MARL_OK) raise(MARL_ERR_SCHEMA, marl_last_error());
+    if (ps.in_dim > 1024 || ps.n_actions > 64) raise(MARL_ERR_SCHEMA, "rollout: input wider than 1024 or > 64 actions");
+    if (precision == 1 && !rollout_policy_bf16_supported(ps.in_dim, ps.n_actions, width))
+      raise(MARL_ERR_SCHEMA, "rollout: the tcgen05 bf16 policy needs in_dim <= 32, n_actions <= 16, fc_width == 64");
+    if (precision != 0 && precision != 1) raise(MARL_ERR_SCHEMA, "rollout: precision must be 0 (fp32) or 1 (bf16)");
+    set_device(h);
+    auto r = std::make_unique<marl_rollout>();
+    r->h = h;
+    r->T = T;
+    const Env& e = *h->env;
+    r->R = h->n * e.A;
+    r->row0 = h->off * e.A;
+    r->R_global = h->gn * e.A;
+    r->in_dim = ps.in_dim;
+    r->n_act = ps.n_actions;
+    r->width = width;
+    r->relu = relu;
+    r->precision = precision;
+    r->n_actor = ps.n_actor_params;
+    r->n_critic = ps.n_critic_params;
+    for (size_t k = 0; k < e.info_names.size(); ++k)
+      if (e.info_names[k] == "shaped_reward") r->shaped_idx = int(k);
+    const size_t TR = size_t(T) * size_t(r->R);
+    Arena& ar = r->arena;
+    ar.add(&r->b.obs, TR * size_t(r->in_dim));
+    ar.add(&r->b.actions, TR);
+    ar.add(&r->b.rewards, TR);
+    ar.add(&r->b.dones, TR);
+    ar.add(&r->b.resets, TR);
+    ar.add(&r->b.logp, TR);
+    ar.add(&r->b.value, TR);
+    ar.add(&r->b.legal, TR * size_t(r->n_act));
+    ar.add(&r->b.active, TR);
+    ar.add(&r->b.adv, TR);
+    ar.add(&r->b.vtarg, TR);
+    ar.add(&r->b.last_value, size_t(r->R));
+    ar.add(&r->params, size_t(r->n_actor + r->n_critic));
+    ar.add(&r->images, size_t(128 * 32 + 2 * 64 * 64 + 2 * 16 * 64));
+    ar.add(&r->bias, size_t(4 * 64 + 2 * 16));
+    ar.add(&r->agent_actions, size_t(e.A));
+    ar.commit();
+    cuda_check(cudaMemcpy(r->agent_actions, e.n_actions.data(), size_t(e.A) * 4, cudaMemcpyHostToDevice), "cudaMemcpy");
+    *out = r.release();
+  });
+}
+
+int marl_rollout_set_params(marl_rollout* r, const float* actor, const float* critic) {
+  return guarded([&] {
+    if (!r || !actor || !critic) raise(MARL_ERR_CONTRACT, "marl_rollout_set_params: NULL argument");
+    set_device(r->h);
+    cuda_check(cudaMemcpy(r->params, actor, size_t(r->n_actor) * 4, cudaMemcpyHostToDevice), "cudaMemcpy");
+    cuda_check(cudaMemcpy(r->params + r->n_actor, critic, size_t(r->n_critic) * 4, cudaMemcpyHostToDevice),
+               "cudaMemcpy");
+    if (r->precision == 1) {
+      rollout_pack_bf16(net_of(r), r->images, r->bias, r->h->stream);
+      after_launch();
+    }
+    r->has_params = true;
+  });
+}
+
+// Collector constructor (ppo.cpp:189-192): reset with fold_in(key, 1), act_key
+// = fold_in(key, 2), every row starts an episode.
+int marl_rollout_begin(marl_rollout* r, const uint32_t key[4]) {
+  return guarded([&] {
+    if (!r || !key) raise(MARL_ERR_CONTRACT, "marl_rollout_begin: NULL argument");
+    uint32_t rk[4];
+    marl_prng_fold_in(key, 1, rk);
+    if (marl_venv_reset(r->h, rk) != MARL_OK) raise(MARL_ERR_CUDA, marl_last_error());
+    marl_prng_fold_in(key, 2, r->act_key);
+    r->begun = true;
+    r->first = true;
+  });
+}
+
+// Collector::collect(nets, T, seq_base, shaping) (ppo.cpp:206-323).
+int marl_rollout_collect(marl_rollout* r, int64_t seq_base, double gamma, double lambda, double shaping) {
+  return guarded([&] {
+    if (!r) raise(MARL_ERR_CONTRACT, "marl_rollout_collect: NULL rollout");
+    if (!r->begun) raise(MARL_ERR_CONTRACT, "rollout: call begin() before collect()");
+    if (!r->has_params) raise(MARL_ERR_CONTRACT, "rollout: call set_params() before collect()");
+    marl_venv* h = r->h;
+    set_device(h);
+    const Env& e = *h->env;
+    for (int t = 0; t < r->T; ++t) {
+      run_policy(r, t, false, seq_base);
+      launch_step(h, false, nullptr, r->b.actions + size_t(t) * size_t(r->R));
+      rollout_record(r->b, t, r->R, e.A, h->v.rewards, h->v.infos, e.n_info, r->shaped_idx, shaping,
+                     h->v.finished, h->stream);
+      after_launch();
+      r->first = false;
+    }
+    run_policy(r, r->T, true, seq_base);  // bootstrap values (ppo.cpp:285-299)
+    rollout_gae(r->b, r->T, r->R, float(gamma), float(lambda), h->stream);
+    after_launch();
+  });
+}
+
+int marl_rollout_get_views(marl_rollout* r, marl_rollout_views* o) {
+  return guarded([&] {
+    if (!r || !o) raise(MARL_ERR_CONTRACT, "marl_rollout_get_views: NULL argument");
+    o->obs = r->b.obs;
+    o->actions = r->b.actions;
+    o->rewards = r->b.rewards;
+    o->dones = r->b.dones;
+    o->resets = r->b.resets;
+    o->logp = r->b.logp;
+    o->value = r->b.value;
+    o->legal = r->b.legal;
+    o->active = r->b.active;
+    o->adv = r->b.adv;
+    o->vtarg = r->b.vtarg;
+    o->last_value = r->b.last_value;
+    o->T = r->T;
+    o->R = r->R;
+    o->in_dim = r->in_dim;
+    o->n_actions = r->n_act;
+  });
+}
+
+int marl_rollout_destroy(marl_rollout* r) {
+  return guarded([&] {
+    if (!r) return;
+    set_device(r->h);
+    cudaStreamSynchronize(r->h->stream);
+    delete r;
+  });
+}
+
+}  // extern "C"
+
 int marl_venv_state_hash(marl_venv* h, uint64_t* d_out) {
   return guarded([&] {
     set_device(h);
