@@ -21,10 +21,13 @@
 //   * fp32 (this file, policy_fp32_kernel): one thread per row, weights in
 //     shared memory, every dot product accumulated in the reference's order
 //     with -fmad=false -- the parity path.
-//   * bf16 on the 5th-generation tensor cores (rollout_tc.cu): the three
+//   * bf16 on the 5th-generation tensor cores (policy_tc_kernel below): the three
 //     layers of actor+critic as tcgen05.mma with TMEM accumulators -- the
 //     throughput path.
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
+
+#include <algorithm>
 
 #include "common.cuh"
 #include "engine.h"
@@ -214,9 +217,327 @@ void rollout_record(const RolloutBufs& b, int t, int64_t R, int A, const double*
   ++g_launches;
 }
 
-bool rollout_policy_bf16_supported(int in_dim, int n_act, int width) { return false; }
-void rollout_policy_bf16(const PolicyNet&, const PolicyNetBf16&, const PolicyStep&, const RolloutBufs&, cudaStream_t) {}
-void rollout_pack_bf16(const PolicyNet&, uint16_t*, float*, cudaStream_t) {}
+
+// ===================================================================== tcgen05
+// The bf16 throughput path.  One CTA of 128 threads owns a 128-row tile
+// (UMMA M = 128, row r of the tile = TMEM lane r = thread r):
+//   L1  D[0:128)   = X[128x32]  . [W1_actor ; W1_critic]^T   (N = 128, K = 32)
+//   L2  D[0:64)    = H1a[128x64] . W2_actor^T                 (N = 64,  K = 64)
+//       D[64:128)  = H1c[128x64] . W2_critic^T
+//   L3  D[128:144) = H2a . W3_actor^T (5 rows, padded to 16)  (N = 16,  K = 64)
+//       D[144:160) = H2c . W3_critic^T (1 row, padded)
+// Operands are bf16 in shared memory in the UMMA canonical K-major layout
+// without swizzle (8-row x 16-byte core matrices; LBO = 128 B between the
+// two K halves of a core-matrix pair, SBO = (K/8)*128 B between 8-row
+// groups); accumulators are fp32 in TMEM (256 columns allocated).  One
+// elected thread issues tcgen05.mma and tcgen05.commit to an mbarrier; every
+// thread pulls its row back with tcgen05.ld for the bias + tanh epilogue,
+// converts to bf16 and writes the next layer's A operand.  The weights are
+// staged once per persistent CTA.
+namespace {
+
+constexpr int kTcRows = 128;
+constexpr uint32_t kTmemCols = 256;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// byte offset of element (n, k) in a K-major no-swizzle canonical [N x K] bf16 tile
+__host__ __device__ __forceinline__ uint32_t canon_off(int n, int k, int K) {
+  return uint32_t((n >> 3) * ((K >> 3) * 128) + (k >> 3) * 128 + (n & 7) * 16 + (k & 7) * 2);
+}
+
+__device__ __forceinline__ uint64_t umma_desc(const void* tile, int K, int k0) {
+  const uint32_t addr = smem_u32(tile) + uint32_t(k0 >> 3) * 128u;  // K slice start
+  const uint32_t lbo = 128u, sbo = uint32_t(K >> 3) * 128u;
+  uint64_t d = 0;
+  d |= uint64_t((addr >> 4) & 0x3FFFu);
+  d |= uint64_t((lbo >> 4) & 0x3FFFu) << 16;
+  d |= uint64_t((sbo >> 4) & 0x3FFFu) << 32;
+  d |= uint64_t(1) << 46;  // descriptor version 1 (sm_100); base offset 0; layout SWIZZLE_NONE
+  return d;
+}
+
+// kind::f16 instruction descriptor: bf16 A/B, fp32 D, both K-major, M x N.
+__host__ __device__ constexpr uint32_t idesc_bf16(int M, int N) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(N >> 3) << 17) | (uint32_t(M >> 4) << 24);
+}
+
+__device__ __forceinline__ void umma_bf16(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tWAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}\n" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// 16 consecutive fp32 columns of this thread's TMEM lane.
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
+  const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<const uint32_t*>(&h);
+}
+
+__device__ __forceinline__ float tanh_fast(float x) {  // MUFU.TANH: ~2^-11 relative, below bf16's 2^-8
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// Row `row` of an activation operand: 16 fp32 values at K offset k0 -> bf16
+// into the canonical tile (two 16-byte chunks).
+__device__ __forceinline__ void put16(uint8_t* tile, int K, int row, int k0, const float* v) {
+#pragma unroll
+  for (int c = 0; c < 2; ++c) {
+    uint4 q;
+    q.x = pack_bf16(v[8 * c + 0], v[8 * c + 1]);
+    q.y = pack_bf16(v[8 * c + 2], v[8 * c + 3]);
+    q.z = pack_bf16(v[8 * c + 4], v[8 * c + 5]);
+    q.w = pack_bf16(v[8 * c + 6], v[8 * c + 7]);
+    *reinterpret_cast<uint4*>(tile + canon_off(row, k0 + 8 * c, K)) = q;
+  }
+}
+
+struct TcSmem {  // all tiles 1024-byte aligned
+  uint8_t w1[128 * 32 * 2];  // [W1a ; W1c]  (N=128, K=32)
+  uint8_t w2a[64 * 64 * 2];
+  uint8_t w2c[64 * 64 * 2];
+  uint8_t w3a[16 * 64 * 2];
+  uint8_t w3c[16 * 64 * 2];
+  uint8_t x[kTcRows * 32 * 2];    // layer-1 A operand
+  uint8_t ha[kTcRows * 64 * 2];   // actor hidden (A of L2, then of L3)
+  uint8_t hc[kTcRows * 64 * 2];   // critic hidden
+  float bias[4 * 64 + 2 * 16];
+  uint64_t bar;
+  uint32_t tmem_base;
+};
+
+__global__ void __launch_bounds__(kTcRows) policy_tc_kernel(PolicyNetBf16 nb, int in_dim, int n_act, PolicyStep s,
+                                                            RolloutBufs b) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  TcSmem& S = *reinterpret_cast<TcSmem*>(smem_raw);
+  const int tid = threadIdx.x, warp = tid >> 5;
+
+  // one-time: weights (already in canonical layout) + biases, barrier, TMEM
+  {
+    const uint4* src[5] = {reinterpret_cast<const uint4*>(nb.a1), reinterpret_cast<const uint4*>(nb.a2),
+                           reinterpret_cast<const uint4*>(nb.c2), reinterpret_cast<const uint4*>(nb.h3),
+                           reinterpret_cast<const uint4*>(nb.hc3)};
+    uint4* dst[5] = {reinterpret_cast<uint4*>(S.w1), reinterpret_cast<uint4*>(S.w2a),
+                     reinterpret_cast<uint4*>(S.w2c), reinterpret_cast<uint4*>(S.w3a),
+                     reinterpret_cast<uint4*>(S.w3c)};
+    const int n16[5] = {128 * 32 * 2 / 16, 64 * 64 * 2 / 16, 64 * 64 * 2 / 16, 16 * 64 * 2 / 16, 16 * 64 * 2 / 16};
+    for (int m = 0; m < 5; ++m)
+      for (int q = tid; q < n16[m]; q += blockDim.x) dst[m][q] = __ldg(src[m] + q);
+    for (int q = tid; q < 4 * 64 + 2 * 16; q += blockDim.x) S.bias[q] = __ldg(nb.bias + q);
+    if (tid == 0) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&S.bar)) : "memory");
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 0) {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&S.tmem_base)),
+                   "r"(kTmemCols)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    fence_proxy_async_smem();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+  }
+  const uint32_t tmem = S.tmem_base;
+  const uint32_t lane_base = uint32_t(warp * 32) << 16;
+  uint32_t phase = 0;
+
+  const int64_t n_tiles = (s.R + kTcRows - 1) / kTcRows;
+  for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+    const int64_t r = tile * kTcRows + tid;
+    const bool live = r < s.R;
+    // ---- layer-1 operand: the TeamLayout row (+ buffer writes)
+    {
+      float x[32];
+      if (live) {
+        fill_row(s, b, r, in_dim, n_act, x, !s.bootstrap);
+      }
+#pragma unroll
+      for (int k = 0; k < 32; ++k)
+        if (!live || k >= in_dim) x[k] = 0.0f;
+      put16(S.x, 32, tid, 0, x);
+      put16(S.x, 32, tid, 16, x + 16);
+    }
+    fence_proxy_async_smem();
+    __syncthreads();
+    if (tid == 0) {
+      tc_fence_after();
+      const uint32_t id = idesc_bf16(128, 128);
+      for (int k = 0; k < 32; k += 16) umma_bf16(tmem + 0, umma_desc(S.x, 32, k), umma_desc(S.w1, 32, k), id, k > 0);
+      umma_commit(&S.bar);
+    }
+    mbar_wait(&S.bar, phase);
+    phase ^= 1;
+    tc_fence_after();
+    // ---- epilogue 1: bias + tanh -> bf16 hidden rows
+    for (int c = 0; c < 128; c += 16) {
+      float v[16];
+      tmem_ld16(tmem + lane_base + uint32_t(c), v);
+#pragma unroll
+      for (int i = 0; i < 16; ++i) v[i] = tanh_fast(v[i] + S.bias[c + i]);
+      if (c < 64) put16(S.ha, 64, tid, c, v);
+      else put16(S.hc, 64, tid, c - 64, v);
+    }
+    tc_fence_before();
+    fence_proxy_async_smem();
+    __syncthreads();
+    if (tid == 0) {
+      tc_fence_after();
+      const uint32_t id = idesc_bf16(128, 64);
+      for (int k = 0; k < 64; k += 16) umma_bf16(tmem + 0, umma_desc(S.ha, 64, k), umma_desc(S.w2a, 64, k), id, k > 0);
+      for (int k = 0; k < 64; k += 16) umma_bf16(tmem + 64, umma_desc(S.hc, 64, k), umma_desc(S.w2c, 64, k), id, k > 0);
+      umma_commit(&S.bar);
+    }
+    mbar_wait(&S.bar, phase);
+    phase ^= 1;
+    tc_fence_after();
+    // ---- epilogue 2
+    for (int c = 0; c < 128; c += 16) {
+      float v[16];
+      tmem_ld16(tmem + lane_base + uint32_t(c), v);
+#pragma unroll
+      for (int i = 0; i < 16; ++i) v[i] = tanh_fast(v[i] + S.bias[128 + c + i]);
+      if (c < 64) put16(S.ha, 64, tid, c, v);
+      else put16(S.hc, 64, tid, c - 64, v);
+    }
+    tc_fence_before();
+    fence_proxy_async_smem();
+    __syncthreads();
+    if (tid == 0) {
+      tc_fence_after();
+      const uint32_t id = idesc_bf16(128, 16);
+      for (int k = 0; k < 64; k += 16) umma_bf16(tmem + 128, umma_desc(S.ha, 64, k), umma_desc(S.w3a, 64, k), id, k > 0);
+      for (int k = 0; k < 64; k += 16) umma_bf16(tmem + 144, umma_desc(S.hc, 64, k), umma_desc(S.w3c, 64, k), id, k > 0);
+      umma_commit(&S.bar);
+    }
+    mbar_wait(&S.bar, phase);
+    phase ^= 1;
+    tc_fence_after();
+    // ---- epilogue 3: heads, sampling, buffer writes
+    float lg[16], vv[16];
+    tmem_ld16(tmem + lane_base + 128u, lg);
+    tmem_ld16(tmem + lane_base + 144u, vv);
+    tc_fence_before();
+    if (live) {
+      const float value = vv[0] + S.bias[256 + 16];
+      if (s.bootstrap) {
+        b.last_value[r] = value;
+      } else {
+        float logits[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) logits[j] = lg[j] + S.bias[256 + j];
+        sample_and_record(s, b, r, logits, n_act, value);
+      }
+    }
+    __syncthreads();  // TMEM columns and operand tiles are reused by the next tile
+  }
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols) : "memory");
+}
+
+// fp32 parameters -> canonical bf16 operand images + bias block.
+__global__ void pack_bf16_kernel(PolicyNet n, uint16_t* img, float* bias) {
+  const int in = n.in_dim, NA = n.n_act;
+  uint16_t* a1 = img;
+  uint16_t* a2 = a1 + 128 * 32;
+  uint16_t* c2 = a2 + 64 * 64;
+  uint16_t* h3 = c2 + 64 * 64;
+  uint16_t* hc3 = h3 + 16 * 64;
+  auto bf = [](float v) {
+    const __nv_bfloat16 h = __float2bfloat16_rn(v);
+    return *reinterpret_cast<const uint16_t*>(&h);
+  };
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < 128 * 32; q += gridDim.x * blockDim.x) {
+    const int row = q / 32, k = q % 32;
+    float v = 0.0f;
+    if (k < in) v = row < 64 ? n.w1[row * in + k] : n.cw1[(row - 64) * in + k];
+    a1[canon_off(row, k, 32) / 2] = bf(v);
+  }
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < 64 * 64; q += gridDim.x * blockDim.x) {
+    const int row = q / 64, k = q % 64;
+    a2[canon_off(row, k, 64) / 2] = bf(n.w2[row * 64 + k]);
+    c2[canon_off(row, k, 64) / 2] = bf(n.cw2[row * 64 + k]);
+  }
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < 16 * 64; q += gridDim.x * blockDim.x) {
+    const int row = q / 64, k = q % 64;
+    h3[canon_off(row, k, 64) / 2] = bf(row < NA ? n.w3[row * 64 + k] : 0.0f);
+    hc3[canon_off(row, k, 64) / 2] = bf(row == 0 ? n.cw3[k] : 0.0f);
+  }
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < 64; q += gridDim.x * blockDim.x) {
+    bias[q] = n.b1[q];
+    bias[64 + q] = n.cb1[q];
+    bias[128 + q] = n.b2[q];
+    bias[192 + q] = n.cb2[q];
+    if (q < 16) {
+      bias[256 + q] = q < NA ? n.b3[q] : 0.0f;
+      bias[272 + q] = q == 0 ? n.cb3[0] : 0.0f;
+    }
+  }
+}
+
+}  // namespace
+
+bool rollout_policy_bf16_supported(int in_dim, int n_act, int width) {
+  return in_dim <= 32 && n_act <= 16 && width == 64;
+}
+
+void rollout_pack_bf16(const PolicyNet& net, uint16_t* images, float* bias, cudaStream_t st) {
+  pack_bf16_kernel<<<16, 256, 0, st>>>(net, images, bias);
+  ++g_launches;
+}
+
+void rollout_policy_bf16(const PolicyNet& net, const PolicyNetBf16& nb, const PolicyStep& s, const RolloutBufs& b,
+                         cudaStream_t st) {
+  static int sms = 0;
+  if (sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const size_t sm = sizeof(TcSmem) + 1024;  // + alignment slack
+  cudaFuncSetAttribute(policy_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+  const int64_t tiles = (s.R + kTcRows - 1) / kTcRows;
+  const int64_t grid = std::min<int64_t>(tiles, int64_t(sms) * 2);  // two CTAs (2 x 256 TMEM columns) per SM
+  policy_tc_kernel<<<unsigned(grid), kTcRows, sm, st>>>(nb, net.in_dim, net.n_act, s, b);
+  ++g_launches;
+}
 
 void rollout_gae(const RolloutBufs& b, int T, int64_t R, float gamma, float lambda, cudaStream_t st) {
   gae_kernel<<<unsigned((R + 255) / 256), 256, 0, st>>>(b, T, R, gamma, lambda);
