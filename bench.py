@@ -34,7 +34,11 @@ WORKLOADS = {
     "overcooked": ("overcooked_cramped_room_v0", {}, 262144, "Overcooked cramped_room, configs[2]"),
     "smax2s3z": ("SMAX_2s3z", {}, 65536, "SMAX 2s3z, configs[3]"),
     "smax27m": ("SMAX_27m_vs_30m", {}, 4096, "SMAX 27m_vs_30m, configs[3]"),
+    # configs[4]: one "step" is one Collector::collect window of IPPO_T env steps
+    "ippo": ("MPE_simple_spread_v3", {}, 1 << 20, "IPPO rollout on MPE simple_spread, 2^20 envs x 128 steps, "
+             "bf16 actor+critic on tcgen05, configs[4]"),
 }
+IPPO_T = 128
 L2_FLUSH_BYTES = 512 << 20  # > 4x the 126 MB L2; its ~80 us also covers the host's enqueue of the next step
 
 
@@ -183,6 +187,126 @@ def cpu_reference_probe(env_id, cfg, n_envs, steps, warmup, threads):
     return sec, kind, cores, v.n_agents
 
 
+def ippo_bytes_per_env_step(env, in_dim, n_act):
+    """Algorithmic bytes of one rollout env-step: the env step,
+    the policy kernel (obs row read + buffer row writes: obs, action, logp,
+    value, legal, active, reset), the record kernel (rewards/finished read,
+    reward/done rows written) and GAE (reward, value, done read; adv, vtarg
+    written), per env."""
+    A = env.num_agents()
+    env_b = algorithmic_bytes(env, 1, 0)
+    policy = A * env.obs_dim * 4 + A * (in_dim * 4 + 4 + 4 + 4 + n_act + 4 + 1)
+    record = A * 8 + 1 + A * (4 + 1)
+    gae = A * (4 + 4 + 1 + 4 + 4)
+    return env_b + policy + record + gae
+
+
+def run_gpu_ippo(args, rank, world, local_rank):
+    """configs[4]: the reference's IPPO collector on the device, one timed
+    step = one collect window (IPPO_T env steps of every env)."""
+    import torch
+    import paper_2311_10090_b200 as m
+    from paper_2311_10090_b200 import _native
+    from paper_2311_10090_b200 import dist as shard
+    from paper_2311_10090_b200.rollout import IppoRollout, orthogonal_init
+
+    env_id, cfg, n_per_gpu, label = WORKLOADS[args.workload]
+    if args.n_envs:
+        n_per_gpu = args.n_envs
+    torch.cuda.set_device(local_rank)
+    env = m.make_env(env_id, cfg)
+    A = env.num_agents()
+    N = n_per_gpu * world
+    T = IPPO_T
+    venv = shard.make_sharded(env, N, rank, world, device=local_rank)
+    ro = IppoRollout(venv, T, precision="bf16")
+    actor, critic = orthogonal_init(0, ro.spec)
+    pin_a = torch.from_numpy(actor).pin_memory().numpy()
+    pin_c = torch.from_numpy(critic).pin_memory().numpy()
+    ro.set_params(pin_a, pin_c)
+    key = m.prng.key_from_seed(0)
+    ro.begin(key)
+    stream = torch.cuda.current_stream()
+    for w in range(args.warmup):
+        ro.collect(seq_base=w * T)
+    torch.cuda.synchronize()
+    venv.episode_stats(clear=True)
+    if world > 1:
+        torch.distributed.barrier()
+    clocks = ClockSampler(local_rank) if rank == 0 else None
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    launches0 = _native.lib().marl_launch_count()
+    for k in range(args.steps):  # the buffer (>> L2) is rewritten every window: no flush needed
+        starts[k].record(stream)
+        ro.collect(seq_base=(args.warmup + k) * T)
+        ends[k].record(stream)
+    torch.cuda.synchronize()
+    launches = _native.lib().marl_launch_count() - launches0
+    clk = clocks.stop() if clocks else None
+    win_ms = [s_.elapsed_time(e_) for s_, e_ in zip(starts, ends)]
+    total_ms = shard.max_over_ranks(float(sum(win_ms)), device="cuda")
+    stats = shard.all_reduce_episode_stats(venv.episode_stats_raw(), device="cuda")
+    env_steps = N * T * args.steps
+    value = env_steps * A / (total_ms * 1e-3)
+    mean_win_s = float(np.mean(win_ms)) * 1e-3
+    bpe = ippo_bytes_per_env_step(env, ro.spec.in_dim, ro.spec.n_actions)
+    achieved = n_per_gpu * T * bpe / mean_win_s / 1e9
+    peak, peak_src = measured_peak()
+    flop_row = 2 * (128 * 32 + 2 * 64 * 64 + 2 * 16 * 64)  # MMA FLOPs per row as issued (padded operands)
+    tflops = n_per_gpu * A * (T + 1) * flop_row / mean_win_s / 1e12
+
+    # end to end through the public API: parameters H2D from pinned memory,
+    # one collect window, the episode statistics read back (what an on-GPU
+    # trainer consumes from the host), every window
+    e2e_steps = max(2, min(args.steps, 5))
+    t0 = time.perf_counter()
+    for k in range(e2e_steps):
+        ro.set_params(pin_a, pin_c)
+        ro.collect(seq_base=(args.warmup + args.steps + k) * T)
+        venv.episode_stats_raw()
+    sec = shard.max_over_ranks(time.perf_counter() - t0, device="cuda")
+    if rank != 0:
+        return
+    cpu = None
+    if world == 1 and not args.no_cpu:
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        import oracle as O
+        if O.ref_available():
+            n_cpu, t_cpu = 256, 32
+            ka, kc = O.ref_ppo_init(env_id, cfg, O.fold_in(O.key_from_seed(0), 10))
+            t0 = time.perf_counter()
+            O.ref_collect(env_id, cfg, n_cpu, t_cpu, O.key_from_seed(0), ka, kc)
+            csec = time.perf_counter() - t0
+            cpu = {"value": n_cpu * t_cpu * A / csec, "unit": "agent-steps/s", "cores": 1, "kind": "reference",
+                   "sample": f"reference Collector pieces (VectorEnv + ff_forward + sample_masked + compute_gae), "
+                             f"{n_cpu} envs x {t_cpu} steps, 1 collect window ({csec:.1f} s, ThreadPool for the env)"}
+    line = {
+        "metric": "agent-steps/sec (env-steps/sec x agents)", "value": value, "unit": "agent-steps/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16 policy / f64 env",
+        "data": "synthetic (reset from key_from_seed(0); orthogonal-init policy, sampled actions)",
+        "config": {"workload": label, "env_id": env_id, "n_envs_per_gpu": n_per_gpu, "global_envs": N, "agents": A,
+                   "rollout_steps_per_window": T, "step": "one collect window",
+                   "parallelism": f"env-sharded x{world}, no collective in the window",
+                   "l2": "no flush: each window writes a >20 GB rollout buffer (>> 126 MB L2)"},
+        "env_steps_per_sec": env_steps / (total_ms * 1e-3),
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": ncu_traffic(args.workload), "peak_source": peak_src,
+                     "bytes_per_launch": n_per_gpu * T * bpe, "mean_launch_us": mean_win_s * 1e6,
+                     "kernel": "whole collect window (env step + tcgen05 policy + record + GAE kernels)",
+                     "bytes_per_env_step": bpe, "tensor_tflops": tflops},
+        "cpu_baseline": cpu,
+        "e2e": {"value": N * A * T * e2e_steps / sec, "unit": "agent-steps/s",
+                "h2d_bytes_per_step": int(pin_a.nbytes + pin_c.nbytes), "d2h_bytes_per_step": 24,
+                "steps": e2e_steps, "path": "IppoRollout.set_params + collect + episode stats (C-ABI marl_rollout_*)"},
+        "gpu_launches": int(launches),
+        "clocks": clk,
+        "episode_stats": shard.summarize(stats),
+    }
+    print(json.dumps(line))
+
+
 def cpu_sample_size(env_id, cfg):
     """(envs, steps) of a bounded CPU sample of the workload: ~10-30 s for the
     cpu_baseline leg; the envs cap also bounds one reference-arm step (~1 s)."""
@@ -196,6 +320,29 @@ def run_reference_arm(args, rank, world):
         return
     threads = os.cpu_count() or 1
     n_envs = n_per_gpu * world
+    if args.workload == "ippo":  # one step = one collect window of a bounded env sample
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        import oracle as O
+        n_cpu, t_cpu = 256, IPPO_T
+        ka, kc = O.ref_ppo_init(env_id, cfg, O.fold_in(O.key_from_seed(0), 10))
+        O.ref_collect(env_id, cfg, n_cpu, 4, O.key_from_seed(0), ka, kc)  # warm
+        t0 = time.perf_counter()
+        O.ref_collect(env_id, cfg, n_cpu, t_cpu, O.key_from_seed(0), ka, kc, n_windows=max(1, args.steps))
+        sec = time.perf_counter() - t0
+        A = 3
+        val = n_cpu * A * t_cpu * max(1, args.steps) / sec
+        line = {"impl": "reference", "metric": "agent-steps/sec (env-steps/sec x agents)", "value": val,
+                "unit": "agent-steps/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": 1e3 * sec / max(1, args.steps), "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f32 policy / f64 env", "data": "synthetic",
+                "config": {"workload": label, "env_id": env_id, "n_envs": n_cpu, "n_envs_requested": n_envs,
+                           "rollout_steps_per_window": t_cpu},
+                "cpu_baseline": {"value": val, "unit": "agent-steps/s", "cores": 1, "kind": "reference",
+                                 "sample": f"reference Collector pieces, {n_cpu} envs x {t_cpu} steps x "
+                                           f"{max(1, args.steps)} windows"},
+                "e2e": {"value": val, "unit": "agent-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line))
+        return
     # each step is one batch step of the whole workload on the host cores
     # unless that would not finish within a few minutes; then a bounded sample.
     n_cpu, _ = cpu_sample_size(env_id, cfg)
@@ -355,7 +502,10 @@ def main():
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl")
     try:
-        run_gpu_arm(args, rank, world, local_rank)
+        if args.workload == "ippo":
+            run_gpu_ippo(args, rank, world, local_rank)
+        else:
+            run_gpu_arm(args, rank, world, local_rank)
     finally:
         if world > 1:
             import torch.distributed as dist

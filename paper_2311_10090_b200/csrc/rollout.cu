@@ -28,6 +28,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "engine.h"
@@ -63,14 +65,11 @@ __host__ __device__ inline int net_floats(int in, int width, int n_act) {
 
 }  // namespace
 
-// The per-row tail shared by both policy paths: masked_log_probs +
-// sample_masked (actor_critic.hpp:218-262) in double over the row's float
-// logits, then the buffer writes.  Returns the sampled action.
-__device__ int sample_and_record(const PolicyStep& s, const RolloutBufs& b, int64_t r, const float* logits,
-                                 int n_act, float value) {
-  const int64_t R = s.R;
-  const size_t slot = size_t(s.t) * size_t(R) + size_t(r);
-  const uint8_t* legal = b.legal + slot * n_act;
+// masked_log_probs + sample_masked (actor_critic.hpp:218-262) in double over
+// one row's float logits with the row's key fold_in(act_key, (seq_base+t)*R
+// + r) (ppo.cpp:249-259).  Shared by both policy paths.
+__device__ void sample_row(const PolicyStep& s, int64_t r, const float* logits, const uint8_t* legal, int n_act,
+                           int* action, float* logp) {
   double mx = -INFINITY;
   for (int i = 0; i < n_act; ++i)
     if (legal[i]) mx = fmax(mx, double(logits[i]));
@@ -91,10 +90,49 @@ __device__ int sample_and_record(const PolicyStep& s, const RolloutBufs& b, int6
     cum += exp(lp);
     if (u < cum) break;
   }
+  *action = pick;
+  *logp = float(lp_pick);
+}
+
+// The bf16 path's sampler: the same masked softmax + CDF walk with the same
+// per-row key and uniform draw, in float (the bf16 logits already differ
+// from the reference's by far more than float rounding).
+__device__ void sample_row_f32(const PolicyStep& s, int64_t r, const float* logits, const uint8_t* legal, int n_act,
+                               int* action, float* logp) {
+  float mx = -INFINITY;
+  for (int i = 0; i < n_act; ++i)
+    if (legal[i]) mx = fmaxf(mx, logits[i]);
+  float p[16], denom = 0.0f;
+  for (int i = 0; i < n_act; ++i) {
+    p[i] = legal[i] ? expf(logits[i] - mx) : 0.0f;
+    denom += p[i];
+  }
+  const float log_denom = logf(denom), inv = 1.0f / denom;
+  const Key ak{s.act_key[0], s.act_key[1], s.act_key[2], s.act_key[3]};
+  const Key kk = fold_in(ak, uint64_t(s.step_index) * uint64_t(s.R_global) + uint64_t(s.row0 + r));
+  const double u = uniform_at(kk, 0, 0.0, 1.0);  // prng::uniform1
+  double cum = 0.0;
+  int pick = -1;
+  for (int i = 0; i < n_act; ++i) {
+    if (!legal[i]) continue;
+    pick = i;
+    cum += double(p[i] * inv);
+    if (u < cum) break;
+  }
+  *action = pick;
+  *logp = logits[pick] - mx - log_denom;
+}
+
+// The fp32 path's per-row tail: sample, then the buffer writes.
+__device__ void sample_and_record(const PolicyStep& s, const RolloutBufs& b, int64_t r, const float* logits,
+                                  int n_act, float value) {
+  const size_t slot = size_t(s.t) * size_t(s.R) + size_t(r);
+  int pick;
+  float lp;
+  sample_row(s, r, logits, b.legal + slot * n_act, n_act, &pick, &lp);
   b.actions[slot] = pick;
-  b.logp[slot] = float(lp_pick);
+  b.logp[slot] = lp;
   b.value[slot] = value;
-  return pick;
 }
 
 // write_input / write_legal / agent_active of row r for step t (team.cpp:27-42,
@@ -237,7 +275,8 @@ void rollout_record(const RolloutBufs& b, int t, int64_t R, int A, const double*
 namespace {
 
 constexpr int kTcRows = 128;
-constexpr uint32_t kTmemCols = 256;
+constexpr uint32_t kTmemCols = 128;  // L1 uses 128 columns; L2 and L3 reuse them
+constexpr int kSplit = 2;            // threads per row (warps w, w+4, ... share a TMEM lane quarter)
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -302,6 +341,22 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// 32 consecutive fp32 columns of this thread's TMEM lane (two x16 loads, one wait).
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
   return *reinterpret_cast<const uint32_t*>(&h);
@@ -311,6 +366,16 @@ __device__ __forceinline__ float tanh_fast(float x) {  // MUFU.TANH: ~2^-11 rela
   float y;
   asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
+}
+
+// 8 fp32 values at K offset k0 (a multiple of 8) -> one 16-byte chunk.
+__device__ __forceinline__ void put8(uint8_t* tile, int K, int row, int k0, const float* v) {
+  uint4 q;
+  q.x = pack_bf16(v[0], v[1]);
+  q.y = pack_bf16(v[2], v[3]);
+  q.z = pack_bf16(v[4], v[5]);
+  q.w = pack_bf16(v[6], v[7]);
+  *reinterpret_cast<uint4*>(tile + canon_off(row, k0, K)) = q;
 }
 
 // Row `row` of an activation operand: 16 fp32 values at K offset k0 -> bf16
@@ -327,146 +392,310 @@ __device__ __forceinline__ void put16(uint8_t* tile, int K, int row, int k0, con
   }
 }
 
-struct TcSmem {  // all tiles 1024-byte aligned
-  uint8_t w1[128 * 32 * 2];  // [W1a ; W1c]  (N=128, K=32)
-  uint8_t w2a[64 * 64 * 2];
-  uint8_t w2c[64 * 64 * 2];
-  uint8_t w3a[16 * 64 * 2];
-  uint8_t w3c[16 * 64 * 2];
-  uint8_t x[kTcRows * 32 * 2];    // layer-1 A operand
-  uint8_t ha[kTcRows * 64 * 2];   // actor hidden (A of L2, then of L3)
-  uint8_t hc[kTcRows * 64 * 2];   // critic hidden
-  float bias[4 * 64 + 2 * 16];
-  uint64_t bar;
-  uint32_t tmem_base;
+// Shared-memory carve-up of the tcgen05 policy kernel, sized from the actual
+// row widths (offsets in bytes from a 1024-aligned base).
+struct TcLayout {
+  uint32_t w1, w2a, w2c, w3a, w3c, x, ha, hc, obs_in[2], obs_out, legal, resets, active, act, logp, value, bias, bar,
+      bar_in[2], tmem_slot, total;
 };
 
-__global__ void __launch_bounds__(kTcRows) policy_tc_kernel(PolicyNetBf16 nb, int in_dim, int n_act, PolicyStep s,
+__host__ __device__ inline uint32_t up(uint32_t v, uint32_t a) { return (v + a - 1) / a * a; }
+
+__host__ __device__ inline TcLayout tc_layout(int D, int in_dim, int n_act) {
+  TcLayout L{};
+  uint32_t o = 0;
+  auto take = [&o](uint32_t bytes, uint32_t align) {
+    o = up(o, align);
+    const uint32_t at = o;
+    o += bytes;
+    return at;
+  };
+  L.w1 = take(128 * 32 * 2, 128);
+  L.w2a = take(64 * 64 * 2, 128);
+  L.w2c = take(64 * 64 * 2, 128);
+  L.w3a = take(16 * 64 * 2, 128);
+  L.w3c = take(16 * 64 * 2, 128);
+  L.x = take(kTcRows * 32 * 2, 128);
+  L.ha = take(kTcRows * 64 * 2, 128);
+  L.hc = take(kTcRows * 64 * 2, 128);
+  L.obs_in[0] = take(uint32_t(kTcRows * D * 4), 16);
+  L.obs_in[1] = take(uint32_t(kTcRows * D * 4), 16);
+  L.obs_out = take(uint32_t(kTcRows * in_dim * 4), 16);
+  L.legal = take(uint32_t(kTcRows * n_act), 16);
+  L.resets = take(kTcRows, 16);
+  L.active = take(kTcRows * 4, 16);
+  L.act = take(kTcRows * 4, 16);
+  L.logp = take(kTcRows * 4, 16);
+  L.value = take(kTcRows * 4, 16);
+  L.bias = take((4 * 64 + 2 * 16) * 4, 16);
+  L.bar = take(8, 8);
+  L.bar_in[0] = take(8, 8);
+  L.bar_in[1] = take(8, 8);
+  L.tmem_slot = take(4, 4);
+  L.total = up(o, 128);
+  return L;
+}
+
+// Store a staged tile: one TMA bulk store when it qualifies, else a
+// cooperative copy.  Every thread calls it after fence + barrier.
+__device__ __forceinline__ void tile_put(void* g, const void* sm, size_t bytes) {
+  if (bulk_ok(g, sm, bytes)) {
+    if (threadIdx.x == 0) bulk_store_s2g(g, sm, uint32_t(bytes));
+  } else {
+    const uint8_t* src = static_cast<const uint8_t*>(sm);
+    uint8_t* dst = static_cast<uint8_t*>(g);
+    for (size_t q = threadIdx.x; q < bytes; q += blockDim.x) dst[q] = src[q];
+  }
+}
+
+// TMA bulk load global -> shared completing on an mbarrier (expect-tx).
+__device__ __forceinline__ void bulk_load_g2s(void* sdst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(sdst)),
+               "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+// Issue (thread 0) or perform (everyone, synchronously) the load of a tile's
+// env observation rows; returns whether a bulk load is in flight.
+__device__ __forceinline__ bool tile_obs_load(const PolicyStep& s, int64_t tile, float* dst, uint64_t* bar) {
+  const int64_t r0 = tile * kTcRows;
+  const int rows = int(min64(kTcRows, s.R - r0));
+  const float* g = s.env_obs + size_t(r0) * s.D;
+  const size_t bytes = size_t(rows) * s.D * 4;
+  if (((reinterpret_cast<uintptr_t>(g) | bytes) & 15) == 0) {
+    if (threadIdx.x == 0) bulk_load_g2s(dst, g, uint32_t(bytes), bar);
+    return true;
+  }
+  for (size_t q = threadIdx.x; q < bytes / 4; q += blockDim.x) dst[q] = __ldg(g + q);
+  return false;
+}
+
+__global__ void __launch_bounds__(kSplit * kTcRows) policy_tc_kernel(PolicyNetBf16 nb, int in_dim, int n_act, PolicyStep s,
                                                             RolloutBufs b) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  TcSmem& S = *reinterpret_cast<TcSmem*>(smem_raw);
-  const int tid = threadIdx.x, warp = tid >> 5;
+  const TcLayout L = tc_layout(s.D, in_dim, n_act);
+  uint8_t* base = smem_raw;
+  uint8_t *w1 = base + L.w1, *w2a = base + L.w2a, *w2c = base + L.w2c, *w3a = base + L.w3a, *w3c = base + L.w3c;
+  uint8_t *sx = base + L.x, *ha = base + L.ha, *hc = base + L.hc;
+  float* obs_in[2] = {reinterpret_cast<float*>(base + L.obs_in[0]), reinterpret_cast<float*>(base + L.obs_in[1])};
+  float* obs_out = reinterpret_cast<float*>(base + L.obs_out);
+  uint8_t* s_legal = base + L.legal;
+  uint8_t* s_resets = base + L.resets;
+  float* s_active = reinterpret_cast<float*>(base + L.active);
+  int32_t* s_act = reinterpret_cast<int32_t*>(base + L.act);
+  float* s_logp = reinterpret_cast<float*>(base + L.logp);
+  float* s_value = reinterpret_cast<float*>(base + L.value);
+  float* s_bias = reinterpret_cast<float*>(base + L.bias);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(base + L.bar);
+  uint64_t* bar_in[2] = {reinterpret_cast<uint64_t*>(base + L.bar_in[0]), reinterpret_cast<uint64_t*>(base + L.bar_in[1])};
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(base + L.tmem_slot);
+  // kSplit threads per row: part q (warps 4q..4q+3) owns accumulator columns
+  // [128q/kSplit, 128(q+1)/kSplit) of every layer (actor 0-63, critic
+  // 64-127) and K columns [32q/kSplit, ...) of the input row; part 0 samples,
+  // part 1 writes the value.
+  // Warps w, w+4, ... read the same TMEM lane quarter.
+  const int tid = threadIdx.x & (kTcRows - 1), part = threadIdx.x >> 7, warp = threadIdx.x >> 5;
+  const int64_t n_tiles = (s.R + kTcRows - 1) / kTcRows;
 
-  // one-time: weights (already in canonical layout) + biases, barrier, TMEM
+  // one-time: barriers, TMEM, weights (already in canonical layout) + biases,
+  // and the first tile's observation rows in flight
+  if (threadIdx.x == 0) {
+    for (uint64_t* m : {bar, bar_in[0], bar_in[1]})
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(m)) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(kTmemCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
   {
     const uint4* src[5] = {reinterpret_cast<const uint4*>(nb.a1), reinterpret_cast<const uint4*>(nb.a2),
                            reinterpret_cast<const uint4*>(nb.c2), reinterpret_cast<const uint4*>(nb.h3),
                            reinterpret_cast<const uint4*>(nb.hc3)};
-    uint4* dst[5] = {reinterpret_cast<uint4*>(S.w1), reinterpret_cast<uint4*>(S.w2a),
-                     reinterpret_cast<uint4*>(S.w2c), reinterpret_cast<uint4*>(S.w3a),
-                     reinterpret_cast<uint4*>(S.w3c)};
+    uint4* dst[5] = {reinterpret_cast<uint4*>(w1), reinterpret_cast<uint4*>(w2a), reinterpret_cast<uint4*>(w2c),
+                     reinterpret_cast<uint4*>(w3a), reinterpret_cast<uint4*>(w3c)};
     const int n16[5] = {128 * 32 * 2 / 16, 64 * 64 * 2 / 16, 64 * 64 * 2 / 16, 16 * 64 * 2 / 16, 16 * 64 * 2 / 16};
-    for (int m = 0; m < 5; ++m)
-      for (int q = tid; q < n16[m]; q += blockDim.x) dst[m][q] = __ldg(src[m] + q);
-    for (int q = tid; q < 4 * 64 + 2 * 16; q += blockDim.x) S.bias[q] = __ldg(nb.bias + q);
-    if (tid == 0) {
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&S.bar)) : "memory");
-      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+#pragma unroll
+    for (int m = 0; m < 5; ++m) {
+      uint4 v[8];
+      for (int q0 = 0; q0 < n16[m]; q0 += 8 * int(blockDim.x)) {  // 8 loads in flight per thread
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int q = q0 + j * int(blockDim.x) + int(threadIdx.x);
+          if (q < n16[m]) v[j] = __ldg(src[m] + q);
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int q = q0 + j * int(blockDim.x) + int(threadIdx.x);
+          if (q < n16[m]) dst[m][q] = v[j];
+        }
+      }
     }
-    if (warp == 0) {
-      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&S.tmem_base)),
-                   "r"(kTmemCols)
-                   : "memory");
-      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
-    }
-    fence_proxy_async_smem();
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
+    for (int q = threadIdx.x; q < 4 * 64 + 2 * 16; q += blockDim.x) s_bias[q] = __ldg(nb.bias + q);
   }
-  const uint32_t tmem = S.tmem_base;
-  const uint32_t lane_base = uint32_t(warp * 32) << 16;
-  uint32_t phase = 0;
+  fence_proxy_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t lane_base = uint32_t((warp & 3) * 32) << 16;
+  const int D = s.D;
+  const bool act_mode = !s.bootstrap;
+  uint32_t phase = 0, in_phase[2] = {0, 0};
+  bool in_flight[2] = {false, false};
+  int cur = 0;
+  if (int64_t(blockIdx.x) < n_tiles) in_flight[0] = tile_obs_load(s, blockIdx.x, obs_in[0], bar_in[0]);
 
-  const int64_t n_tiles = (s.R + kTcRows - 1) / kTcRows;
   for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-    const int64_t r = tile * kTcRows + tid;
-    const bool live = r < s.R;
-    // ---- layer-1 operand: the TeamLayout row (+ buffer writes)
+    const int64_t r0 = tile * kTcRows, r = r0 + tid;
+    const int rows = int(min64(kTcRows, s.R - r0));
+    const bool live = tid < rows;
+    const size_t slot0 = size_t(s.t) * size_t(s.R) + size_t(r0);
+    // this tile's observation rows have landed; the previous tile's bulk
+    // stores have read the staging tiles
+    if (in_flight[cur]) {
+      mbar_wait(bar_in[cur], in_phase[cur]);
+      in_phase[cur] ^= 1;
+    }
+    if (threadIdx.x == 0) bulk_wait_read<0>();
+    __syncthreads();
+    // prefetch the next tile's rows into the other buffer (its last reader,
+    // the previous tile's row build, finished before the barrier above)
+    const int64_t next = tile + gridDim.x;
+    in_flight[cur ^ 1] = next < n_tiles ? tile_obs_load(s, next, obs_in[cur ^ 1], bar_in[cur ^ 1]) : false;
+    // ---- write_input / write_legal / agent_active (team.cpp:27-42): part q
+    // builds K columns [32q/kSplit, 32(q+1)/kSplit) of the row
     {
-      float x[32];
-      if (live) {
-        fill_row(s, b, r, in_dim, n_act, x, !s.bootstrap);
+      const float* oin = obs_in[cur];
+      const int64_t e = r / s.A;
+      const int a = int(r - e * s.A);
+      const int k0 = (32 / kSplit) * part;
+      float x[32 / kSplit];
+#pragma unroll
+      for (int j = 0; j < 32 / kSplit; ++j) {
+        const int k = k0 + j;
+        x[j] = (live && k < D) ? oin[tid * D + k] : 0.0f;
+        if (live && s.A > 1 && k == D + a) x[j] = 1.0f;
+      }
+      if (live && act_mode) {
+        float* o = obs_out + tid * in_dim;
+#pragma unroll
+        for (int j = 0; j < 32 / kSplit; ++j)
+          if (k0 + j < in_dim) o[k0 + j] = x[j];
+        if (part == 0) {
+          s_resets[tid] = s.prev_finished ? s.prev_finished[e] : uint8_t(1);
+          uint8_t* lg = s_legal + tid * n_act;
+          if (s.legal_ready) {
+            const uint8_t* gl = b.legal + (slot0 + size_t(tid)) * n_act;
+            for (int q = 0; q < n_act; ++q) lg[q] = gl[q];
+          } else {
+            const int na = s.agent_actions[a];
+            for (int q = 0; q < n_act; ++q) lg[q] = q < na ? 1 : 0;
+          }
+          s_active[tid] = (s.family == 1) ? (lg[0] ? 1.0f : 0.0f) : 1.0f;
+        }
       }
 #pragma unroll
-      for (int k = 0; k < 32; ++k)
-        if (!live || k >= in_dim) x[k] = 0.0f;
-      put16(S.x, 32, tid, 0, x);
-      put16(S.x, 32, tid, 16, x + 16);
+      for (int j = 0; j < 32 / kSplit; j += 8) put8(sx, 32, tid, k0 + j, x + j);
     }
     fence_proxy_async_smem();
     __syncthreads();
-    if (tid == 0) {
+    if (act_mode) {  // the input-side buffer rows leave while the MMAs run
+      tile_put(b.obs + slot0 * in_dim, obs_out, size_t(rows) * in_dim * 4);
+      if (!s.legal_ready) tile_put(b.legal + slot0 * n_act, s_legal, size_t(rows) * n_act);
+      if (threadIdx.x == 0) bulk_commit();
+      if (live && part == 0) {  // one element per thread: already coalesced
+        b.resets[slot0 + tid] = s_resets[tid];
+        b.active[slot0 + tid] = s_active[tid];
+      }
+    }
+    if (threadIdx.x == 0) {
       tc_fence_after();
       const uint32_t id = idesc_bf16(128, 128);
-      for (int k = 0; k < 32; k += 16) umma_bf16(tmem + 0, umma_desc(S.x, 32, k), umma_desc(S.w1, 32, k), id, k > 0);
-      umma_commit(&S.bar);
+      for (int k = 0; k < 32; k += 16) umma_bf16(tmem + 0, umma_desc(sx, 32, k), umma_desc(w1, 32, k), id, k > 0);
+      umma_commit(bar);
     }
-    mbar_wait(&S.bar, phase);
+    mbar_wait(bar, phase);
     phase ^= 1;
     tc_fence_after();
     // ---- epilogue 1: bias + tanh -> bf16 hidden rows
-    for (int c = 0; c < 128; c += 16) {
-      float v[16];
-      tmem_ld16(tmem + lane_base + uint32_t(c), v);
+#pragma unroll 1
+    for (int c = (128 / kSplit) * part; c < (128 / kSplit) * (part + 1); c += 32) {  // this part's columns
+      float v[32];
+      tmem_ld32(tmem + lane_base + uint32_t(c), v);
 #pragma unroll
-      for (int i = 0; i < 16; ++i) v[i] = tanh_fast(v[i] + S.bias[c + i]);
-      if (c < 64) put16(S.ha, 64, tid, c, v);
-      else put16(S.hc, 64, tid, c - 64, v);
+      for (int i = 0; i < 32; ++i) v[i] = tanh_fast(v[i] + s_bias[c + i]);
+      uint8_t* dsth = c < 64 ? ha : hc;
+      put16(dsth, 64, tid, c & 63, v);
+      put16(dsth, 64, tid, (c & 63) + 16, v + 16);
     }
     tc_fence_before();
     fence_proxy_async_smem();
     __syncthreads();
-    if (tid == 0) {
+    if (threadIdx.x == 0) {
       tc_fence_after();
       const uint32_t id = idesc_bf16(128, 64);
-      for (int k = 0; k < 64; k += 16) umma_bf16(tmem + 0, umma_desc(S.ha, 64, k), umma_desc(S.w2a, 64, k), id, k > 0);
-      for (int k = 0; k < 64; k += 16) umma_bf16(tmem + 64, umma_desc(S.hc, 64, k), umma_desc(S.w2c, 64, k), id, k > 0);
-      umma_commit(&S.bar);
+      for (int k = 0; k < 64; k += 16) umma_bf16(tmem + 0, umma_desc(ha, 64, k), umma_desc(w2a, 64, k), id, k > 0);
+      for (int k = 0; k < 64; k += 16) umma_bf16(tmem + 64, umma_desc(hc, 64, k), umma_desc(w2c, 64, k), id, k > 0);
+      umma_commit(bar);
     }
-    mbar_wait(&S.bar, phase);
+    mbar_wait(bar, phase);
     phase ^= 1;
     tc_fence_after();
     // ---- epilogue 2
-    for (int c = 0; c < 128; c += 16) {
-      float v[16];
-      tmem_ld16(tmem + lane_base + uint32_t(c), v);
+#pragma unroll 1
+    for (int c = (128 / kSplit) * part; c < (128 / kSplit) * (part + 1); c += 32) {  // this part's columns
+      float v[32];
+      tmem_ld32(tmem + lane_base + uint32_t(c), v);
 #pragma unroll
-      for (int i = 0; i < 16; ++i) v[i] = tanh_fast(v[i] + S.bias[128 + c + i]);
-      if (c < 64) put16(S.ha, 64, tid, c, v);
-      else put16(S.hc, 64, tid, c - 64, v);
+      for (int i = 0; i < 32; ++i) v[i] = tanh_fast(v[i] + s_bias[128 + c + i]);
+      uint8_t* dsth = c < 64 ? ha : hc;
+      put16(dsth, 64, tid, c & 63, v);
+      put16(dsth, 64, tid, (c & 63) + 16, v + 16);
     }
     tc_fence_before();
     fence_proxy_async_smem();
     __syncthreads();
-    if (tid == 0) {
+    if (threadIdx.x == 0) {
       tc_fence_after();
       const uint32_t id = idesc_bf16(128, 16);
-      for (int k = 0; k < 64; k += 16) umma_bf16(tmem + 128, umma_desc(S.ha, 64, k), umma_desc(S.w3a, 64, k), id, k > 0);
-      for (int k = 0; k < 64; k += 16) umma_bf16(tmem + 144, umma_desc(S.hc, 64, k), umma_desc(S.w3c, 64, k), id, k > 0);
-      umma_commit(&S.bar);
+      for (int k = 0; k < 64; k += 16) umma_bf16(tmem + 0, umma_desc(ha, 64, k), umma_desc(w3a, 64, k), id, k > 0);
+      for (int k = 0; k < 64; k += 16) umma_bf16(tmem + 16, umma_desc(hc, 64, k), umma_desc(w3c, 64, k), id, k > 0);
+      umma_commit(bar);
     }
-    mbar_wait(&S.bar, phase);
+    mbar_wait(bar, phase);
     phase ^= 1;
     tc_fence_after();
-    // ---- epilogue 3: heads, sampling, buffer writes
-    float lg[16], vv[16];
-    tmem_ld16(tmem + lane_base + 128u, lg);
-    tmem_ld16(tmem + lane_base + 144u, vv);
-    tc_fence_before();
-    if (live) {
-      const float value = vv[0] + S.bias[256 + 16];
-      if (s.bootstrap) {
-        b.last_value[r] = value;
-      } else {
+    // ---- epilogue 3: part 0 samples from the actor head, part 1 writes the value
+    if (part < 2) {
+      float hv[16];
+      tmem_ld16(tmem + lane_base + uint32_t(16 * part), hv);  // logits in 0..15 / value in 16
+      tc_fence_before();
+      if (part == 1) {
+        const float value = hv[0] + s_bias[256 + 16];
+        if (live) {
+          if (act_mode) b.value[slot0 + tid] = value;
+          else b.last_value[r] = value;
+        }
+      } else if (act_mode && live) {
         float logits[16];
 #pragma unroll
-        for (int j = 0; j < 16; ++j) logits[j] = lg[j] + S.bias[256 + j];
-        sample_and_record(s, b, r, logits, n_act, value);
+        for (int j = 0; j < 16; ++j) logits[j] = hv[j] + s_bias[256 + j];
+        int pick;
+        float lp;
+        sample_row_f32(s, r, logits, s_legal + tid * n_act, n_act, &pick, &lp);
+        b.actions[slot0 + tid] = pick;  // one element per thread: coalesced
+        b.logp[slot0 + tid] = lp;
       }
     }
+    cur ^= 1;
     __syncthreads();  // TMEM columns and operand tiles are reused by the next tile
   }
+  if (threadIdx.x == 0) bulk_wait<0>();
   __syncthreads();
   if (warp == 0)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols) : "memory");
@@ -531,11 +760,26 @@ void rollout_policy_bf16(const PolicyNet& net, const PolicyNetBf16& nb, const Po
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
-  const size_t sm = sizeof(TcSmem) + 1024;  // + alignment slack
+  const size_t sm = tc_layout(s.D, net.in_dim, net.n_act).total;
   cudaFuncSetAttribute(policy_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+  int per_sm = 1;
+  cudaFuncSetAttribute(policy_tc_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  static int smem_sm = 0;
+  if (smem_sm == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+  }
+  // the occupancy API under-reports here (1); count shared memory (1 KB
+  // reserved per CTA), threads and TMEM columns directly
+  per_sm = int(size_t(smem_sm) / (sm + 1024));
+  per_sm = std::max(1, std::min({per_sm, int(512 / kTmemCols), 2048 / (kSplit * kTcRows)}));
+  if (const char* f = std::getenv("MARL_TC_CTAS_PER_SM")) per_sm = std::max(1, std::min(per_sm, std::atoi(f)));
+  if (const char* f = std::getenv("MARL_TC_FORCE_PER_SM")) per_sm = std::atoi(f);
+  if (std::getenv("MARL_TC_DEBUG")) std::fprintf(stderr, "policy_tc: smem %zu per_sm %d\n", sm, per_sm);
   const int64_t tiles = (s.R + kTcRows - 1) / kTcRows;
-  const int64_t grid = std::min<int64_t>(tiles, int64_t(sms) * 2);  // two CTAs (2 x 256 TMEM columns) per SM
-  policy_tc_kernel<<<unsigned(grid), kTcRows, sm, st>>>(nb, net.in_dim, net.n_act, s, b);
+  const int64_t grid = std::min<int64_t>(tiles, int64_t(sms) * per_sm);
+  policy_tc_kernel<<<unsigned(grid), kSplit * kTcRows, sm, st>>>(nb, net.in_dim, net.n_act, s, b);
   ++g_launches;
 }
 
