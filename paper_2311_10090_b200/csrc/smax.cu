@@ -699,7 +699,7 @@ __global__ void __launch_bounds__(kThreads) smax_reset_kernel(const Params* __re
 }
 
 template <int G, int UPL, bool RANDOM>
-__global__ void __launch_bounds__(kThreads, 3) smax_step_kernel(const Params* __restrict__ gP, SmaxState st,
+__global__ void __launch_bounds__(kThreads, (G <= 8 ? 4 : 3)) smax_step_kernel(const Params* __restrict__ gP, SmaxState st,
                                                              LaunchCommon lc, Key step_key, Plan plan) {
   constexpr int EPB = kThreads / G, EPW = 32 / G, CAP = G * UPL;
   extern __shared__ __align__(16) uint8_t smem[];
