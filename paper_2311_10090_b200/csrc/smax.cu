@@ -934,8 +934,8 @@ int shape_id(const SmaxConfig& c) {
   const int n = c.na + c.ne;
   if (const char* f = std::getenv("MARL_SMAX_SHAPE")) {  // tuning override: 0 (8x1) 1 (16x1) 2 (32x1) 3 (32x2) 4 (4x2)
     const int v = std::atoi(f);
-    const int lanes[5] = {8, 16, 32, 32, 4}, upl[5] = {1, 1, 1, 2, 2};
-    if (v >= 0 && v < 5 && lanes[v] * upl[v] >= n) return v;
+    const int lanes[6] = {8, 16, 32, 32, 4, 2}, upl[6] = {1, 1, 1, 2, 2, 4};
+    if (v >= 0 && v < 6 && lanes[v] * upl[v] >= n) return v;
   }
   return n <= 8 ? 0 : n <= 16 ? 1 : n <= 32 ? 2 : 3;
 }
@@ -975,6 +975,7 @@ void launch_step_g(const SmaxConfig& c, const Params* dP, const SmaxState& s, co
   switch (shape_id(c)) {                    \
     case 0: FN<8, 1>(__VA_ARGS__); break;   \
     case 4: FN<4, 2>(__VA_ARGS__); break;   \
+    case 5: FN<2, 4>(__VA_ARGS__); break;   \
     case 1: FN<16, 1>(__VA_ARGS__); break;  \
     case 2: FN<32, 1>(__VA_ARGS__); break;  \
     default: FN<32, 2>(__VA_ARGS__); break; \

@@ -1,0 +1,24 @@
+#!/bin/bash
+# Round evidence on one B200: gpu tests, bench lines for every workload, launch lists and one
+# `ncu --set full` capture per step kernel (SMAX captured in steady state, after 30 launches).
+TAG=${1:-r01}
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu_${TAG}.log 2>&1; tail -2 gpurun_out/pytest_gpu_${TAG}.log
+: > gpurun_out/bench_${TAG}.jsonl
+for w in smax3m mpe mpe_large overcooked smax2s3z smax27m ippo; do
+  timeout 600 python bench.py --workload $w --steps 30 --warmup 5 2>/dev/null | grep '^{' >> gpurun_out/bench_${TAG}.jsonl
+done
+timeout 300 python bench.py --impl reference --workload smax3m --steps 3 --warmup 1 2>/dev/null | grep '^{' >> gpurun_out/bench_${TAG}.jsonl
+wc -l gpurun_out/bench_${TAG}.jsonl
+NCU=/usr/local/cuda/bin/ncu
+for w in smax3m mpe_large overcooked smax27m; do
+  SKIP=4; [[ $w == smax* ]] && SKIP=30
+  timeout 600 $NCU --metrics gpu__time_duration.sum --clock-control none -c 200 --csv \
+    --log-file gpurun_out/launches_${TAG}_$w.csv python bench.py --workload $w --steps 5 --warmup 3 --no-e2e --no-cpu \
+    > /dev/null 2>&1
+  timeout 900 $NCU --set full --clock-control none --import-source on -k regex:step_kernel -s $SKIP -c 1 \
+    -o gpurun_out/prof_${TAG}_$w -f python bench.py --workload $w --steps 3 --warmup 30 --no-e2e --no-cpu \
+    > /dev/null 2>&1
+done
+bash scripts/prof_ippo.sh ${TAG} > /dev/null 2>&1
+ls gpurun_out | grep ${TAG}
