@@ -292,7 +292,7 @@ def run_gpu_ippo(args, rank, world, local_rank):
                    "l2": "no flush: each window writes a >20 GB rollout buffer (>> 126 MB L2)"},
         "env_steps_per_sec": env_steps / (total_ms * 1e-3),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": ncu_traffic(args.workload), "peak_source": peak_src,
+                     "traffic": None, "peak_source": peak_src,
                      "bytes_per_launch": n_per_gpu * T * bpe, "mean_launch_us": mean_win_s * 1e6,
                      "kernel": "whole collect window (env step + tcgen05 policy + record + GAE kernels)",
                      "bytes_per_env_step": bpe, "tensor_tflops": tflops},
