@@ -140,6 +140,15 @@ def measured_peak():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
+def ncu_metrics(workload):
+    """SM / DRAM utilisation of the step kernel from the committed ncu capture."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_metrics.json")) as f:
+            return json.load(f).get(workload)
+    except Exception:
+        return None
+
+
 def ncu_traffic(workload):
     """dram bytes per launch of the step kernel from the committed ncu --set full capture."""
     try:
@@ -468,7 +477,8 @@ def run_gpu_arm(args, rank, world, local_rank):
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                      "bytes_per_launch": bytes_per_launch, "mean_launch_us": mean_launch_s * 1e6,
-                     "kernel": "fused step kernel (step_random)"},
+                     "kernel": "fused step kernel (step_random)",
+                     "ncu": ncu_metrics(args.workload)},
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": int(launches),

@@ -103,6 +103,16 @@ def main():
                 if key in d:
                     v, u = d[key]
                     md.append(f"| {label} (`{key}`) | {v} {u} |")
+            smt = d.get("sm__throughput.avg.pct_of_peak_sustained_elapsed")
+            if smt:
+                mpath = os.path.join(PROF, "ncu_metrics.json")
+                mm = json.load(open(mpath)) if os.path.exists(mpath) else {}
+                mm[w] = {"sm_throughput_pct": float(smt[0].replace(",", "")),
+                         "dram_throughput_pct": float(d.get("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
+                                                            ("0", ""))[0].replace(",", "")),
+                         "capture": f"profiles/{tag}_summary.md"}
+                with open(mpath, "w") as f:
+                    json.dump(mm, f, indent=1, sort_keys=True)
             rd, wr = d.get("dram__bytes_read.sum"), d.get("dram__bytes_write.sum")
             if rd and wr:
                 tb = float(rd[0].replace(",", "")) * SCALE.get(rd[1], 1) + \
