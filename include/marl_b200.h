@@ -176,6 +176,11 @@ int marl_copy_device_to_host(void* dst, const void* src, size_t bytes);
 /* Env::legal_actions (env.hpp:71-73; smax.cpp:195-211) for the current
  * state: d_out [N][A][n_actions] u8 (device). */
 int marl_venv_legal(marl_venv* h, uint8_t* d_out);
+/* Env::world_state (smax.cpp:272-289, mpe.cpp:229-242, overcooked.cpp:315-319)
+ * of the current per-env states -- the MAPPO critic input: d_out [N][W] f32
+ * (device), W from marl_venv_world_state_size (Env::world_state_size). */
+int marl_venv_world_state_size(const marl_venv* h, int32_t* out);
+int marl_venv_world_state(marl_venv* h, float* d_out);
 /* Env::state_hash (mpe.cpp:254-269, smax.cpp:312-337, overcooked.cpp:348-364)
  * of the current per-env states: d_out [N] u64 (device). */
 int marl_venv_state_hash(marl_venv* h, uint64_t* d_out);

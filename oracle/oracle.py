@@ -355,6 +355,7 @@ def ref_lib():
         L.mref_set_threads.argtypes = [C.c_int]
         L.mref_reset.argtypes = [C.c_void_p, _u32p, _f32p, _u32p, _u64p]
         L.mref_legal.argtypes = [C.c_void_p, _u8p]
+        L.mref_world_state.argtypes = [C.c_void_p, _f32p, _P(C.c_int)]
         L.mref_random_actions.argtypes = [C.c_void_p, _u32p, _i32p]
         L.mref_step.argtypes = [C.c_void_p, _i32p, _f32p, _f64p, _u8p, _u8p, _f32p, _f64p, _i32p,
                                 _f64p, C.c_int, _f64p, _i32p, _u32p, _u64p]
@@ -421,6 +422,14 @@ class RefVenv:
         m = np.zeros((self.n, self.n_agents, self.n_actions), np.uint8)
         self._chk(ref_lib().mref_legal(self.h, _ptr(m, C.c_uint8)))
         return m
+
+    def world_state(self):
+        """Env::world_state of every env's current state, [N][W] f32."""
+        w = C.c_int()
+        self._chk(ref_lib().mref_world_state(self.h, None, C.byref(w)))
+        out = np.zeros((self.n, w.value), np.float32)
+        self._chk(ref_lib().mref_world_state(self.h, _ptr(out, C.c_float), C.byref(w)))
+        return out
 
     def step(self, actions):
         actions = np.ascontiguousarray(actions, dtype=np.int32)

@@ -143,6 +143,21 @@ int mref_reset(void* p, const uint32_t key[4], float* obs, uint32_t* keys, uint6
   });
 }
 
+// Env::world_state of the current batch state (smax.cpp:272-289, mpe.cpp:229-242,
+// overcooked.cpp:315-319): [N][W] f32, W = world_state_size().
+int mref_world_state(void* p, float* out, int* width) {
+  auto* h = static_cast<Handle*>(p);
+  return guarded([&] {
+    const int W = h->env->world_state_size();
+    *width = W;
+    if (!out) return;
+    for (int i = 0; i < h->n; ++i) {
+      auto w = h->env->world_state(*h->state.states[size_t(i)]);
+      std::copy(w->begin(), w->end(), out + size_t(i) * W);
+    }
+  });
+}
+
 // Legal masks of the current batch state: [N][A][n_act] u8.
 int mref_legal(void* p, uint8_t* legal) {
   auto* h = static_cast<Handle*>(p);

@@ -53,6 +53,7 @@ EXPORTS = [
     "marl_venv_episode_stats", "marl_venv_sync", "marl_throughput_probe",
     "marl_prng_key_from_seed", "marl_prng_split", "marl_prng_fold_in", "marl_prng_bits",
     "marl_threefry2x32", "marl_last_error", "marl_launch_count", "marl_version",
+    "marl_venv_world_state_size", "marl_venv_world_state",
     "marl_rollout_policy_spec", "marl_rollout_create", "marl_rollout_set_params", "marl_rollout_begin",
     "marl_rollout_collect", "marl_rollout_get_views", "marl_rollout_destroy",
 ]
@@ -91,6 +92,8 @@ def lib() -> C.CDLL:
     L.marl_venv_views.argtypes = [vp, C.POINTER(Views)]
     L.marl_copy_device_to_host.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t]
     L.marl_venv_legal.argtypes = [vp, vp]
+    L.marl_venv_world_state_size.argtypes = [vp, i32p]
+    L.marl_venv_world_state.argtypes = [vp, vp]
     L.marl_venv_state_hash.argtypes = [vp, vp]
     L.marl_venv_episode_stats.argtypes = [vp, i64p, C.c_int]
     L.marl_venv_sync.argtypes = [vp]

@@ -208,6 +208,15 @@ void rollout_record(const RolloutBufs& b, int t, int64_t R, int A, const double*
 // GAE per row (compute_gae, actor_critic.hpp:282-299)
 void rollout_gae(const RolloutBufs& b, int T, int64_t R, float gamma, float lambda, cudaStream_t st);
 
+// Env::world_state (smax.cpp:272-289): 18 floats per unit + t/max_steps.
+void smax_launch_world_state(const SmaxConfig& c, const SmaxState& s, int64_t n, float* out, cudaStream_t st);
+// world_state as a gather from the observation view: MPE concatenates every
+// agent's unpadded row (mpe.cpp:229-242), Overcooked is agent 0's row
+// (overcooked.cpp:315-319).  seg_src/seg_len: [n_seg] (offset in the env's
+// [A][D] obs block, length), written back to back.
+void launch_obs_gather(const float* obs, int64_t n, int row_floats, const int32_t* seg_src, const int32_t* seg_len,
+                       int n_seg, int width, float* out, cudaStream_t st);
+
 // ------------------------------------------------------------ common
 // Device-side Env::validate_actions (env.cpp:7-14): n_actions per agent.
 void launch_validate(const int32_t* actions, int64_t n, int A, const int32_t* n_actions_dev,

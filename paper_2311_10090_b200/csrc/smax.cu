@@ -888,6 +888,35 @@ __global__ void smax_hash_kernel(const Params* __restrict__ gP, SmaxState st, in
   out[i] = h;
 }
 
+// world_state (smax.cpp:272-289), one thread per env: per unit alive, x/map,
+// y/map, health/max, cooldown/max, team, type one-hot, action-bucket one-hot;
+// then t/max_steps.
+__global__ void smax_world_state_kernel(const Params* __restrict__ gP, SmaxState st, int64_t n, float* out) {
+  __shared__ __align__(16) Params sP;
+  stage_params(&sP, gP);
+  const Params& P = sP;
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int W = 18 * P.n + 1;
+  float* w = out + size_t(i) * W;
+  for (int u = 0; u < P.n; ++u) {
+    const TypeStat& t = P.ts[P.type[u]];
+    const double h = st.health[u * n + i];
+    const int pa = int(st.mem[u * n + i] & 0xffu);
+    const int bucket = pa <= kStop ? pa : kStop + 1;
+    float* o = w + 18 * u;
+    o[0] = h > 0.0 ? 1.0f : 0.0f;
+    o[1] = float(st.x[u * n + i] / P.map);
+    o[2] = float(st.y[u * n + i] / P.map);
+    o[3] = float(h / t.hmax);
+    o[4] = float(st.cooldown[u * n + i] / t.cdmax);
+    o[5] = float(u < P.na ? 0 : 1);
+    for (int q = 0; q < kTypes; ++q) o[6 + q] = q == P.type[u] ? 1.0f : 0.0f;
+    for (int q = 0; q < 6; ++q) o[12 + q] = q == bucket ? 1.0f : 0.0f;
+  }
+  w[18 * P.n] = float(double(st.t[i]) / P.max_steps);
+}
+
 // ------------------------------------------------------------------ host
 Key to_key(KeyWords k) { return Key{k.w[0], k.w[1], k.w[2], k.w[3]}; }
 
@@ -1014,6 +1043,12 @@ void smax_launch_legal(const SmaxConfig& c, const SmaxState& s, int64_t n, int n
                        cudaStream_t st) {
   smax_legal_kernel<<<unsigned((n + 127) / 128), 128, 0, st>>>(static_cast<const Params*>(c.dev_params), s, n,
                                                                 n_act, out);
+  ++g_launches;
+}
+
+void smax_launch_world_state(const SmaxConfig& c, const SmaxState& s, int64_t n, float* out, cudaStream_t st) {
+  smax_world_state_kernel<<<unsigned((n + 127) / 128), 128, 0, st>>>(static_cast<const Params*>(c.dev_params), s, n,
+                                                                     out);
   ++g_launches;
 }
 

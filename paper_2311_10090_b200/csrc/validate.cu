@@ -34,4 +34,30 @@ void launch_validate(const int32_t* actions, int64_t n, int A, const int32_t* n_
   ++g_launches;
 }
 
+namespace {
+// out[i][*] = the env's obs segments back to back; one warp per env.
+__global__ void obs_gather_kernel(const float* __restrict__ obs, int64_t n, int row_floats,
+                                  const int32_t* __restrict__ seg_src, const int32_t* __restrict__ seg_len, int n_seg,
+                                  int width, float* __restrict__ out) {
+  const int64_t i = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (i >= n) return;
+  const float* src = obs + size_t(i) * row_floats;
+  float* dst = out + size_t(i) * width;
+  int off = 0;
+  for (int sgm = 0; sgm < n_seg; ++sgm) {
+    const int len = seg_len[sgm], from = seg_src[sgm];
+    for (int k = lane; k < len; k += 32) dst[off + k] = src[from + k];
+    off += len;
+  }
+}
+}  // namespace
+
+void launch_obs_gather(const float* obs, int64_t n, int row_floats, const int32_t* seg_src, const int32_t* seg_len,
+                       int n_seg, int width, float* out, cudaStream_t st) {
+  obs_gather_kernel<<<unsigned((n * 32 + 255) / 256), 256, 0, st>>>(obs, n, row_floats, seg_src, seg_len, n_seg,
+                                                                    width, out);
+  ++g_launches;
+}
+
 }  // namespace marl_b200

@@ -469,6 +469,8 @@ struct marl_venv {
   unsigned long long* stats = nullptr;
   int* err = nullptr;
   int32_t* n_actions_dev = nullptr;
+  int32_t* ws_seg = nullptr;  // world_state gather segments: [src offsets | lengths] (MPE, Overcooked)
+  int ws_nseg = 0, ws_width = 0;
   MpeState mpe{};
   SmaxState smax{};
   OcState oc{};
@@ -581,6 +583,7 @@ void create(const char* env_id, const char* cfg, int64_t n_local, int64_t offset
   ar.add(&h->stats, 3);
   ar.add(&h->err, 4);
   ar.add(&h->n_actions_dev, A);
+  ar.add(&h->ws_seg, 2 * A);
   if (e.family == MARL_FAMILY_MPE) {
     int s = e.mpe.scenario;
     ar.add(&h->mpe.pos, N * 2 * size_t(mpe_n_entities(s)));
@@ -607,6 +610,22 @@ void create(const char* env_id, const char* cfg, int64_t n_local, int64_t offset
   const int zero[4] = {0, 0x7fffffff, 0, 0};
   cuda_check(cudaMemcpy(h->err, zero, sizeof zero, cudaMemcpyHostToDevice), "cudaMemcpy");
   cuda_check(cudaMemcpy(h->n_actions_dev, e.n_actions.data(), A * 4, cudaMemcpyHostToDevice), "cudaMemcpy");
+  {  // world_state segments (mpe.cpp:229-242: every agent's row; overcooked.cpp:315-319: agent 0's)
+    std::vector<int32_t> seg;
+    if (e.family == MARL_FAMILY_MPE) {
+      for (int a = 0; a < e.A; ++a) seg.push_back(a * e.D);
+      for (int a = 0; a < e.A; ++a) seg.push_back(e.obs_size[size_t(a)]);
+      h->ws_nseg = e.A;
+    } else if (e.family == MARL_FAMILY_OVERCOOKED) {
+      seg = {0, e.D};
+      h->ws_nseg = 1;
+    }
+    h->ws_width = 0;
+    for (int k = 0; k < h->ws_nseg; ++k) h->ws_width += seg[size_t(h->ws_nseg + k)];
+    if (e.family == MARL_FAMILY_SMAX) h->ws_width = 18 * (e.smax.na + e.smax.ne) + 1;  // smax.cpp:161
+    if (!seg.empty())
+      cuda_check(cudaMemcpy(h->ws_seg, seg.data(), seg.size() * 4, cudaMemcpyHostToDevice), "cudaMemcpy");
+  }
   if (e.family == MARL_FAMILY_SMAX) smax_prepare(h->env->smax);
   if (e.family == MARL_FAMILY_OVERCOOKED)
     cuda_check(cudaMemcpy(h->oc_templ, e.oc_templ.data(), D * 4, cudaMemcpyHostToDevice), "cudaMemcpy");
@@ -1085,6 +1104,30 @@ int marl_rollout_destroy(marl_rollout* r) {
 }
 
 }  // extern "C"
+
+int marl_venv_world_state_size(const marl_venv* h, int32_t* out) {
+  return guarded([&] {
+    if (!h || !out) raise(MARL_ERR_CONTRACT, "marl_venv_world_state_size: NULL argument");
+    *out = h->ws_width;
+  });
+}
+
+// Env::world_state of every env's current state (the MAPPO critic input,
+// ppo.cpp:341-346): d_out [N][world_state_size] f32 (device).
+int marl_venv_world_state(marl_venv* h, float* d_out) {
+  return guarded([&] {
+    set_device(h);
+    require_state(h);
+    if (!d_out) raise(MARL_ERR_CONTRACT, "marl_venv_world_state: NULL output");
+    const Env& e = *h->env;
+    if (e.family == MARL_FAMILY_SMAX)
+      smax_launch_world_state(e.smax, h->smax, h->n, d_out, h->stream);
+    else
+      launch_obs_gather(h->v.obs, h->n, e.A * e.D, h->ws_seg, h->ws_seg + h->ws_nseg, h->ws_nseg, h->ws_width, d_out,
+                        h->stream);
+    after_launch();
+  });
+}
 
 int marl_venv_state_hash(marl_venv* h, uint64_t* d_out) {
   return guarded([&] {

@@ -296,6 +296,15 @@ class VectorEnv:
         N.check(N.lib().marl_venv_legal(self._h, C.c_void_p(out.data_ptr())))
         return out
 
+    def world_state(self):
+        """Env::world_state of every env (smax.cpp:272-289, mpe.cpp:229-242,
+        overcooked.cpp:315-319): float32 [N, world_state_size]."""
+        w = C.c_int32()
+        N.check(N.lib().marl_venv_world_state_size(self._h, C.byref(w)))
+        out = self._torch.empty((self._n, w.value), dtype=self._torch.float32, device=f"cuda:{self._device}")
+        N.check(N.lib().marl_venv_world_state(self._h, C.c_void_p(out.data_ptr())))
+        return out
+
     def state_hash(self):
         """Env::state_hash of every env (int64 tensor holding the u64 bits)."""
         out = self._torch.zeros(self._n, dtype=self._torch.int64, device=f"cuda:{self._device}")

@@ -166,3 +166,30 @@ def test_legal_masks_match_oracle(env_id, cfg):
         assert np.array_equal(v.legal_actions().cpu().numpy(), o.legal()), t
         v.step_random(ak[t])
         o.step_random(ak[t])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("env_id,cfg,n,T", [
+    ("SMAX_5m_vs_6m", THREE_M, 64, 40), ("SMAX_2s3z", {}, 32, 40), ("MPE_simple_spread_v3", {}, 64, 30),
+    ("MPE_simple_speaker_listener_v4", {}, 32, 30), ("overcooked_cramped_room_v0", {"max_steps": 25}, 32, 30)])
+def test_world_state_matches_reference(env_id, cfg, n, T):
+    """Env::world_state (MAPPO critic input) of the live batch vs the reference
+    after the same random-legal steps: exact for SMAX/Overcooked, MPE within
+    the env's bar."""
+    if not O.ref_available():
+        pytest.skip("oracle/_ref not built")
+    v = _venv(env_id, cfg, n, device=0)
+    r = O.RefVenv(env_id, cfg, n)
+    key, ak = probe_keys(21, T)
+    v.reset(key)
+    r.reset(key)
+    for t in range(T):
+        v.step_random(ak[t])
+        r.step_random(ak[t])
+        if t % 7 == 6 or t == T - 1:
+            a, b = v.world_state().cpu().numpy(), r.world_state()
+            assert a.shape == b.shape, (a.shape, b.shape)
+            if env_id.startswith("MPE"):
+                assert np.allclose(a, b, rtol=MPE_RTOL, atol=MPE_ATOL), (t, np.abs(a - b).max())
+            else:
+                assert np.array_equal(a, b), (env_id, t)
