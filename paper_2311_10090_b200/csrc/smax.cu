@@ -83,21 +83,27 @@ struct EnvSm {
   int8_t fire[CAP];
 };
 
-// A group of G lanes of one warp.
+// A group of G lanes of one warp (G need not be a power of two: a warp holds
+// EPW = 32/G groups; the 32 - EPW*G leftover lanes are "dead" and own no env).
 template <int G>
 struct Grp {
+  static constexpr int EPW = 32 / G;
   int gl;         // lane within the group
+  int base;       // warp lane of the group's lane 0
   unsigned mask;  // the group's lanes within the warp
+  bool dead;
   __device__ __forceinline__ Grp() {
-    const int lane = threadIdx.x & 31;
-    gl = lane & (G - 1);
-    mask = G == 32 ? 0xffffffffu : (((1u << G) - 1u) << (lane & ~(G - 1)));
+    const int lane = threadIdx.x & 31, slot = lane / G;
+    dead = slot >= EPW;
+    base = slot * G;
+    gl = lane - base;
+    mask = dead ? (1u << lane) : G == 32 ? 0xffffffffu : (((1u << G) - 1u) << base);
   }
   __device__ __forceinline__ void sync() const { __syncwarp(mask); }
   __device__ __forceinline__ bool any(bool p) const { return (__ballot_sync(mask, p) & mask) != 0u; }
   __device__ __forceinline__ bool all(bool p) const { return (__ballot_sync(mask, p) & mask) == mask; }
   __device__ __forceinline__ int count(bool p) const { return __popc(__ballot_sync(mask, p) & mask); }
-  __device__ __forceinline__ double bcast(double v, int src) const { return __shfl_sync(mask, v, src, G); }
+  __device__ __forceinline__ double bcast(double v, int src) const { return __shfl_sync(mask, v, base + src); }
 };
 
 __device__ __forceinline__ double dclamp(double v, double lo, double hi) {  // std::clamp
@@ -146,7 +152,7 @@ __device__ __forceinline__ unsigned long long bits_above(int i) { return i >= 63
 // Unit bitmask (bit u) of a per-unit predicate held by the owning lanes.
 template <int G, int UPL>
 __device__ __forceinline__ unsigned long long unit_mask(const Grp<G>& g, const bool* pred) {
-  const int base = (threadIdx.x & 31) & ~(G - 1);
+  const int base = g.base;
   const unsigned gbits = G == 32 ? 0xffffffffu : ((1u << G) - 1u);
   unsigned long long m = 0;
 #pragma unroll
@@ -194,8 +200,8 @@ __device__ __forceinline__ void separation_pass(const Params& P, EnvSm<CAP>& e, 
       const unsigned long long hits = unit_mask<G, UPL>(g, hit);
       if (!hits) break;
       const int b = __ffsll((long long)hits) - 1;
-      if (g.gl == (b & (G - 1))) {  // b's lane applies the reference push
-        const int j = b / G;
+      if (g.gl == b % G) {  // b's lane applies the reference push
+        const int j = b / G;  // which of the lane's units
         double dx = hdx[0], dy = hdy[0], dd = hd[0];
 #pragma unroll
         for (int q = 1; q < UPL; ++q)
@@ -537,12 +543,12 @@ __host__ __device__ inline size_t a16(size_t b) { return (b + 15) & ~size_t(15);
 
 template <int G>
 __host__ __device__ inline size_t warp_tile_floats(int D, int rb) {
-  return (size_t(32 / G) * rb * D + 3) & ~size_t(3);
+  return (size_t(Grp<G>::EPW) * rb * D + 3) & ~size_t(3);
 }
 
 template <int G, int UPL>
 __host__ __device__ inline size_t smem_bytes(int D, int rb) {
-  constexpr int EPB = kThreads / G, CAP = G * UPL;
+  constexpr int EPB = kWarps * Grp<G>::EPW, CAP = G * UPL;
   return a16(sizeof(Params)) + a16(EPB * sizeof(EnvSm<CAP>)) + kWarps * warp_tile_floats<G>(D, rb) * 4;
 }
 
@@ -580,9 +586,9 @@ template <int G, int UPL, int CAP>
 __device__ __noinline__ void emit_obs(const Params& P, const EnvSm<CAP>& e, const Grp<G>& g, bool active,
                                          float* tile, float* __restrict__ gdst, int64_t w0, int wvalid, int rb,
                                          unsigned sel) {
-  constexpr int EPW = 32 / G;
+  constexpr int EPW = Grp<G>::EPW;
   const int A = P.A, D = P.D;
-  const int wslot = (threadIdx.x & 31) / G;
+  const int wslot = (threadIdx.x & 31) / G;  // >= EPW only on dead lanes, which never build rows
   for (int a0 = 0; a0 < A; a0 += rb) {
     const int rows = min(rb, A - a0);
     if (active)
@@ -658,7 +664,7 @@ struct Smem {
 
 template <int G, int UPL>
 __device__ __forceinline__ Smem carve(uint8_t* base, int D, int rb) {
-  constexpr int EPB = kThreads / G, CAP = G * UPL;
+  constexpr int EPB = kWarps * Grp<G>::EPW, CAP = G * UPL;
   Smem m;
   m.envs = base + a16(sizeof(Params));
   float* tiles = reinterpret_cast<float*>(m.envs + a16(EPB * sizeof(EnvSm<CAP>)));
@@ -669,19 +675,19 @@ __device__ __forceinline__ Smem carve(uint8_t* base, int D, int rb) {
 template <int G, int UPL>
 __global__ void __launch_bounds__(kThreads) smax_reset_kernel(const Params* __restrict__ gP, SmaxState st,
                                                               LaunchCommon lc, Key key, Key carry_parent, Plan plan) {
-  constexpr int EPB = kThreads / G, EPW = 32 / G, CAP = G * UPL;
+  constexpr int EPW = Grp<G>::EPW, EPB = kWarps * EPW, CAP = G * UPL;
   extern __shared__ __align__(16) uint8_t smem[];
   stage_params(reinterpret_cast<Params*>(smem), gP);
   const Params& P = *reinterpret_cast<const Params*>(smem);
   Smem m = carve<G, UPL>(smem, P.D, plan.rb);
   const Grp<G> g;
-  const int slot = threadIdx.x / G;
+  const int slot = (threadIdx.x >> 5) * EPW + (g.dead ? 0 : (threadIdx.x & 31) / G);
   EnvSm<CAP>& e = reinterpret_cast<EnvSm<CAP>*>(m.envs)[slot];
   const int64_t i = int64_t(blockIdx.x) * EPB + slot;
   const int64_t w0 = int64_t(blockIdx.x) * EPB + (threadIdx.x >> 5) * EPW;
   const int wvalid = int(max(int64_t(0), min64(EPW, lc.n - w0)));
   if (wvalid == 0) return;  // whole warp past the end (warp-uniform)
-  const bool live = i < lc.n;
+  const bool live = !g.dead && i < lc.n;
   int tg[UPL], sw[UPL];
   if (live) {
     const uint64_t gi = uint64_t(lc.offset + i);
@@ -701,20 +707,20 @@ __global__ void __launch_bounds__(kThreads) smax_reset_kernel(const Params* __re
 template <int G, int UPL, bool RANDOM>
 __global__ void __launch_bounds__(kThreads, (G <= 8 ? 4 : 3)) smax_step_kernel(const Params* __restrict__ gP, SmaxState st,
                                                              LaunchCommon lc, Key step_key, Plan plan) {
-  constexpr int EPB = kThreads / G, EPW = 32 / G, CAP = G * UPL;
+  constexpr int EPW = Grp<G>::EPW, EPB = kWarps * EPW, CAP = G * UPL;
   extern __shared__ __align__(16) uint8_t smem[];
   if (*(volatile int*)lc.err) return;  // a pending contract error freezes the batch
   stage_params(reinterpret_cast<Params*>(smem), gP);
   const Params& P = *reinterpret_cast<const Params*>(smem);
   Smem m = carve<G, UPL>(smem, P.D, plan.rb);
   const Grp<G> g;
-  const int slot = threadIdx.x / G;
+  const int slot = (threadIdx.x >> 5) * EPW + (g.dead ? 0 : (threadIdx.x & 31) / G);
   EnvSm<CAP>& e = reinterpret_cast<EnvSm<CAP>*>(m.envs)[slot];
   const int64_t i = int64_t(blockIdx.x) * EPB + slot;
   const int64_t w0 = int64_t(blockIdx.x) * EPB + (threadIdx.x >> 5) * EPW;
   const int wvalid = int(max(int64_t(0), min64(EPW, lc.n - w0)));
   if (wvalid == 0) return;  // whole warp past the end (warp-uniform)
-  const bool live = i < lc.n;
+  const bool live = !g.dead && i < lc.n;
   const int A = P.A;
 
   int tg[UPL], sw[UPL];
@@ -958,21 +964,22 @@ Params make_params(const SmaxConfig& c) {
   return P;
 }
 
-// Group shape for a roster of n units: lanes per env and units per lane.
+// Group shape for a roster of n units: lanes per env (the smallest listed G
+// >= n, so few lanes idle) and units per lane.
 int shape_id(const SmaxConfig& c) {
   const int n = c.na + c.ne;
-  if (const char* f = std::getenv("MARL_SMAX_SHAPE")) {  // tuning override: 0 (8x1) 1 (16x1) 2 (32x1) 3 (32x2) 4 (4x2)
+  if (const char* f = std::getenv("MARL_SMAX_SHAPE")) {  // tuning override, see MARL_SMAX_SHAPES
     const int v = std::atoi(f);
-    const int lanes[6] = {8, 16, 32, 32, 4, 2}, upl[6] = {1, 1, 1, 2, 2, 4};
-    if (v >= 0 && v < 6 && lanes[v] * upl[v] >= n) return v;
+    const int lanes[8] = {4, 6, 8, 10, 12, 16, 32, 32}, upl[8] = {1, 1, 1, 1, 1, 1, 1, 2};
+    if (v >= 0 && v < 8 && lanes[v] * upl[v] >= n) return v;
   }
-  return n <= 8 ? 0 : n <= 16 ? 1 : n <= 32 ? 2 : 3;
+  return n <= 4 ? 0 : n <= 6 ? 1 : n <= 8 ? 2 : n <= 10 ? 3 : n <= 12 ? 4 : n <= 16 ? 5 : n <= 32 ? 6 : 7;
 }
 
 template <int G, int UPL>
 Plan make_plan(const SmaxConfig& c, size_t* smem) {
   const int n = c.na + c.ne, A = c.na + (c.enemy_controlled ? c.ne : 0), D = 10 + 17 * (n - 1);
-  constexpr int EPW = 32 / G;
+  constexpr int EPW = Grp<G>::EPW;
   int rb = int(kWarpStageBytes / (size_t(EPW) * D * 4));
   rb = rb < 1 ? 1 : rb > A ? A : rb;
   *smem = smem_bytes<G, UPL>(D, rb);
@@ -985,7 +992,7 @@ void launch_reset_g(const SmaxConfig& c, const Params* dP, const SmaxState& s, c
   Plan plan = make_plan<G, UPL>(c, &sm);
   auto fn = smax_reset_kernel<G, UPL>;
   cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
-  constexpr int EPB = kThreads / G;
+  constexpr int EPB = kWarps * Grp<G>::EPW;
   fn<<<unsigned((lc.n + EPB - 1) / EPB), kThreads, sm, lc.stream>>>(dP, s, lc, k, cp, plan);
 }
 
@@ -996,17 +1003,19 @@ void launch_step_g(const SmaxConfig& c, const Params* dP, const SmaxState& s, co
   Plan plan = make_plan<G, UPL>(c, &sm);
   auto fn = random ? smax_step_kernel<G, UPL, true> : smax_step_kernel<G, UPL, false>;
   cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
-  constexpr int EPB = kThreads / G;
+  constexpr int EPB = kWarps * Grp<G>::EPW;
   fn<<<unsigned((lc.n + EPB - 1) / EPB), kThreads, sm, lc.stream>>>(dP, s, lc, k, plan);
 }
 
 #define MARL_SMAX_SHAPES(FN, ...)           \
   switch (shape_id(c)) {                    \
-    case 0: FN<8, 1>(__VA_ARGS__); break;   \
-    case 4: FN<4, 2>(__VA_ARGS__); break;   \
-    case 5: FN<2, 4>(__VA_ARGS__); break;   \
-    case 1: FN<16, 1>(__VA_ARGS__); break;  \
-    case 2: FN<32, 1>(__VA_ARGS__); break;  \
+    case 0: FN<4, 1>(__VA_ARGS__); break;   \
+    case 1: FN<6, 1>(__VA_ARGS__); break;   \
+    case 2: FN<8, 1>(__VA_ARGS__); break;   \
+    case 3: FN<10, 1>(__VA_ARGS__); break;  \
+    case 4: FN<12, 1>(__VA_ARGS__); break;  \
+    case 5: FN<16, 1>(__VA_ARGS__); break;  \
+    case 6: FN<32, 1>(__VA_ARGS__); break;  \
     default: FN<32, 2>(__VA_ARGS__); break; \
   }
 
