@@ -11,7 +11,8 @@ import os
 
 from .errors import raise_for_status
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libmarl_b200.so")
+LIB_PATH = os.environ.get("MARL_B200_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib",
+                                                             "libmarl_b200.so")
 
 
 class Spec(C.Structure):

@@ -230,48 +230,78 @@ __device__ __forceinline__ void separation_pass(const Params& P, EnvSm<CAP>& e, 
   }
 }
 
+// This lane's share of the pairs (a, b>a): indices gl, gl+G, ... of the
+// reference's row-major pair order.  For G < 32 the (at most ceil((G-1)/2))
+// pairs are listed once per kernel in registers; G = 32 walks them.
+template <int G>
+struct LanePairs {
+  static constexpr int MAXP = G < 32 ? (G - 1 + 1) / 2 : 1;
+  int np = 0;
+  uint16_t ab[MAXP];  // a | b << 8
+  __device__ __forceinline__ LanePairs(int gl, int n) {
+    if (G >= 32) return;
+    int k = 0;
+    for (PairIt it(gl, n); it.valid() && k < MAXP; it.advance(G)) ab[k++] = uint16_t(it.a | (it.b << 8));
+    np = k;
+  }
+};
+
+template <int G, class F>
+__device__ __forceinline__ bool for_lane_pairs(const LanePairs<G>& lp, int gl, int n, F&& f) {
+  // f(a, b) returns true to stop the walk early; returns whether it stopped
+  if constexpr (G < 32) {
+#pragma unroll
+    for (int k = 0; k < LanePairs<G>::MAXP; ++k)
+      if (k < lp.np && f(int(lp.ab[k] & 0xff), int(lp.ab[k] >> 8))) return true;
+    return false;
+  } else {
+    for (PairIt it(gl, n); it.valid(); it.advance(G))
+      if (f(it.a, it.b)) return true;
+    return false;
+  }
+}
+
 // Does any living pair of this lane's share overlap right now (the exact
 // reference test, hypot only inside the rounding band)?  If no pair overlaps
 // at the start of a pass, the pass pushes nothing -- so it is skipped.
 template <int G, int CAP>
-__device__ __forceinline__ bool lane_pairs_overlap(const Params& P, const EnvSm<CAP>& e, int gl) {
-  for (PairIt it(gl, P.n); it.valid(); it.advance(G)) {
-    const int a = it.a, b = it.b;
-    if (e.h[a] <= 0.0 || e.h[b] <= 0.0) continue;
+__device__ __forceinline__ bool lane_pairs_overlap(const Params& P, const EnvSm<CAP>& e, const LanePairs<G>& lp,
+                                                   int gl) {
+  return for_lane_pairs<G>(lp, gl, P.n, [&](int a, int b) {
+    if (e.h[a] <= 0.0 || e.h[b] <= 0.0) return false;
     const double dx = e.x[b] - e.x[a], dy = e.y[b] - e.y[a];
     const double d2 = dx * dx + dy * dy;
-    if (d2 > P.sep_r2hi) continue;  // farther than any radius sum
+    if (d2 > P.sep_r2hi) return false;  // farther than any radius sum
     const Thresh& R = P.ps[P.type[a]][P.type[b]].rsum;
-    if (d2 > R.r2hi) continue;
-    if (d2 < R.r2lo || R.r - hypot_glibc(dx, dy) > 0.0) return true;
-  }
-  return false;
+    if (d2 > R.r2hi) return false;
+    return d2 < R.r2lo || R.r - hypot_glibc(dx, dy) > 0.0;
+  });
 }
 
 // max_overlap(s) <= kSeparationTol restricted to this lane's pairs (smax.cpp:569-580).
 template <int G, int CAP>
-__device__ __forceinline__ bool lane_pairs_within_tol(const Params& P, const EnvSm<CAP>& e, int gl) {
-  for (PairIt it(gl, P.n); it.valid(); it.advance(G)) {
-    const int a = it.a, b = it.b;
-    if (e.h[a] <= 0.0 || e.h[b] <= 0.0) continue;
+__device__ __forceinline__ bool lane_pairs_within_tol(const Params& P, const EnvSm<CAP>& e, const LanePairs<G>& lp,
+                                                      int gl) {
+  return !for_lane_pairs<G>(lp, gl, P.n, [&](int a, int b) {
+    if (e.h[a] <= 0.0 || e.h[b] <= 0.0) return false;
     const PairStat& S = P.ps[P.type[a]][P.type[b]];
-    double dx = e.x[a] - e.x[b], dy = e.y[a] - e.y[b];
-    double d2 = dx * dx + dy * dy;
-    if (d2 > S.otol.r2hi) continue;      // surely sum - d <= tol
-    if (d2 < S.otol.r2lo) return false;  // surely sum - d > tol
-    if (!(S.rsum.r - hypot_glibc(dx, dy) <= kSepTol)) return false;
-  }
-  return true;
+    const double dx = e.x[a] - e.x[b], dy = e.y[a] - e.y[b];
+    const double d2 = dx * dx + dy * dy;
+    if (d2 > S.otol.r2hi) return false;      // surely sum - d <= tol
+    if (d2 < S.otol.r2lo) return true;       // surely sum - d > tol
+    return !(S.rsum.r - hypot_glibc(dx, dy) <= kSepTol);
+  });
 }
 
 // separate(s, to_fixpoint), smax.cpp:542-567.  A pass is a no-op exactly when
 // no living pair overlaps, which the parallel pre-check proves in the common
 // case (and then max_overlap <= 0 <= tol ends the fixpoint loop as well).
 template <int G, int UPL, int CAP>
-__device__ __forceinline__ void separate(const Params& P, EnvSm<CAP>& e, const Grp<G>& g, bool fixpoint) {
+__device__ __forceinline__ void separate(const Params& P, EnvSm<CAP>& e, const Grp<G>& g, const LanePairs<G>& lp,
+                                         bool fixpoint) {
   unsigned long long alive = 0;
   for (int pass = 0; pass < (fixpoint ? 256 : 1); ++pass) {
-    if (!g.any(lane_pairs_overlap<G>(P, e, g.gl))) break;
+    if (!g.any(lane_pairs_overlap<G>(P, e, lp, g.gl))) break;
     if (pass == 0) {  // health is constant during separation
       bool al[UPL];
 #pragma unroll
@@ -280,7 +310,7 @@ __device__ __forceinline__ void separate(const Params& P, EnvSm<CAP>& e, const G
     }
     separation_pass<G, UPL>(P, e, g, alive);
     if (!fixpoint) break;
-    if (g.all(lane_pairs_within_tol<G>(P, e, g.gl))) break;
+    if (g.all(lane_pairs_within_tol<G>(P, e, lp, g.gl))) break;
   }
 }
 
@@ -385,7 +415,8 @@ __device__ __forceinline__ int heuristic(const Params& P, const EnvSm<CAP>& e, i
 
 // simulate_tick (smax.cpp:503-537), one unit per lane per phase.
 template <int G, int UPL, int CAP>
-__device__ __forceinline__ void tick(const Params& P, EnvSm<CAP>& e, const Grp<G>& g, bool final_tick) {
+__device__ __forceinline__ void tick(const Params& P, EnvSm<CAP>& e, const Grp<G>& g, const LanePairs<G>& lp,
+                                     bool final_tick) {
   // weapons recharge, then moves: each lane touches only its own units
 #pragma unroll
   for (int j = 0; j < UPL; ++j) {
@@ -442,7 +473,7 @@ __device__ __forceinline__ void tick(const Params& P, EnvSm<CAP>& e, const Grp<G
   for (int j = 0; j < UPL; ++j)
     if (newh[j] >= 0.0) e.h[g.gl + G * j] = newh[j];
   g.sync();
-  separate<G, UPL>(P, e, g, final_tick);
+  separate<G, UPL>(P, e, g, lp, final_tick);
 }
 
 // pool(s, 0) and pool(s, 1) (smax.cpp:365-372): the per-unit ratios are one
@@ -565,18 +596,24 @@ __device__ __forceinline__ void stage_params(Params* dst, const Params* __restri
 // ends are 16-byte aligned, else 4-byte words.
 __device__ __forceinline__ void warp_store(float* __restrict__ gdst, const float* src, int nfloats) {
   const int lane = threadIdx.x & 31;
-  if (((reinterpret_cast<uintptr_t>(gdst) | reinterpret_cast<uintptr_t>(src)) & 15) == 0) {
-    const int nv = nfloats >> 2;
-    const float4* s4 = reinterpret_cast<const float4*>(src);
-    float4* d4 = reinterpret_cast<float4*>(gdst);
+  // scalar head up to the first 16-byte aligned destination, then 16-byte
+  // stores (reading the shared source as one or four words per vector)
+  int head = int(((16u - (uint32_t(reinterpret_cast<uintptr_t>(gdst)) & 15u)) & 15u) >> 2);
+  head = head < nfloats ? head : nfloats;
+  if (lane < head) __stcs(gdst + lane, src[lane]);
+  const float* s = src + head;
+  float4* d4 = reinterpret_cast<float4*>(gdst + head);
+  const int nv = (nfloats - head) >> 2;
+  if ((reinterpret_cast<uintptr_t>(s) & 15) == 0) {
+    const float4* s4 = reinterpret_cast<const float4*>(s);
 #pragma unroll 1
     for (int q = lane; q < nv; q += 32) __stcs(d4 + q, s4[q]);
-#pragma unroll 1
-    for (int q = (nv << 2) + lane; q < nfloats; q += 32) __stcs(gdst + q, src[q]);
   } else {
 #pragma unroll 1
-    for (int q = lane; q < nfloats; q += 32) __stcs(gdst + q, src[q]);
+    for (int q = lane; q < nv; q += 32) __stcs(d4 + q, make_float4(s[4 * q], s[4 * q + 1], s[4 * q + 2], s[4 * q + 3]));
   }
+#pragma unroll 1
+  for (int q = head + (nv << 2) + lane; q < nfloats; q += 32) __stcs(gdst + q, src[q]);
 }
 
 // All observation rows of the warp's envs -> gdst ([N][A][D]).  Warp-uniform
@@ -654,7 +691,8 @@ __device__ __noinline__ void env_reset(const Params& P, EnvSm<CAP>& e, const Grp
     if (u < P.n) spawn_unit(P, e, u, key);
   }
   g.sync();
-  separate<G, UPL>(P, e, g, true);
+  const LanePairs<G> lp(g.gl, P.n);  // rare path: built here rather than passed
+  separate<G, UPL>(P, e, g, lp, true);
 }
 
 struct Smem {
@@ -705,7 +743,7 @@ __global__ void __launch_bounds__(kThreads) smax_reset_kernel(const Params* __re
 }
 
 template <int G, int UPL, bool RANDOM>
-__global__ void __launch_bounds__(kThreads, (G <= 8 ? 4 : 3)) smax_step_kernel(const Params* __restrict__ gP, SmaxState st,
+__global__ void __launch_bounds__(kThreads, 3) smax_step_kernel(const Params* __restrict__ gP, SmaxState st,
                                                              LaunchCommon lc, Key step_key, Plan plan) {
   constexpr int EPW = Grp<G>::EPW, EPB = kWarps * EPW, CAP = G * UPL;
   extern __shared__ __align__(16) uint8_t smem[];
@@ -763,8 +801,9 @@ __global__ void __launch_bounds__(kThreads, (G <= 8 ? 4 : 3)) smax_step_kernel(c
     g.sync();
 
     // ---- physics (smax.cpp:242-254)
+    const LanePairs<G> lp(g.gl, P.n);
 #pragma unroll 1
-    for (int k = 0; k < kTicks; ++k) tick<G, UPL>(P, e, g, k == kTicks - 1);
+    for (int k = 0; k < kTicks; ++k) tick<G, UPL>(P, e, g, lp, k == kTicks - 1);
     int ally_alive = 0, enemy_alive = 0;
 #pragma unroll
     for (int j = 0; j < UPL; ++j) {
