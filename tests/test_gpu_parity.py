@@ -193,3 +193,27 @@ def test_world_state_matches_reference(env_id, cfg, n, T):
                 assert np.allclose(a, b, rtol=MPE_RTOL, atol=MPE_ATOL), (t, np.abs(a - b).max())
             else:
                 assert np.array_equal(a, b), (env_id, t)
+
+
+RAGGED = [(env_id, cfg, n) for env_id, cfg in
+          [("MPE_simple_spread_v3", {}), ("SMAX_5m_vs_6m", THREE_M), ("SMAX_2s3z", {}),
+           ("overcooked_cramped_room_v0", {"max_steps": 12})]
+          for n in (1, 7, 41, 257)]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("env_id,cfg,n", RAGGED)
+def test_ragged_batch_sizes_match_oracle(env_id, cfg, n):
+    """Batch sizes that leave partial warps / blocks / bulk-store tiles (one
+    env, odd counts, one past a block): every field still equals the oracle."""
+    v = _venv(env_id, cfg, n, device=0)
+    o = O.PortVenv(env_id, cfg, n)
+    key, ak = probe_keys(31 + n, 30)
+    v.reset(key)
+    o.reset(key)
+    for t in range(30):
+        v.step_random(ak[t])
+        a = gpu_outputs(v, o.n_info)
+        b = o.step_random(ak[t])
+        _compare(env_id, a, b, t)
+

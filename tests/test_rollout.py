@@ -117,3 +117,26 @@ def test_bf16_tensor_core_rollout_agrees_with_fp32():
     # the whole window is a valid rollout: legal actions, GAE identity
     assert (b16["actions"] >= 0).all() and (b16["actions"] < 5).all()
     assert np.array_equal(b16["vtarg"], b16["adv"] + b16["value"])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+@pytest.mark.parametrize("n", [1, 5, 43])
+def test_rollout_ragged_rows(precision, n):
+    """Row counts that leave partial 128-row tensor-core tiles and unaligned
+    bulk-copy tails: the fp32 path still equals the reference collector, the
+    bf16 path stays a valid rollout that agrees on the first step."""
+    _need_ref()
+    env_id, cfg, T = "MPE_simple_spread_v3", {}, 6
+    key = O.key_from_seed(40 + n)
+    a, c = O.ref_ppo_init(env_id, cfg, O.fold_in(key, 10))
+    ref = O.ref_collect(env_id, cfg, n, T, key, a, c)
+    got = _gpu_collect(env_id, cfg, n, T, 1, 0.0, precision, key, a, c)
+    assert np.array_equal(got["resets"], ref["resets"]) and np.array_equal(got["legal"], ref["legal"])
+    assert np.array_equal(got["obs"][0], ref["obs"][0])
+    if precision == "fp32":
+        assert np.array_equal(got["actions"], ref["actions"])
+        assert np.allclose(got["value"], ref["value"], rtol=2e-5, atol=2e-6)
+    else:
+        assert np.allclose(got["value"][0], ref["value"][0], rtol=0.05, atol=0.03)
+        assert np.array_equal(got["vtarg"], got["adv"] + got["value"])
