@@ -97,8 +97,14 @@ __device__ void sample_row(const PolicyStep& s, int64_t r, const float* logits, 
 // The bf16 path's sampler: the same masked softmax + CDF walk with the same
 // per-row key and uniform draw, in float (the bf16 logits already differ
 // from the reference's by far more than float rounding).
-__device__ void sample_row_f32(const PolicyStep& s, int64_t r, const float* logits, const uint8_t* legal, int n_act,
-                               int* action, float* logp) {
+__device__ __forceinline__ double row_uniform(const PolicyStep& s, int64_t r) {
+  const Key ak{s.act_key[0], s.act_key[1], s.act_key[2], s.act_key[3]};
+  const Key kk = fold_in(ak, uint64_t(s.step_index) * uint64_t(s.R_global) + uint64_t(s.row0 + r));
+  return uniform_at(kk, 0, 0.0, 1.0);  // prng::uniform1
+}
+
+__device__ void sample_row_f32(double u, const float* logits, const uint8_t* legal, int n_act, int* action,
+                               float* logp) {
   float mx = -INFINITY;
   for (int i = 0; i < n_act; ++i)
     if (legal[i]) mx = fmaxf(mx, logits[i]);
@@ -108,9 +114,6 @@ __device__ void sample_row_f32(const PolicyStep& s, int64_t r, const float* logi
     denom += p[i];
   }
   const float log_denom = logf(denom), inv = 1.0f / denom;
-  const Key ak{s.act_key[0], s.act_key[1], s.act_key[2], s.act_key[3]};
-  const Key kk = fold_in(ak, uint64_t(s.step_index) * uint64_t(s.R_global) + uint64_t(s.row0 + r));
-  const double u = uniform_at(kk, 0, 0.0, 1.0);  // prng::uniform1
   double cum = 0.0;
   int pick = -1;
   for (int i = 0; i < n_act; ++i) {
@@ -395,8 +398,8 @@ __device__ __forceinline__ void put16(uint8_t* tile, int K, int row, int k0, con
 // Shared-memory carve-up of the tcgen05 policy kernel, sized from the actual
 // row widths (offsets in bytes from a 1024-aligned base).
 struct TcLayout {
-  uint32_t w1, w2a, w2c, w3a, w3c, x, ha, hc, obs_in[2], obs_out, legal, resets, active, act, logp, value, bias, bar,
-      bar_in[2], tmem_slot, total;
+  uint32_t w1, w2a, w2c, w3a, w3c, x, ha, hc, obs_in[2], obs_out, legal, resets, active, act, logp, value, u, bias,
+      bar, bar_in[2], tmem_slot, total;
 };
 
 __host__ __device__ inline uint32_t up(uint32_t v, uint32_t a) { return (v + a - 1) / a * a; }
@@ -427,6 +430,7 @@ __host__ __device__ inline TcLayout tc_layout(int D, int in_dim, int n_act) {
   L.act = take(kTcRows * 4, 16);
   L.logp = take(kTcRows * 4, 16);
   L.value = take(kTcRows * 4, 16);
+  L.u = take(kTcRows * 8, 16);
   L.bias = take((4 * 64 + 2 * 16) * 4, 16);
   L.bar = take(8, 8);
   L.bar_in[0] = take(8, 8);
@@ -488,6 +492,7 @@ __global__ void __launch_bounds__(kSplit * kTcRows) policy_tc_kernel(PolicyNetBf
   float* s_logp = reinterpret_cast<float*>(base + L.logp);
   float* s_value = reinterpret_cast<float*>(base + L.value);
   float* s_bias = reinterpret_cast<float*>(base + L.bias);
+  double* s_u = reinterpret_cast<double*>(base + L.u);
   uint64_t* bar = reinterpret_cast<uint64_t*>(base + L.bar);
   uint64_t* bar_in[2] = {reinterpret_cast<uint64_t*>(base + L.bar_in[0]), reinterpret_cast<uint64_t*>(base + L.bar_in[1])};
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(base + L.tmem_slot);
@@ -571,7 +576,7 @@ __global__ void __launch_bounds__(kSplit * kTcRows) policy_tc_kernel(PolicyNetBf
     // builds K columns [32q/kSplit, 32(q+1)/kSplit) of the row
     {
       const float* oin = obs_in[cur];
-      const int64_t e = r / s.A;
+      const int64_t e = r < 0x7fffffff ? int64_t(uint32_t(r) / uint32_t(s.A)) : r / s.A;
       const int a = int(r - e * s.A);
       const int k0 = (32 / kSplit) * part;
       float x[32 / kSplit];
@@ -619,6 +624,9 @@ __global__ void __launch_bounds__(kSplit * kTcRows) policy_tc_kernel(PolicyNetBf
       for (int k = 0; k < 32; k += 16) umma_bf16(tmem + 0, umma_desc(sx, 32, k), umma_desc(w1, 32, k), id, k > 0);
       umma_commit(bar);
     }
+    // the row's sampling uniform (two Threefry blocks) is drawn by part 1
+    // while the layer-1 MMA runs; part 0 samples with it after layer 3
+    if (part == 1 && live && act_mode) s_u[tid] = row_uniform(s, r);
     mbar_wait(bar, phase);
     phase ^= 1;
     tc_fence_after();
@@ -687,7 +695,7 @@ __global__ void __launch_bounds__(kSplit * kTcRows) policy_tc_kernel(PolicyNetBf
         for (int j = 0; j < 16; ++j) logits[j] = hv[j] + s_bias[256 + j];
         int pick;
         float lp;
-        sample_row_f32(s, r, logits, s_legal + tid * n_act, n_act, &pick, &lp);
+        sample_row_f32(s_u[tid], logits, s_legal + tid * n_act, n_act, &pick, &lp);
         b.actions[slot0 + tid] = pick;  // one element per thread: coalesced
         b.logp[slot0 + tid] = lp;
       }
