@@ -205,6 +205,7 @@ typedef struct marl_rollout marl_rollout;
 
 typedef struct {
   int32_t in_dim;           /* PpoNetSpec::in_dim: padded obs + agent one-hot (ppo.cpp:80-107) */
+  int32_t critic_in;        /* PpoNetSpec::critic_in: in_dim (IPPO) or world_state_size (MAPPO) */
   int32_t n_actions;        /* PpoNetSpec::n_actions (padded action head) */
   int32_t width, n_layers, relu;
   int32_t n_actor_params;   /* floats in PpoNets::pack_actor() order (nn::pack, nn.hpp:326-341) */
@@ -225,16 +226,20 @@ typedef struct { /* device pointers, [T][R] row-major */
   float* adv;
   float* vtarg;
   float* last_value; /* [R] */
+  float* critic_in;  /* [T][R][critic_dim] MAPPO critic rows (NULL for IPPO: the critic reads obs) */
+  int32_t critic_dim;
   int32_t T;
   int64_t R;
   int32_t in_dim, n_actions;
 } marl_rollout_views;
 
-/* ppo_net_spec(env, cfg, false) for fc_width/n_fc_layers/activation. */
-int marl_rollout_policy_spec(const marl_venv* h, int width, int n_layers, int relu, marl_policy_spec* out);
+/* ppo_net_spec(env, cfg, centralized) for fc_width/n_fc_layers/activation;
+ * centralized = 1 is train_mappo's critic on Env::world_state (ppo.hpp:99). */
+int marl_rollout_policy_spec(const marl_venv* h, int width, int n_layers, int relu, int centralized,
+                             marl_policy_spec* out);
 /* precision 0: fp32 in the reference's accumulation order (parity path);
  * precision 1: bf16 operands, fp32 accumulation on tcgen05 tensor cores. */
-int marl_rollout_create(marl_venv* h, int T, int width, int n_layers, int relu, int precision,
+int marl_rollout_create(marl_venv* h, int T, int width, int n_layers, int relu, int centralized, int precision,
                         marl_rollout** out);
 /* Host parameters in PpoNets::pack_actor()/pack_critic() order. */
 int marl_rollout_set_params(marl_rollout* r, const float* actor, const float* critic);

@@ -366,9 +366,10 @@ def ref_lib():
         L.mref_hypot.argtypes = [C.c_double, C.c_double]
         L.mref_hypot.restype = C.c_double
         L.mref_rollout_last_error.restype = C.c_char_p
-        L.mref_ppo_spec.argtypes = [C.c_char_p, C.c_char_p] + [_P(C.c_int)] * 4
-        L.mref_ppo_init.argtypes = [C.c_char_p, C.c_char_p, _u32p, _f32p, _f32p]
-        L.mref_collect.argtypes = [C.c_char_p, C.c_char_p, C.c_int, C.c_int, C.c_int, _u32p, _f32p, _f32p,
+        L.mref_ppo_spec.argtypes = [C.c_char_p, C.c_char_p, C.c_int] + [_P(C.c_int)] * 5
+        L.mref_ppo_init.argtypes = [C.c_char_p, C.c_char_p, C.c_int, _u32p, _f32p, _f32p]
+        L.mref_collect.argtypes = [C.c_char_p, C.c_char_p, C.c_int, _f32p, C.c_int, C.c_int, C.c_int, _u32p,
+                                   _f32p, _f32p,
                                    C.c_double, C.c_double, C.c_double, _f32p, _i32p, _f32p, _u8p, _u8p, _f32p,
                                    _f32p, _u8p, _f32p, _f32p, _f32p, _f64p, _P(C.c_int64)]
         _ref = L
@@ -468,34 +469,38 @@ def ref_probe(env_id, config, n_envs, n_steps, key, threads=None):
 
 
 # --------------------------------------------------------- IPPO rollout (C5)
-def ref_ppo_spec(env_id, config=None):
-    """ppo_net_spec + packed parameter counts from the reference (ppo.cpp:80-124)."""
+def ref_ppo_spec(env_id, config=None, centralized=False):
+    """ppo_net_spec + packed parameter counts from the reference (ppo.cpp:80-124);
+    centralized: the MAPPO critic on world_state (train_mappo, ppo.hpp:99)."""
     L = ref_lib()
-    v = [C.c_int() for _ in range(4)]
-    rc = L.mref_ppo_spec(env_id.encode(), json.dumps(config or {}).encode(), *[C.byref(x) for x in v])
+    v = [C.c_int() for _ in range(5)]
+    rc = L.mref_ppo_spec(env_id.encode(), json.dumps(config or {}).encode(), int(centralized),
+                         *[C.byref(x) for x in v])
     if rc:
         raise RuntimeError(L.mref_rollout_last_error().decode())
-    return {"in_dim": v[0].value, "n_actions": v[1].value, "n_actor": v[2].value, "n_critic": v[3].value}
+    return {"in_dim": v[0].value, "critic_in": v[1].value, "n_actions": v[2].value, "n_actor": v[3].value,
+            "n_critic": v[4].value}
 
 
-def ref_ppo_init(env_id, config, key):
+def ref_ppo_init(env_id, config, key, centralized=False):
     """ppo_init_nets(key, spec) packed (pack_actor, pack_critic)."""
     L = ref_lib()
-    sp = ref_ppo_spec(env_id, config)
+    sp = ref_ppo_spec(env_id, config, centralized)
     a = np.zeros(sp["n_actor"], np.float32)
     c = np.zeros(sp["n_critic"], np.float32)
-    rc = L.mref_ppo_init(env_id.encode(), json.dumps(config or {}).encode(), _ptr(_key(key), C.c_uint32),
-                         _ptr(a, C.c_float), _ptr(c, C.c_float))
+    rc = L.mref_ppo_init(env_id.encode(), json.dumps(config or {}).encode(), int(centralized),
+                         _ptr(_key(key), C.c_uint32), _ptr(a, C.c_float), _ptr(c, C.c_float))
     if rc:
         raise RuntimeError(L.mref_rollout_last_error().decode())
     return a, c
 
 
-def ref_collect(env_id, config, n_envs, T, key, actor, critic, n_windows=1, gamma=0.99, lam=1.0, shaping=0.0):
+def ref_collect(env_id, config, n_envs, T, key, actor, critic, n_windows=1, gamma=0.99, lam=1.0, shaping=0.0,
+                centralized=False):
     """The reference Collector (restated over its public pieces, ref_rollout.cpp):
     buffers of the last window, [T][R]."""
     L = ref_lib()
-    sp = ref_ppo_spec(env_id, config)
+    sp = ref_ppo_spec(env_id, config, centralized)
     v = RefVenv(env_id, config, 1)  # agents per env (TeamLayout rows)
     A = v.n_agents
     R = n_envs * A
@@ -504,12 +509,13 @@ def ref_collect(env_id, config, n_envs, T, key, actor, critic, n_windows=1, gamm
            "resets": np.zeros((T, R), np.uint8), "logp": np.zeros((T, R), np.float32),
            "value": np.zeros((T, R), np.float32), "legal": np.zeros((T, R, sp["n_actions"]), np.uint8),
            "active": np.zeros((T, R), np.float32), "adv": np.zeros((T, R), np.float32),
-           "vtarg": np.zeros((T, R), np.float32)}
+           "vtarg": np.zeros((T, R), np.float32), "critic_in": np.zeros((T, R, sp["critic_in"]), np.float32)}
     ep_sum = C.c_double()
     eps = C.c_int64()
     a = np.ascontiguousarray(actor, np.float32)
     c = np.ascontiguousarray(critic, np.float32)
-    rc = L.mref_collect(env_id.encode(), json.dumps(config or {}).encode(), n_envs, T, n_windows,
+    rc = L.mref_collect(env_id.encode(), json.dumps(config or {}).encode(), int(centralized),
+                        _ptr(out["critic_in"], C.c_float), n_envs, T, n_windows,
                         _ptr(_key(key), C.c_uint32), _ptr(a, C.c_float), _ptr(c, C.c_float), gamma, lam, shaping,
                         _ptr(out["obs"], C.c_float), _ptr(out["actions"], C.c_int32), _ptr(out["rewards"], C.c_float),
                         _ptr(out["dones"], C.c_uint8), _ptr(out["resets"], C.c_uint8), _ptr(out["logp"], C.c_float),

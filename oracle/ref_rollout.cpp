@@ -44,9 +44,9 @@ int guarded(F&& f) {
 Config parse(const char* cfg) { return (cfg && *cfg) ? Config::parse(cfg) : Config::object(); }
 PrngKey key_of(const uint32_t k[4]) { return PrngKey{k[0], k[1], k[2], k[3]}; }
 
-PpoNetSpec spec_for(const Env& env) {
+PpoNetSpec spec_for(const Env& env, int centralized) {
   PpoConfig pc;  // defaults: fc_width 64, n_fc_layers 2, tanh (ppo.hpp:38-57)
-  return ppo_net_spec(env, pc, false);
+  return ppo_net_spec(env, pc, centralized != 0);  // centralized: the MAPPO critic reads world_state
 }
 }  // namespace
 
@@ -55,10 +55,12 @@ extern "C" {
 const char* mref_rollout_last_error(void) { return g_err.c_str(); }
 
 // ppo_net_spec (ppo.cpp:80-107) and the packed parameter counts.
-int mref_ppo_spec(const char* env_id, const char* cfg, int* in_dim, int* n_actions, int* n_actor, int* n_critic) {
+int mref_ppo_spec(const char* env_id, const char* cfg, int centralized, int* in_dim, int* critic_in, int* n_actions,
+                  int* n_actor, int* n_critic) {
   return guarded([&] {
     auto env = make_env(env_id, parse(cfg));
-    PpoNetSpec s = spec_for(*env);
+    PpoNetSpec s = spec_for(*env, centralized);
+    *critic_in = s.critic_in;
     PpoNets nets = ppo_init_nets(prng::key_from_seed(0), s);
     *in_dim = s.in_dim;
     *n_actions = s.n_actions;
@@ -68,26 +70,28 @@ int mref_ppo_spec(const char* env_id, const char* cfg, int* in_dim, int* n_actio
 }
 
 // ppo_init_nets(key, spec) (ppo.cpp:109-124), packed in nn::pack order.
-int mref_ppo_init(const char* env_id, const char* cfg, const uint32_t key[4], float* actor, float* critic) {
+int mref_ppo_init(const char* env_id, const char* cfg, int centralized, const uint32_t key[4], float* actor,
+                  float* critic) {
   return guarded([&] {
     auto env = make_env(env_id, parse(cfg));
-    PpoNets nets = ppo_init_nets(key_of(key), spec_for(*env));
+    PpoNets nets = ppo_init_nets(key_of(key), spec_for(*env, centralized));
     auto a = nets.pack_actor(), c = nets.pack_critic();
     std::memcpy(actor, a.data(), a.size() * sizeof(float));
     std::memcpy(critic, c.data(), c.size() * sizeof(float));
   });
 }
 
-// Collector(env, cfg, spec, false, key) + n_windows x collect(nets, T, w*T, shaping);
+// Collector(env, cfg, spec, centralized, key) + n_windows x collect(nets, T, w*T, shaping);
 // the buffers of the LAST window are returned ([T][R] row-major, R = n_envs * A).
-int mref_collect(const char* env_id, const char* cfg, int n_envs, int T, int n_windows, const uint32_t key[4],
+int mref_collect(const char* env_id, const char* cfg, int centralized, float* o_critic_in, int n_envs, int T,
+                 int n_windows, const uint32_t key[4],
                  const float* actor, const float* critic, double gamma, double lambda, double shaping,
                  float* o_obs, int32_t* o_actions, float* o_rewards, uint8_t* o_dones, uint8_t* o_resets,
                  float* o_logp, float* o_value, uint8_t* o_legal, float* o_active, float* o_adv, float* o_vtarg,
                  double* o_ep_return_sum, int64_t* o_episodes) {
   return guarded([&] {
     auto env = make_env(env_id, parse(cfg));
-    const PpoNetSpec spec = spec_for(*env);
+    const PpoNetSpec spec = spec_for(*env, centralized);
     PpoNets nets = ppo_init_nets(prng::key_from_seed(0), spec);
     {
       auto a = nets.pack_actor(), c = nets.pack_critic();
@@ -104,16 +108,22 @@ int mref_collect(const char* env_id, const char* cfg, int n_envs, int T, int n_w
     BatchedState state = std::move(state0);
     const int E = n_envs, A = layout.n_agents(), R = E * A;
     std::vector<uint8_t> prev_finished(size_t(E), 1);
-    const int in_dim = spec.in_dim, na = spec.n_actions;
+    const int in_dim = spec.in_dim, na = spec.n_actions, cin = spec.critic_in;
     double ep_sum = 0.0;
     int64_t episodes = 0;
 
-    auto fill_inputs = [&](nn::Mat<float>& x, uint8_t* legal, float* active) {  // ppo.cpp:333-360 (IPPO)
+    auto fill_inputs = [&](nn::Mat<float>& x, nn::Mat<float>& xc, uint8_t* legal, float* active) {  // ppo.cpp:333-360
+      std::vector<float> ws;
       for (int e = 0; e < E; ++e) {
         const auto& st = *state.states[size_t(e)];
+        if (centralized) ws = *env->world_state(st);
         for (int a = 0; a < A; ++a) {
           const int r = e * A + a;
           layout.write_input(cur_obs[size_t(e)].at(layout.agents[size_t(a)]), a, &x.a[size_t(r) * size_t(in_dim)]);
+          if (centralized)
+            std::memcpy(&xc.a[size_t(r) * size_t(cin)], ws.data(), ws.size() * sizeof(float));
+          else
+            std::memcpy(&xc.a[size_t(r) * size_t(cin)], &x.a[size_t(r) * size_t(in_dim)], size_t(in_dim) * 4);
           if (legal) layout.write_legal(*env, st, a, legal + size_t(r) * size_t(na));
           if (active) active[r] = env->agent_active(st, layout.agents[size_t(a)]) ? 1.0f : 0.0f;
         }
@@ -124,7 +134,8 @@ int mref_collect(const char* env_id, const char* cfg, int n_envs, int T, int n_w
     std::vector<uint8_t> don_buf;
     for (int w = 0; w < n_windows; ++w) {
       const int64_t seq_base = int64_t(w) * T;
-      std::vector<float> obs(size_t(T) * R * in_dim), rewards(size_t(T) * R), logp(size_t(T) * R),
+      std::vector<float> obs(size_t(T) * R * in_dim), crit(size_t(T) * R * cin), rewards(size_t(T) * R),
+          logp(size_t(T) * R),
           value(size_t(T) * R), active(size_t(T) * R);
       std::vector<int32_t> actions(size_t(T) * R);
       std::vector<uint8_t> dones(size_t(T) * R), resets(size_t(T) * R), legal(size_t(T) * R * na);
@@ -133,11 +144,12 @@ int mref_collect(const char* env_id, const char* cfg, int n_envs, int T, int n_w
       for (int t = 0; t < T; ++t) {  // ppo.cpp:229-281
         const size_t base = size_t(t) * size_t(R);
         for (int r = 0; r < R; ++r) resets[base + size_t(r)] = prev_finished[size_t(r / A)];
-        nn::Mat<float> x(R, in_dim);
-        fill_inputs(x, &legal[base * size_t(na)], &active[base]);
+        nn::Mat<float> x(R, in_dim), xc(R, cin);
+        fill_inputs(x, xc, &legal[base * size_t(na)], &active[base]);
         std::memcpy(&obs[base * size_t(in_dim)], x.a.data(), x.a.size() * sizeof(float));
+        std::memcpy(&crit[base * size_t(cin)], xc.a.data(), xc.a.size() * sizeof(float));
         nn::Mat<float> logits = nn::ff_forward(nets.actor_ff, x, spec.act);
-        nn::Mat<float> values = nn::ff_forward(nets.critic_ff, x, spec.act);  // IPPO: critic_in == x
+        nn::Mat<float> values = nn::ff_forward(nets.critic_ff, xc, spec.act);
         std::vector<AgentMap<Action>> acts(static_cast<size_t>(E));
         for (int r = 0; r < R; ++r) {
           auto kk = prng::fold_in(act_key, uint64_t(seq_base + t) * uint64_t(R) + uint64_t(r));
@@ -172,9 +184,9 @@ int mref_collect(const char* env_id, const char* cfg, int n_envs, int T, int n_w
         state = std::move(res.next);
       }
       // bootstrap values, ppo.cpp:285-299
-      nn::Mat<float> x(R, in_dim);
-      fill_inputs(x, nullptr, nullptr);
-      nn::Mat<float> lastv = nn::ff_forward(nets.critic_ff, x, spec.act);
+      nn::Mat<float> x(R, in_dim), xc(R, cin);
+      fill_inputs(x, xc, nullptr, nullptr);
+      nn::Mat<float> lastv = nn::ff_forward(nets.critic_ff, xc, spec.act);
       // GAE per row, ppo.cpp:301-321
       std::vector<float> adv(size_t(T) * R), vtarg(size_t(T) * R);
       std::vector<float> rw(static_cast<size_t>(T)), vl(static_cast<size_t>(T));
@@ -199,6 +211,7 @@ int mref_collect(const char* env_id, const char* cfg, int n_envs, int T, int n_w
           if (d) std::memcpy(d, s, n);
         };
         cp(o_obs, obs.data(), obs.size() * 4);
+        cp(o_critic_in, crit.data(), crit.size() * 4);
         cp(o_actions, actions.data(), actions.size() * 4);
         cp(o_rewards, rewards.data(), rewards.size() * 4);
         cp(o_dones, dones.data(), dones.size());

@@ -29,14 +29,15 @@ class Views(C.Structure):
 
 
 class PolicySpec(C.Structure):
-    _fields_ = [(n, C.c_int32) for n in ("in_dim", "n_actions", "width", "n_layers", "relu",
+    _fields_ = [(n, C.c_int32) for n in ("in_dim", "critic_in", "n_actions", "width", "n_layers", "relu",
                                          "n_actor_params", "n_critic_params", "rows_per_env")]
 
 
 class RolloutViews(C.Structure):
     _fields_ = [(n, C.c_void_p) for n in ("obs", "actions", "rewards", "dones", "resets", "logp", "value",
-                                          "legal", "active", "adv", "vtarg", "last_value")] + \
-               [("T", C.c_int32), ("R", C.c_int64), ("in_dim", C.c_int32), ("n_actions", C.c_int32)]
+                                          "legal", "active", "adv", "vtarg", "last_value", "critic_in")] + \
+               [("critic_dim", C.c_int32), ("T", C.c_int32), ("R", C.c_int64), ("in_dim", C.c_int32),
+                ("n_actions", C.c_int32)]
 
 
 class HostStep(C.Structure):
@@ -106,8 +107,8 @@ def lib() -> C.CDLL:
     L.marl_prng_bits.argtypes = [u32p, C.c_uint64]
     L.marl_prng_bits.restype = C.c_uint64
     L.marl_threefry2x32.argtypes = [C.c_uint32] * 4 + [u32p]
-    L.marl_rollout_policy_spec.argtypes = [vp, C.c_int, C.c_int, C.c_int, C.POINTER(PolicySpec)]
-    L.marl_rollout_create.argtypes = [vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(vp)]
+    L.marl_rollout_policy_spec.argtypes = [vp, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(PolicySpec)]
+    L.marl_rollout_create.argtypes = [vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(vp)]
     L.marl_rollout_set_params.argtypes = [vp, vp, vp]
     L.marl_rollout_begin.argtypes = [vp, u32p]
     L.marl_rollout_collect.argtypes = [vp, C.c_int64, C.c_double, C.c_double, C.c_double]

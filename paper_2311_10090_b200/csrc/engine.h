@@ -161,6 +161,7 @@ struct RolloutBufs {
   float* adv;          // [T][R]
   float* vtarg;        // [T][R]
   float* last_value;   // [R]  bootstrap values after the window (ppo.cpp:285-299)
+  float* critic_in;    // [T][R][critic_in] centralised (MAPPO) critic rows, else null
 };
 
 // Feed-forward actor and critic (ff_forward, actor_critic.hpp:49-52) with two
@@ -170,6 +171,7 @@ struct PolicyNet {
   const float *w1, *b1, *w2, *b2, *w3, *b3;
   const float *cw1, *cb1, *cw2, *cb2, *cw3, *cb3;
   int in_dim, n_act, width, relu;
+  int critic_in;  // == in_dim (IPPO) or world_state_size (MAPPO, ppo.cpp:90-100)
 };
 
 // bf16 operand images for the tcgen05 path (K-major, no swizzle, UMMA
@@ -193,6 +195,7 @@ struct PolicyStep {
   int64_t step_index;          // seq_base + t
   int t;
   int bootstrap;               // 1: critic only -> last_value (ppo.cpp:285-299)
+  const float* ws;             // [E][critic_in] world_state rows (MAPPO critic input) or null (IPPO)
   int legal_ready;             // 1: bufs.legal slice t already filled by the env's legal kernel
 };
 

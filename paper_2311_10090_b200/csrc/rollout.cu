@@ -58,9 +58,9 @@ struct SmemNet {  // the net staged in shared memory, same packing as PolicyNet
   const float *w1, *b1, *w2, *b2, *w3, *b3, *cw1, *cb1, *cw2, *cb2, *cw3, *cb3;
 };
 
-__host__ __device__ inline int net_floats(int in, int width, int n_act) {
+__host__ __device__ inline int net_floats(int in, int cin, int width, int n_act) {
   return (width * in + width + width * width + width + n_act * width + n_act) +
-         (width * in + width + width * width + width + width + 1);
+         (width * cin + width + width * width + width + width + 1);
 }
 
 }  // namespace
@@ -167,11 +167,11 @@ namespace {
 
 __global__ void __launch_bounds__(128) policy_fp32_kernel(PolicyNet net, PolicyStep s, RolloutBufs b, int staged) {
   extern __shared__ __align__(16) float smem[];
-  const int in = net.in_dim, W = net.width, NA = net.n_act;
+  const int in = net.in_dim, CI = net.critic_in, W = net.width, NA = net.n_act;
   // stage the packed actor+critic parameters (one contiguous device block)
   // when they fit in shared memory; wide inputs (Overcooked's 543) read them
   // through L1 instead
-  const int total = net_floats(in, W, NA);
+  const int total = net_floats(in, CI, W, NA);
   if (staged) {
     for (int q = threadIdx.x; q < total; q += blockDim.x) smem[q] = __ldg(net.w1 + q);
     __syncthreads();
@@ -184,7 +184,7 @@ __global__ void __launch_bounds__(128) policy_fp32_kernel(PolicyNet net, PolicyS
   m.w3 = m.b2 + W;
   m.b3 = m.w3 + NA * W;
   m.cw1 = m.b3 + NA;
-  m.cb1 = m.cw1 + W * in;
+  m.cb1 = m.cw1 + W * CI;
   m.cw2 = m.cb1 + W;
   m.cb2 = m.cw2 + W * W;
   m.cw3 = m.cb2 + W;
@@ -194,8 +194,17 @@ __global__ void __launch_bounds__(128) policy_fp32_kernel(PolicyNet net, PolicyS
   if (r >= s.R) return;
   float x[kMaxIn], h1[kMaxWidth], h2[kMaxWidth];
   fill_row(s, b, r, in, NA, x, !s.bootstrap);
-  // critic (the value head of ff_forward on the same row: IPPO critic_in == x)
-  for (int o = 0; o < W; ++o) h1[o] = activate(__fadd_rn(dot_ref(x, m.cw1 + o * in, in), m.cb1[o]), net.relu);
+  // critic: IPPO reads the same row (critic_in == x); MAPPO reads the env's
+  // world_state (ppo.cpp:341-346), kept in the buffer's critic_in rows
+  const float* xc = x;
+  if (s.ws) {
+    xc = s.ws + size_t(r / s.A) * CI;
+    if (!s.bootstrap) {
+      float* bc = b.critic_in + (size_t(s.t) * size_t(s.R) + size_t(r)) * CI;
+      for (int k = 0; k < CI; ++k) bc[k] = xc[k];
+    }
+  }
+  for (int o = 0; o < W; ++o) h1[o] = activate(__fadd_rn(dot_ref(xc, m.cw1 + o * CI, CI), m.cb1[o]), net.relu);
   for (int o = 0; o < W; ++o) h2[o] = activate(__fadd_rn(dot_ref(h1, m.cw2 + o * W, W), m.cb2[o]), net.relu);
   const float value = __fadd_rn(dot_ref(h2, m.cw3, W), m.cb3[0]);
   if (s.bootstrap) {
@@ -243,7 +252,7 @@ __global__ void gae_kernel(RolloutBufs b, int T, int64_t R, float gamma, float l
 }  // namespace
 
 void rollout_policy_fp32(const PolicyNet& net, const PolicyStep& s, const RolloutBufs& b, cudaStream_t st) {
-  size_t sm = size_t(net_floats(net.in_dim, net.width, net.n_act)) * sizeof(float);
+  size_t sm = size_t(net_floats(net.in_dim, net.critic_in, net.width, net.n_act)) * sizeof(float);
   const int staged = sm <= size_t(160) * 1024;
   if (!staged) sm = 0;
   cudaFuncSetAttribute(policy_fp32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));

@@ -870,6 +870,8 @@ struct marl_rollout {
   int T = 0;
   int64_t R = 0, R_global = 0, row0 = 0;
   int in_dim = 0, n_act = 0, width = 64, relu = 0, precision = 0;
+  int critic_in = 0, centralized = 0;
+  float* ws = nullptr;  // [E][critic_in] world_state scratch (MAPPO)
   int n_actor = 0, n_critic = 0, shaped_idx = -1;
   Arena arena;
   RolloutBufs b{};
@@ -883,12 +885,16 @@ struct marl_rollout {
 
 namespace {
 
-// ppo_net_spec (ppo.cpp:80-107) over TeamLayout::from_env (team.cpp:10-25).
-void policy_dims(const Env& e, int width, int* in_dim, int* n_act, int* n_actor, int* n_critic) {
+// ppo_net_spec (ppo.cpp:80-107) over TeamLayout::from_env (team.cpp:10-25);
+// centralized: the MAPPO critic reads world_state (ppo.cpp:90-97).
+void policy_dims(const marl_venv* h, int width, int centralized, int* in_dim, int* critic_in, int* n_act,
+                 int* n_actor, int* n_critic) {
+  const Env& e = *h->env;
   *in_dim = e.D + (e.A > 1 ? e.A : 0);
+  *critic_in = centralized ? h->ws_width : *in_dim;
   *n_act = *std::max_element(e.n_actions.begin(), e.n_actions.end());
   *n_actor = width * *in_dim + width + width * width + width + *n_act * width + *n_act;
-  *n_critic = width * *in_dim + width + width * width + width + width + 1;
+  *n_critic = width * *critic_in + width + width * width + width + width + 1;
 }
 
 PolicyNet net_of(const marl_rollout* r) {
@@ -901,12 +907,13 @@ PolicyNet net_of(const marl_rollout* r) {
   n.w3 = n.b2 + W;
   n.b3 = n.w3 + NA * W;
   n.cw1 = n.b3 + NA;
-  n.cb1 = n.cw1 + W * in;
+  n.cb1 = n.cw1 + W * r->critic_in;
   n.cw2 = n.cb1 + W;
   n.cb2 = n.cw2 + W * W;
   n.cw3 = n.cb2 + W;
   n.cb3 = n.cw3 + W;
   n.in_dim = in;
+  n.critic_in = r->critic_in;
   n.n_act = NA;
   n.width = W;
   n.relu = r->relu;
@@ -941,6 +948,10 @@ void run_policy(marl_rollout* r, int t, bool bootstrap, int64_t seq_base) {
   s.step_index = seq_base + t;
   s.t = t;
   s.bootstrap = bootstrap ? 1 : 0;
+  if (r->centralized) {  // Env::world_state of the current states (ppo.cpp:341-346)
+    if (marl_venv_world_state(h, r->ws) != MARL_OK) raise(MARL_ERR_CUDA, marl_last_error());
+    s.ws = r->ws;
+  }
   s.legal_ready = (!bootstrap && e.family == MARL_FAMILY_SMAX) ? 1 : 0;
   if (s.legal_ready)  // Env::legal_actions straight into the buffer slice (team.cpp:35-42)
     smax_launch_legal(e.smax, h->smax, h->n, r->n_act, r->b.legal + size_t(t) * size_t(r->R) * r->n_act, h->stream);
@@ -955,13 +966,15 @@ void run_policy(marl_rollout* r, int t, bool bootstrap, int64_t seq_base) {
 
 extern "C" {
 
-int marl_rollout_policy_spec(const marl_venv* h, int width, int n_layers, int relu, marl_policy_spec* out) {
+int marl_rollout_policy_spec(const marl_venv* h, int width, int n_layers, int relu, int centralized,
+                             marl_policy_spec* out) {
   return guarded([&] {
     if (!h || !out) raise(MARL_ERR_CONTRACT, "marl_rollout_policy_spec: NULL argument");
     if (n_layers != 2) raise(MARL_ERR_SCHEMA, "rollout: the B200 policy kernels implement n_fc_layers = 2");
     if (width < 1 || width > 64) raise(MARL_ERR_SCHEMA, "rollout: fc_width must be in [1, 64]");
     *out = marl_policy_spec{};
-    policy_dims(*h->env, width, &out->in_dim, &out->n_actions, &out->n_actor_params, &out->n_critic_params);
+    policy_dims(h, width, centralized, &out->in_dim, &out->critic_in, &out->n_actions, &out->n_actor_params,
+                &out->n_critic_params);
     out->width = width;
     out->n_layers = n_layers;
     out->relu = relu;
@@ -969,12 +982,17 @@ int marl_rollout_policy_spec(const marl_venv* h, int width, int n_layers, int re
   });
 }
 
-int marl_rollout_create(marl_venv* h, int T, int width, int n_layers, int relu, int precision, marl_rollout** out) {
+int marl_rollout_create(marl_venv* h, int T, int width, int n_layers, int relu, int centralized, int precision,
+                        marl_rollout** out) {
   return guarded([&] {
     if (!h || !out) raise(MARL_ERR_CONTRACT, "marl_rollout_create: NULL argument");
     if (T < 1) raise(MARL_ERR_CONTRACT, "rollout: n_rollout_steps must be >= 1");
     marl_policy_spec ps{};
-    if (marl_rollout_policy_spec(h, width, n_layers, relu, &ps) != MARL_OK) raise(MARL_ERR_SCHEMA, marl_last_error());
+    if (marl_rollout_policy_spec(h, width, n_layers, relu, centralized, &ps) != MARL_OK)
+      raise(MARL_ERR_SCHEMA, marl_last_error());
+    if (centralized && precision == 1)
+      raise(MARL_ERR_SCHEMA, "rollout: the tcgen05 bf16 policy serves IPPO; use precision 0 for MAPPO");
+    if (ps.critic_in > 1024) raise(MARL_ERR_SCHEMA, "rollout: critic input wider than 1024");
     if (ps.in_dim > 1024 || ps.n_actions > 64) raise(MARL_ERR_SCHEMA, "rollout: input wider than 1024 or > 64 actions");
     if (precision == 1 && !rollout_policy_bf16_supported(ps.in_dim, ps.n_actions, width))
       raise(MARL_ERR_SCHEMA, "rollout: the tcgen05 bf16 policy needs in_dim <= 32, n_actions <= 16, fc_width == 64");
@@ -988,6 +1006,8 @@ int marl_rollout_create(marl_venv* h, int T, int width, int n_layers, int relu, 
     r->row0 = h->off * e.A;
     r->R_global = h->gn * e.A;
     r->in_dim = ps.in_dim;
+    r->critic_in = ps.critic_in;
+    r->centralized = centralized ? 1 : 0;
     r->n_act = ps.n_actions;
     r->width = width;
     r->relu = relu;
@@ -1010,6 +1030,10 @@ int marl_rollout_create(marl_venv* h, int T, int width, int n_layers, int relu, 
     ar.add(&r->b.adv, TR);
     ar.add(&r->b.vtarg, TR);
     ar.add(&r->b.last_value, size_t(r->R));
+    if (r->centralized) {
+      ar.add(&r->b.critic_in, TR * size_t(r->critic_in));
+      ar.add(&r->ws, size_t(h->n) * size_t(r->critic_in));
+    }
     ar.add(&r->params, size_t(r->n_actor + r->n_critic));
     ar.add(&r->images, size_t(128 * 32 + 2 * 64 * 64 + 2 * 16 * 64));
     ar.add(&r->bias, size_t(4 * 64 + 2 * 16));
@@ -1087,6 +1111,8 @@ int marl_rollout_get_views(marl_rollout* r, marl_rollout_views* o) {
     o->adv = r->b.adv;
     o->vtarg = r->b.vtarg;
     o->last_value = r->b.last_value;
+    o->critic_in = r->b.critic_in;
+    o->critic_dim = r->critic_in;
     o->T = r->T;
     o->R = r->R;
     o->in_dim = r->in_dim;

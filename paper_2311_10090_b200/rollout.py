@@ -24,10 +24,12 @@ from .venv import VectorEnv, _DevArray, _key_arr, _u32p
 _PREC = {"fp32": 0, "bf16": 1}
 
 
-def policy_spec(venv: VectorEnv, fc_width: int = 64, n_fc_layers: int = 2, activation: str = "tanh") -> N.PolicySpec:
-    """ppo_net_spec(env, cfg, false) (ppo.cpp:80-107)."""
+def policy_spec(venv: VectorEnv, fc_width: int = 64, n_fc_layers: int = 2, activation: str = "tanh",
+                centralized: bool = False) -> N.PolicySpec:
+    """ppo_net_spec(env, cfg, centralized) (ppo.cpp:80-107)."""
     ps = N.PolicySpec()
-    N.check(N.lib().marl_rollout_policy_spec(venv._h, fc_width, n_fc_layers, int(activation == "relu"), C.byref(ps)))
+    N.check(N.lib().marl_rollout_policy_spec(venv._h, fc_width, n_fc_layers, int(activation == "relu"),
+                                             int(centralized), C.byref(ps)))
     return ps
 
 
@@ -53,32 +55,44 @@ def orthogonal_init(key_seed: int, spec: N.PolicySpec):
                  orth(out, W, head_gain), np.zeros(out, np.float32)]
         return np.concatenate([p.ravel() for p in parts]).astype(np.float32)
 
-    return branch(spec.n_actions, 0.01), branch(1, 1.0)
+    def critic():
+        W = spec.width
+        parts = [orth(W, spec.critic_in, np.sqrt(2)), np.zeros(W, np.float32),
+                 orth(W, W, np.sqrt(2)), np.zeros(W, np.float32), orth(1, W, 1.0), np.zeros(1, np.float32)]
+        return np.concatenate([p.ravel() for p in parts]).astype(np.float32)
+
+    return branch(spec.n_actions, 0.01), critic()
 
 
 class IppoRollout:
     """Device rollout buffer + collector over one VectorEnv (or shard)."""
 
     FIELDS = {"obs": "<f4", "actions": "<i4", "rewards": "<f4", "dones": "|u1", "resets": "|u1", "logp": "<f4",
-              "value": "<f4", "legal": "|u1", "active": "<f4", "adv": "<f4", "vtarg": "<f4", "last_value": "<f4"}
+              "value": "<f4", "legal": "|u1", "active": "<f4", "adv": "<f4", "vtarg": "<f4", "last_value": "<f4",
+              "critic_in": "<f4"}
 
     def __init__(self, venv: VectorEnv, n_rollout_steps: int, fc_width: int = 64, n_fc_layers: int = 2,
-                 activation: str = "tanh", precision: str = "fp32"):
+                 activation: str = "tanh", precision: str = "fp32", centralized: bool = False):
+        """centralized=True is train_mappo's collector: the critic reads
+        Env::world_state (ppo.cpp:341-346) instead of the agent's row."""
         import torch
         self._torch = torch
         self.venv = venv
-        self.spec = policy_spec(venv, fc_width, n_fc_layers, activation)
+        self.spec = policy_spec(venv, fc_width, n_fc_layers, activation, centralized)
         h = C.c_void_p()
         N.check(N.lib().marl_rollout_create(venv._h, n_rollout_steps, fc_width, n_fc_layers,
-                                            int(activation == "relu"), _PREC[precision], C.byref(h)))
+                                            int(activation == "relu"), int(centralized), _PREC[precision],
+                                            C.byref(h)))
         self._h = h
         v = N.RolloutViews()
         N.check(N.lib().marl_rollout_get_views(self._h, C.byref(v)))
         self.T, self.R = int(v.T), int(v.R)
         shapes = {"obs": (self.T, self.R, self.spec.in_dim), "legal": (self.T, self.R, self.spec.n_actions),
-                  "last_value": (self.R,)}
+                  "last_value": (self.R,), "critic_in": (self.T, self.R, int(v.critic_dim))}
         self._views = {}
         for name, ts in self.FIELDS.items():
+            if name == "critic_in" and not v.critic_in:
+                continue
             shape = shapes.get(name, (self.T, self.R))
             self._views[name] = torch.as_tensor(_DevArray(getattr(v, name), shape, ts), device=f"cuda:{venv._device}")
 

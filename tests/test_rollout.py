@@ -140,3 +140,32 @@ def test_rollout_ragged_rows(precision, n):
     else:
         assert np.allclose(got["value"][0], ref["value"][0], rtol=0.05, atol=0.03)
         assert np.array_equal(got["vtarg"], got["adv"] + got["value"])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("env_id,cfg,n,T", [("MPE_simple_spread_v3", {}, 24, 30), ("SMAX_5m_vs_6m", THREE_M, 16, 24),
+                                            ("overcooked_cramped_room_v0", {"max_steps": 20}, 4, 24)])
+def test_mappo_rollout_matches_reference_collector(env_id, cfg, n, T):
+    """train_mappo's collector (centralized=true): the critic reads
+    Env::world_state (ppo.cpp:341-346); critic rows, values and GAE vs the
+    reference."""
+    _need_ref()
+    import paper_2311_10090_b200 as m
+    from paper_2311_10090_b200.rollout import IppoRollout
+    key = O.key_from_seed(17)
+    a, c = O.ref_ppo_init(env_id, cfg, O.fold_in(key, 10), centralized=True)
+    ref = O.ref_collect(env_id, cfg, n, T, key, a, c, centralized=True)
+    v = m.VectorEnv(m.make_env(env_id, cfg), n, device=0)
+    ro = IppoRollout(v, T, precision="fp32", centralized=True)
+    ro.set_params(a, c)
+    ro.begin(key)
+    got = {k: t.cpu().numpy() for k, t in ro.collect().items()}
+    for f in ("actions", "resets", "dones", "legal", "active"):
+        assert np.array_equal(got[f], ref[f]), f
+    if env_id.startswith("MPE"):
+        assert np.allclose(got["critic_in"], ref["critic_in"], rtol=1e-5, atol=1e-6)
+    else:
+        assert np.array_equal(got["critic_in"], ref["critic_in"])
+    for f in ("value", "adv", "vtarg"):
+        err = np.abs(got[f].astype(np.float64) - ref[f])
+        assert np.all(err <= 2e-6 + 2e-5 * np.abs(ref[f])), (f, err.max())
