@@ -208,6 +208,37 @@ __device__ __forceinline__ void patch_row(float* o, const Kitchen& s, const OcCo
   o[kPlanes * cells] = CLEAR ? 0.0f : float(s.t) / float(c.max_steps);
 }
 
+// The same cells as a list: emit(index in the row, value).  Used to build a
+// per-env patch list that the whole warp then applies.
+template <class F>
+__device__ __forceinline__ void patch_cells(const Kitchen& s, const OcConfig& c, int me, F&& emit) {
+  const int cells = c.h * c.w, other = 1 - me;
+  emit(0 * cells + s.pos[me], 1.0f);
+  emit(1 * cells + s.pos[other], 1.0f);
+  emit((2 + s.facing[me]) * cells + s.pos[me], 1.0f);
+  emit((6 + s.facing[other]) * cells + s.pos[other], 1.0f);
+  for (int p = 0; p < c.n_pots; ++p) {
+    const int cell = c.pot_cells[p];
+    emit(15 * cells + cell, float(s.onions[p]));
+    emit(16 * cells + cell, float(s.timer[p]) / float(c.cook_time));
+    if (s.onions[p] == 3 && s.timer[p] == 0) emit(17 * cells + cell, 1.0f);
+  }
+  if (s.held[me] != kNone) emit((18 + s.held[me] - 1) * cells + s.pos[me], 1.0f);
+  if (s.held[other] != kNone) emit((21 + s.held[other] - 1) * cells + s.pos[other], 1.0f);
+  for (int wd = 0; wd < 2; ++wd) {
+    const uint64_t w = s.counters[wd];
+    for (uint64_t occ = (w | (w >> 1)) & 0x5555555555555555ull; occ; occ &= occ - 1) {
+      const int bit = __ffsll((long long)occ) - 1;
+      const int item = int((w >> bit) & 3u);
+      emit((24 + item - 1) * cells + c.counter_cells[wd * 32 + (bit >> 1)], 1.0f);
+    }
+  }
+  emit(kPlanes * cells, float(s.t) / float(c.max_steps));
+}
+
+// Upper bound of patch entries for one env (both rows).
+__host__ __device__ inline int oc_max_patches(const OcConfig& c) { return 2 * (7 + 3 * c.n_pots + c.n_counters); }
+
 // ------------------------------------------------------------ row streaming
 // A warp's envs own a contiguous run of observation rows ([N][2][D] f32).
 // The static planes of every row are identical (the layout template), so the
@@ -291,8 +322,8 @@ __global__ void __launch_bounds__(kThreads) oc_reset_kernel(OcConfig c, const fl
 // write the template's zeros back into exactly the cells they patched.  No
 // row is ever copied through registers; the TMA engine streams 8.6 KB per
 // instruction while the warp steps the next pair.
-__host__ __device__ inline size_t oc_tma_smem_floats(int D, int warps) {
-  return 4 * tmpl_floats(D) + size_t(warps) * 2 * 4 * D;
+__host__ __device__ inline size_t oc_tma_smem_floats(int D, int warps, int max_patches) {
+  return 4 * tmpl_floats(D) + size_t(warps) * (2 * 4 * D + 32 * 2 * size_t(max_patches) + 32);
 }
 
 template <bool RANDOM>
@@ -303,7 +334,12 @@ __global__ void __launch_bounds__(kThreads) oc_step_kernel(OcConfig c, const flo
   const int D = kPlanes * c.h * c.w + 1;
   const Tmpl t = stage_template(smem, gtempl, D);
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, warps = blockDim.x >> 5;
-  float* bufs = smem + 4 * tmpl_floats(D) + size_t(wid) * 2 * 4 * D;
+  const int MP = oc_max_patches(c);
+  float* wbase = smem + 4 * tmpl_floats(D) + size_t(wid) * (2 * 4 * D + 32 * 2 * size_t(MP) + 32);
+  float* bufs = wbase;                                               // 2 x [4 rows][D]
+  uint32_t* p_idx = reinterpret_cast<uint32_t*>(wbase + 2 * 4 * D);  // [32][MP] row-relative cell (+ row * D)
+  float* p_val = wbase + 2 * 4 * D + 32 * size_t(MP);               // [32][MP]
+  int* p_n = reinterpret_cast<int*>(wbase + 2 * 4 * D + 64 * size_t(MP));  // [32]
   if (tma) {  // both buffers start as four template rows
     for (int idx = lane; idx < 2 * 4 * D; idx += 32) bufs[idx] = t.s[0][idx % D];
     __syncwarp();
@@ -368,19 +404,39 @@ __global__ void __launch_bounds__(kThreads) oc_step_kernel(OcConfig c, const flo
       }
     }
 
-    // observation rows
+    // observation rows: every lane lists its env's dynamic cells (both rows,
+    // index relative to the env's first row), then per pair of envs the whole
+    // warp writes the two lists into a 4-row template buffer (and, two rounds
+    // later, writes the template's zeros back), one lane issues the bulk store
     const int pairs = tma ? wvalid >> 1 : 0;
+    if (pairs > 0) {
+      if (mine) {
+        int k = 0;
+        for (int a = 0; a < 2; ++a)
+          patch_cells(s, c, a, [&](int idx, float v) {
+            p_idx[lane * MP + k] = uint32_t(a * D + idx);
+            p_val[lane * MP + k] = v;
+            ++k;
+          });
+        p_n[lane] = k;
+      }
+      __syncwarp();
+    }
     for (int p = 0; p < pairs; ++p) {
       float* buf = bufs + (p & 1) * 4 * D;
-      if (p >= 2) {  // the buffer's previous store must have read it; then undo that pair's cells
+      if (p >= 2) {  // the buffer's previous store must have read it; undo that pair's cells
         if (lane == 0) bulk_wait_read<1>();
         __syncwarp();
-        if ((lane >> 1) == p - 2)
-          for (int a = 0; a < 2; ++a) patch_row<true>(buf + ((lane & 1) * 2 + a) * D, s, c, a);
+        for (int e2 = 0; e2 < 2; ++e2) {
+          const int src = 2 * (p - 2) + e2;
+          for (int q = lane; q < p_n[src]; q += 32) buf[e2 * 2 * D + p_idx[src * MP + q]] = 0.0f;
+        }
         __syncwarp();
       }
-      if ((lane >> 1) == p)
-        for (int a = 0; a < 2; ++a) patch_row(buf + ((lane & 1) * 2 + a) * D, s, c, a);
+      for (int e2 = 0; e2 < 2; ++e2) {
+        const int src = 2 * p + e2;
+        for (int q = lane; q < p_n[src]; q += 32) buf[e2 * 2 * D + p_idx[src * MP + q]] = p_val[src * MP + q];
+      }
       fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) {
@@ -391,8 +447,13 @@ __global__ void __launch_bounds__(kThreads) oc_step_kernel(OcConfig c, const flo
     if (pairs > 0) {  // leave both buffers as clean template rows for the next chunk
       if (lane == 0) bulk_wait_read<0>();
       __syncwarp();
-      if ((lane >> 1) >= pairs - 2 && (lane >> 1) < pairs)
-        for (int a = 0; a < 2; ++a) patch_row<true>(bufs + ((lane >> 1) & 1) * 4 * D + ((lane & 1) * 2 + a) * D, s, c, a);
+      for (int p = pairs >= 2 ? pairs - 2 : 0; p < pairs; ++p) {
+        float* buf = bufs + (p & 1) * 4 * D;
+        for (int e2 = 0; e2 < 2; ++e2) {
+          const int src = 2 * p + e2;
+          for (int q = lane; q < p_n[src]; q += 32) buf[e2 * 2 * D + p_idx[src * MP + q]] = 0.0f;
+        }
+      }
       __syncwarp();
     }
     const int direct0 = 2 * pairs;  // envs not covered by a bulk store (odd tail / no TMA)
@@ -462,8 +523,9 @@ void oc_launch_step_t(const OcConfig& c, const float* templ, const OcState& s, c
     cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   }
   int warps = kThreads / 32, tma = 1;
-  while (warps > 1 && oc_tma_smem_floats(D, warps) * 4 > size_t(max_smem)) --warps;
-  size_t sm = oc_tma_smem_floats(D, warps) * 4;
+  const int mp = oc_max_patches(c);
+  while (warps > 1 && oc_tma_smem_floats(D, warps, mp) * 4 > size_t(max_smem)) --warps;
+  size_t sm = oc_tma_smem_floats(D, warps, mp) * 4;
   if (sm > size_t(max_smem)) {  // layout too large for the buffers: plain streaming stores
     tma = 0;
     warps = kThreads / 32;
