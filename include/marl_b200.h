@@ -250,6 +250,38 @@ int marl_rollout_collect(marl_rollout* r, int64_t seq_base, double gamma, double
 int marl_rollout_get_views(marl_rollout* r, marl_rollout_views* out);
 int marl_rollout_destroy(marl_rollout* r);
 
+/* ---------------------------------------------------------------- PPO update
+ * train_ippo / train_mappo (ppo.hpp:96-99, ppo.cpp:518-651) with the rollout
+ * above and the minibatch update on the device:
+ * PpoConfig JSON (ppo.cpp:38-62, same keys, defaults and SchemaErrors),
+ * ppo_init_nets (ppo.cpp:109-124), permutation minibatches (prng.cpp:151-159),
+ * ff_minibatch + ppo_row_loss + ff_backward (ppo.cpp:409-441,
+ * actor_critic.hpp:340-412), clip_global_norm + Adam (nn.hpp:417-452), the
+ * DivergenceError rollback (ppo.cpp:630-634) and the per-update metrics row.
+ * Feed-forward policies only (recurrent = true is a SchemaError). */
+typedef struct marl_ppo marl_ppo;
+/* n_envs in the config must equal the VectorEnv's env count. precision as marl_rollout_create. */
+int marl_ppo_create(marl_venv* h, const char* ppo_config_json, int centralized, int precision, marl_ppo** out);
+/* ppo_init_nets(key, spec) for a feed-forward spec into host arrays (no device needed) */
+int marl_ppo_init_nets(int in_dim, int critic_in, int n_actions, int fc_width, int n_fc_layers, const uint32_t key[4],
+                       float* actor, float* critic);
+int marl_ppo_begin(marl_ppo* p, const uint32_t key[4]);  /* nets fold_in(key,10), collector fold_in(key,11) */
+int marl_ppo_n_updates(const marl_ppo* p, int64_t* out);  /* total_timesteps / (n_envs * n_rollout_steps) */
+int marl_ppo_set_params(marl_ppo* p, const float* actor, const float* critic);
+int marl_ppo_get_params(marl_ppo* p, float* actor, float* critic);
+int marl_ppo_rollout(marl_ppo* p, marl_rollout** out);  /* borrowed: views of the current window */
+int marl_ppo_collect(marl_ppo* p);
+/* row[12] = {step, update, mean_return, n_episodes, loss, pg_loss, v_loss, entropy, approx_kl,
+ * clip_frac, grad_norm, lr} (ppo.cpp:524-527); diverged = 1 after a DivergenceError rollback. */
+int marl_ppo_update(marl_ppo* p, double row[12], int* diverged);
+int marl_ppo_step(marl_ppo* p, double row[12], int* diverged);  /* collect + update */
+/* ff_minibatch's gradient (actor | critic, nn::pack order) and {loss, pg, v, entropy, kl, clip_frac}
+ * for device slot indices d_idx[M] over the current window, no optimizer step. */
+int marl_ppo_minibatch_grad(marl_ppo* p, const int32_t* d_idx, int64_t M, float* grad_out, double* stats_out);
+int marl_ppo_destroy(marl_ppo* p);
+/* prng::permutation(key, n) (prng.cpp:151-159) into device memory d_out[n] on `device`. */
+int marl_ppo_permutation(const uint32_t key[4], int64_t n, int32_t* d_out, int device);
+
 /* ---- the reference's own benchmark --------------------------------------- */
 
 /* throughput_probe(env_id, n_envs, n_steps, key, config) (vector_env.cpp:

@@ -372,6 +372,12 @@ def ref_lib():
                                    _f32p, _f32p,
                                    C.c_double, C.c_double, C.c_double, _f32p, _i32p, _f32p, _u8p, _u8p, _f32p,
                                    _f32p, _u8p, _f32p, _f32p, _f32p, _f64p, _P(C.c_int64)]
+        L.mref_permutation.argtypes = [_u32p, C.c_int, _i32p]
+        L.mref_ff_minibatch.argtypes = [C.c_char_p, C.c_char_p, C.c_int, _f32p, _f32p, _f32p, _f32p, _i32p, _f32p,
+                                        _f32p, _f32p, _f32p, _f32p, _u8p, _i32p, C.c_int, C.c_double, C.c_double,
+                                        C.c_double, _f32p, _f64p]
+        L.mref_train.argtypes = [C.c_char_p, C.c_char_p, C.c_char_p, C.c_int, _u32p, _f64p, C.c_int,
+                                 _P(C.c_int), _f32p, _f32p, _P(C.c_int), _P(C.c_int64)]
         _ref = L
     return _ref
 
@@ -526,3 +532,58 @@ def ref_collect(env_id, config, n_envs, T, key, actor, critic, n_windows=1, gamm
     out["episode_return_sum"] = ep_sum.value
     out["episodes"] = eps.value
     return out
+
+
+# ------------------------------------------------------------- PPO update
+PPO_COLUMNS = ["step", "update", "mean_return", "n_episodes", "loss", "pg_loss", "v_loss", "entropy", "approx_kl",
+               "clip_frac", "grad_norm", "lr"]
+
+
+def ref_permutation(key, n):
+    """prng::permutation(key, n) (prng.cpp:151-159)."""
+    L = ref_lib()
+    out = np.zeros(max(n, 1), np.int32)
+    rc = L.mref_permutation(_ptr(_key(key), C.c_uint32), int(n), _ptr(out, C.c_int32))
+    if rc:
+        raise RuntimeError(L.mref_rollout_last_error().decode())
+    return out[:n]
+
+
+def ref_ff_minibatch(env_id, config, actor, critic, buf, idx, clip_eps=0.3, ent_coef=0.01, vf_coef=1.0,
+                     centralized=False):
+    """ff_minibatch (ppo.cpp:409-441) over a [T][R] buffer dict -> (flat grad, stats[6])."""
+    L = ref_lib()
+    sp = ref_ppo_spec(env_id, config, centralized)
+    g = np.zeros(sp["n_actor"] + sp["n_critic"], np.float32)
+    st = np.zeros(6, np.float64)
+    f = {k: np.ascontiguousarray(buf[k]) for k in ("obs", "actions", "logp", "adv", "vtarg", "value", "active",
+                                                    "legal")}
+    ci = np.ascontiguousarray(buf.get("critic_in", f["obs"]), np.float32)
+    ix = np.ascontiguousarray(idx, np.int32)
+    a = np.ascontiguousarray(actor, np.float32)
+    c = np.ascontiguousarray(critic, np.float32)
+    rc = L.mref_ff_minibatch(env_id.encode(), json.dumps(config or {}).encode(), int(centralized),
+                             _ptr(a, C.c_float), _ptr(c, C.c_float), _ptr(f["obs"], C.c_float), _ptr(ci, C.c_float),
+                             _ptr(f["actions"], C.c_int32), _ptr(f["logp"], C.c_float), _ptr(f["adv"], C.c_float),
+                             _ptr(f["vtarg"], C.c_float), _ptr(f["value"], C.c_float), _ptr(f["active"], C.c_float),
+                             _ptr(f["legal"], C.c_uint8), _ptr(ix, C.c_int32), len(ix), clip_eps, ent_coef, vf_coef,
+                             _ptr(g, C.c_float), _ptr(st, C.c_double))
+    if rc:
+        raise RuntimeError(L.mref_rollout_last_error().decode())
+    return g, st
+
+
+def ref_train(env_id, config, ppo_config, key, centralized=False, max_rows=4096):
+    """The reference's train_ippo / train_mappo (ppo.cpp:518-651)."""
+    L = ref_lib()
+    sp = ref_ppo_spec(env_id, config, centralized)
+    m = np.zeros((max_rows, 12), np.float64)
+    a = np.zeros(sp["n_actor"], np.float32)
+    c = np.zeros(sp["n_critic"], np.float32)
+    nr, dv, sd = C.c_int(), C.c_int(), C.c_int64()
+    rc = L.mref_train(env_id.encode(), json.dumps(config or {}).encode(), json.dumps(ppo_config).encode(),
+                      int(centralized), _ptr(_key(key), C.c_uint32), _ptr(m, C.c_double), max_rows, C.byref(nr),
+                      _ptr(a, C.c_float), _ptr(c, C.c_float), C.byref(dv), C.byref(sd))
+    if rc:
+        raise RuntimeError(L.mref_rollout_last_error().decode())
+    return {"metrics": m[:nr.value], "actor": a, "critic": c, "diverged": bool(dv.value), "steps_done": sd.value}

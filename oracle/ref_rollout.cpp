@@ -229,4 +229,104 @@ int mref_collect(const char* env_id, const char* cfg, int centralized, float* o_
   });
 }
 
+// ---------------------------------------------------------------- PPO update
+// prng::permutation(key, n) (prng.cpp:151-159): the reference's Fisher-Yates.
+int mref_permutation(const uint32_t key[4], int n, int32_t* out) {
+  return guarded([&] {
+    auto p = prng::permutation(key_of(key), n);
+    std::memcpy(out, p.data(), p.size() * sizeof(int32_t));
+  });
+}
+
+// ff_minibatch (ppo.cpp:409-441) + gather_rows (ppo.cpp:382-406), which are
+// private to ppo.cpp, restated over the reference's public pieces:
+// nn::normalize_advantages, nn::ff_forward, nn::ppo_row_loss, nn::ff_backward,
+// nn::pack.  Inputs are a [T][R] rollout buffer (the flat slot s = t*R + r);
+// out: the flat gradient (actor then critic) and {loss, pg, v, entropy, kl,
+// clip_frac}.
+int mref_ff_minibatch(const char* env_id, const char* cfg, int centralized, const float* actor, const float* critic,
+                      const float* obs, const float* critic_in, const int32_t* actions, const float* logp,
+                      const float* adv, const float* vtarg, const float* value, const float* active,
+                      const uint8_t* legal, const int32_t* idx, int M, double clip_eps, double ent_coef,
+                      double vf_coef, float* grad_out, double* stats_out) {
+  return guarded([&] {
+    auto env = make_env(env_id, parse(cfg));
+    const PpoNetSpec spec = spec_for(*env, centralized);
+    PpoNets nets = ppo_init_nets(prng::key_from_seed(0), spec);
+    {
+      auto a = nets.pack_actor(), c = nets.pack_critic();
+      nets.unpack_actor(std::vector<float>(actor, actor + a.size()));
+      nets.unpack_critic(std::vector<float>(critic, critic + c.size()));
+    }
+    const int in = spec.in_dim, cin = spec.critic_in, na = spec.n_actions;
+    const size_t m = size_t(M);
+    nn::Mat<float> x(M, in), xc(M, cin);
+    nn::PpoRows<float> rows;
+    rows.n_actions = na;
+    rows.actions.resize(m);
+    rows.old_log_probs.resize(m);
+    rows.advantages.resize(m);
+    rows.value_targets.resize(m);
+    rows.old_values.resize(m);
+    rows.legal.resize(m * size_t(na));
+    rows.weights.resize(m);
+    for (size_t i = 0; i < m; ++i) {
+      const size_t s = size_t(idx[i]);
+      std::memcpy(&x.a[i * size_t(in)], obs + s * size_t(in), size_t(in) * sizeof(float));
+      const float* xs = centralized ? critic_in + s * size_t(cin) : obs + s * size_t(in);
+      std::memcpy(&xc.a[i * size_t(cin)], xs, size_t(cin) * sizeof(float));
+      rows.actions[i] = actions[s];
+      rows.old_log_probs[i] = logp[s];
+      rows.advantages[i] = adv[s];
+      rows.value_targets[i] = vtarg[s];
+      rows.old_values[i] = value[s];
+      rows.weights[i] = active[s];
+      std::memcpy(&rows.legal[i * size_t(na)], legal + s * size_t(na), size_t(na));
+    }
+    nn::normalize_advantages(rows.advantages, rows.weights);
+    nn::FfCache<float> ac, cc;
+    auto logits = nn::ff_forward(nets.actor_ff, x, spec.act, &ac);
+    auto vmat = nn::ff_forward(nets.critic_ff, xc, spec.act, &cc);
+    std::vector<float> values(m);
+    for (size_t i = 0; i < m; ++i) values[i] = vmat(int(i), 0);
+    nn::PpoLossConfig lcfg{clip_eps, ent_coef, vf_coef};
+    auto loss = nn::ppo_row_loss(logits, values, rows, lcfg);
+    auto ga = nn::ff_backward(nets.actor_ff, ac, spec.act, loss.dlogits);
+    nn::Mat<float> dv(M, 1);
+    for (size_t i = 0; i < m; ++i) dv(int(i), 0) = loss.dvalues[i];
+    auto gc = nn::ff_backward(nets.critic_ff, cc, spec.act, dv);
+    std::vector<float> flat;
+    nn::pack(ga, flat);
+    nn::pack(gc, flat);
+    std::memcpy(grad_out, flat.data(), flat.size() * sizeof(float));
+    stats_out[0] = double(loss.loss);
+    stats_out[1] = loss.pg_loss;
+    stats_out[2] = loss.v_loss;
+    stats_out[3] = loss.entropy;
+    stats_out[4] = loss.approx_kl;
+    stats_out[5] = loss.clip_frac;
+  });
+}
+
+// The reference's own public trainer: train_ippo / train_mappo (ppo.cpp:518-651)
+// with PpoConfig::from_config.  metrics: rows x 12 (ppo.cpp:524-527 columns).
+int mref_train(const char* env_id, const char* cfg, const char* ppo_cfg, int centralized, const uint32_t key[4],
+               double* metrics, int max_rows, int* n_rows, float* actor, float* critic, int* diverged,
+               int64_t* steps_done) {
+  return guarded([&] {
+    auto env = make_env(env_id, parse(cfg));
+    PpoConfig pc = PpoConfig::from_config(parse(ppo_cfg));
+    PpoRunResult res = centralized ? train_mappo(env, pc, key_of(key)) : train_ippo(env, pc, key_of(key));
+    const auto& rows = res.metrics.rows;
+    *n_rows = int(rows.size());
+    for (size_t r = 0; r < rows.size() && int(r) < max_rows; ++r)
+      for (size_t c = 0; c < rows[r].size(); ++c) metrics[r * rows[r].size() + c] = rows[r][c];
+    auto a = res.nets.pack_actor(), c = res.nets.pack_critic();
+    std::memcpy(actor, a.data(), a.size() * sizeof(float));
+    std::memcpy(critic, c.data(), c.size() * sizeof(float));
+    *diverged = res.diverged ? 1 : 0;
+    *steps_done = res.steps_done;
+  });
+}
+
 }  // extern "C"

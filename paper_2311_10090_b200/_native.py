@@ -58,6 +58,9 @@ EXPORTS = [
     "marl_venv_world_state_size", "marl_venv_world_state",
     "marl_rollout_policy_spec", "marl_rollout_create", "marl_rollout_set_params", "marl_rollout_begin",
     "marl_rollout_collect", "marl_rollout_get_views", "marl_rollout_destroy",
+    "marl_ppo_create", "marl_ppo_init_nets", "marl_ppo_begin", "marl_ppo_n_updates", "marl_ppo_set_params",
+    "marl_ppo_get_params", "marl_ppo_rollout", "marl_ppo_collect", "marl_ppo_update", "marl_ppo_step",
+    "marl_ppo_minibatch_grad", "marl_ppo_destroy", "marl_ppo_permutation",
 ]
 
 _lib = None
@@ -114,6 +117,20 @@ def lib() -> C.CDLL:
     L.marl_rollout_collect.argtypes = [vp, C.c_int64, C.c_double, C.c_double, C.c_double]
     L.marl_rollout_get_views.argtypes = [vp, C.POINTER(RolloutViews)]
     L.marl_rollout_destroy.argtypes = [vp]
+    f32p, f64p = C.POINTER(C.c_float), C.POINTER(C.c_double)
+    L.marl_ppo_create.argtypes = [vp, C.c_char_p, C.c_int, C.c_int, C.POINTER(vp)]
+    L.marl_ppo_init_nets.argtypes = [C.c_int] * 5 + [u32p, f32p, f32p]
+    L.marl_ppo_begin.argtypes = [vp, u32p]
+    L.marl_ppo_n_updates.argtypes = [vp, i64p]
+    L.marl_ppo_set_params.argtypes = [vp, f32p, f32p]
+    L.marl_ppo_get_params.argtypes = [vp, f32p, f32p]
+    L.marl_ppo_rollout.argtypes = [vp, C.POINTER(vp)]
+    L.marl_ppo_collect.argtypes = [vp]
+    L.marl_ppo_update.argtypes = [vp, f64p, C.POINTER(C.c_int)]
+    L.marl_ppo_step.argtypes = [vp, f64p, C.POINTER(C.c_int)]
+    L.marl_ppo_minibatch_grad.argtypes = [vp, vp, C.c_int64, f32p, f64p]
+    L.marl_ppo_destroy.argtypes = [vp]
+    L.marl_ppo_permutation.argtypes = [u32p, C.c_int64, vp, C.c_int]
     L.marl_last_error.restype = C.c_char_p
     L.marl_launch_count.restype = C.c_uint64
     L.marl_version.restype = C.c_char_p

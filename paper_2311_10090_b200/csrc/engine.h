@@ -220,6 +220,55 @@ void smax_launch_world_state(const SmaxConfig& c, const SmaxState& s, int64_t n,
 void launch_obs_gather(const float* obs, int64_t n, int row_floats, const int32_t* seg_src, const int32_t* seg_len,
                        int n_seg, int width, float* out, cudaStream_t st);
 
+// ------------------------------------------------------------ PPO update
+// train_ppo_impl's minibatch loop (ppo.cpp:588-628) over a RolloutBufs.
+constexpr int kPpoMaxAct = 64;
+
+struct PpoMbStats {  // normalize_advantages over one minibatch (actor_critic.hpp:416-433)
+  double mean, std, total_w;
+  int normalize;
+};
+
+struct PpoBranchArgs {  // one branch (actor or critic) of one minibatch
+  const float* params;   // the branch's packed parameters (nn::pack order)
+  float* gpart;          // [grid][P] per-CTA gradient partials
+  double* spart;         // [grid][6] per-CTA loss sums
+  const int32_t* idx;    // minibatch slots (t*R + r)
+  int64_t M;
+  const float* x;        // input rows: obs (actor, IPPO critic) or critic_in (MAPPO critic)
+  const int32_t* actions;
+  const float *old_logp, *adv, *vtarg, *old_value, *active;
+  const uint8_t* legal;
+  const PpoMbStats* st;
+  int* err;              // stored action illegal -> ContractError (actor_critic.hpp:366)
+  int in, W, out, relu, TR, staged;
+  double clip_eps, ent_coef, vf_coef;
+};
+
+struct PpoApplyArgs {
+  float *params, *grad, *m, *v;  // whole flat vector: actor | critic
+  int P;
+  const double *actor_stats, *critic_stats;
+  int n_actor_parts, n_critic_parts;
+  const PpoMbStats* st;
+  double vf_coef, ent_coef;
+  float max_norm, lr, beta1, beta2, eps, c1, c2;
+  double* metrics;   // [8]: loss, pg, v, entropy, kl, clip_frac, grad_norm, counted
+  int* diverged;     // sticky DivergenceError flag
+};
+
+size_t ppo_perm_scratch_bytes(int64_t n);
+// prng::permutation(key, n) (prng.cpp:151-159) into out[n] on the device.
+void ppo_permutation(KeyWords key, int64_t n, int32_t* out, void* scratch, size_t scratch_bytes, cudaStream_t st);
+int ppo_stat_blocks(int64_t M);
+void ppo_adv_stats(const RolloutBufs& b, const int32_t* idx, int64_t M, double* part, double* part2, PpoMbStats* st,
+                   cudaStream_t s);
+void ppo_branch_geometry(int in, int W, int out, int* TR, int* staged, size_t* smem);
+int ppo_branch_grid(int in, int W, int out, int64_t M);
+void ppo_branch(PpoBranchArgs a, bool actor, int grid, cudaStream_t s);
+void ppo_grad_reduce(const float* part, int nparts, int P, float* grad, cudaStream_t s);
+void ppo_clip_adam(const PpoApplyArgs& a, cudaStream_t s);
+
 // ------------------------------------------------------------ common
 // Device-side Env::validate_actions (env.cpp:7-14): n_actions per agent.
 void launch_validate(const int32_t* actions, int64_t n, int A, const int32_t* n_actions_dev,

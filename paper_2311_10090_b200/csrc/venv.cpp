@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -66,6 +67,13 @@ class ConfigView {
     if (!cfg_.is_object() && !cfg_.is_null()) raise(MARL_ERR_SCHEMA, ctx_ + ": expected a JSON object");
   }
   bool has(const std::string& k) const { return cfg_.is_object() && cfg_.contains(k); }
+  int64_t get_int64(const std::string& k, int64_t dflt) {
+    seen_.insert(k);
+    if (!has(k)) return dflt;
+    const json& v = cfg_.at(k);
+    if (!v.is_number_integer() && !v.is_number_unsigned()) bad(k, "integer");
+    return v.get<int64_t>();
+  }
   int get_int(const std::string& k, int dflt) {
     seen_.insert(k);
     if (!has(k)) return dflt;
@@ -1073,26 +1081,40 @@ int marl_rollout_begin(marl_rollout* r, const uint32_t key[4]) {
   });
 }
 
-// Collector::collect(nets, T, seq_base, shaping) (ppo.cpp:206-323).
+}  // extern "C"
+
+extern "C++" {
+namespace {
+// Collector::collect(nets, T, seq_base, shaping_at) (ppo.cpp:206-323);
+// shaping(seq) is the annealed shaped-reward weight of batch step seq.
+template <class Shaping>
+void collect_impl(marl_rollout* r, int64_t seq_base, double gamma, double lambda, Shaping shaping) {
+  if (!r->begun) raise(MARL_ERR_CONTRACT, "rollout: call begin() before collect()");
+  if (!r->has_params) raise(MARL_ERR_CONTRACT, "rollout: call set_params() before collect()");
+  marl_venv* h = r->h;
+  set_device(h);
+  const Env& e = *h->env;
+  for (int t = 0; t < r->T; ++t) {
+    run_policy(r, t, false, seq_base);
+    launch_step(h, false, nullptr, r->b.actions + size_t(t) * size_t(r->R));
+    rollout_record(r->b, t, r->R, e.A, h->v.rewards, h->v.infos, e.n_info, r->shaped_idx, shaping(seq_base + t),
+                   h->v.finished, h->stream);
+    after_launch();
+    r->first = false;
+  }
+  run_policy(r, r->T, true, seq_base);  // bootstrap values (ppo.cpp:285-299)
+  rollout_gae(r->b, r->T, r->R, float(gamma), float(lambda), h->stream);
+  after_launch();
+}
+}  // namespace
+}  // extern "C++"
+
+extern "C" {
+
 int marl_rollout_collect(marl_rollout* r, int64_t seq_base, double gamma, double lambda, double shaping) {
   return guarded([&] {
     if (!r) raise(MARL_ERR_CONTRACT, "marl_rollout_collect: NULL rollout");
-    if (!r->begun) raise(MARL_ERR_CONTRACT, "rollout: call begin() before collect()");
-    if (!r->has_params) raise(MARL_ERR_CONTRACT, "rollout: call set_params() before collect()");
-    marl_venv* h = r->h;
-    set_device(h);
-    const Env& e = *h->env;
-    for (int t = 0; t < r->T; ++t) {
-      run_policy(r, t, false, seq_base);
-      launch_step(h, false, nullptr, r->b.actions + size_t(t) * size_t(r->R));
-      rollout_record(r->b, t, r->R, e.A, h->v.rewards, h->v.infos, e.n_info, r->shaped_idx, shaping,
-                     h->v.finished, h->stream);
-      after_launch();
-      r->first = false;
-    }
-    run_policy(r, r->T, true, seq_base);  // bootstrap values (ppo.cpp:285-299)
-    rollout_gae(r->b, r->T, r->R, float(gamma), float(lambda), h->stream);
-    after_launch();
+    collect_impl(r, seq_base, gamma, lambda, [shaping](int64_t) { return shaping; });
   });
 }
 
@@ -1255,6 +1277,546 @@ uint64_t marl_prng_bits(const uint32_t key[4], uint64_t index) {
 }
 void marl_threefry2x32(uint32_t k0, uint32_t k1, uint32_t x0, uint32_t x1, uint32_t out[2]) {
   threefry2x32(k0, k1, x0, x1, out[0], out[1]);
+}
+
+}  // extern "C"
+
+// ====================================================================== PPO
+// train_ippo / train_mappo (ppo.cpp:518-651) around the device update
+// (ppo.cu): PpoConfig::from_config + validate (ppo.cpp:18-62), ppo_init_nets
+// (ppo.cpp:109-124) on the host, and the update loop with its metrics row.
+namespace {
+
+struct PpoCfg {  // PpoConfig (ppo.hpp:30-55) with its defaults
+  int64_t total_timesteps = 1000000;
+  int n_envs = 16, n_rollout_steps = 128;
+  double lr = 5e-4;
+  bool anneal_lr = true;
+  int update_epochs = 5, n_minibatches = 2;
+  double gamma = 0.99, gae_lambda = 1.0, clip_eps = 0.3, ent_coef = 0.01, vf_coef = 1.0, max_grad_norm = 0.5;
+  std::string activation = "tanh";
+  bool recurrent = false;
+  int n_fc_layers = 2, fc_width = 64, hidden_width = 128;
+  bool shaped_rewards = true;
+};
+
+PpoCfg parse_ppo_config(const char* text) {
+  json j = (text && *text) ? json::parse(text) : json::object();
+  ConfigView v(j, "ppo config");
+  PpoCfg c;
+  c.total_timesteps = v.get_int64("total_timesteps", c.total_timesteps);
+  c.n_envs = v.get_int("n_envs", c.n_envs);
+  c.n_rollout_steps = v.get_int("n_rollout_steps", c.n_rollout_steps);
+  c.lr = v.get_double("lr", c.lr);
+  c.anneal_lr = v.get_bool("anneal_lr", c.anneal_lr);
+  c.update_epochs = v.get_int("update_epochs", c.update_epochs);
+  c.n_minibatches = v.get_int("n_minibatches", c.n_minibatches);
+  c.gamma = v.get_double("gamma", c.gamma);
+  c.gae_lambda = v.get_double("gae_lambda", c.gae_lambda);
+  c.clip_eps = v.get_double("clip_eps", c.clip_eps);
+  c.ent_coef = v.get_double("ent_coef", c.ent_coef);
+  c.vf_coef = v.get_double("vf_coef", c.vf_coef);
+  c.max_grad_norm = v.get_double("max_grad_norm", c.max_grad_norm);
+  c.activation = v.get_string("activation", c.activation);
+  c.recurrent = v.get_bool("recurrent", c.recurrent);
+  c.n_fc_layers = v.get_int("n_fc_layers", c.n_fc_layers);
+  c.fc_width = v.get_int("fc_width", c.fc_width);
+  c.hidden_width = v.get_int("hidden_width", c.hidden_width);
+  c.shaped_rewards = v.get_bool("shaped_rewards", c.shaped_rewards);
+  v.check_no_extras();
+  auto bad = [](const std::string& what) { raise(MARL_ERR_SCHEMA, "ppo config: " + what); };
+  if (c.total_timesteps < 0) bad("total_timesteps must be >= 0");
+  if (c.n_envs <= 0) bad("n_envs must be positive");
+  if (c.n_rollout_steps <= 0) bad("n_rollout_steps must be positive");
+  if (c.lr <= 0) bad("lr must be positive");
+  if (c.update_epochs <= 0) bad("update_epochs must be positive");
+  if (c.n_minibatches <= 0) bad("n_minibatches must be positive");
+  if (c.gamma < 0 || c.gamma > 1) bad("gamma must lie in [0, 1]");
+  if (c.gae_lambda < 0 || c.gae_lambda > 1) bad("gae_lambda must lie in [0, 1]");
+  if (c.clip_eps <= 0 || c.clip_eps >= 1) bad("clip_eps must lie in (0, 1)");
+  if (c.ent_coef < 0) bad("ent_coef must be >= 0");
+  if (c.vf_coef < 0) bad("vf_coef must be >= 0");
+  if (c.max_grad_norm <= 0) bad("max_grad_norm must be positive");
+  if (c.activation != "tanh" && c.activation != "relu") bad("activation must be 'tanh' or 'relu'");
+  if (c.n_fc_layers <= 0) bad("n_fc_layers must be positive");
+  if (c.fc_width <= 0) bad("fc_width must be positive");
+  if (c.hidden_width <= 0) bad("hidden_width must be positive");
+  return c;
+}
+
+Key key4(const uint32_t k[4]) { return Key{k[0], k[1], k[2], k[3]}; }
+void put_key(const Key& k, uint32_t out[4]) {
+  out[0] = k.k0;
+  out[1] = k.k1;
+  out[2] = k.c0;
+  out[3] = k.c1;
+}
+
+// prng::normal (prng.cpp:161-175): Box-Muller over the key's blocks.
+std::vector<double> host_normal(const Key& key, size_t n) {
+  constexpr double kPi = 3.14159265358979323846;  // std::numbers::pi
+  std::vector<double> out(n);
+  const size_t pairs = (n + 1) / 2;
+  for (size_t p = 0; p < pairs; ++p) {
+    const double u1 = double((block_at(key, 2 * p) >> 11) + 1) * 0x1.0p-53;
+    const double u2 = to_unit(block_at(key, 2 * p + 1));
+    const double r = std::sqrt(-2.0 * std::log(u1));
+    const double theta = 2.0 * kPi * u2;
+    out[2 * p] = r * std::cos(theta);
+    if (2 * p + 1 < n) out[2 * p + 1] = r * std::sin(theta);
+  }
+  return out;
+}
+
+// nn::orthogonal (nn.hpp:457-486): modified Gram-Schmidt on a big x small
+// normal draw; the smaller dimension is orthonormal, scaled by gain.
+void host_orthogonal(const Key& key, int rows, int cols, float gain, float* w) {
+  const int big = std::max(rows, cols), small = std::min(rows, cols);
+  auto draws = host_normal(key, size_t(big) * size_t(small));
+  std::vector<std::vector<double>> q(size_t(small), std::vector<double>(size_t(big), 0.0));
+  for (int c = 0; c < small; ++c)
+    for (int r = 0; r < big; ++r) q[size_t(c)][size_t(r)] = draws[size_t(r) * size_t(small) + size_t(c)];
+  for (int c = 0; c < small; ++c) {
+    auto& col = q[size_t(c)];
+    for (int prev = 0; prev < c; ++prev) {
+      const auto& pv = q[size_t(prev)];
+      double dot = 0.0;
+      for (int r = 0; r < big; ++r) dot += col[size_t(r)] * pv[size_t(r)];
+      for (int r = 0; r < big; ++r) col[size_t(r)] -= dot * pv[size_t(r)];
+    }
+    double nrm = 0.0;
+    for (double x : col) nrm += x * x;
+    nrm = std::sqrt(nrm);
+    if (!(nrm > 1e-12)) raise(MARL_ERR_CONTRACT, "nn: orthogonal: degenerate draw");
+    for (double& x : col) x /= nrm;
+  }
+  for (int r = 0; r < rows; ++r)
+    for (int c = 0; c < cols; ++c) {
+      const double x = rows >= cols ? q[size_t(c)][size_t(r)] : q[size_t(r)][size_t(c)];
+      w[size_t(r) * size_t(cols) + size_t(c)] = float(double(gain) * x);
+    }
+}
+
+// ff_init (actor_critic.hpp:36-46) packed: torso layer l = dense_init(fold_in(
+// fold_in(key,1), l), W, in_l, sqrt 2) with zero bias, head = dense_init(
+// fold_in(key,2), out, W, head_gain).
+void host_ff_init(const Key& key, int in, int n_layers, int W, int out, float head_gain, float* dst) {
+  const Key torso = fold_in(key, 1);
+  const float g = float(std::sqrt(2.0));
+  int prev = in;
+  for (int l = 0; l < n_layers; ++l) {
+    host_orthogonal(fold_in(torso, uint64_t(l)), W, prev, g, dst);
+    dst += size_t(W) * size_t(prev);
+    std::fill(dst, dst + W, 0.0f);
+    dst += W;
+    prev = W;
+  }
+  host_orthogonal(fold_in(key, 2), out, W, head_gain, dst);
+  dst += size_t(out) * size_t(W);
+  std::fill(dst, dst + out, 0.0f);
+}
+
+}  // namespace
+
+struct marl_ppo {
+  marl_venv* h = nullptr;
+  marl_rollout* ro = nullptr;
+  PpoCfg cfg;
+  int centralized = 0, precision = 0;
+  int64_t n_updates = 0, update = 0, adam_t = 0, batch = 0, per = 0;
+  uint32_t train_key[4] = {0, 0, 0, 0};
+  double last_mean_return = 0.0;
+  int64_t window_episodes = 0;
+  double window_return = 0.0;
+  bool begun = false, collected = false;
+  Arena arena;
+  int P = 0, Pa = 0, Pc = 0, grid_a = 0, grid_c = 0;
+  float *m = nullptr, *v = nullptr, *grad = nullptr, *snapshot = nullptr, *gpart_a = nullptr, *gpart_c = nullptr;
+  double *spart_a = nullptr, *spart_c = nullptr, *adv_part = nullptr, *adv_part2 = nullptr, *metrics = nullptr;
+  PpoMbStats* mbst = nullptr;
+  int32_t* perm = nullptr;
+  uint8_t* perm_scratch = nullptr;
+  size_t perm_scratch_bytes = 0;
+  int* flags = nullptr;  // [0] diverged, [1] illegal stored action
+  ~marl_ppo() {
+    if (ro) marl_rollout_destroy(ro);
+  }
+};
+
+namespace {
+
+PpoBranchArgs branch_args(marl_ppo* p, bool actor, const int32_t* idx, int64_t M) {
+  marl_rollout* r = p->ro;
+  PpoBranchArgs a{};
+  a.params = actor ? r->params : r->params + r->n_actor;
+  a.gpart = actor ? p->gpart_a : p->gpart_c;
+  a.spart = actor ? p->spart_a : p->spart_c;
+  a.idx = idx;
+  a.M = M;
+  a.x = (!actor && r->centralized) ? r->b.critic_in : r->b.obs;
+  a.actions = r->b.actions;
+  a.old_logp = r->b.logp;
+  a.adv = r->b.adv;
+  a.vtarg = r->b.vtarg;
+  a.old_value = r->b.value;
+  a.active = r->b.active;
+  a.legal = r->b.legal;
+  a.st = p->mbst;
+  a.err = p->flags + 1;
+  a.in = actor ? r->in_dim : r->critic_in;
+  a.W = r->width;
+  a.out = actor ? r->n_act : 1;
+  a.relu = r->relu;
+  a.clip_eps = p->cfg.clip_eps;
+  a.ent_coef = p->cfg.ent_coef;
+  a.vf_coef = p->cfg.vf_coef;
+  return a;
+}
+
+// ff_minibatch's gradient (ppo.cpp:409-441) into p->grad (actor | critic).
+void minibatch_grad(marl_ppo* p, const int32_t* idx, int64_t M) {
+  cudaStream_t st = p->h->stream;
+  ppo_adv_stats(p->ro->b, idx, M, p->adv_part, p->adv_part2, p->mbst, st);
+  ppo_branch(branch_args(p, true, idx, M), true, p->grid_a, st);
+  ppo_branch(branch_args(p, false, idx, M), false, p->grid_c, st);
+  ppo_grad_reduce(p->gpart_a, p->grid_a, p->Pa, p->grad, st);
+  ppo_grad_reduce(p->gpart_c, p->grid_c, p->Pc, p->grad + p->Pa, st);
+  after_launch();
+}
+
+// clip_global_norm + adam_update for one minibatch (ppo.cpp:605-608).
+void minibatch_apply(marl_ppo* p, double lr_u, double* metrics_slot) {
+  p->adam_t += 1;
+  const float b1 = 0.9f, b2 = 0.999f;  // AdamState defaults (nn.hpp:408-414)
+  PpoApplyArgs a{};
+  a.params = p->ro->params;
+  a.grad = p->grad;
+  a.m = p->m;
+  a.v = p->v;
+  a.P = p->P;
+  a.actor_stats = p->spart_a;
+  a.critic_stats = p->spart_c;
+  a.n_actor_parts = p->grid_a;
+  a.n_critic_parts = p->grid_c;
+  a.st = p->mbst;
+  a.vf_coef = p->cfg.vf_coef;
+  a.ent_coef = p->cfg.ent_coef;
+  a.max_norm = float(p->cfg.max_grad_norm);
+  a.lr = float(lr_u);
+  a.beta1 = b1;
+  a.beta2 = b2;
+  a.eps = 1e-8f;
+  a.c1 = 1.0f - std::pow(b1, float(p->adam_t));
+  a.c2 = 1.0f - std::pow(b2, float(p->adam_t));
+  a.metrics = metrics_slot;
+  a.diverged = p->flags;
+  ppo_clip_adam(a, p->h->stream);
+  after_launch();
+}
+
+void ppo_collect_impl(marl_ppo* p) {
+  marl_venv* h = p->h;
+  int64_t s[3];
+  if (marl_venv_episode_stats(h, s, 1) != MARL_OK) raise(MARL_ERR_CUDA, marl_last_error());
+  const double half = 0.5 * double(p->cfg.total_timesteps);
+  const double n_envs = double(p->cfg.n_envs);
+  const bool shaped = p->cfg.shaped_rewards;
+  auto shaping_at = [half, n_envs, shaped](int64_t seq) {  // ppo.cpp:572-576
+    if (!shaped) return 0.0;
+    const double done = double(seq) * n_envs;
+    return std::max(0.0, 1.0 - done / std::max(half, 1.0));
+  };
+  collect_impl(p->ro, p->update * p->cfg.n_rollout_steps, p->cfg.gamma, p->cfg.gae_lambda, shaping_at);
+  if (marl_venv_episode_stats(h, s, 1) != MARL_OK) raise(MARL_ERR_CUDA, marl_last_error());
+  p->window_episodes = s[0];
+  p->window_return = double(s[2]) / 16777216.0;  // stats keep returns in 2^-24 fixed point
+  p->collected = true;
+}
+
+void ppo_update_impl(marl_ppo* p, double row[12], int* diverged) {
+  marl_rollout* r = p->ro;
+  cudaStream_t st = p->h->stream;
+  const PpoCfg& c = p->cfg;
+  const double lr_u = c.anneal_lr ? c.lr * (1.0 - double(p->update) / double(std::max<int64_t>(p->n_updates, 1)))
+                                  : c.lr;
+  const int n_mb_total = c.update_epochs * c.n_minibatches;
+  cuda_check(cudaMemcpyAsync(p->snapshot, r->params, size_t(p->P) * 4, cudaMemcpyDeviceToDevice, st), "cudaMemcpy");
+  cuda_check(cudaMemsetAsync(p->flags, 0, 2 * sizeof(int), st), "cudaMemset");
+  cuda_check(cudaMemsetAsync(p->metrics, 0, size_t(n_mb_total) * 8 * sizeof(double), st), "cudaMemset");
+  int k = 0;
+  for (int epoch = 0; epoch < c.update_epochs; ++epoch) {
+    uint32_t pk[4];
+    put_key(fold_in(key4(p->train_key), uint64_t(p->update) * uint64_t(c.update_epochs) + uint64_t(epoch)), pk);
+    KeyWords kw{};
+    std::memcpy(kw.w, pk, 16);
+    ppo_permutation(kw, p->batch, p->perm, p->perm_scratch, p->perm_scratch_bytes, st);
+    after_launch();
+    for (int mb = 0; mb < c.n_minibatches; ++mb, ++k) {
+      minibatch_grad(p, p->perm + size_t(mb) * size_t(p->per), p->per);
+      minibatch_apply(p, lr_u, p->metrics + size_t(k) * 8);
+    }
+  }
+  std::vector<double> m(size_t(n_mb_total) * 8);
+  int flags[2];
+  cuda_check(cudaMemcpyAsync(m.data(), p->metrics, m.size() * sizeof(double), cudaMemcpyDeviceToHost, st), "D2H");
+  cuda_check(cudaMemcpyAsync(flags, p->flags, sizeof flags, cudaMemcpyDeviceToHost, st), "D2H");
+  cuda_check(cudaStreamSynchronize(st), "cudaStreamSynchronize");
+  if (flags[1]) raise(MARL_ERR_CONTRACT, "nn: ppo_row_loss: stored action not legal");
+  double sums[7] = {0, 0, 0, 0, 0, 0, 0};
+  int n_mb = 0;
+  for (int q = 0; q < n_mb_total; ++q) {
+    if (m[size_t(q) * 8 + 7] != 1.0) break;  // minibatches after a DivergenceError never ran
+    for (int j = 0; j < 7; ++j) sums[j] += m[size_t(q) * 8 + j];
+    ++n_mb;
+  }
+  if (flags[0]) {  // roll back to the last completed update (ppo.cpp:630-634)
+    cuda_check(cudaMemcpyAsync(r->params, p->snapshot, size_t(p->P) * 4, cudaMemcpyDeviceToDevice, st), "cudaMemcpy");
+  }
+  if (r->precision == 1) {
+    rollout_pack_bf16(net_of(r), r->images, r->bias, st);
+    after_launch();
+  }
+  const int64_t steps_per_update = int64_t(c.n_envs) * int64_t(c.n_rollout_steps);
+  if (p->window_episodes > 0) p->last_mean_return = p->window_return / double(p->window_episodes);
+  const double inv = n_mb > 0 ? 1.0 / double(n_mb) : 0.0;
+  row[0] = double((p->update + 1) * steps_per_update);
+  row[1] = double(p->update);
+  row[2] = p->last_mean_return;
+  row[3] = double(p->window_episodes);
+  for (int j = 0; j < 7; ++j) row[4 + j] = sums[j] * inv;
+  row[11] = lr_u;
+  *diverged = flags[0];
+  p->update += 1;
+  p->collected = false;
+}
+
+}  // namespace
+
+extern "C" {
+
+int marl_ppo_create(marl_venv* h, const char* ppo_config_json, int centralized, int precision, marl_ppo** out) {
+  return guarded([&] {
+    if (!h || !out) raise(MARL_ERR_CONTRACT, "marl_ppo_create: NULL argument");
+    PpoCfg c = parse_ppo_config(ppo_config_json);
+    if (c.recurrent) raise(MARL_ERR_SCHEMA, "ppo: the B200 update implements feed-forward policies (recurrent=false)");
+    if (int64_t(c.n_envs) != h->gn) raise(MARL_ERR_CONTRACT, "ppo: n_envs must equal the VectorEnv's env count");
+    if (h->n != h->gn) raise(MARL_ERR_CONTRACT, "ppo: the device update runs on an unsharded VectorEnv");
+    set_device(h);
+    auto p = std::make_unique<marl_ppo>();
+    p->h = h;
+    p->cfg = c;
+    p->centralized = centralized ? 1 : 0;
+    p->precision = precision;
+    if (marl_rollout_create(h, c.n_rollout_steps, c.fc_width, c.n_fc_layers, c.activation == "relu", centralized,
+                            precision, &p->ro) != MARL_OK)
+      raise(MARL_ERR_SCHEMA, marl_last_error());
+    marl_rollout* r = p->ro;
+    if (r->n_act > kPpoMaxAct) raise(MARL_ERR_SCHEMA, "ppo: more than 64 actions");
+    const int64_t steps_per_update = int64_t(c.n_envs) * int64_t(c.n_rollout_steps);
+    p->n_updates = c.total_timesteps / steps_per_update;
+    p->batch = int64_t(c.n_rollout_steps) * r->R;
+    if (p->batch % c.n_minibatches != 0)
+      raise(MARL_ERR_SCHEMA, "ppo: batch size (" + std::to_string(p->batch) + ") must be divisible by n_minibatches (" +
+                                 std::to_string(c.n_minibatches) + ")");
+    if (p->batch >= (int64_t(1) << 31)) raise(MARL_ERR_SCHEMA, "ppo: batch (n_rollout_steps * rows) must be < 2^31");
+    p->per = p->batch / c.n_minibatches;
+    p->Pa = r->n_actor;
+    p->Pc = r->n_critic;
+    p->P = p->Pa + p->Pc;
+    p->grid_a = ppo_branch_grid(r->in_dim, r->width, r->n_act, p->per);
+    p->grid_c = ppo_branch_grid(r->critic_in, r->width, 1, p->per);
+    p->perm_scratch_bytes = ppo_perm_scratch_bytes(p->batch);
+    const int nb = ppo_stat_blocks(p->per);
+    Arena& ar = p->arena;
+    ar.add(&p->m, size_t(p->P));
+    ar.add(&p->v, size_t(p->P));
+    ar.add(&p->grad, size_t(p->P));
+    ar.add(&p->snapshot, size_t(p->P));
+    ar.add(&p->gpart_a, size_t(p->grid_a) * size_t(p->Pa));
+    ar.add(&p->gpart_c, size_t(p->grid_c) * size_t(p->Pc));
+    ar.add(&p->spart_a, size_t(p->grid_a) * 6);
+    ar.add(&p->spart_c, size_t(p->grid_c) * 6);
+    ar.add(&p->adv_part, size_t(nb) * 2);
+    ar.add(&p->adv_part2, size_t(nb));
+    ar.add(&p->metrics, size_t(c.update_epochs) * size_t(c.n_minibatches) * 8);
+    ar.add(&p->mbst, 1);
+    ar.add(&p->perm, size_t(p->batch));
+    ar.add(&p->perm_scratch, p->perm_scratch_bytes);
+    ar.add(&p->flags, 2);
+    ar.commit();
+    *out = p.release();
+  });
+}
+
+// ppo_init_nets(key, spec) (ppo.cpp:109-124) on the host, nn::pack order
+// (feed-forward spec; no device needed).
+int marl_ppo_init_nets(int in_dim, int critic_in, int n_actions, int fc_width, int n_fc_layers, const uint32_t key[4],
+                       float* actor, float* critic) {
+  return guarded([&] {
+    if (!key || !actor || !critic) raise(MARL_ERR_CONTRACT, "marl_ppo_init_nets: NULL argument");
+    if (in_dim < 1 || critic_in < 1 || n_actions < 1 || fc_width < 1 || n_fc_layers < 1)
+      raise(MARL_ERR_CONTRACT, "marl_ppo_init_nets: dimensions must be positive");
+    const Key k = key4(key);
+    host_ff_init(fold_in(k, 1), in_dim, n_fc_layers, fc_width, n_actions, 0.01f, actor);
+    host_ff_init(fold_in(k, 2), critic_in, n_fc_layers, fc_width, 1, 1.0f, critic);
+  });
+}
+
+// train_ppo_impl's setup (ppo.cpp:522-570): nets from fold_in(key, 10), the
+// Collector on fold_in(key, 11), the minibatch permutations on fold_in(key, 12).
+int marl_ppo_begin(marl_ppo* p, const uint32_t key[4]) {
+  return guarded([&] {
+    if (!p || !key) raise(MARL_ERR_CONTRACT, "marl_ppo_begin: NULL argument");
+    const Key k = key4(key);
+    uint32_t k10[4], k11[4];
+    put_key(fold_in(k, 10), k10);
+    put_key(fold_in(k, 11), k11);
+    put_key(fold_in(k, 12), p->train_key);
+    std::vector<float> a(size_t(p->Pa)), c(size_t(p->Pc));
+    const marl_rollout* r = p->ro;
+    if (marl_ppo_init_nets(r->in_dim, r->critic_in, r->n_act, r->width, p->cfg.n_fc_layers, k10, a.data(), c.data()) !=
+        MARL_OK)
+      raise(MARL_ERR_CONTRACT, marl_last_error());
+    if (marl_rollout_set_params(p->ro, a.data(), c.data()) != MARL_OK) raise(MARL_ERR_CUDA, marl_last_error());
+    if (marl_rollout_begin(p->ro, k11) != MARL_OK) raise(MARL_ERR_CUDA, marl_last_error());
+    set_device(p->h);
+    cuda_check(cudaMemset(p->m, 0, size_t(p->P) * 4), "cudaMemset");
+    cuda_check(cudaMemset(p->v, 0, size_t(p->P) * 4), "cudaMemset");
+    p->update = 0;
+    p->adam_t = 0;
+    p->last_mean_return = 0.0;
+    p->begun = true;
+    p->collected = false;
+  });
+}
+
+int marl_ppo_n_updates(const marl_ppo* p, int64_t* out) {
+  return guarded([&] {
+    if (!p || !out) raise(MARL_ERR_CONTRACT, "marl_ppo_n_updates: NULL argument");
+    *out = p->n_updates;
+  });
+}
+
+int marl_ppo_set_params(marl_ppo* p, const float* actor, const float* critic) {
+  return guarded([&] {
+    if (!p) raise(MARL_ERR_CONTRACT, "marl_ppo_set_params: NULL handle");
+    if (marl_rollout_set_params(p->ro, actor, critic) != MARL_OK) raise(MARL_ERR_CONTRACT, marl_last_error());
+  });
+}
+
+int marl_ppo_get_params(marl_ppo* p, float* actor, float* critic) {
+  return guarded([&] {
+    if (!p || !actor || !critic) raise(MARL_ERR_CONTRACT, "marl_ppo_get_params: NULL argument");
+    set_device(p->h);
+    cuda_check(cudaStreamSynchronize(p->h->stream), "cudaStreamSynchronize");
+    cuda_check(cudaMemcpy(actor, p->ro->params, size_t(p->Pa) * 4, cudaMemcpyDeviceToHost), "cudaMemcpy");
+    cuda_check(cudaMemcpy(critic, p->ro->params + p->Pa, size_t(p->Pc) * 4, cudaMemcpyDeviceToHost), "cudaMemcpy");
+  });
+}
+
+int marl_ppo_rollout(marl_ppo* p, marl_rollout** out) {
+  return guarded([&] {
+    if (!p || !out) raise(MARL_ERR_CONTRACT, "marl_ppo_rollout: NULL argument");
+    *out = p->ro;
+  });
+}
+
+// Collector::collect for the current update (ppo.cpp:587-588).
+int marl_ppo_collect(marl_ppo* p) {
+  return guarded([&] {
+    if (!p) raise(MARL_ERR_CONTRACT, "marl_ppo_collect: NULL handle");
+    if (!p->begun) raise(MARL_ERR_CONTRACT, "ppo: call begin() first");
+    ppo_collect_impl(p);
+  });
+}
+
+// The update epochs over the collected window (ppo.cpp:590-636); row = the
+// metrics row {step, update, mean_return, n_episodes, loss, pg_loss, v_loss,
+// entropy, approx_kl, clip_frac, grad_norm, lr} (ppo.cpp:524-527, 641-645).
+int marl_ppo_update(marl_ppo* p, double row[12], int* diverged) {
+  return guarded([&] {
+    if (!p || !row || !diverged) raise(MARL_ERR_CONTRACT, "marl_ppo_update: NULL argument");
+    if (!p->collected) raise(MARL_ERR_CONTRACT, "ppo: call collect() before update()");
+    set_device(p->h);
+    ppo_update_impl(p, row, diverged);
+  });
+}
+
+int marl_ppo_step(marl_ppo* p, double row[12], int* diverged) {
+  return guarded([&] {
+    if (!p || !row || !diverged) raise(MARL_ERR_CONTRACT, "marl_ppo_step: NULL argument");
+    if (!p->begun) raise(MARL_ERR_CONTRACT, "ppo: call begin() first");
+    ppo_collect_impl(p);
+    ppo_update_impl(p, row, diverged);
+  });
+}
+
+// One minibatch's flat gradient (actor | critic) and loss statistics
+// {loss, pg, v, entropy, kl, clip_frac} without the optimizer step:
+// ff_minibatch (ppo.cpp:409-441) over the current buffer.  d_idx: device slots.
+int marl_ppo_minibatch_grad(marl_ppo* p, const int32_t* d_idx, int64_t M, float* grad_out, double* stats_out) {
+  return guarded([&] {
+    if (!p || !d_idx || !grad_out || !stats_out) raise(MARL_ERR_CONTRACT, "marl_ppo_minibatch_grad: NULL argument");
+    if (M < 1 || M > p->per) raise(MARL_ERR_CONTRACT, "ppo: minibatch size must be in [1, batch / n_minibatches]");
+    set_device(p->h);
+    cudaStream_t st = p->h->stream;
+    cuda_check(cudaMemsetAsync(p->flags, 0, 2 * sizeof(int), st), "cudaMemset");
+    minibatch_grad(p, d_idx, M);
+    std::vector<double> sa(size_t(p->grid_a) * 6), sc(size_t(p->grid_c) * 6);
+    PpoMbStats ms{};
+    int flags[2];
+    cuda_check(cudaMemcpyAsync(grad_out, p->grad, size_t(p->P) * 4, cudaMemcpyDeviceToHost, st), "D2H");
+    cuda_check(cudaMemcpyAsync(sa.data(), p->spart_a, sa.size() * 8, cudaMemcpyDeviceToHost, st), "D2H");
+    cuda_check(cudaMemcpyAsync(sc.data(), p->spart_c, sc.size() * 8, cudaMemcpyDeviceToHost, st), "D2H");
+    cuda_check(cudaMemcpyAsync(&ms, p->mbst, sizeof ms, cudaMemcpyDeviceToHost, st), "D2H");
+    cuda_check(cudaMemcpyAsync(flags, p->flags, sizeof flags, cudaMemcpyDeviceToHost, st), "D2H");
+    cuda_check(cudaStreamSynchronize(st), "cudaStreamSynchronize");
+    if (flags[1]) raise(MARL_ERR_CONTRACT, "nn: ppo_row_loss: stored action not legal");
+    double s[6] = {0, 0, 0, 0, 0, 0}, vt = 0.0;
+    for (int c = 0; c < p->grid_a; ++c)
+      for (int j = 0; j < 6; ++j) s[j] += sa[size_t(c) * 6 + j];
+    for (int c = 0; c < p->grid_c; ++c) vt += sc[size_t(c) * 6 + 1];
+    const double tw = ms.total_w;
+    if (tw > 0.0) {
+      stats_out[0] = double(float((s[0] + p->cfg.vf_coef * vt - p->cfg.ent_coef * s[2]) / tw));
+      stats_out[1] = s[0] / tw;
+      stats_out[2] = vt / tw;
+      stats_out[3] = s[2] / tw;
+      stats_out[4] = s[3] / tw;
+      stats_out[5] = s[4] / tw;
+    } else {
+      for (int j = 0; j < 6; ++j) stats_out[j] = 0.0;
+    }
+  });
+}
+
+int marl_ppo_destroy(marl_ppo* p) {
+  return guarded([&] {
+    if (!p) return;
+    set_device(p->h);
+    cudaStreamSynchronize(p->h->stream);
+    delete p;
+  });
+}
+
+// prng::permutation(key, n) (prng.cpp:151-159) into device memory.
+int marl_ppo_permutation(const uint32_t key[4], int64_t n, int32_t* d_out, int device) {
+  return guarded([&] {
+    if (!key || (!d_out && n > 0)) raise(MARL_ERR_CONTRACT, "marl_ppo_permutation: NULL argument");
+    if (n < 0) raise(MARL_ERR_CONTRACT, "permutation: n must be >= 0");
+    if (n >= (int64_t(1) << 31)) raise(MARL_ERR_CONTRACT, "permutation: n must be < 2^31");
+    if (n == 0) return;
+    cuda_check(cudaSetDevice(device), "cudaSetDevice");
+    const size_t bytes = ppo_perm_scratch_bytes(n);
+    void* scratch = nullptr;
+    cuda_check(cudaMalloc(&scratch, bytes), "cudaMalloc");
+    KeyWords kw{};
+    std::memcpy(kw.w, key, 16);
+    ppo_permutation(kw, n, d_out, scratch, bytes, nullptr);
+    cudaError_t e = cudaDeviceSynchronize();
+    cudaFree(scratch);
+    cuda_check(e, "permutation");
+  });
 }
 
 }  // extern "C"

@@ -72,17 +72,21 @@ class IppoRollout:
               "critic_in": "<f4"}
 
     def __init__(self, venv: VectorEnv, n_rollout_steps: int, fc_width: int = 64, n_fc_layers: int = 2,
-                 activation: str = "tanh", precision: str = "fp32", centralized: bool = False):
+                 activation: str = "tanh", precision: str = "fp32", centralized: bool = False, _borrowed=None):
         """centralized=True is train_mappo's collector: the critic reads
         Env::world_state (ppo.cpp:341-346) instead of the agent's row."""
         import torch
         self._torch = torch
         self.venv = venv
         self.spec = policy_spec(venv, fc_width, n_fc_layers, activation, centralized)
-        h = C.c_void_p()
-        N.check(N.lib().marl_rollout_create(venv._h, n_rollout_steps, fc_width, n_fc_layers,
-                                            int(activation == "relu"), int(centralized), _PREC[precision],
-                                            C.byref(h)))
+        if _borrowed is not None:  # a collector owned by a PpoTrainer (marl_ppo_rollout)
+            h, self._owned = _borrowed, False
+        else:
+            h = C.c_void_p()
+            N.check(N.lib().marl_rollout_create(venv._h, n_rollout_steps, fc_width, n_fc_layers,
+                                                int(activation == "relu"), int(centralized), _PREC[precision],
+                                                C.byref(h)))
+            self._owned = True
         self._h = h
         v = N.RolloutViews()
         N.check(N.lib().marl_rollout_get_views(self._h, C.byref(v)))
@@ -98,7 +102,7 @@ class IppoRollout:
 
     def __del__(self):
         try:
-            if getattr(self, "_h", None):
+            if getattr(self, "_h", None) and getattr(self, "_owned", False):
                 N.lib().marl_rollout_destroy(self._h)
         except Exception:
             pass
