@@ -37,6 +37,9 @@ WORKLOADS = {
     # configs[4]: one "step" is one Collector::collect window of IPPO_T env steps
     "ippo": ("MPE_simple_spread_v3", {}, 1 << 20, "IPPO rollout on MPE simple_spread, 2^20 envs x 128 steps, "
              "bf16 actor+critic on tcgen05, configs[4]"),
+    # one "step" is one train_ippo update (collect + update_epochs x n_minibatches)
+    "ppo": ("MPE_simple_spread_v3", {}, 1 << 16, "IPPO training update on MPE simple_spread (collect 128 steps + "
+            "5 epochs x 2 minibatches of PPO), PpoConfig defaults"),
 }
 IPPO_T = 128
 L2_FLUSH_BYTES = 512 << 20  # > 4x the 126 MB L2; its ~80 us also covers the host's enqueue of the next step
@@ -316,6 +319,121 @@ def run_gpu_ippo(args, rank, world, local_rank):
     print(json.dumps(line))
 
 
+def ppo_flop_per_row(in_dim, cin, W, na):
+    fwd = W * in_dim + W * W + na * W + W * cin + W * W + W      # actor + critic forward MACs
+    bwd = (na * W + W * W) + (W + W * W)                         # dx of head and layer 2 (both nets)
+    wg = W * in_dim + W * W + na * W + W * cin + W * W + W        # weight gradients
+    return 2 * (fwd + bwd + wg)
+
+
+def run_gpu_ppo(args, rank, world, local_rank):
+    """One timed step = one PPO update of train_ippo (ppo.cpp:585-636): the
+    rollout window on the device then update_epochs x n_minibatches of
+    permutation + ff_minibatch + clip + Adam."""
+    import torch
+    import paper_2311_10090_b200 as m
+    from paper_2311_10090_b200 import _native
+    from paper_2311_10090_b200.ppo import PpoTrainer
+
+    env_id, cfg, n_envs, label = WORKLOADS[args.workload]
+    if args.n_envs:
+        n_envs = args.n_envs
+    torch.cuda.set_device(local_rank)
+    env = m.make_env(env_id, cfg)
+    A = env.num_agents()
+    T = IPPO_T
+    pc = {"n_envs": n_envs, "n_rollout_steps": T, "total_timesteps": (args.warmup + args.steps + 8) * n_envs * T}
+    venv = m.VectorEnv(env, n_envs, device=local_rank)
+    tr = PpoTrainer(venv, pc, False, "bf16")
+    tr.begin(m.prng.key_from_seed(rank))
+    stream = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        tr.step()
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    clocks = ClockSampler(local_rank) if rank == 0 else None
+    launches0 = _native.lib().marl_launch_count()
+    col_ms, upd_ms, rows = [], [], []
+    for k in range(args.steps):
+        e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        e0.record(stream)
+        tr.collect()
+        e1.record(stream)
+        row, div = tr.update()
+        e2.record(stream)
+        torch.cuda.synchronize()
+        col_ms.append(e0.elapsed_time(e1))
+        upd_ms.append(e1.elapsed_time(e2))
+        rows.append(row)
+    launches = _native.lib().marl_launch_count() - launches0
+    clk = clocks.stop() if clocks else None
+    step_ms = [c + u for c, u in zip(col_ms, upd_ms)]
+    from paper_2311_10090_b200 import dist as shard
+    total_ms = shard.max_over_ranks(float(sum(step_ms)), device="cuda")
+    value = world * n_envs * A * T * args.steps / (total_ms * 1e-3)
+    sp = tr.spec
+    fpr = ppo_flop_per_row(sp.in_dim, sp.critic_in, sp.width, sp.n_actions)
+    R = n_envs * A
+    upd_s = float(np.mean(upd_ms)) * 1e-3
+    tflops = T * R * 5 * fpr / upd_s / 1e12
+    # end to end through the public API: step() then the new parameters to the host
+    e2e_steps = max(2, min(args.steps, 3))
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        tr.step()
+        a, c = tr.params()
+    sec = shard.max_over_ranks(time.perf_counter() - t0, device="cuda")
+    if rank != 0:
+        return
+    cpu = None
+    if world == 1 and not args.no_cpu:
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        import oracle as O
+        if O.ref_available():
+            n_cpu, t_cpu = 64, 32
+            rc = {"n_envs": n_cpu, "n_rollout_steps": t_cpu, "total_timesteps": n_cpu * t_cpu}
+            t0 = time.perf_counter()
+            O.ref_train(env_id, cfg, rc, O.key_from_seed(0))
+            csec = time.perf_counter() - t0
+            cpu = {"value": n_cpu * t_cpu * A / csec, "unit": "agent-steps/s", "cores": 1, "kind": "reference",
+                   "sample": f"reference train_ippo, {n_cpu} envs x {t_cpu} steps, 1 update (5 epochs x 2 "
+                             f"minibatches), {csec:.1f} s"}
+    peak = None
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            peak = float(json.load(f)["bf16_tflops"])
+    except Exception:
+        peak = 2250.0
+    line = {
+        "metric": "agent-steps/sec (env-steps/sec x agents)", "value": value, "unit": "agent-steps/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "bf16 rollout policy / f32 PPO update / f64 env", "data": "synthetic (key_from_seed(rank))",
+        "config": {"workload": label, "env_id": env_id, "n_envs_per_gpu": n_envs, "agents": A,
+                   "rollout_steps": T, "update_epochs": 5, "n_minibatches": 2, "batch_rows": T * R,
+                   "step": "one PPO update = collect + update",
+                   "parallelism": "replicas only" if world > 1 else "single device",
+                   "l2": "no flush: the rollout buffer (> 1 GB) is rewritten every step"},
+        "collect_ms": float(np.mean(col_ms)), "update_ms": float(np.mean(upd_ms)),
+        "update_row_passes_per_sec": T * R * 5 / upd_s,
+        "roofline": {"bound": "tensor", "achieved": tflops, "peak": peak, "unit": "TFLOP/s", "frac": tflops / peak,
+                     "traffic": None, "peak_source": "MEASURED_PEAKS.json bf16_tflops (dense)",
+                     "kernel": "PPO update phase (ppo_branch_kernel dominant; fp32 CUDA-core math)",
+                     "flop_per_row_pass": fpr},
+        "cpu_baseline": cpu,
+        "e2e": {"value": n_envs * A * T * e2e_steps / sec, "unit": "agent-steps/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": int(a.nbytes + c.nbytes + 12 * 8), "steps": e2e_steps,
+                "path": "PpoTrainer.step + params() (C-ABI marl_ppo_step / marl_ppo_get_params)"},
+        "gpu_launches": int(launches),
+        "clocks": clk,
+        "last_metrics": {k: float(v) for k, v in zip(["step", "update", "mean_return", "n_episodes", "loss",
+                                                        "pg_loss", "v_loss", "entropy", "approx_kl", "clip_frac",
+                                                        "grad_norm", "lr"], rows[-1])},
+    }
+    print(json.dumps(line))
+
+
 def cpu_sample_size(env_id, cfg):
     """(envs, steps) of a bounded CPU sample of the workload: ~10-30 s for the
     cpu_baseline leg; the envs cap also bounds one reference-arm step (~1 s)."""
@@ -329,6 +447,27 @@ def run_reference_arm(args, rank, world):
         return
     threads = os.cpu_count() or 1
     n_envs = n_per_gpu * world
+    if args.workload == "ppo":  # one step = one train_ippo update of a bounded sample
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        import oracle as O
+        n_cpu, t_cpu = 64, 32
+        steps = max(1, args.steps)
+        rc = {"n_envs": n_cpu, "n_rollout_steps": t_cpu, "total_timesteps": n_cpu * t_cpu * steps}
+        t0 = time.perf_counter()
+        O.ref_train(env_id, cfg, rc, O.key_from_seed(0))
+        sec = time.perf_counter() - t0
+        val = n_cpu * 3 * t_cpu * steps / sec
+        line = {"impl": "reference", "metric": "agent-steps/sec (env-steps/sec x agents)", "value": val,
+                "unit": "agent-steps/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": 1e3 * sec / steps, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f32 nets / f64 env", "data": "synthetic",
+                "config": {"workload": label, "env_id": env_id, "n_envs": n_cpu, "n_envs_requested": n_envs,
+                           "rollout_steps": t_cpu},
+                "cpu_baseline": {"value": val, "unit": "agent-steps/s", "cores": 1, "kind": "reference",
+                                 "sample": f"reference train_ippo, {n_cpu} envs x {t_cpu} steps x {steps} updates"},
+                "e2e": {"value": val, "unit": "agent-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line))
+        return
     if args.workload == "ippo":  # one step = one collect window of a bounded env sample
         sys.path.insert(0, os.path.join(ROOT, "oracle"))
         import oracle as O
@@ -514,6 +653,8 @@ def main():
     try:
         if args.workload == "ippo":
             run_gpu_ippo(args, rank, world, local_rank)
+        elif args.workload == "ppo":
+            run_gpu_ppo(args, rank, world, local_rank)
         else:
             run_gpu_arm(args, rank, world, local_rank)
     finally:

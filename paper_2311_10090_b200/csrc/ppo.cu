@@ -30,6 +30,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "engine.h"
@@ -421,6 +422,422 @@ __global__ void __launch_bounds__(kThreads) ppo_branch_kernel(PpoBranchArgs a) {
   }
 }
 
+// ------------------------------------------------- register-tiled branch
+// The C5 shape (in <= 32, width 64, <= 16 outputs): every layer of the tile is
+// a 64-row GEMM computed as 4x4 register micro-tiles with FMA, operands read
+// as float4 from shared memory.  Each activation is kept in both layouts --
+// feature-major ([k][row], the A operand of the forward / input-gradient
+// GEMMs) and row-major ([row][k], the operands of the weight-gradient GEMMs
+// dW = dY^T X) -- so every inner-loop load is one LDS.128 feeding 16 FMAs.
+// Weight gradients accumulate in registers across the CTA's tiles.  Padded
+// rows / inputs / outputs are zero, so they add exact zeros.
+constexpr int kTR = 64;   // rows per tile
+constexpr int kTW = 64;   // torso width
+constexpr int kTIn = 32;  // padded input width
+constexpr int kLD = 68;   // padded leading dim of the 64-wide arrays (float4-aligned, bank-shifted)
+constexpr int kLDX = 36;  // padded leading dim of x[row][k]
+
+template <int NOP>
+struct TiledSmem {
+  float x[2][kTR][kLDX], xt[2][kTIn][kLD];  // double-buffered input tile (cp.async gather)
+  float h1[kTR][kLD], h1t[kTW][kLD], h2[kTR][kLD], h2t[kTW][kLD];
+  float dz2[kTR][kLD], dz2t[kTW][kLD], dz1[kTR][kLD];
+  float dl[kTR][NOP + 4], dlt[NOP][kLD];
+  float w1t[kTIn][kTW], w2t[kTW][kTW], w2[kTW][kTW], w3[NOP][kTW], w3t[kTW][NOP];
+  float b1[kTW], b2[kTW], b3[NOP];
+  float bred[4][kTW + 16];  // bias-gradient partials (4 row quarters)
+  int32_t slot[3][kTR];     // slots of tiles it, it+1 (gather in flight), it+2 (loading)
+  // per-row loss inputs, gathered with the tile: active, (adv | vtarg), (old logp | old value), action, legal words
+  float r_active[2][kTR], r_a[2][kTR], r_b[2][kTR];
+  int32_t r_act[2][kTR];
+  uint32_t r_legal[2][kTR][5];
+};
+
+__device__ __forceinline__ void cp_async4(void* sdst, const void* gsrc, int src_bytes) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(
+                   static_cast<uint32_t>(__cvta_generic_to_shared(sdst))),
+               "l"(gsrc), "r"(src_bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// per-row inputs of the loss, loaded ahead of the tile's forward GEMMs
+struct RowIn {
+  float active, adv, logp, vtarg, value;
+  int action;
+  int legal;
+};
+
+// c[i][j] += A[k*lda + i] * B[k*ldb + j] over k < K  (MI x NJ register tile)
+template <int MI, int NJ>
+__device__ __forceinline__ void mm(const float* __restrict__ A, int lda, const float* __restrict__ B, int ldb, int K,
+                                   float (&c)[4][4]) {
+#pragma unroll 8
+  for (int k = 0; k < K; ++k) {
+    float av[4], bv[4];
+    if (MI == 4) {
+      const float4 v = *reinterpret_cast<const float4*>(A + k * lda);
+      av[0] = v.x, av[1] = v.y, av[2] = v.z, av[3] = v.w;
+    } else {
+      av[0] = A[k * lda];
+    }
+    if (NJ == 4) {
+      const float4 v = *reinterpret_cast<const float4*>(B + k * ldb);
+      bv[0] = v.x, bv[1] = v.y, bv[2] = v.z, bv[3] = v.w;
+    } else {
+      bv[0] = B[k * ldb];
+    }
+#pragma unroll
+    for (int i = 0; i < MI; ++i)
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) c[i][j] = fmaf(av[i], bv[j], c[i][j]);
+  }
+}
+
+__device__ __forceinline__ void zero44(float (&c)[4][4]) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) c[i][j] = 0.0f;
+}
+
+// store a 4x4 block (rows r0.., cols c0..) row-major and/or feature-major
+template <int LDR, int LDT>
+__device__ __forceinline__ void put44(float (*rm)[LDR], float (*fm)[LDT], int r0, int c0, const float (&c)[4][4]) {
+  if (rm)
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      *reinterpret_cast<float4*>(&rm[r0 + i][c0]) = make_float4(c[i][0], c[i][1], c[i][2], c[i][3]);
+  if (fm)
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      *reinterpret_cast<float4*>(&fm[c0 + j][r0]) = make_float4(c[0][j], c[1][j], c[2][j], c[3][j]);
+}
+
+// d(-surr - ent_coef*H)/dz for one actor row, NOP lanes of a warp segment per
+// row, lane j = action j (actor_critic.hpp:360-392 in double; the softmax
+// sums are tree-reduced over the segment).  Returns the lane's dz.
+template <int NOP>
+__device__ __forceinline__ float actor_row_grad(const PpoBranchArgs& a, const PpoMbStats& st, double total_w,
+                                                const RowIn& ri, bool row_ok, float z, int j, double* pg, double* ent,
+                                                double* kl, double* clipn) {
+  const int NO = a.out;
+  const unsigned full = 0xffffffffu;
+  // every lane of the warp runs the shuffles; rows without weight are masked at the end
+  const double w = row_ok ? double(ri.active) : 0.0;
+  const bool on = w != 0.0 && total_w > 0.0;
+  const bool lg = on && j < NO && ri.legal;
+  double mx = lg ? double(z) : -INFINITY;
+#pragma unroll
+  for (int o = NOP / 2; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(full, mx, o, NOP));
+  const double e = lg ? exp(double(z) - mx) : 0.0;
+  double denom = e;
+#pragma unroll
+  for (int o = NOP / 2; o > 0; o >>= 1) denom += __shfl_xor_sync(full, denom, o, NOP);
+  const double lp = lg ? double(z) - mx - log(denom) : -1e30;
+  const int act = on ? ri.action : 0;
+  if (on && j == 0 && (act < 0 || act >= NO || !(mx > -INFINITY))) atomicExch(a.err, 1);
+  const int ac = act < 0 ? 0 : (act >= NO ? NO - 1 : act);
+  const double lp_a = __shfl_sync(full, lp, ac, NOP);
+  const int lg_a = __shfl_sync(full, int(lg), ac, NOP);
+  if (on && j == 0 && !lg_a) atomicExch(a.err, 1);
+  const double pi = lg ? exp(lp) : 0.0;
+  double h = lg ? -pi * lp : 0.0;
+#pragma unroll
+  for (int o = NOP / 2; o > 0; o >>= 1) h += __shfl_xor_sync(full, h, o, NOP);
+  if (!on) return 0.0f;
+  float advf = ri.adv;
+  if (st.normalize) advf = float((double(advf) - st.mean) / (st.std + 1e-8));
+  const double adv = double(advf);
+  const double ratio = exp(lp_a - double(ri.logp));
+  const double unclipped = ratio * adv;
+  const double rho_c = fmin(fmax(ratio, 1.0 - a.clip_eps), 1.0 + a.clip_eps);
+  const double clipped = rho_c * adv;
+  const double dsurr = unclipped <= clipped ? ratio * adv : 0.0;
+  if (j == 0) {
+    *pg += w * -fmin(unclipped, clipped);
+    *ent += w * h;
+    *kl += w * (ratio - 1.0 - log(ratio));
+    *clipn += w * (fabs(ratio - 1.0) > a.clip_eps ? 1.0 : 0.0);
+  }
+  if (!lg) return 0.0f;
+  const double dlogp = (j == ac ? 1.0 : 0.0) - pi;
+  const double dH = -pi * (lp + h);
+  return float(w / total_w * (-dsurr * dlogp - a.ent_coef * dH));
+}
+
+template <bool ACTOR, int NOP>
+__global__ void __launch_bounds__(kThreads, 1) ppo_branch_tiled_kernel(PpoBranchArgs a) {
+  extern __shared__ __align__(16) uint8_t sm_raw[];
+  TiledSmem<NOP>& s = *reinterpret_cast<TiledSmem<NOP>*>(sm_raw);
+  __shared__ double s_stats[kThreads / 32][kStats];
+  const int in = a.in, NO = a.out, t = threadIdx.x;
+  const float* p = a.params;
+  const float *W1 = p, *B1 = W1 + kTW * in, *W2 = B1 + kTW, *B2 = W2 + kTW * kTW, *W3 = B2 + kTW,
+              *B3 = W3 + NO * kTW;
+  // stage the branch: W1^T (zero-padded to 32 inputs), W2 and W2^T, W3 and W3^T (zero rows)
+  for (int e = t; e < kTIn * kTW; e += kThreads) {
+    const int k = e / kTW, o = e % kTW;
+    s.w1t[k][o] = k < in ? __ldg(W1 + o * in + k) : 0.0f;
+  }
+  for (int e = t; e < kTW * kTW; e += kThreads) {
+    const int o = e / kTW, i = e % kTW;
+    const float w = __ldg(W2 + e);
+    s.w2[o][i] = w;
+    s.w2t[i][o] = w;
+  }
+  for (int e = t; e < NOP * kTW; e += kThreads) {
+    const int o = e / kTW, i = e % kTW;
+    const float w = o < NO ? __ldg(W3 + o * kTW + i) : 0.0f;
+    s.w3[o][i] = w;
+    s.w3t[i][o] = w;
+  }
+  if (t < kTW) {
+    s.b1[t] = __ldg(B1 + t);
+    s.b2[t] = __ldg(B2 + t);
+  }
+  if (t < NOP) s.b3[t] = t < NO ? __ldg(B3 + t) : 0.0f;
+
+  const PpoMbStats st = *a.st;
+  const double total_w = st.total_w;
+  // persistent gradient accumulators: gW2 tile (every thread), gW1 tile
+  // (threads 128..255), gW3 tile (threads 0..NOP*16/4-1, 1x4), bias partials
+  float g2[4][4], g1[4][4], g3[4][4];
+  zero44(g2);
+  zero44(g1);
+  zero44(g3);
+  float gb1 = 0.0f, gb2 = 0.0f, gb3 = 0.0f;
+  double pg = 0.0, vt = 0.0, ent = 0.0, kl = 0.0, clipn = 0.0;
+  const int rg = t % 16, cg = t / 16;  // 64x64 GEMMs: rows/outs 4*rg.., cols 4*cg..
+  const int bo = t % kTW, bq = t / kTW;  // bias sums: output bo over rows 16*bq..
+
+  const int64_t ntiles = (a.M + kTR - 1) / kTR;
+  const int64_t G = gridDim.x;
+  auto slot_load = [&](int64_t tile, int sb) {
+    if (t < kTR) {
+      const int64_t i = tile * kTR + t;
+      s.slot[sb][t] = (tile < ntiles && i < a.M) ? a.idx[i] : -1;
+    }
+  };
+  // gather of a tile's input rows (ff_minibatch's memcpy, ppo.cpp:413-420) into
+  // buffer xb, row-major and feature-major, zero-filled padding, asynchronous
+  auto gather = [&](int xb, int sb) {
+    for (int e = t; e < kTR * kTIn; e += kThreads) {
+      const int r = e / kTIn, k = e % kTIn;
+      const int sl = s.slot[sb][r];
+      const bool ok = sl >= 0 && k < in;
+      const float* src = ok ? a.x + size_t(sl) * size_t(in) + k : a.x;
+      cp_async4(&s.x[xb][r][k], src, ok ? 4 : 0);
+      cp_async4(&s.xt[xb][k][r], src, ok ? 4 : 0);
+    }
+    if (t < kTR) {
+      const int sl = s.slot[sb][t];
+      const int n = sl >= 0 ? 4 : 0;
+      const int64_t q = sl >= 0 ? sl : 0;
+      cp_async4(&s.r_active[xb][t], a.active + q, n);
+      cp_async4(&s.r_a[xb][t], (ACTOR ? a.adv : a.vtarg) + q, n);
+      cp_async4(&s.r_b[xb][t], (ACTOR ? a.old_logp : a.old_value) + q, n);
+      if (ACTOR) {
+        cp_async4(&s.r_act[xb][t], a.actions + q, n);
+        const int64_t base = q * NO, w0 = base & ~int64_t(3);
+        const int nw = int(((base & 3) + NO + 3) / 4);
+#pragma unroll
+        for (int w = 0; w < 5; ++w) cp_async4(&s.r_legal[xb][t][w], a.legal + w0 + 4 * w, (n && w < nw) ? 4 : 0);
+      }
+    }
+    cp_async_commit();
+  };
+  slot_load(blockIdx.x, 0);
+  slot_load(blockIdx.x + G, 1);
+  __syncthreads();
+  gather(0, 0);
+  int it = 0;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += G, ++it) {
+    const int xb = it & 1, sb = it % 3;
+    __syncthreads();  // the previous tile is consumed: its x buffer and slot buffer are free
+    gather(xb ^ 1, (it + 1) % 3);  // tile + G (an empty group past the end)
+    slot_load(tile + 2 * G, (it + 2) % 3);
+    constexpr int kRows = ACTOR ? (kTR * NOP + kThreads - 1) / kThreads : 1;
+    cp_async_wait<1>();  // this tile's gather has landed
+    __syncthreads();
+    const auto& X = s.x[xb];
+    const auto& XT = s.xt[xb];
+    // this thread's loss rows (staged with the tile)
+    RowIn ri[kRows];
+#pragma unroll
+    for (int q = 0; q < kRows; ++q) {
+      const int r = ACTOR ? t / NOP + q * (kThreads / NOP) : t;
+      ri[q] = RowIn{0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0, 0};
+      if (r < kTR && s.slot[sb][r] >= 0) {
+        ri[q].active = s.r_active[xb][r];
+        if (ACTOR) {
+          ri[q].adv = s.r_a[xb][r];
+          ri[q].logp = s.r_b[xb][r];
+          ri[q].action = s.r_act[xb][r];
+          const int j = t % NOP;
+          if (j < NO) {
+            const int b = int((int64_t(s.slot[sb][r]) * NO) & 3) + j;
+            ri[q].legal = (s.r_legal[xb][r][b >> 2] >> (8 * (b & 3))) & 0xffu;
+          }
+        } else {
+          ri[q].vtarg = s.r_a[xb][r];
+          ri[q].value = s.r_b[xb][r];
+        }
+      }
+    }
+    float c[4][4];
+    // F1: h1 = act(x W1^T + b1)
+    zero44(c);
+    mm<4, 4>(&XT[0][4 * rg], kLD, &s.w1t[0][4 * cg], kTW, kTIn, c);
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) c[i][j] = act_fwd(c[i][j] + s.b1[4 * cg + j], a.relu);
+    put44<kLD, kLD>(s.h1, s.h1t, 4 * rg, 4 * cg, c);
+    __syncthreads();
+    // F2: h2 = act(h1 W2^T + b2)
+    zero44(c);
+    mm<4, 4>(&s.h1t[0][4 * rg], kLD, &s.w2t[0][4 * cg], kTW, kTW, c);
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) c[i][j] = act_fwd(c[i][j] + s.b2[4 * cg + j], a.relu);
+    put44<kLD, kLD>(s.h2, s.h2t, 4 * rg, 4 * cg, c);
+    __syncthreads();
+    // F3: head -> dl (row-major): 4 rows x 1 output per thread
+    if (t < 16 * NOP) {
+      const int o = t / 16;
+      zero44(c);
+      mm<4, 1>(&s.h2t[0][4 * rg], kLD, &s.w3t[0][o], NOP, kTW, c);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) s.dl[4 * rg + i][o] = c[i][0] + s.b3[o];
+    }
+    __syncthreads();
+    // the row's part of ppo_row_loss (actor_critic.hpp:360-402)
+    if (ACTOR) {
+      constexpr int kSlots = kThreads / NOP;
+      const int j = t % NOP;
+#pragma unroll
+      for (int q = 0; q < kRows; ++q) {
+        const int r = t / NOP + q * kSlots;
+        if (r < kTR) {  // uniform per warp
+          const float g = actor_row_grad<NOP>(a, st, total_w, ri[q], s.slot[sb][r] >= 0, s.dl[r][j], j, &pg, &ent,
+                                              &kl, &clipn);
+          s.dl[r][j] = g;
+          s.dlt[j][r] = g;
+        }
+      }
+    } else if (t < kTR) {
+      const int r = t;
+      const double w = s.slot[sb][r] >= 0 ? double(ri[0].active) : 0.0;
+      float g = 0.0f;
+      if (w != 0.0 && total_w > 0.0) {
+        const double v = double(s.dl[r][0]);
+        const double targ = double(ri[0].vtarg);
+        const double v_old = double(ri[0].value);
+        const double v_clip = v_old + fmin(fmax(v - v_old, -a.clip_eps), a.clip_eps);
+        const double sq = (v - targ) * (v - targ), sq_c = (v_clip - targ) * (v_clip - targ);
+        vt += w * (0.5 * fmax(sq, sq_c));
+        g = float(w / total_w * a.vf_coef * (sq >= sq_c ? (v - targ) : 0.0));
+      }
+      for (int o = 0; o < NOP; ++o) {
+        s.dl[r][o] = o == 0 ? g : 0.0f;
+        s.dlt[o][r] = o == 0 ? g : 0.0f;
+      }
+    }
+    __syncthreads();
+    // B1: dz2 = (dl W3) * act'(h2)
+    zero44(c);
+    mm<4, 4>(&s.dlt[0][4 * rg], kLD, &s.w3[0][4 * cg], kTW, NOP, c);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float4 y = *reinterpret_cast<const float4*>(&s.h2[4 * rg + i][4 * cg]);
+      c[i][0] = act_bwd(c[i][0], y.x, a.relu);
+      c[i][1] = act_bwd(c[i][1], y.y, a.relu);
+      c[i][2] = act_bwd(c[i][2], y.z, a.relu);
+      c[i][3] = act_bwd(c[i][3], y.w, a.relu);
+    }
+    put44<kLD, kLD>(s.dz2, s.dz2t, 4 * rg, 4 * cg, c);
+    __syncthreads();
+    // B2: dz1 = (dz2 W2) * act'(h1)
+    zero44(c);
+    mm<4, 4>(&s.dz2t[0][4 * rg], kLD, &s.w2[0][4 * cg], kTW, kTW, c);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float4 y = *reinterpret_cast<const float4*>(&s.h1[4 * rg + i][4 * cg]);
+      c[i][0] = act_bwd(c[i][0], y.x, a.relu);
+      c[i][1] = act_bwd(c[i][1], y.y, a.relu);
+      c[i][2] = act_bwd(c[i][2], y.z, a.relu);
+      c[i][3] = act_bwd(c[i][3], y.w, a.relu);
+    }
+    put44<kLD, 1>(s.dz1, nullptr, 4 * rg, 4 * cg, c);
+    __syncthreads();
+    // weight gradients of the tile (dense_backward: g.w = dy^T x, g.b = sum dy)
+    mm<4, 4>(&s.dz2[0][4 * rg], kLD, &s.h1[0][4 * cg], kLD, kTR, g2);
+    if (t >= 128) mm<4, 4>(&s.dz1[0][4 * rg], kLD, &X[0][4 * (cg - 8)], kLDX, kTR, g1);
+    if (t < 16 * NOP) mm<1, 4>(&s.dl[0][t / 16], NOP + 4, &s.h2[0][4 * rg], kLD, kTR, g3);
+    {
+      float s1 = 0.0f, s2 = 0.0f;
+#pragma unroll 4
+      for (int r = 16 * bq; r < 16 * bq + 16; ++r) {
+        s1 += s.dz1[r][bo];
+        s2 += s.dz2[r][bo];
+      }
+      gb1 += s1;
+      gb2 += s2;
+      if (bo < NOP) {
+        float s3 = 0.0f;
+        for (int r = 16 * bq; r < 16 * bq + 16; ++r) s3 += s.dl[r][bo];
+        gb3 += s3;
+      }
+    }
+  }
+  cp_async_wait<0>();
+  // write the CTA's partial gradient in nn::pack order
+  float* gp = a.gpart + size_t(blockIdx.x) * size_t(kTW * in + kTW + kTW * kTW + kTW + NO * kTW + NO);
+  float *G1 = gp, *GB1 = G1 + kTW * in, *G2 = GB1 + kTW, *GB2 = G2 + kTW * kTW, *G3 = GB2 + kTW, *GB3 = G3 + NO * kTW;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) G2[(4 * rg + i) * kTW + 4 * cg + j] = g2[i][j];
+  if (t >= 128)
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (4 * (cg - 8) + j < in) G1[(4 * rg + i) * in + 4 * (cg - 8) + j] = g1[i][j];
+  if (t < 16 * NOP && t / 16 < NO)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) G3[(t / 16) * kTW + 4 * rg + j] = g3[0][j];
+  // bias partials of the 4 row quarters, summed in quarter order
+  __syncthreads();
+  s.bred[bq][bo] = gb1;
+  __syncthreads();
+  if (t < kTW) GB1[t] = ((s.bred[0][t] + s.bred[1][t]) + s.bred[2][t]) + s.bred[3][t];
+  __syncthreads();
+  s.bred[bq][bo] = gb2;
+  __syncthreads();
+  if (t < kTW) GB2[t] = ((s.bred[0][t] + s.bred[1][t]) + s.bred[2][t]) + s.bred[3][t];
+  __syncthreads();
+  if (bo < NOP) s.bred[bq][bo] = gb3;
+  __syncthreads();
+  if (t < NO) GB3[t] = ((s.bred[0][t] + s.bred[1][t]) + s.bred[2][t]) + s.bred[3][t];
+  double v5[kStats] = {pg, vt, ent, kl, clipn, 0.0};
+  for (int cc = 0; cc < kStats; ++cc) {
+    double v = v5[cc];
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    if ((t & 31) == 0) s_stats[t >> 5][cc] = v;
+  }
+  __syncthreads();
+  if (t < kStats) {
+    double v = 0.0;
+    for (int w = 0; w < kThreads / 32; ++w) v += s_stats[w][t];
+    a.spart[size_t(blockIdx.x) * kStats + t] = v;
+  }
+}
+
 // Sum the per-CTA partial rows in CTA order: grad[p] = sum_c part[c][p].
 __global__ void grad_reduce_kernel(const float* __restrict__ part, int nparts, int P, float* __restrict__ grad) {
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
@@ -588,10 +1005,16 @@ void ppo_branch_geometry(int in, int W, int out, int* TR, int* staged, size_t* s
   *smem = size_t(8) * size_t(ldx + 4 * ldw + ldo + 1) * 4;
 }
 
+bool ppo_tiled_ok(int in, int W, int out);
+
 int ppo_branch_grid(int in, int W, int out, int64_t M) {
   int TR, staged;
   size_t sm;
   ppo_branch_geometry(in, W, out, &TR, &staged, &sm);
+  if (ppo_tiled_ok(in, W, out) && !getenv("MARL_PPO_GENERIC")) {
+    TR = kTR;
+    sm = 200 * 1024;  // one CTA per SM
+  }
   static int sms = 0;
   if (!sms) {
     int dev = 0;
@@ -619,7 +1042,28 @@ static void launch_branch(PpoBranchArgs a, int grid, size_t sm, cudaStream_t s) 
   ++g_launches;
 }
 
+bool ppo_tiled_ok(int in, int W, int out) { return in <= kTIn && W == kTW && out <= 16; }
+
+template <bool ACTOR, int NOP>
+static void launch_tiled(const PpoBranchArgs& a, int grid, cudaStream_t s) {
+  const size_t sm = sizeof(TiledSmem<NOP>);
+  cudaFuncSetAttribute(ppo_branch_tiled_kernel<ACTOR, NOP>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+  ppo_branch_tiled_kernel<ACTOR, NOP><<<grid, kThreads, sm, s>>>(a);
+  ++g_launches;
+}
+
 void ppo_branch(PpoBranchArgs a, bool actor, int grid, cudaStream_t s) {
+  if (ppo_tiled_ok(a.in, a.W, a.out) && !getenv("MARL_PPO_GENERIC")) {
+    const int nop = a.out <= 4 ? 4 : a.out <= 8 ? 8 : 16;
+    if (actor) {
+      if (nop == 4) launch_tiled<true, 4>(a, grid, s);
+      else if (nop == 8) launch_tiled<true, 8>(a, grid, s);
+      else launch_tiled<true, 16>(a, grid, s);
+    } else {
+      launch_tiled<false, 4>(a, grid, s);
+    }
+    return;
+  }
   size_t sm;
   ppo_branch_geometry(a.in, a.W, a.out, &a.TR, &a.staged, &sm);
   if (actor)

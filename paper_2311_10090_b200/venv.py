@@ -208,7 +208,10 @@ class VectorEnv:
     def __del__(self):
         h = getattr(self, "_h", None)
         if h:
-            N.lib().marl_venv_destroy(h)
+            try:
+                N.lib().marl_venv_destroy(h)
+            except Exception:  # interpreter shutdown: module globals already torn down
+                pass
             self._h = None
 
     # ---- metadata
