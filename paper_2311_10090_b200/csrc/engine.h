@@ -257,6 +257,27 @@ struct PpoApplyArgs {
   int* diverged;     // sticky DivergenceError flag
 };
 
+// The tcgen05 minibatch step (ppo_tc.cu): actor + critic of an IPPO net with
+// input <= 31, width 64, <= 16 actions, bf16 operands, fp32 TMEM accumulators.
+struct PpoTcArgs {
+  const float *actor, *critic;  // packed fp32 parameters (current)
+  float *gpart_a, *gpart_c;     // [grid][Pa], [grid][Pc]
+  double *spart_a, *spart_c;    // [grid][6]
+  const int32_t* idx;
+  int64_t M;
+  const float* obs;
+  const int32_t* actions;
+  const float *old_logp, *adv, *vtarg, *old_value, *active;
+  const uint8_t* legal;
+  const PpoMbStats* st;
+  int* err;
+  int in, n_act, relu;
+  double clip_eps, ent_coef, vf_coef;
+};
+bool ppo_tc_supported(int in_dim, int critic_in, int width, int n_act);
+int ppo_tc_grid(int64_t M);
+void ppo_update_tc(const PpoTcArgs& a, int grid, cudaStream_t s);
+
 size_t ppo_perm_scratch_bytes(int64_t n);
 // prng::permutation(key, n) (prng.cpp:151-159) into out[n] on the device.
 void ppo_permutation(KeyWords key, int64_t n, int32_t* out, void* scratch, size_t scratch_bytes, cudaStream_t st);

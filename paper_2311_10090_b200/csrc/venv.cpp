@@ -10,6 +10,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -1431,6 +1432,7 @@ struct marl_ppo {
   bool begun = false, collected = false;
   Arena arena;
   int P = 0, Pa = 0, Pc = 0, grid_a = 0, grid_c = 0;
+  bool tc = false;  // minibatch step on tcgen05 (bf16 precision, the C5 shape)
   float *m = nullptr, *v = nullptr, *grad = nullptr, *snapshot = nullptr, *gpart_a = nullptr, *gpart_c = nullptr;
   double *spart_a = nullptr, *spart_c = nullptr, *adv_part = nullptr, *adv_part2 = nullptr, *metrics = nullptr;
   PpoMbStats* mbst = nullptr;
@@ -1477,8 +1479,38 @@ PpoBranchArgs branch_args(marl_ppo* p, bool actor, const int32_t* idx, int64_t M
 void minibatch_grad(marl_ppo* p, const int32_t* idx, int64_t M) {
   cudaStream_t st = p->h->stream;
   ppo_adv_stats(p->ro->b, idx, M, p->adv_part, p->adv_part2, p->mbst, st);
-  ppo_branch(branch_args(p, true, idx, M), true, p->grid_a, st);
-  ppo_branch(branch_args(p, false, idx, M), false, p->grid_c, st);
+  if (p->tc) {
+    const marl_rollout* r = p->ro;
+    PpoTcArgs a{};
+    a.actor = r->params;
+    a.critic = r->params + r->n_actor;
+    a.gpart_a = p->gpart_a;
+    a.gpart_c = p->gpart_c;
+    a.spart_a = p->spart_a;
+    a.spart_c = p->spart_c;
+    a.idx = idx;
+    a.M = M;
+    a.obs = r->b.obs;
+    a.actions = r->b.actions;
+    a.old_logp = r->b.logp;
+    a.adv = r->b.adv;
+    a.vtarg = r->b.vtarg;
+    a.old_value = r->b.value;
+    a.active = r->b.active;
+    a.legal = r->b.legal;
+    a.st = p->mbst;
+    a.err = p->flags + 1;
+    a.in = r->in_dim;
+    a.n_act = r->n_act;
+    a.relu = r->relu;
+    a.clip_eps = p->cfg.clip_eps;
+    a.ent_coef = p->cfg.ent_coef;
+    a.vf_coef = p->cfg.vf_coef;
+    ppo_update_tc(a, p->grid_a, st);
+  } else {
+    ppo_branch(branch_args(p, true, idx, M), true, p->grid_a, st);
+    ppo_branch(branch_args(p, false, idx, M), false, p->grid_c, st);
+  }
   ppo_grad_reduce(p->gpart_a, p->grid_a, p->Pa, p->grad, st);
   ppo_grad_reduce(p->gpart_c, p->grid_c, p->Pc, p->grad + p->Pa, st);
   after_launch();
@@ -1623,8 +1655,16 @@ int marl_ppo_create(marl_venv* h, const char* ppo_config_json, int centralized, 
     p->Pa = r->n_actor;
     p->Pc = r->n_critic;
     p->P = p->Pa + p->Pc;
-    p->grid_a = ppo_branch_grid(r->in_dim, r->width, r->n_act, p->per);
-    p->grid_c = ppo_branch_grid(r->critic_in, r->width, 1, p->per);
+    // precision 1: the minibatch step runs on tcgen05 where the shape allows
+    // (MARL_PPO_UPDATE_FP32=1 forces the fp32 CUDA-core path)
+    p->tc = precision == 1 && !centralized && ppo_tc_supported(r->in_dim, r->critic_in, r->width, r->n_act) &&
+            !std::getenv("MARL_PPO_UPDATE_FP32");
+    if (p->tc) {
+      p->grid_a = p->grid_c = ppo_tc_grid(p->per);
+    } else {
+      p->grid_a = ppo_branch_grid(r->in_dim, r->width, r->n_act, p->per);
+      p->grid_c = ppo_branch_grid(r->critic_in, r->width, 1, p->per);
+    }
     p->perm_scratch_bytes = ppo_perm_scratch_bytes(p->batch);
     const int nb = ppo_stat_blocks(p->per);
     Arena& ar = p->arena;
