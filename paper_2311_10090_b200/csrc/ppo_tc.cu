@@ -190,20 +190,22 @@ __global__ void __launch_bounds__(kThr, 1) ppo_update_tc_kernel(PpoTcArgs a) {
     gb3w[t] = 0.0f;  // 8 warps x 32
   }
   // ---- gather of a tile's rows into the staging area (cp.async, zero-filled)
+  // slots arrive by cp.async (zero-filled past the end); validity is index arithmetic
+  auto slot_ok = [&](int64_t tile, int r) { return tile < ntiles && tile * kRows + r < a.M; };
   auto slot_load = [&](int64_t tile, int sb) {
     if (t < kRows) {
-      const int64_t i = tile * kRows + t;
-      slot[sb * kRows + t] = (tile < ntiles && i < a.M) ? a.idx[i] : -1;
+      const bool ok = slot_ok(tile, t);
+      cpa4(slot + sb * kRows + t, ok ? a.idx + tile * kRows + t : a.idx, ok ? 4 : 0);
     }
   };
-  auto gather = [&](int sb) {
+  auto gather = [&](int64_t tile, int sb) {
     for (int e = t; e < kRows * in; e += kThr) {
       const int r = e / in, k = e - r * in;
-      const int sl = slot[sb * kRows + r];
+      const int sl = slot_ok(tile, r) ? slot[sb * kRows + r] : -1;
       cpa4(st_x + e, sl >= 0 ? a.obs + size_t(sl) * size_t(in) + k : a.obs, sl >= 0 ? 4 : 0);
     }
     if (t < kRows) {
-      const int sl = slot[sb * kRows + t];
+      const int sl = slot_ok(tile, t) ? slot[sb * kRows + t] : -1;
       const int n = sl >= 0 ? 4 : 0;
       const int64_t q = sl >= 0 ? sl : 0;
       cpa4(st_f + 0 * kRows + t, a.active + q, n);
@@ -221,8 +223,10 @@ __global__ void __launch_bounds__(kThr, 1) ppo_update_tc_kernel(PpoTcArgs a) {
   };
   slot_load(blockIdx.x, 0);
   slot_load(blockIdx.x + G, 1);
+  asm volatile("cp.async.commit_group;" ::: "memory");
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
   __syncthreads();
-  gather(0);
+  gather(blockIdx.x, 0);
   fence_proxy_async_smem();
   tc_fence_before();
   __syncthreads();
@@ -248,7 +252,7 @@ __global__ void __launch_bounds__(kThr, 1) ppo_update_tc_kernel(PpoTcArgs a) {
     __syncthreads();
     tc_fence_after();
     // ---- staging -> X operand (bf16; column 31 carries the constant 1 of the bias gradient)
-    const bool live = slot[sb * kRows + row] >= 0;
+    const bool live = slot_ok(tile, row);
     float r_w = 0.0f, r_adv = 0.0f, r_lp = 0.0f, r_vt = 0.0f, r_v = 0.0f;
     int r_act = 0;
     uint32_t r_lg[5] = {0, 0, 0, 0, 0};
@@ -277,9 +281,10 @@ __global__ void __launch_bounds__(kThr, 1) ppo_update_tc_kernel(PpoTcArgs a) {
     const int64_t sl_row = slot[sb * kRows + row];
     fence_proxy_async_smem();
     __syncthreads();
-    // the staging area is free: gather the next tile while this one computes
-    gather((it + 1) % 3);
+    // the staging area is free: gather the next tile (and the slots of the one
+    // after it) while this one computes
     slot_load(tile + 2 * G, (it + 2) % 3);
+    gather(tile + G, (it + 1) % 3);
     if (t == 0) {
       tc_fence_after();
       const uint32_t id = idesc_bf16(128, 128);

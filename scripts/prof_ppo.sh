@@ -6,7 +6,7 @@ N=${N:-65536}
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/ppo_launches.csv \
     python scripts/ppo_time.py $N 128 bf16 > gpurun_out/ppo_ncu_run.log 2>&1
 if [ -n "$FULL" ]; then
-  ncu --set full --clock-control none --import-source on -k regex:ppo_branch_tiled -s 2 -c 1 \
+  ncu --set full --clock-control none --import-source on -k regex:ppo_update_tc -s 2 -c 1 \
       -o gpurun_out/ppo_branch_full -f python scripts/ppo_time.py $N 128 bf16 > gpurun_out/ppo_full_run.log 2>&1
 fi
 python - <<'PY'
