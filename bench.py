@@ -376,7 +376,7 @@ def run_gpu_ppo(args, rank, world, local_rank):
     fpr = ppo_flop_per_row(sp.in_dim, sp.critic_in, sp.width, sp.n_actions)
     R = n_envs * A
     upd_s = float(np.mean(upd_ms)) * 1e-3
-    tflops = T * R * 5 * fpr / upd_s / 1e12
+    tflops = T * R * 5 * fpr / upd_s / 1e12  # algorithmic FLOPs (unpadded) per second of update
     # end to end through the public API: step() then the new parameters to the host
     e2e_steps = max(2, min(args.steps, 3))
     t0 = time.perf_counter()
@@ -409,7 +409,7 @@ def run_gpu_ppo(args, rank, world, local_rank):
         "metric": "agent-steps/sec (env-steps/sec x agents)", "value": value, "unit": "agent-steps/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "bf16 rollout policy / f32 PPO update / f64 env", "data": "synthetic (key_from_seed(rank))",
+        "dtype": "bf16 rollout policy + bf16 tcgen05 PPO update (fp32 accumulate) / f64 env", "data": "synthetic (key_from_seed(rank))",
         "config": {"workload": label, "env_id": env_id, "n_envs_per_gpu": n_envs, "agents": A,
                    "rollout_steps": T, "update_epochs": 5, "n_minibatches": 2, "batch_rows": T * R,
                    "step": "one PPO update = collect + update",
@@ -419,7 +419,8 @@ def run_gpu_ppo(args, rank, world, local_rank):
         "update_row_passes_per_sec": T * R * 5 / upd_s,
         "roofline": {"bound": "tensor", "achieved": tflops, "peak": peak, "unit": "TFLOP/s", "frac": tflops / peak,
                      "traffic": None, "peak_source": "MEASURED_PEAKS.json bf16_tflops (dense)",
-                     "kernel": "PPO update phase (ppo_branch_kernel dominant; fp32 CUDA-core math)",
+                     "kernel": "PPO update phase (ppo_update_tc_kernel dominant: bf16 tcgen05 forward, input- "
+                               "and weight-gradient GEMMs, fp32 TMEM accumulation)",
                      "flop_per_row_pass": fpr},
         "cpu_baseline": cpu,
         "e2e": {"value": n_envs * A * T * e2e_steps / sec, "unit": "agent-steps/s", "h2d_bytes_per_step": 0,
