@@ -36,8 +36,9 @@ struct Carry {
 };
 
 struct LaunchCommon {
-  int64_t n;            // local envs
+  int64_t n;            // local envs (also the stride of every [component][N] state array)
   int64_t offset;       // global index of local env 0
+  int64_t begin, end;   // the step kernels process local envs [begin, end) (a chunk of the batch)
   Carry carry;
   StepViews v;
   unsigned long long* stats;  // [3] episode statistics (see stats_add)

@@ -354,10 +354,10 @@ __global__ void __launch_bounds__(kThreads) mpe_step_kernel(MpeState st, LaunchC
   __shared__ uint8_t s_fin[kThreads];
   if (*(volatile int*)lc.err) return;  // a pending contract error freezes the batch
 
-  const int64_t i0 = int64_t(blockIdx.x) * kThreads;
+  const int64_t i0 = lc.begin + int64_t(blockIdx.x) * kThreads;
   const int64_t i = i0 + threadIdx.x;
-  const int nvalid = int(min64(kThreads, lc.n - i0));
-  const bool live = i < lc.n;
+  const int nvalid = int(min64(kThreads, lc.end - i0));
+  const bool live = i < lc.end;
   float* my_obs = s_obs + threadIdx.x * ROW;
 
   Local<Sc> s;
@@ -501,7 +501,7 @@ void mpe_launch_reset(const MpeConfig& c, const MpeState& s, const LaunchCommon&
 
 void mpe_launch_step(const MpeConfig& c, const MpeState& s, const LaunchCommon& lc, bool random,
                      KeyWords step_key) {
-  unsigned g = grid_for(lc.n, kThreads);
+  unsigned g = grid_for(lc.end - lc.begin, kThreads);
   Key k = to_key(step_key);
 #define MARL_MPE_STEP(S)                                                                  \
   random ? mpe_step_kernel<S, true><<<g, kThreads, 0, lc.stream>>>(s, lc, k, c.coop_prey) \

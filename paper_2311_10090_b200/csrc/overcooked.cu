@@ -344,10 +344,10 @@ __global__ void __launch_bounds__(kThreads) oc_step_kernel(OcConfig c, const flo
     for (int idx = lane; idx < 2 * 4 * D; idx += 32) bufs[idx] = t.s[0][idx % D];
     __syncwarp();
   }
-  const int64_t nchunks = (lc.n + 31) >> 5;
+  const int64_t nchunks = (lc.end - lc.begin + 31) >> 5;  // begin is a multiple of 32
   for (int64_t chunk = int64_t(blockIdx.x) * warps + wid; chunk < nchunks; chunk += int64_t(gridDim.x) * warps) {
-    const int64_t w0 = chunk << 5;
-    const int wvalid = int(min64(32, lc.n - w0));
+    const int64_t w0 = lc.begin + (chunk << 5);
+    const int wvalid = int(min64(32, lc.end - w0));
     const int64_t i = w0 + lane;
     const bool mine = lane < wvalid;
 
@@ -535,7 +535,7 @@ void oc_launch_step_t(const OcConfig& c, const float* templ, const OcState& s, c
   cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, warps * 32, sm);
-  const int64_t chunks = (lc.n + 31) / 32;
+  const int64_t chunks = (lc.end - lc.begin + 31) / 32;
   const int64_t want = (chunks + warps - 1) / warps;
   const int64_t cap = int64_t(std::max(per_sm, 1)) * sms;
   fn<<<unsigned(std::min(want, cap)), warps * 32, sm, lc.stream>>>(c, templ, s, lc, to_key(step_key), tma);

@@ -754,11 +754,11 @@ __global__ void __launch_bounds__(kThreads, 3) smax_step_kernel(const Params* __
   const Grp<G> g;
   const int slot = (threadIdx.x >> 5) * EPW + (g.dead ? 0 : (threadIdx.x & 31) / G);
   EnvSm<CAP>& e = reinterpret_cast<EnvSm<CAP>*>(m.envs)[slot];
-  const int64_t i = int64_t(blockIdx.x) * EPB + slot;
-  const int64_t w0 = int64_t(blockIdx.x) * EPB + (threadIdx.x >> 5) * EPW;
-  const int wvalid = int(max(int64_t(0), min64(EPW, lc.n - w0)));
+  const int64_t i = lc.begin + int64_t(blockIdx.x) * EPB + slot;
+  const int64_t w0 = lc.begin + int64_t(blockIdx.x) * EPB + (threadIdx.x >> 5) * EPW;
+  const int wvalid = int(max(int64_t(0), min64(EPW, lc.end - w0)));
   if (wvalid == 0) return;  // whole warp past the end (warp-uniform)
-  const bool live = !g.dead && i < lc.n;
+  const bool live = !g.dead && i < lc.end;
   const int A = P.A;
 
   int tg[UPL], sw[UPL];
@@ -1043,7 +1043,7 @@ void launch_step_g(const SmaxConfig& c, const Params* dP, const SmaxState& s, co
   auto fn = random ? smax_step_kernel<G, UPL, true> : smax_step_kernel<G, UPL, false>;
   cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
   constexpr int EPB = kWarps * Grp<G>::EPW;
-  fn<<<unsigned((lc.n + EPB - 1) / EPB), kThreads, sm, lc.stream>>>(dP, s, lc, k, plan);
+  fn<<<unsigned((lc.end - lc.begin + EPB - 1) / EPB), kThreads, sm, lc.stream>>>(dP, s, lc, k, plan);
 }
 
 #define MARL_SMAX_SHAPES(FN, ...)           \

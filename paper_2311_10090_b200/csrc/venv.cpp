@@ -485,6 +485,8 @@ struct marl_venv {
   OcState oc{};
   float* oc_templ = nullptr;
   std::vector<int32_t> host_actions_scratch;
+  cudaStream_t copy_stream = nullptr;  // host-buffer steps: D2H of finished chunks
+  cudaEvent_t chunk_ev[4] = {nullptr, nullptr, nullptr, nullptr};
 };
 
 namespace {
@@ -495,6 +497,8 @@ LaunchCommon common(marl_venv* h) {
   LaunchCommon lc;
   lc.n = h->n;
   lc.offset = h->off;
+  lc.begin = 0;
+  lc.end = h->n;
   lc.carry = h->carry;
   lc.v = h->v;
   lc.stats = h->stats;
@@ -523,9 +527,12 @@ void check_device_error(marl_venv* h) {
                                std::to_string(idx / A) + " is outside its action space");
 }
 
-void launch_step(marl_venv* h, bool random, const uint32_t* step_key, const int32_t* d_actions) {
+void launch_step(marl_venv* h, bool random, const uint32_t* step_key, const int32_t* d_actions, int64_t begin = 0,
+                 int64_t end = -1) {
   require_state(h);
   LaunchCommon lc = common(h);
+  lc.begin = begin;
+  lc.end = end < 0 ? h->n : end;
   KeyWords k{};
   if (step_key) std::memcpy(k.w, step_key, 16);
   if (!random) lc.v.actions = const_cast<int32_t*>(d_actions);
@@ -535,6 +542,61 @@ void launch_step(marl_venv* h, bool random, const uint32_t* step_key, const int3
     default: oc_launch_step_t(h->env->oc, h->oc_templ, h->oc, lc, random, k); break;
   }
   after_launch();
+}
+
+// Rows [b, e) of every requested output view -> the host buffers, on stream st.
+void download_range(marl_venv* h, const marl_host_step* o, int64_t b, int64_t e, cudaStream_t st) {
+  const Env& E = *h->env;
+  const size_t A = size_t(E.A), D = size_t(E.D), rows = size_t(e - b);
+  auto cp = [&](void* dst, const void* src, size_t row_bytes) {
+    if (dst)
+      cuda_check(cudaMemcpyAsync(static_cast<uint8_t*>(dst) + size_t(b) * row_bytes,
+                                 static_cast<const uint8_t*>(src) + size_t(b) * row_bytes, rows * row_bytes,
+                                 cudaMemcpyDeviceToHost, st),
+                 "cudaMemcpyAsync D2H");
+  };
+  cp(o->obs, h->v.obs, A * D * 4);
+  cp(o->rewards, h->v.rewards, A * 8);
+  cp(o->dones, h->v.dones, A + 1);
+  cp(o->finished, h->v.finished, 1);
+  cp(o->final_obs, h->v.final_obs, A * D * 4);
+  cp(o->final_returns, h->v.final_returns, 8);
+  cp(o->final_lengths, h->v.final_lengths, 4);
+  if (E.n_info) cp(o->infos, h->v.infos, A * size_t(E.n_info) * 8);
+  cp(o->actions, h->v.actions, A * 4);
+}
+
+// A step whose outputs go to host buffers: the batch runs as up to four env
+// chunks on the compute stream and each chunk's rows are copied back on a
+// second stream as soon as its kernel finishes, so the PCIe transfer of one
+// chunk overlaps the step of the next (the step is per-env independent, so
+// chunking changes nothing in the results).
+void step_to_host(marl_venv* h, bool random, const uint32_t* step_key, const int32_t* d_actions,
+                  const marl_host_step* o) {
+  const int64_t n = h->n;
+  const int K = n >= 32768 ? 4 : 1;
+  if (K == 1) {
+    launch_step(h, random, step_key, d_actions);
+    download_range(h, o, 0, n, h->stream);
+    cuda_check(cudaStreamSynchronize(h->stream), "cudaStreamSynchronize");
+    return;
+  }
+  if (!h->copy_stream) {
+    cuda_check(cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking), "cudaStreamCreate");
+    for (auto& ev : h->chunk_ev) cuda_check(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "cudaEventCreate");
+  }
+  int64_t b = 0;
+  for (int c = 0; c < K; ++c) {
+    const int64_t e = c == K - 1 ? n : std::min(n, ((n * (c + 1) / K) + 255) / 256 * 256);
+    if (e <= b) continue;
+    launch_step(h, random, step_key, d_actions, b, e);
+    cuda_check(cudaEventRecord(h->chunk_ev[c], h->stream), "cudaEventRecord");
+    cuda_check(cudaStreamWaitEvent(h->copy_stream, h->chunk_ev[c], 0), "cudaStreamWaitEvent");
+    download_range(h, o, b, e, h->copy_stream);
+    b = e;
+  }
+  cuda_check(cudaStreamSynchronize(h->copy_stream), "cudaStreamSynchronize");
+  cuda_check(cudaStreamSynchronize(h->stream), "cudaStreamSynchronize");
 }
 
 void download(marl_venv* h, const marl_host_step* o) {
@@ -702,6 +764,11 @@ int marl_venv_destroy(marl_venv* h) {
     cudaSetDevice(h->device);
     cudaStreamSynchronize(h->stream);
     if (h->env && h->env->family == MARL_FAMILY_SMAX) smax_release(h->env->smax);
+    if (h->copy_stream) {
+      cudaStreamSynchronize(h->copy_stream);
+      cudaStreamDestroy(h->copy_stream);
+      for (auto ev : h->chunk_ev) cudaEventDestroy(ev);
+    }
     if (h->own_stream) cudaStreamDestroy(h->stream);
     delete h;
   });
@@ -806,18 +873,25 @@ int marl_venv_step_host(marl_venv* h, const int32_t* h_actions, const marl_host_
     }
     cuda_check(cudaMemcpyAsync(h->v.actions, h_actions, size_t(total) * 4, cudaMemcpyHostToDevice, h->stream),
                "cudaMemcpyAsync H2D");
-    launch_step(h, false, nullptr, h->v.actions);
-    if (out) download(h, out);
-    else cuda_check(cudaStreamSynchronize(h->stream), "cudaStreamSynchronize");
+    if (out) {
+      step_to_host(h, false, nullptr, h->v.actions, out);
+    } else {
+      launch_step(h, false, nullptr, h->v.actions);
+      cuda_check(cudaStreamSynchronize(h->stream), "cudaStreamSynchronize");
+    }
   });
 }
 
 int marl_venv_step_random_host(marl_venv* h, const uint32_t step_key[4], const marl_host_step* out) {
   return guarded([&] {
     set_device(h);
-    launch_step(h, true, step_key, nullptr);
-    if (out) download(h, out);
-    else cuda_check(cudaStreamSynchronize(h->stream), "cudaStreamSynchronize");
+    require_state(h);
+    if (out) {
+      step_to_host(h, true, step_key, nullptr, out);
+    } else {
+      launch_step(h, true, step_key, nullptr);
+      cuda_check(cudaStreamSynchronize(h->stream), "cudaStreamSynchronize");
+    }
   });
 }
 

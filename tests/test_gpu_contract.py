@@ -150,3 +150,32 @@ def test_throughput_probe_runs():
     assert res.sps > 0 and np.isfinite(res.sps) and res.cold_seconds > 0
     assert res.csv_row().startswith("MPE_simple_spread_v3,1024,50,")
     assert m.ThroughputResult.csv_header() == "env_id,n_envs,steps,seconds,sps"
+
+
+@pytest.mark.parametrize("env_id,cfg,n", [("SMAX_5m_vs_6m", THREE_M, 40_003), ("MPE_simple_spread_v3", {}, 70_001),
+                                          ("overcooked_cramped_room_v0", {"max_steps": 3}, 33_001)])
+def test_host_buffer_step_matches_device_views(env_id, cfg, n):
+    """The host-buffer step (C-ABI marl_venv_step_random_host / _step_host, run
+    as env chunks whose outputs stream back while later chunks compute) equals
+    the one-launch device step of a twin VectorEnv, every field, exactly."""
+    m = _m()
+    a = m.VectorEnv(env_id, n, config=cfg)
+    b = m.VectorEnv(env_id, n, config=cfg)
+    a.reset(O.key_from_seed(3))
+    b.reset(O.key_from_seed(3))
+    fields = ("obs", "rewards", "dones", "finished", "final_obs", "final_returns", "final_lengths", "infos",
+              "actions")
+    if not a.info_names:
+        fields = tuple(f for f in fields if f != "infos")
+    for k in range(4):
+        key = O.fold_in(O.key_from_seed(9), k)
+        a.step_random(key)
+        want = a.download(fields)
+        got = {f: np.zeros_like(want[f]) for f in fields}
+        if k % 2 == 0:
+            b.host_step_random(key, got)
+        else:
+            b.host_step(want["actions"], got)
+        for f in fields:
+            assert np.array_equal(got[f], want[f]), (k, f)
+    assert np.array_equal(a.state_hash().cpu().numpy(), b.state_hash().cpu().numpy())
