@@ -342,10 +342,21 @@ def run_gpu_ppo(args, rank, world, local_rank):
     env = m.make_env(env_id, cfg)
     A = env.num_agents()
     T = IPPO_T
-    pc = {"n_envs": n_envs, "n_rollout_steps": T, "total_timesteps": (args.warmup + args.steps + 8) * n_envs * T}
-    venv = m.VectorEnv(env, n_envs, device=local_rank)
+    # weak scaling: n_envs per GPU fixed; N > 1 is data-parallel training over env shards with the
+    # update's sums all-reduced over NCCL (identical parameters on every rank)
+    gn = n_envs * world
+    pc = {"n_envs": gn, "n_rollout_steps": T, "total_timesteps": (args.warmup + args.steps + 8) * gn * T}
+    from paper_2311_10090_b200 import dist as shard_mod
+    venv = shard_mod.make_sharded(env, gn, rank, world, device=local_rank) if world > 1 else \
+        m.VectorEnv(env, n_envs, device=local_rank)
     tr = PpoTrainer(venv, pc, False, "bf16")
-    tr.begin(m.prng.key_from_seed(rank))
+    if world > 1:
+        import torch.distributed as tdist
+        from paper_2311_10090_b200.ppo import nccl_unique_id
+        uid = [nccl_unique_id() if rank == 0 else None]
+        tdist.broadcast_object_list(uid, src=0)
+        tr.use_nccl(uid[0], rank, world)
+    tr.begin(m.prng.key_from_seed(0))
     stream = torch.cuda.current_stream()
     for _ in range(args.warmup):
         tr.step()
@@ -413,7 +424,8 @@ def run_gpu_ppo(args, rank, world, local_rank):
         "config": {"workload": label, "env_id": env_id, "n_envs_per_gpu": n_envs, "agents": A,
                    "rollout_steps": T, "update_epochs": 5, "n_minibatches": 2, "batch_rows": T * R,
                    "step": "one PPO update = collect + update",
-                   "parallelism": "replicas only" if world > 1 else "single device",
+                   "parallelism": f"dp{world}: env shards, update sums all-reduced over NCCL" if world > 1
+                   else "single device",
                    "l2": "no flush: the rollout buffer (> 1 GB) is rewritten every step"},
         "collect_ms": float(np.mean(col_ms)), "update_ms": float(np.mean(upd_ms)),
         "update_row_passes_per_sec": T * R * 5 / upd_s,
@@ -423,7 +435,7 @@ def run_gpu_ppo(args, rank, world, local_rank):
                                "and weight-gradient GEMMs, fp32 TMEM accumulation)",
                      "flop_per_row_pass": fpr},
         "cpu_baseline": cpu,
-        "e2e": {"value": n_envs * A * T * e2e_steps / sec, "unit": "agent-steps/s", "h2d_bytes_per_step": 0,
+        "e2e": {"value": world * n_envs * A * T * e2e_steps / sec, "unit": "agent-steps/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": int(a.nbytes + c.nbytes + 12 * 8), "steps": e2e_steps,
                 "path": "PpoTrainer.step + params() (C-ABI marl_ppo_step / marl_ppo_get_params)"},
         "gpu_launches": int(launches),

@@ -279,6 +279,16 @@ int marl_ppo_step(marl_ppo* p, double row[12], int* diverged);  /* collect + upd
  * for device slot indices d_idx[M] over the current window, no optimizer step. */
 int marl_ppo_minibatch_grad(marl_ppo* p, const int32_t* d_idx, int64_t M, float* grad_out, double* stats_out);
 int marl_ppo_destroy(marl_ppo* p);
+/* Data-parallel update over env shards (marl_venv_create_shard; n_envs = the global count): every
+ * rank draws the same global permutation, keeps the minibatch rows it owns and sums advantage
+ * statistics, gradient, loss sums and episode counts over the ranks -- the single-device update's
+ * arithmetic, split by rows.  The exchange is an in-place SUM all-reduce: either a callback (the
+ * stream is synchronised before the call; return 0 with the sums in place) or native NCCL. */
+enum { MARL_DTYPE_F32 = 0, MARL_DTYPE_F64 = 1, MARL_DTYPE_I64 = 2 };
+typedef int (*marl_allreduce_fn)(void* ctx, void* dev_buf, int64_t count, int dtype, void* stream);
+int marl_ppo_set_allreduce(marl_ppo* p, marl_allreduce_fn fn, void* ctx);
+int marl_nccl_unique_id(uint8_t out[128]);
+int marl_ppo_set_nccl(marl_ppo* p, const uint8_t id[128], int rank, int world);
 /* prng::permutation(key, n) (prng.cpp:151-159) into device memory d_out[n] on `device`. */
 int marl_ppo_permutation(const uint32_t key[4], int64_t n, int32_t* d_out, int device);
 

@@ -60,8 +60,13 @@ EXPORTS = [
     "marl_rollout_collect", "marl_rollout_get_views", "marl_rollout_destroy",
     "marl_ppo_create", "marl_ppo_init_nets", "marl_ppo_begin", "marl_ppo_n_updates", "marl_ppo_set_params",
     "marl_ppo_get_params", "marl_ppo_rollout", "marl_ppo_collect", "marl_ppo_update", "marl_ppo_step",
-    "marl_ppo_minibatch_grad", "marl_ppo_destroy", "marl_ppo_permutation",
+    "marl_ppo_minibatch_grad", "marl_ppo_destroy", "marl_ppo_permutation", "marl_ppo_set_allreduce",
+    "marl_nccl_unique_id", "marl_ppo_set_nccl",
 ]
+
+# int (*marl_allreduce_fn)(void* ctx, void* dev_buf, int64_t count, int dtype, void* stream)
+ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_int64, C.c_int, C.c_void_p)
+DTYPE_F32, DTYPE_F64, DTYPE_I64 = 0, 1, 2
 
 _lib = None
 
@@ -131,6 +136,9 @@ def lib() -> C.CDLL:
     L.marl_ppo_minibatch_grad.argtypes = [vp, vp, C.c_int64, f32p, f64p]
     L.marl_ppo_destroy.argtypes = [vp]
     L.marl_ppo_permutation.argtypes = [u32p, C.c_int64, vp, C.c_int]
+    L.marl_ppo_set_allreduce.argtypes = [vp, ALLREDUCE_FN, vp]
+    L.marl_nccl_unique_id.argtypes = [C.POINTER(C.c_uint8)]
+    L.marl_ppo_set_nccl.argtypes = [vp, C.POINTER(C.c_uint8), C.c_int, C.c_int]
     L.marl_last_error.restype = C.c_char_p
     L.marl_launch_count.restype = C.c_uint64
     L.marl_version.restype = C.c_char_p

@@ -4,6 +4,8 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <functional>
+
 #include <cstdint>
 
 namespace marl_b200 {
@@ -283,8 +285,14 @@ size_t ppo_perm_scratch_bytes(int64_t n);
 // prng::permutation(key, n) (prng.cpp:151-159) into out[n] on the device.
 void ppo_permutation(KeyWords key, int64_t n, int32_t* out, void* scratch, size_t scratch_bytes, cudaStream_t st);
 int ppo_stat_blocks(int64_t M);
-void ppo_adv_stats(const RolloutBufs& b, const int32_t* idx, int64_t M, double* part, double* part2, PpoMbStats* st,
-                   cudaStream_t s);
+// g: device double[4] scratch; allreduce (optional): sum g[0:2) then g[2:3) over the data-parallel ranks
+void ppo_adv_stats(const RolloutBufs& b, const int32_t* idx, int64_t M, double* part, double* part2, double* g,
+                   PpoMbStats* st, cudaStream_t s, const std::function<void(double*, int)>& allreduce);
+// sharded update: the global minibatch slots this shard owns, as local slots (order kept), count -> d_count
+size_t ppo_compact_scratch_bytes(int64_t M);
+void ppo_shard_compact(const int32_t* idx, int64_t M, int64_t Rg, int64_t row0, int64_t Rl, int32_t* tmp,
+                       int32_t* out, int64_t* d_count, void* scratch, size_t scratch_bytes, cudaStream_t s);
+void ppo_stats_fold(double* spart, int nparts, cudaStream_t s);
 void ppo_branch_geometry(int in, int W, int out, int* TR, int* staged, size_t* smem);
 int ppo_branch_grid(int in, int W, int out, int64_t M);
 void ppo_branch(PpoBranchArgs a, bool actor, int grid, cudaStream_t s);

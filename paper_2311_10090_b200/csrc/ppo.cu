@@ -31,6 +31,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <functional>
 
 #include "common.cuh"
 #include "engine.h"
@@ -129,28 +130,25 @@ __global__ void adv_sum_kernel(const float* __restrict__ adv, const float* __res
   }
 }
 
-__device__ __forceinline__ void mean_of(const double* part, int nb, double* mean, double* n) {
+// fold the per-block partials in block order: g[0] = sum(w * adv), g[1] = sum(w)
+__global__ void adv_fold_kernel(const double* __restrict__ part, int nb, double* __restrict__ g) {
+  if (threadIdx.x != 0) return;
   double s = 0.0, c = 0.0;
   for (int q = 0; q < nb; ++q) {
     s += part[2 * q];
     c += part[2 * q + 1];
   }
-  *n = c;
-  *mean = c > 0.0 ? s / c : 0.0;
+  g[0] = s;
+  g[1] = c;
 }
 
-// pass 2: sum(w * (adv - mean)^2) (actor_critic.hpp:424-429)
+// pass 2: sum(w * (adv - mean)^2) (actor_critic.hpp:424-429) with the
+// (all-reduced) mean of g
 __global__ void adv_var_kernel(const float* __restrict__ adv, const float* __restrict__ active,
-                               const int32_t* __restrict__ idx, int64_t M, const double* __restrict__ part, int nb,
+                               const int32_t* __restrict__ idx, int64_t M, const double* __restrict__ g,
                                double* __restrict__ part2) {
   __shared__ double sh[32];
-  __shared__ double s_mean;
-  if (threadIdx.x == 0) {
-    double n;
-    mean_of(part, nb, &s_mean, &n);
-  }
-  __syncthreads();
-  const double mean = s_mean;
+  const double mean = g[1] > 0.0 ? g[0] / g[1] : 0.0;
   double v = 0.0;
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < M; i += int64_t(gridDim.x) * blockDim.x) {
     const int64_t r = idx[i];
@@ -161,17 +159,42 @@ __global__ void adv_var_kernel(const float* __restrict__ adv, const float* __res
   if (threadIdx.x == 0) part2[blockIdx.x] = v;
 }
 
-__global__ void adv_final_kernel(const double* __restrict__ part, const double* __restrict__ part2, int nb,
-                                 PpoMbStats* st) {
+__global__ void adv_fold2_kernel(const double* __restrict__ part2, int nb, double* __restrict__ g) {
   if (threadIdx.x != 0) return;
-  double mean, n;
-  mean_of(part, nb, &mean, &n);
-  double var = 0.0;
-  for (int q = 0; q < nb; ++q) var += part2[q];
+  double v = 0.0;
+  for (int q = 0; q < nb; ++q) v += part2[q];
+  g[2] = v;
+}
+
+__global__ void adv_final_kernel(const double* __restrict__ g, PpoMbStats* st) {
+  if (threadIdx.x != 0) return;
+  const double n = g[1];
   st->total_w = n;
   st->normalize = n > 0.0 ? 1 : 0;  // n <= 0: advantages left as they are
-  st->mean = mean;
-  st->std = n > 0.0 ? sqrt(var / n) : 0.0;
+  st->mean = n > 0.0 ? g[0] / n : 0.0;
+  st->std = n > 0.0 ? sqrt(g[2] / n) : 0.0;
+}
+
+// global minibatch slots (t*R_g + r_g) -> this shard's local slots (t*R_l + r_g - row0) or -1
+__global__ void shard_map_kernel(const int32_t* __restrict__ idx, int64_t M, int64_t Rg, int64_t row0, int64_t Rl,
+                                 int32_t* __restrict__ out) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= M) return;
+  const int64_t s = idx[i], t = s / Rg, r = s - t * Rg - row0;
+  out[i] = (r >= 0 && r < Rl) ? int32_t(t * Rl + r) : -1;
+}
+
+struct NonNegative {
+  __device__ __forceinline__ bool operator()(const int32_t x) const { return x >= 0; }
+};
+
+// sum the per-CTA loss statistics into row 0 (the sharded path all-reduces that row)
+__global__ void stats_fold_kernel(double* __restrict__ sp, int nparts) {
+  const int k = threadIdx.x;
+  if (k >= 6) return;
+  double v = 0.0;
+  for (int c = 0; c < nparts; ++c) v += sp[size_t(c) * 6 + k];
+  sp[k] = v;  // thread k owns column k
 }
 
 // ----------------------------------------------------------- branch kernel
@@ -976,13 +999,37 @@ void ppo_permutation(KeyWords key, int64_t n, int32_t* out, void* scratch, size_
 
 int ppo_stat_blocks(int64_t M) { return int(std::min<int64_t>(std::max<int64_t>((M + 255) / 256, 1), 1184)); }
 
-void ppo_adv_stats(const RolloutBufs& b, const int32_t* idx, int64_t M, double* part, double* part2, PpoMbStats* st,
-                   cudaStream_t s) {
+void ppo_adv_stats(const RolloutBufs& b, const int32_t* idx, int64_t M, double* part, double* part2, double* g,
+                   PpoMbStats* st, cudaStream_t s, const std::function<void(double*, int)>& allreduce) {
   const int nb = ppo_stat_blocks(M);
   adv_sum_kernel<<<nb, kRedThreads, 0, s>>>(b.adv, b.active, idx, M, part);
-  adv_var_kernel<<<nb, kRedThreads, 0, s>>>(b.adv, b.active, idx, M, part, nb, part2);
-  adv_final_kernel<<<1, 32, 0, s>>>(part, part2, nb, st);
-  g_launches += 3;
+  adv_fold_kernel<<<1, 32, 0, s>>>(part, nb, g);
+  if (allreduce) allreduce(g, 2);
+  adv_var_kernel<<<nb, kRedThreads, 0, s>>>(b.adv, b.active, idx, M, g, part2);
+  adv_fold2_kernel<<<1, 32, 0, s>>>(part2, nb, g);
+  if (allreduce) allreduce(g + 2, 1);
+  adv_final_kernel<<<1, 32, 0, s>>>(g, st);
+  g_launches += 6;
+}
+
+size_t ppo_compact_scratch_bytes(int64_t M) {
+  size_t temp = 0;
+  cub::DeviceSelect::If(nullptr, temp, static_cast<const int32_t*>(nullptr), static_cast<int32_t*>(nullptr),
+                        static_cast<int64_t*>(nullptr), int(std::max<int64_t>(M, 1)), NonNegative());
+  return temp + 256;
+}
+
+void ppo_shard_compact(const int32_t* idx, int64_t M, int64_t Rg, int64_t row0, int64_t Rl, int32_t* tmp,
+                       int32_t* out, int64_t* d_count, void* scratch, size_t scratch_bytes, cudaStream_t s) {
+  shard_map_kernel<<<blocks_for(std::max<int64_t>(M, 1), 256), 256, 0, s>>>(idx, M, Rg, row0, Rl, tmp);
+  size_t temp = scratch_bytes;
+  cub::DeviceSelect::If(scratch, temp, static_cast<const int32_t*>(tmp), out, d_count, int(M), NonNegative(), s);
+  g_launches += 2;
+}
+
+void ppo_stats_fold(double* spart, int nparts, cudaStream_t s) {
+  stats_fold_kernel<<<1, 32, 0, s>>>(spart, nparts);
+  ++g_launches;
 }
 
 // Tile geometry of a branch: the largest TR in {64, 32, 16, 8} whose smem fits.

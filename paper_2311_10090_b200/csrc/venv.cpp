@@ -5,6 +5,8 @@
 // dynamics: every reset/step is a kernel launch (mpe.cu, smax.cu,
 // overcooked.cu); a missing GPU is a MARL_ERR_CUDA, never a CPU fallback.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <cmath>
@@ -1514,12 +1516,85 @@ struct marl_ppo {
   uint8_t* perm_scratch = nullptr;
   size_t perm_scratch_bytes = 0;
   int* flags = nullptr;  // [0] diverged, [1] illegal stored action
-  ~marl_ppo() {
-    if (ro) marl_rollout_destroy(ro);
-  }
+  // data-parallel update over env shards: the global permutation's rows this
+  // shard owns; sums all-reduced through `hook` (a callback or native NCCL)
+  bool sharded = false;
+  int64_t R_local = 0, R_global = 0, row0 = 0;
+  int32_t *cmp_tmp = nullptr, *cmp_out = nullptr;
+  int64_t* cmp_count = nullptr;
+  uint8_t* cmp_scratch = nullptr;
+  size_t cmp_scratch_bytes = 0;
+  double* adv_g = nullptr;      // [4] advantage sums (all-reduced)
+  int64_t* ep_dev = nullptr;    // [3] episode statistics (all-reduced)
+  marl_allreduce_fn hook = nullptr;
+  void* hook_ctx = nullptr;
+  void* nccl_comm = nullptr;
+  ~marl_ppo();
 };
 
 namespace {
+
+// (definition below, after the NCCL loader)
+// NCCL, loaded at run time (the process's libnccl.so.2 -- torch's, when torch
+// is loaded -- so the library has no link-time NCCL dependency).
+struct Nccl {
+  void* lib = nullptr;
+  ncclResult_t (*get_unique_id)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*comm_init_rank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*all_reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) =
+      nullptr;
+  ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
+  const char* (*error_string)(ncclResult_t) = nullptr;
+};
+
+const Nccl& nccl() {
+  static Nccl n = [] {
+    Nccl x;
+    for (const char* name : {"libnccl.so.2", "libnccl.so"}) {
+      x.lib = dlopen(name, RTLD_NOW | RTLD_GLOBAL);
+      if (x.lib) break;
+    }
+    if (!x.lib) return x;
+    x.get_unique_id = reinterpret_cast<decltype(x.get_unique_id)>(dlsym(x.lib, "ncclGetUniqueId"));
+    x.comm_init_rank = reinterpret_cast<decltype(x.comm_init_rank)>(dlsym(x.lib, "ncclCommInitRank"));
+    x.all_reduce = reinterpret_cast<decltype(x.all_reduce)>(dlsym(x.lib, "ncclAllReduce"));
+    x.comm_destroy = reinterpret_cast<decltype(x.comm_destroy)>(dlsym(x.lib, "ncclCommDestroy"));
+    x.error_string = reinterpret_cast<decltype(x.error_string)>(dlsym(x.lib, "ncclGetErrorString"));
+    return x;
+  }();
+  if (!n.lib || !n.comm_init_rank || !n.all_reduce || !n.get_unique_id)
+    raise(MARL_ERR_CUDA, "NCCL (libnccl.so.2) is not loadable in this process");
+  return n;
+}
+
+// the native hook: an in-place NCCL sum on the trainer's stream (no host sync)
+int nccl_hook(void* ctx, void* buf, int64_t count, int dtype, void* stream) {
+  const Nccl& n = nccl();
+  const ncclDataType_t t = dtype == MARL_DTYPE_F32 ? ncclFloat32 : dtype == MARL_DTYPE_F64 ? ncclFloat64 : ncclInt64;
+  const ncclResult_t r = n.all_reduce(buf, buf, size_t(count), t, ncclSum, static_cast<ncclComm_t>(ctx),
+                                      static_cast<cudaStream_t>(stream));
+  return r == ncclSuccess ? 0 : int(r);
+}
+
+}  // namespace
+
+marl_ppo::~marl_ppo() {
+  if (nccl_comm) nccl().comm_destroy(static_cast<ncclComm_t>(nccl_comm));
+  if (ro) marl_rollout_destroy(ro);
+}
+
+namespace {
+
+// Sum `count` values at device `buf` over the data-parallel ranks.  A user
+// hook sees the stream already synchronised and must return with the sum in
+// place; the native NCCL hook is stream-ordered.
+void allreduce(marl_ppo* p, void* buf, int64_t count, int dtype) {
+  if (!p->hook) return;
+  cudaStream_t st = p->h->stream;
+  if (p->hook != nccl_hook) cuda_check(cudaStreamSynchronize(st), "cudaStreamSynchronize");
+  const int rc = p->hook(p->hook_ctx, buf, count, dtype, st);
+  if (rc != 0) raise(MARL_ERR_CUDA, "ppo: all-reduce hook failed (" + std::to_string(rc) + ")");
+}
 
 PpoBranchArgs branch_args(marl_ppo* p, bool actor, const int32_t* idx, int64_t M) {
   marl_rollout* r = p->ro;
@@ -1550,9 +1625,23 @@ PpoBranchArgs branch_args(marl_ppo* p, bool actor, const int32_t* idx, int64_t M
 }
 
 // ff_minibatch's gradient (ppo.cpp:409-441) into p->grad (actor | critic).
-void minibatch_grad(marl_ppo* p, const int32_t* idx, int64_t M) {
+// global: idx are slots of the GLOBAL rollout (t*R_global + r); a sharded
+// trainer keeps the ones it owns and all-reduces the sums.
+void minibatch_grad(marl_ppo* p, const int32_t* idx, int64_t M, bool global = false) {
   cudaStream_t st = p->h->stream;
-  ppo_adv_stats(p->ro->b, idx, M, p->adv_part, p->adv_part2, p->mbst, st);
+  if (global && p->sharded) {
+    ppo_shard_compact(idx, M, p->R_global, p->row0, p->R_local, p->cmp_tmp, p->cmp_out, p->cmp_count,
+                      p->cmp_scratch, p->cmp_scratch_bytes, st);
+    after_launch();
+    int64_t m_local = 0;
+    cuda_check(cudaMemcpyAsync(&m_local, p->cmp_count, 8, cudaMemcpyDeviceToHost, st), "D2H");
+    cuda_check(cudaStreamSynchronize(st), "cudaStreamSynchronize");
+    idx = p->cmp_out;
+    M = m_local;
+  }
+  std::function<void(double*, int)> red;
+  if (p->hook) red = [p](double* g, int n) { allreduce(p, g, n, MARL_DTYPE_F64); };
+  ppo_adv_stats(p->ro->b, idx, M, p->adv_part, p->adv_part2, p->adv_g, p->mbst, st, red);
   if (p->tc) {
     const marl_rollout* r = p->ro;
     PpoTcArgs a{};
@@ -1588,6 +1677,14 @@ void minibatch_grad(marl_ppo* p, const int32_t* idx, int64_t M) {
   ppo_grad_reduce(p->gpart_a, p->grid_a, p->Pa, p->grad, st);
   ppo_grad_reduce(p->gpart_c, p->grid_c, p->Pc, p->grad + p->Pa, st);
   after_launch();
+  if (p->hook) {  // the data-parallel exchange: gradient and loss sums over the ranks
+    ppo_stats_fold(p->spart_a, p->grid_a, st);
+    ppo_stats_fold(p->spart_c, p->grid_c, st);
+    after_launch();
+    allreduce(p, p->grad, p->P, MARL_DTYPE_F32);
+    allreduce(p, p->spart_a, 6, MARL_DTYPE_F64);
+    allreduce(p, p->spart_c, 6, MARL_DTYPE_F64);
+  }
 }
 
 // clip_global_norm + adam_update for one minibatch (ppo.cpp:605-608).
@@ -1602,8 +1699,8 @@ void minibatch_apply(marl_ppo* p, double lr_u, double* metrics_slot) {
   a.P = p->P;
   a.actor_stats = p->spart_a;
   a.critic_stats = p->spart_c;
-  a.n_actor_parts = p->grid_a;
-  a.n_critic_parts = p->grid_c;
+  a.n_actor_parts = p->hook ? 1 : p->grid_a;  // folded + all-reduced into row 0
+  a.n_critic_parts = p->hook ? 1 : p->grid_c;
   a.st = p->mbst;
   a.vf_coef = p->cfg.vf_coef;
   a.ent_coef = p->cfg.ent_coef;
@@ -1634,6 +1731,12 @@ void ppo_collect_impl(marl_ppo* p) {
   };
   collect_impl(p->ro, p->update * p->cfg.n_rollout_steps, p->cfg.gamma, p->cfg.gae_lambda, shaping_at);
   if (marl_venv_episode_stats(h, s, 1) != MARL_OK) raise(MARL_ERR_CUDA, marl_last_error());
+  if (p->hook) {  // episodes finished on every shard
+    cuda_check(cudaMemcpy(p->ep_dev, s, sizeof s, cudaMemcpyHostToDevice), "cudaMemcpy");
+    allreduce(p, p->ep_dev, 3, MARL_DTYPE_I64);
+    cuda_check(cudaStreamSynchronize(h->stream), "cudaStreamSynchronize");
+    cuda_check(cudaMemcpy(s, p->ep_dev, sizeof s, cudaMemcpyDeviceToHost), "cudaMemcpy");
+  }
   p->window_episodes = s[0];
   p->window_return = double(s[2]) / 16777216.0;  // stats keep returns in 2^-24 fixed point
   p->collected = true;
@@ -1658,7 +1761,7 @@ void ppo_update_impl(marl_ppo* p, double row[12], int* diverged) {
     ppo_permutation(kw, p->batch, p->perm, p->perm_scratch, p->perm_scratch_bytes, st);
     after_launch();
     for (int mb = 0; mb < c.n_minibatches; ++mb, ++k) {
-      minibatch_grad(p, p->perm + size_t(mb) * size_t(p->per), p->per);
+      minibatch_grad(p, p->perm + size_t(mb) * size_t(p->per), p->per, true);
       minibatch_apply(p, lr_u, p->metrics + size_t(k) * 8);
     }
   }
@@ -1705,8 +1808,8 @@ int marl_ppo_create(marl_venv* h, const char* ppo_config_json, int centralized, 
     if (!h || !out) raise(MARL_ERR_CONTRACT, "marl_ppo_create: NULL argument");
     PpoCfg c = parse_ppo_config(ppo_config_json);
     if (c.recurrent) raise(MARL_ERR_SCHEMA, "ppo: the B200 update implements feed-forward policies (recurrent=false)");
-    if (int64_t(c.n_envs) != h->gn) raise(MARL_ERR_CONTRACT, "ppo: n_envs must equal the VectorEnv's env count");
-    if (h->n != h->gn) raise(MARL_ERR_CONTRACT, "ppo: the device update runs on an unsharded VectorEnv");
+    if (int64_t(c.n_envs) != h->gn)
+      raise(MARL_ERR_CONTRACT, "ppo: n_envs must equal the VectorEnv's (global) env count");
     set_device(h);
     auto p = std::make_unique<marl_ppo>();
     p->h = h;
@@ -1720,7 +1823,11 @@ int marl_ppo_create(marl_venv* h, const char* ppo_config_json, int centralized, 
     if (r->n_act > kPpoMaxAct) raise(MARL_ERR_SCHEMA, "ppo: more than 64 actions");
     const int64_t steps_per_update = int64_t(c.n_envs) * int64_t(c.n_rollout_steps);
     p->n_updates = c.total_timesteps / steps_per_update;
-    p->batch = int64_t(c.n_rollout_steps) * r->R;
+    p->R_local = r->R;
+    p->R_global = r->R_global;
+    p->row0 = r->row0;
+    p->sharded = r->R != r->R_global;
+    p->batch = int64_t(c.n_rollout_steps) * r->R_global;  // the permutation spans the global rollout
     if (p->batch % c.n_minibatches != 0)
       raise(MARL_ERR_SCHEMA, "ppo: batch size (" + std::to_string(p->batch) + ") must be divisible by n_minibatches (" +
                                  std::to_string(c.n_minibatches) + ")");
@@ -1757,6 +1864,15 @@ int marl_ppo_create(marl_venv* h, const char* ppo_config_json, int centralized, 
     ar.add(&p->perm, size_t(p->batch));
     ar.add(&p->perm_scratch, p->perm_scratch_bytes);
     ar.add(&p->flags, 2);
+    ar.add(&p->adv_g, 4);
+    ar.add(&p->ep_dev, 3);
+    if (p->sharded) {
+      p->cmp_scratch_bytes = ppo_compact_scratch_bytes(p->per);
+      ar.add(&p->cmp_tmp, size_t(p->per));
+      ar.add(&p->cmp_out, size_t(p->per));
+      ar.add(&p->cmp_count, 1);
+      ar.add(&p->cmp_scratch, p->cmp_scratch_bytes);
+    }
     ar.commit();
     *out = p.release();
   });
@@ -1901,6 +2017,46 @@ int marl_ppo_minibatch_grad(marl_ppo* p, const int32_t* d_idx, int64_t M, float*
     } else {
       for (int j = 0; j < 6; ++j) stats_out[j] = 0.0;
     }
+  });
+}
+
+// Data-parallel update: sum the update's exchanges (advantage sums, gradient,
+// loss sums, episode counts) over the ranks with a caller-supplied all-reduce.
+int marl_ppo_set_allreduce(marl_ppo* p, marl_allreduce_fn fn, void* ctx) {
+  return guarded([&] {
+    if (!p) raise(MARL_ERR_CONTRACT, "marl_ppo_set_allreduce: NULL handle");
+    p->hook = fn;
+    p->hook_ctx = ctx;
+  });
+}
+
+int marl_nccl_unique_id(uint8_t out[128]) {
+  return guarded([&] {
+    if (!out) raise(MARL_ERR_CONTRACT, "marl_nccl_unique_id: NULL argument");
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId");
+    ncclUniqueId id;
+    const ncclResult_t r = nccl().get_unique_id(&id);
+    if (r != ncclSuccess) raise(MARL_ERR_CUDA, std::string("ncclGetUniqueId: ") + nccl().error_string(r));
+    std::memcpy(out, &id, 128);
+  });
+}
+
+// The native exchange: an NCCL communicator over `world` ranks (one GPU each)
+// whose all-reduces are stream-ordered with the update kernels.
+int marl_ppo_set_nccl(marl_ppo* p, const uint8_t id[128], int rank, int world) {
+  return guarded([&] {
+    if (!p || !id) raise(MARL_ERR_CONTRACT, "marl_ppo_set_nccl: NULL argument");
+    if (world < 1 || rank < 0 || rank >= world) raise(MARL_ERR_CONTRACT, "marl_ppo_set_nccl: bad rank / world");
+    set_device(p->h);
+    ncclUniqueId uid;
+    std::memcpy(&uid, id, 128);
+    ncclComm_t comm = nullptr;
+    const ncclResult_t r = nccl().comm_init_rank(&comm, world, uid, rank);
+    if (r != ncclSuccess) raise(MARL_ERR_CUDA, std::string("ncclCommInitRank: ") + nccl().error_string(r));
+    if (p->nccl_comm) nccl().comm_destroy(static_cast<ncclComm_t>(p->nccl_comm));
+    p->nccl_comm = comm;
+    p->hook = nccl_hook;
+    p->hook_ctx = comm;
   });
 }
 

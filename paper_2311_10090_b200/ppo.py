@@ -167,6 +167,33 @@ class PpoTrainer:
                                                 _fp(g, C.c_float), _fp(st, C.c_double)))
         return g, st
 
+    # ---- data-parallel update over env shards
+    def set_allreduce(self, fn) -> None:
+        """fn(buf: torch cuda tensor view) -> None sums the view in place over
+        the ranks; called (stream synchronised) at each exchange of the update:
+        advantage sums, gradient, loss sums, episode counts."""
+        import torch
+        dev = self.venv._device
+        dts = {N.DTYPE_F32: torch.float32, N.DTYPE_F64: torch.float64, N.DTYPE_I64: torch.int64}
+
+        def cb(ctx, ptr, count, dtype, stream):
+            try:
+                t = _device_tensor(ptr, int(count), dts[dtype], dev)
+                fn(t)
+                return 0
+            except Exception:  # never unwind through the C frames
+                import traceback
+                traceback.print_exc()
+                return 1
+
+        self._hook = N.ALLREDUCE_FN(cb)  # kept alive with the trainer
+        N.check(N.lib().marl_ppo_set_allreduce(self._h, self._hook, None))
+
+    def use_nccl(self, unique_id: bytes, rank: int, world: int) -> None:
+        """The native exchange: NCCL all-reduces stream-ordered with the update."""
+        buf = (C.c_uint8 * 128).from_buffer_copy(bytes(unique_id))
+        N.check(N.lib().marl_ppo_set_nccl(self._h, buf, int(rank), int(world)))
+
     def train(self, key) -> PpoRunResult:
         self.begin(key)
         table = MetricTable()
@@ -180,6 +207,33 @@ class PpoTrainer:
                 break
         a, c = self.params()
         return PpoRunResult(a, c, table, diverged, steps)
+
+
+def nccl_unique_id() -> bytes:
+    buf = (C.c_uint8 * 128)()
+    N.check(N.lib().marl_nccl_unique_id(buf))
+    return bytes(buf)
+
+
+def _device_tensor(ptr: int, count: int, dtype, device: int):
+    """A zero-copy torch view of `count` elements at device address ptr."""
+    import torch
+    from .venv import _DevArray
+    ts = {torch.float32: "<f4", torch.float64: "<f8", torch.int64: "<i8"}[dtype]
+    return torch.as_tensor(_DevArray(int(ptr), (count,), ts), device=f"cuda:{device}")
+
+
+def torch_allreduce(group=None):
+    """An exchange through torch.distributed (any backend that reduces CUDA
+    tensors): sum in place, then synchronise."""
+    import torch
+    import torch.distributed as dist
+
+    def fn(t):
+        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+        if t.is_cuda:
+            torch.cuda.synchronize(t.device)
+    return fn
 
 
 def _train(env, config, key, centralized, device, precision):
