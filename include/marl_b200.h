@@ -168,6 +168,14 @@ int marl_venv_step_random_host(marl_venv* h, const uint32_t step_key[4], const m
 int marl_venv_download(marl_venv* h, const marl_host_step* out);
 
 int marl_venv_views(marl_venv* h, marl_views* out);
+/* Box action spaces (MPE continuous_actions, mpe.cpp:91-99): actions are [N][A][action_dim] f32,
+ * agent a's first n_actions[a] entries in [0, 1] (SpaceDescriptor::contains, spaces.cpp:36-46),
+ * the rest padding.  action_dim = 0 for discrete envs.  marl_venv_step_random draws
+ * space.sample(fold_in(env_key, j)) (vector_env.cpp:179-181) into the f32 action view. */
+int marl_venv_action_dim(const marl_venv* h, int32_t* out);
+int marl_venv_actions_f32(marl_venv* h, float** out);                 /* device [N][A][action_dim] */
+int marl_venv_step_continuous(marl_venv* h, const float* d_actions);  /* VectorEnv::step, device */
+int marl_venv_step_continuous_host(marl_venv* h, const float* h_actions, const marl_host_step* out);
 /* Synchronous copy of `bytes` from a device pointer (e.g. a marl_views field)
  * to host memory: lets C/C++ callers without the CUDA runtime read views
  * (used by the reference-side adapter include/marl_b200_vector_env.hpp). */

@@ -59,6 +59,7 @@ class VectorEnv {
       throw_status(marl_venv_agent(h, a, name, sizeof name, &obs_size, &n_act));
       agents_.emplace_back(name);
       obs_size_.push_back(obs_size);
+      n_actions_.push_back(n_act);  // discrete n, or the box's flat size
     }
     for (int k = 0; k < spec_.n_info; ++k) {
       char name[128];
@@ -87,13 +88,25 @@ class VectorEnv {
                              const std::vector<marl::AgentMap<marl::Action>>& actions) const {
     if (state.keys.size() != size_t(n_envs_) || actions.size() != size_t(n_envs_))
       throw marl::ContractError("VectorEnv::step: batch size mismatch");
-    std::vector<int32_t> flat(size_t(n_envs_) * spec_.n_agents);
+    int32_t box = 0;  // > 0: box action spaces (continuous MPE), rows of `box` floats
+    throw_status(marl_venv_action_dim(h_.get(), &box));
+    std::vector<int32_t> flat(box ? 0 : size_t(n_envs_) * spec_.n_agents);
+    std::vector<float> flat_f(box ? size_t(n_envs_) * spec_.n_agents * size_t(box) : 0, 0.0f);
     for (int e = 0; e < n_envs_; ++e)
       for (int a = 0; a < spec_.n_agents; ++a) {
         const marl::Action& act = actions[size_t(e)].at(agents_[size_t(a)]);
-        if (!std::holds_alternative<int>(act))
-          throw marl::ContractError("VectorEnv::step: marl-b200 implements discrete actions only");
-        flat[size_t(e) * spec_.n_agents + a] = std::get<int>(act);
+        if (box) {  // Env::validate_actions: the vector must have the space's flat size
+          const auto* v = std::get_if<std::vector<float>>(&act);
+          if (!v || v->size() > size_t(box) || int(v->size()) != n_actions_[size_t(a)])
+            throw marl::ContractError(env_->id() + ": action for agent '" + agents_[size_t(a)] +
+                                      "' is outside its action space");
+          std::copy(v->begin(), v->end(), flat_f.begin() + (size_t(e) * spec_.n_agents + a) * size_t(box));
+        } else {
+          if (!std::holds_alternative<int>(act))
+            throw marl::ContractError(env_->id() + ": action for agent '" + agents_[size_t(a)] +
+                                      "' is outside its action space");
+          flat[size_t(e) * spec_.n_agents + a] = std::get<int>(act);
+        }
       }
     const size_t N = size_t(n_envs_), A = size_t(spec_.n_agents), D = size_t(spec_.obs_dim);
     std::vector<float> obs(N * A * D), final_obs(N * A * D);
@@ -102,7 +115,10 @@ class VectorEnv {
     std::vector<int32_t> final_lengths(N);
     marl_host_step out{obs.data(), rewards.data(), dones.data(), finished.data(), final_obs.data(),
                        final_returns.data(), final_lengths.data(), infos.data(), nullptr};
-    throw_status(marl_venv_step_host(h_.get(), flat.data(), &out));
+    if (box)
+      throw_status(marl_venv_step_continuous_host(h_.get(), flat_f.data(), &out));
+    else
+      throw_status(marl_venv_step_host(h_.get(), flat.data(), &out));
 
     marl::StepBatchResult r;
     r.obs = unflatten_obs(obs.data());
@@ -175,7 +191,7 @@ class VectorEnv {
   std::shared_ptr<marl_venv> h_;
   marl_spec spec_{};
   std::vector<std::string> agents_, info_names_;
-  std::vector<int32_t> obs_size_;
+  std::vector<int32_t> obs_size_, n_actions_;
 };
 
 }  // namespace marl_b200

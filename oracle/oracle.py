@@ -357,8 +357,11 @@ def ref_lib():
         L.mref_legal.argtypes = [C.c_void_p, _u8p]
         L.mref_world_state.argtypes = [C.c_void_p, _f32p, _P(C.c_int)]
         L.mref_random_actions.argtypes = [C.c_void_p, _u32p, _i32p]
+        L.mref_random_actions_box.argtypes = [C.c_void_p, _u32p, C.c_int, _f32p]
         L.mref_step.argtypes = [C.c_void_p, _i32p, _f32p, _f64p, _u8p, _u8p, _f32p, _f64p, _i32p,
                                 _f64p, C.c_int, _f64p, _i32p, _u32p, _u64p]
+        L.mref_step_box.argtypes = [C.c_void_p, _f32p, C.c_int, _f32p, _f64p, _u8p, _u8p, _f32p, _f64p, _i32p,
+                                    _f64p, C.c_int, _f64p, _i32p, _u32p, _u64p]
         L.mref_probe.argtypes = [C.c_char_p, C.c_char_p, C.c_int, C.c_int, _u32p, _f64p, _f64p]
         L.mref_threefry.argtypes = [C.c_uint32] * 4 + [_u32p]
         L.mref_split.argtypes = [_u32p, C.c_uint64, _u32p]
@@ -438,13 +441,25 @@ class RefVenv:
         self._chk(ref_lib().mref_world_state(self.h, _ptr(out, C.c_float), C.byref(w)))
         return out
 
+    BOX_DIM = 5  # the engine's padded box-action row (continuous MPE)
+
+    def random_actions_box(self, step_key):
+        act = np.zeros((self.n, self.n_agents, self.BOX_DIM), np.float32)
+        self._chk(ref_lib().mref_random_actions_box(self.h, _ptr(_key(step_key), C.c_uint32), self.BOX_DIM,
+                                                    _ptr(act, C.c_float)))
+        return act
+
     def step(self, actions):
-        actions = np.ascontiguousarray(actions, dtype=np.int32)
+        actions = np.asarray(actions)
+        box = actions.dtype.kind == "f"
+        actions = np.ascontiguousarray(actions, dtype=np.float32 if box else np.int32)
         o = _alloc_step(self.n, self.n_agents, self.obs_dim, self.n_info)
         ret = np.zeros(self.n, np.float64)
         ln = np.zeros(self.n, np.int32)
-        self._chk(ref_lib().mref_step(
-            self.h, _ptr(actions, C.c_int32), _ptr(o["obs"], C.c_float), _ptr(o["rewards"], C.c_double),
+        fn = ref_lib().mref_step_box if box else ref_lib().mref_step
+        head = [self.h, _ptr(actions, C.c_float), self.BOX_DIM] if box else [self.h, _ptr(actions, C.c_int32)]
+        self._chk(fn(
+            *head, _ptr(o["obs"], C.c_float), _ptr(o["rewards"], C.c_double),
             _ptr(o["dones"], C.c_uint8), _ptr(o["finished"], C.c_uint8), _ptr(o["final_obs"], C.c_float),
             _ptr(o["final_returns"], C.c_double), _ptr(o["final_lengths"], C.c_int32),
             _ptr(o["infos"], C.c_double), self.n_info, _ptr(ret, C.c_double), _ptr(ln, C.c_int32),

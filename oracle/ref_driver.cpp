@@ -190,16 +190,16 @@ int mref_random_actions(void* p, const uint32_t step_key[4], int32_t* actions) {
 
 // VectorEnv::step with explicit actions [N][A] i32; every output optional.
 // infos: [N][A][n_info] f64 in std::map key order minus episode_*.
-int mref_step(void* p, const int32_t* actions, float* obs, double* rewards, uint8_t* dones,
-              uint8_t* finished, float* final_obs, double* final_returns, int32_t* final_lengths,
-              double* infos, int n_info, double* ep_returns, int32_t* ep_lengths, uint32_t* keys,
-              uint64_t* hashes) {
-  auto* h = static_cast<Handle*>(p);
-  return guarded([&] {
-    std::vector<AgentMap<Action>> acts(size_t(h->n));
-    for (int i = 0; i < h->n; ++i)
-      for (int a = 0; a < h->A; ++a)
-        acts[size_t(i)].emplace(h->env->agents()[size_t(a)], int(actions[size_t(i) * h->A + a]));
+}  // extern "C"
+
+namespace {
+#define MREF_STEP_OUTS                                                                                     \
+  float *obs, double *rewards, uint8_t *dones, uint8_t *finished, float *final_obs, double *final_returns, \
+      int32_t *final_lengths, double *infos, int n_info, double *ep_returns, int32_t *ep_lengths,         \
+      uint32_t *keys, uint64_t *hashes
+
+void step_and_emit(Handle* h, const std::vector<AgentMap<Action>>& acts, MREF_STEP_OUTS) {
+  {
     StepBatchResult r = h->venv->step(h->state, acts);
     for (int i = 0; i < h->n; ++i) {
       size_t ui = size_t(i);
@@ -229,6 +229,60 @@ int mref_step(void* p, const int32_t* actions, float* obs, double* rewards, uint
       if (hashes) hashes[ui] = h->env->state_hash(*r.next.states[ui]);
     }
     h->state = std::move(r.next);
+  }
+}
+}  // namespace
+
+extern "C" {
+
+// VectorEnv::step with explicit discrete actions [N][A] i32; every output optional.
+// infos: [N][A][n_info] f64 in std::map key order minus episode_*.
+int mref_step(void* p, const int32_t* actions, MREF_STEP_OUTS) {
+  auto* h = static_cast<Handle*>(p);
+  return guarded([&] {
+    std::vector<AgentMap<Action>> acts(size_t(h->n));
+    for (int i = 0; i < h->n; ++i)
+      for (int a = 0; a < h->A; ++a)
+        acts[size_t(i)].emplace(h->env->agents()[size_t(a)], int(actions[size_t(i) * h->A + a]));
+    step_and_emit(h, acts, obs, rewards, dones, finished, final_obs, final_returns, final_lengths, infos, n_info,
+                  ep_returns, ep_lengths, keys, hashes);
+  });
+}
+
+// The same with box actions [N][A][dim] f32: agent a's vector is its first
+// action_space(a).flat_size() floats.
+int mref_step_box(void* p, const float* actions, int dim, MREF_STEP_OUTS) {
+  auto* h = static_cast<Handle*>(p);
+  return guarded([&] {
+    std::vector<AgentMap<Action>> acts(size_t(h->n));
+    for (int i = 0; i < h->n; ++i)
+      for (int a = 0; a < h->A; ++a) {
+        const auto& ag = h->env->agents()[size_t(a)];
+        const int n = h->env->action_space(ag).flat_size();
+        const float* v = actions + (size_t(i) * h->A + a) * size_t(dim);
+        acts[size_t(i)].emplace(ag, std::vector<float>(v, v + n));
+      }
+    step_and_emit(h, acts, obs, rewards, dones, finished, final_obs, final_returns, final_lengths, infos, n_info,
+                  ep_returns, ep_lengths, keys, hashes);
+  });
+}
+
+// random_legal_actions for box spaces: space.sample(fold_in(env_key, j))
+// (vector_env.cpp:179-181), [N][A][dim] f32 zero-padded.
+int mref_random_actions_box(void* p, const uint32_t step_key[4], int dim, float* actions) {
+  auto* h = static_cast<Handle*>(p);
+  return guarded([&] {
+    auto env_keys = prng::split(to_key(step_key), size_t(h->n));
+    for (int i = 0; i < h->n; ++i) {
+      uint64_t j = 0;
+      for (const auto& agent : h->env->agents()) {
+        auto act = h->env->action_space(agent).sample(prng::fold_in(env_keys[size_t(i)], j));
+        const auto& v = std::get<std::vector<float>>(act);
+        float* o = actions + (size_t(i) * h->A + j) * size_t(dim);
+        for (int k = 0; k < dim; ++k) o[k] = k < int(v.size()) ? v[size_t(k)] : 0.0f;
+        ++j;
+      }
+    }
   });
 }
 

@@ -28,7 +28,12 @@ struct StepViews {
   int32_t* final_lengths;
   double* infos;
   int32_t* actions;
+  float* actions_f;  // [N][A][kBoxActDim] box actions (continuous MPE), else null
 };
+
+// Box action rows (continuous MPE, mpe.cpp:91-99): every agent's flat vector
+// padded to the widest (movement: 5 floats in [0, 1]; speaker: dim_c floats).
+constexpr int kBoxActDim = 5;
 
 // BatchedState carry (vector_env.hpp:13-20) beside the env-specific state.
 struct Carry {
@@ -62,6 +67,7 @@ struct MpeState {
 struct MpeConfig {
   int scenario;
   int coop_prey;
+  int continuous;  // box action spaces (continuous_actions, mpe.cpp:398)
 };
 
 int mpe_obs_dim(int scenario);
@@ -303,6 +309,10 @@ void ppo_clip_adam(const PpoApplyArgs& a, cudaStream_t s);
 // Device-side Env::validate_actions (env.cpp:7-14): n_actions per agent.
 void launch_validate(const int32_t* actions, int64_t n, int A, const int32_t* n_actions_dev,
                      int* err, cudaStream_t st);
+// Box spaces (SpaceDescriptor::contains, spaces.cpp:36-46): the first
+// flat_size[a] floats of every [kBoxActDim] row finite and in [0, 1].
+void launch_validate_box(const float* actions, int64_t n, int A, const int32_t* flat_size_dev, int* err,
+                         cudaStream_t st);
 
 // Kernel launches issued by this library since load (evidence counter).
 extern unsigned long long g_launches;

@@ -218,9 +218,11 @@ __device__ __forceinline__ double reward(const Local<Sc>& s, int i, bool coop_pr
   return rew;
 }
 
-// MpeEnv::step physics (mpe.cpp:137-214), in place.
-template <class Sc>
-__device__ __forceinline__ void physics(Local<Sc>& s, const int* act) {
+// MpeEnv::step physics (mpe.cpp:137-214), in place.  CONT: box actions, the
+// agent's row of kBoxActDim floats (u = (v1 - v2, v3 - v4), comm = v[0:dim_c],
+// mpe.cpp:144-166); else discrete ids.
+template <class Sc, bool CONT>
+__device__ __forceinline__ void physics(Local<Sc>& s, const int* act, const float* actf) {
   double force[2 * Sc::E];
 #pragma unroll
   for (int q = 0; q < 2 * Sc::E; ++q) force[q] = 0.0;
@@ -228,11 +230,17 @@ __device__ __forceinline__ void physics(Local<Sc>& s, const int* act) {
   for (int i = 0; i < Sc::A; ++i) {
     if (Sc::movable(i)) {
       double u0 = 0.0, u1 = 0.0;
-      int a = act[i];
-      if (a == 1) u0 = -1.0;
-      if (a == 2) u0 = +1.0;
-      if (a == 3) u1 = -1.0;
-      if (a == 4) u1 = +1.0;
+      if (CONT) {
+        const float* v = actf + i * kBoxActDim;
+        u0 = double(v[1]) - double(v[2]);
+        u1 = double(v[3]) - double(v[4]);
+      } else {
+        int a = act[i];
+        if (a == 1) u0 = -1.0;
+        if (a == 2) u0 = +1.0;
+        if (a == 3) u1 = -1.0;
+        if (a == 4) u1 = +1.0;
+      }
       constexpr double dflt = kDefaultSens;
       double sens = Sc::accel(i) > 0 ? Sc::accel(i) : dflt;
       force[2 * i] += u0 * sens;
@@ -240,7 +248,8 @@ __device__ __forceinline__ void physics(Local<Sc>& s, const int* act) {
     }
     if (!Sc::silent(i)) {
 #pragma unroll
-      for (int c = 0; c < Sc::DC; ++c) s.comm[i * Sc::DC + c] = c == act[i] ? 1.0 : 0.0;
+      for (int c = 0; c < Sc::DC; ++c)
+        s.comm[i * Sc::DC + c] = CONT ? double(actf[i * kBoxActDim + c]) : (c == act[i] ? 1.0 : 0.0);
     }
   }
 #pragma unroll
@@ -342,7 +351,7 @@ __global__ void __launch_bounds__(kThreads) mpe_reset_kernel(MpeState st, Launch
   block_store(lc.v.obs + i0 * ROW, s_obs, size_t(nvalid) * ROW * sizeof(float));
 }
 
-template <int S, bool RANDOM>
+template <int S, bool RANDOM, bool CONT>
 __global__ void __launch_bounds__(kThreads) mpe_step_kernel(MpeState st, LaunchCommon lc, Key step_key,
                                                             int coop_prey) {
   using Sc = Scen<S>;
@@ -373,7 +382,31 @@ __global__ void __launch_bounds__(kThreads) mpe_step_kernel(MpeState st, LaunchC
     load_state<Sc, S>(s, st, i, lc.n);
 
     int act[A];
-    if (RANDOM) {
+    float actf[CONT ? A * kBoxActDim : 1];
+    if (RANDOM && CONT) {
+      // box spaces: space.sample(fold_in(env_key, j)) = float(uniform(key, flat, 0, 1))
+      // (vector_env.cpp:179-181, spaces.cpp:48-54)
+      Key ek = split_child(step_key, uint64_t(lc.offset + i));
+#pragma unroll
+      for (int j = 0; j < A; ++j) {
+        const Key kj = fold_in(ek, uint64_t(j));
+#pragma unroll
+        for (int k = 0; k < kBoxActDim; ++k)
+          actf[j * kBoxActDim + k] = k < Sc::n_actions(j) ? float(uniform_at(kj, uint64_t(k), 0.0, 1.0)) : 0.0f;
+      }
+      float4* dst = reinterpret_cast<float4*>(lc.v.actions_f + i * A * kBoxActDim);
+      if ((A * kBoxActDim) % 4 == 0) {
+#pragma unroll
+        for (int q = 0; q < A * kBoxActDim / 4; ++q)
+          dst[q] = make_float4(actf[4 * q], actf[4 * q + 1], actf[4 * q + 2], actf[4 * q + 3]);
+      } else {
+#pragma unroll
+        for (int q = 0; q < A * kBoxActDim; ++q) lc.v.actions_f[i * A * kBoxActDim + q] = actf[q];
+      }
+    } else if (CONT) {
+#pragma unroll
+      for (int q = 0; q < A * kBoxActDim; ++q) actf[q] = lc.v.actions_f[i * A * kBoxActDim + q];
+    } else if (RANDOM) {
       // random_legal_actions (vector_env.cpp:169-187); MPE masks are all-legal
       // (env.hpp:71-73) so the draw is bits(env_key, j) % n_actions.
       Key ek = split_child(step_key, uint64_t(lc.offset + i));
@@ -387,7 +420,7 @@ __global__ void __launch_bounds__(kThreads) mpe_step_kernel(MpeState st, LaunchC
       for (int j = 0; j < A; ++j) act[j] = lc.v.actions[i * A + j];
     }
 
-    physics<Sc>(s, act);
+    physics<Sc, CONT>(s, act, actf);
     done = s.steps >= kEpisodeSteps;
     double sum = 0.0;
 #pragma unroll
@@ -436,7 +469,7 @@ __global__ void __launch_bounds__(kThreads) mpe_step_kernel(MpeState st, LaunchC
   tile_store(lc.v.obs + i0 * ROW, s_obs, size_t(nvalid) * ROW * sizeof(float));
   tile_store(lc.v.rewards + i0 * A, s_rew, size_t(nvalid) * A * sizeof(double));
   tile_store(lc.v.dones + i0 * (A + 1), s_done, size_t(nvalid) * (A + 1));
-  if (RANDOM) tile_store(lc.v.actions + i0 * A, s_act, size_t(nvalid) * A * sizeof(int32_t));
+  if (RANDOM && !CONT) tile_store(lc.v.actions + i0 * A, s_act, size_t(nvalid) * A * sizeof(int32_t));
   tile_store_drain();
 }
 
@@ -504,8 +537,10 @@ void mpe_launch_step(const MpeConfig& c, const MpeState& s, const LaunchCommon& 
   unsigned g = grid_for(lc.end - lc.begin, kThreads);
   Key k = to_key(step_key);
 #define MARL_MPE_STEP(S)                                                                  \
-  random ? mpe_step_kernel<S, true><<<g, kThreads, 0, lc.stream>>>(s, lc, k, c.coop_prey) \
-         : mpe_step_kernel<S, false><<<g, kThreads, 0, lc.stream>>>(s, lc, k, c.coop_prey)
+  c.continuous ? (random ? mpe_step_kernel<S, true, true><<<g, kThreads, 0, lc.stream>>>(s, lc, k, c.coop_prey)   \
+                         : mpe_step_kernel<S, false, true><<<g, kThreads, 0, lc.stream>>>(s, lc, k, c.coop_prey)) \
+               : (random ? mpe_step_kernel<S, true, false><<<g, kThreads, 0, lc.stream>>>(s, lc, k, c.coop_prey)  \
+                         : mpe_step_kernel<S, false, false><<<g, kThreads, 0, lc.stream>>>(s, lc, k, c.coop_prey))
   switch (c.scenario) {
     case kMpeSpread: MARL_MPE_STEP(kMpeSpread); break;
     case kMpeSpeakerListener: MARL_MPE_STEP(kMpeSpeakerListener); break;

@@ -27,6 +27,31 @@ __global__ void validate_kernel(const int32_t* __restrict__ actions, int64_t tot
 }
 }  // namespace
 
+namespace {
+__global__ void validate_box_kernel(const float* __restrict__ actions, int64_t total, int A,
+                                    const int32_t* __restrict__ flat, int* err) {
+  const int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;  // (env, agent)
+  if (idx >= total) return;
+  const int a = int(idx % A), n = __ldg(flat + a);
+  bool ok = true;
+  for (int k = 0; k < n; ++k) {
+    const float v = actions[idx * kBoxActDim + k];
+    ok = ok && v >= 0.0f && v <= 1.0f && isfinite(v);
+  }
+  if (!ok) {
+    atomicMin(err + 1, int(min64(idx, 0x7fffffff)));
+    atomicExch(err + 0, 3);
+  }
+}
+}  // namespace
+
+void launch_validate_box(const float* actions, int64_t n, int A, const int32_t* flat_size_dev, int* err,
+                         cudaStream_t st) {
+  const int64_t total = n * A;
+  validate_box_kernel<<<unsigned((total + 255) / 256), 256, 0, st>>>(actions, total, A, flat_size_dev, err);
+  ++g_launches;
+}
+
 void launch_validate(const int32_t* actions, int64_t n, int A, const int32_t* n_actions_dev, int* err,
                      cudaStream_t st) {
   int64_t total = n * A;

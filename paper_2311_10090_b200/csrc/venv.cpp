@@ -193,7 +193,8 @@ struct Env {  // resolved make_env(id, config)
   int A = 0, D = 0, n_info = 0, max_steps = 0;
   bool cooperative = false;
   std::vector<std::string> agents, info_names;
-  std::vector<int> obs_size, n_actions;
+  std::vector<int> obs_size, n_actions;  // n_actions: discrete n, or the box's flat size
+  bool continuous = false;               // box action spaces (continuous MPE)
   MpeConfig mpe{};
   SmaxConfig smax{};
   OcConfig oc{};
@@ -206,11 +207,11 @@ void make_mpe(Env& e, const std::string& scen, const json& cfg) {  // mpe.cpp:45
   bool continuous = v.get_bool("continuous_actions", false);
   bool coop = s == kMpeTag ? v.get_bool("cooperative_prey_reward", false) : false;
   v.check_no_extras();
-  if (continuous)
-    raise(MARL_ERR_SCHEMA, "MPE " + scen + ": continuous_actions=true is not implemented by the B200 engine");
   e.family = MARL_FAMILY_MPE;
   e.mpe.scenario = s;
   e.mpe.coop_prey = coop;
+  e.mpe.continuous = continuous ? 1 : 0;
+  e.continuous = continuous;
   e.A = mpe_n_agents(s);
   e.D = mpe_obs_dim(s);
   e.max_steps = 25;
@@ -529,7 +530,8 @@ void check_device_error(marl_venv* h) {
                                std::to_string(idx / A) + " is outside its action space");
 }
 
-void launch_step(marl_venv* h, bool random, const uint32_t* step_key, const int32_t* d_actions, int64_t begin = 0,
+// d_actions: [N][A] int32 ids, or [N][A][kBoxActDim] floats for box action spaces
+void launch_step(marl_venv* h, bool random, const uint32_t* step_key, const void* d_actions, int64_t begin = 0,
                  int64_t end = -1) {
   require_state(h);
   LaunchCommon lc = common(h);
@@ -537,7 +539,12 @@ void launch_step(marl_venv* h, bool random, const uint32_t* step_key, const int3
   lc.end = end < 0 ? h->n : end;
   KeyWords k{};
   if (step_key) std::memcpy(k.w, step_key, 16);
-  if (!random) lc.v.actions = const_cast<int32_t*>(d_actions);
+  if (!random) {
+    if (h->env->continuous)
+      lc.v.actions_f = static_cast<float*>(const_cast<void*>(d_actions));
+    else
+      lc.v.actions = static_cast<int32_t*>(const_cast<void*>(d_actions));
+  }
   switch (h->env->family) {
     case MARL_FAMILY_MPE: mpe_launch_step(h->env->mpe, h->mpe, lc, random, k); break;
     case MARL_FAMILY_SMAX: smax_launch_step(h->env->smax, h->smax, lc, random, k); break;
@@ -573,7 +580,7 @@ void download_range(marl_venv* h, const marl_host_step* o, int64_t b, int64_t e,
 // second stream as soon as its kernel finishes, so the PCIe transfer of one
 // chunk overlaps the step of the next (the step is per-env independent, so
 // chunking changes nothing in the results).
-void step_to_host(marl_venv* h, bool random, const uint32_t* step_key, const int32_t* d_actions,
+void step_to_host(marl_venv* h, bool random, const uint32_t* step_key, const void* d_actions,
                   const marl_host_step* o) {
   const int64_t n = h->n;
   const int K = n >= 32768 ? 4 : 1;
@@ -650,6 +657,7 @@ void create(const char* env_id, const char* cfg, int64_t n_local, int64_t offset
   ar.add(&h->v.final_lengths, N);
   ar.add(&h->v.infos, N * A * size_t(std::max(e.n_info, 1)));
   ar.add(&h->v.actions, N * A);
+  if (e.continuous) ar.add(&h->v.actions_f, N * A * size_t(kBoxActDim));
   ar.add(&h->carry.keys, N);
   ar.add(&h->carry.ep_return, N);
   ar.add(&h->carry.ep_length, N);
@@ -848,6 +856,8 @@ int marl_venv_step(marl_venv* h, const int32_t* d_actions) {
     set_device(h);
     require_state(h);
     if (!d_actions) raise(MARL_ERR_CONTRACT, "VectorEnv::step: actions is NULL");
+    if (h->env->continuous)
+      raise(MARL_ERR_CONTRACT, h->env->id + ": box action spaces take float actions (marl_venv_step_continuous)");
     launch_validate(d_actions, h->n, h->env->A, h->n_actions_dev, h->err, h->stream);
     after_launch();
     launch_step(h, false, nullptr, d_actions);
@@ -866,6 +876,8 @@ int marl_venv_step_host(marl_venv* h, const int32_t* h_actions, const marl_host_
     set_device(h);
     require_state(h);
     const Env& e = *h->env;
+    if (e.continuous)
+      raise(MARL_ERR_CONTRACT, e.id + ": box action spaces take float actions (marl_venv_step_continuous_host)");
     const int64_t total = h->n * e.A;
     for (int64_t q = 0; q < total; ++q) {  // Env::validate_actions, env.cpp:7-14
       int a = int(q % e.A);
@@ -892,6 +904,62 @@ int marl_venv_step_random_host(marl_venv* h, const uint32_t step_key[4], const m
       step_to_host(h, true, step_key, nullptr, out);
     } else {
       launch_step(h, true, step_key, nullptr);
+      cuda_check(cudaStreamSynchronize(h->stream), "cudaStreamSynchronize");
+    }
+  });
+}
+
+// ---- box action spaces (continuous MPE, mpe.cpp:91-99, 144-166)
+int marl_venv_action_dim(const marl_venv* h, int32_t* out) {
+  return guarded([&] {
+    if (!h || !out) raise(MARL_ERR_CONTRACT, "marl_venv_action_dim: NULL argument");
+    *out = h->env->continuous ? kBoxActDim : 0;
+  });
+}
+
+int marl_venv_actions_f32(marl_venv* h, float** out) {
+  return guarded([&] {
+    if (!h || !out) raise(MARL_ERR_CONTRACT, "marl_venv_actions_f32: NULL argument");
+    *out = h->v.actions_f;
+  });
+}
+
+int marl_venv_step_continuous(marl_venv* h, const float* d_actions) {
+  return guarded([&] {
+    set_device(h);
+    require_state(h);
+    if (!d_actions) raise(MARL_ERR_CONTRACT, "VectorEnv::step: actions is NULL");
+    if (!h->env->continuous) raise(MARL_ERR_CONTRACT, h->env->id + ": discrete action spaces take int32 actions");
+    launch_validate_box(d_actions, h->n, h->env->A, h->n_actions_dev, h->err, h->stream);
+    after_launch();
+    launch_step(h, false, nullptr, d_actions);
+  });
+}
+
+int marl_venv_step_continuous_host(marl_venv* h, const float* h_actions, const marl_host_step* out) {
+  return guarded([&] {
+    set_device(h);
+    require_state(h);
+    const Env& e = *h->env;
+    if (!h_actions) raise(MARL_ERR_CONTRACT, "VectorEnv::step: actions is NULL");
+    if (!e.continuous) raise(MARL_ERR_CONTRACT, e.id + ": discrete action spaces take int32 actions");
+    const int64_t rows = h->n * e.A;
+    for (int64_t q = 0; q < rows; ++q) {  // Env::validate_actions -> SpaceDescriptor::contains (spaces.cpp:36-46)
+      const int a = int(q % e.A);
+      for (int k = 0; k < e.n_actions[size_t(a)]; ++k) {
+        const float v = h_actions[q * kBoxActDim + k];
+        if (!(v >= 0.0f && v <= 1.0f) || !std::isfinite(v))
+          raise(MARL_ERR_CONTRACT, e.id + ": action for agent '" + e.agents[size_t(a)] + "' of env " +
+                                       std::to_string(q / e.A) + " is outside its action space");
+      }
+    }
+    cuda_check(cudaMemcpyAsync(h->v.actions_f, h_actions, size_t(rows) * kBoxActDim * 4, cudaMemcpyHostToDevice,
+                               h->stream),
+               "cudaMemcpyAsync H2D");
+    if (out) {
+      step_to_host(h, false, nullptr, h->v.actions_f, out);
+    } else {
+      launch_step(h, false, nullptr, h->v.actions_f);
       cuda_check(cudaStreamSynchronize(h->stream), "cudaStreamSynchronize");
     }
   });
@@ -1075,6 +1143,8 @@ int marl_rollout_create(marl_venv* h, int T, int width, int n_layers, int relu, 
     marl_policy_spec ps{};
     if (marl_rollout_policy_spec(h, width, n_layers, relu, centralized, &ps) != MARL_OK)
       raise(MARL_ERR_SCHEMA, marl_last_error());
+    if (h->env->continuous)
+      raise(MARL_ERR_SCHEMA, "rollout: the PPO policy is categorical; box action spaces are not supported");
     if (centralized && precision == 1)
       raise(MARL_ERR_SCHEMA, "rollout: the tcgen05 bf16 policy serves IPPO; use precision 0 for MAPPO");
     if (ps.critic_in > 1024) raise(MARL_ERR_SCHEMA, "rollout: critic input wider than 1024");

@@ -199,6 +199,14 @@ class VectorEnv:
             "final_lengths": ((n,), "<i4"), "infos": ((n, A, I), "<f8"), "actions": ((n, A), "<i4"),
             "keys": ((n, 4), "<i4"), "episode_returns": ((n,), "<f8"), "episode_lengths": ((n,), "<i4"),
         }
+        ad = C.c_int32()
+        N.check(L.marl_venv_action_dim(self._h, C.byref(ad)))
+        self.action_dim = int(ad.value)  # > 0: box action spaces ([N, A, action_dim] f32 actions)
+        if self.action_dim:
+            pf = C.POINTER(C.c_float)()
+            N.check(L.marl_venv_actions_f32(self._h, C.byref(pf)))
+            self._actions_f_ptr = C.cast(pf, C.c_void_p).value
+            self._shapes["actions_f"] = ((n, A, self.action_dim), "<f4")
         self.info_names = []
         buf = C.create_string_buffer(64)
         for k in range(I):
@@ -234,7 +242,7 @@ class VectorEnv:
         t = cache.get(name)
         if t is None:
             shape, ts = self._shapes[name]
-            ptr = getattr(self._views, name)
+            ptr = self._actions_f_ptr if name == "actions_f" else getattr(self._views, name)
             t = cache[name] = self._torch.as_tensor(_DevArray(ptr, shape, ts), device=f"cuda:{self._device}")
         return t
 
@@ -245,7 +253,8 @@ class VectorEnv:
     def _result(self) -> StepBatchResult:
         g = self.view
         return StepBatchResult(g("obs"), g("rewards"), g("dones"), g("infos"), g("finished"), g("final_obs"),
-                               g("final_returns"), g("final_lengths"), g("actions"), self._state(),
+                               g("final_returns"), g("final_lengths"),
+                               g("actions_f") if self.action_dim else g("actions"), self._state(),
                                list(self.info_names))
 
     # ---- hot path
@@ -268,6 +277,8 @@ class VectorEnv:
         self._check_state(state)
         L = N.lib()
         t = self._torch
+        if self.action_dim:
+            return self._step_box(actions, sync)
         if t is not None and isinstance(actions, t.Tensor) and actions.is_cuda:
             if tuple(actions.shape) != (self._n, self._env.num_agents()):
                 raise ContractError(f"VectorEnv::step: expected actions of shape {(self._n, self._env.num_agents())}")
@@ -281,6 +292,27 @@ class VectorEnv:
                 raise ContractError(f"VectorEnv::step: expected {self._n} action rows of "
                                     f"{self._env.num_agents()} agents, got shape {a.shape}")
             N.check(L.marl_venv_step_host(self._h, C.c_void_p(a.ctypes.data), None))
+        self._version += 1
+        return self._result()
+
+    def _step_box(self, actions, sync: bool) -> StepBatchResult:
+        """Box action spaces: [N, A, action_dim] float32, agent a's first
+        n_actions[a] entries in [0, 1] (spaces.cpp:36-46)."""
+        L = N.lib()
+        t = self._torch
+        shape = (self._n, self._env.num_agents(), self.action_dim)
+        if t is not None and isinstance(actions, t.Tensor) and actions.is_cuda:
+            if tuple(actions.shape) != shape:
+                raise ContractError(f"VectorEnv::step: expected box actions of shape {shape}")
+            a = actions.to(t.float32).contiguous()
+            N.check(L.marl_venv_step_continuous(self._h, C.c_void_p(a.data_ptr())))
+            if sync:
+                N.check(L.marl_venv_sync(self._h))
+        else:
+            a = np.ascontiguousarray(np.asarray(actions, dtype=np.float32))
+            if a.shape != shape:
+                raise ContractError(f"VectorEnv::step: expected box actions of shape {shape}, got {a.shape}")
+            N.check(L.marl_venv_step_continuous_host(self._h, C.c_void_p(a.ctypes.data), None))
         self._version += 1
         return self._result()
 
@@ -353,8 +385,12 @@ class VectorEnv:
         hs = N.HostStep()
         for f, arr in out.items():
             setattr(hs, f, arr.ctypes.data)
-        a = np.ascontiguousarray(actions, dtype=np.int32)
-        N.check(N.lib().marl_venv_step_host(self._h, C.c_void_p(a.ctypes.data), C.byref(hs)))
+        if self.action_dim:
+            a = np.ascontiguousarray(actions, dtype=np.float32)
+            N.check(N.lib().marl_venv_step_continuous_host(self._h, C.c_void_p(a.ctypes.data), C.byref(hs)))
+        else:
+            a = np.ascontiguousarray(actions, dtype=np.int32)
+            N.check(N.lib().marl_venv_step_host(self._h, C.c_void_p(a.ctypes.data), C.byref(hs)))
         self._version += 1
 
     def keys_numpy(self) -> np.ndarray:

@@ -8,7 +8,9 @@ timeout 900 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu_${TAG}.log 
 for w in smax3m mpe mpe_large overcooked smax2s3z smax27m ippo; do
   timeout 600 python bench.py --workload $w --steps 30 --warmup 5 2>/dev/null | grep '^{' >> gpurun_out/bench_${TAG}.jsonl
 done
+timeout 600 python bench.py --workload ppo --steps 10 --warmup 3 2>/dev/null | grep '^{' >> gpurun_out/bench_${TAG}.jsonl
 timeout 300 python bench.py --impl reference --workload smax3m --steps 3 --warmup 1 2>/dev/null | grep '^{' >> gpurun_out/bench_${TAG}.jsonl
+timeout 300 python bench.py --impl reference --workload ppo --steps 2 --warmup 3 2>/dev/null | grep '^{' >> gpurun_out/bench_${TAG}.jsonl
 wc -l gpurun_out/bench_${TAG}.jsonl
 NCU=/usr/local/cuda/bin/ncu
 for w in smax3m mpe_large overcooked smax27m; do
@@ -21,4 +23,6 @@ for w in smax3m mpe_large overcooked smax27m; do
     > /dev/null 2>&1
 done
 bash scripts/prof_ippo.sh ${TAG} > /dev/null 2>&1
+timeout 600 $NCU --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_${TAG}_ppo.csv \
+  python bench.py --workload ppo --steps 1 --warmup 3 --no-cpu > /dev/null 2>&1
 ls gpurun_out | grep ${TAG}
