@@ -266,7 +266,7 @@ int marl_rollout_destroy(marl_rollout* r);
  * ff_minibatch + ppo_row_loss + ff_backward (ppo.cpp:409-441,
  * actor_critic.hpp:340-412), clip_global_norm + Adam (nn.hpp:417-452), the
  * DivergenceError rollback (ppo.cpp:630-634) and the per-update metrics row.
- * Feed-forward policies only (recurrent = true is a SchemaError). */
+ * Feed-forward and recurrent (GRU) policies. */
 typedef struct marl_ppo marl_ppo;
 /* n_envs in the config must equal the VectorEnv's env count. precision as marl_rollout_create. */
 int marl_ppo_create(marl_venv* h, const char* ppo_config_json, int centralized, int precision, marl_ppo** out);
@@ -275,6 +275,11 @@ int marl_ppo_init_nets(int in_dim, int critic_in, int n_actions, int fc_width, i
                        float* actor, float* critic);
 int marl_ppo_begin(marl_ppo* p, const uint32_t key[4]);  /* nets fold_in(key,10), collector fold_in(key,11) */
 int marl_ppo_n_updates(const marl_ppo* p, int64_t* out);  /* total_timesteps / (n_envs * n_rollout_steps) */
+int marl_ppo_param_counts(const marl_ppo* p, int32_t* n_actor, int32_t* n_critic);
+/* recurrent=true: RnnBranch nets (embed fc_width, GRU hidden_width, post, head; actor_critic.hpp:74-200)
+ * trained by rnn_minibatch (ppo.cpp:444-509), fp32; ppo_init_nets for that spec into host arrays: */
+int marl_ppo_init_rnn(int in_dim, int critic_in, int n_actions, int fc_width, int hidden_width, const uint32_t key[4],
+                      float* actor, float* critic);
 int marl_ppo_set_params(marl_ppo* p, const float* actor, const float* critic);
 int marl_ppo_get_params(marl_ppo* p, float* actor, float* critic);
 int marl_ppo_rollout(marl_ppo* p, marl_rollout** out);  /* borrowed: views of the current window */

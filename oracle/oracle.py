@@ -376,11 +376,13 @@ def ref_lib():
                                    C.c_double, C.c_double, C.c_double, _f32p, _i32p, _f32p, _u8p, _u8p, _f32p,
                                    _f32p, _u8p, _f32p, _f32p, _f32p, _f64p, _P(C.c_int64)]
         L.mref_permutation.argtypes = [_u32p, C.c_int, _i32p]
+        L.mref_ppo_init_rnn.argtypes = [C.c_char_p, C.c_char_p, C.c_int, C.c_int, C.c_int, _u32p, _f32p, _f32p,
+                                        _P(C.c_int), _P(C.c_int)]
         L.mref_ff_minibatch.argtypes = [C.c_char_p, C.c_char_p, C.c_int, _f32p, _f32p, _f32p, _f32p, _i32p, _f32p,
                                         _f32p, _f32p, _f32p, _f32p, _u8p, _i32p, C.c_int, C.c_double, C.c_double,
                                         C.c_double, _f32p, _f64p]
         L.mref_train.argtypes = [C.c_char_p, C.c_char_p, C.c_char_p, C.c_int, _u32p, _f64p, C.c_int,
-                                 _P(C.c_int), _f32p, _f32p, _P(C.c_int), _P(C.c_int64)]
+                                 _P(C.c_int), _f32p, _P(C.c_int), _f32p, _P(C.c_int), _P(C.c_int), _P(C.c_int64)]
         _ref = L
     return _ref
 
@@ -591,14 +593,34 @@ def ref_ff_minibatch(env_id, config, actor, critic, buf, idx, clip_eps=0.3, ent_
 def ref_train(env_id, config, ppo_config, key, centralized=False, max_rows=4096):
     """The reference's train_ippo / train_mappo (ppo.cpp:518-651)."""
     L = ref_lib()
-    sp = ref_ppo_spec(env_id, config, centralized)
     m = np.zeros((max_rows, 12), np.float64)
-    a = np.zeros(sp["n_actor"], np.float32)
-    c = np.zeros(sp["n_critic"], np.float32)
+    a = np.zeros(1 << 20, np.float32)  # capacities; the reference reports the true sizes
+    c = np.zeros(1 << 20, np.float32)
+    na, nc = C.c_int(a.size), C.c_int(c.size)
     nr, dv, sd = C.c_int(), C.c_int(), C.c_int64()
     rc = L.mref_train(env_id.encode(), json.dumps(config or {}).encode(), json.dumps(ppo_config).encode(),
                       int(centralized), _ptr(_key(key), C.c_uint32), _ptr(m, C.c_double), max_rows, C.byref(nr),
-                      _ptr(a, C.c_float), _ptr(c, C.c_float), C.byref(dv), C.byref(sd))
+                      _ptr(a, C.c_float), C.byref(na), _ptr(c, C.c_float), C.byref(nc), C.byref(dv), C.byref(sd))
     if rc:
         raise RuntimeError(L.mref_rollout_last_error().decode())
+    if na.value > a.size or nc.value > c.size:
+        raise RuntimeError("ref_train: parameter buffers too small")
+    a, c = a[: na.value].copy(), c[: nc.value].copy()
     return {"metrics": m[:nr.value], "actor": a, "critic": c, "diverged": bool(dv.value), "steps_done": sd.value}
+
+
+def ref_ppo_init_rnn(env_id, config, key, fc_width=64, hidden_width=128, centralized=False):
+    """ppo_init_nets for a recurrent spec, packed (pack_actor, pack_critic)."""
+    L = ref_lib()
+    na, nc = C.c_int(), C.c_int()
+    args = (env_id.encode(), json.dumps(config or {}).encode(), int(centralized), fc_width, hidden_width,
+            _ptr(_key(key), C.c_uint32))
+    rc = L.mref_ppo_init_rnn(*args, None, None, C.byref(na), C.byref(nc))
+    if rc:
+        raise RuntimeError(L.mref_rollout_last_error().decode())
+    a = np.zeros(na.value, np.float32)
+    c = np.zeros(nc.value, np.float32)
+    rc = L.mref_ppo_init_rnn(*args, _ptr(a, C.c_float), _ptr(c, C.c_float), C.byref(na), C.byref(nc))
+    if rc:
+        raise RuntimeError(L.mref_rollout_last_error().decode())
+    return a, c

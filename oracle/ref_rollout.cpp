@@ -230,6 +230,24 @@ int mref_collect(const char* env_id, const char* cfg, int centralized, float* o_
 }
 
 // ---------------------------------------------------------------- PPO update
+// ppo_init_nets(key, spec) for a recurrent spec (PpoConfig recurrent=true, fc_width, hidden_width).
+int mref_ppo_init_rnn(const char* env_id, const char* cfg, int centralized, int fc_width, int hidden_width,
+                      const uint32_t key[4], float* actor, float* critic, int* n_actor, int* n_critic) {
+  return guarded([&] {
+    auto env = make_env(env_id, parse(cfg));
+    PpoConfig pc;
+    pc.recurrent = true;
+    pc.fc_width = fc_width;
+    pc.hidden_width = hidden_width;
+    PpoNets nets = ppo_init_nets(key_of(key), ppo_net_spec(*env, pc, centralized != 0));
+    auto a = nets.pack_actor(), c = nets.pack_critic();
+    *n_actor = int(a.size());
+    *n_critic = int(c.size());
+    if (actor) std::memcpy(actor, a.data(), a.size() * sizeof(float));
+    if (critic) std::memcpy(critic, c.data(), c.size() * sizeof(float));
+  });
+}
+
 // prng::permutation(key, n) (prng.cpp:151-159): the reference's Fisher-Yates.
 int mref_permutation(const uint32_t key[4], int n, int32_t* out) {
   return guarded([&] {
@@ -311,8 +329,8 @@ int mref_ff_minibatch(const char* env_id, const char* cfg, int centralized, cons
 // The reference's own public trainer: train_ippo / train_mappo (ppo.cpp:518-651)
 // with PpoConfig::from_config.  metrics: rows x 12 (ppo.cpp:524-527 columns).
 int mref_train(const char* env_id, const char* cfg, const char* ppo_cfg, int centralized, const uint32_t key[4],
-               double* metrics, int max_rows, int* n_rows, float* actor, float* critic, int* diverged,
-               int64_t* steps_done) {
+               double* metrics, int max_rows, int* n_rows, float* actor, int* actor_cap, float* critic,
+               int* critic_cap, int* diverged, int64_t* steps_done) {
   return guarded([&] {
     auto env = make_env(env_id, parse(cfg));
     PpoConfig pc = PpoConfig::from_config(parse(ppo_cfg));
@@ -322,8 +340,10 @@ int mref_train(const char* env_id, const char* cfg, const char* ppo_cfg, int cen
     for (size_t r = 0; r < rows.size() && int(r) < max_rows; ++r)
       for (size_t c = 0; c < rows[r].size(); ++c) metrics[r * rows[r].size() + c] = rows[r][c];
     auto a = res.nets.pack_actor(), c = res.nets.pack_critic();
-    std::memcpy(actor, a.data(), a.size() * sizeof(float));
-    std::memcpy(critic, c.data(), c.size() * sizeof(float));
+    if (int(a.size()) <= *actor_cap) std::memcpy(actor, a.data(), a.size() * sizeof(float));
+    if (int(c.size()) <= *critic_cap) std::memcpy(critic, c.data(), c.size() * sizeof(float));
+    *actor_cap = int(a.size());  // the true sizes (the caller re-runs with larger buffers if short)
+    *critic_cap = int(c.size());
     *diverged = res.diverged ? 1 : 0;
     *steps_done = res.steps_done;
   });

@@ -62,7 +62,7 @@ EXPORTS = [
     "marl_ppo_get_params", "marl_ppo_rollout", "marl_ppo_collect", "marl_ppo_update", "marl_ppo_step",
     "marl_ppo_minibatch_grad", "marl_ppo_destroy", "marl_ppo_permutation", "marl_ppo_set_allreduce",
     "marl_nccl_unique_id", "marl_ppo_set_nccl", "marl_venv_action_dim", "marl_venv_actions_f32",
-    "marl_venv_step_continuous", "marl_venv_step_continuous_host",
+    "marl_venv_step_continuous", "marl_venv_step_continuous_host", "marl_ppo_param_counts", "marl_ppo_init_rnn",
 ]
 
 # int (*marl_allreduce_fn)(void* ctx, void* dev_buf, int64_t count, int dtype, void* stream)
@@ -139,6 +139,8 @@ def lib() -> C.CDLL:
     L.marl_ppo_permutation.argtypes = [u32p, C.c_int64, vp, C.c_int]
     L.marl_ppo_set_allreduce.argtypes = [vp, ALLREDUCE_FN, vp]
     L.marl_venv_action_dim.argtypes = [vp, C.POINTER(C.c_int32)]
+    L.marl_ppo_param_counts.argtypes = [vp, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]
+    L.marl_ppo_init_rnn.argtypes = [C.c_int] * 5 + [u32p, C.POINTER(C.c_float), C.POINTER(C.c_float)]
     L.marl_venv_actions_f32.argtypes = [vp, C.POINTER(C.POINTER(C.c_float))]
     L.marl_venv_step_continuous.argtypes = [vp, vp]
     L.marl_venv_step_continuous_host.argtypes = [vp, vp, C.POINTER(HostStep)]

@@ -229,6 +229,55 @@ void smax_launch_world_state(const SmaxConfig& c, const SmaxState& s, int64_t n,
 void launch_obs_gather(const float* obs, int64_t n, int row_floats, const int32_t* seg_src, const int32_t* seg_len,
                        int n_seg, int width, float* out, cudaStream_t st);
 
+// ------------------------------------------------------------ recurrent policy
+struct PpoMbStats;
+// RnnBranch (actor_critic.hpp:74-200): embed in->F, GRU F->H, post H->F, head.
+inline int rnn_branch_params(int in, int F, int H, int out) {
+  return F * in + F + 3 * H * F + 3 * H * H + 6 * H + F * H + F + out * F + out;
+}
+
+struct RnnPolicyArgs {
+  const float *actor, *critic;  // packed branches (nn::pack order)
+  float *h_actor, *h_critic;    // [R][H] carried hidden states (ppo.cpp:194-198)
+  int in_dim, critic_in, n_act, F, H, relu;
+};
+void rnn_policy(const RnnPolicyArgs& a, const PolicyStep& s, const RolloutBufs& b, cudaStream_t st);
+
+// rnn_seq_forward caches of one branch over K = T*M (t, row) entries, k = t*M + i
+struct RnnCache {
+  float *x, *y, *e, *h, *z, *r, *c, *ah, *p, *hn;  // forward
+  float *dy, *dzp, *daz, *dar, *dac, *dah, *dze;   // backward deltas
+};
+inline size_t rnn_cache_floats(int in, int F, int H, int out) {
+  return size_t(in) + 2 * size_t(out) + 4 * size_t(F) + 10 * size_t(H);
+}
+
+struct RnnSeqArgs {
+  const float *actor, *critic;
+  const float *h0_actor, *h0_critic;  // [R][H] hidden at the window start (ppo.cpp:219-222)
+  const int32_t* rows;                // [M] minibatch rows
+  int64_t M;
+  int T;
+  int64_t R;
+  int in_dim, critic_in, n_act, F, H, relu;
+  const float* obs;          // [T][R][in_dim]
+  const float* critic_rows;  // [T][R][critic_in] (MAPPO) or null
+  const uint8_t* resets;     // [T][R]
+  RnnCache ca, cc;
+};
+void rnn_forward(const RnnSeqArgs& a, bool actor, cudaStream_t st);
+void rnn_backward(const RnnSeqArgs& a, bool actor, cudaStream_t st);
+void rnn_outer_sum(const float* D, int ldd, const float* X, int ldx, int64_t K, int O, int I, float* G,
+                   cudaStream_t st);
+// flat[k = t*M + i] = t*R + rows[i] (the loss rows of rnn_minibatch, ppo.cpp:472-477)
+void rnn_flat_slots(const int32_t* rows, int64_t M, int T, int64_t R, int32_t* flat, cudaStream_t st);
+// ppo_row_loss over the K flat rows from the cached head outputs -> ca.dy, cc.dy;
+// per-block loss sums -> spart_a / spart_c [blocks][6]
+int rnn_loss_blocks(int64_t K);
+void rnn_loss(const RnnSeqArgs& a, const int32_t* flat, int64_t K, const RolloutBufs& b, const PpoMbStats* st,
+              double clip_eps, double ent_coef, double vf_coef, double* spart_a, double* spart_c, int* err,
+              cudaStream_t s);
+
 // ------------------------------------------------------------ PPO update
 // train_ppo_impl's minibatch loop (ppo.cpp:588-628) over a RolloutBufs.
 constexpr int kPpoMaxAct = 64;

@@ -1034,6 +1034,10 @@ struct marl_rollout {
   int32_t* agent_actions = nullptr;
   uint32_t act_key[4] = {0, 0, 0, 0};
   bool has_params = false, begun = false, first = true;
+  // recurrent (GRU) policy: embed F, hidden H (ppo.hpp:52-53); carried hidden
+  // states and their copy at the window start (Rollout::h0_*, ppo.cpp:175, 219-222)
+  int recurrent = 0, F = 0, H = 0;
+  float *h_actor = nullptr, *h_critic = nullptr, *h0_actor = nullptr, *h0_critic = nullptr;
 };
 
 namespace {
@@ -1108,10 +1112,24 @@ void run_policy(marl_rollout* r, int t, bool bootstrap, int64_t seq_base) {
   s.legal_ready = (!bootstrap && e.family == MARL_FAMILY_SMAX) ? 1 : 0;
   if (s.legal_ready)  // Env::legal_actions straight into the buffer slice (team.cpp:35-42)
     smax_launch_legal(e.smax, h->smax, h->n, r->n_act, r->b.legal + size_t(t) * size_t(r->R) * r->n_act, h->stream);
-  if (r->precision == 1)
+  if (r->recurrent) {
+    RnnPolicyArgs ra{};
+    ra.actor = r->params;
+    ra.critic = r->params + r->n_actor;
+    ra.h_actor = r->h_actor;
+    ra.h_critic = r->h_critic;
+    ra.in_dim = r->in_dim;
+    ra.critic_in = r->critic_in;
+    ra.n_act = r->n_act;
+    ra.F = r->F;
+    ra.H = r->H;
+    ra.relu = r->relu;
+    rnn_policy(ra, s, r->b, h->stream);
+  } else if (r->precision == 1) {
     rollout_policy_bf16(net_of(r), net_bf16_of(r), s, r->b, h->stream);
-  else
+  } else {
     rollout_policy_fp32(net_of(r), s, r->b, h->stream);
+  }
   after_launch();
 }
 
@@ -1135,14 +1153,22 @@ int marl_rollout_policy_spec(const marl_venv* h, int width, int n_layers, int re
   });
 }
 
-int marl_rollout_create(marl_venv* h, int T, int width, int n_layers, int relu, int centralized, int precision,
-                        marl_rollout** out) {
-  return guarded([&] {
-    if (!h || !out) raise(MARL_ERR_CONTRACT, "marl_rollout_create: NULL argument");
+}  // extern "C"
+
+// hidden > 0: the recurrent policy (RnnBranch, fc width `width`, GRU `hidden`)
+static marl_rollout* rollout_create_impl(marl_venv* h, int T, int width, int n_layers, int relu, int centralized,
+                                         int precision, int hidden) {
+    if (!h) raise(MARL_ERR_CONTRACT, "marl_rollout_create: NULL argument");
     if (T < 1) raise(MARL_ERR_CONTRACT, "rollout: n_rollout_steps must be >= 1");
     marl_policy_spec ps{};
-    if (marl_rollout_policy_spec(h, width, n_layers, relu, centralized, &ps) != MARL_OK)
+    if (marl_rollout_policy_spec(h, width, hidden > 0 ? 2 : n_layers, relu, centralized, &ps) != MARL_OK)
       raise(MARL_ERR_SCHEMA, marl_last_error());
+    if (hidden > 0) {
+      if (precision != 0) raise(MARL_ERR_SCHEMA, "rollout: the recurrent policy runs in fp32 (precision 0)");
+      if (hidden > 128) raise(MARL_ERR_SCHEMA, "rollout: hidden_width must be in [1, 128]");
+      ps.n_actor_params = rnn_branch_params(ps.in_dim, width, hidden, ps.n_actions);
+      ps.n_critic_params = rnn_branch_params(ps.critic_in, width, hidden, 1);
+    }
     if (h->env->continuous)
       raise(MARL_ERR_SCHEMA, "rollout: the PPO policy is categorical; box action spaces are not supported");
     if (centralized && precision == 1)
@@ -1193,9 +1219,25 @@ int marl_rollout_create(marl_venv* h, int T, int width, int n_layers, int relu, 
     ar.add(&r->images, size_t(128 * 32 + 2 * 64 * 64 + 2 * 16 * 64));
     ar.add(&r->bias, size_t(4 * 64 + 2 * 16));
     ar.add(&r->agent_actions, size_t(e.A));
+    if (hidden > 0) {
+      r->recurrent = 1;
+      r->F = width;
+      r->H = hidden;
+      for (float** q : {&r->h_actor, &r->h_critic, &r->h0_actor, &r->h0_critic})
+        ar.add(q, size_t(r->R) * size_t(hidden));
+    }
     ar.commit();
     cuda_check(cudaMemcpy(r->agent_actions, e.n_actions.data(), size_t(e.A) * 4, cudaMemcpyHostToDevice), "cudaMemcpy");
-    *out = r.release();
+    return r.release();
+}
+
+extern "C" {
+
+int marl_rollout_create(marl_venv* h, int T, int width, int n_layers, int relu, int centralized, int precision,
+                        marl_rollout** out) {
+  return guarded([&] {
+    if (!out) raise(MARL_ERR_CONTRACT, "marl_rollout_create: NULL argument");
+    *out = rollout_create_impl(h, T, width, n_layers, relu, centralized, precision, 0);
   });
 }
 
@@ -1223,6 +1265,10 @@ int marl_rollout_begin(marl_rollout* r, const uint32_t key[4]) {
     marl_prng_fold_in(key, 1, rk);
     if (marl_venv_reset(r->h, rk) != MARL_OK) raise(MARL_ERR_CUDA, marl_last_error());
     marl_prng_fold_in(key, 2, r->act_key);
+    if (r->recurrent) {  // fresh Collector: zero hidden states (ppo.cpp:194-198)
+      cuda_check(cudaMemset(r->h_actor, 0, size_t(r->R) * size_t(r->H) * 4), "cudaMemset");
+      cuda_check(cudaMemset(r->h_critic, 0, size_t(r->R) * size_t(r->H) * 4), "cudaMemset");
+    }
     r->begun = true;
     r->first = true;
   });
@@ -1241,6 +1287,11 @@ void collect_impl(marl_rollout* r, int64_t seq_base, double gamma, double lambda
   marl_venv* h = r->h;
   set_device(h);
   const Env& e = *h->env;
+  if (r->recurrent) {  // ro.h0_* = the hidden states at the window start (ppo.cpp:219-222)
+    const size_t bytes = size_t(r->R) * size_t(r->H) * 4;
+    cuda_check(cudaMemcpyAsync(r->h0_actor, r->h_actor, bytes, cudaMemcpyDeviceToDevice, h->stream), "D2D");
+    cuda_check(cudaMemcpyAsync(r->h0_critic, r->h_critic, bytes, cudaMemcpyDeviceToDevice, h->stream), "D2D");
+  }
   for (int t = 0; t < r->T; ++t) {
     run_policy(r, t, false, seq_base);
     launch_step(h, false, nullptr, r->b.actions + size_t(t) * size_t(r->R));
@@ -1563,6 +1614,35 @@ void host_ff_init(const Key& key, int in, int n_layers, int W, int out, float he
   std::fill(dst, dst + out, 0.0f);
 }
 
+// rnn_init (actor_critic.hpp:82-90) packed: embed = dense(fold_in(fold_in(k,1),0)),
+// gru_init(fold_in(k,2)) (nn.hpp:508-517), post = dense(fold_in(fold_in(k,3),0)),
+// head = dense(fold_in(k,4), head_gain); biases zero.
+void host_rnn_init(const Key& key, int in, int F, int H, int out, float head_gain, float* dst) {
+  const float g = float(std::sqrt(2.0));
+  host_orthogonal(fold_in(fold_in(key, 1), 0), F, in, g, dst);
+  dst += size_t(F) * size_t(in);
+  std::fill(dst, dst + F, 0.0f);
+  dst += F;
+  const Key kg = fold_in(key, 2);
+  for (int j = 0; j < 3; ++j) {
+    host_orthogonal(fold_in(kg, uint64_t(j)), H, F, 1.0f, dst);
+    dst += size_t(H) * size_t(F);
+  }
+  for (int j = 3; j < 6; ++j) {
+    host_orthogonal(fold_in(kg, uint64_t(j)), H, H, 1.0f, dst);
+    dst += size_t(H) * size_t(H);
+  }
+  std::fill(dst, dst + 6 * H, 0.0f);
+  dst += 6 * H;
+  host_orthogonal(fold_in(fold_in(key, 3), 0), F, H, g, dst);
+  dst += size_t(F) * size_t(H);
+  std::fill(dst, dst + F, 0.0f);
+  dst += F;
+  host_orthogonal(fold_in(key, 4), out, F, head_gain, dst);
+  dst += size_t(out) * size_t(F);
+  std::fill(dst, dst + out, 0.0f);
+}
+
 }  // namespace
 
 struct marl_ppo {
@@ -1599,6 +1679,10 @@ struct marl_ppo {
   marl_allreduce_fn hook = nullptr;
   void* hook_ctx = nullptr;
   void* nccl_comm = nullptr;
+  // recurrent update (rnn_minibatch, ppo.cpp:444-509): BPTT caches for one minibatch
+  bool recurrent = false;
+  RnnCache rca{}, rcc{};
+  int32_t* rnn_flat = nullptr;
   ~marl_ppo();
 };
 
@@ -1757,6 +1841,72 @@ void minibatch_grad(marl_ppo* p, const int32_t* idx, int64_t M, bool global = fa
   }
 }
 
+// rnn_minibatch's gradient (ppo.cpp:444-509): rnn_seq_forward with cache over
+// the rows' whole sequences, ppo_row_loss over the [t][i] rows, rnn_seq_backward,
+// and the weight gradients summed over every (t, row) in nn::pack order.
+void minibatch_grad_rnn(marl_ppo* p, const int32_t* rows, int64_t M) {
+  marl_rollout* r = p->ro;
+  cudaStream_t st = p->h->stream;
+  const int T = r->T;
+  const int64_t K = int64_t(T) * M;
+  rnn_flat_slots(rows, M, T, r->R, p->rnn_flat, st);
+  ppo_adv_stats(r->b, p->rnn_flat, K, p->adv_part, p->adv_part2, p->adv_g, p->mbst, st, {});
+  RnnSeqArgs a{};
+  a.actor = r->params;
+  a.critic = r->params + r->n_actor;
+  a.h0_actor = r->h0_actor;
+  a.h0_critic = r->h0_critic;
+  a.rows = rows;
+  a.M = M;
+  a.T = T;
+  a.R = r->R;
+  a.in_dim = r->in_dim;
+  a.critic_in = r->critic_in;
+  a.n_act = r->n_act;
+  a.F = r->F;
+  a.H = r->H;
+  a.relu = r->relu;
+  a.obs = r->b.obs;
+  a.critic_rows = r->centralized ? r->b.critic_in : nullptr;
+  a.resets = r->b.resets;
+  a.ca = p->rca;
+  a.cc = p->rcc;
+  rnn_forward(a, true, st);
+  rnn_forward(a, false, st);
+  rnn_loss(a, p->rnn_flat, K, r->b, p->mbst, p->cfg.clip_eps, p->cfg.ent_coef, p->cfg.vf_coef, p->spart_a,
+           p->spart_c, p->flags + 1, st);
+  rnn_backward(a, true, st);
+  rnn_backward(a, false, st);
+  float* G = p->grad;
+  for (int branch = 0; branch < 2; ++branch) {
+    const RnnCache& c = branch == 0 ? p->rca : p->rcc;
+    const int in = branch == 0 ? r->in_dim : r->critic_in, out = branch == 0 ? r->n_act : 1, F = r->F, H = r->H;
+    auto mat = [&](const float* D, int ldd, const float* X, int ldx, int O, int I) {
+      rnn_outer_sum(D, ldd, X, ldx, K, O, I, G, st);
+      G += size_t(O) * size_t(X ? I : 1);
+    };
+    mat(c.dze, F, c.x, in, F, in);  // embed w, b
+    mat(c.dze, F, nullptr, 0, F, 1);
+    mat(c.daz, H, c.e, F, H, F);    // gru wz, wr, wn
+    mat(c.dar, H, c.e, F, H, F);
+    mat(c.dac, H, c.e, F, H, F);
+    mat(c.daz, H, c.h, H, H, H);    // uz, ur, un
+    mat(c.dar, H, c.h, H, H, H);
+    mat(c.dah, H, c.h, H, H, H);
+    mat(c.daz, H, nullptr, 0, H, 1);  // bzx, brx, bnx, bzh, brh, bnh
+    mat(c.dar, H, nullptr, 0, H, 1);
+    mat(c.dac, H, nullptr, 0, H, 1);
+    mat(c.daz, H, nullptr, 0, H, 1);
+    mat(c.dar, H, nullptr, 0, H, 1);
+    mat(c.dah, H, nullptr, 0, H, 1);
+    mat(c.dzp, F, c.hn, H, F, H);   // post w, b
+    mat(c.dzp, F, nullptr, 0, F, 1);
+    mat(c.dy, out, c.p, F, out, F);  // head w, b
+    mat(c.dy, out, nullptr, 0, out, 1);
+  }
+  after_launch();
+}
+
 // clip_global_norm + adam_update for one minibatch (ppo.cpp:605-608).
 void minibatch_apply(marl_ppo* p, double lr_u, double* metrics_slot) {
   p->adam_t += 1;
@@ -1831,7 +1981,10 @@ void ppo_update_impl(marl_ppo* p, double row[12], int* diverged) {
     ppo_permutation(kw, p->batch, p->perm, p->perm_scratch, p->perm_scratch_bytes, st);
     after_launch();
     for (int mb = 0; mb < c.n_minibatches; ++mb, ++k) {
-      minibatch_grad(p, p->perm + size_t(mb) * size_t(p->per), p->per, true);
+      if (p->recurrent)  // whole row sequences (ppo.cpp:594-601)
+        minibatch_grad_rnn(p, p->perm + size_t(mb) * size_t(p->per), p->per);
+      else
+        minibatch_grad(p, p->perm + size_t(mb) * size_t(p->per), p->per, true);
       minibatch_apply(p, lr_u, p->metrics + size_t(k) * 8);
     }
   }
@@ -1877,7 +2030,9 @@ int marl_ppo_create(marl_venv* h, const char* ppo_config_json, int centralized, 
   return guarded([&] {
     if (!h || !out) raise(MARL_ERR_CONTRACT, "marl_ppo_create: NULL argument");
     PpoCfg c = parse_ppo_config(ppo_config_json);
-    if (c.recurrent) raise(MARL_ERR_SCHEMA, "ppo: the B200 update implements feed-forward policies (recurrent=false)");
+    if (c.recurrent && precision != 0)
+      raise(MARL_ERR_SCHEMA, "ppo: recurrent policies run in fp32 (precision 0)");
+    if (c.recurrent && h->n != h->gn) raise(MARL_ERR_CONTRACT, "ppo: the recurrent update runs on an unsharded VectorEnv");
     if (int64_t(c.n_envs) != h->gn)
       raise(MARL_ERR_CONTRACT, "ppo: n_envs must equal the VectorEnv's (global) env count");
     set_device(h);
@@ -1886,9 +2041,9 @@ int marl_ppo_create(marl_venv* h, const char* ppo_config_json, int centralized, 
     p->cfg = c;
     p->centralized = centralized ? 1 : 0;
     p->precision = precision;
-    if (marl_rollout_create(h, c.n_rollout_steps, c.fc_width, c.n_fc_layers, c.activation == "relu", centralized,
-                            precision, &p->ro) != MARL_OK)
-      raise(MARL_ERR_SCHEMA, marl_last_error());
+    p->ro = rollout_create_impl(h, c.n_rollout_steps, c.fc_width, c.n_fc_layers, c.activation == "relu", centralized,
+                                precision, c.recurrent ? c.hidden_width : 0);
+    p->recurrent = c.recurrent;
     marl_rollout* r = p->ro;
     if (r->n_act > kPpoMaxAct) raise(MARL_ERR_SCHEMA, "ppo: more than 64 actions");
     const int64_t steps_per_update = int64_t(c.n_envs) * int64_t(c.n_rollout_steps);
@@ -1898,9 +2053,15 @@ int marl_ppo_create(marl_venv* h, const char* ppo_config_json, int centralized, 
     p->row0 = r->row0;
     p->sharded = r->R != r->R_global;
     p->batch = int64_t(c.n_rollout_steps) * r->R_global;  // the permutation spans the global rollout
-    if (p->batch % c.n_minibatches != 0)
+    if (c.recurrent) {  // minibatches of whole row sequences (ppo.cpp:548-552, 594-596)
+      p->batch = r->R_global;
+      if (p->batch % c.n_minibatches != 0)
+        raise(MARL_ERR_SCHEMA, "ppo: recurrent minibatches need n_envs*n_agents (" + std::to_string(p->batch) +
+                                   ") divisible by n_minibatches (" + std::to_string(c.n_minibatches) + ")");
+    } else if (p->batch % c.n_minibatches != 0) {
       raise(MARL_ERR_SCHEMA, "ppo: batch size (" + std::to_string(p->batch) + ") must be divisible by n_minibatches (" +
                                  std::to_string(c.n_minibatches) + ")");
+    }
     if (p->batch >= (int64_t(1) << 31)) raise(MARL_ERR_SCHEMA, "ppo: batch (n_rollout_steps * rows) must be < 2^31");
     p->per = p->batch / c.n_minibatches;
     p->Pa = r->n_actor;
@@ -1910,7 +2071,18 @@ int marl_ppo_create(marl_venv* h, const char* ppo_config_json, int centralized, 
     // (MARL_PPO_UPDATE_FP32=1 forces the fp32 CUDA-core path)
     p->tc = precision == 1 && !centralized && ppo_tc_supported(r->in_dim, r->critic_in, r->width, r->n_act) &&
             !std::getenv("MARL_PPO_UPDATE_FP32");
-    if (p->tc) {
+    int64_t rnn_K = 0;
+    if (p->recurrent) {
+      rnn_K = int64_t(c.n_rollout_steps) * p->per;
+      const size_t floats = size_t(rnn_K) * (rnn_cache_floats(r->in_dim, r->F, r->H, r->n_act) +
+                                             rnn_cache_floats(r->critic_in, r->F, r->H, 1));
+      size_t free_b = 0, total_b = 0;
+      cuda_check(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
+      if (floats * 4 > free_b / 2)
+        raise(MARL_ERR_SCHEMA, "ppo: the recurrent update's BPTT caches (" + std::to_string(floats * 4 >> 20) +
+                                   " MiB) exceed half the free device memory; use more n_minibatches or fewer envs");
+      p->grid_a = p->grid_c = rnn_loss_blocks(rnn_K);
+    } else if (p->tc) {
       p->grid_a = p->grid_c = ppo_tc_grid(p->per);
     } else {
       p->grid_a = ppo_branch_grid(r->in_dim, r->width, r->n_act, p->per);
@@ -1927,8 +2099,23 @@ int marl_ppo_create(marl_venv* h, const char* ppo_config_json, int centralized, 
     ar.add(&p->gpart_c, size_t(p->grid_c) * size_t(p->Pc));
     ar.add(&p->spart_a, size_t(p->grid_a) * 6);
     ar.add(&p->spart_c, size_t(p->grid_c) * 6);
-    ar.add(&p->adv_part, size_t(nb) * 2);
-    ar.add(&p->adv_part2, size_t(nb));
+    ar.add(&p->adv_part, size_t(std::max(nb, ppo_stat_blocks(rnn_K))) * 2);
+    ar.add(&p->adv_part2, size_t(std::max(nb, ppo_stat_blocks(rnn_K))));
+    if (p->recurrent) {
+      ar.add(&p->rnn_flat, size_t(rnn_K));
+      const int F = r->F, H = r->H;
+      for (int br = 0; br < 2; ++br) {
+        RnnCache& cc = br == 0 ? p->rca : p->rcc;
+        const int in = br == 0 ? r->in_dim : r->critic_in, out = br == 0 ? r->n_act : 1;
+        const size_t K = size_t(rnn_K);
+        ar.add(&cc.x, K * in);
+        ar.add(&cc.y, K * out);
+        ar.add(&cc.dy, K * out);
+        for (float** q : {&cc.e, &cc.p, &cc.dzp, &cc.dze}) ar.add(q, K * F);
+        for (float** q : {&cc.h, &cc.z, &cc.r, &cc.c, &cc.ah, &cc.hn, &cc.daz, &cc.dar, &cc.dac, &cc.dah})
+          ar.add(q, K * H);
+      }
+    }
     ar.add(&p->metrics, size_t(c.update_epochs) * size_t(c.n_minibatches) * 8);
     ar.add(&p->mbst, 1);
     ar.add(&p->perm, size_t(p->batch));
@@ -1974,9 +2161,13 @@ int marl_ppo_begin(marl_ppo* p, const uint32_t key[4]) {
     put_key(fold_in(k, 12), p->train_key);
     std::vector<float> a(size_t(p->Pa)), c(size_t(p->Pc));
     const marl_rollout* r = p->ro;
-    if (marl_ppo_init_nets(r->in_dim, r->critic_in, r->n_act, r->width, p->cfg.n_fc_layers, k10, a.data(), c.data()) !=
-        MARL_OK)
+    if (p->recurrent) {  // ppo_init_nets, recurrent spec (ppo.cpp:112-118)
+      host_rnn_init(fold_in(key4(k10), 1), r->in_dim, r->F, r->H, r->n_act, 0.01f, a.data());
+      host_rnn_init(fold_in(key4(k10), 2), r->critic_in, r->F, r->H, 1, 1.0f, c.data());
+    } else if (marl_ppo_init_nets(r->in_dim, r->critic_in, r->n_act, r->width, p->cfg.n_fc_layers, k10, a.data(),
+                                  c.data()) != MARL_OK) {
       raise(MARL_ERR_CONTRACT, marl_last_error());
+    }
     if (marl_rollout_set_params(p->ro, a.data(), c.data()) != MARL_OK) raise(MARL_ERR_CUDA, marl_last_error());
     if (marl_rollout_begin(p->ro, k11) != MARL_OK) raise(MARL_ERR_CUDA, marl_last_error());
     set_device(p->h);
@@ -1987,6 +2178,25 @@ int marl_ppo_begin(marl_ppo* p, const uint32_t key[4]) {
     p->last_mean_return = 0.0;
     p->begun = true;
     p->collected = false;
+  });
+}
+
+int marl_ppo_param_counts(const marl_ppo* p, int32_t* n_actor, int32_t* n_critic) {
+  return guarded([&] {
+    if (!p || !n_actor || !n_critic) raise(MARL_ERR_CONTRACT, "marl_ppo_param_counts: NULL argument");
+    *n_actor = p->Pa;
+    *n_critic = p->Pc;
+  });
+}
+
+// rnn_init-based ppo_init_nets for a recurrent spec (ppo.cpp:112-118), host arrays.
+int marl_ppo_init_rnn(int in_dim, int critic_in, int n_actions, int fc_width, int hidden_width, const uint32_t key[4],
+                      float* actor, float* critic) {
+  return guarded([&] {
+    if (!key || !actor || !critic) raise(MARL_ERR_CONTRACT, "marl_ppo_init_rnn: NULL argument");
+    const Key k = key4(key);
+    host_rnn_init(fold_in(k, 1), in_dim, fc_width, hidden_width, n_actions, 0.01f, actor);
+    host_rnn_init(fold_in(k, 2), critic_in, fc_width, hidden_width, 1, 1.0f, critic);
   });
 }
 

@@ -91,6 +91,23 @@ def init_nets(in_dim: int, critic_in: int, n_actions: int, key, fc_width: int = 
     return a, c
 
 
+def init_rnn(in_dim: int, critic_in: int, n_actions: int, key, fc_width: int = 64, hidden_width: int = 128):
+    """ppo_init_nets(key, spec) for a recurrent spec (rnn_init, actor_critic.hpp:82-90), packed."""
+    return _init_rnn(in_dim, critic_in, n_actions, key, fc_width, hidden_width)
+
+
+def _rnn_count(i, F, H, o):
+    return F * i + F + 3 * H * F + 3 * H * H + 6 * H + F * H + F + o * F + o
+
+
+def _init_rnn(in_dim, critic_in, n_actions, key, fc_width, hidden_width):
+    a = np.zeros(_rnn_count(in_dim, fc_width, hidden_width, n_actions), np.float32)
+    c = np.zeros(_rnn_count(critic_in, fc_width, hidden_width, 1), np.float32)
+    N.check(N.lib().marl_ppo_init_rnn(in_dim, critic_in, n_actions, fc_width, hidden_width, _u32p(_key_arr(key)),
+                                      _fp(a, C.c_float), _fp(c, C.c_float)))
+    return a, c
+
+
 def permutation(key, n: int, device: int = 0):
     """prng::permutation(key, n) computed on the device; returns a cuda int32 tensor."""
     import torch
@@ -119,6 +136,9 @@ class PpoTrainer:
                                    int(self.config.get("fc_width", 64)), int(self.config.get("n_fc_layers", 2)),
                                    self.config.get("activation", "tanh"), precision, centralized, _borrowed=r)
         self.spec = self.rollout.spec
+        na, nc = C.c_int32(), C.c_int32()
+        N.check(N.lib().marl_ppo_param_counts(self._h, C.byref(na), C.byref(nc)))
+        self.n_actor_params, self.n_critic_params = int(na.value), int(nc.value)
 
     def __del__(self):
         try:
@@ -132,13 +152,19 @@ class PpoTrainer:
         N.check(N.lib().marl_ppo_begin(self._h, _u32p(_key_arr(key))))
 
     def params(self):
-        a = np.zeros(self.spec.n_actor_params, np.float32)
-        c = np.zeros(self.spec.n_critic_params, np.float32)
+        a = np.zeros(self.n_actor_params, np.float32)
+        c = np.zeros(self.n_critic_params, np.float32)
         N.check(N.lib().marl_ppo_get_params(self._h, _fp(a, C.c_float), _fp(c, C.c_float)))
         return a, c
 
     def set_params(self, actor, critic) -> None:
-        self.rollout.set_params(actor, critic)
+        a = np.ascontiguousarray(actor, dtype=np.float32)
+        c = np.ascontiguousarray(critic, dtype=np.float32)
+        if a.size != self.n_actor_params or c.size != self.n_critic_params:
+            from .errors import ContractError
+            raise ContractError(f"ppo: expected {self.n_actor_params}/{self.n_critic_params} parameters, "
+                                f"got {a.size}/{c.size}")
+        N.check(N.lib().marl_ppo_set_params(self._h, _fp(a, C.c_float), _fp(c, C.c_float)))
 
     def collect(self) -> None:
         N.check(N.lib().marl_ppo_collect(self._h))

@@ -204,7 +204,8 @@ def test_ppo_config_schema_errors():
     from paper_2311_10090_b200.ppo import PpoTrainer
     v = m.VectorEnv(m.make_env("MPE_simple_spread_v3", {}), 4, device=0)
     for bad in ({"n_envs": 4, "bogus": 1}, {"n_envs": 4, "clip_eps": 1.5}, {"n_envs": 4, "activation": "gelu"},
-                {"n_envs": 4, "n_rollout_steps": 5, "n_minibatches": 7}, {"n_envs": 4, "recurrent": True}):
+                {"n_envs": 4, "n_rollout_steps": 5, "n_minibatches": 7},
+                {"n_envs": 4, "recurrent": True, "n_minibatches": 5}):  # 12 rows % 5 (ppo.cpp:548-552)
         with pytest.raises(SchemaError):
             PpoTrainer(v, bad)
     with pytest.raises(ContractError):
