@@ -93,6 +93,7 @@ constexpr int kSmaxMaxUnits = 64;
 struct SmaxConfig {
   int na, ne;
   int enemy_controlled;
+  int random_types;  // smacv2_*: units per team with per-episode random types (smax.cpp:88-93)
   int max_steps;
   double map;
   double jitter;

@@ -67,7 +67,8 @@ struct Params {
   int na, ne, n, A, controlled, max_steps, D, n_pairs;
   double map, jitter;
   double sep_r2hi;  // max rsum.r2hi over the roster's type pairs: conservative overlap pre-check
-  double pad;
+  int random_types;  // smacv2_*: per-episode random unit types and spawns (smax.cpp:169-181, 456-479)
+  int pad_;
   int8_t type[kSmaxMaxUnits];
   TypeStat ts[kTypes];
   PairStat ps[kTypes][kTypes];
@@ -81,6 +82,7 @@ struct EnvSm {
   int act[CAP];
   int8_t pa[CAP];
   int8_t fire[CAP];
+  int8_t ty[CAP];  // unit types of this env (the roster, or smacv2's per-episode draw)
 };
 
 // A group of G lanes of one warp (G need not be a power of two: a warp holds
@@ -112,13 +114,13 @@ __device__ __forceinline__ double dclamp(double v, double lo, double hi) {  // s
 
 template <int CAP>
 __device__ __forceinline__ bool in_range(const Params& P, const EnvSm<CAP>& e, int a, int b) {
-  const Thresh& r = P.ps[P.type[a]][P.type[b]].reach;  // smax.cpp:497-501
+  const Thresh& r = P.ps[e.ty[a]][e.ty[b]].reach;  // smax.cpp:497-501
   return dist_le(e.x[a] - e.x[b], e.y[a] - e.y[b], r.r, r.r2lo, r.r2hi);
 }
 
 template <int CAP>
 __device__ __forceinline__ bool sees(const Params& P, const EnvSm<CAP>& e, int a, int b) {
-  const Thresh& r = P.ts[P.type[a]].sight;  // center_dist(a, b) <= sight(a), smax.cpp:383,613
+  const Thresh& r = P.ts[e.ty[a]].sight;  // center_dist(a, b) <= sight(a), smax.cpp:383,613
   return dist_le(e.x[a] - e.x[b], e.y[a] - e.y[b], r.r, r.r2lo, r.r2hi);
 }
 
@@ -177,7 +179,7 @@ __device__ __forceinline__ void separation_pass(const Params& P, EnvSm<CAP>& e, 
   for (int a = 0; a < n - 1; ++a) {
     if (!(alive >> a & 1ull)) continue;
     unsigned long long row = alive & bits_above(a);
-    const int ta = P.type[a];
+    const int ta = e.ty[a];
     while (row) {  // group-uniform
       bool hit[UPL];
       double hdx[UPL], hdy[UPL], hd[UPL];
@@ -189,7 +191,7 @@ __device__ __forceinline__ void separation_pass(const Params& P, EnvSm<CAP>& e, 
         hdx[j] = hdy[j] = hd[j] = 0.0;
         if (!(row >> b & 1ull)) continue;
         const double dx = e.x[b] - xa, dy = e.y[b] - ya;
-        const Thresh& R = P.ps[ta][P.type[b]].rsum;
+        const Thresh& R = P.ps[ta][e.ty[b]].rsum;
         if (dx * dx + dy * dy > R.r2hi) continue;  // hypot(dx,dy) > ra+rb: overlap <= 0
         const double dd = hypot_glibc(dx, dy);
         hit[j] = R.r - dd > 0.0;
@@ -210,7 +212,7 @@ __device__ __forceinline__ void separation_pass(const Params& P, EnvSm<CAP>& e, 
             dy = hdy[q];
             dd = hd[q];
           }
-        const double overlap = P.ps[ta][P.type[b]].rsum.r - dd;
+        const double overlap = P.ps[ta][e.ty[b]].rsum.r - dd;
         double nx = 1.0, ny = 0.0;  // coincident centres get a fixed nudge axis
         if (dd > 1e-12) {
           nx = dx / dd;
@@ -218,7 +220,7 @@ __device__ __forceinline__ void separation_pass(const Params& P, EnvSm<CAP>& e, 
         }
         const double push = 0.5 * overlap;
         const TypeStat& A_ = P.ts[ta];
-        const TypeStat& B_ = P.ts[P.type[b]];
+        const TypeStat& B_ = P.ts[e.ty[b]];
         e.x[a] = dclamp(xa - nx * push, A_.rad, A_.hi);
         e.y[a] = dclamp(ya - ny * push, A_.rad, A_.hi);
         e.x[b] = dclamp(e.x[b] + nx * push, B_.rad, B_.hi);
@@ -272,7 +274,7 @@ __device__ __forceinline__ bool lane_pairs_overlap(const Params& P, const EnvSm<
     const double dx = e.x[b] - e.x[a], dy = e.y[b] - e.y[a];
     const double d2 = dx * dx + dy * dy;
     if (d2 > P.sep_r2hi) return false;  // farther than any radius sum
-    const Thresh& R = P.ps[P.type[a]][P.type[b]].rsum;
+    const Thresh& R = P.ps[e.ty[a]][e.ty[b]].rsum;
     if (d2 > R.r2hi) return false;
     return d2 < R.r2lo || R.r - hypot_glibc(dx, dy) > 0.0;
   });
@@ -284,7 +286,7 @@ __device__ __forceinline__ bool lane_pairs_within_tol(const Params& P, const Env
                                                       int gl) {
   return !for_lane_pairs<G>(lp, gl, P.n, [&](int a, int b) {
     if (e.h[a] <= 0.0 || e.h[b] <= 0.0) return false;
-    const PairStat& S = P.ps[P.type[a]][P.type[b]];
+    const PairStat& S = P.ps[e.ty[a]][e.ty[b]];
     const double dx = e.x[a] - e.x[b], dy = e.y[a] - e.y[b];
     const double d2 = dx * dx + dy * dy;
     if (d2 > S.otol.r2hi) return false;      // surely sum - d <= tol
@@ -322,20 +324,60 @@ __device__ __forceinline__ double uniform_at_nl(const Key& k, double lo, double 
   return v;
 }
 
-// Spawn of unit u: spawn_clusters / place_jittered (smax.cpp:448-454,481-492).
+// Spawn of unit u: spawn_clusters / place_jittered (smax.cpp:448-454,481-492),
+// or spawn_smacv2 (smax.cpp:456-479) for the random-type scenarios; the
+// unit's type (e.ty[u]) is already set.
+__device__ __forceinline__ void place_at(double bx, double by, double rad, double hi, double* x, double* y) {
+  *x = dclamp(bx, rad, hi);  // place (smax.cpp:481-485)
+  *y = dclamp(by, rad, hi);
+}
+
+// spawn_smacv2 (smax.cpp:456-479) for unit u: kept out of line (rare, and
+// the fixed-roster step kernel's instruction footprint stays as it was).
 template <int CAP>
-__device__ __forceinline__ void spawn_unit(const Params& P, EnvSm<CAP>& e, int u, const Key& key) {
+__device__ __noinline__ void spawn_smacv2(const Params& P, EnvSm<CAP>& e, int u, const Key& key) {
   const bool ally = u < P.na;
   const int i = ally ? u : u - P.na;
-  double bx = ally ? 0.25 * P.map - 1.5 * (i / 5) : 0.75 * P.map + 1.5 * (i / 5);
-  double by = 0.5 * P.map + 1.5 * (i % 5 - 2);
-  if (P.jitter > 0.0) {
-    bx += uniform_at_nl(fold_in_nl(key, 3000 + 2 * uint64_t(u)), -P.jitter, P.jitter);
-    by += uniform_at_nl(fold_in_nl(key, 3001 + 2 * uint64_t(u)), -P.jitter, P.jitter);
+  const TypeStat& t = P.ts[e.ty[u]];
+  if (to_unit(block_at_nl(fold_in_nl(key, 1), 0)) < 0.5) {
+    // reflected uniform spawns: enemy i mirrors ally i's draws
+    const double ax = uniform_at_nl(fold_in_nl(key, 1000 + 2 * uint64_t(i)), 0.1 * P.map, 0.4 * P.map);
+    const double ay = uniform_at_nl(fold_in_nl(key, 1001 + 2 * uint64_t(i)), 0.1 * P.map, 0.9 * P.map);
+    place_at(ally ? ax : P.map - ax, ay, t.rad, t.hi, &e.x[u], &e.y[u]);
+    return;
   }
-  const TypeStat& t = P.ts[P.type[u]];
-  e.x[u] = dclamp(bx, t.rad, t.hi);
-  e.y[u] = dclamp(by, t.rad, t.hi);
+  // one team at the center, the other on a ring (a coin decides which)
+  const bool allies_center = to_unit(block_at_nl(fold_in_nl(key, 2), 0)) < 0.5;
+  if (ally == allies_center) {
+    double bx = 0.5 * P.map + 1.5 * (i / 5), by = 0.5 * P.map + 1.5 * (i % 5 - 2);
+    if (P.jitter > 0.0) {  // place_jittered (smax.cpp:486-492)
+      bx += uniform_at_nl(fold_in_nl(key, 3000 + 2 * uint64_t(u)), -P.jitter, P.jitter);
+      by += uniform_at_nl(fold_in_nl(key, 3001 + 2 * uint64_t(u)), -P.jitter, P.jitter);
+    }
+    place_at(bx, by, t.rad, t.hi, &e.x[u], &e.y[u]);
+  } else {
+    const double theta = uniform_at_nl(fold_in_nl(key, 2000 + 2 * uint64_t(i)), 0.0, 6.283185307179586);
+    const double rho = uniform_at_nl(fold_in_nl(key, 2001 + 2 * uint64_t(i)), 0.25 * P.map, 0.45 * P.map);
+    place_at(0.5 * P.map + rho * cos(theta), 0.5 * P.map + rho * sin(theta), t.rad, t.hi, &e.x[u], &e.y[u]);
+  }
+}
+
+template <int CAP>
+__device__ __forceinline__ void spawn_unit(const Params& P, EnvSm<CAP>& e, int u, const Key& key) {
+  const TypeStat& t = P.ts[e.ty[u]];
+  if (P.random_types) {
+    spawn_smacv2(P, e, u, key);
+  } else {
+    const bool ally = u < P.na;
+    const int i = ally ? u : u - P.na;
+    double bx = ally ? 0.25 * P.map - 1.5 * (i / 5) : 0.75 * P.map + 1.5 * (i / 5);
+    double by = 0.5 * P.map + 1.5 * (i % 5 - 2);
+    if (P.jitter > 0.0) {
+      bx += uniform_at_nl(fold_in_nl(key, 3000 + 2 * uint64_t(u)), -P.jitter, P.jitter);
+      by += uniform_at_nl(fold_in_nl(key, 3001 + 2 * uint64_t(u)), -P.jitter, P.jitter);
+    }
+    place_at(bx, by, t.rad, t.hi, &e.x[u], &e.y[u]);
+  }
   e.h[u] = t.hmax;
   e.cd[u] = 0.0;
   e.pa[u] = int8_t(kStop);
@@ -426,7 +468,7 @@ __device__ __forceinline__ void tick(const Params& P, EnvSm<CAP>& e, const Grp<G
     e.cd[u] = (0.0 < v) ? v : 0.0;  // std::max(0.0, v)
     const int a = e.act[u];
     if (a > kWest) continue;
-    const TypeStat& t = P.ts[P.type[u]];
+    const TypeStat& t = P.ts[e.ty[u]];
     const double dxs = a == kEast ? 1.0 : a == kWest ? -1.0 : 0.0;    // kDirX
     const double dys = a == kNorth ? 1.0 : a == kSouth ? -1.0 : 0.0;  // kDirY
     e.x[u] = dclamp(e.x[u] + t.spdt * dxs, t.rad, t.hi);
@@ -444,7 +486,7 @@ __device__ __forceinline__ void tick(const Params& P, EnvSm<CAP>& e, const Grp<G
     if (a >= kAttackBase && e.h[u] > 0.0) {
       const int o = (u < P.na ? P.na : 0) + (a - kAttackBase);
       fire = e.h[o] > 0.0 && !(e.cd[u] > 0.0) && in_range(P, e, u, o);
-      if (fire) e.cd[u] = P.ts[P.type[u]].cdmax;
+      if (fire) e.cd[u] = P.ts[e.ty[u]].cdmax;
     }
     e.fire[u] = fire;
   }
@@ -461,7 +503,7 @@ __device__ __forceinline__ void tick(const Params& P, EnvSm<CAP>& e, const Grp<G
     double damage = 0.0;
     for (int k = 0; k < opp_n; ++k) {  // shooters in unit order
       const int u = opp0 + k;
-      if (e.fire[u] && e.act[u] - kAttackBase == me) damage += P.ts[P.type[u]].dmg;
+      if (e.fire[u] && e.act[u] - kAttackBase == me) damage += P.ts[e.ty[u]].dmg;
     }
     if (damage > 0.0) {
       double v = e.h[o] - damage;
@@ -485,7 +527,7 @@ __device__ __forceinline__ void pools(const Params& P, const EnvSm<CAP>& e, cons
 #pragma unroll
   for (int j = 0; j < UPL; ++j) {
     const int u = g.gl + G * j;
-    ratio[j] = u < P.n ? e.h[u] / P.ts[P.type[u]].hmax : 0.0;
+    ratio[j] = u < P.n ? e.h[u] / P.ts[e.ty[u]].hmax : 0.0;
   }
   p0 = 0.0;
   p1 = 0.0;
@@ -523,7 +565,7 @@ __device__ __forceinline__ int obs_slot(const Params& P, int me, int u) {
 template <int G, int UPL, int CAP>
 __device__ __forceinline__ void observe_part(const Params& P, const EnvSm<CAP>& e, int gl, int me, float* row) {
   const bool me_alive = e.h[me] > 0.0;
-  const TypeStat& my = P.ts[P.type[me]];
+  const TypeStat& my = P.ts[e.ty[me]];
 #pragma unroll
   for (int j = 0; j < UPL; ++j) {
     const int u = gl + G * j;
@@ -540,7 +582,7 @@ __device__ __forceinline__ void observe_part(const Params& P, const EnvSm<CAP>& 
       o[2] = float(e.x[me] / P.map);
       o[3] = float(e.y[me] / P.map);
 #pragma unroll
-      for (int q = 0; q < kTypes; ++q) o[4 + q] = q == P.type[me] ? 1.0f : 0.0f;
+      for (int q = 0; q < kTypes; ++q) o[4 + q] = q == e.ty[me] ? 1.0f : 0.0f;
       continue;
     }
     float* o = row + 10 + 17 * obs_slot(P, me, u);
@@ -549,14 +591,14 @@ __device__ __forceinline__ void observe_part(const Params& P, const EnvSm<CAP>& 
       for (int q = 0; q < 17; ++q) o[q] = 0.0f;
       continue;
     }
-    const TypeStat& st = P.ts[P.type[u]];
+    const TypeStat& st = P.ts[e.ty[u]];
     const double sight = my.sight.r;
     o[0] = 1.0f;
     o[1] = float((e.x[u] - e.x[me]) / sight);
     o[2] = float((e.y[u] - e.y[me]) / sight);
     o[3] = float(e.h[u] / st.hmax);
     o[4] = float(e.cd[u] / st.cdmax);
-    const int tu = P.type[u];
+    const int tu = e.ty[u];
 #pragma unroll
     for (int q = 0; q < kTypes; ++q) o[5 + q] = q == tu ? 1.0f : 0.0f;
     const int bucket = e.pa[u] <= kStop ? e.pa[u] : kStop + 1;  // action_bucket, smax.cpp:589
@@ -655,8 +697,9 @@ __device__ __forceinline__ void load_env(const Params& P, EnvSm<CAP>& e, const S
     e.y[u] = st.y[u * n + i];
     e.h[u] = st.health[u * n + i];
     e.cd[u] = st.cooldown[u * n + i];
-    const uint32_t m = st.mem[u * n + i];  // prev_action | ai_target<<8 | ai_sweep<<16
+    const uint32_t m = st.mem[u * n + i];  // prev_action | ai_target<<8 | ai_sweep<<16 | type<<24
     e.pa[u] = int8_t(m & 0xffu);
+    e.ty[u] = int8_t(m >> 24);
     tg[j] = int(int8_t((m >> 8) & 0xffu));
     sw[j] = int(int8_t((m >> 16) & 0xffu));
   }
@@ -674,7 +717,7 @@ __device__ __forceinline__ void store_env(const Params& P, const EnvSm<CAP>& e, 
     st.health[u * n + i] = e.h[u];
     st.cooldown[u * n + i] = e.cd[u];
     st.mem[u * n + i] = uint32_t(uint8_t(e.pa[u])) | (uint32_t(uint8_t(int8_t(tg[j]))) << 8) |
-                        (uint32_t(uint8_t(int8_t(sw[j]))) << 16);
+                        (uint32_t(uint8_t(int8_t(sw[j]))) << 16) | (uint32_t(uint8_t(e.ty[u])) << 24);
   }
 }
 
@@ -688,7 +731,14 @@ __device__ __noinline__ void env_reset(const Params& P, EnvSm<CAP>& e, const Grp
     const int u = g.gl + G * j;
     tg[j] = -1;
     sw[j] = -1;
-    if (u < P.n) spawn_unit(P, e, u, key);
+    if (u >= P.n) continue;
+    if (P.random_types) {  // randint1(fold_in(key, 10 + i | 500 + i), 0, kTypeCount) (smax.cpp:169-175)
+      const uint64_t d = u < P.na ? 10 + uint64_t(u) : 500 + uint64_t(u - P.na);
+      e.ty[u] = int8_t(block_at_nl(fold_in_nl(key, d), 0) % uint64_t(kTypes));
+    } else {
+      e.ty[u] = P.type[u];
+    }
+    spawn_unit(P, e, u, key);
   }
   g.sync();
   const LanePairs<G> lp(g.gl, P.n);  // rare path: built here rather than passed
@@ -887,8 +937,12 @@ __global__ void __launch_bounds__(kThreads, 3) smax_step_kernel(const Params* __
 // ------------------------------------------------- non-hot helper kernels
 // Env::legal_actions (smax.cpp:195-211) and state_hash (smax.cpp:312-337):
 // one thread per env straight from the HBM state.
+__device__ __forceinline__ int g_type(const SmaxState& st, int64_t n, int64_t i, int u) {
+  return int(int8_t(st.mem[u * n + i] >> 24));
+}
+
 __device__ __forceinline__ bool g_in_range(const Params& P, const SmaxState& st, int64_t n, int64_t i, int a, int b) {
-  const Thresh& r = P.ps[P.type[a]][P.type[b]].reach;
+  const Thresh& r = P.ps[g_type(st, n, i, a)][g_type(st, n, i, b)].reach;
   return dist_le(st.x[a * n + i] - st.x[b * n + i], st.y[a * n + i] - st.y[b * n + i], r.r, r.r2lo, r.r2hi);
 }
 
@@ -923,7 +977,7 @@ __global__ void smax_hash_kernel(const Params* __restrict__ gP, SmaxState st, in
     mix(__double_as_longlong(st.y[u * n + i]));
     mix(__double_as_longlong(st.health[u * n + i]));
     mix(__double_as_longlong(st.cooldown[u * n + i]));
-    mix(uint64_t(uint8_t(sP.type[u])));
+    mix(uint64_t(uint8_t(m >> 24)));  // type
     mix(uint64_t(uint16_t(int16_t(int8_t(m & 0xffu)))));         // prev_action
     mix(uint64_t(uint16_t(int16_t(int8_t((m >> 8) & 0xffu)))));  // ai_target
     mix(uint64_t(uint8_t((m >> 16) & 0xffu)));                   // ai_sweep
@@ -945,7 +999,8 @@ __global__ void smax_world_state_kernel(const Params* __restrict__ gP, SmaxState
   const int W = 18 * P.n + 1;
   float* w = out + size_t(i) * W;
   for (int u = 0; u < P.n; ++u) {
-    const TypeStat& t = P.ts[P.type[u]];
+    const int ty = g_type(st, n, i, u);
+    const TypeStat& t = P.ts[ty];
     const double h = st.health[u * n + i];
     const int pa = int(st.mem[u * n + i] & 0xffu);
     const int bucket = pa <= kStop ? pa : kStop + 1;
@@ -956,7 +1011,7 @@ __global__ void smax_world_state_kernel(const Params* __restrict__ gP, SmaxState
     o[3] = float(h / t.hmax);
     o[4] = float(st.cooldown[u * n + i] / t.cdmax);
     o[5] = float(u < P.na ? 0 : 1);
-    for (int q = 0; q < kTypes; ++q) o[6 + q] = q == P.type[u] ? 1.0f : 0.0f;
+    for (int q = 0; q < kTypes; ++q) o[6 + q] = q == ty ? 1.0f : 0.0f;
     for (int q = 0; q < 6; ++q) o[12 + q] = q == bucket ? 1.0f : 0.0f;
   }
   w[18 * P.n] = float(double(st.t[i]) / P.max_steps);
@@ -978,6 +1033,7 @@ Params make_params(const SmaxConfig& c) {
   P.map = c.map;
   P.jitter = c.jitter;
   for (int u = 0; u < P.n; ++u) P.type[u] = c.type[u];
+  P.random_types = c.random_types;
   for (int t = 0; t < kTypes; ++t) {
     const double* st = c.stats[t];  // health damage cooldown speed sight range radius
     TypeStat& T = P.ts[t];
@@ -1000,6 +1056,9 @@ Params make_params(const SmaxConfig& c) {
   P.sep_r2hi = 0.0;
   for (int a = 0; a < P.n; ++a)
     for (int b = 0; b < P.n; ++b) P.sep_r2hi = std::max(P.sep_r2hi, P.ps[P.type[a]][P.type[b]].rsum.r2hi);
+  if (c.random_types)  // any type pair can meet
+    for (int ta = 0; ta < kTypes; ++ta)
+      for (int tb = 0; tb < kTypes; ++tb) P.sep_r2hi = std::max(P.sep_r2hi, P.ps[ta][tb].rsum.r2hi);
   return P;
 }
 

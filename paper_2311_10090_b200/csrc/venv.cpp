@@ -287,9 +287,11 @@ void make_smax(Env& e, const std::string& scen, const json& cfg) {  // smax.cpp:
       raise(MARL_ERR_SCHEMA, e.id + ": random-type scenarios need both ally_units and enemy_units");
     random_types = 0;
   }
-  if (random_types > 0)
-    raise(MARL_ERR_NOT_FOUND, e.id + ": per-episode random unit types (smacv2 spawns, smax.cpp:456-479) are "
-                                     "not implemented by the B200 engine; pass ally_units and enemy_units");
+  c.random_types = random_types;
+  if (random_types > 0) {  // smax.cpp:144-146: both teams have random_types units
+    ally.assign(size_t(random_types), 0);
+    enemy.assign(size_t(random_types), 0);
+  }
   c.na = int(ally.size());
   c.ne = int(enemy.size());
   if (c.na < 1 || c.ne < 1) raise(MARL_ERR_SCHEMA, e.id + ": both teams need at least one unit");
