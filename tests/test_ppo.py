@@ -291,3 +291,25 @@ def test_tc_training_run_is_sane():
     assert not res.diverged and np.isfinite(m).all() and m.shape[0] == 4
     assert m[-1, 6] < m[0, 6]  # v_loss
     assert np.isfinite(res.actor).all() and np.isfinite(res.critic).all()
+
+
+@pytest.mark.gpu
+def test_divergence_rolls_back_the_update():
+    """A non-finite loss is the reference's DivergenceError (actor_critic.hpp:403-405):
+    the update's parameters are restored, the row counts no minibatch and the
+    run stops (ppo.cpp:630-650)."""
+    import paper_2311_10090_b200 as m
+    from paper_2311_10090_b200.ppo import PpoTrainer
+    v = m.VectorEnv(m.make_env("MPE_simple_spread_v3", {}), 16, device=0)
+    tr = PpoTrainer(v, {"n_envs": 16, "n_rollout_steps": 8, "total_timesteps": 5 * 16 * 8})
+    tr.begin(O.key_from_seed(4))
+    a, c = tr.params()
+    c = c.copy()
+    c[-1] = np.inf  # the critic head bias: every value is inf -> non-finite v_loss
+    tr.set_params(a, c)
+    tr.collect()
+    row, diverged = tr.update()
+    assert diverged
+    a2, c2 = tr.params()
+    assert np.array_equal(a2, a) and np.array_equal(c2[:-1], c[:-1]) and np.isinf(c2[-1])
+    assert np.all(row[4:11] == 0.0)  # no minibatch completed: the sums are empty
