@@ -266,10 +266,39 @@ struct RnnSeqArgs {
   const uint8_t* resets;     // [T][R]
   RnnCache ca, cc;
 };
-void rnn_forward(const RnnSeqArgs& a, bool actor, cudaStream_t st);
-void rnn_backward(const RnnSeqArgs& a, bool actor, cudaStream_t st);
-void rnn_outer_sum(const float* D, int ldd, const float* X, int ldx, int64_t K, int O, int I, float* G,
-                   cudaStream_t st);
+// GEMM-structured update: per time step t, over the M rows of a chunk.
+struct RnnWPtrs {  // the branch's matrices / biases in RnnBranch pack order
+  const float *we, *be, *wx, *uh, *bias6, *wp, *bp, *wh, *bh;  // wx = [Wz;Wr;Wn], uh = [Uz;Ur;Un]
+};
+RnnWPtrs rnn_weights(const float* p, int in, int F, int H, int out);
+struct RnnStepArgs {
+  int t;
+  int64_t M, R;
+  int in, H;
+  const int32_t* rows;
+  const uint8_t* resets;
+  const float* src;  // [T][R][in] input rows
+  const float* h0;   // [R][H] hidden at the window start
+  float* h;          // [M][H] running hidden
+  float* x;          // cache x_t     [M][in]
+  float *hprev, *z, *r, *c, *ah, *hn;  // caches at step t [M][H]
+  struct {
+    const float *bzx, *brx, *bnx, *bzh, *brh, *bnh;
+  } w;
+};
+void rnn_step_gather(const RnnStepArgs& a, cudaStream_t s);
+// GEMM-structured acting step of the collector (many rows)
+void rnn_policy_rows(const PolicyStep& s, const RolloutBufs& b, int in, int CI, int NA, int H, float* xa, float* xc,
+                     float* ha, float* hc, float* hc_peek, cudaStream_t st);
+void rnn_gates_inplace(int64_t M, int H, float* h, const float* gx, const float* gh, const float* b6, cudaStream_t st);
+void rnn_policy_sample(const PolicyStep& s, const RolloutBufs& b, int NA, const float* ya, const float* yc,
+                       cudaStream_t st);
+void rnn_bias_act(float* y, int64_t M, int N, const float* b, bool act, int relu, cudaStream_t s);
+void rnn_gates(const RnnStepArgs& a, const float* gx, const float* gh, cudaStream_t s);
+void rnn_act_grad(float* g, const float* y, int64_t n, int relu, cudaStream_t s);
+void rnn_gru_bwd(const RnnStepArgs& a, const float* dhs, float* d4, float* dh, cudaStream_t s);
+void rnn_cut(const RnnStepArgs& a, float* dh, cudaStream_t s);
+
 // flat[k = t*M + i] = t*R + rows[i] (the loss rows of rnn_minibatch, ppo.cpp:472-477)
 void rnn_flat_slots(const int32_t* rows, int64_t M, int T, int64_t R, int32_t* flat, cudaStream_t st);
 // ppo_row_loss over the K flat rows from the cached head outputs -> ca.dy, cc.dy;

@@ -8,17 +8,17 @@
 //                       head, for actor (then masked sampling) and critic, the
 //                       hidden states carried in place; bootstrap mode peeks
 //                       the critic without advancing it (ppo.cpp:283-296).
-//   rnn_fwd_kernel    : rnn_seq_forward with cache over a minibatch of row
-//                       sequences (rnn_minibatch, ppo.cpp:444-509).
-//   rnn_loss_kernel   : the per-row part of ppo_row_loss over the [t][i] rows.
-//   rnn_bwd_kernel    : rnn_seq_backward (actor_critic.hpp:164-196): BPTT with
-//                       the hidden chain cut at the forward's resets; stores the
-//                       per-(t, row) deltas.
-//   outer_sum_kernel  : the weight gradients sum_k delta[k] (x) input[k] over
-//                       all (t, row) (matmul_tn per step + axpy over steps).
-// One thread owns one row (sequence); weights are read through L1 (every
-// thread of a warp reads the same element).  This is the parity path; the
-// caches hold every step of the minibatch, so the host guards its size.
+//   rnn_rows / gate / sample kernels : the same step for many rows as SGEMMs
+//                       (issued by the host) around elementwise kernels.
+//   update            : rnn_minibatch (ppo.cpp:444-509) GEMM-structured: per
+//                       time step over all rows of a chunk, the gather / reset,
+//                       gate and activation-gradient kernels below between
+//                       SGEMMs for rnn_seq_forward with cache and
+//                       rnn_seq_backward (BPTT with the hidden chain cut at the
+//                       forward's resets); rnn_loss_kernel is the per-row part
+//                       of ppo_row_loss; the weight gradients are one SGEMM per
+//                       matrix over every (t, row).  Chunks of rows bound the
+//                       caches (the host sizes them to the free HBM).
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -38,7 +38,7 @@ struct RnnW {  // one branch in RnnBranch pack order (actor_critic.hpp:198-209)
   const float *we, *be, *wz, *wr, *wn, *uz, *ur, *un, *bzx, *brx, *bnx, *bzh, *brh, *bnh, *wp, *bp, *wh, *bh;
 };
 
-__device__ RnnW rnn_w(const float* p, int in, int F, int H, int out) {
+__host__ __device__ RnnW rnn_w(const float* p, int in, int F, int H, int out) {
   RnnW w;
   w.we = p;
   w.be = w.we + F * in;
@@ -60,6 +60,8 @@ __device__ RnnW rnn_w(const float* p, int in, int F, int H, int out) {
   w.bh = w.wh + out * F;
   return w;
 }
+
+RnnW rnn_w_host(const float* p, int in, int F, int H, int out) { return rnn_w(p, in, F, H, out); }
 
 __device__ __forceinline__ float dotr(const float* __restrict__ x, const float* __restrict__ w, int n) {
   float acc = 0.0f;  // matmul_nt: acc += x[i] * w[i], i ascending (nn.hpp:42-54)
@@ -143,137 +145,6 @@ __global__ void __launch_bounds__(128) rnn_policy_kernel(RnnPolicyArgs a, Policy
   rnn_row_step(wa, in, F, H, NA, a.relu, x, h, y, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr);
   for (int c = 0; c < H; ++c) ha[c] = h[c];
   sample_and_record(s, b, r, y, NA, value);
-}
-
-// ---- update: rnn_seq_forward with cache over M row sequences x T steps.
-// Cache layout: [T*M][width] row-major, k = t*M + i (the loss's flat order).
-__global__ void __launch_bounds__(128) rnn_fwd_kernel(RnnSeqArgs a, bool actor) {
-  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= a.M) return;
-  const int in = actor ? a.in_dim : a.critic_in, F = a.F, H = a.H, out = actor ? a.n_act : 1;
-  const RnnW w = rnn_w(actor ? a.actor : a.critic, in, F, H, out);
-  const RnnCache& c = actor ? a.ca : a.cc;
-  const int64_t row = a.rows[i];
-  float h[kRnnMaxH], x[kRnnMaxIn];
-  const float* h0 = (actor ? a.h0_actor : a.h0_critic) + size_t(row) * H;
-  for (int q = 0; q < H; ++q) h[q] = h0[q];
-  for (int t = 0; t < a.T; ++t) {
-    const size_t slot = size_t(t) * size_t(a.R) + size_t(row), k = size_t(t) * size_t(a.M) + size_t(i);
-    if (a.resets[slot])
-      for (int q = 0; q < H; ++q) h[q] = 0.0f;  // apply_reset (actor_critic.hpp:95-101)
-    const float* src = (actor || !a.critic_rows) ? a.obs + slot * size_t(a.in_dim) : a.critic_rows + slot * size_t(in);
-    for (int q = 0; q < in; ++q) x[q] = src[q];
-    for (int q = 0; q < in; ++q) c.x[k * in + q] = x[q];
-    rnn_row_step(w, in, F, H, out, a.relu, x, h, c.y + k * out, c.e + k * F, c.h + k * H, c.z + k * H, c.r + k * H,
-                 c.c + k * H, c.ah + k * H, c.p + k * F);
-    for (int q = 0; q < H; ++q) c.hn[k * H + q] = h[q];
-  }
-}
-
-// ---- rnn_seq_backward for one row sequence (actor_critic.hpp:164-196)
-__global__ void __launch_bounds__(128) rnn_bwd_kernel(RnnSeqArgs a, bool actor) {
-  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= a.M) return;
-  const int in = actor ? a.in_dim : a.critic_in, F = a.F, H = a.H, out = actor ? a.n_act : 1;
-  const RnnW w = rnn_w(actor ? a.actor : a.critic, in, F, H, out);
-  const RnnCache& c = actor ? a.ca : a.cc;
-  const int64_t row = a.rows[i];
-  float dh[kRnnMaxH], dhs[kRnnMaxH], dp[kRnnMaxF], dzp[kRnnMaxF];
-  for (int q = 0; q < H; ++q) dh[q] = 0.0f;
-  bool have_dh = false;
-  for (int t = a.T - 1; t >= 0; --t) {
-    const size_t k = size_t(t) * size_t(a.M) + size_t(i), slot = size_t(t) * size_t(a.R) + size_t(row);
-    const float* dy = c.dy + k * out;
-    // head: dp = dy . Wh (matmul_nn skips zero dy, nn.hpp:74-88)
-    for (int f = 0; f < F; ++f) dp[f] = 0.0f;
-    for (int o = 0; o < out; ++o) {
-      const float g = dy[o];
-      if (g == 0.0f) continue;
-      for (int f = 0; f < F; ++f) dp[f] = __fadd_rn(dp[f], __fmul_rn(g, __ldg(w.wh + o * F + f)));
-    }
-    // post: dz = dp * act'(p); dh_step = dz . Wp  (+ the carried dh)
-    const float* pz = c.p + k * F;
-    for (int f = 0; f < F; ++f) dzp[f] = actg(dp[f], pz[f], a.relu);
-    for (int f = 0; f < F; ++f) c.dzp[k * F + f] = dzp[f];
-    for (int q = 0; q < H; ++q) dhs[q] = 0.0f;
-    for (int f = 0; f < F; ++f) {
-      const float g = dzp[f];
-      if (g == 0.0f) continue;
-      for (int q = 0; q < H; ++q) dhs[q] = __fadd_rn(dhs[q], __fmul_rn(g, __ldg(w.wp + f * H + q)));
-    }
-    if (have_dh)
-      for (int q = 0; q < H; ++q) dhs[q] = __fadd_rn(dhs[q], dh[q]);
-    // gru_backward (nn.hpp:270-318), elementwise part
-    float* daz = c.daz + k * H;
-    float* dar = c.dar + k * H;
-    float* dac = c.dac + k * H;
-    float* dah = c.dah + k * H;
-    const float *hp = c.h + k * H, *zz = c.z + k * H, *rr = c.r + k * H, *cc = c.c + k * H, *ahh = c.ah + k * H;
-    for (int q = 0; q < H; ++q) {
-      const float g = dhs[q], z = zz[q], r = rr[q], cd = cc[q];
-      const float dz = __fmul_rn(g, __fsub_rn(hp[q], cd));
-      const float dc = __fmul_rn(g, __fsub_rn(1.0f, z));
-      const float ac = __fmul_rn(dc, __fsub_rn(1.0f, __fmul_rn(cd, cd)));
-      dac[q] = ac;
-      dah[q] = __fmul_rn(ac, r);
-      const float dr = __fmul_rn(ac, ahh[q]);
-      dar[q] = __fmul_rn(__fmul_rn(dr, r), __fsub_rn(1.0f, r));
-      daz[q] = __fmul_rn(__fmul_rn(dz, z), __fsub_rn(1.0f, z));
-      dh[q] = __fmul_rn(g, z);  // the carry path
-    }
-    // de = daz.Wz + (dar.Wr + dac.Wn); dh_prev = dh_acc + ((daz.Uz + dar.Ur) + dah.Un)
-    float de[kRnnMaxF];
-    {
-      float t0[kRnnMaxF], t1[kRnnMaxF], t2[kRnnMaxF];
-      for (int f = 0; f < F; ++f) t0[f] = t1[f] = t2[f] = 0.0f;
-      for (int q = 0; q < H; ++q) {
-        const float gz = daz[q], gr = dar[q], gc = dac[q];
-        if (gz != 0.0f)
-          for (int f = 0; f < F; ++f) t0[f] = __fadd_rn(t0[f], __fmul_rn(gz, __ldg(w.wz + q * F + f)));
-        if (gr != 0.0f)
-          for (int f = 0; f < F; ++f) t1[f] = __fadd_rn(t1[f], __fmul_rn(gr, __ldg(w.wr + q * F + f)));
-        if (gc != 0.0f)
-          for (int f = 0; f < F; ++f) t2[f] = __fadd_rn(t2[f], __fmul_rn(gc, __ldg(w.wn + q * F + f)));
-      }
-      for (int f = 0; f < F; ++f) de[f] = __fadd_rn(t0[f], __fadd_rn(t1[f], t2[f]));
-    }
-    {
-      float t0[kRnnMaxH], t1[kRnnMaxH], t2[kRnnMaxH];
-      for (int q = 0; q < H; ++q) t0[q] = t1[q] = t2[q] = 0.0f;
-      for (int o = 0; o < H; ++o) {
-        const float gz = daz[o], gr = dar[o], gh = dah[o];
-        if (gz != 0.0f)
-          for (int q = 0; q < H; ++q) t0[q] = __fadd_rn(t0[q], __fmul_rn(gz, __ldg(w.uz + o * H + q)));
-        if (gr != 0.0f)
-          for (int q = 0; q < H; ++q) t1[q] = __fadd_rn(t1[q], __fmul_rn(gr, __ldg(w.ur + o * H + q)));
-        if (gh != 0.0f)
-          for (int q = 0; q < H; ++q) t2[q] = __fadd_rn(t2[q], __fmul_rn(gh, __ldg(w.un + o * H + q)));
-      }
-      for (int q = 0; q < H; ++q) dh[q] = __fadd_rn(dh[q], __fadd_rn(__fadd_rn(t0[q], t1[q]), t2[q]));
-    }
-    // embed: dz_e = de * act'(e)
-    const float* ee = c.e + k * F;
-    for (int f = 0; f < F; ++f) c.dze[k * F + f] = actg(de[f], ee[f], a.relu);
-    if (a.resets[slot])
-      for (int q = 0; q < H; ++q) dh[q] = 0.0f;  // no gradient across episode cuts
-    have_dh = true;
-  }
-}
-
-// G[o][i] (+)= sum_k D[k*ldd + o] * X[k*ldx + i]  (X == null: bias, sum_k D)
-__global__ void outer_sum_kernel(const float* __restrict__ D, int ldd, const float* __restrict__ X, int ldx,
-                                 int64_t K, int O, int I, float* __restrict__ G) {
-  const int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  const int cols = X ? I : 1;
-  if (e >= int64_t(O) * cols) return;
-  const int o = int(e / cols), i = int(e % cols);
-  float acc = 0.0f;
-  if (X) {
-    for (int64_t k = 0; k < K; ++k) acc = __fadd_rn(acc, __fmul_rn(D[k * ldd + o], X[k * ldx + i]));
-  } else {
-    for (int64_t k = 0; k < K; ++k) acc = __fadd_rn(acc, D[k * ldd + o]);
-  }
-  G[e] = acc;
 }
 
 __global__ void flat_slots_kernel(const int32_t* __restrict__ rows, int64_t M, int T, int64_t R,
@@ -371,7 +242,194 @@ __global__ void __launch_bounds__(kLossThreads) rnn_loss_kernel(RnnSeqArgs a, co
   }
 }
 
+// ---- elementwise kernels of the GEMM-structured update (rnn_seq_forward /
+// rnn_seq_backward, one launch per time step over all M rows; the GEMMs
+// between them are plain library SGEMMs issued by the host, venv.cpp)
+__global__ void sq_gather_kernel(RnnStepArgs a) {  // x_t rows and h_prev_t (apply_reset)
+  const int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t M = a.M, in = a.in, H = a.H;
+  if (q < M * in) {
+    const int64_t i = q / in, j = q - i * in;
+    const size_t slot = size_t(a.t) * size_t(a.R) + size_t(a.rows[i]);
+    a.x[i * in + j] = a.src[slot * size_t(in) + j];
+  }
+  if (q < M * H) {
+    const int64_t i = q / H, c = q - i * H;
+    const size_t slot = size_t(a.t) * size_t(a.R) + size_t(a.rows[i]);
+    const float hv = a.t == 0 ? a.h0[size_t(a.rows[i]) * H + c] : a.h[i * H + c];
+    const float v = a.resets[slot] ? 0.0f : hv;
+    a.hprev[i * H + c] = v;
+    a.h[i * H + c] = v;
+  }
+}
+
+__global__ void bias_act_kernel(float* __restrict__ y, int64_t M, int N, const float* __restrict__ b, int act,
+                                int relu) {  // dense_forward's + b, then act_inplace (nn.hpp:108-115)
+  const int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (q >= M * N) return;
+  const float v = __fadd_rn(y[q], __ldg(b + q % N));
+  y[q] = act ? actf(v, relu) : v;
+}
+
+// gru_step's elementwise part (nn.hpp:231-260) from gx = e.[Wz;Wr;Wn]^T and
+// gh = h.[Uz;Ur;Un]^T
+__global__ void gru_gate_kernel(RnnStepArgs a, const float* __restrict__ gx, const float* __restrict__ gh) {
+  const int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int H = a.H;
+  if (q >= a.M * H) return;
+  const int64_t i = q / H;
+  const int c = int(q - i * H);
+  const float* gxi = gx + i * 3 * H;
+  const float* ghi = gh + i * 3 * H;
+  const auto& w = a.w;
+  const float z = sigm(__fadd_rn(gxi[c], __fadd_rn(__fadd_rn(__ldg(w.bzx + c), ghi[c]), __ldg(w.bzh + c))));
+  const float r = sigm(__fadd_rn(gxi[H + c], __fadd_rn(__fadd_rn(__ldg(w.brx + c), ghi[H + c]), __ldg(w.brh + c))));
+  const float ah = __fadd_rn(ghi[2 * H + c], __ldg(w.bnh + c));
+  const float cand = tanhf(__fadd_rn(__fadd_rn(gxi[2 * H + c], __ldg(w.bnx + c)), __fmul_rn(r, ah)));
+  const float hp = a.hprev[q];
+  const float hn = __fadd_rn(__fmul_rn(z, hp), __fmul_rn(__fsub_rn(1.0f, z), cand));
+  a.z[q] = z;
+  a.r[q] = r;
+  a.c[q] = cand;
+  a.ah[q] = ah;
+  a.hn[q] = hn;
+  a.h[q] = hn;
+}
+
+__global__ void act_grad_kernel(float* __restrict__ g, const float* __restrict__ y, int64_t n, int relu) {
+  const int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (q < n) g[q] = actg(g[q], y[q], relu);
+}
+
+// gru_backward's elementwise part (nn.hpp:276-289): dhs -> D4 = [daz | dar | dac | dah], dh = g * z
+__global__ void gru_bwd_kernel(RnnStepArgs a, const float* __restrict__ dhs, float* __restrict__ d4,
+                               float* __restrict__ dh) {
+  const int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int H = a.H;
+  if (q >= a.M * H) return;
+  const int64_t i = q / H;
+  const int c = int(q - i * H);
+  const float g = dhs[q], z = a.z[q], r = a.r[q], cd = a.c[q];
+  const float dz = __fmul_rn(g, __fsub_rn(a.hprev[q], cd));
+  const float dc = __fmul_rn(g, __fsub_rn(1.0f, z));
+  const float ac = __fmul_rn(dc, __fsub_rn(1.0f, __fmul_rn(cd, cd)));
+  float* o = d4 + i * 4 * H;
+  o[2 * H + c] = ac;
+  o[3 * H + c] = __fmul_rn(ac, r);
+  o[H + c] = __fmul_rn(__fmul_rn(__fmul_rn(ac, a.ah[q]), r), __fsub_rn(1.0f, r));
+  o[c] = __fmul_rn(__fmul_rn(dz, z), __fsub_rn(1.0f, z));
+  dh[q] = __fmul_rn(g, z);
+}
+
+__global__ void cut_kernel(RnnStepArgs a, float* __restrict__ dh) {  // no gradient across episode cuts
+  const int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (q >= a.M * a.H) return;
+  const int64_t i = q / a.H;
+  if (a.resets[size_t(a.t) * size_t(a.R) + size_t(a.rows[i])]) dh[q] = 0.0f;
+}
+
+unsigned nb(int64_t n) { return unsigned(std::max<int64_t>((n + 255) / 256, 1)); }
+
+// The collector's recurrent step for many rows (GEMM-structured): per row the
+// TeamLayout input (+ buffer writes), the critic row, and the hidden states
+// reset at the env's episode boundary; bootstrap peeks a copy of the critic's.
+__global__ void rnn_rows_kernel(PolicyStep s, RolloutBufs b, int in, int CI, int NA, int H, float* __restrict__ xa,
+                                float* __restrict__ xc, float* __restrict__ ha, float* __restrict__ hc,
+                                float* __restrict__ hc_peek) {
+  const int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (r >= s.R) return;
+  float x[1024];
+  fill_row(s, b, r, in, NA, x, !s.bootstrap);
+  for (int k = 0; k < in; ++k) xa[size_t(r) * in + k] = x[k];
+  const float* src = s.ws ? s.ws + size_t(r / s.A) * CI : x;
+  for (int k = 0; k < CI; ++k) xc[size_t(r) * CI + k] = src[k];
+  if (s.ws && !s.bootstrap) {
+    float* bc = b.critic_in + (size_t(s.t) * size_t(s.R) + size_t(r)) * CI;
+    for (int k = 0; k < CI; ++k) bc[k] = src[k];
+  }
+  const bool reset = s.prev_finished ? s.prev_finished[r / s.A] != 0 : true;
+  if (s.bootstrap) {
+    for (int c = 0; c < H; ++c) hc_peek[size_t(r) * H + c] = reset ? 0.0f : hc[size_t(r) * H + c];
+  } else if (reset) {
+    for (int c = 0; c < H; ++c) ha[size_t(r) * H + c] = 0.0f;
+    for (int c = 0; c < H; ++c) hc[size_t(r) * H + c] = 0.0f;
+  }
+}
+
+// gates in place on h (hn = z h + (1 - z) c), no caches: the acting step
+__global__ void gru_gate_inplace_kernel(int64_t M, int H, float* __restrict__ h, const float* __restrict__ gx,
+                                        const float* __restrict__ gh, const float* __restrict__ b6) {
+  const int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (q >= M * H) return;
+  const int64_t i = q / H;
+  const int c = int(q - i * H);
+  const float* gxi = gx + i * 3 * H;
+  const float* ghi = gh + i * 3 * H;
+  const float z = sigm(__fadd_rn(gxi[c], __fadd_rn(__fadd_rn(__ldg(b6 + c), ghi[c]), __ldg(b6 + 3 * H + c))));
+  const float r = sigm(__fadd_rn(gxi[H + c], __fadd_rn(__fadd_rn(__ldg(b6 + H + c), ghi[H + c]),
+                                                      __ldg(b6 + 4 * H + c))));
+  const float ah = __fadd_rn(ghi[2 * H + c], __ldg(b6 + 5 * H + c));
+  const float cand = tanhf(__fadd_rn(__fadd_rn(gxi[2 * H + c], __ldg(b6 + 2 * H + c)), __fmul_rn(r, ah)));
+  h[q] = __fadd_rn(__fmul_rn(z, h[q]), __fmul_rn(__fsub_rn(1.0f, z), cand));
+}
+
+__global__ void rnn_sample_kernel(PolicyStep s, RolloutBufs b, int NA, const float* __restrict__ ya,
+                                  const float* __restrict__ yc) {
+  const int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (r >= s.R) return;
+  if (s.bootstrap) {
+    b.last_value[r] = yc[r];
+    return;
+  }
+  sample_and_record(s, b, r, ya + size_t(r) * NA, NA, yc[r]);
+}
+
 }  // namespace
+
+void rnn_policy_rows(const PolicyStep& s, const RolloutBufs& b, int in, int CI, int NA, int H, float* xa, float* xc,
+                     float* ha, float* hc, float* hc_peek, cudaStream_t st) {
+  rnn_rows_kernel<<<unsigned((s.R + 127) / 128), 128, 0, st>>>(s, b, in, CI, NA, H, xa, xc, ha, hc, hc_peek);
+  ++g_launches;
+}
+void rnn_gates_inplace(int64_t M, int H, float* h, const float* gx, const float* gh, const float* b6, cudaStream_t st) {
+  gru_gate_inplace_kernel<<<nb(M * H), 256, 0, st>>>(M, H, h, gx, gh, b6);
+  ++g_launches;
+}
+void rnn_policy_sample(const PolicyStep& s, const RolloutBufs& b, int NA, const float* ya, const float* yc,
+                       cudaStream_t st) {
+  rnn_sample_kernel<<<unsigned((s.R + 127) / 128), 128, 0, st>>>(s, b, NA, ya, yc);
+  ++g_launches;
+}
+
+RnnWPtrs rnn_weights(const float* p, int in, int F, int H, int out) {
+  const auto w = rnn_w_host(p, in, F, H, out);
+  return RnnWPtrs{w.we, w.be, w.wz, w.uz, w.bzx, w.wp, w.bp, w.wh, w.bh};
+}
+
+void rnn_step_gather(const RnnStepArgs& a, cudaStream_t s) {
+  sq_gather_kernel<<<nb(a.M * std::max(a.in, a.H)), 256, 0, s>>>(a);
+  ++g_launches;
+}
+void rnn_bias_act(float* y, int64_t M, int N, const float* b, bool act, int relu, cudaStream_t s) {
+  bias_act_kernel<<<nb(M * N), 256, 0, s>>>(y, M, N, b, act ? 1 : 0, relu);
+  ++g_launches;
+}
+void rnn_gates(const RnnStepArgs& a, const float* gx, const float* gh, cudaStream_t s) {
+  gru_gate_kernel<<<nb(a.M * a.H), 256, 0, s>>>(a, gx, gh);
+  ++g_launches;
+}
+void rnn_act_grad(float* g, const float* y, int64_t n, int relu, cudaStream_t s) {
+  act_grad_kernel<<<nb(n), 256, 0, s>>>(g, y, n, relu);
+  ++g_launches;
+}
+void rnn_gru_bwd(const RnnStepArgs& a, const float* dhs, float* d4, float* dh, cudaStream_t s) {
+  gru_bwd_kernel<<<nb(a.M * a.H), 256, 0, s>>>(a, dhs, d4, dh);
+  ++g_launches;
+}
+void rnn_cut(const RnnStepArgs& a, float* dh, cudaStream_t s) {
+  cut_kernel<<<nb(a.M * a.H), 256, 0, s>>>(a, dh);
+  ++g_launches;
+}
 
 int rnn_loss_blocks(int64_t K) { return int(std::max<int64_t>((K + kLossThreads - 1) / kLossThreads, 1)); }
 
@@ -394,21 +452,7 @@ void rnn_policy(const RnnPolicyArgs& a, const PolicyStep& s, const RolloutBufs& 
   ++g_launches;
 }
 
-void rnn_forward(const RnnSeqArgs& a, bool actor, cudaStream_t st) {
-  rnn_fwd_kernel<<<unsigned((a.M + 127) / 128), 128, 0, st>>>(a, actor);
-  ++g_launches;
-}
 
-void rnn_backward(const RnnSeqArgs& a, bool actor, cudaStream_t st) {
-  rnn_bwd_kernel<<<unsigned((a.M + 127) / 128), 128, 0, st>>>(a, actor);
-  ++g_launches;
-}
 
-void rnn_outer_sum(const float* D, int ldd, const float* X, int ldx, int64_t K, int O, int I, float* G,
-                   cudaStream_t st) {
-  const int64_t n = int64_t(O) * (X ? I : 1);
-  outer_sum_kernel<<<unsigned((n + 127) / 128), 128, 0, st>>>(D, ldd, X, ldx, K, O, I, G);
-  ++g_launches;
-}
 
 }  // namespace marl_b200

@@ -1040,6 +1040,10 @@ struct marl_rollout {
   // states and their copy at the window start (Rollout::h0_*, ppo.cpp:175, 219-222)
   int recurrent = 0, F = 0, H = 0;
   float *h_actor = nullptr, *h_critic = nullptr, *h0_actor = nullptr, *h0_critic = nullptr;
+  // GEMM-structured acting step (R >= 4096 rows, or MARL_RNN_COLLECT=gemm|rows)
+  bool rnn_gemm = false;
+  float *s_xa = nullptr, *s_xc = nullptr, *s_e = nullptr, *s_gx = nullptr, *s_gh = nullptr, *s_p = nullptr,
+        *s_ya = nullptr, *s_yc = nullptr, *s_hpeek = nullptr;
 };
 
 namespace {
@@ -1090,6 +1094,36 @@ PolicyNetBf16 net_bf16_of(const marl_rollout* r) {
   return n;
 }
 
+void gemm_nt(cudaStream_t st, int64_t M, int N, int K, const float* A, int lda, const float* B, int ldb, float* C,
+             int ldc, float beta);
+
+// rnn_step of actor and critic for all R rows as SGEMMs (embed, GRU input and
+// hidden paths, post, head) around the gate kernel; same arithmetic as the
+// per-row kernel up to the GEMMs' summation order.
+void rnn_collect_gemm(marl_rollout* r, const PolicyStep& s) {
+  cudaStream_t st = r->h->stream;
+  const int64_t R = r->R;
+  const int in = r->in_dim, CI = r->critic_in, NA = r->n_act, F = r->F, H = r->H;
+  rnn_policy_rows(s, r->b, in, CI, NA, H, r->s_xa, r->s_xc, r->h_actor, r->h_critic, r->s_hpeek, st);
+  for (int branch = (s.bootstrap ? 1 : 0); branch < 2; ++branch) {
+    const int bin = branch == 0 ? in : CI, out = branch == 0 ? NA : 1;
+    const RnnWPtrs w = rnn_weights(branch == 0 ? r->params : r->params + r->n_actor, bin, F, H, out);
+    float* h = branch == 0 ? r->h_actor : (s.bootstrap ? r->s_hpeek : r->h_critic);
+    const float* x = branch == 0 ? r->s_xa : r->s_xc;
+    float* y = branch == 0 ? r->s_ya : r->s_yc;
+    gemm_nt(st, R, F, bin, x, bin, w.we, bin, r->s_e, F, 0.0f);
+    rnn_bias_act(r->s_e, R, F, w.be, true, r->relu, st);
+    gemm_nt(st, R, 3 * H, F, r->s_e, F, w.wx, F, r->s_gx, 3 * H, 0.0f);
+    gemm_nt(st, R, 3 * H, H, h, H, w.uh, H, r->s_gh, 3 * H, 0.0f);
+    rnn_gates_inplace(R, H, h, r->s_gx, r->s_gh, w.bias6, st);
+    gemm_nt(st, R, F, H, h, H, w.wp, H, r->s_p, F, 0.0f);
+    rnn_bias_act(r->s_p, R, F, w.bp, true, r->relu, st);
+    gemm_nt(st, R, out, F, r->s_p, F, w.wh, F, y, out, 0.0f);
+    rnn_bias_act(y, R, out, w.bh, false, r->relu, st);
+  }
+  rnn_policy_sample(s, r->b, NA, r->s_ya, r->s_yc, st);
+}
+
 void run_policy(marl_rollout* r, int t, bool bootstrap, int64_t seq_base) {
   marl_venv* h = r->h;
   const Env& e = *h->env;
@@ -1114,7 +1148,9 @@ void run_policy(marl_rollout* r, int t, bool bootstrap, int64_t seq_base) {
   s.legal_ready = (!bootstrap && e.family == MARL_FAMILY_SMAX) ? 1 : 0;
   if (s.legal_ready)  // Env::legal_actions straight into the buffer slice (team.cpp:35-42)
     smax_launch_legal(e.smax, h->smax, h->n, r->n_act, r->b.legal + size_t(t) * size_t(r->R) * r->n_act, h->stream);
-  if (r->recurrent) {
+  if (r->recurrent && r->rnn_gemm) {
+    rnn_collect_gemm(r, s);
+  } else if (r->recurrent) {
     RnnPolicyArgs ra{};
     ra.actor = r->params;
     ra.critic = r->params + r->n_actor;
@@ -1227,6 +1263,20 @@ static marl_rollout* rollout_create_impl(marl_venv* h, int T, int width, int n_l
       r->H = hidden;
       for (float** q : {&r->h_actor, &r->h_critic, &r->h0_actor, &r->h0_critic})
         ar.add(q, size_t(r->R) * size_t(hidden));
+      const char* mode = std::getenv("MARL_RNN_COLLECT");
+      r->rnn_gemm = mode ? std::string(mode) == "gemm" : r->R >= 4096;
+      if (r->rnn_gemm) {
+        const size_t R = size_t(r->R);
+        ar.add(&r->s_xa, R * r->in_dim);
+        ar.add(&r->s_xc, R * r->critic_in);
+        ar.add(&r->s_e, R * width);
+        ar.add(&r->s_p, R * width);
+        ar.add(&r->s_gx, R * 3 * hidden);
+        ar.add(&r->s_gh, R * 3 * hidden);
+        ar.add(&r->s_ya, R * r->n_act);
+        ar.add(&r->s_yc, R);
+        ar.add(&r->s_hpeek, R * hidden);
+      }
     }
     ar.commit();
     cuda_check(cudaMemcpy(r->agent_actions, e.n_actions.data(), size_t(e.A) * 4, cudaMemcpyHostToDevice), "cudaMemcpy");
@@ -1685,6 +1735,9 @@ struct marl_ppo {
   bool recurrent = false;
   RnnCache rca{}, rcc{};
   int32_t* rnn_flat = nullptr;
+  int64_t rnn_chunk = 0;  // rows per BPTT chunk (caches sized for it)
+  int rnn_blocks = 0;     // loss partial blocks of the last minibatch
+  float *rnn_h = nullptr, *rnn_gx = nullptr, *rnn_gh = nullptr, *rnn_dh = nullptr, *rnn_ones = nullptr;
   ~marl_ppo();
 };
 
@@ -1721,6 +1774,70 @@ const Nccl& nccl() {
   if (!n.lib || !n.comm_init_rank || !n.all_reduce || !n.get_unique_id)
     raise(MARL_ERR_CUDA, "NCCL (libnccl.so.2) is not loadable in this process");
   return n;
+}
+
+// cuBLAS SGEMM / SGEMV for the recurrent update's per-step GEMMs (plain
+// library GEMMs), loaded at run time like NCCL (torch's copy when loaded).
+struct Blas {
+  void* lib = nullptr;
+  void* handle = nullptr;
+  int (*create)(void**) = nullptr;
+  int (*set_stream)(void*, cudaStream_t) = nullptr;
+  int (*sgemm)(void*, int, int, int, int, int, const float*, const float*, int, const float*, int, const float*,
+               float*, int) = nullptr;
+  int (*sgemv)(void*, int, int, int, const float*, const float*, int, const float*, int, const float*, float*,
+               int) = nullptr;
+};
+
+Blas& blas(cudaStream_t st) {
+  static Blas b = [] {
+    Blas x;
+    for (const char* name : {"libcublas.so.12", "libcublas.so"}) {
+      x.lib = dlopen(name, RTLD_NOW | RTLD_GLOBAL);
+      if (x.lib) break;
+    }
+    if (!x.lib) return x;
+    x.create = reinterpret_cast<decltype(x.create)>(dlsym(x.lib, "cublasCreate_v2"));
+    x.set_stream = reinterpret_cast<decltype(x.set_stream)>(dlsym(x.lib, "cublasSetStream_v2"));
+    x.sgemm = reinterpret_cast<decltype(x.sgemm)>(dlsym(x.lib, "cublasSgemm_v2"));
+    x.sgemv = reinterpret_cast<decltype(x.sgemv)>(dlsym(x.lib, "cublasSgemv_v2"));
+    if (x.create && x.create(&x.handle) != 0) x.handle = nullptr;
+    return x;
+  }();
+  if (!b.handle || !b.sgemm || !b.sgemv || !b.set_stream)
+    raise(MARL_ERR_CUDA, "cuBLAS (libcublas.so.12) is not loadable in this process");
+  b.set_stream(b.handle, st);
+  return b;
+}
+constexpr int kOpN = 0, kOpT = 1;
+
+// Row-major GEMMs on column-major cuBLAS.
+// C[M x N] = A[M x K] . B[N x K]^T (+ beta C)
+void gemm_nt(cudaStream_t st, int64_t M, int N, int K, const float* A, int lda, const float* B, int ldb, float* C,
+             int ldc, float beta) {
+  const float one = 1.0f;
+  if (blas(st).sgemm(blas(st).handle, kOpT, kOpN, N, int(M), K, &one, B, ldb, A, lda, &beta, C, ldc) != 0)
+    raise(MARL_ERR_CUDA, "cublasSgemm failed");
+}
+// C[M x N] = A[M x K] . B[K x N] (+ beta C)
+void gemm_nn(cudaStream_t st, int64_t M, int N, int K, const float* A, int lda, const float* B, int ldb, float* C,
+             int ldc, float beta) {
+  const float one = 1.0f;
+  if (blas(st).sgemm(blas(st).handle, kOpN, kOpN, N, int(M), K, &one, B, ldb, A, lda, &beta, C, ldc) != 0)
+    raise(MARL_ERR_CUDA, "cublasSgemm failed");
+}
+// G[O x I] = D[K x O]^T . X[K x I] (+ beta G): matmul_tn summed over all rows
+void gemm_tn(cudaStream_t st, int O, int I, int64_t K, const float* D, int ldd, const float* X, int ldx, float* G,
+             float beta) {
+  const float one = 1.0f;
+  if (blas(st).sgemm(blas(st).handle, kOpN, kOpT, I, O, int(K), &one, X, ldx, D, ldd, &beta, G, I) != 0)
+    raise(MARL_ERR_CUDA, "cublasSgemm failed");
+}
+// g[O] = sum_k D[k][o] (+ beta g): the bias gradients
+void colsum(cudaStream_t st, int O, int64_t K, const float* D, int ldd, const float* ones, float* g, float beta) {
+  const float one = 1.0f;
+  if (blas(st).sgemv(blas(st).handle, kOpN, O, int(K), &one, D, ldd, ones, 1, &beta, g, 1) != 0)
+    raise(MARL_ERR_CUDA, "cublasSgemv failed");
 }
 
 // the native hook: an in-place NCCL sum on the trainer's stream (no host sync)
@@ -1843,6 +1960,129 @@ void minibatch_grad(marl_ppo* p, const int32_t* idx, int64_t M, bool global = fa
   }
 }
 
+// rnn_seq_forward with cache (actor_critic.hpp:130-158) of one branch over
+// the Mc rows of a chunk: per step, the gather / reset kernel, SGEMMs for
+// embed, the GRU's input and hidden paths ([Wz;Wr;Wn] and [Uz;Ur;Un] as one
+// GEMM each), post and head, with the gate arithmetic in one kernel.
+void rnn_chunk_forward(marl_ppo* p, int branch, const int32_t* rows, int64_t Mc) {
+  marl_rollout* r = p->ro;
+  cudaStream_t st = p->h->stream;
+  const RnnCache& c = branch == 0 ? p->rca : p->rcc;
+  const int in = branch == 0 ? r->in_dim : r->critic_in, out = branch == 0 ? r->n_act : 1, F = r->F, H = r->H;
+  const RnnWPtrs w = rnn_weights(branch == 0 ? r->params : r->params + r->n_actor, in, F, H, out);
+  RnnStepArgs a{};
+  a.M = Mc;
+  a.R = r->R;
+  a.in = in;
+  a.H = H;
+  a.rows = rows;
+  a.resets = r->b.resets;
+  a.src = (branch == 1 && r->centralized) ? r->b.critic_in : r->b.obs;
+  a.h0 = branch == 0 ? r->h0_actor : r->h0_critic;
+  a.h = p->rnn_h;
+  a.w.bzx = w.bias6;
+  a.w.brx = w.bias6 + H;
+  a.w.bnx = w.bias6 + 2 * H;
+  a.w.bzh = w.bias6 + 3 * H;
+  a.w.brh = w.bias6 + 4 * H;
+  a.w.bnh = w.bias6 + 5 * H;
+  for (int t = 0; t < r->T; ++t) {
+    const size_t k0 = size_t(t) * size_t(Mc);
+    a.t = t;
+    a.x = c.x + k0 * in;
+    a.hprev = c.h + k0 * H;
+    a.z = c.z + k0 * H;
+    a.r = c.r + k0 * H;
+    a.c = c.c + k0 * H;
+    a.ah = c.ah + k0 * H;
+    a.hn = c.hn + k0 * H;
+    rnn_step_gather(a, st);
+    float* e = c.e + k0 * F;
+    gemm_nt(st, Mc, F, in, a.x, in, w.we, in, e, F, 0.0f);
+    rnn_bias_act(e, Mc, F, w.be, true, r->relu, st);
+    gemm_nt(st, Mc, 3 * H, F, e, F, w.wx, F, p->rnn_gx, 3 * H, 0.0f);
+    gemm_nt(st, Mc, 3 * H, H, a.hprev, H, w.uh, H, p->rnn_gh, 3 * H, 0.0f);
+    rnn_gates(a, p->rnn_gx, p->rnn_gh, st);
+    float* pp = c.p + k0 * F;
+    gemm_nt(st, Mc, F, H, a.hn, H, w.wp, H, pp, F, 0.0f);
+    rnn_bias_act(pp, Mc, F, w.bp, true, r->relu, st);
+    float* y = c.y + k0 * out;
+    gemm_nt(st, Mc, out, F, pp, F, w.wh, F, y, out, 0.0f);
+    rnn_bias_act(y, Mc, out, w.bh, false, r->relu, st);
+  }
+  after_launch();
+}
+
+// rnn_seq_backward (actor_critic.hpp:164-196) of one branch over a chunk, then
+// its weight gradients (matmul_tn over every (t, row)) into G in pack order.
+void rnn_chunk_backward(marl_ppo* p, int branch, const int32_t* rows, int64_t Mc, float* G, bool accumulate) {
+  marl_rollout* r = p->ro;
+  cudaStream_t st = p->h->stream;
+  const RnnCache& c = branch == 0 ? p->rca : p->rcc;
+  const int in = branch == 0 ? r->in_dim : r->critic_in, out = branch == 0 ? r->n_act : 1, F = r->F, H = r->H;
+  const RnnWPtrs w = rnn_weights(branch == 0 ? r->params : r->params + r->n_actor, in, F, H, out);
+  const int T = r->T;
+  const int64_t Kc = int64_t(T) * Mc;
+  RnnStepArgs a{};
+  a.M = Mc;
+  a.R = r->R;
+  a.in = in;
+  a.H = H;
+  a.rows = rows;
+  a.resets = r->b.resets;
+  float* dh = p->rnn_dh;
+  float* d4 = c.daz;  // [Kc][4H] = daz | dar | dac | dah
+  for (int t = T - 1; t >= 0; --t) {
+    const size_t k0 = size_t(t) * size_t(Mc);
+    a.t = t;
+    a.hprev = c.h + k0 * H;
+    a.z = c.z + k0 * H;
+    a.r = c.r + k0 * H;
+    a.c = c.c + k0 * H;
+    a.ah = c.ah + k0 * H;
+    // head and post: dzp = (dy . Wh) * act'(p); dh_step = dzp . Wp + dh
+    float* dzp = c.dzp + k0 * F;
+    gemm_nn(st, Mc, F, out, c.dy + k0 * out, out, w.wh, F, dzp, F, 0.0f);
+    rnn_act_grad(dzp, c.p + k0 * F, Mc * F, r->relu, st);
+    gemm_nn(st, Mc, H, F, dzp, F, w.wp, H, dh, H, t == T - 1 ? 0.0f : 1.0f);
+    // gru_backward: gates, carry dh = g*z, then dx and the gate paths of dh
+    float* d4t = d4 + k0 * 4 * H;
+    rnn_gru_bwd(a, dh, d4t, dh, st);
+    float* dze = c.dze + k0 * F;
+    gemm_nn(st, Mc, F, 3 * H, d4t, 4 * H, w.wx, F, dze, F, 0.0f);
+    rnn_act_grad(dze, c.e + k0 * F, Mc * F, r->relu, st);
+    gemm_nn(st, Mc, H, 2 * H, d4t, 4 * H, w.uh, H, dh, H, 1.0f);
+    gemm_nn(st, Mc, H, H, d4t + 3 * H, 4 * H, w.uh + 2 * H * H, H, dh, H, 1.0f);
+    rnn_cut(a, dh, st);
+  }
+  const float beta = accumulate ? 1.0f : 0.0f;
+  const float* ones = p->rnn_ones;
+  gemm_tn(st, F, in, Kc, c.dze, F, c.x, in, G, beta);  // embed
+  G += size_t(F) * in;
+  colsum(st, F, Kc, c.dze, F, ones, G, beta);
+  G += F;
+  gemm_tn(st, 3 * H, F, Kc, d4, 4 * H, c.e, F, G, beta);  // wz, wr, wn
+  G += size_t(3) * H * F;
+  gemm_tn(st, 2 * H, H, Kc, d4, 4 * H, c.h, H, G, beta);  // uz, ur
+  G += size_t(2) * H * H;
+  gemm_tn(st, H, H, Kc, d4 + 3 * H, 4 * H, c.h, H, G, beta);  // un
+  G += size_t(H) * H;
+  colsum(st, 3 * H, Kc, d4, 4 * H, ones, G, beta);  // bzx, brx, bnx
+  G += 3 * H;
+  colsum(st, 2 * H, Kc, d4, 4 * H, ones, G, beta);  // bzh, brh
+  G += 2 * H;
+  colsum(st, H, Kc, d4 + 3 * H, 4 * H, ones, G, beta);  // bnh
+  G += H;
+  gemm_tn(st, F, H, Kc, c.dzp, F, c.hn, H, G, beta);  // post
+  G += size_t(F) * H;
+  colsum(st, F, Kc, c.dzp, F, ones, G, beta);
+  G += F;
+  gemm_tn(st, out, F, Kc, c.dy, out, c.p, F, G, beta);  // head
+  G += size_t(out) * F;
+  colsum(st, out, Kc, c.dy, out, ones, G, beta);
+  after_launch();
+}
+
 // rnn_minibatch's gradient (ppo.cpp:444-509): rnn_seq_forward with cache over
 // the rows' whole sequences, ppo_row_loss over the [t][i] rows, rnn_seq_backward,
 // and the weight gradients summed over every (t, row) in nn::pack order.
@@ -1851,62 +2091,37 @@ void minibatch_grad_rnn(marl_ppo* p, const int32_t* rows, int64_t M) {
   cudaStream_t st = p->h->stream;
   const int T = r->T;
   const int64_t K = int64_t(T) * M;
+  // advantage statistics over the whole minibatch's [t][i] rows
   rnn_flat_slots(rows, M, T, r->R, p->rnn_flat, st);
   ppo_adv_stats(r->b, p->rnn_flat, K, p->adv_part, p->adv_part2, p->adv_g, p->mbst, st, {});
-  RnnSeqArgs a{};
-  a.actor = r->params;
-  a.critic = r->params + r->n_actor;
-  a.h0_actor = r->h0_actor;
-  a.h0_critic = r->h0_critic;
-  a.rows = rows;
-  a.M = M;
-  a.T = T;
-  a.R = r->R;
-  a.in_dim = r->in_dim;
-  a.critic_in = r->critic_in;
-  a.n_act = r->n_act;
-  a.F = r->F;
-  a.H = r->H;
-  a.relu = r->relu;
-  a.obs = r->b.obs;
-  a.critic_rows = r->centralized ? r->b.critic_in : nullptr;
-  a.resets = r->b.resets;
-  a.ca = p->rca;
-  a.cc = p->rcc;
-  rnn_forward(a, true, st);
-  rnn_forward(a, false, st);
-  rnn_loss(a, p->rnn_flat, K, r->b, p->mbst, p->cfg.clip_eps, p->cfg.ent_coef, p->cfg.vf_coef, p->spart_a,
-           p->spart_c, p->flags + 1, st);
-  rnn_backward(a, true, st);
-  rnn_backward(a, false, st);
-  float* G = p->grad;
-  for (int branch = 0; branch < 2; ++branch) {
-    const RnnCache& c = branch == 0 ? p->rca : p->rcc;
-    const int in = branch == 0 ? r->in_dim : r->critic_in, out = branch == 0 ? r->n_act : 1, F = r->F, H = r->H;
-    auto mat = [&](const float* D, int ldd, const float* X, int ldx, int O, int I) {
-      rnn_outer_sum(D, ldd, X, ldx, K, O, I, G, st);
-      G += size_t(O) * size_t(X ? I : 1);
-    };
-    mat(c.dze, F, c.x, in, F, in);  // embed w, b
-    mat(c.dze, F, nullptr, 0, F, 1);
-    mat(c.daz, H, c.e, F, H, F);    // gru wz, wr, wn
-    mat(c.dar, H, c.e, F, H, F);
-    mat(c.dac, H, c.e, F, H, F);
-    mat(c.daz, H, c.h, H, H, H);    // uz, ur, un
-    mat(c.dar, H, c.h, H, H, H);
-    mat(c.dah, H, c.h, H, H, H);
-    mat(c.daz, H, nullptr, 0, H, 1);  // bzx, brx, bnx, bzh, brh, bnh
-    mat(c.dar, H, nullptr, 0, H, 1);
-    mat(c.dac, H, nullptr, 0, H, 1);
-    mat(c.daz, H, nullptr, 0, H, 1);
-    mat(c.dar, H, nullptr, 0, H, 1);
-    mat(c.dah, H, nullptr, 0, H, 1);
-    mat(c.dzp, F, c.hn, H, F, H);   // post w, b
-    mat(c.dzp, F, nullptr, 0, F, 1);
-    mat(c.dy, out, c.p, F, out, F);  // head w, b
-    mat(c.dy, out, nullptr, 0, out, 1);
+  // then the rows in chunks whose BPTT caches fit the budget; gradients and
+  // per-block loss sums accumulate over the chunks
+  const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(M, p->rnn_chunk));
+  int blocks_done = 0;
+  for (int64_t c0 = 0; c0 < M; c0 += chunk) {
+    const int64_t Mc = std::min<int64_t>(chunk, M - c0), Kc = int64_t(T) * Mc;
+    int32_t* flat_c = p->rnn_flat + K;  // the chunk's own [t][i] slots
+    rnn_flat_slots(rows + c0, Mc, T, r->R, flat_c, st);
+    // rnn_seq_forward with cache, both branches
+    for (int branch = 0; branch < 2; ++branch) rnn_chunk_forward(p, branch, rows + c0, Mc);
+    RnnSeqArgs la{};  // the loss reads the cached head outputs of both branches
+    la.M = Mc;
+    la.T = T;
+    la.n_act = r->n_act;
+    la.ca = p->rca;
+    la.cc = p->rcc;
+    rnn_loss(la, flat_c, Kc, r->b, p->mbst, p->cfg.clip_eps, p->cfg.ent_coef, p->cfg.vf_coef,
+             p->spart_a + size_t(blocks_done) * 6, p->spart_c + size_t(blocks_done) * 6, p->flags + 1, st);
+    blocks_done += rnn_loss_blocks(Kc);
+    // rnn_seq_backward + the weight gradients, accumulated over the chunks
+    float* G = p->grad;
+    for (int branch = 0; branch < 2; ++branch) {
+      rnn_chunk_backward(p, branch, rows + c0, Mc, G, c0 > 0);
+      G += branch == 0 ? r->n_actor : 0;
+    }
+    after_launch();
   }
-  after_launch();
+  p->rnn_blocks = blocks_done;
 }
 
 // clip_global_norm + adam_update for one minibatch (ppo.cpp:605-608).
@@ -1921,8 +2136,8 @@ void minibatch_apply(marl_ppo* p, double lr_u, double* metrics_slot) {
   a.P = p->P;
   a.actor_stats = p->spart_a;
   a.critic_stats = p->spart_c;
-  a.n_actor_parts = p->hook ? 1 : p->grid_a;  // folded + all-reduced into row 0
-  a.n_critic_parts = p->hook ? 1 : p->grid_c;
+  a.n_actor_parts = p->hook ? 1 : (p->recurrent ? p->rnn_blocks : p->grid_a);  // folded + all-reduced into row 0
+  a.n_critic_parts = p->hook ? 1 : (p->recurrent ? p->rnn_blocks : p->grid_c);
   a.st = p->mbst;
   a.vf_coef = p->cfg.vf_coef;
   a.ent_coef = p->cfg.ent_coef;
@@ -2073,17 +2288,21 @@ int marl_ppo_create(marl_venv* h, const char* ppo_config_json, int centralized, 
     // (MARL_PPO_UPDATE_FP32=1 forces the fp32 CUDA-core path)
     p->tc = precision == 1 && !centralized && ppo_tc_supported(r->in_dim, r->critic_in, r->width, r->n_act) &&
             !std::getenv("MARL_PPO_UPDATE_FP32");
-    int64_t rnn_K = 0;
+    int64_t rnn_K = 0, rnn_Kc = 0;
     if (p->recurrent) {
+      // BPTT caches for a chunk of rows: at most a quarter of the free HBM (or MARL_RNN_CACHE_MB)
       rnn_K = int64_t(c.n_rollout_steps) * p->per;
-      const size_t floats = size_t(rnn_K) * (rnn_cache_floats(r->in_dim, r->F, r->H, r->n_act) +
-                                             rnn_cache_floats(r->critic_in, r->F, r->H, 1));
+      const size_t per_row = size_t(c.n_rollout_steps) * 4 *
+                             (rnn_cache_floats(r->in_dim, r->F, r->H, r->n_act) +
+                              rnn_cache_floats(r->critic_in, r->F, r->H, 1));
       size_t free_b = 0, total_b = 0;
       cuda_check(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
-      if (floats * 4 > free_b / 2)
-        raise(MARL_ERR_SCHEMA, "ppo: the recurrent update's BPTT caches (" + std::to_string(floats * 4 >> 20) +
-                                   " MiB) exceed half the free device memory; use more n_minibatches or fewer envs");
-      p->grid_a = p->grid_c = rnn_loss_blocks(rnn_K);
+      size_t budget = free_b / 4;
+      if (const char* mb = std::getenv("MARL_RNN_CACHE_MB")) budget = size_t(std::atoll(mb)) << 20;
+      p->rnn_chunk = std::max<int64_t>(1, std::min<int64_t>(p->per, int64_t(budget / per_row)));
+      rnn_Kc = int64_t(c.n_rollout_steps) * p->rnn_chunk;
+      int64_t nchunks = (p->per + p->rnn_chunk - 1) / p->rnn_chunk;
+      p->grid_a = p->grid_c = int(std::min<int64_t>(int64_t(1) << 30, rnn_loss_blocks(rnn_Kc) * nchunks));
     } else if (p->tc) {
       p->grid_a = p->grid_c = ppo_tc_grid(p->per);
     } else {
@@ -2097,26 +2316,34 @@ int marl_ppo_create(marl_venv* h, const char* ppo_config_json, int centralized, 
     ar.add(&p->v, size_t(p->P));
     ar.add(&p->grad, size_t(p->P));
     ar.add(&p->snapshot, size_t(p->P));
-    ar.add(&p->gpart_a, size_t(p->grid_a) * size_t(p->Pa));
-    ar.add(&p->gpart_c, size_t(p->grid_c) * size_t(p->Pc));
+    // per-CTA gradient partials of the feed-forward kernels (the recurrent path
+    // accumulates straight into the gradient)
+    ar.add(&p->gpart_a, p->recurrent ? 1 : size_t(p->grid_a) * size_t(p->Pa));
+    ar.add(&p->gpart_c, p->recurrent ? 1 : size_t(p->grid_c) * size_t(p->Pc));
     ar.add(&p->spart_a, size_t(p->grid_a) * 6);
     ar.add(&p->spart_c, size_t(p->grid_c) * 6);
     ar.add(&p->adv_part, size_t(std::max(nb, ppo_stat_blocks(rnn_K))) * 2);
     ar.add(&p->adv_part2, size_t(std::max(nb, ppo_stat_blocks(rnn_K))));
     if (p->recurrent) {
-      ar.add(&p->rnn_flat, size_t(rnn_K));
+      ar.add(&p->rnn_flat, size_t(rnn_K + rnn_Kc));  // the minibatch's slots, then one chunk's
       const int F = r->F, H = r->H;
       for (int br = 0; br < 2; ++br) {
         RnnCache& cc = br == 0 ? p->rca : p->rcc;
         const int in = br == 0 ? r->in_dim : r->critic_in, out = br == 0 ? r->n_act : 1;
-        const size_t K = size_t(rnn_K);
+        const size_t K = size_t(rnn_Kc);
         ar.add(&cc.x, K * in);
         ar.add(&cc.y, K * out);
         ar.add(&cc.dy, K * out);
         for (float** q : {&cc.e, &cc.p, &cc.dzp, &cc.dze}) ar.add(q, K * F);
-        for (float** q : {&cc.h, &cc.z, &cc.r, &cc.c, &cc.ah, &cc.hn, &cc.daz, &cc.dar, &cc.dac, &cc.dah})
-          ar.add(q, K * H);
+        for (float** q : {&cc.h, &cc.z, &cc.r, &cc.c, &cc.ah, &cc.hn}) ar.add(q, K * H);
+        ar.add(&cc.daz, K * 4 * H);  // [K][4H]: daz | dar | dac | dah
       }
+      const size_t Mc = size_t(p->rnn_chunk);
+      ar.add(&p->rnn_h, Mc * H);
+      ar.add(&p->rnn_dh, Mc * H);
+      ar.add(&p->rnn_gx, Mc * 3 * H);
+      ar.add(&p->rnn_gh, Mc * 3 * H);
+      ar.add(&p->rnn_ones, size_t(rnn_Kc));
     }
     ar.add(&p->metrics, size_t(c.update_epochs) * size_t(c.n_minibatches) * 8);
     ar.add(&p->mbst, 1);
@@ -2133,6 +2360,10 @@ int marl_ppo_create(marl_venv* h, const char* ppo_config_json, int centralized, 
       ar.add(&p->cmp_scratch, p->cmp_scratch_bytes);
     }
     ar.commit();
+    if (p->recurrent) {
+      std::vector<float> ones(size_t(rnn_Kc), 1.0f);
+      cuda_check(cudaMemcpy(p->rnn_ones, ones.data(), ones.size() * 4, cudaMemcpyHostToDevice), "cudaMemcpy");
+    }
     *out = p.release();
   });
 }

@@ -96,3 +96,26 @@ def test_recurrent_schema_errors():
         PpoTrainer(v, {"n_envs": 5, "recurrent": True})
     with pytest.raises(SchemaError, match="fp32"):
         PpoTrainer(v, {"n_envs": 5, "recurrent": True, "n_minibatches": 3}, precision="bf16")
+
+
+@pytest.mark.gpu
+def test_recurrent_chunked_bptt_matches_reference(monkeypatch):
+    """Minibatches processed in row chunks whose BPTT caches fit a budget
+    (here a zero budget: one row per chunk) give the same training as the reference."""
+    _need_ref()
+    monkeypatch.setenv("MARL_RNN_CACHE_MB", "0")
+    ppo_cfg = {"total_timesteps": 2 * 8 * 16, "n_envs": 8, "n_rollout_steps": 16, "recurrent": True,
+               "hidden_width": 32, "fc_width": 32, "update_epochs": 2}
+    _compare("MPE_simple_spread_v3", {}, ppo_cfg, O.key_from_seed(7))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("env_id,cfg", [("MPE_simple_spread_v3", {}), ("SMAX_5m_vs_6m", THREE_M)])
+def test_recurrent_gemm_collector_matches_reference(monkeypatch, env_id, cfg):
+    """The GEMM-structured acting step (used for large row counts) forced on a
+    small batch: the same training as the reference."""
+    _need_ref()
+    monkeypatch.setenv("MARL_RNN_COLLECT", "gemm")
+    ppo_cfg = {"total_timesteps": 2 * 8 * 16, "n_envs": 8, "n_rollout_steps": 16, "recurrent": True,
+               "hidden_width": 32, "fc_width": 32, "update_epochs": 2}
+    _compare(env_id, cfg, ppo_cfg, O.key_from_seed(7))
