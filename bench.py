@@ -40,6 +40,8 @@ WORKLOADS = {
     # one "step" is one train_ippo update (collect + update_epochs x n_minibatches)
     "ppo": ("MPE_simple_spread_v3", {}, 1 << 16, "IPPO training update on MPE simple_spread (collect 128 steps + "
             "5 epochs x 2 minibatches of PPO), PpoConfig defaults"),
+    "ppo_rnn": ("MPE_simple_spread_v3", {}, 1 << 14, "recurrent (GRU 128) IPPO training update on MPE simple_spread "
+                "(collect 128 steps + 5 epochs x 2 minibatches, BPTT), PpoConfig defaults + recurrent"),
 }
 IPPO_T = 128
 L2_FLUSH_BYTES = 512 << 20  # > 4x the 126 MB L2; its ~80 us also covers the host's enqueue of the next step
@@ -345,11 +347,14 @@ def run_gpu_ppo(args, rank, world, local_rank):
     # weak scaling: n_envs per GPU fixed; N > 1 is data-parallel training over env shards with the
     # update's sums all-reduced over NCCL (identical parameters on every rank)
     gn = n_envs * world
+    recurrent = args.workload == "ppo_rnn"
     pc = {"n_envs": gn, "n_rollout_steps": T, "total_timesteps": (args.warmup + args.steps + 8) * gn * T}
+    if recurrent:
+        pc["recurrent"] = True
     from paper_2311_10090_b200 import dist as shard_mod
     venv = shard_mod.make_sharded(env, gn, rank, world, device=local_rank) if world > 1 else \
         m.VectorEnv(env, n_envs, device=local_rank)
-    tr = PpoTrainer(venv, pc, False, "bf16")
+    tr = PpoTrainer(venv, pc, False, "fp32" if recurrent else "bf16")
     if world > 1:
         import torch.distributed as tdist
         from paper_2311_10090_b200.ppo import nccl_unique_id
@@ -385,6 +390,11 @@ def run_gpu_ppo(args, rank, world, local_rank):
     value = world * n_envs * A * T * args.steps / (total_ms * 1e-3)
     sp = tr.spec
     fpr = ppo_flop_per_row(sp.in_dim, sp.critic_in, sp.width, sp.n_actions)
+    if recurrent:  # RnnBranch MACs (fc 64, GRU 128) x (forward + 2 x backward) x 2 FLOP
+        F, Hh = 64, 128
+        macs = sum(F * i + 3 * Hh * F + 3 * Hh * Hh + F * Hh + o * F for i, o in ((sp.in_dim, sp.n_actions),
+                                                                              (sp.critic_in, 1)))
+        fpr = 6 * macs
     R = n_envs * A
     upd_s = float(np.mean(upd_ms)) * 1e-3
     tflops = T * R * 5 * fpr / upd_s / 1e12  # algorithmic FLOPs (unpadded) per second of update
@@ -402,8 +412,10 @@ def run_gpu_ppo(args, rank, world, local_rank):
         sys.path.insert(0, os.path.join(ROOT, "oracle"))
         import oracle as O
         if O.ref_available():
-            n_cpu, t_cpu = 64, 32
+            n_cpu, t_cpu = (64, 32) if not recurrent else (16, 32)
             rc = {"n_envs": n_cpu, "n_rollout_steps": t_cpu, "total_timesteps": n_cpu * t_cpu}
+            if recurrent:
+                rc["recurrent"] = True
             t0 = time.perf_counter()
             O.ref_train(env_id, cfg, rc, O.key_from_seed(0))
             csec = time.perf_counter() - t0
@@ -420,7 +432,8 @@ def run_gpu_ppo(args, rank, world, local_rank):
         "metric": "agent-steps/sec (env-steps/sec x agents)", "value": value, "unit": "agent-steps/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "bf16 rollout policy + bf16 tcgen05 PPO update (fp32 accumulate) / f64 env", "data": "synthetic (key_from_seed(rank))",
+        "dtype": ("f32 recurrent policy + f32 BPTT update (cuBLAS SGEMM steps)" if recurrent else
+                  "bf16 rollout policy + bf16 tcgen05 PPO update (fp32 accumulate)") + " / f64 env", "data": "synthetic (key_from_seed(rank))",
         "config": {"workload": label, "env_id": env_id, "n_envs_per_gpu": n_envs, "agents": A,
                    "rollout_steps": T, "update_epochs": 5, "n_minibatches": 2, "batch_rows": T * R,
                    "step": "one PPO update = collect + update",
@@ -431,8 +444,9 @@ def run_gpu_ppo(args, rank, world, local_rank):
         "update_row_passes_per_sec": T * R * 5 / upd_s,
         "roofline": {"bound": "tensor", "achieved": tflops, "peak": peak, "unit": "TFLOP/s", "frac": tflops / peak,
                      "traffic": None, "peak_source": "MEASURED_PEAKS.json bf16_tflops (dense)",
-                     "kernel": "PPO update phase (ppo_update_tc_kernel dominant: bf16 tcgen05 forward, input- "
-                               "and weight-gradient GEMMs, fp32 TMEM accumulation)",
+                     "kernel": ("recurrent PPO update (fp32 cuBLAS SGEMM per time step + gate kernels)" if recurrent
+                                else "PPO update phase (ppo_update_tc_kernel dominant: bf16 tcgen05 forward, input- "
+                                     "and weight-gradient GEMMs, fp32 TMEM accumulation)"),
                      "flop_per_row_pass": fpr},
         "cpu_baseline": cpu,
         "e2e": {"value": world * n_envs * A * T * e2e_steps / sec, "unit": "agent-steps/s", "h2d_bytes_per_step": 0,
@@ -460,12 +474,14 @@ def run_reference_arm(args, rank, world):
         return
     threads = os.cpu_count() or 1
     n_envs = n_per_gpu * world
-    if args.workload == "ppo":  # one step = one train_ippo update of a bounded sample
+    if args.workload in ("ppo", "ppo_rnn"):  # one step = one train_ippo update of a bounded sample
         sys.path.insert(0, os.path.join(ROOT, "oracle"))
         import oracle as O
-        n_cpu, t_cpu = 64, 32
+        n_cpu, t_cpu = (64, 32) if args.workload == "ppo" else (16, 32)
         steps = max(1, args.steps)
         rc = {"n_envs": n_cpu, "n_rollout_steps": t_cpu, "total_timesteps": n_cpu * t_cpu * steps}
+        if args.workload == "ppo_rnn":
+            rc["recurrent"] = True
         t0 = time.perf_counter()
         O.ref_train(env_id, cfg, rc, O.key_from_seed(0))
         sec = time.perf_counter() - t0
@@ -666,7 +682,7 @@ def main():
     try:
         if args.workload == "ippo":
             run_gpu_ippo(args, rank, world, local_rank)
-        elif args.workload == "ppo":
+        elif args.workload in ("ppo", "ppo_rnn"):
             run_gpu_ppo(args, rank, world, local_rank)
         else:
             run_gpu_arm(args, rank, world, local_rank)

@@ -9,8 +9,10 @@ for w in smax3m mpe mpe_large overcooked smax2s3z smax27m ippo; do
   timeout 600 python bench.py --workload $w --steps 30 --warmup 5 2>/dev/null | grep '^{' >> gpurun_out/bench_${TAG}.jsonl
 done
 timeout 600 python bench.py --workload ppo --steps 10 --warmup 3 2>/dev/null | grep '^{' >> gpurun_out/bench_${TAG}.jsonl
+timeout 600 python bench.py --workload ppo_rnn --steps 3 --warmup 3 2>/dev/null | grep '^{' >> gpurun_out/bench_${TAG}.jsonl
 timeout 300 python bench.py --impl reference --workload smax3m --steps 3 --warmup 1 2>/dev/null | grep '^{' >> gpurun_out/bench_${TAG}.jsonl
 timeout 300 python bench.py --impl reference --workload ppo --steps 2 --warmup 3 2>/dev/null | grep '^{' >> gpurun_out/bench_${TAG}.jsonl
+timeout 300 python bench.py --impl reference --workload ppo_rnn --steps 1 --warmup 3 2>/dev/null | grep '^{' >> gpurun_out/bench_${TAG}.jsonl
 wc -l gpurun_out/bench_${TAG}.jsonl
 NCU=/usr/local/cuda/bin/ncu
 for w in smax3m mpe_large overcooked smax27m; do
