@@ -194,4 +194,38 @@ class VectorEnv {
   std::vector<int32_t> obs_size_, n_actions_;
 };
 
+// rollout(venv, policy, n_steps, key) (vector_env.hpp:91-92, vector_env.cpp:131-165)
+// over the adapter: the same loop, checks and TrajectoryBatch as the reference's.
+inline marl::TrajectoryBatch rollout(const VectorEnv& venv, const marl::Policy& policy, int n_steps,
+                                     const marl::PrngKey& key) {
+  if (n_steps < 1) throw marl::ContractError("rollout: n_steps must be >= 1");
+  marl::TrajectoryBatch traj;
+  traj.n_steps = n_steps;
+  traj.n_envs = venv.n_envs();
+  traj.obs.reserve(size_t(n_steps));
+  auto [obs, state] = venv.reset(key);
+  for (int t = 0; t < n_steps; ++t) {
+    marl::PolicyOutput pi = policy(obs);
+    if (pi.actions.size() != size_t(venv.n_envs()))
+      throw marl::ContractError("rollout: policy returned " + std::to_string(pi.actions.size()) +
+                                " action maps for " + std::to_string(venv.n_envs()) + " envs");
+    if (!pi.log_probs.empty() && pi.log_probs.size() != size_t(venv.n_envs()))
+      throw marl::ContractError("rollout: policy log_probs batch size mismatch");
+    if (!pi.values.empty() && pi.values.size() != size_t(venv.n_envs()))
+      throw marl::ContractError("rollout: policy values batch size mismatch");
+    marl::StepBatchResult r = venv.step(state, pi.actions);
+    traj.obs.push_back(std::move(obs));
+    traj.actions.push_back(std::move(pi.actions));
+    traj.rewards.push_back(std::move(r.rewards));
+    traj.dones.push_back(std::move(r.dones));
+    traj.log_probs.push_back(std::move(pi.log_probs));
+    traj.values.push_back(std::move(pi.values));
+    obs = std::move(r.obs);
+    state = std::move(r.next);
+  }
+  traj.final_obs = std::move(obs);
+  traj.final_state = std::move(state);
+  return traj;
+}
+
 }  // namespace marl_b200

@@ -50,6 +50,34 @@ int main(int argc, char** argv) {
       s1 = r1.next;
       s2 = r2.next;
     }
+    // rollout(venv, policy, T, key) (vector_env.cpp:131-165): the adapter's vs the reference's
+    // free function, with a policy that reads the observations (stop is always legal in SMAX)
+    marl::Policy policy = [&](const std::vector<marl::AgentMap<marl::Obs>>& obs) {
+      marl::PolicyOutput out;
+      for (const auto& m : obs) {
+        marl::AgentMap<marl::Action> a;
+        marl::AgentMap<double> lp, v;
+        for (size_t q = 0; q < m.size(); ++q) {
+          const std::string& agent = m.key(q);
+          const marl::Obs& o = m.value(q);
+          a.emplace(agent, 4);
+          lp.emplace(agent, double(o[0]) - double(o[1]));
+          v.emplace(agent, double(o[2]) + 0.5 * double(o[3]));
+        }
+        out.actions.push_back(std::move(a));
+        out.log_probs.push_back(std::move(lp));
+        out.values.push_back(std::move(v));
+      }
+      return out;
+    };
+    auto t1 = marl_b200::rollout(venv, policy, 30, marl::prng::key_from_seed(11));
+    auto t2 = marl::rollout(ref, policy, 30, marl::prng::key_from_seed(11));
+    if (t1.obs != t2.obs || t1.actions != t2.actions || t1.rewards != t2.rewards || t1.dones != t2.dones ||
+        t1.log_probs != t2.log_probs || t1.values != t2.values || t1.final_obs != t2.final_obs ||
+        t1.final_state.keys != t2.final_state.keys || t1.n_steps != t2.n_steps || t1.n_envs != t2.n_envs) {
+      std::puts("ROLLOUT MISMATCH");
+      return 6;
+    }
     std::puts("ADAPTER PARITY OK");
     return 0;
   } catch (const marl::ContractError& e) {

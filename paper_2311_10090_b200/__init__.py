@@ -6,12 +6,12 @@ sm_100a CUDA kernels behind a C-ABI (include/marl_b200.h); this package is
 the Python mirror of the reference's env API on top of it.
 """
 from .errors import ContractError, CudaError, DivergenceError, NotFoundError, SchemaError
-from .venv import (BatchedState, Env, StepBatchResult, ThroughputResult, VectorEnv, make_env,
-                   registered_envs, throughput_probe)
+from .venv import (BatchedState, Env, StepBatchResult, ThroughputResult, TrajectoryBatch, VectorEnv, make_env,
+                   registered_envs, rollout, throughput_probe)
 from . import prng
 
 __all__ = [
     "BatchedState", "ContractError", "CudaError", "DivergenceError", "Env", "NotFoundError",
     "SchemaError", "StepBatchResult", "ThroughputResult", "VectorEnv", "make_env", "prng",
-    "registered_envs", "throughput_probe",
+    "registered_envs", "rollout", "throughput_probe", "TrajectoryBatch",
 ]

@@ -421,3 +421,54 @@ def throughput_probe(env_id: str, n_envs: int, n_steps: int, key, config=None, d
     N.check(N.lib().marl_throughput_probe(env_id.encode(), _cfg(config), int(n_envs), int(n_steps),
                                           _u32p(_key_arr(key)), int(device), C.byref(s), C.byref(cold)))
     return ThroughputResult(env_id, n_envs, n_steps, s.value, n_envs * n_steps / s.value, cold.value)
+
+
+@dataclass
+class TrajectoryBatch:
+    """marl::TrajectoryBatch (vector_env.hpp:45-57) as device tensors indexed
+    [step][env][agent]; log_probs / values are None when the policy gave none."""
+    n_steps: int
+    n_envs: int
+    obs: Any
+    actions: Any
+    rewards: Any
+    dones: Any
+    log_probs: Any
+    values: Any
+    final_obs: Any
+    final_state: BatchedState
+
+
+def rollout(venv: VectorEnv, policy, n_steps: int, key) -> TrajectoryBatch:
+    """rollout(venv, policy, n_steps, key) (vector_env.cpp:131-165): reset with
+    `key`, then n_steps of policy -> VectorEnv::step.  `policy(obs)` takes the
+    [N, A, D] observation tensor and returns (actions [N, A] (or [N, A, dim]
+    for box spaces), log_probs or None, values or None)."""
+    import torch
+    if n_steps < 1:
+        raise ContractError("rollout: n_steps must be >= 1")
+    obs, state = venv.reset(key)
+    N = venv.n_envs()
+    cols = {k: [] for k in ("obs", "actions", "rewards", "dones", "log_probs", "values")}
+    for _ in range(n_steps):
+        actions, log_probs, values = policy(obs)
+        if len(actions) != N:
+            raise ContractError(f"rollout: policy returned {len(actions)} action maps for {N} envs")
+        for name, x in (("log_probs", log_probs), ("values", values)):
+            if x is not None and len(x) != N:
+                raise ContractError(f"rollout: policy {name} batch size mismatch")
+        cols["obs"].append(obs.clone())
+        cols["actions"].append(torch.as_tensor(actions).clone())
+        cols["log_probs"].append(None if log_probs is None else torch.as_tensor(log_probs).clone())
+        cols["values"].append(None if values is None else torch.as_tensor(values).clone())
+        r = venv.step(state, actions)
+        cols["rewards"].append(r.rewards.clone())
+        cols["dones"].append(r.dones.clone())
+        obs, state = r.obs, r.next
+
+    def stack(xs):
+        return None if any(x is None for x in xs) else torch.stack([x.to(xs[0].device) for x in xs])
+
+    return TrajectoryBatch(n_steps, N, stack(cols["obs"]), stack(cols["actions"]), stack(cols["rewards"]),
+                           stack(cols["dones"]), stack(cols["log_probs"]), stack(cols["values"]), obs.clone(),
+                           state)

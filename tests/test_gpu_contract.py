@@ -179,3 +179,33 @@ def test_host_buffer_step_matches_device_views(env_id, cfg, n):
         for f in fields:
             assert np.array_equal(got[f], want[f]), (k, f)
     assert np.array_equal(a.state_hash().cpu().numpy(), b.state_hash().cpu().numpy())
+
+
+def test_generic_rollout_matches_oracle_loop():
+    """rollout(venv, policy, T, key) (vector_env.cpp:131-165) with an
+    observation-dependent policy vs the same loop on the plain-C oracle."""
+    import torch
+    m = _m()
+    n, T = 50, 30
+    env_id, cfg = "SMAX_5m_vs_6m", THREE_M
+    v = m.VectorEnv(env_id, n, config=cfg)
+
+    def policy(obs):  # stop (always legal) + observation-derived log-probs / values
+        acts = torch.full(obs.shape[:2], 4, dtype=torch.int32, device=obs.device)
+        return acts, obs[:, :, 0].double() - obs[:, :, 1].double(), obs[:, :, 2].double()
+
+    tr = m.rollout(v, policy, T, O.key_from_seed(11))
+    assert tr.n_steps == T and tr.n_envs == n and tuple(tr.obs.shape[:2]) == (T, n)
+    o = O.PortVenv(env_id, cfg, n)
+    ob = o.reset(O.key_from_seed(11))
+    for t in range(T):
+        assert np.array_equal(tr.obs[t].cpu().numpy(), ob), t
+        r = o.step(np.full((n, 3), 4, np.int32))
+        assert np.array_equal(tr.rewards[t].cpu().numpy(), r["rewards"]), t
+        assert np.array_equal(tr.dones[t].cpu().numpy(), r["dones"]), t
+        ob = r["obs"]
+    assert np.array_equal(tr.final_obs.cpu().numpy(), ob)
+    assert np.allclose(tr.log_probs.cpu().numpy(), tr.obs[..., 0].double().cpu().numpy() -
+                       tr.obs[..., 1].double().cpu().numpy())
+    with pytest.raises(m.ContractError):
+        m.rollout(v, policy, 0, O.key_from_seed(1))
