@@ -275,6 +275,9 @@ int marl_ppo_init_nets(int in_dim, int critic_in, int n_actions, int fc_width, i
                        float* actor, float* critic);
 int marl_ppo_begin(marl_ppo* p, const uint32_t key[4]);  /* nets fold_in(key,10), collector fold_in(key,11) */
 int marl_ppo_n_updates(const marl_ppo* p, int64_t* out);  /* total_timesteps / (n_envs * n_rollout_steps) */
+/* 1 when the minibatch step runs on tcgen05 (precision bf16, IPPO, width 64,
+ * input <= 191, <= 16 actions), 0 on the fp32 CUDA-core kernels */
+int marl_ppo_tensor_core_update(const marl_ppo* p, int* out);
 int marl_ppo_param_counts(const marl_ppo* p, int32_t* n_actor, int32_t* n_critic);
 /* recurrent=true: RnnBranch nets (embed fc_width, GRU hidden_width, post, head; actor_critic.hpp:74-200)
  * trained by rnn_minibatch (ppo.cpp:444-509), fp32; ppo_init_nets for that spec into host arrays: */

@@ -58,7 +58,7 @@ EXPORTS = [
     "marl_venv_world_state_size", "marl_venv_world_state",
     "marl_rollout_policy_spec", "marl_rollout_create", "marl_rollout_set_params", "marl_rollout_begin",
     "marl_rollout_collect", "marl_rollout_get_views", "marl_rollout_destroy",
-    "marl_ppo_create", "marl_ppo_init_nets", "marl_ppo_begin", "marl_ppo_n_updates", "marl_ppo_set_params",
+    "marl_ppo_create", "marl_ppo_init_nets", "marl_ppo_begin", "marl_ppo_n_updates", "marl_ppo_tensor_core_update", "marl_ppo_set_params",
     "marl_ppo_get_params", "marl_ppo_rollout", "marl_ppo_collect", "marl_ppo_update", "marl_ppo_step",
     "marl_ppo_minibatch_grad", "marl_ppo_destroy", "marl_ppo_permutation", "marl_ppo_set_allreduce",
     "marl_nccl_unique_id", "marl_ppo_set_nccl", "marl_venv_action_dim", "marl_venv_actions_f32",
@@ -128,6 +128,7 @@ def lib() -> C.CDLL:
     L.marl_ppo_init_nets.argtypes = [C.c_int] * 5 + [u32p, f32p, f32p]
     L.marl_ppo_begin.argtypes = [vp, u32p]
     L.marl_ppo_n_updates.argtypes = [vp, i64p]
+    L.marl_ppo_tensor_core_update.argtypes = [vp, C.POINTER(C.c_int)]
     L.marl_ppo_set_params.argtypes = [vp, f32p, f32p]
     L.marl_ppo_get_params.argtypes = [vp, f32p, f32p]
     L.marl_ppo_rollout.argtypes = [vp, C.POINTER(vp)]

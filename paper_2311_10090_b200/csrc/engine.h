@@ -187,7 +187,7 @@ struct PolicyNet {
 // bf16 operand images for the tcgen05 path (K-major, no swizzle, UMMA
 // canonical layout); built once per parameter upload.
 struct PolicyNetBf16 {
-  const uint16_t* a1;   // [128 x 32] : actor W1 rows 0..63, critic W1 rows 64..127, K padded to 32
+  const uint16_t* a1;   // [128 x kx] : actor W1 rows 0..63, critic W1 rows 64..127, K padded to kx = round16(in)
   const uint16_t* a2;   // [64 x 64]  actor W2
   const uint16_t* c2;   // [64 x 64]  critic W2
   const uint16_t* h3;   // [16 x 64]  actor head (rows 0..n_act-1), zero padded
@@ -211,6 +211,7 @@ struct PolicyStep {
 
 void rollout_policy_fp32(const PolicyNet& net, const PolicyStep& s, const RolloutBufs& b, cudaStream_t st);
 bool rollout_policy_bf16_supported(int in_dim, int n_act, int width);
+int rollout_tc_kx(int in_dim);  // K of the tcgen05 policy's layer 1: round16(in_dim), <= 192
 void rollout_policy_bf16(const PolicyNet& net, const PolicyNetBf16& nb, const PolicyStep& s, const RolloutBufs& b,
                          cudaStream_t st);
 void rollout_pack_bf16(const PolicyNet& net, uint16_t* images, float* bias, cudaStream_t st);
@@ -346,22 +347,25 @@ struct PpoApplyArgs {
 };
 
 // The tcgen05 minibatch step (ppo_tc.cu): actor + critic of an IPPO net with
-// input <= 31, width 64, <= 16 actions, bf16 operands, fp32 TMEM accumulators.
+// input <= 191, width 64, <= 16 actions, bf16 operands, fp32 TMEM accumulators.
 struct PpoTcArgs {
   const float *actor, *critic;  // packed fp32 parameters (current)
   float *gpart_a, *gpart_c;     // [grid][Pa], [grid][Pc]
   double *spart_a, *spart_c;    // [grid][6]
   const int32_t* idx;
   int64_t M;
-  const float* obs;
+  const uint16_t* obs_bf;  // [T*R][kx] bf16 rows (ppo_obs_bf16)
   const int32_t* actions;
   const float *old_logp, *adv, *vtarg, *old_value, *active;
   const uint8_t* legal;
   const PpoMbStats* st;
   int* err;
-  int in, n_act, relu;
+  int in, kx, n_act, relu;
   double clip_eps, ent_coef, vf_coef;
 };
+int ppo_tc_kx(int in_dim);  // round16(in + 1): the bf16 row width incl. the bias column
+// the rollout observations as bf16 rows of kx (column kx-1 = 1), once per update
+void ppo_obs_bf16(const float* obs, int64_t rows, int in, int kx, uint16_t* out, cudaStream_t s);
 bool ppo_tc_supported(int in_dim, int critic_in, int width, int n_act);
 int ppo_tc_grid(int64_t M);
 void ppo_update_tc(const PpoTcArgs& a, int grid, cudaStream_t s);

@@ -355,7 +355,7 @@ void minibatch_grad(marl_ppo* p, const int32_t* idx, int64_t M, bool global = fa
     a.spart_c = p->spart_c;
     a.idx = idx;
     a.M = M;
-    a.obs = r->b.obs;
+    a.obs_bf = p->obs_bf;
     a.actions = r->b.actions;
     a.old_logp = r->b.logp;
     a.adv = r->b.adv;
@@ -366,6 +366,7 @@ void minibatch_grad(marl_ppo* p, const int32_t* idx, int64_t M, bool global = fa
     a.st = p->mbst;
     a.err = p->flags + 1;
     a.in = r->in_dim;
+    a.kx = ppo_tc_kx(r->in_dim);
     a.n_act = r->n_act;
     a.relu = r->relu;
     a.clip_eps = p->cfg.clip_eps;
@@ -608,6 +609,14 @@ void ppo_collect_impl(marl_ppo* p) {
   p->collected = true;
 }
 
+// the tcgen05 step gathers bf16 observation rows: convert the window's rows once
+void tc_obs(marl_ppo* p) {
+  if (!p->tc) return;
+  const marl_rollout* r = p->ro;
+  ppo_obs_bf16(r->b.obs, int64_t(r->T) * r->R, r->in_dim, ppo_tc_kx(r->in_dim), p->obs_bf, p->h->stream);
+  after_launch();
+}
+
 void ppo_update_impl(marl_ppo* p, double row[12], int* diverged) {
   marl_rollout* r = p->ro;
   cudaStream_t st = p->h->stream;
@@ -618,6 +627,7 @@ void ppo_update_impl(marl_ppo* p, double row[12], int* diverged) {
   cuda_check(cudaMemcpyAsync(p->snapshot, r->params, size_t(p->P) * 4, cudaMemcpyDeviceToDevice, st), "cudaMemcpy");
   cuda_check(cudaMemsetAsync(p->flags, 0, 2 * sizeof(int), st), "cudaMemset");
   cuda_check(cudaMemsetAsync(p->metrics, 0, size_t(n_mb_total) * 8 * sizeof(double), st), "cudaMemset");
+  tc_obs(p);
   int k = 0;
   for (int epoch = 0; epoch < c.update_epochs; ++epoch) {
     uint32_t pk[4];
@@ -780,6 +790,7 @@ int marl_ppo_create(marl_venv* h, const char* ppo_config_json, int centralized, 
     ar.add(&p->perm_scratch, p->perm_scratch_bytes);
     ar.add(&p->flags, 2);
     ar.add(&p->adv_g, 4);
+    if (p->tc) ar.add(&p->obs_bf, size_t(r->T) * size_t(r->R) * size_t(ppo_tc_kx(r->in_dim)));
     ar.add(&p->ep_dev, 3);
     if (p->sharded) {
       p->cmp_scratch_bytes = ppo_compact_scratch_bytes(p->per);
@@ -869,6 +880,13 @@ int marl_ppo_n_updates(const marl_ppo* p, int64_t* out) {
   });
 }
 
+int marl_ppo_tensor_core_update(const marl_ppo* p, int* out) {
+  return guarded([&] {
+    if (!p || !out) raise(MARL_ERR_CONTRACT, "marl_ppo_tensor_core_update: NULL argument");
+    *out = p->tc ? 1 : 0;
+  });
+}
+
 int marl_ppo_set_params(marl_ppo* p, const float* actor, const float* critic) {
   return guarded([&] {
     if (!p) raise(MARL_ERR_CONTRACT, "marl_ppo_set_params: NULL handle");
@@ -933,6 +951,7 @@ int marl_ppo_minibatch_grad(marl_ppo* p, const int32_t* d_idx, int64_t M, float*
     set_device(p->h);
     cudaStream_t st = p->h->stream;
     cuda_check(cudaMemsetAsync(p->flags, 0, 2 * sizeof(int), st), "cudaMemset");
+    tc_obs(p);
     minibatch_grad(p, d_idx, M);
     std::vector<double> sa(size_t(p->grid_a) * 6), sc(size_t(p->grid_c) * 6);
     PpoMbStats ms{};

@@ -1,28 +1,34 @@
 // The PPO minibatch step on the 5th-generation tensor cores (bf16 operands,
 // fp32 accumulation in TMEM): ff_minibatch (proj/core/src/algo/ppo.cpp:409-441)
-// for the C5 shape (IPPO, input <= 31, width 64, <= 16 actions), actor and
-// critic in one persistent kernel, one CTA (256 threads, all 512 TMEM
-// columns) per SM, 128 gathered rows per tile:
+// for IPPO nets of width 64, input <= 191 (MPE, SMAX 3m / 2s3z / 5m_vs_6m) and
+// <= 16 actions, actor and critic in one persistent kernel, one CTA (256
+// threads, all 512 TMEM columns) per SM, 128 gathered rows per tile.  The
+// input rows are a bf16 copy of the rollout observations made once per update
+// (ppo_obs_bf16), Kx = round16(in + 1) wide with the constant 1 in column
+// Kx-1, gathered into the canonical operand tile by 16-byte cp.async:
 //
-//   F1  D[0:128)   = X[128x32] . [W1a ; W1c]^T                 forward
+//   F1  D[0:128)   = X[128xKx] . [W1a ; W1c]^T                 forward
 //   F2  D[0:64)    = H1a . W2a^T,  D[64:128) = H1c . W2c^T
 //   F3  D[0:16)    = H2a . W3a^T,  D[16:32)  = H2c . W3c^T
 //   --  ppo_row_loss per row (actor_critic.hpp:340-412) -> dL[128x32]
 //   B1  D[0:64)    = dLa . W3a,    D[64:128) = dLc . W3c        input gradients
+//       + G3  Dg3[128x32] += H2^T . dL   (gW3^T: actor columns 0..15, critic 16)
 //   B2  D[0:64)    = dZ2a . W2a,   D[64:128) = dZ2c . W2c
-//   G1  Dg1[128x32]  += dZ1^T . X      (gW1 both nets; X column 31 == 1 -> gb1)
-//   G2  Dg2[128x128] += dZ2^T . H1     (gW2: the two diagonal 64x64 blocks)
-//   G3  Dg3[128x32]  += H2^T . dL      (gW3^T: actor columns 0..15, critic 16)
-//   Gb  Db2[128x16]  += dZ2^T . 1      (gb2)
+//       + G2  Dg2[128x128] += dZ2^T . H1 (gW2: the two diagonal 64x64 blocks)
+//       + Gb  Dgb[128x32]  += dZ2^T . dL (column 31 of dL is 1 -> gb2)
+//   G1  Dg1[128xKx] += dZ1^T . X       (gW1 both nets; X column Kx-1 == 1 -> gb1)
 //
 // Every activation / gradient tile is written once, bf16, in the canonical
 // K-major no-swizzle layout [rows x features]; the input-gradient GEMMs read
 // the forward weight images and the weight-gradient GEMMs read the activation
 // tiles TRANSPOSED through MN-major descriptors (tc.cuh umma_desc_mn), so no
-// operand is ever re-laid-out.  The weight-gradient accumulators live in TMEM
-// for all the CTA's tiles and are read out once.  The next tile's rows are
-// gathered with cp.async while the current tile computes.  The row loss is
-// evaluated in float (the operands are bf16 already).
+// operand is ever re-laid-out.  Each weight-gradient GEMM is issued with the
+// input-gradient GEMM that last needs its activation tile, so dZ2 overwrites
+// H2 and dZ1 overwrites H1 in place (two activation tiles, not four).  The
+// weight-gradient accumulators live in TMEM for all the CTA's tiles and are
+// read out once.  The next tile's rows are gathered while the current tile
+// computes (two X buffers when shared memory allows, else after G1).  The row
+// loss is evaluated in float (the operands are bf16 already).
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -40,17 +46,19 @@ namespace {
 constexpr int kRows = 128;
 constexpr int kThr = 256;
 constexpr uint32_t kCols = 512;
-constexpr uint32_t cWork = 0, cG1 = 128, cG3 = 160, cB2 = 192, cG2 = 256;
+constexpr uint32_t cWork = 0, cG2 = 128, cG3 = 256, cGb = 288, cG1 = 320;  // cG1 + Kx <= 512
+constexpr int kMaxKx = 192;
+constexpr int kSmemMax = 232448;  // 227 KB opt-in per CTA
 constexpr int kStat = 6;
 
 struct UpdLayout {
-  uint32_t w1, w2a, w2c, w3a, w3c, ones, x, h1, h2, dz2, dz1, dl, st_x, st_f, st_i, st_l, slot, bias, gb3w, bar, bar_g,
-      tmem_slot, total;
+  uint32_t w1, w2a, w2c, w3a, w3c, x, ha, hb, dl, st_f, st_i, st_l, slot, bias, gb3w, bar, bar_g, tmem_slot, total;
+  int nx;  // X buffers (2: the next tile's rows land while this one computes)
 };
 
 __host__ __device__ inline uint32_t upd_up(uint32_t v, uint32_t a) { return (v + a - 1) / a * a; }
 
-__host__ __device__ inline UpdLayout upd_layout(int in) {
+__host__ __device__ inline UpdLayout upd_layout(int kx, int nx) {
   UpdLayout L{};
   uint32_t o = 0;
   auto take = [&o](uint32_t bytes, uint32_t align) {
@@ -59,22 +67,19 @@ __host__ __device__ inline UpdLayout upd_layout(int in) {
     o += bytes;
     return at;
   };
-  L.w1 = take(128 * 32 * 2, 128);
+  L.nx = nx;
+  L.w1 = take(128 * kx * 2, 128);
   L.w2a = take(64 * 64 * 2, 128);
   L.w2c = take(64 * 64 * 2, 128);
   L.w3a = take(16 * 64 * 2, 128);
   L.w3c = take(16 * 64 * 2, 128);
-  L.ones = take(16 * 128 * 2, 128);
-  L.x = take(kRows * 32 * 2, 128);
-  L.h1 = take(kRows * 128 * 2, 128);
-  L.h2 = take(kRows * 128 * 2, 128);
-  L.dz2 = take(kRows * 128 * 2, 128);
-  L.dz1 = take(kRows * 128 * 2, 128);
+  L.x = take(uint32_t(nx) * kRows * kx * 2, 128);
+  L.ha = take(kRows * 128 * 2, 128);  // H1, then dZ1
+  L.hb = take(kRows * 128 * 2, 128);  // H2, then dZ2
   L.dl = take(kRows * 32 * 2, 128);
-  L.st_x = take(uint32_t(kRows * in * 4), 16);  // staged input rows of the next tile
-  L.st_f = take(kRows * 5 * 4, 16);             // active, adv, old logp, vtarg, old value
-  L.st_i = take(kRows * 4, 16);                 // action
-  L.st_l = take(kRows * 5 * 4, 16);             // legal words
+  L.st_f = take(kRows * 5 * 4, 16);  // active, adv, old logp, vtarg, old value
+  L.st_i = take(kRows * 4, 16);      // action
+  L.st_l = take(kRows * 5 * 4, 16);  // legal words
   L.slot = take(3 * kRows * 4, 16);
   L.bias = take((4 * 64 + 2 * 16) * 4, 16);
   L.gb3w = take(8 * 32 * 4, 16);
@@ -85,8 +90,18 @@ __host__ __device__ inline UpdLayout upd_layout(int in) {
   return L;
 }
 
+__host__ __device__ inline UpdLayout upd_layout(int kx) {
+  const UpdLayout two = upd_layout(kx, 2);
+  return two.total <= uint32_t(kSmemMax) ? two : upd_layout(kx, 1);
+}
+
 __device__ __forceinline__ void cpa4(void* sdst, const void* gsrc, int src_bytes) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(smem_u32(sdst)), "l"(gsrc), "r"(src_bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void cpa16(void* sdst, const void* gsrc, int src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(sdst)), "l"(gsrc), "r"(src_bytes)
                : "memory");
 }
 
@@ -116,15 +131,35 @@ __device__ __forceinline__ uint16_t bf16_bits(float v) {
   return *reinterpret_cast<const uint16_t*>(&h);
 }
 
+// rows x in fp32 -> rows x kx bf16, column kx-1 = 1 (the bias column), zero padding between
+__global__ void obs_bf16_kernel(const float* __restrict__ obs, int64_t rows, int in, int kx, uint4* __restrict__ out) {
+  const int chunks = kx / 8;
+  const int64_t n = rows * chunks;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n; e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t r = e / chunks;
+    const int c0 = int(e - r * chunks) * 8;
+    float v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int k = c0 + j;
+      v[j] = k < in ? __ldg(obs + r * in + k) : (k == kx - 1 ? 1.0f : 0.0f);
+    }
+    uint4 q;
+    q.x = pack_bf16(v[0], v[1]);
+    q.y = pack_bf16(v[2], v[3]);
+    q.z = pack_bf16(v[4], v[5]);
+    q.w = pack_bf16(v[6], v[7]);
+    out[e] = q;
+  }
+}
+
 __global__ void __launch_bounds__(kThr, 1) ppo_update_tc_kernel(PpoTcArgs a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  const int in = a.in, NA = a.n_act;
-  const UpdLayout L = upd_layout(in);
+  const int in = a.in, NA = a.n_act, KX = a.kx;
+  const UpdLayout L = upd_layout(KX);
   uint8_t* base = smem_raw;
   uint8_t *w1 = base + L.w1, *w2a = base + L.w2a, *w2c = base + L.w2c, *w3a = base + L.w3a, *w3c = base + L.w3c,
-          *ones = base + L.ones, *sx = base + L.x, *h1 = base + L.h1, *h2 = base + L.h2, *dz2 = base + L.dz2,
-          *dz1 = base + L.dz1, *sdl = base + L.dl;
-  float* st_x = reinterpret_cast<float*>(base + L.st_x);
+          *xb = base + L.x, *ha = base + L.ha, *hb = base + L.hb, *sdl = base + L.dl;
   float* st_f = reinterpret_cast<float*>(base + L.st_f);
   int32_t* st_i = reinterpret_cast<int32_t*>(base + L.st_i);
   uint32_t* st_l = reinterpret_cast<uint32_t*>(base + L.st_l);
@@ -134,6 +169,7 @@ __global__ void __launch_bounds__(kThr, 1) ppo_update_tc_kernel(PpoTcArgs a) {
   uint64_t* bar = reinterpret_cast<uint64_t*>(base + L.bar);
   uint64_t* bar_g = reinterpret_cast<uint64_t*>(base + L.bar_g);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(base + L.tmem_slot);
+  const uint32_t xbytes = uint32_t(kRows) * uint32_t(KX) * 2u;
   const int t = threadIdx.x, row = t & (kRows - 1), part = t >> 7, warp = t >> 5;
   const int64_t ntiles = (a.M + kRows - 1) / kRows;
   const int64_t G = gridDim.x;
@@ -157,11 +193,11 @@ __global__ void __launch_bounds__(kThr, 1) ppo_update_tc_kernel(PpoTcArgs a) {
     const float *cw1 = pc, *cb1 = cw1 + 64 * in, *cw2 = cb1 + 64, *cb2 = cw2 + 64 * 64, *cw3 = cb2 + 64,
                 *cb3 = cw3 + 64;
     uint16_t* W1 = reinterpret_cast<uint16_t*>(w1);
-    for (int q = t; q < 128 * 32; q += kThr) {
-      const int r = q / 32, k = q % 32;
-      float v = 0.0f;
+    for (int q = t; q < 128 * KX; q += kThr) {
+      const int r = q / KX, k = q - r * KX;
+      float v = 0.0f;  // the bias column Kx-1 and the padding multiply zero weights
       if (k < in) v = r < 64 ? __ldg(aw1 + r * in + k) : __ldg(cw1 + (r - 64) * in + k);
-      W1[canon_off(r, k, 32) / 2] = bf16_bits(v);
+      W1[canon_off(r, k, KX) / 2] = bf16_bits(v);
     }
     for (int q = t; q < 64 * 64; q += kThr) {
       const int r = q / 64, k = q % 64;
@@ -172,10 +208,6 @@ __global__ void __launch_bounds__(kThr, 1) ppo_update_tc_kernel(PpoTcArgs a) {
       const int r = q / 64, k = q % 64;
       reinterpret_cast<uint16_t*>(w3a)[canon_off(r, k, 64) / 2] = bf16_bits(r < NA ? __ldg(aw3 + r * 64 + k) : 0.0f);
       reinterpret_cast<uint16_t*>(w3c)[canon_off(r, k, 64) / 2] = bf16_bits(r == 0 ? __ldg(cw3 + k) : 0.0f);
-    }
-    for (int q = t; q < 16 * 128; q += kThr) {
-      const int n = q / 128, k = q % 128;
-      reinterpret_cast<uint16_t*>(ones)[canon_off(n, k, 128) / 2] = bf16_bits(n == 0 ? 1.0f : 0.0f);
     }
     if (t < 64) {
       bias[t] = __ldg(ab1 + t);
@@ -189,8 +221,8 @@ __global__ void __launch_bounds__(kThr, 1) ppo_update_tc_kernel(PpoTcArgs a) {
     }
     gb3w[t] = 0.0f;  // 8 warps x 32
   }
-  // ---- gather of a tile's rows into the staging area (cp.async, zero-filled)
-  // slots arrive by cp.async (zero-filled past the end); validity is index arithmetic
+  // ---- gather of a tile's rows (cp.async, zero-filled): X straight into its
+  // canonical operand buffer, the loss inputs into the staging area
   auto slot_ok = [&](int64_t tile, int r) { return tile < ntiles && tile * kRows + r < a.M; };
   auto slot_load = [&](int64_t tile, int sb) {
     if (t < kRows) {
@@ -198,11 +230,13 @@ __global__ void __launch_bounds__(kThr, 1) ppo_update_tc_kernel(PpoTcArgs a) {
       cpa4(slot + sb * kRows + t, ok ? a.idx + tile * kRows + t : a.idx, ok ? 4 : 0);
     }
   };
-  auto gather = [&](int64_t tile, int sb) {
-    for (int e = t; e < kRows * in; e += kThr) {
-      const int r = e / in, k = e - r * in;
+  auto gather = [&](int64_t tile, int sb, uint8_t* xdst) {
+    const int ch = KX / 8;
+    for (int e = t; e < kRows * ch; e += kThr) {
+      const int r = e / ch, c = e - r * ch;
       const int sl = slot_ok(tile, r) ? slot[sb * kRows + r] : -1;
-      cpa4(st_x + e, sl >= 0 ? a.obs + size_t(sl) * size_t(in) + k : a.obs, sl >= 0 ? 4 : 0);
+      cpa16(xdst + canon_off(r, 8 * c, KX), sl >= 0 ? a.obs_bf + (size_t(sl) * size_t(KX) + size_t(8 * c)) : a.obs_bf,
+            sl >= 0 ? 16 : 0);
     }
     if (t < kRows) {
       const int sl = slot_ok(tile, t) ? slot[sb * kRows + t] : -1;
@@ -226,7 +260,7 @@ __global__ void __launch_bounds__(kThr, 1) ppo_update_tc_kernel(PpoTcArgs a) {
   asm volatile("cp.async.commit_group;" ::: "memory");
   asm volatile("cp.async.wait_group 0;" ::: "memory");
   __syncthreads();
-  gather(blockIdx.x, 0);
+  gather(blockIdx.x, 0, xb);
   fence_proxy_async_smem();
   tc_fence_before();
   __syncthreads();
@@ -237,60 +271,44 @@ __global__ void __launch_bounds__(kThr, 1) ppo_update_tc_kernel(PpoTcArgs a) {
   const float inv_tw = st.total_w > 0.0 ? float(1.0 / st.total_w) : 0.0f;
   double pg = 0.0, vt = 0.0, ent = 0.0, kl = 0.0, clipn = 0.0;
   uint32_t phase = 0, phase_g = 0;
-  bool g_pending = false, g_first = true;
+  bool g_first = true;
   int it = 0;
 
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += G, ++it) {
     const int sb = it % 3;
-    // this tile's rows have landed; the previous tile's G MMAs have read the operand tiles
+    uint8_t* sx = xb + (L.nx == 2 ? uint32_t(it & 1) * xbytes : 0u);
+    // this tile's rows have landed (generic-proxy cp.async writes -> visible to the MMA's async proxy)
     asm volatile("cp.async.wait_group 0;" ::: "memory");
-    if (g_pending) {
-      mbar_wait(bar_g, phase_g);
-      phase_g ^= 1;
-      g_pending = false;
-    }
+    fence_proxy_async_smem();
     __syncthreads();
     tc_fence_after();
-    // ---- staging -> X operand (bf16; column 31 carries the constant 1 of the bias gradient)
     const bool live = slot_ok(tile, row);
     float r_w = 0.0f, r_adv = 0.0f, r_lp = 0.0f, r_vt = 0.0f, r_v = 0.0f;
     int r_act = 0;
     uint32_t r_lg[5] = {0, 0, 0, 0, 0};
-    {
-      float x[16];
+    if (live) {
+      r_w = st_f[row];
+      if (part == 0) {
+        r_adv = st_f[kRows + row];
+        r_lp = st_f[2 * kRows + row];
+        r_act = st_i[row];
 #pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const int k = 16 * part + j;
-        x[j] = (live && k < in) ? st_x[row * in + k] : ((live && k == 31) ? 1.0f : 0.0f);
-      }
-      put16(sx, 32, row, 16 * part, x);
-      if (live) {
-        r_w = st_f[row];
-        if (part == 0) {
-          r_adv = st_f[kRows + row];
-          r_lp = st_f[2 * kRows + row];
-          r_act = st_i[row];
-#pragma unroll
-          for (int w = 0; w < 5; ++w) r_lg[w] = st_l[w * kRows + row];
-        } else {
-          r_vt = st_f[3 * kRows + row];
-          r_v = st_f[4 * kRows + row];
-        }
+        for (int w = 0; w < 5; ++w) r_lg[w] = st_l[w * kRows + row];
+      } else {
+        r_vt = st_f[3 * kRows + row];
+        r_v = st_f[4 * kRows + row];
       }
     }
     const int64_t sl_row = slot[sb * kRows + row];
-    fence_proxy_async_smem();
-    __syncthreads();
-    // the staging area is free: gather the next tile (and the slots of the one
-    // after it) while this one computes
-    slot_load(tile + 2 * G, (it + 2) % 3);
-    gather(tile + G, (it + 1) % 3);
     if (t == 0) {
       tc_fence_after();
       const uint32_t id = idesc_bf16(128, 128);
-      for (int k = 0; k < 32; k += 16) umma_bf16(tmem + cWork, umma_desc(sx, 32, k), umma_desc(w1, 32, k), id, k > 0);
+      for (int k = 0; k < KX; k += 16) umma_bf16(tmem + cWork, umma_desc(sx, KX, k), umma_desc(w1, KX, k), id, k > 0);
       umma_commit(bar);
     }
+    __syncthreads();  // the staging area is free
+    slot_load(tile + 2 * G, (it + 2) % 3);
+    if (L.nx == 2) gather(tile + G, (it + 1) % 3, xb + uint32_t((it + 1) & 1) * xbytes);
     mbar_wait(bar, phase);
     phase ^= 1;
     tc_fence_after();
@@ -301,8 +319,8 @@ __global__ void __launch_bounds__(kThr, 1) ppo_update_tc_kernel(PpoTcArgs a) {
       tmem_ld32(tmem + lane_base + cWork + uint32_t(c), v);
 #pragma unroll
       for (int i = 0; i < 32; ++i) v[i] = act_f(v[i] + bias[c + i], a.relu);
-      put16(h1, 128, row, c, v);
-      put16(h1, 128, row, c + 16, v + 16);
+      put16(ha, 128, row, c, v);
+      put16(ha, 128, row, c + 16, v + 16);
     }
     tc_fence_before();
     fence_proxy_async_smem();
@@ -310,8 +328,8 @@ __global__ void __launch_bounds__(kThr, 1) ppo_update_tc_kernel(PpoTcArgs a) {
     if (t == 0) {
       tc_fence_after();
       const uint32_t id = idesc_bf16(128, 64);
-      for (int k = 0; k < 64; k += 16) umma_bf16(tmem + 0, umma_desc(h1, 128, k), umma_desc(w2a, 64, k), id, k > 0);
-      for (int k = 0; k < 64; k += 16) umma_bf16(tmem + 64, umma_desc(h1, 128, 64 + k), umma_desc(w2c, 64, k), id, k > 0);
+      for (int k = 0; k < 64; k += 16) umma_bf16(tmem + 0, umma_desc(ha, 128, k), umma_desc(w2a, 64, k), id, k > 0);
+      for (int k = 0; k < 64; k += 16) umma_bf16(tmem + 64, umma_desc(ha, 128, 64 + k), umma_desc(w2c, 64, k), id, k > 0);
       umma_commit(bar);
     }
     mbar_wait(bar, phase);
@@ -323,8 +341,8 @@ __global__ void __launch_bounds__(kThr, 1) ppo_update_tc_kernel(PpoTcArgs a) {
       tmem_ld32(tmem + lane_base + uint32_t(c), v);
 #pragma unroll
       for (int i = 0; i < 32; ++i) v[i] = act_f(v[i] + bias[128 + c + i], a.relu);
-      put16(h2, 128, row, c, v);
-      put16(h2, 128, row, c + 16, v + 16);
+      put16(hb, 128, row, c, v);
+      put16(hb, 128, row, c + 16, v + 16);
     }
     tc_fence_before();
     fence_proxy_async_smem();
@@ -332,8 +350,8 @@ __global__ void __launch_bounds__(kThr, 1) ppo_update_tc_kernel(PpoTcArgs a) {
     if (t == 0) {
       tc_fence_after();
       const uint32_t id = idesc_bf16(128, 16);
-      for (int k = 0; k < 64; k += 16) umma_bf16(tmem + 0, umma_desc(h2, 128, k), umma_desc(w3a, 64, k), id, k > 0);
-      for (int k = 0; k < 64; k += 16) umma_bf16(tmem + 16, umma_desc(h2, 128, 64 + k), umma_desc(w3c, 64, k), id, k > 0);
+      for (int k = 0; k < 64; k += 16) umma_bf16(tmem + 0, umma_desc(hb, 128, k), umma_desc(w3a, 64, k), id, k > 0);
+      for (int k = 0; k < 64; k += 16) umma_bf16(tmem + 16, umma_desc(hb, 128, 64 + k), umma_desc(w3c, 64, k), id, k > 0);
       umma_commit(bar);
     }
     mbar_wait(bar, phase);
@@ -406,8 +424,6 @@ __global__ void __launch_bounds__(kThr, 1) ppo_update_tc_kernel(PpoTcArgs a) {
         vt += w * double(0.5f * fmaxf(sq, sq_c));
         d[0] = r_w * inv_tw * float(a.vf_coef) * (sq >= sq_c ? (v - r_vt) : 0.0f);
       }
-      tc_fence_before();
-      put16(sdl, 32, row, 16 * part, d);
       // gb3: per-warp column sums, each warp owning its own slots (deterministic)
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
@@ -416,78 +432,85 @@ __global__ void __launch_bounds__(kThr, 1) ppo_update_tc_kernel(PpoTcArgs a) {
         for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
         if ((t & 31) == 0) gb3w[warp * 32 + 16 * part + j] += s;
       }
+      if (part == 1) d[15] = 1.0f;  // dL column 31: the constant of the gb2 GEMM (W3c row 15 is zero)
+      tc_fence_before();
+      put16(sdl, 32, row, 16 * part, d);
     }
     fence_proxy_async_smem();
     __syncthreads();
-    if (t == 0) {  // B1: dH2 = dL . W3 (the forward head images read MN-major)
+    if (t == 0) {  // B1: dH2 = dL . W3 (the forward head images read MN-major); G3 reads H2 before it is overwritten
       tc_fence_after();
-      const uint32_t id = idesc_bf16(128, 64, 0, 1);
+      const uint32_t id = idesc_bf16(128, 64, 0, 1), i3 = idesc_bf16(128, 32, 1, 1);
       umma_bf16(tmem + 0, umma_desc(sdl, 32, 0), umma_desc_mn(w3a, 64, 0), id, 0);
       umma_bf16(tmem + 64, umma_desc(sdl, 32, 16), umma_desc_mn(w3c, 64, 0), id, 0);
+      for (int r0 = 0; r0 < kRows; r0 += 16)
+        umma_bf16(tmem + cG3, umma_desc_mn(hb, 128, r0), umma_desc_mn(sdl, 32, r0), i3, (g_first && r0 == 0) ? 0u : 1u);
       umma_commit(bar);
     }
     mbar_wait(bar, phase);
     phase ^= 1;
     tc_fence_after();
 #pragma unroll 1
-    for (int c = 64 * part; c < 64 * part + 64; c += 32) {
+    for (int c = 64 * part; c < 64 * part + 64; c += 32) {  // dZ2 over H2, element by element of this row
       float v[32], y[32];
       tmem_ld32(tmem + lane_base + uint32_t(c), v);
-      get16(h2, 128, row, c, y);
-      get16(h2, 128, row, c + 16, y + 16);
+      get16(hb, 128, row, c, y);
+      get16(hb, 128, row, c + 16, y + 16);
 #pragma unroll
       for (int i = 0; i < 32; ++i) v[i] = act_d(v[i], y[i], a.relu);
-      put16(dz2, 128, row, c, v);
-      put16(dz2, 128, row, c + 16, v + 16);
+      put16(hb, 128, row, c, v);
+      put16(hb, 128, row, c + 16, v + 16);
     }
     tc_fence_before();
     fence_proxy_async_smem();
     __syncthreads();
-    if (t == 0) {  // B2: dH1 = dZ2 . W2
+    if (t == 0) {  // B2: dH1 = dZ2 . W2; G2 and Gb read dZ2 and H1 before H1 is overwritten
       tc_fence_after();
-      const uint32_t id = idesc_bf16(128, 64, 0, 1);
-      for (int k = 0; k < 64; k += 16) umma_bf16(tmem + 0, umma_desc(dz2, 128, k), umma_desc_mn(w2a, 64, k), id, k > 0);
+      const uint32_t id = idesc_bf16(128, 64, 0, 1), i2 = idesc_bf16(128, 128, 1, 1), ib = idesc_bf16(128, 32, 1, 1);
+      for (int k = 0; k < 64; k += 16) umma_bf16(tmem + 0, umma_desc(hb, 128, k), umma_desc_mn(w2a, 64, k), id, k > 0);
       for (int k = 0; k < 64; k += 16)
-        umma_bf16(tmem + 64, umma_desc(dz2, 128, 64 + k), umma_desc_mn(w2c, 64, k), id, k > 0);
-      umma_commit(bar);
-    }
-    mbar_wait(bar, phase);
-    phase ^= 1;
-    tc_fence_after();
-#pragma unroll 1
-    for (int c = 64 * part; c < 64 * part + 64; c += 32) {
-      float v[32], y[32];
-      tmem_ld32(tmem + lane_base + uint32_t(c), v);
-      get16(h1, 128, row, c, y);
-      get16(h1, 128, row, c + 16, y + 16);
-#pragma unroll
-      for (int i = 0; i < 32; ++i) v[i] = act_d(v[i], y[i], a.relu);
-      put16(dz1, 128, row, c, v);
-      put16(dz1, 128, row, c + 16, v + 16);
-    }
-    tc_fence_before();
-    fence_proxy_async_smem();
-    __syncthreads();
-    if (t == 0) {  // G: weight gradients of the tile, accumulated in TMEM across tiles
-      tc_fence_after();
-      const uint32_t i1 = idesc_bf16(128, 32, 1, 1), i2 = idesc_bf16(128, 128, 1, 1), ib = idesc_bf16(128, 16, 1, 0);
+        umma_bf16(tmem + 64, umma_desc(hb, 128, 64 + k), umma_desc_mn(w2c, 64, k), id, k > 0);
       for (int r0 = 0; r0 < kRows; r0 += 16) {
         const uint32_t acc = (g_first && r0 == 0) ? 0u : 1u;
-        umma_bf16(tmem + cG1, umma_desc_mn(dz1, 128, r0), umma_desc_mn(sx, 32, r0), i1, acc);
-        umma_bf16(tmem + cG2, umma_desc_mn(dz2, 128, r0), umma_desc_mn(h1, 128, r0), i2, acc);
-        umma_bf16(tmem + cG3, umma_desc_mn(h2, 128, r0), umma_desc_mn(sdl, 32, r0), i1, acc);
-        umma_bf16(tmem + cB2, umma_desc_mn(dz2, 128, r0), umma_desc(ones, 128, r0), ib, acc);
+        umma_bf16(tmem + cG2, umma_desc_mn(hb, 128, r0), umma_desc_mn(ha, 128, r0), i2, acc);
+        umma_bf16(tmem + cGb, umma_desc_mn(hb, 128, r0), umma_desc_mn(sdl, 32, r0), ib, acc);
       }
+      umma_commit(bar);
+    }
+    mbar_wait(bar, phase);
+    phase ^= 1;
+    tc_fence_after();
+#pragma unroll 1
+    for (int c = 64 * part; c < 64 * part + 64; c += 32) {  // dZ1 over H1
+      float v[32], y[32];
+      tmem_ld32(tmem + lane_base + uint32_t(c), v);
+      get16(ha, 128, row, c, y);
+      get16(ha, 128, row, c + 16, y + 16);
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] = act_d(v[i], y[i], a.relu);
+      put16(ha, 128, row, c, v);
+      put16(ha, 128, row, c + 16, v + 16);
+    }
+    tc_fence_before();
+    fence_proxy_async_smem();
+    __syncthreads();
+    if (t == 0) {  // G1: weight gradient of the first layer, accumulated in TMEM across tiles
+      tc_fence_after();
+      const uint32_t i1 = idesc_bf16(128, KX, 1, 1);
+      for (int r0 = 0; r0 < kRows; r0 += 16)
+        umma_bf16(tmem + cG1, umma_desc_mn(ha, 128, r0), umma_desc_mn(sx, KX, r0), i1, (g_first && r0 == 0) ? 0u : 1u);
       umma_commit(bar_g);
     }
-    g_pending = true;
     g_first = false;
-  }
-  asm volatile("cp.async.wait_group 0;" ::: "memory");
-  if (g_pending) {
+    // H1 / X are rewritten by the next tile only after G1 has read them
     mbar_wait(bar_g, phase_g);
     phase_g ^= 1;
+    if (L.nx == 1) {
+      tc_fence_after();
+      gather(tile + G, (it + 1) % 3, xb);
+    }
   }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
   __syncthreads();
   tc_fence_after();
   // ---- read the accumulators once: TMEM lane m = output feature m (actor 0..63, critic 64..127)
@@ -497,15 +520,19 @@ __global__ void __launch_bounds__(kThr, 1) ppo_update_tc_kernel(PpoTcArgs a) {
   const int Pa = 64 * in + 64 + 64 * 64 + 64 + NA * 64 + NA, Pc = 64 * in + 64 + 64 * 64 + 64 + 64 + 1;
   float* gp = critic ? a.gpart_c + size_t(blockIdx.x) * Pc : a.gpart_a + size_t(blockIdx.x) * Pa;
   const int NO = critic ? 1 : NA;
-  float *G1 = gp, *GB1 = G1 + 64 * in, *G2 = GB1 + 64, *GB2 = G2 + 64 * 64, *G3 = GB2 + 64, *GB3 = G3 + NO * 64;
+  float *G1 = gp, *GB1 = G1 + 64 * in, *G2 = GB1 + 64, *GB2 = G2 + 64 * 64, *G3 = GB2 + 64;
+  (void)NO;
   if (!g_first) {
     float v[16];
-    tmem_ld16(tmem + lane_base + cG1 + uint32_t(16 * part), v);  // gW1 columns k (31: gb1)
+#pragma unroll 1
+    for (int c = 16 * part; c < KX; c += 32) {  // gW1 columns k (Kx-1: gb1)
+      tmem_ld16(tmem + lane_base + cG1 + uint32_t(c), v);
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      const int k = 16 * part + j;
-      if (k < in) G1[o * in + k] = v[j];
-      if (k == 31) GB1[o] = v[j];
+      for (int j = 0; j < 16; ++j) {
+        const int k = c + j;
+        if (k < in) G1[o * in + k] = v[j];
+        if (k == KX - 1) GB1[o] = v[j];
+      }
     }
     float w[32];
     tmem_ld32(tmem + lane_base + cG2 + uint32_t((critic ? 64 : 0) + 32 * part), w);  // diagonal block
@@ -518,8 +545,8 @@ __global__ void __launch_bounds__(kThr, 1) ppo_update_tc_kernel(PpoTcArgs a) {
         if (j < NA) G3[j * 64 + o] = v[j];
     }
     if (critic && part == 1) G3[o] = v[0];
-    tmem_ld16(tmem + lane_base + cB2, v);
-    if (part == 0) GB2[o] = v[0];
+    tmem_ld16(tmem + lane_base + cGb + 16u, v);  // column 31: dZ2^T . 1
+    if (part == 0) GB2[o] = v[15];
   } else {
     for (int e = t; e < Pa; e += kThr) a.gpart_a[size_t(blockIdx.x) * Pa + e] = 0.0f;
     for (int e = t; e < Pc; e += kThr) a.gpart_c[size_t(blockIdx.x) * Pc + e] = 0.0f;
@@ -553,13 +580,15 @@ __global__ void __launch_bounds__(kThr, 1) ppo_update_tc_kernel(PpoTcArgs a) {
     a.spart_c[size_t(blockIdx.x) * kStat + t] = (t == 1) ? s0 : 0.0;
   }
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kCols) : "memory");
-  (void)GB3;
 }
 
 }  // namespace
 
+int ppo_tc_kx(int in_dim) { return (in_dim + 1 + 15) / 16 * 16; }
+
 bool ppo_tc_supported(int in_dim, int critic_in, int width, int n_act) {
-  return in_dim <= 31 && critic_in == in_dim && width == 64 && n_act <= 16;
+  return in_dim >= 1 && ppo_tc_kx(in_dim) <= kMaxKx && critic_in == in_dim && width == 64 && n_act <= 16 &&
+         upd_layout(ppo_tc_kx(in_dim)).total <= uint32_t(kSmemMax);
 }
 
 int ppo_tc_grid(int64_t M) {
@@ -573,8 +602,16 @@ int ppo_tc_grid(int64_t M) {
   return int(std::max<int64_t>(1, std::min<int64_t>(tiles, sms)));
 }
 
+void ppo_obs_bf16(const float* obs, int64_t rows, int in, int kx, uint16_t* out, cudaStream_t s) {
+  const int64_t n = rows * (kx / 8);
+  if (n <= 0) return;
+  const int blocks = int(std::min<int64_t>((n + 255) / 256, 148 * 16));
+  obs_bf16_kernel<<<blocks, 256, 0, s>>>(obs, rows, in, kx, reinterpret_cast<uint4*>(out));
+  ++g_launches;
+}
+
 void ppo_update_tc(const PpoTcArgs& a, int grid, cudaStream_t s) {
-  const size_t sm = upd_layout(a.in).total;
+  const size_t sm = upd_layout(a.kx).total;
   cudaFuncSetAttribute(ppo_update_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
   ppo_update_tc_kernel<<<grid, kThr, sm, s>>>(a);
   ++g_launches;

@@ -199,12 +199,23 @@ constexpr int kSplit = 2;            // threads per row (warps w, w+4, ... share
 struct TcLayout {
   uint32_t w1, w2a, w2c, w3a, w3c, x, ha, hc, obs_in[2], obs_out, legal, resets, active, act, logp, value, u, bias,
       bar, bar_in[2], tmem_slot, total;
+  int kx;       // K of layer 1: round16(in_dim)
+  int nbuf;     // staged observation tiles: 2 (next tile prefetched), 1 (prefetched after the row build), 0 (rows read from L2)
+  int has_out;  // the buffer's input rows leave as one staged bulk store (else a coalesced cooperative store)
 };
+constexpr uint32_t kTcSmemMax = 232448;  // 227 KB opt-in per CTA
+constexpr int kTcMaxKx = 192;
 
 __host__ __device__ inline uint32_t up(uint32_t v, uint32_t a) { return (v + a - 1) / a * a; }
 
-__host__ __device__ inline TcLayout tc_layout(int D, int in_dim, int n_act) {
+__host__ __device__ inline int tc_kx(int in_dim) { return in_dim <= 32 ? 32 : (in_dim + 15) / 16 * 16; }
+
+// mode 3: two staged tiles + staged buffer rows; 2: two tiles; 1: one tile; 0: none
+__host__ __device__ inline TcLayout tc_layout_mode(int D, int in_dim, int n_act, int mode) {
   TcLayout L{};
+  L.kx = tc_kx(in_dim);
+  L.nbuf = mode >= 2 ? 2 : mode;
+  L.has_out = mode == 3;
   uint32_t o = 0;
   auto take = [&o](uint32_t bytes, uint32_t align) {
     o = up(o, align);
@@ -212,17 +223,17 @@ __host__ __device__ inline TcLayout tc_layout(int D, int in_dim, int n_act) {
     o += bytes;
     return at;
   };
-  L.w1 = take(128 * 32 * 2, 128);
+  L.w1 = take(128 * L.kx * 2, 128);
   L.w2a = take(64 * 64 * 2, 128);
   L.w2c = take(64 * 64 * 2, 128);
   L.w3a = take(16 * 64 * 2, 128);
   L.w3c = take(16 * 64 * 2, 128);
-  L.x = take(kTcRows * 32 * 2, 128);
+  L.x = take(kTcRows * L.kx * 2, 128);
   L.ha = take(kTcRows * 64 * 2, 128);
   L.hc = take(kTcRows * 64 * 2, 128);
-  L.obs_in[0] = take(uint32_t(kTcRows * D * 4), 16);
-  L.obs_in[1] = take(uint32_t(kTcRows * D * 4), 16);
-  L.obs_out = take(uint32_t(kTcRows * in_dim * 4), 16);
+  L.obs_in[0] = L.nbuf >= 1 ? take(uint32_t(kTcRows * D * 4), 16) : 0;
+  L.obs_in[1] = L.nbuf >= 2 ? take(uint32_t(kTcRows * D * 4), 16) : L.obs_in[0];
+  L.obs_out = L.has_out ? take(uint32_t(kTcRows * in_dim * 4), 16) : 0;
   L.legal = take(uint32_t(kTcRows * n_act), 16);
   L.resets = take(kTcRows, 16);
   L.active = take(kTcRows * 4, 16);
@@ -237,6 +248,14 @@ __host__ __device__ inline TcLayout tc_layout(int D, int in_dim, int n_act) {
   L.tmem_slot = take(4, 4);
   L.total = up(o, 128);
   return L;
+}
+
+__host__ __device__ inline TcLayout tc_layout(int D, int in_dim, int n_act) {
+  for (int mode = 3; mode > 0; --mode) {
+    const TcLayout L = tc_layout_mode(D, in_dim, n_act, mode);
+    if (L.total <= kTcSmemMax) return L;
+  }
+  return tc_layout_mode(D, in_dim, n_act, 0);
 }
 
 // Store a staged tile: one TMA bulk store when it qualifies, else a
@@ -275,10 +294,15 @@ __device__ __forceinline__ bool tile_obs_load(const PolicyStep& s, int64_t tile,
   return false;
 }
 
+// KXT = 32: the small-input instance (K, staging mode 3 compile-time); 0: any width
+template <int KXT>
 __global__ void __launch_bounds__(kSplit * kTcRows) policy_tc_kernel(PolicyNetBf16 nb, int in_dim, int n_act, PolicyStep s,
                                                             RolloutBufs b) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  const TcLayout L = tc_layout(s.D, in_dim, n_act);
+  const TcLayout L = KXT ? tc_layout_mode(s.D, in_dim, n_act, 3) : tc_layout(s.D, in_dim, n_act);
+  const int KX = KXT ? KXT : L.kx;
+  const int NBUF = KXT ? 2 : L.nbuf;
+  const bool HAS_OUT = KXT ? true : bool(L.has_out);
   uint8_t* base = smem_raw;
   uint8_t *w1 = base + L.w1, *w2a = base + L.w2a, *w2c = base + L.w2c, *w3a = base + L.w3a, *w3c = base + L.w3c;
   uint8_t *sx = base + L.x, *ha = base + L.ha, *hc = base + L.hc;
@@ -322,7 +346,7 @@ __global__ void __launch_bounds__(kSplit * kTcRows) policy_tc_kernel(PolicyNetBf
                            reinterpret_cast<const uint4*>(nb.hc3)};
     uint4* dst[5] = {reinterpret_cast<uint4*>(w1), reinterpret_cast<uint4*>(w2a), reinterpret_cast<uint4*>(w2c),
                      reinterpret_cast<uint4*>(w3a), reinterpret_cast<uint4*>(w3c)};
-    const int n16[5] = {128 * 32 * 2 / 16, 64 * 64 * 2 / 16, 64 * 64 * 2 / 16, 16 * 64 * 2 / 16, 16 * 64 * 2 / 16};
+    const int n16[5] = {128 * KX * 2 / 16, 64 * 64 * 2 / 16, 64 * 64 * 2 / 16, 16 * 64 * 2 / 16, 16 * 64 * 2 / 16};
 #pragma unroll
     for (int m = 0; m < 5; ++m) {
       uint4 v[8];
@@ -352,7 +376,7 @@ __global__ void __launch_bounds__(kSplit * kTcRows) policy_tc_kernel(PolicyNetBf
   uint32_t phase = 0, in_phase[2] = {0, 0};
   bool in_flight[2] = {false, false};
   int cur = 0;
-  if (int64_t(blockIdx.x) < n_tiles) in_flight[0] = tile_obs_load(s, blockIdx.x, obs_in[0], bar_in[0]);
+  if (NBUF > 0 && int64_t(blockIdx.x) < n_tiles) in_flight[0] = tile_obs_load(s, blockIdx.x, obs_in[0], bar_in[0]);
 
   for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
     const int64_t r0 = tile * kTcRows, r = r0 + tid;
@@ -370,26 +394,60 @@ __global__ void __launch_bounds__(kSplit * kTcRows) policy_tc_kernel(PolicyNetBf
     // prefetch the next tile's rows into the other buffer (its last reader,
     // the previous tile's row build, finished before the barrier above)
     const int64_t next = tile + gridDim.x;
-    in_flight[cur ^ 1] = next < n_tiles ? tile_obs_load(s, next, obs_in[cur ^ 1], bar_in[cur ^ 1]) : false;
+    if (NBUF == 2)
+      in_flight[cur ^ 1] = next < n_tiles ? tile_obs_load(s, next, obs_in[cur ^ 1], bar_in[cur ^ 1]) : false;
+    // the tile's env observation rows: staged, or read through L2
+    const float* tile_obs = NBUF > 0 ? obs_in[cur] : s.env_obs + size_t(r0) * size_t(D);
     // ---- write_input / write_legal / agent_active (team.cpp:27-42): part q
-    // builds K columns [32q/kSplit, 32(q+1)/kSplit) of the row
+    // builds K columns [KX q/kSplit, KX (q+1)/kSplit) of the row
     {
-      const float* oin = obs_in[cur];
       const int64_t e = r < 0x7fffffff ? int64_t(uint32_t(r) / uint32_t(s.A)) : r / s.A;
       const int a = int(r - e * s.A);
-      const int k0 = (32 / kSplit) * part;
-      float x[32 / kSplit];
+      const int k0 = (KX / kSplit) * part;
+      auto build = [&](auto load) {
+#pragma unroll 2
+        for (int kk = 0; kk < KX / kSplit; kk += 8) {
+          float x[8];
 #pragma unroll
-      for (int j = 0; j < 32 / kSplit; ++j) {
-        const int k = k0 + j;
-        x[j] = (live && k < D) ? oin[tid * D + k] : 0.0f;
-        if (live && s.A > 1 && k == D + a) x[j] = 1.0f;
+          for (int j = 0; j < 8; ++j) {
+            const int k = k0 + kk + j;
+            x[j] = (live && k < D) ? load(k) : 0.0f;
+            if (live && s.A > 1 && k == D + a) x[j] = 1.0f;
+          }
+          if (live && act_mode && HAS_OUT) {
+            float* o = obs_out + tid * in_dim;
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              if (k0 + kk + j < in_dim) o[k0 + kk + j] = x[j];
+          }
+          put8(sx, KX, tid, k0 + kk, x);
+        }
+      };
+      if constexpr (KXT != 0) {  // small rows: every load issued before any store
+        const float* so = obs_in[cur] + tid * D;
+        float x[KXT / kSplit];
+#pragma unroll
+        for (int j = 0; j < KXT / kSplit; ++j) {
+          const int k = k0 + j;
+          x[j] = (live && k < D) ? so[k] : 0.0f;
+          if (live && s.A > 1 && k == D + a) x[j] = 1.0f;
+        }
+        if (live && act_mode) {
+          float* o = obs_out + tid * in_dim;
+#pragma unroll
+          for (int j = 0; j < KXT / kSplit; ++j)
+            if (k0 + j < in_dim) o[k0 + j] = x[j];
+        }
+#pragma unroll
+        for (int j = 0; j < KXT / kSplit; j += 8) put8(sx, KXT, tid, k0 + j, x + j);
+      } else if (NBUF > 0) {  // staged (shared) rows
+        const float* so = obs_in[cur] + tid * D;
+        build([&](int k) { return so[k]; });
+      } else {  // rows through L2
+        const float* go = s.env_obs + size_t(r) * size_t(D);
+        build([&](int k) { return __ldg(go + k); });
       }
       if (live && act_mode) {
-        float* o = obs_out + tid * in_dim;
-#pragma unroll
-        for (int j = 0; j < 32 / kSplit; ++j)
-          if (k0 + j < in_dim) o[k0 + j] = x[j];
         if (part == 0) {
           s_resets[tid] = s.prev_finished ? s.prev_finished[e] : uint8_t(1);
           uint8_t* lg = s_legal + tid * n_act;
@@ -403,13 +461,22 @@ __global__ void __launch_bounds__(kSplit * kTcRows) policy_tc_kernel(PolicyNetBf
           s_active[tid] = (s.family == 1) ? (lg[0] ? 1.0f : 0.0f) : 1.0f;
         }
       }
-#pragma unroll
-      for (int j = 0; j < 32 / kSplit; j += 8) put8(sx, 32, tid, k0 + j, x + j);
     }
     fence_proxy_async_smem();
     __syncthreads();
     if (act_mode) {  // the input-side buffer rows leave while the MMAs run
-      tile_put(b.obs + slot0 * in_dim, obs_out, size_t(rows) * in_dim * 4);
+      if (HAS_OUT) {
+        tile_put(b.obs + slot0 * in_dim, obs_out, size_t(rows) * in_dim * 4);
+      } else {  // rebuilt from the tile's observation rows, coalesced
+        float* go = b.obs + slot0 * in_dim;
+        const int n = rows * in_dim;
+        for (int q = threadIdx.x; q < n; q += blockDim.x) {
+          const int rr = q / in_dim, k = q - rr * in_dim;
+          const int a = int((r0 + rr) % s.A);
+          go[q] = k < D ? (NBUF > 0 ? tile_obs[rr * D + k] : __ldg(tile_obs + size_t(rr) * D + k))
+                        : ((s.A > 1 && k == D + a) ? 1.0f : 0.0f);
+        }
+      }
       if (!s.legal_ready) tile_put(b.legal + slot0 * n_act, s_legal, size_t(rows) * n_act);
       if (threadIdx.x == 0) bulk_commit();
       if (live && part == 0) {  // one element per thread: already coalesced
@@ -417,10 +484,14 @@ __global__ void __launch_bounds__(kSplit * kTcRows) policy_tc_kernel(PolicyNetBf
         b.active[slot0 + tid] = s_active[tid];
       }
     }
+    if (NBUF == 1) {  // the single staging tile has been read: prefetch the next tile into it
+      __syncthreads();
+      in_flight[0] = next < n_tiles ? tile_obs_load(s, next, obs_in[0], bar_in[0]) : false;
+    }
     if (threadIdx.x == 0) {
       tc_fence_after();
       const uint32_t id = idesc_bf16(128, 128);
-      for (int k = 0; k < 32; k += 16) umma_bf16(tmem + 0, umma_desc(sx, 32, k), umma_desc(w1, 32, k), id, k > 0);
+      for (int k = 0; k < KX; k += 16) umma_bf16(tmem + 0, umma_desc(sx, KX, k), umma_desc(w1, KX, k), id, k > 0);
       umma_commit(bar);
     }
     // the row's sampling uniform (two Threefry blocks) is drawn by part 1
@@ -499,7 +570,7 @@ __global__ void __launch_bounds__(kSplit * kTcRows) policy_tc_kernel(PolicyNetBf
         b.logp[slot0 + tid] = lp;
       }
     }
-    cur ^= 1;
+    if (NBUF == 2) cur ^= 1;
     __syncthreads();  // TMEM columns and operand tiles are reused by the next tile
   }
   if (threadIdx.x == 0) bulk_wait<0>();
@@ -510,9 +581,9 @@ __global__ void __launch_bounds__(kSplit * kTcRows) policy_tc_kernel(PolicyNetBf
 
 // fp32 parameters -> canonical bf16 operand images + bias block.
 __global__ void pack_bf16_kernel(PolicyNet n, uint16_t* img, float* bias) {
-  const int in = n.in_dim, NA = n.n_act;
+  const int in = n.in_dim, NA = n.n_act, KX = tc_kx(in);
   uint16_t* a1 = img;
-  uint16_t* a2 = a1 + 128 * 32;
+  uint16_t* a2 = a1 + 128 * KX;
   uint16_t* c2 = a2 + 64 * 64;
   uint16_t* h3 = c2 + 64 * 64;
   uint16_t* hc3 = h3 + 16 * 64;
@@ -520,11 +591,11 @@ __global__ void pack_bf16_kernel(PolicyNet n, uint16_t* img, float* bias) {
     const __nv_bfloat16 h = __float2bfloat16_rn(v);
     return *reinterpret_cast<const uint16_t*>(&h);
   };
-  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < 128 * 32; q += gridDim.x * blockDim.x) {
-    const int row = q / 32, k = q % 32;
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < 128 * KX; q += gridDim.x * blockDim.x) {
+    const int row = q / KX, k = q % KX;
     float v = 0.0f;
     if (k < in) v = row < 64 ? n.w1[row * in + k] : n.cw1[(row - 64) * in + k];
-    a1[canon_off(row, k, 32) / 2] = bf(v);
+    a1[canon_off(row, k, KX) / 2] = bf(v);
   }
   for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < 64 * 64; q += gridDim.x * blockDim.x) {
     const int row = q / 64, k = q % 64;
@@ -550,8 +621,12 @@ __global__ void pack_bf16_kernel(PolicyNet n, uint16_t* img, float* bias) {
 
 }  // namespace
 
+int rollout_tc_kx(int in_dim) { return tc_kx(in_dim); }
+
 bool rollout_policy_bf16_supported(int in_dim, int n_act, int width) {
-  return in_dim <= 32 && n_act <= 16 && width == 64;
+  // D <= in_dim: the layout without staged tiles bounds every mode
+  return in_dim >= 1 && tc_kx(in_dim) <= kTcMaxKx && n_act <= 16 && width == 64 &&
+         tc_layout_mode(in_dim, in_dim, n_act, 0).total <= kTcSmemMax;
 }
 
 void rollout_pack_bf16(const PolicyNet& net, uint16_t* images, float* bias, cudaStream_t st) {
@@ -568,9 +643,12 @@ void rollout_policy_bf16(const PolicyNet& net, const PolicyNetBf16& nb, const Po
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
   const size_t sm = tc_layout(s.D, net.in_dim, net.n_act).total;
-  cudaFuncSetAttribute(policy_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+  const TcLayout L = tc_layout(s.D, net.in_dim, net.n_act);
+  const bool small = L.kx == 32 && L.nbuf == 2 && L.has_out;
+  auto kern = small ? policy_tc_kernel<32> : policy_tc_kernel<0>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
   int per_sm = 1;
-  cudaFuncSetAttribute(policy_tc_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   static int smem_sm = 0;
   if (smem_sm == 0) {
     int dev = 0;
@@ -586,7 +664,7 @@ void rollout_policy_bf16(const PolicyNet& net, const PolicyNetBf16& nb, const Po
   if (std::getenv("MARL_TC_DEBUG")) std::fprintf(stderr, "policy_tc: smem %zu per_sm %d\n", sm, per_sm);
   const int64_t tiles = (s.R + kTcRows - 1) / kTcRows;
   const int64_t grid = std::min<int64_t>(tiles, int64_t(sms) * per_sm);
-  policy_tc_kernel<<<unsigned(grid), kSplit * kTcRows, sm, st>>>(nb, net.in_dim, net.n_act, s, b);
+  kern<<<unsigned(grid), kSplit * kTcRows, sm, st>>>(nb, net.in_dim, net.n_act, s, b);
   ++g_launches;
 }
 

@@ -130,6 +130,9 @@ class PpoTrainer:
         n = C.c_int64()
         N.check(N.lib().marl_ppo_n_updates(self._h, C.byref(n)))
         self.n_updates = int(n.value)
+        tcu = C.c_int()
+        N.check(N.lib().marl_ppo_tensor_core_update(self._h, C.byref(tcu)))
+        self.tensor_core_update = bool(tcu.value)  # the minibatch step runs on tcgen05
         r = C.c_void_p()
         N.check(N.lib().marl_ppo_rollout(self._h, C.byref(r)))
         self.rollout = IppoRollout(venv, int(self.config.get("n_rollout_steps", 128)),

@@ -235,13 +235,19 @@ def _assert_blocks_close(g, gr, blocks, what):
         assert abs(np.linalg.norm(x) / np.linalg.norm(y) - 1) < 0.03, (what, lo, hi)
 
 
+# input widths: 18 (Kx 32), 95 (Kx 96, two X buffers), 163 (Kx 176, one X buffer), 180 (Kx 192, the widest)
+TC_SHAPES = [("MPE_simple_spread_v3", {}), ("SMAX_5m_vs_6m", THREE_M), ("SMAX_2s3z", {}), ("SMAX_5m_vs_6m", {})]
+
+
 @pytest.mark.gpu
-def test_tc_minibatch_gradient_matches_reference():
+@pytest.mark.parametrize("env_id,cfg", TC_SHAPES)
+def test_tc_minibatch_gradient_matches_reference(env_id, cfg):
     """The bf16 tensor-core step (ppo_tc.cu) vs ff_minibatch on the same buffers:
     every parameter block's gradient has cosine >= 0.995 and norm within 3 %;
     loss statistics within 2 %."""
     _need_ref()
-    tr = _trainer("MPE_simple_spread_v3", {}, 64, 32, precision="bf16")
+    tr = _trainer(env_id, cfg, 64, 32, precision="bf16")
+    assert tr.tensor_core_update
     tr.begin(O.key_from_seed(31))
     tr.collect()
     buf = {k: t.cpu().numpy() for k, t in tr.rollout._views.items()}
@@ -251,19 +257,20 @@ def test_tc_minibatch_gradient_matches_reference():
     for M in (200, 3000):
         idx = rng.choice(32 * R, size=M, replace=False).astype(np.int32)
         g, st = tr.minibatch_grad(idx)
-        gr, sr = O.ref_ff_minibatch("MPE_simple_spread_v3", {}, a, c, buf, idx)
+        gr, sr = O.ref_ff_minibatch(env_id, cfg, a, c, buf, idx)
         _assert_blocks_close(g, gr, _blocks(tr.spec), M)
         assert np.allclose(st, sr, rtol=2e-2, atol=1e-4), (st, sr)
 
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("activation", ["relu", "tanh"])
-def test_tc_minibatch_gradient_matches_fp32_path(activation):
+@pytest.mark.parametrize("env_id,cfg", TC_SHAPES[:2])
+def test_tc_minibatch_gradient_matches_fp32_path(activation, env_id, cfg):
     """bf16 tcgen05 step vs the fp32 step (itself pinned to the reference above)
     on identical buffers copied between two trainers; relu covers the other
     activation the reference supports."""
-    tc = _trainer("MPE_simple_spread_v3", {}, 64, 32, precision="bf16", activation=activation)
-    f32 = _trainer("MPE_simple_spread_v3", {}, 64, 32, precision="fp32", activation=activation)
+    tc = _trainer(env_id, cfg, 64, 32, precision="bf16", activation=activation)
+    f32 = _trainer(env_id, cfg, 64, 32, precision="fp32", activation=activation)
     key = O.key_from_seed(41)
     tc.begin(key)
     f32.begin(key)
