@@ -42,7 +42,10 @@ WORKLOADS = {
             "5 epochs x 2 minibatches of PPO), PpoConfig defaults"),
     "ppo_rnn": ("MPE_simple_spread_v3", {}, 1 << 14, "recurrent (GRU 128) IPPO training update on MPE simple_spread "
                 "(collect 128 steps + 5 epochs x 2 minibatches, BPTT), PpoConfig defaults + recurrent"),
+    "ppo_smax": ("SMAX_5m_vs_6m", THREE_M, 1 << 14, "IPPO training update on SMAX 3m (collect 128 steps + 5 epochs x "
+                 "2 minibatches of PPO; 95-wide observations), PpoConfig defaults"),
 }
+PPO_WORKLOADS = ("ppo", "ppo_rnn", "ppo_smax")
 IPPO_T = 128
 L2_FLUSH_BYTES = 512 << 20  # > 4x the 126 MB L2; its ~80 us also covers the host's enqueue of the next step
 
@@ -474,10 +477,10 @@ def run_reference_arm(args, rank, world):
         return
     threads = os.cpu_count() or 1
     n_envs = n_per_gpu * world
-    if args.workload in ("ppo", "ppo_rnn"):  # one step = one train_ippo update of a bounded sample
+    if args.workload in PPO_WORKLOADS:  # one step = one train_ippo update of a bounded sample
         sys.path.insert(0, os.path.join(ROOT, "oracle"))
         import oracle as O
-        n_cpu, t_cpu = (64, 32) if args.workload == "ppo" else (16, 32)
+        n_cpu, t_cpu = (16, 32) if args.workload == "ppo_rnn" else (64, 32)
         steps = max(1, args.steps)
         rc = {"n_envs": n_cpu, "n_rollout_steps": t_cpu, "total_timesteps": n_cpu * t_cpu * steps}
         if args.workload == "ppo_rnn":
@@ -682,7 +685,7 @@ def main():
     try:
         if args.workload == "ippo":
             run_gpu_ippo(args, rank, world, local_rank)
-        elif args.workload in ("ppo", "ppo_rnn"):
+        elif args.workload in PPO_WORKLOADS:
             run_gpu_ppo(args, rank, world, local_rank)
         else:
             run_gpu_arm(args, rank, world, local_rank)

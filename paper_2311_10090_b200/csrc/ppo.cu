@@ -130,16 +130,23 @@ __global__ void adv_sum_kernel(const float* __restrict__ adv, const float* __res
   }
 }
 
-// fold the per-block partials in block order: g[0] = sum(w * adv), g[1] = sum(w)
-__global__ void adv_fold_kernel(const double* __restrict__ part, int nb, double* __restrict__ g) {
-  if (threadIdx.x != 0) return;
+// fold the per-block partials (fixed order: thread t takes blocks t, t+256, ...,
+// then a fixed tree): g[0] = sum(w * adv), g[1] = sum(w)
+constexpr int kFoldThreads = 256;
+__global__ void __launch_bounds__(kFoldThreads) adv_fold_kernel(const double* __restrict__ part, int nb,
+                                                                double* __restrict__ g) {
+  __shared__ double sh[32];
   double s = 0.0, c = 0.0;
-  for (int q = 0; q < nb; ++q) {
+  for (int q = threadIdx.x; q < nb; q += kFoldThreads) {
     s += part[2 * q];
     c += part[2 * q + 1];
   }
-  g[0] = s;
-  g[1] = c;
+  s = block_sum(s, sh);
+  c = block_sum(c, sh);
+  if (threadIdx.x == 0) {
+    g[0] = s;
+    g[1] = c;
+  }
 }
 
 // pass 2: sum(w * (adv - mean)^2) (actor_critic.hpp:424-429) with the
@@ -159,11 +166,13 @@ __global__ void adv_var_kernel(const float* __restrict__ adv, const float* __res
   if (threadIdx.x == 0) part2[blockIdx.x] = v;
 }
 
-__global__ void adv_fold2_kernel(const double* __restrict__ part2, int nb, double* __restrict__ g) {
-  if (threadIdx.x != 0) return;
+__global__ void __launch_bounds__(kFoldThreads) adv_fold2_kernel(const double* __restrict__ part2, int nb,
+                                                                 double* __restrict__ g) {
+  __shared__ double sh[32];
   double v = 0.0;
-  for (int q = 0; q < nb; ++q) v += part2[q];
-  g[2] = v;
+  for (int q = threadIdx.x; q < nb; q += kFoldThreads) v += part2[q];
+  v = block_sum(v, sh);
+  if (threadIdx.x == 0) g[2] = v;
 }
 
 __global__ void adv_final_kernel(const double* __restrict__ g, PpoMbStats* st) {
@@ -189,12 +198,22 @@ struct NonNegative {
 };
 
 // sum the per-CTA loss statistics into row 0 (the sharded path all-reduces that row)
-__global__ void stats_fold_kernel(double* __restrict__ sp, int nparts) {
-  const int k = threadIdx.x;
-  if (k >= 6) return;
+// Column `col` of n per-CTA stat rows summed by one warp: lane-strided, then a
+// fixed shuffle tree (valid on lane 0).  clip_adam_kernel folds with the same
+// order, so folding first (the data-parallel path) changes nothing at one rank.
+__device__ __forceinline__ double warp_fold_col(const double* __restrict__ src, int n, int col) {
+  const int lane = threadIdx.x & 31;
   double v = 0.0;
-  for (int c = 0; c < nparts; ++c) v += sp[size_t(c) * 6 + k];
-  sp[k] = v;  // thread k owns column k
+  for (int c = lane; c < n; c += 32) v += src[size_t(c) * 6 + col];
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__global__ void stats_fold_kernel(double* __restrict__ sp, int nparts) {
+  const int k = threadIdx.x >> 5;  // warp k owns column k
+  if (k >= 6) return;
+  const double v = warp_fold_col(sp, nparts, k);
+  if ((threadIdx.x & 31) == 0) sp[k] = v;
 }
 
 // ----------------------------------------------------------- branch kernel
@@ -878,13 +897,22 @@ __global__ void __launch_bounds__(1024) clip_adam_kernel(PpoApplyArgs a) {
   __shared__ float s_scale;
   __shared__ int s_clip;
   const int t = threadIdx.x;
+  __shared__ double s_st[kStats + 1];
   if (*a.diverged) return;  // an earlier minibatch threw: the update is being rolled back
+  // the per-CTA loss sums: warp k < 6 folds actor column k, warp 6 the critic's v term
+  // (lane-strided, then a fixed shuffle tree)
+  if ((t >> 5) <= kStats) {
+    const int k = t >> 5;
+    const bool cr = k == kStats;
+    const double v = warp_fold_col(cr ? a.critic_stats : a.actor_stats, cr ? a.n_critic_parts : a.n_actor_parts,
+                                   cr ? 1 : k);
+    if ((t & 31) == 0) s_st[k] = v;
+  }
+  __syncthreads();
   if (t == 0) {
-    double st[kStats] = {0, 0, 0, 0, 0, 0};
-    for (int c = 0; c < a.n_actor_parts; ++c)
-      for (int k = 0; k < kStats; ++k) st[k] += a.actor_stats[size_t(c) * kStats + k];
-    double vt = 0.0;
-    for (int c = 0; c < a.n_critic_parts; ++c) vt += a.critic_stats[size_t(c) * kStats + 1];
+    double st[kStats];
+    for (int k = 0; k < kStats; ++k) st[k] = s_st[k];
+    const double vt = s_st[kStats];
     const double tw = a.st->total_w;
     double* m = a.metrics;
     if (tw > 0.0) {
@@ -1003,10 +1031,10 @@ void ppo_adv_stats(const RolloutBufs& b, const int32_t* idx, int64_t M, double* 
                    PpoMbStats* st, cudaStream_t s, const std::function<void(double*, int)>& allreduce) {
   const int nb = ppo_stat_blocks(M);
   adv_sum_kernel<<<nb, kRedThreads, 0, s>>>(b.adv, b.active, idx, M, part);
-  adv_fold_kernel<<<1, 32, 0, s>>>(part, nb, g);
+  adv_fold_kernel<<<1, kFoldThreads, 0, s>>>(part, nb, g);
   if (allreduce) allreduce(g, 2);
   adv_var_kernel<<<nb, kRedThreads, 0, s>>>(b.adv, b.active, idx, M, g, part2);
-  adv_fold2_kernel<<<1, 32, 0, s>>>(part2, nb, g);
+  adv_fold2_kernel<<<1, kFoldThreads, 0, s>>>(part2, nb, g);
   if (allreduce) allreduce(g + 2, 1);
   adv_final_kernel<<<1, 32, 0, s>>>(g, st);
   g_launches += 6;
@@ -1028,7 +1056,7 @@ void ppo_shard_compact(const int32_t* idx, int64_t M, int64_t Rg, int64_t row0, 
 }
 
 void ppo_stats_fold(double* spart, int nparts, cudaStream_t s) {
-  stats_fold_kernel<<<1, 32, 0, s>>>(spart, nparts);
+  stats_fold_kernel<<<1, 6 * 32, 0, s>>>(spart, nparts);
   ++g_launches;
 }
 

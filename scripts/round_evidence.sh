@@ -10,9 +10,11 @@ for w in smax3m mpe mpe_large overcooked smax2s3z smax27m ippo; do
 done
 timeout 600 python bench.py --workload ppo --steps 10 --warmup 3 2>/dev/null | grep '^{' >> gpurun_out/bench_${TAG}.jsonl
 timeout 600 python bench.py --workload ppo_rnn --steps 3 --warmup 3 2>/dev/null | grep '^{' >> gpurun_out/bench_${TAG}.jsonl
+timeout 600 python bench.py --workload ppo_smax --steps 10 --warmup 3 2>/dev/null | grep '^{' >> gpurun_out/bench_${TAG}.jsonl
 timeout 300 python bench.py --impl reference --workload smax3m --steps 3 --warmup 1 2>/dev/null | grep '^{' >> gpurun_out/bench_${TAG}.jsonl
 timeout 300 python bench.py --impl reference --workload ppo --steps 2 --warmup 3 2>/dev/null | grep '^{' >> gpurun_out/bench_${TAG}.jsonl
 timeout 300 python bench.py --impl reference --workload ppo_rnn --steps 1 --warmup 3 2>/dev/null | grep '^{' >> gpurun_out/bench_${TAG}.jsonl
+timeout 300 python bench.py --impl reference --workload ppo_smax --steps 1 --warmup 3 2>/dev/null | grep '^{' >> gpurun_out/bench_${TAG}.jsonl
 wc -l gpurun_out/bench_${TAG}.jsonl
 NCU=/usr/local/cuda/bin/ncu
 for w in smax3m mpe_large overcooked smax27m; do
@@ -27,4 +29,9 @@ done
 bash scripts/prof_ippo.sh ${TAG} > /dev/null 2>&1
 timeout 600 $NCU --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_${TAG}_ppo.csv \
   python bench.py --workload ppo --steps 1 --warmup 3 --no-cpu > /dev/null 2>&1
+timeout 600 $NCU --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_${TAG}_ppo_smax.csv \
+  python bench.py --workload ppo_smax --steps 1 --warmup 3 --no-cpu > /dev/null 2>&1
+timeout 900 $NCU --set full --clock-control none --import-source on -k regex:ppo_update_tc -s 20 -c 1 \
+  -o gpurun_out/prof_${TAG}_ppo_smax_update -f python bench.py --workload ppo_smax --steps 1 --warmup 3 --no-cpu --no-e2e \
+  > /dev/null 2>&1
 ls gpurun_out | grep ${TAG}
