@@ -354,18 +354,34 @@ struct PpoTcArgs {
   double *spart_a, *spart_c;    // [grid][6]
   const int32_t* idx;
   int64_t M;
-  const uint16_t* obs_bf;  // [T*R][kx] bf16 rows (ppo_obs_bf16)
-  const int32_t* actions;
-  const float *old_logp, *adv, *vtarg, *old_value, *active;
-  const uint8_t* legal;
+  const uint16_t* obs_bf;     // [T*R][kx] bf16 rows (ppo_tc_pack)
+  const struct PpoRowRec* rec;  // [T*R] loss-input records (ppo_tc_pack)
   const PpoMbStats* st;
   int* err;
   int in, kx, n_act, relu;
   double clip_eps, ent_coef, vf_coef;
 };
 int ppo_tc_kx(int in_dim);  // round16(in + 1): the bf16 row width incl. the bias column
-// the rollout observations as bf16 rows of kx (column kx-1 = 1), once per update
-void ppo_obs_bf16(const float* obs, int64_t rows, int in, int kx, uint16_t* out, cudaStream_t s);
+// One slot's loss inputs for the tcgen05 step (32 bytes, one gather per row).
+struct PpoRowRec {
+  float active, adv, logp, vtarg, value;
+  int32_t action;
+  uint32_t legal;  // bit j: action j legal (n_act <= 16)
+  uint32_t pad;
+};
+struct PpoTcPack {
+  const float* obs;  // [rows][in]
+  const float *active, *adv, *old_logp, *vtarg, *old_value;
+  const int32_t* actions;
+  const uint8_t* legal;  // [rows][n_act]
+  int64_t rows;
+  int in, kx, n_act;
+  uint16_t* obs_bf;  // [rows][kx]
+  PpoRowRec* rec;    // [rows]
+};
+// the window's rows for the tcgen05 step (bf16 observations, column kx-1 = 1,
+// and the loss-input records), once per update
+void ppo_tc_pack(const PpoTcPack& p, cudaStream_t s);
 bool ppo_tc_supported(int in_dim, int critic_in, int width, int n_act);
 int ppo_tc_grid(int64_t M);
 void ppo_update_tc(const PpoTcArgs& a, int grid, cudaStream_t s);

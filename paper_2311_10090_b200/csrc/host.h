@@ -260,7 +260,8 @@ struct marl_ppo {
   Arena arena;
   int P = 0, Pa = 0, Pc = 0, grid_a = 0, grid_c = 0;
   bool tc = false;  // minibatch step on tcgen05 (bf16 precision, IPPO width 64, input <= 191)
-  uint16_t* obs_bf = nullptr;  // [T*R][kx] bf16 observation rows of the window (tcgen05 step)
+  uint16_t* obs_bf = nullptr;      // [T*R][kx] bf16 observation rows of the window (tcgen05 step)
+  PpoRowRec* rows_rec = nullptr;   // [T*R] their loss-input records
   float *m = nullptr, *v = nullptr, *grad = nullptr, *snapshot = nullptr, *gpart_a = nullptr, *gpart_c = nullptr;
   double *spart_a = nullptr, *spart_c = nullptr, *adv_part = nullptr, *adv_part2 = nullptr, *metrics = nullptr;
   PpoMbStats* mbst = nullptr;

@@ -356,13 +356,7 @@ void minibatch_grad(marl_ppo* p, const int32_t* idx, int64_t M, bool global = fa
     a.idx = idx;
     a.M = M;
     a.obs_bf = p->obs_bf;
-    a.actions = r->b.actions;
-    a.old_logp = r->b.logp;
-    a.adv = r->b.adv;
-    a.vtarg = r->b.vtarg;
-    a.old_value = r->b.value;
-    a.active = r->b.active;
-    a.legal = r->b.legal;
+    a.rec = p->rows_rec;
     a.st = p->mbst;
     a.err = p->flags + 1;
     a.in = r->in_dim;
@@ -613,7 +607,22 @@ void ppo_collect_impl(marl_ppo* p) {
 void tc_obs(marl_ppo* p) {
   if (!p->tc) return;
   const marl_rollout* r = p->ro;
-  ppo_obs_bf16(r->b.obs, int64_t(r->T) * r->R, r->in_dim, ppo_tc_kx(r->in_dim), p->obs_bf, p->h->stream);
+  PpoTcPack k{};
+  k.obs = r->b.obs;
+  k.active = r->b.active;
+  k.adv = r->b.adv;
+  k.old_logp = r->b.logp;
+  k.vtarg = r->b.vtarg;
+  k.old_value = r->b.value;
+  k.actions = r->b.actions;
+  k.legal = r->b.legal;
+  k.rows = int64_t(r->T) * r->R;
+  k.in = r->in_dim;
+  k.kx = ppo_tc_kx(r->in_dim);
+  k.n_act = r->n_act;
+  k.obs_bf = p->obs_bf;
+  k.rec = p->rows_rec;
+  ppo_tc_pack(k, p->h->stream);
   after_launch();
 }
 
@@ -790,7 +799,10 @@ int marl_ppo_create(marl_venv* h, const char* ppo_config_json, int centralized, 
     ar.add(&p->perm_scratch, p->perm_scratch_bytes);
     ar.add(&p->flags, 2);
     ar.add(&p->adv_g, 4);
-    if (p->tc) ar.add(&p->obs_bf, size_t(r->T) * size_t(r->R) * size_t(ppo_tc_kx(r->in_dim)));
+    if (p->tc) {
+      ar.add(&p->obs_bf, size_t(r->T) * size_t(r->R) * size_t(ppo_tc_kx(r->in_dim)));
+      ar.add(&p->rows_rec, size_t(r->T) * size_t(r->R));
+    }
     ar.add(&p->ep_dev, 3);
     if (p->sharded) {
       p->cmp_scratch_bytes = ppo_compact_scratch_bytes(p->per);

@@ -4,8 +4,9 @@
 // <= 16 actions, actor and critic in one persistent kernel, one CTA (256
 // threads, all 512 TMEM columns) per SM, 128 gathered rows per tile.  The
 // input rows are a bf16 copy of the rollout observations made once per update
-// (ppo_obs_bf16), Kx = round16(in + 1) wide with the constant 1 in column
-// Kx-1, gathered into the canonical operand tile by 16-byte cp.async:
+// (ppo_tc_pack), Kx = round16(in + 1) wide with the constant 1 in column
+// Kx-1, gathered into the canonical operand tile by 16-byte cp.async, and
+// its loss inputs packed into one 32-byte record per row:
 //
 //   F1  D[0:128)   = X[128xKx] . [W1a ; W1c]^T                 forward
 //   F2  D[0:64)    = H1a . W2a^T,  D[64:128) = H1c . W2c^T
@@ -52,7 +53,7 @@ constexpr int kSmemMax = 232448;  // 227 KB opt-in per CTA
 constexpr int kStat = 6;
 
 struct UpdLayout {
-  uint32_t w1, w2a, w2c, w3a, w3c, x, ha, hb, dl, st_f, st_i, st_l, slot, bias, gb3w, bar, bar_g, tmem_slot, total;
+  uint32_t w1, w2a, w2c, w3a, w3c, x, ha, hb, dl, st_r, slot, bias, gb3w, bar, bar_g, tmem_slot, total;
   int nx;  // X buffers (2: the next tile's rows land while this one computes)
 };
 
@@ -77,9 +78,7 @@ __host__ __device__ inline UpdLayout upd_layout(int kx, int nx) {
   L.ha = take(kRows * 128 * 2, 128);  // H1, then dZ1
   L.hb = take(kRows * 128 * 2, 128);  // H2, then dZ2
   L.dl = take(kRows * 32 * 2, 128);
-  L.st_f = take(kRows * 5 * 4, 16);  // active, adv, old logp, vtarg, old value
-  L.st_i = take(kRows * 4, 16);      // action
-  L.st_l = take(kRows * 5 * 4, 16);  // legal words
+  L.st_r = take(kRows * sizeof(PpoRowRec), 16);  // the tile's loss-input records
   L.slot = take(3 * kRows * 4, 16);
   L.bias = take((4 * 64 + 2 * 16) * 4, 16);
   L.gb3w = take(8 * 32 * 4, 16);
@@ -131,25 +130,42 @@ __device__ __forceinline__ uint16_t bf16_bits(float v) {
   return *reinterpret_cast<const uint16_t*>(&h);
 }
 
-// rows x in fp32 -> rows x kx bf16, column kx-1 = 1 (the bias column), zero padding between
-__global__ void obs_bf16_kernel(const float* __restrict__ obs, int64_t rows, int in, int kx, uint4* __restrict__ out) {
-  const int chunks = kx / 8;
-  const int64_t n = rows * chunks;
-  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n; e += int64_t(gridDim.x) * blockDim.x) {
+// Once per update, for every slot of the window: the observation row as bf16
+// [kx] (column kx-1 = 1, the bias column; zero padding between) and the
+// row's loss inputs as one 32-byte record (legal actions as a bit mask).
+__global__ void pack_rows_kernel(PpoTcPack p) {
+  const int chunks = p.kx / 8;
+  const int64_t n = p.rows * chunks;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < n; e += stride) {
     const int64_t r = e / chunks;
     const int c0 = int(e - r * chunks) * 8;
     float v[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       const int k = c0 + j;
-      v[j] = k < in ? __ldg(obs + r * in + k) : (k == kx - 1 ? 1.0f : 0.0f);
+      v[j] = k < p.in ? __ldg(p.obs + r * p.in + k) : (k == p.kx - 1 ? 1.0f : 0.0f);
     }
     uint4 q;
     q.x = pack_bf16(v[0], v[1]);
     q.y = pack_bf16(v[2], v[3]);
     q.z = pack_bf16(v[4], v[5]);
     q.w = pack_bf16(v[6], v[7]);
-    out[e] = q;
+    reinterpret_cast<uint4*>(p.obs_bf)[e] = q;
+  }
+  for (int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; r < p.rows; r += stride) {
+    PpoRowRec rec;
+    rec.active = __ldg(p.active + r);
+    rec.adv = __ldg(p.adv + r);
+    rec.logp = __ldg(p.old_logp + r);
+    rec.vtarg = __ldg(p.vtarg + r);
+    rec.value = __ldg(p.old_value + r);
+    rec.action = __ldg(p.actions + r);
+    uint32_t m = 0;
+    for (int j = 0; j < p.n_act; ++j) m |= (__ldg(p.legal + r * p.n_act + j) ? 1u : 0u) << j;
+    rec.legal = m;
+    rec.pad = 0;
+    p.rec[r] = rec;
   }
 }
 
@@ -160,9 +176,7 @@ __global__ void __launch_bounds__(kThr, 1) ppo_update_tc_kernel(PpoTcArgs a) {
   uint8_t* base = smem_raw;
   uint8_t *w1 = base + L.w1, *w2a = base + L.w2a, *w2c = base + L.w2c, *w3a = base + L.w3a, *w3c = base + L.w3c,
           *xb = base + L.x, *ha = base + L.ha, *hb = base + L.hb, *sdl = base + L.dl;
-  float* st_f = reinterpret_cast<float*>(base + L.st_f);
-  int32_t* st_i = reinterpret_cast<int32_t*>(base + L.st_i);
-  uint32_t* st_l = reinterpret_cast<uint32_t*>(base + L.st_l);
+  PpoRowRec* st_r = reinterpret_cast<PpoRowRec*>(base + L.st_r);
   int32_t* slot = reinterpret_cast<int32_t*>(base + L.slot);
   float* bias = reinterpret_cast<float*>(base + L.bias);
   float* gb3w = reinterpret_cast<float*>(base + L.gb3w);
@@ -242,16 +256,9 @@ __global__ void __launch_bounds__(kThr, 1) ppo_update_tc_kernel(PpoTcArgs a) {
       const int sl = slot_ok(tile, t) ? slot[sb * kRows + t] : -1;
       const int n = sl >= 0 ? 4 : 0;
       const int64_t q = sl >= 0 ? sl : 0;
-      cpa4(st_f + 0 * kRows + t, a.active + q, n);
-      cpa4(st_f + 1 * kRows + t, a.adv + q, n);
-      cpa4(st_f + 2 * kRows + t, a.old_logp + q, n);
-      cpa4(st_f + 3 * kRows + t, a.vtarg + q, n);
-      cpa4(st_f + 4 * kRows + t, a.old_value + q, n);
-      cpa4(st_i + t, a.actions + q, n);
-      const int64_t b0 = q * NA, w0 = b0 & ~int64_t(3);
-      const int nw = int(((b0 & 3) + NA + 3) / 4);
-#pragma unroll
-      for (int w = 0; w < 5; ++w) cpa4(st_l + w * kRows + t, a.legal + w0 + 4 * w, (n && w < nw) ? 4 : 0);
+      const uint8_t* src = reinterpret_cast<const uint8_t*>(a.rec + q);
+      cpa16(reinterpret_cast<uint8_t*>(st_r + t), src, 4 * n);
+      cpa16(reinterpret_cast<uint8_t*>(st_r + t) + 16, src + 16, 4 * n);
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
@@ -285,21 +292,20 @@ __global__ void __launch_bounds__(kThr, 1) ppo_update_tc_kernel(PpoTcArgs a) {
     const bool live = slot_ok(tile, row);
     float r_w = 0.0f, r_adv = 0.0f, r_lp = 0.0f, r_vt = 0.0f, r_v = 0.0f;
     int r_act = 0;
-    uint32_t r_lg[5] = {0, 0, 0, 0, 0};
+    uint32_t r_lg = 0;
     if (live) {
-      r_w = st_f[row];
+      const PpoRowRec& rr = st_r[row];
+      r_w = rr.active;
       if (part == 0) {
-        r_adv = st_f[kRows + row];
-        r_lp = st_f[2 * kRows + row];
-        r_act = st_i[row];
-#pragma unroll
-        for (int w = 0; w < 5; ++w) r_lg[w] = st_l[w * kRows + row];
+        r_adv = rr.adv;
+        r_lp = rr.logp;
+        r_act = rr.action;
+        r_lg = rr.legal;
       } else {
-        r_vt = st_f[3 * kRows + row];
-        r_v = st_f[4 * kRows + row];
+        r_vt = rr.vtarg;
+        r_v = rr.value;
       }
     }
-    const int64_t sl_row = slot[sb * kRows + row];
     if (t == 0) {
       tc_fence_after();
       const uint32_t id = idesc_bf16(128, 128);
@@ -371,12 +377,10 @@ __global__ void __launch_bounds__(kThr, 1) ppo_update_tc_kernel(PpoTcArgs a) {
           float z[16], lp[16];
           bool lg[16];
           float mx = -INFINITY;
-          const int b0 = int((sl_row * NA) & 3);
 #pragma unroll
           for (int j = 0; j < 16; ++j) {
             z[j] = hv[j] + bias[256 + j];
-            const int b = b0 + j;
-            lg[j] = j < NA && ((r_lg[b >> 2] >> (8 * (b & 3))) & 0xffu);
+            lg[j] = j < NA && ((r_lg >> j) & 1u);
             if (lg[j]) mx = fmaxf(mx, z[j]);
           }
           float den = 0.0f;
@@ -602,11 +606,11 @@ int ppo_tc_grid(int64_t M) {
   return int(std::max<int64_t>(1, std::min<int64_t>(tiles, sms)));
 }
 
-void ppo_obs_bf16(const float* obs, int64_t rows, int in, int kx, uint16_t* out, cudaStream_t s) {
-  const int64_t n = rows * (kx / 8);
+void ppo_tc_pack(const PpoTcPack& p, cudaStream_t s) {
+  const int64_t n = p.rows * (p.kx / 8);
   if (n <= 0) return;
   const int blocks = int(std::min<int64_t>((n + 255) / 256, 148 * 16));
-  obs_bf16_kernel<<<blocks, 256, 0, s>>>(obs, rows, in, kx, reinterpret_cast<uint4*>(out));
+  pack_rows_kernel<<<blocks, 256, 0, s>>>(p);
   ++g_launches;
 }
 
