@@ -112,12 +112,14 @@ __device__ double block_sum(double v, double* sh) {
 }
 
 // pass 1: sum(w * adv), sum(w) over the minibatch rows (actor_critic.hpp:418-421)
-__global__ void adv_sum_kernel(const float* __restrict__ adv, const float* __restrict__ active,
+// adv / active of slot r at [r * stride] (stride 1: the rollout buffer; 8: the
+// tcgen05 step's packed 32-byte records, one sector per row)
+__global__ void adv_sum_kernel(const float* __restrict__ adv, const float* __restrict__ active, int stride,
                                const int32_t* __restrict__ idx, int64_t M, double* __restrict__ part) {
   __shared__ double sh[32];
   double s = 0.0, n = 0.0;
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < M; i += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t r = idx[i];
+    const int64_t r = int64_t(idx[i]) * stride;
     const double w = double(active[r]);
     s += w * double(adv[r]);
     n += w;
@@ -151,14 +153,14 @@ __global__ void __launch_bounds__(kFoldThreads) adv_fold_kernel(const double* __
 
 // pass 2: sum(w * (adv - mean)^2) (actor_critic.hpp:424-429) with the
 // (all-reduced) mean of g
-__global__ void adv_var_kernel(const float* __restrict__ adv, const float* __restrict__ active,
+__global__ void adv_var_kernel(const float* __restrict__ adv, const float* __restrict__ active, int stride,
                                const int32_t* __restrict__ idx, int64_t M, const double* __restrict__ g,
                                double* __restrict__ part2) {
   __shared__ double sh[32];
   const double mean = g[1] > 0.0 ? g[0] / g[1] : 0.0;
   double v = 0.0;
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < M; i += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t r = idx[i];
+    const int64_t r = int64_t(idx[i]) * stride;
     const double d = double(adv[r]) - mean;
     v += double(active[r]) * d * d;
   }
@@ -1028,12 +1030,16 @@ void ppo_permutation(KeyWords key, int64_t n, int32_t* out, void* scratch, size_
 int ppo_stat_blocks(int64_t M) { return int(std::min<int64_t>(std::max<int64_t>((M + 255) / 256, 1), 1184)); }
 
 void ppo_adv_stats(const RolloutBufs& b, const int32_t* idx, int64_t M, double* part, double* part2, double* g,
-                   PpoMbStats* st, cudaStream_t s, const std::function<void(double*, int)>& allreduce) {
+                   PpoMbStats* st, cudaStream_t s, const std::function<void(double*, int)>& allreduce,
+                   const PpoRowRec* rec) {
   const int nb = ppo_stat_blocks(M);
-  adv_sum_kernel<<<nb, kRedThreads, 0, s>>>(b.adv, b.active, idx, M, part);
+  const float* adv = rec ? &rec->adv : b.adv;
+  const float* active = rec ? &rec->active : b.active;
+  const int stride = rec ? int(sizeof(PpoRowRec) / sizeof(float)) : 1;
+  adv_sum_kernel<<<nb, kRedThreads, 0, s>>>(adv, active, stride, idx, M, part);
   adv_fold_kernel<<<1, kFoldThreads, 0, s>>>(part, nb, g);
   if (allreduce) allreduce(g, 2);
-  adv_var_kernel<<<nb, kRedThreads, 0, s>>>(b.adv, b.active, idx, M, g, part2);
+  adv_var_kernel<<<nb, kRedThreads, 0, s>>>(adv, active, stride, idx, M, g, part2);
   adv_fold2_kernel<<<1, kFoldThreads, 0, s>>>(part2, nb, g);
   if (allreduce) allreduce(g + 2, 1);
   adv_final_kernel<<<1, 32, 0, s>>>(g, st);

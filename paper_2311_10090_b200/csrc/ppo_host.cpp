@@ -343,7 +343,8 @@ void minibatch_grad(marl_ppo* p, const int32_t* idx, int64_t M, bool global = fa
   }
   std::function<void(double*, int)> red;
   if (p->hook) red = [p](double* g, int n) { allreduce(p, g, n, MARL_DTYPE_F64); };
-  ppo_adv_stats(p->ro->b, idx, M, p->adv_part, p->adv_part2, p->adv_g, p->mbst, st, red);
+  ppo_adv_stats(p->ro->b, idx, M, p->adv_part, p->adv_part2, p->adv_g, p->mbst, st, red,
+                p->tc ? p->rows_rec : nullptr);
   if (p->tc) {
     const marl_rollout* r = p->ro;
     PpoTcArgs a{};
