@@ -34,4 +34,7 @@ timeout 600 $NCU --metrics gpu__time_duration.sum --clock-control none --csv --l
 timeout 900 $NCU --set full --clock-control none --import-source on -k regex:ppo_update_tc -s 20 -c 1 \
   -o gpurun_out/prof_${TAG}_ppo_smax_update -f python bench.py --workload ppo_smax --steps 1 --warmup 3 --no-cpu --no-e2e \
   > /dev/null 2>&1
+timeout 900 $NCU --set full --clock-control none --import-source on -k regex:ppo_update_tc -s 20 -c 1 \
+  -o gpurun_out/prof_${TAG}_ppo_update -f python bench.py --workload ppo --steps 1 --warmup 3 --no-cpu --no-e2e \
+  > /dev/null 2>&1
 ls gpurun_out | grep ${TAG}
