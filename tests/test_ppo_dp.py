@@ -9,7 +9,8 @@ tests/test_ppo.py) up to float summation order.
 
 * GPU: two ranks emulated by two threads on one B200, exchanging through a
   pairwise-sum hook -- vs the unsharded trainer: step / update / n_episodes /
-  lr exact, losses and final parameters within 1e-3 relative.
+  lr exact, losses and final parameters within 1e-3 relative (fp32; 1e-2 for
+  the bf16 tcgen05 step).
 * GPU: the native NCCL exchange at world size 1 is the identity: bitwise the
   unsharded, hook-free run.
 * CPU (gloo, 2 processes): the torch.distributed hook sums in place.
@@ -59,18 +60,22 @@ def _close(x, y, rel=1e-3, absf=1e-4):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
 @pytest.mark.parametrize("env_id,cfg,n,T", [("MPE_simple_spread_v3", {}, 64, 16),
                                             ("SMAX_5m_vs_6m", {"ally_units": ["marine"] * 3,
                                                                "enemy_units": ["marine"] * 3}, 32, 32)])
-def test_two_rank_update_matches_single_device(env_id, cfg, n, T):
+def test_two_rank_update_matches_single_device(env_id, cfg, n, T, precision):
+    """fp32: the CUDA-core minibatch kernels; bf16: the tcgen05 step over each
+    shard's packed rows (the sharded minibatch is compacted to local slots)."""
     import paper_2311_10090_b200 as m
     from paper_2311_10090_b200 import dist as D
     env = m.make_env(env_id, cfg)
     key = O.key_from_seed(12)
-    single = _trainer(m.VectorEnv(env, n, device=0), n, T).train(key)
+    single = _trainer(m.VectorEnv(env, n, device=0), n, T, precision).train(key)
 
     pair = _PairSum()
-    trainers = [_trainer(D.make_sharded(env, n, r, 2, device=0), n, T) for r in range(2)]
+    trainers = [_trainer(D.make_sharded(env, n, r, 2, device=0), n, T, precision) for r in range(2)]
+    assert all(tr.tensor_core_update == (precision == "bf16") for tr in trainers)
     for r, tr in enumerate(trainers):
         tr.set_allreduce(pair.hook(r))
     out, err = [None, None], []
@@ -97,9 +102,12 @@ def test_two_rank_update_matches_single_device(env_id, cfg, n, T):
     for col in (0, 1, 3, 11):  # step, update, n_episodes, lr
         assert np.array_equal(m1[:, col], m2[:, col]), col
     assert np.allclose(m2[:, 2], m1[:, 2], rtol=1e-5, atol=1e-5)
+    # bf16 operands turn the float reassociation of the sharded sums into occasional
+    # rounding flips from the second update on: a 1e-2 bar there, 1e-3 for fp32
+    rel = 1e-3 if precision == "fp32" else 1e-2
     for col in range(4, 11):
-        assert np.allclose(m2[:, col], m1[:, col], rtol=1e-3, atol=1e-5), (col, m2[:, col], m1[:, col])
-    assert _close(a.actor, single.actor) and _close(a.critic, single.critic)
+        assert np.allclose(m2[:, col], m1[:, col], rtol=rel, atol=1e-5), (col, m2[:, col], m1[:, col])
+    assert _close(a.actor, single.actor, rel) and _close(a.critic, single.critic, rel)
 
 
 @pytest.mark.gpu
