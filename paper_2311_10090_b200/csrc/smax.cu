@@ -76,13 +76,16 @@ struct Params {
 static_assert(sizeof(Params) % 16 == 0, "Params is staged with 16-byte copies");
 
 // One env's unit state during a step (shared memory).
-template <int CAP>
+// HT >= 0: every unit of the roster has type HT (fixed single-type rosters such
+// as 3m / 5m_vs_6m / 27m_vs_30m): type lookups fold to compile-time constants.
+template <int CAP, int HT = -1>
 struct EnvSm {
   double x[CAP], y[CAP], h[CAP], cd[CAP];
   int act[CAP];
   int8_t pa[CAP];
   int8_t fire[CAP];
   int8_t ty[CAP];  // unit types of this env (the roster, or smacv2's per-episode draw)
+  __device__ __forceinline__ int T(int u) const { return HT >= 0 ? HT : int(ty[u]); }
 };
 
 // A group of G lanes of one warp (G need not be a power of two: a warp holds
@@ -112,15 +115,15 @@ __device__ __forceinline__ double dclamp(double v, double lo, double hi) {  // s
   return (v < lo) ? lo : (hi < v) ? hi : v;
 }
 
-template <int CAP>
-__device__ __forceinline__ bool in_range(const Params& P, const EnvSm<CAP>& e, int a, int b) {
-  const Thresh& r = P.ps[e.ty[a]][e.ty[b]].reach;  // smax.cpp:497-501
+template <int CAP, int HT>
+__device__ __forceinline__ bool in_range(const Params& P, const EnvSm<CAP, HT>& e, int a, int b) {
+  const Thresh& r = P.ps[e.T(a)][e.T(b)].reach;  // smax.cpp:497-501
   return dist_le(e.x[a] - e.x[b], e.y[a] - e.y[b], r.r, r.r2lo, r.r2hi);
 }
 
-template <int CAP>
-__device__ __forceinline__ bool sees(const Params& P, const EnvSm<CAP>& e, int a, int b) {
-  const Thresh& r = P.ts[e.ty[a]].sight;  // center_dist(a, b) <= sight(a), smax.cpp:383,613
+template <int CAP, int HT>
+__device__ __forceinline__ bool sees(const Params& P, const EnvSm<CAP, HT>& e, int a, int b) {
+  const Thresh& r = P.ts[e.T(a)].sight;  // center_dist(a, b) <= sight(a), smax.cpp:383,613
   return dist_le(e.x[a] - e.x[b], e.y[a] - e.y[b], r.r, r.r2lo, r.r2hi);
 }
 
@@ -172,14 +175,14 @@ __device__ __forceinline__ unsigned long long unit_mask(const Grp<G>& g, const b
 // the lowest hit by ballot, lets b's lane apply the reference push, and
 // repeats from there: rounds per row = pushes in the row + 1, and the
 // trajectory is the sequential one bit for bit.
-template <int G, int UPL, int CAP>
-__device__ __forceinline__ void separation_pass(const Params& P, EnvSm<CAP>& e, const Grp<G>& g,
+template <int G, int UPL, int CAP, int HT>
+__device__ __forceinline__ void separation_pass(const Params& P, EnvSm<CAP, HT>& e, const Grp<G>& g,
                                                 unsigned long long alive) {
   const int n = P.n;
   for (int a = 0; a < n - 1; ++a) {
     if (!(alive >> a & 1ull)) continue;
     unsigned long long row = alive & bits_above(a);
-    const int ta = e.ty[a];
+    const int ta = e.T(a);
     while (row) {  // group-uniform
       bool hit[UPL];
       double hdx[UPL], hdy[UPL], hd[UPL];
@@ -191,7 +194,7 @@ __device__ __forceinline__ void separation_pass(const Params& P, EnvSm<CAP>& e, 
         hdx[j] = hdy[j] = hd[j] = 0.0;
         if (!(row >> b & 1ull)) continue;
         const double dx = e.x[b] - xa, dy = e.y[b] - ya;
-        const Thresh& R = P.ps[ta][e.ty[b]].rsum;
+        const Thresh& R = P.ps[ta][e.T(b)].rsum;
         if (dx * dx + dy * dy > R.r2hi) continue;  // hypot(dx,dy) > ra+rb: overlap <= 0
         const double dd = hypot_glibc(dx, dy);
         hit[j] = R.r - dd > 0.0;
@@ -212,7 +215,7 @@ __device__ __forceinline__ void separation_pass(const Params& P, EnvSm<CAP>& e, 
             dy = hdy[q];
             dd = hd[q];
           }
-        const double overlap = P.ps[ta][e.ty[b]].rsum.r - dd;
+        const double overlap = P.ps[ta][e.T(b)].rsum.r - dd;
         double nx = 1.0, ny = 0.0;  // coincident centres get a fixed nudge axis
         if (dd > 1e-12) {
           nx = dx / dd;
@@ -220,7 +223,7 @@ __device__ __forceinline__ void separation_pass(const Params& P, EnvSm<CAP>& e, 
         }
         const double push = 0.5 * overlap;
         const TypeStat& A_ = P.ts[ta];
-        const TypeStat& B_ = P.ts[e.ty[b]];
+        const TypeStat& B_ = P.ts[e.T(b)];
         e.x[a] = dclamp(xa - nx * push, A_.rad, A_.hi);
         e.y[a] = dclamp(ya - ny * push, A_.rad, A_.hi);
         e.x[b] = dclamp(e.x[b] + nx * push, B_.rad, B_.hi);
@@ -266,27 +269,27 @@ __device__ __forceinline__ bool for_lane_pairs(const LanePairs<G>& lp, int gl, i
 // Does any living pair of this lane's share overlap right now (the exact
 // reference test, hypot only inside the rounding band)?  If no pair overlaps
 // at the start of a pass, the pass pushes nothing -- so it is skipped.
-template <int G, int CAP>
-__device__ __forceinline__ bool lane_pairs_overlap(const Params& P, const EnvSm<CAP>& e, const LanePairs<G>& lp,
+template <int G, int CAP, int HT>
+__device__ __forceinline__ bool lane_pairs_overlap(const Params& P, const EnvSm<CAP, HT>& e, const LanePairs<G>& lp,
                                                    int gl) {
   return for_lane_pairs<G>(lp, gl, P.n, [&](int a, int b) {
     if (e.h[a] <= 0.0 || e.h[b] <= 0.0) return false;
     const double dx = e.x[b] - e.x[a], dy = e.y[b] - e.y[a];
     const double d2 = dx * dx + dy * dy;
     if (d2 > P.sep_r2hi) return false;  // farther than any radius sum
-    const Thresh& R = P.ps[e.ty[a]][e.ty[b]].rsum;
+    const Thresh& R = P.ps[e.T(a)][e.T(b)].rsum;
     if (d2 > R.r2hi) return false;
     return d2 < R.r2lo || R.r - hypot_glibc(dx, dy) > 0.0;
   });
 }
 
 // max_overlap(s) <= kSeparationTol restricted to this lane's pairs (smax.cpp:569-580).
-template <int G, int CAP>
-__device__ __forceinline__ bool lane_pairs_within_tol(const Params& P, const EnvSm<CAP>& e, const LanePairs<G>& lp,
+template <int G, int CAP, int HT>
+__device__ __forceinline__ bool lane_pairs_within_tol(const Params& P, const EnvSm<CAP, HT>& e, const LanePairs<G>& lp,
                                                       int gl) {
   return !for_lane_pairs<G>(lp, gl, P.n, [&](int a, int b) {
     if (e.h[a] <= 0.0 || e.h[b] <= 0.0) return false;
-    const PairStat& S = P.ps[e.ty[a]][e.ty[b]];
+    const PairStat& S = P.ps[e.T(a)][e.T(b)];
     const double dx = e.x[a] - e.x[b], dy = e.y[a] - e.y[b];
     const double d2 = dx * dx + dy * dy;
     if (d2 > S.otol.r2hi) return false;      // surely sum - d <= tol
@@ -298,8 +301,8 @@ __device__ __forceinline__ bool lane_pairs_within_tol(const Params& P, const Env
 // separate(s, to_fixpoint), smax.cpp:542-567.  A pass is a no-op exactly when
 // no living pair overlaps, which the parallel pre-check proves in the common
 // case (and then max_overlap <= 0 <= tol ends the fixpoint loop as well).
-template <int G, int UPL, int CAP>
-__device__ __forceinline__ void separate(const Params& P, EnvSm<CAP>& e, const Grp<G>& g, const LanePairs<G>& lp,
+template <int G, int UPL, int CAP, int HT>
+__device__ __forceinline__ void separate(const Params& P, EnvSm<CAP, HT>& e, const Grp<G>& g, const LanePairs<G>& lp,
                                          bool fixpoint) {
   unsigned long long alive = 0;
   for (int pass = 0; pass < (fixpoint ? 256 : 1); ++pass) {
@@ -326,7 +329,7 @@ __device__ __forceinline__ double uniform_at_nl(const Key& k, double lo, double 
 
 // Spawn of unit u: spawn_clusters / place_jittered (smax.cpp:448-454,481-492),
 // or spawn_smacv2 (smax.cpp:456-479) for the random-type scenarios; the
-// unit's type (e.ty[u]) is already set.
+// unit's type (e.T(u)) is already set.
 __device__ __forceinline__ void place_at(double bx, double by, double rad, double hi, double* x, double* y) {
   *x = dclamp(bx, rad, hi);  // place (smax.cpp:481-485)
   *y = dclamp(by, rad, hi);
@@ -334,11 +337,11 @@ __device__ __forceinline__ void place_at(double bx, double by, double rad, doubl
 
 // spawn_smacv2 (smax.cpp:456-479) for unit u: kept out of line (rare, and
 // the fixed-roster step kernel's instruction footprint stays as it was).
-template <int CAP>
-__device__ __noinline__ void spawn_smacv2(const Params& P, EnvSm<CAP>& e, int u, const Key& key) {
+template <int CAP, int HT>
+__device__ __noinline__ void spawn_smacv2(const Params& P, EnvSm<CAP, HT>& e, int u, const Key& key) {
   const bool ally = u < P.na;
   const int i = ally ? u : u - P.na;
-  const TypeStat& t = P.ts[e.ty[u]];
+  const TypeStat& t = P.ts[e.T(u)];
   if (to_unit(block_at_nl(fold_in_nl(key, 1), 0)) < 0.5) {
     // reflected uniform spawns: enemy i mirrors ally i's draws
     const double ax = uniform_at_nl(fold_in_nl(key, 1000 + 2 * uint64_t(i)), 0.1 * P.map, 0.4 * P.map);
@@ -362,9 +365,9 @@ __device__ __noinline__ void spawn_smacv2(const Params& P, EnvSm<CAP>& e, int u,
   }
 }
 
-template <int CAP>
-__device__ __forceinline__ void spawn_unit(const Params& P, EnvSm<CAP>& e, int u, const Key& key) {
-  const TypeStat& t = P.ts[e.ty[u]];
+template <int CAP, int HT>
+__device__ __forceinline__ void spawn_unit(const Params& P, EnvSm<CAP, HT>& e, int u, const Key& key) {
+  const TypeStat& t = P.ts[e.T(u)];
   if (P.random_types) {
     spawn_smacv2(P, e, u, key);
   } else {
@@ -386,8 +389,8 @@ __device__ __forceinline__ void spawn_unit(const Params& P, EnvSm<CAP>& e, int u
 // The pick-th legal action of unit u (smax.cpp:195-211 with legal_uniform,
 // vector_env.cpp:21-32).  Legal order: moves 0-3, stop, attacks on living
 // opponents in range; a dead unit's only legal action is stop.
-template <int CAP>
-__device__ __forceinline__ int random_legal(const Params& P, const EnvSm<CAP>& e, int u, const Key& ek) {
+template <int CAP, int HT>
+__device__ __forceinline__ int random_legal(const Params& P, const EnvSm<CAP, HT>& e, int u, const Key& ek) {
   if (e.h[u] <= 0.0) return kStop;
   const bool ally = u < P.na;
   const int opp0 = ally ? P.na : 0, opp_n = ally ? P.ne : P.na;
@@ -412,8 +415,8 @@ __device__ __forceinline__ bool hypot_less(double dxa, double dya, double d2a, d
 }
 
 // heuristic_action (smax.cpp:374-419) of unit u on the pre-step state.
-template <int CAP>
-__device__ __forceinline__ int heuristic(const Params& P, const EnvSm<CAP>& e, int u, int& target, int& sweep) {
+template <int CAP, int HT>
+__device__ __forceinline__ int heuristic(const Params& P, const EnvSm<CAP, HT>& e, int u, int& target, int& sweep) {
   if (e.h[u] <= 0.0) return kStop;
   const int team = u < P.na ? 0 : 1;
   const int opp0 = team == 0 ? P.na : 0, opp_n = team == 0 ? P.ne : P.na;
@@ -456,8 +459,8 @@ __device__ __forceinline__ int heuristic(const Params& P, const EnvSm<CAP>& e, i
 }
 
 // simulate_tick (smax.cpp:503-537), one unit per lane per phase.
-template <int G, int UPL, int CAP>
-__device__ __forceinline__ void tick(const Params& P, EnvSm<CAP>& e, const Grp<G>& g, const LanePairs<G>& lp,
+template <int G, int UPL, int CAP, int HT>
+__device__ __forceinline__ void tick(const Params& P, EnvSm<CAP, HT>& e, const Grp<G>& g, const LanePairs<G>& lp,
                                      bool final_tick) {
   // weapons recharge, then moves: each lane touches only its own units
 #pragma unroll
@@ -468,7 +471,7 @@ __device__ __forceinline__ void tick(const Params& P, EnvSm<CAP>& e, const Grp<G
     e.cd[u] = (0.0 < v) ? v : 0.0;  // std::max(0.0, v)
     const int a = e.act[u];
     if (a > kWest) continue;
-    const TypeStat& t = P.ts[e.ty[u]];
+    const TypeStat& t = P.ts[e.T(u)];
     const double dxs = a == kEast ? 1.0 : a == kWest ? -1.0 : 0.0;    // kDirX
     const double dys = a == kNorth ? 1.0 : a == kSouth ? -1.0 : 0.0;  // kDirY
     e.x[u] = dclamp(e.x[u] + t.spdt * dxs, t.rad, t.hi);
@@ -486,7 +489,7 @@ __device__ __forceinline__ void tick(const Params& P, EnvSm<CAP>& e, const Grp<G
     if (a >= kAttackBase && e.h[u] > 0.0) {
       const int o = (u < P.na ? P.na : 0) + (a - kAttackBase);
       fire = e.h[o] > 0.0 && !(e.cd[u] > 0.0) && in_range(P, e, u, o);
-      if (fire) e.cd[u] = P.ts[e.ty[u]].cdmax;
+      if (fire) e.cd[u] = P.ts[e.T(u)].cdmax;
     }
     e.fire[u] = fire;
   }
@@ -503,7 +506,7 @@ __device__ __forceinline__ void tick(const Params& P, EnvSm<CAP>& e, const Grp<G
     double damage = 0.0;
     for (int k = 0; k < opp_n; ++k) {  // shooters in unit order
       const int u = opp0 + k;
-      if (e.fire[u] && e.act[u] - kAttackBase == me) damage += P.ts[e.ty[u]].dmg;
+      if (e.fire[u] && e.act[u] - kAttackBase == me) damage += P.ts[e.T(u)].dmg;
     }
     if (damage > 0.0) {
       double v = e.h[o] - damage;
@@ -521,13 +524,13 @@ __device__ __forceinline__ void tick(const Params& P, EnvSm<CAP>& e, const Grp<G
 // pool(s, 0) and pool(s, 1) (smax.cpp:365-372): the per-unit ratios are one
 // division per lane; the sums run in the reference's unit order over
 // shuffled values.
-template <int G, int UPL, int CAP>
-__device__ __forceinline__ void pools(const Params& P, const EnvSm<CAP>& e, const Grp<G>& g, double& p0, double& p1) {
+template <int G, int UPL, int CAP, int HT>
+__device__ __forceinline__ void pools(const Params& P, const EnvSm<CAP, HT>& e, const Grp<G>& g, double& p0, double& p1) {
   double ratio[UPL];
 #pragma unroll
   for (int j = 0; j < UPL; ++j) {
     const int u = g.gl + G * j;
-    ratio[j] = u < P.n ? e.h[u] / P.ts[e.ty[u]].hmax : 0.0;
+    ratio[j] = u < P.n ? e.h[u] / P.ts[e.T(u)].hmax : 0.0;
   }
   p0 = 0.0;
   p1 = 0.0;
@@ -562,10 +565,10 @@ __device__ __forceinline__ int obs_slot(const Params& P, int me, int u) {
 }
 
 // This lane's part of observe(s, me) (smax.cpp:601-634) into row[D].
-template <int G, int UPL, int CAP>
-__device__ __forceinline__ void observe_part(const Params& P, const EnvSm<CAP>& e, int gl, int me, float* row) {
+template <int G, int UPL, int CAP, int HT>
+__device__ __forceinline__ void observe_part(const Params& P, const EnvSm<CAP, HT>& e, int gl, int me, float* row) {
   const bool me_alive = e.h[me] > 0.0;
-  const TypeStat& my = P.ts[e.ty[me]];
+  const TypeStat& my = P.ts[e.T(me)];
 #pragma unroll
   for (int j = 0; j < UPL; ++j) {
     const int u = gl + G * j;
@@ -582,7 +585,7 @@ __device__ __forceinline__ void observe_part(const Params& P, const EnvSm<CAP>& 
       o[2] = float(e.x[me] / P.map);
       o[3] = float(e.y[me] / P.map);
 #pragma unroll
-      for (int q = 0; q < kTypes; ++q) o[4 + q] = q == e.ty[me] ? 1.0f : 0.0f;
+      for (int q = 0; q < kTypes; ++q) o[4 + q] = q == e.T(me) ? 1.0f : 0.0f;
       continue;
     }
     float* o = row + 10 + 17 * obs_slot(P, me, u);
@@ -591,14 +594,14 @@ __device__ __forceinline__ void observe_part(const Params& P, const EnvSm<CAP>& 
       for (int q = 0; q < 17; ++q) o[q] = 0.0f;
       continue;
     }
-    const TypeStat& st = P.ts[e.ty[u]];
+    const TypeStat& st = P.ts[e.T(u)];
     const double sight = my.sight.r;
     o[0] = 1.0f;
     o[1] = float((e.x[u] - e.x[me]) / sight);
     o[2] = float((e.y[u] - e.y[me]) / sight);
     o[3] = float(e.h[u] / st.hmax);
     o[4] = float(e.cd[u] / st.cdmax);
-    const int tu = e.ty[u];
+    const int tu = e.T(u);
 #pragma unroll
     for (int q = 0; q < kTypes; ++q) o[5 + q] = q == tu ? 1.0f : 0.0f;
     const int bucket = e.pa[u] <= kStop ? e.pa[u] : kStop + 1;  // action_bucket, smax.cpp:589
@@ -661,8 +664,8 @@ __device__ __forceinline__ void warp_store(float* __restrict__ gdst, const float
 // All observation rows of the warp's envs -> gdst ([N][A][D]).  Warp-uniform
 // call; `active` says whether this lane's group builds rows, `sel` (bitmask
 // over the warp's EPW env slots) which envs are stored.
-template <int G, int UPL, int CAP>
-__device__ __noinline__ void emit_obs(const Params& P, const EnvSm<CAP>& e, const Grp<G>& g, bool active,
+template <int G, int UPL, int CAP, int HT>
+__device__ __noinline__ void emit_obs(const Params& P, const EnvSm<CAP, HT>& e, const Grp<G>& g, bool active,
                                          float* tile, float* __restrict__ gdst, int64_t w0, int wvalid, int rb,
                                          unsigned sel) {
   constexpr int EPW = Grp<G>::EPW;
@@ -684,8 +687,8 @@ __device__ __noinline__ void emit_obs(const Params& P, const EnvSm<CAP>& e, cons
   }
 }
 
-template <int G, int UPL, int CAP>
-__device__ __forceinline__ void load_env(const Params& P, EnvSm<CAP>& e, const SmaxState& st, int gl, int64_t i,
+template <int G, int UPL, int CAP, int HT>
+__device__ __forceinline__ void load_env(const Params& P, EnvSm<CAP, HT>& e, const SmaxState& st, int gl, int64_t i,
                                          int64_t n, int* tg, int* sw) {
 #pragma unroll
   for (int j = 0; j < UPL; ++j) {
@@ -705,8 +708,8 @@ __device__ __forceinline__ void load_env(const Params& P, EnvSm<CAP>& e, const S
   }
 }
 
-template <int G, int UPL, int CAP>
-__device__ __forceinline__ void store_env(const Params& P, const EnvSm<CAP>& e, const SmaxState& st, int gl,
+template <int G, int UPL, int CAP, int HT>
+__device__ __forceinline__ void store_env(const Params& P, const EnvSm<CAP, HT>& e, const SmaxState& st, int gl,
                                           int64_t i, int64_t n, const int* tg, const int* sw) {
 #pragma unroll
   for (int j = 0; j < UPL; ++j) {
@@ -717,14 +720,14 @@ __device__ __forceinline__ void store_env(const Params& P, const EnvSm<CAP>& e, 
     st.health[u * n + i] = e.h[u];
     st.cooldown[u * n + i] = e.cd[u];
     st.mem[u * n + i] = uint32_t(uint8_t(e.pa[u])) | (uint32_t(uint8_t(int8_t(tg[j]))) << 8) |
-                        (uint32_t(uint8_t(int8_t(sw[j]))) << 16) | (uint32_t(uint8_t(e.ty[u])) << 24);
+                        (uint32_t(uint8_t(int8_t(sw[j]))) << 16) | (uint32_t(uint8_t(e.T(u))) << 24);
   }
 }
 
 // SmaxEnv::reset (smax.cpp:163-193): spawns (one unit per lane), separation
 // to the fixpoint, fresh heuristic memory.
-template <int G, int UPL, int CAP>
-__device__ __noinline__ void env_reset(const Params& P, EnvSm<CAP>& e, const Grp<G>& g, const Key& key, int* tg,
+template <int G, int UPL, int CAP, int HT>
+__device__ __noinline__ void env_reset(const Params& P, EnvSm<CAP, HT>& e, const Grp<G>& g, const Key& key, int* tg,
                                           int* sw) {
 #pragma unroll
   for (int j = 0; j < UPL; ++j) {
@@ -792,7 +795,7 @@ __global__ void __launch_bounds__(kThreads) smax_reset_kernel(const Params* __re
   emit_obs<G, UPL>(P, e, g, live, m.tile, lc.v.obs, w0, wvalid, plan.rb, (1u << EPW) - 1u);
 }
 
-template <int G, int UPL, bool RANDOM>
+template <int G, int UPL, bool RANDOM, int HT>
 __global__ void __launch_bounds__(kThreads, 3) smax_step_kernel(const Params* __restrict__ gP, SmaxState st,
                                                              LaunchCommon lc, Key step_key, Plan plan) {
   constexpr int EPW = Grp<G>::EPW, EPB = kWarps * EPW, CAP = G * UPL;
@@ -803,7 +806,7 @@ __global__ void __launch_bounds__(kThreads, 3) smax_step_kernel(const Params* __
   Smem m = carve<G, UPL>(smem, P.D, plan.rb);
   const Grp<G> g;
   const int slot = (threadIdx.x >> 5) * EPW + (g.dead ? 0 : (threadIdx.x & 31) / G);
-  EnvSm<CAP>& e = reinterpret_cast<EnvSm<CAP>*>(m.envs)[slot];
+  EnvSm<CAP, HT>& e = reinterpret_cast<EnvSm<CAP, HT>*>(m.envs)[slot];
   const int64_t i = lc.begin + int64_t(blockIdx.x) * EPB + slot;
   const int64_t w0 = lc.begin + int64_t(blockIdx.x) * EPB + (threadIdx.x >> 5) * EPW;
   const int wvalid = int(max(int64_t(0), min64(EPW, lc.end - w0)));
@@ -1099,7 +1102,12 @@ void launch_step_g(const SmaxConfig& c, const Params* dP, const SmaxState& s, co
                    Key k) {
   size_t sm;
   Plan plan = make_plan<G, UPL>(c, &sm);
-  auto fn = random ? smax_step_kernel<G, UPL, true> : smax_step_kernel<G, UPL, false>;
+  // a fixed roster of marines only (3m, 5m_vs_6m, 27m_vs_30m, ...): the type-folded instance
+  bool marines = !c.random_types;
+  for (int u = 0; u < c.na + c.ne && marines; ++u) marines = c.type[u] == 0;
+  if (std::getenv("MARL_SMAX_GENERIC")) marines = false;
+  auto fn = marines ? (random ? smax_step_kernel<G, UPL, true, 0> : smax_step_kernel<G, UPL, false, 0>)
+                    : (random ? smax_step_kernel<G, UPL, true, -1> : smax_step_kernel<G, UPL, false, -1>);
   cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
   constexpr int EPB = kWarps * Grp<G>::EPW;
   fn<<<unsigned((lc.end - lc.begin + EPB - 1) / EPB), kThreads, sm, lc.stream>>>(dP, s, lc, k, plan);

@@ -217,3 +217,30 @@ def test_ragged_batch_sizes_match_oracle(env_id, cfg, n):
         b = o.step_random(ak[t])
         _compare(env_id, a, b, t)
 
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("env_id,cfg", [("SMAX_5m_vs_6m", THREE_M), ("SMAX_5m_vs_6m", {}),
+                                        ("SMAX_5m_vs_6m", {"enemy_controlled": True})])
+def test_smax_marine_roster_instance_equals_generic(env_id, cfg, monkeypatch):
+    """All-marine rosters run a step kernel with the unit type folded to a
+    compile-time constant; MARL_SMAX_GENERIC=1 forces the per-unit-type kernel.
+    Both must produce the same bytes (obs, rewards, dones, state) every step."""
+    import paper_2311_10090_b200 as m
+    n, T = 300, 40
+    runs = []
+    for generic in (False, True):
+        if generic:
+            monkeypatch.setenv("MARL_SMAX_GENERIC", "1")
+        v = m.VectorEnv(env_id, n, config=cfg)
+        v.reset(O.key_from_seed(17))
+        out = []
+        for k in range(T):
+            v.step_random(O.fold_in(O.key_from_seed(18), k))
+            d = v.download(("obs", "rewards", "dones", "finished"))
+            d["hash"] = v.state_hash().cpu().numpy().copy()
+            out.append(d)
+        runs.append(out)
+    for k, (a, b) in enumerate(zip(*runs)):
+        for f in a:
+            assert np.array_equal(a[f], b[f]), (k, f)
