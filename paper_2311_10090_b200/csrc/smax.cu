@@ -36,6 +36,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <type_traits>
 
 #include "common.cuh"
 #include "engine.h"
@@ -78,7 +79,9 @@ static_assert(sizeof(Params) % 16 == 0, "Params is staged with 16-byte copies");
 // One env's unit state during a step (shared memory).
 // HT >= 0: every unit of the roster has type HT (fixed single-type rosters such
 // as 3m / 5m_vs_6m / 27m_vs_30m): type lookups fold to compile-time constants.
-template <int CAP, int HT = -1>
+// FU: the roster fills the lane group exactly (n == CAP, e.g. 3m, 2s3z): the
+// unit count is a compile-time constant and the u < n tests vanish.
+template <int CAP, int HT = -1, bool FU = false>
 struct EnvSm {
   double x[CAP], y[CAP], h[CAP], cd[CAP];
   int act[CAP];
@@ -86,6 +89,7 @@ struct EnvSm {
   int8_t fire[CAP];
   int8_t ty[CAP];  // unit types of this env (the roster, or smacv2's per-episode draw)
   __device__ __forceinline__ int T(int u) const { return HT >= 0 ? HT : int(ty[u]); }
+  __device__ __forceinline__ int nu(const Params& P) const { return FU ? CAP : P.n; }
 };
 
 // A group of G lanes of one warp (G need not be a power of two: a warp holds
@@ -115,14 +119,14 @@ __device__ __forceinline__ double dclamp(double v, double lo, double hi) {  // s
   return (v < lo) ? lo : (hi < v) ? hi : v;
 }
 
-template <int CAP, int HT>
-__device__ __forceinline__ bool in_range(const Params& P, const EnvSm<CAP, HT>& e, int a, int b) {
+template <int CAP, int HT, bool FU>
+__device__ __forceinline__ bool in_range(const Params& P, const EnvSm<CAP, HT, FU>& e, int a, int b) {
   const Thresh& r = P.ps[e.T(a)][e.T(b)].reach;  // smax.cpp:497-501
   return dist_le(e.x[a] - e.x[b], e.y[a] - e.y[b], r.r, r.r2lo, r.r2hi);
 }
 
-template <int CAP, int HT>
-__device__ __forceinline__ bool sees(const Params& P, const EnvSm<CAP, HT>& e, int a, int b) {
+template <int CAP, int HT, bool FU>
+__device__ __forceinline__ bool sees(const Params& P, const EnvSm<CAP, HT, FU>& e, int a, int b) {
   const Thresh& r = P.ts[e.T(a)].sight;  // center_dist(a, b) <= sight(a), smax.cpp:383,613
   return dist_le(e.x[a] - e.x[b], e.y[a] - e.y[b], r.r, r.r2lo, r.r2hi);
 }
@@ -175,10 +179,10 @@ __device__ __forceinline__ unsigned long long unit_mask(const Grp<G>& g, const b
 // the lowest hit by ballot, lets b's lane apply the reference push, and
 // repeats from there: rounds per row = pushes in the row + 1, and the
 // trajectory is the sequential one bit for bit.
-template <int G, int UPL, int CAP, int HT>
-__device__ __forceinline__ void separation_pass(const Params& P, EnvSm<CAP, HT>& e, const Grp<G>& g,
+template <int G, int UPL, int CAP, int HT, bool FU>
+__device__ __forceinline__ void separation_pass(const Params& P, EnvSm<CAP, HT, FU>& e, const Grp<G>& g,
                                                 unsigned long long alive) {
-  const int n = P.n;
+  const int n = e.nu(P);
   for (int a = 0; a < n - 1; ++a) {
     if (!(alive >> a & 1ull)) continue;
     unsigned long long row = alive & bits_above(a);
@@ -269,10 +273,10 @@ __device__ __forceinline__ bool for_lane_pairs(const LanePairs<G>& lp, int gl, i
 // Does any living pair of this lane's share overlap right now (the exact
 // reference test, hypot only inside the rounding band)?  If no pair overlaps
 // at the start of a pass, the pass pushes nothing -- so it is skipped.
-template <int G, int CAP, int HT>
-__device__ __forceinline__ bool lane_pairs_overlap(const Params& P, const EnvSm<CAP, HT>& e, const LanePairs<G>& lp,
+template <int G, int CAP, int HT, bool FU>
+__device__ __forceinline__ bool lane_pairs_overlap(const Params& P, const EnvSm<CAP, HT, FU>& e, const LanePairs<G>& lp,
                                                    int gl) {
-  return for_lane_pairs<G>(lp, gl, P.n, [&](int a, int b) {
+  return for_lane_pairs<G>(lp, gl, e.nu(P), [&](int a, int b) {
     if (e.h[a] <= 0.0 || e.h[b] <= 0.0) return false;
     const double dx = e.x[b] - e.x[a], dy = e.y[b] - e.y[a];
     const double d2 = dx * dx + dy * dy;
@@ -284,10 +288,10 @@ __device__ __forceinline__ bool lane_pairs_overlap(const Params& P, const EnvSm<
 }
 
 // max_overlap(s) <= kSeparationTol restricted to this lane's pairs (smax.cpp:569-580).
-template <int G, int CAP, int HT>
-__device__ __forceinline__ bool lane_pairs_within_tol(const Params& P, const EnvSm<CAP, HT>& e, const LanePairs<G>& lp,
+template <int G, int CAP, int HT, bool FU>
+__device__ __forceinline__ bool lane_pairs_within_tol(const Params& P, const EnvSm<CAP, HT, FU>& e, const LanePairs<G>& lp,
                                                       int gl) {
-  return !for_lane_pairs<G>(lp, gl, P.n, [&](int a, int b) {
+  return !for_lane_pairs<G>(lp, gl, e.nu(P), [&](int a, int b) {
     if (e.h[a] <= 0.0 || e.h[b] <= 0.0) return false;
     const PairStat& S = P.ps[e.T(a)][e.T(b)];
     const double dx = e.x[a] - e.x[b], dy = e.y[a] - e.y[b];
@@ -301,8 +305,8 @@ __device__ __forceinline__ bool lane_pairs_within_tol(const Params& P, const Env
 // separate(s, to_fixpoint), smax.cpp:542-567.  A pass is a no-op exactly when
 // no living pair overlaps, which the parallel pre-check proves in the common
 // case (and then max_overlap <= 0 <= tol ends the fixpoint loop as well).
-template <int G, int UPL, int CAP, int HT>
-__device__ __forceinline__ void separate(const Params& P, EnvSm<CAP, HT>& e, const Grp<G>& g, const LanePairs<G>& lp,
+template <int G, int UPL, int CAP, int HT, bool FU>
+__device__ __forceinline__ void separate(const Params& P, EnvSm<CAP, HT, FU>& e, const Grp<G>& g, const LanePairs<G>& lp,
                                          bool fixpoint) {
   unsigned long long alive = 0;
   for (int pass = 0; pass < (fixpoint ? 256 : 1); ++pass) {
@@ -310,7 +314,7 @@ __device__ __forceinline__ void separate(const Params& P, EnvSm<CAP, HT>& e, con
     if (pass == 0) {  // health is constant during separation
       bool al[UPL];
 #pragma unroll
-      for (int j = 0; j < UPL; ++j) al[j] = g.gl + G * j < P.n && e.h[g.gl + G * j] > 0.0;
+      for (int j = 0; j < UPL; ++j) al[j] = g.gl + G * j < e.nu(P) && e.h[g.gl + G * j] > 0.0;
       alive = unit_mask<G, UPL>(g, al);
     }
     separation_pass<G, UPL>(P, e, g, alive);
@@ -337,8 +341,8 @@ __device__ __forceinline__ void place_at(double bx, double by, double rad, doubl
 
 // spawn_smacv2 (smax.cpp:456-479) for unit u: kept out of line (rare, and
 // the fixed-roster step kernel's instruction footprint stays as it was).
-template <int CAP, int HT>
-__device__ __noinline__ void spawn_smacv2(const Params& P, EnvSm<CAP, HT>& e, int u, const Key& key) {
+template <int CAP, int HT, bool FU>
+__device__ __noinline__ void spawn_smacv2(const Params& P, EnvSm<CAP, HT, FU>& e, int u, const Key& key) {
   const bool ally = u < P.na;
   const int i = ally ? u : u - P.na;
   const TypeStat& t = P.ts[e.T(u)];
@@ -365,8 +369,8 @@ __device__ __noinline__ void spawn_smacv2(const Params& P, EnvSm<CAP, HT>& e, in
   }
 }
 
-template <int CAP, int HT>
-__device__ __forceinline__ void spawn_unit(const Params& P, EnvSm<CAP, HT>& e, int u, const Key& key) {
+template <int CAP, int HT, bool FU>
+__device__ __forceinline__ void spawn_unit(const Params& P, EnvSm<CAP, HT, FU>& e, int u, const Key& key) {
   const TypeStat& t = P.ts[e.T(u)];
   if (P.random_types) {
     spawn_smacv2(P, e, u, key);
@@ -389,8 +393,8 @@ __device__ __forceinline__ void spawn_unit(const Params& P, EnvSm<CAP, HT>& e, i
 // The pick-th legal action of unit u (smax.cpp:195-211 with legal_uniform,
 // vector_env.cpp:21-32).  Legal order: moves 0-3, stop, attacks on living
 // opponents in range; a dead unit's only legal action is stop.
-template <int CAP, int HT>
-__device__ __forceinline__ int random_legal(const Params& P, const EnvSm<CAP, HT>& e, int u, const Key& ek) {
+template <int CAP, int HT, bool FU>
+__device__ __forceinline__ int random_legal(const Params& P, const EnvSm<CAP, HT, FU>& e, int u, const Key& ek) {
   if (e.h[u] <= 0.0) return kStop;
   const bool ally = u < P.na;
   const int opp0 = ally ? P.na : 0, opp_n = ally ? P.ne : P.na;
@@ -415,8 +419,8 @@ __device__ __forceinline__ bool hypot_less(double dxa, double dya, double d2a, d
 }
 
 // heuristic_action (smax.cpp:374-419) of unit u on the pre-step state.
-template <int CAP, int HT>
-__device__ __forceinline__ int heuristic(const Params& P, const EnvSm<CAP, HT>& e, int u, int& target, int& sweep) {
+template <int CAP, int HT, bool FU>
+__device__ __forceinline__ int heuristic(const Params& P, const EnvSm<CAP, HT, FU>& e, int u, int& target, int& sweep) {
   if (e.h[u] <= 0.0) return kStop;
   const int team = u < P.na ? 0 : 1;
   const int opp0 = team == 0 ? P.na : 0, opp_n = team == 0 ? P.ne : P.na;
@@ -459,14 +463,14 @@ __device__ __forceinline__ int heuristic(const Params& P, const EnvSm<CAP, HT>& 
 }
 
 // simulate_tick (smax.cpp:503-537), one unit per lane per phase.
-template <int G, int UPL, int CAP, int HT>
-__device__ __forceinline__ void tick(const Params& P, EnvSm<CAP, HT>& e, const Grp<G>& g, const LanePairs<G>& lp,
+template <int G, int UPL, int CAP, int HT, bool FU>
+__device__ __forceinline__ void tick(const Params& P, EnvSm<CAP, HT, FU>& e, const Grp<G>& g, const LanePairs<G>& lp,
                                      bool final_tick) {
   // weapons recharge, then moves: each lane touches only its own units
 #pragma unroll
   for (int j = 0; j < UPL; ++j) {
     const int u = g.gl + G * j;
-    if (u >= P.n || e.h[u] <= 0.0) continue;
+    if (u >= e.nu(P) || e.h[u] <= 0.0) continue;
     double v = e.cd[u] - kDt;
     e.cd[u] = (0.0 < v) ? v : 0.0;  // std::max(0.0, v)
     const int a = e.act[u];
@@ -483,7 +487,7 @@ __device__ __forceinline__ void tick(const Params& P, EnvSm<CAP, HT>& e, const G
 #pragma unroll
   for (int j = 0; j < UPL; ++j) {
     const int u = g.gl + G * j;
-    if (u >= P.n) continue;
+    if (u >= e.nu(P)) continue;
     bool fire = false;
     const int a = e.act[u];
     if (a >= kAttackBase && e.h[u] > 0.0) {
@@ -499,7 +503,7 @@ __device__ __forceinline__ void tick(const Params& P, EnvSm<CAP, HT>& e, const G
   for (int j = 0; j < UPL; ++j) {
     const int o = g.gl + G * j;
     newh[j] = -1.0;
-    if (o >= P.n) continue;
+    if (o >= e.nu(P)) continue;
     // o's shooters are its opponents; `me` is o's index among THEIR opponents
     const int opp0 = o < P.na ? P.na : 0, opp_n = o < P.na ? P.ne : P.na;
     const int me = o < P.na ? o : o - P.na;
@@ -524,13 +528,13 @@ __device__ __forceinline__ void tick(const Params& P, EnvSm<CAP, HT>& e, const G
 // pool(s, 0) and pool(s, 1) (smax.cpp:365-372): the per-unit ratios are one
 // division per lane; the sums run in the reference's unit order over
 // shuffled values.
-template <int G, int UPL, int CAP, int HT>
-__device__ __forceinline__ void pools(const Params& P, const EnvSm<CAP, HT>& e, const Grp<G>& g, double& p0, double& p1) {
+template <int G, int UPL, int CAP, int HT, bool FU>
+__device__ __forceinline__ void pools(const Params& P, const EnvSm<CAP, HT, FU>& e, const Grp<G>& g, double& p0, double& p1) {
   double ratio[UPL];
 #pragma unroll
   for (int j = 0; j < UPL; ++j) {
     const int u = g.gl + G * j;
-    ratio[j] = u < P.n ? e.h[u] / P.ts[e.T(u)].hmax : 0.0;
+    ratio[j] = u < e.nu(P) ? e.h[u] / P.ts[e.T(u)].hmax : 0.0;
   }
   p0 = 0.0;
   p1 = 0.0;
@@ -539,7 +543,7 @@ __device__ __forceinline__ void pools(const Params& P, const EnvSm<CAP, HT>& e, 
     for (int l = 0; l < G; ++l) {
       const int u = l + G * j;
       const double r = g.bcast(ratio[j], l);  // group-uniform loop: every lane shuffles
-      if (u >= P.n) continue;
+      if (u >= e.nu(P)) continue;
       const double alive = e.h[u] > 0.0 ? 1.0 : 0.0;
       if (u < P.na) {
         p0 += r;
@@ -565,14 +569,14 @@ __device__ __forceinline__ int obs_slot(const Params& P, int me, int u) {
 }
 
 // This lane's part of observe(s, me) (smax.cpp:601-634) into row[D].
-template <int G, int UPL, int CAP, int HT>
-__device__ __forceinline__ void observe_part(const Params& P, const EnvSm<CAP, HT>& e, int gl, int me, float* row) {
+template <int G, int UPL, int CAP, int HT, bool FU>
+__device__ __forceinline__ void observe_part(const Params& P, const EnvSm<CAP, HT, FU>& e, int gl, int me, float* row) {
   const bool me_alive = e.h[me] > 0.0;
   const TypeStat& my = P.ts[e.T(me)];
 #pragma unroll
   for (int j = 0; j < UPL; ++j) {
     const int u = gl + G * j;
-    if (u >= P.n) continue;
+    if (u >= e.nu(P)) continue;
     if (u == me) {
       float* o = row;
       if (!me_alive) {
@@ -664,8 +668,8 @@ __device__ __forceinline__ void warp_store(float* __restrict__ gdst, const float
 // All observation rows of the warp's envs -> gdst ([N][A][D]).  Warp-uniform
 // call; `active` says whether this lane's group builds rows, `sel` (bitmask
 // over the warp's EPW env slots) which envs are stored.
-template <int G, int UPL, int CAP, int HT>
-__device__ __noinline__ void emit_obs(const Params& P, const EnvSm<CAP, HT>& e, const Grp<G>& g, bool active,
+template <int G, int UPL, int CAP, int HT, bool FU>
+__device__ __noinline__ void emit_obs(const Params& P, const EnvSm<CAP, HT, FU>& e, const Grp<G>& g, bool active,
                                          float* tile, float* __restrict__ gdst, int64_t w0, int wvalid, int rb,
                                          unsigned sel) {
   constexpr int EPW = Grp<G>::EPW;
@@ -687,15 +691,15 @@ __device__ __noinline__ void emit_obs(const Params& P, const EnvSm<CAP, HT>& e, 
   }
 }
 
-template <int G, int UPL, int CAP, int HT>
-__device__ __forceinline__ void load_env(const Params& P, EnvSm<CAP, HT>& e, const SmaxState& st, int gl, int64_t i,
+template <int G, int UPL, int CAP, int HT, bool FU>
+__device__ __forceinline__ void load_env(const Params& P, EnvSm<CAP, HT, FU>& e, const SmaxState& st, int gl, int64_t i,
                                          int64_t n, int* tg, int* sw) {
 #pragma unroll
   for (int j = 0; j < UPL; ++j) {
     const int u = gl + G * j;
     tg[j] = -1;
     sw[j] = -1;
-    if (u >= P.n) continue;
+    if (u >= e.nu(P)) continue;
     e.x[u] = st.x[u * n + i];
     e.y[u] = st.y[u * n + i];
     e.h[u] = st.health[u * n + i];
@@ -708,13 +712,13 @@ __device__ __forceinline__ void load_env(const Params& P, EnvSm<CAP, HT>& e, con
   }
 }
 
-template <int G, int UPL, int CAP, int HT>
-__device__ __forceinline__ void store_env(const Params& P, const EnvSm<CAP, HT>& e, const SmaxState& st, int gl,
+template <int G, int UPL, int CAP, int HT, bool FU>
+__device__ __forceinline__ void store_env(const Params& P, const EnvSm<CAP, HT, FU>& e, const SmaxState& st, int gl,
                                           int64_t i, int64_t n, const int* tg, const int* sw) {
 #pragma unroll
   for (int j = 0; j < UPL; ++j) {
     const int u = gl + G * j;
-    if (u >= P.n) continue;
+    if (u >= e.nu(P)) continue;
     st.x[u * n + i] = e.x[u];
     st.y[u * n + i] = e.y[u];
     st.health[u * n + i] = e.h[u];
@@ -726,15 +730,15 @@ __device__ __forceinline__ void store_env(const Params& P, const EnvSm<CAP, HT>&
 
 // SmaxEnv::reset (smax.cpp:163-193): spawns (one unit per lane), separation
 // to the fixpoint, fresh heuristic memory.
-template <int G, int UPL, int CAP, int HT>
-__device__ __noinline__ void env_reset(const Params& P, EnvSm<CAP, HT>& e, const Grp<G>& g, const Key& key, int* tg,
+template <int G, int UPL, int CAP, int HT, bool FU>
+__device__ __noinline__ void env_reset(const Params& P, EnvSm<CAP, HT, FU>& e, const Grp<G>& g, const Key& key, int* tg,
                                           int* sw) {
 #pragma unroll
   for (int j = 0; j < UPL; ++j) {
     const int u = g.gl + G * j;
     tg[j] = -1;
     sw[j] = -1;
-    if (u >= P.n) continue;
+    if (u >= e.nu(P)) continue;
     if (P.random_types) {  // randint1(fold_in(key, 10 + i | 500 + i), 0, kTypeCount) (smax.cpp:169-175)
       const uint64_t d = u < P.na ? 10 + uint64_t(u) : 500 + uint64_t(u - P.na);
       e.ty[u] = int8_t(block_at_nl(fold_in_nl(key, d), 0) % uint64_t(kTypes));
@@ -744,7 +748,7 @@ __device__ __noinline__ void env_reset(const Params& P, EnvSm<CAP, HT>& e, const
     spawn_unit(P, e, u, key);
   }
   g.sync();
-  const LanePairs<G> lp(g.gl, P.n);  // rare path: built here rather than passed
+  const LanePairs<G> lp(g.gl, e.nu(P));  // rare path: built here rather than passed
   separate<G, UPL>(P, e, g, lp, true);
 }
 
@@ -795,7 +799,7 @@ __global__ void __launch_bounds__(kThreads) smax_reset_kernel(const Params* __re
   emit_obs<G, UPL>(P, e, g, live, m.tile, lc.v.obs, w0, wvalid, plan.rb, (1u << EPW) - 1u);
 }
 
-template <int G, int UPL, bool RANDOM, int HT>
+template <int G, int UPL, bool RANDOM, int HT, bool FU>
 __global__ void __launch_bounds__(kThreads, 3) smax_step_kernel(const Params* __restrict__ gP, SmaxState st,
                                                              LaunchCommon lc, Key step_key, Plan plan) {
   constexpr int EPW = Grp<G>::EPW, EPB = kWarps * EPW, CAP = G * UPL;
@@ -806,7 +810,7 @@ __global__ void __launch_bounds__(kThreads, 3) smax_step_kernel(const Params* __
   Smem m = carve<G, UPL>(smem, P.D, plan.rb);
   const Grp<G> g;
   const int slot = (threadIdx.x >> 5) * EPW + (g.dead ? 0 : (threadIdx.x & 31) / G);
-  EnvSm<CAP, HT>& e = reinterpret_cast<EnvSm<CAP, HT>*>(m.envs)[slot];
+  EnvSm<CAP, HT, FU>& e = reinterpret_cast<EnvSm<CAP, HT, FU>*>(m.envs)[slot];
   const int64_t i = lc.begin + int64_t(blockIdx.x) * EPB + slot;
   const int64_t w0 = lc.begin + int64_t(blockIdx.x) * EPB + (threadIdx.x >> 5) * EPW;
   const int wvalid = int(max(int64_t(0), min64(EPW, lc.end - w0)));
@@ -837,7 +841,7 @@ __global__ void __launch_bounds__(kThreads, 3) smax_step_kernel(const Params* __
     for (int j = 0; j < UPL; ++j) {
       const int u = g.gl + G * j;
       act[j] = kStop;
-      if (u >= P.n) continue;
+      if (u >= e.nu(P)) continue;
       if (u < A) {
         act[j] = RANDOM ? random_legal(P, e, u, ek) : lc.v.actions[i * A + u];
         if (RANDOM) lc.v.actions[i * A + u] = act[j];
@@ -850,18 +854,18 @@ __global__ void __launch_bounds__(kThreads, 3) smax_step_kernel(const Params* __
     g.sync();  // every lane has read the pre-step state
 #pragma unroll
     for (int j = 0; j < UPL; ++j)
-      if (g.gl + G * j < P.n) e.act[g.gl + G * j] = act[j];
+      if (g.gl + G * j < e.nu(P)) e.act[g.gl + G * j] = act[j];
     g.sync();
 
     // ---- physics (smax.cpp:242-254)
-    const LanePairs<G> lp(g.gl, P.n);
+    const LanePairs<G> lp(g.gl, e.nu(P));
 #pragma unroll 1
     for (int k = 0; k < kTicks; ++k) tick<G, UPL>(P, e, g, lp, k == kTicks - 1);
     int ally_alive = 0, enemy_alive = 0;
 #pragma unroll
     for (int j = 0; j < UPL; ++j) {
       const int u = g.gl + G * j;
-      const bool alive = u < P.n && e.h[u] > 0.0;
+      const bool alive = u < e.nu(P) && e.h[u] > 0.0;
       ally_alive += g.count(alive && u < P.na);
       enemy_alive += g.count(alive && u >= P.na);
     }
@@ -906,7 +910,7 @@ __global__ void __launch_bounds__(kThreads, 3) smax_step_kernel(const Params* __
     // prev_action <- this step's actions (smax.cpp:243)
 #pragma unroll
     for (int j = 0; j < UPL; ++j)
-      if (g.gl + G * j < P.n) e.pa[g.gl + G * j] = int8_t(e.act[g.gl + G * j]);
+      if (g.gl + G * j < e.nu(P)) e.pa[g.gl + G * j] = int8_t(e.act[g.gl + G * j]);
     g.sync();
   }
   stats_add(lc.stats, done && g.gl == 0, ep_len, ep_ret);
@@ -1106,8 +1110,15 @@ void launch_step_g(const SmaxConfig& c, const Params* dP, const SmaxState& s, co
   bool marines = !c.random_types;
   for (int u = 0; u < c.na + c.ne && marines; ++u) marines = c.type[u] == 0;
   if (std::getenv("MARL_SMAX_GENERIC")) marines = false;
-  auto fn = marines ? (random ? smax_step_kernel<G, UPL, true, 0> : smax_step_kernel<G, UPL, false, 0>)
-                    : (random ? smax_step_kernel<G, UPL, true, -1> : smax_step_kernel<G, UPL, false, -1>);
+  const bool full = c.na + c.ne == G * UPL && !std::getenv("MARL_SMAX_GENERIC");
+  auto pick = [&](auto ht, auto fu) {
+    return random ? smax_step_kernel<G, UPL, true, decltype(ht)::value, decltype(fu)::value>
+                  : smax_step_kernel<G, UPL, false, decltype(ht)::value, decltype(fu)::value>;
+  };
+  using Marine = std::integral_constant<int, 0>;
+  using AnyType = std::integral_constant<int, -1>;
+  auto fn = marines ? (full ? pick(Marine{}, std::true_type{}) : pick(Marine{}, std::false_type{}))
+                    : (full ? pick(AnyType{}, std::true_type{}) : pick(AnyType{}, std::false_type{}));
   cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
   constexpr int EPB = kWarps * Grp<G>::EPW;
   fn<<<unsigned((lc.end - lc.begin + EPB - 1) / EPB), kThreads, sm, lc.stream>>>(dP, s, lc, k, plan);

@@ -221,11 +221,13 @@ def test_ragged_batch_sizes_match_oracle(env_id, cfg, n):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("env_id,cfg", [("SMAX_5m_vs_6m", THREE_M), ("SMAX_5m_vs_6m", {}),
-                                        ("SMAX_5m_vs_6m", {"enemy_controlled": True})])
-def test_smax_marine_roster_instance_equals_generic(env_id, cfg, monkeypatch):
+                                        ("SMAX_5m_vs_6m", {"enemy_controlled": True}), ("SMAX_2s3z", {})])
+def test_smax_folded_instances_equal_generic(env_id, cfg, monkeypatch):
     """All-marine rosters run a step kernel with the unit type folded to a
-    compile-time constant; MARL_SMAX_GENERIC=1 forces the per-unit-type kernel.
-    Both must produce the same bytes (obs, rewards, dones, state) every step."""
+    compile-time constant, and rosters that fill their lane group (3m: 6 of 6,
+    2s3z: 10 of 10) one with the unit count folded; MARL_SMAX_GENERIC=1 forces
+    the general kernel. Both must produce the same bytes (obs, rewards, dones,
+    state) every step."""
     import paper_2311_10090_b200 as m
     n, T = 300, 40
     runs = []
