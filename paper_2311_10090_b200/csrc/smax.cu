@@ -79,8 +79,9 @@ static_assert(sizeof(Params) % 16 == 0, "Params is staged with 16-byte copies");
 // One env's unit state during a step (shared memory).
 // HT >= 0: every unit of the roster has type HT (fixed single-type rosters such
 // as 3m / 5m_vs_6m / 27m_vs_30m): type lookups fold to compile-time constants.
-// FU: the roster fills the lane group exactly (n == CAP, e.g. 3m, 2s3z): the
-// unit count is a compile-time constant and the u < n tests vanish.
+// FU: the roster fills the lane group exactly with two equal teams (n == CAP,
+// na == ne: 3m, 2s3z): unit and team counts are compile-time constants and the
+// u < n / team tests fold.
 template <int CAP, int HT = -1, bool FU = false>
 struct EnvSm {
   double x[CAP], y[CAP], h[CAP], cd[CAP];
@@ -90,6 +91,8 @@ struct EnvSm {
   int8_t ty[CAP];  // unit types of this env (the roster, or smacv2's per-episode draw)
   __device__ __forceinline__ int T(int u) const { return HT >= 0 ? HT : int(ty[u]); }
   __device__ __forceinline__ int nu(const Params& P) const { return FU ? CAP : P.n; }
+  __device__ __forceinline__ int na(const Params& P) const { return FU ? CAP / 2 : P.na; }
+  __device__ __forceinline__ int ne(const Params& P) const { return FU ? CAP / 2 : P.ne; }
 };
 
 // A group of G lanes of one warp (G need not be a power of two: a warp holds
@@ -343,8 +346,8 @@ __device__ __forceinline__ void place_at(double bx, double by, double rad, doubl
 // the fixed-roster step kernel's instruction footprint stays as it was).
 template <int CAP, int HT, bool FU>
 __device__ __noinline__ void spawn_smacv2(const Params& P, EnvSm<CAP, HT, FU>& e, int u, const Key& key) {
-  const bool ally = u < P.na;
-  const int i = ally ? u : u - P.na;
+  const bool ally = u < e.na(P);
+  const int i = ally ? u : u - e.na(P);
   const TypeStat& t = P.ts[e.T(u)];
   if (to_unit(block_at_nl(fold_in_nl(key, 1), 0)) < 0.5) {
     // reflected uniform spawns: enemy i mirrors ally i's draws
@@ -375,8 +378,8 @@ __device__ __forceinline__ void spawn_unit(const Params& P, EnvSm<CAP, HT, FU>& 
   if (P.random_types) {
     spawn_smacv2(P, e, u, key);
   } else {
-    const bool ally = u < P.na;
-    const int i = ally ? u : u - P.na;
+    const bool ally = u < e.na(P);
+    const int i = ally ? u : u - e.na(P);
     double bx = ally ? 0.25 * P.map - 1.5 * (i / 5) : 0.75 * P.map + 1.5 * (i / 5);
     double by = 0.5 * P.map + 1.5 * (i % 5 - 2);
     if (P.jitter > 0.0) {
@@ -396,8 +399,8 @@ __device__ __forceinline__ void spawn_unit(const Params& P, EnvSm<CAP, HT, FU>& 
 template <int CAP, int HT, bool FU>
 __device__ __forceinline__ int random_legal(const Params& P, const EnvSm<CAP, HT, FU>& e, int u, const Key& ek) {
   if (e.h[u] <= 0.0) return kStop;
-  const bool ally = u < P.na;
-  const int opp0 = ally ? P.na : 0, opp_n = ally ? P.ne : P.na;
+  const bool ally = u < e.na(P);
+  const int opp0 = ally ? e.na(P) : 0, opp_n = ally ? e.ne(P) : e.na(P);
   uint64_t att = 0;
   for (int k = 0; k < opp_n; ++k) {
     const int o = opp0 + k;
@@ -422,8 +425,8 @@ __device__ __forceinline__ bool hypot_less(double dxa, double dya, double d2a, d
 template <int CAP, int HT, bool FU>
 __device__ __forceinline__ int heuristic(const Params& P, const EnvSm<CAP, HT, FU>& e, int u, int& target, int& sweep) {
   if (e.h[u] <= 0.0) return kStop;
-  const int team = u < P.na ? 0 : 1;
-  const int opp0 = team == 0 ? P.na : 0, opp_n = team == 0 ? P.ne : P.na;
+  const int team = u < e.na(P) ? 0 : 1;
+  const int opp0 = team == 0 ? e.na(P) : 0, opp_n = team == 0 ? e.ne(P) : e.na(P);
   if (target < 0 || target >= opp_n || !(e.h[opp0 + target] > 0.0 && sees(P, e, u, opp0 + target))) {
     target = -1;
     for (int k = 0; k < opp_n; ++k) {  // lowest-index opponent already in reach
@@ -491,7 +494,7 @@ __device__ __forceinline__ void tick(const Params& P, EnvSm<CAP, HT, FU>& e, con
     bool fire = false;
     const int a = e.act[u];
     if (a >= kAttackBase && e.h[u] > 0.0) {
-      const int o = (u < P.na ? P.na : 0) + (a - kAttackBase);
+      const int o = (u < e.na(P) ? e.na(P) : 0) + (a - kAttackBase);
       fire = e.h[o] > 0.0 && !(e.cd[u] > 0.0) && in_range(P, e, u, o);
       if (fire) e.cd[u] = P.ts[e.T(u)].cdmax;
     }
@@ -505,8 +508,8 @@ __device__ __forceinline__ void tick(const Params& P, EnvSm<CAP, HT, FU>& e, con
     newh[j] = -1.0;
     if (o >= e.nu(P)) continue;
     // o's shooters are its opponents; `me` is o's index among THEIR opponents
-    const int opp0 = o < P.na ? P.na : 0, opp_n = o < P.na ? P.ne : P.na;
-    const int me = o < P.na ? o : o - P.na;
+    const int opp0 = o < e.na(P) ? e.na(P) : 0, opp_n = o < e.na(P) ? e.ne(P) : e.na(P);
+    const int me = o < e.na(P) ? o : o - e.na(P);
     double damage = 0.0;
     for (int k = 0; k < opp_n; ++k) {  // shooters in unit order
       const int u = opp0 + k;
@@ -545,7 +548,7 @@ __device__ __forceinline__ void pools(const Params& P, const EnvSm<CAP, HT, FU>&
       const double r = g.bcast(ratio[j], l);  // group-uniform loop: every lane shuffles
       if (u >= e.nu(P)) continue;
       const double alive = e.h[u] > 0.0 ? 1.0 : 0.0;
-      if (u < P.na) {
+      if (u < e.na(P)) {
         p0 += r;
         p0 += alive;
       } else {
@@ -740,7 +743,7 @@ __device__ __noinline__ void env_reset(const Params& P, EnvSm<CAP, HT, FU>& e, c
     sw[j] = -1;
     if (u >= e.nu(P)) continue;
     if (P.random_types) {  // randint1(fold_in(key, 10 + i | 500 + i), 0, kTypeCount) (smax.cpp:169-175)
-      const uint64_t d = u < P.na ? 10 + uint64_t(u) : 500 + uint64_t(u - P.na);
+      const uint64_t d = u < e.na(P) ? 10 + uint64_t(u) : 500 + uint64_t(u - e.na(P));
       e.ty[u] = int8_t(block_at_nl(fold_in_nl(key, d), 0) % uint64_t(kTypes));
     } else {
       e.ty[u] = P.type[u];
@@ -866,8 +869,8 @@ __global__ void __launch_bounds__(kThreads, 3) smax_step_kernel(const Params* __
     for (int j = 0; j < UPL; ++j) {
       const int u = g.gl + G * j;
       const bool alive = u < e.nu(P) && e.h[u] > 0.0;
-      ally_alive += g.count(alive && u < P.na);
-      enemy_alive += g.count(alive && u >= P.na);
+      ally_alive += g.count(alive && u < e.na(P));
+      enemy_alive += g.count(alive && u >= e.na(P));
     }
     t += 1;
     int winner = -1;
@@ -880,15 +883,15 @@ __global__ void __launch_bounds__(kThreads, 3) smax_step_kernel(const Params* __
     // ---- reward_map (smax.cpp:352-363), infos and dones (smax.cpp:256-268)
     double pool_next0, pool_next1;
     pools<G, UPL>(P, e, g, pool_next0, pool_next1);
-    double ally_r = 0.5 * (pool_prev1 - pool_next1) / (2.0 * P.ne);
-    double enemy_r = 0.5 * (pool_prev0 - pool_next0) / (2.0 * P.na);
+    double ally_r = 0.5 * (pool_prev1 - pool_next1) / (2.0 * e.ne(P));
+    double enemy_r = 0.5 * (pool_prev0 - pool_next0) / (2.0 * e.na(P));
     if (winner == 0) ally_r += 0.5;
     if (winner == 1) enemy_r += 0.5;
 #pragma unroll
     for (int j = 0; j < UPL; ++j) {
       const int a = g.gl + G * j;
       if (a >= A) continue;
-      const int team = a < P.na ? 0 : 1;
+      const int team = a < e.na(P) ? 0 : 1;
       lc.v.rewards[i * A + a] = team == 0 ? ally_r : enemy_r;
       double* inf = lc.v.infos + (i * A + a) * 3;
       inf[0] = e.h[a] > 0.0 ? 1.0 : 0.0;   // alive
@@ -899,7 +902,7 @@ __global__ void __launch_bounds__(kThreads, 3) smax_step_kernel(const Params* __
     if (g.gl == 0) {
       double sum = 0.0;
 #pragma unroll 1
-      for (int a = 0; a < A; ++a) sum += a < P.na ? ally_r : enemy_r;
+      for (int a = 0; a < A; ++a) sum += a < e.na(P) ? ally_r : enemy_r;
       ep_ret = ep_ret + sum / double(A);  // team_reward, vector_env.cpp:14-18,99
       ep_len = ep_len + 1;
       lc.v.dones[i * (A + 1) + A] = done;
@@ -1110,7 +1113,7 @@ void launch_step_g(const SmaxConfig& c, const Params* dP, const SmaxState& s, co
   bool marines = !c.random_types;
   for (int u = 0; u < c.na + c.ne && marines; ++u) marines = c.type[u] == 0;
   if (std::getenv("MARL_SMAX_GENERIC")) marines = false;
-  const bool full = c.na + c.ne == G * UPL && !std::getenv("MARL_SMAX_GENERIC");
+  const bool full = c.na + c.ne == G * UPL && c.na == c.ne && !std::getenv("MARL_SMAX_GENERIC");
   auto pick = [&](auto ht, auto fu) {
     return random ? smax_step_kernel<G, UPL, true, decltype(ht)::value, decltype(fu)::value>
                   : smax_step_kernel<G, UPL, false, decltype(ht)::value, decltype(fu)::value>;
