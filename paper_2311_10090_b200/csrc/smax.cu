@@ -79,9 +79,10 @@ static_assert(sizeof(Params) % 16 == 0, "Params is staged with 16-byte copies");
 // One env's unit state during a step (shared memory).
 // HT >= 0: every unit of the roster has type HT (fixed single-type rosters such
 // as 3m / 5m_vs_6m / 27m_vs_30m): type lookups fold to compile-time constants.
-// FU: the roster fills the lane group exactly with two equal teams (n == CAP,
-// na == ne: 3m, 2s3z): unit and team counts are compile-time constants and the
-// u < n / team tests fold.
+// FU: the roster fills the lane group exactly with two equal teams and only the
+// allies are agents (n == CAP, na == ne == A: 3m, 2s3z): unit, team, agent
+// counts and the observation width are compile-time constants and the u < n /
+// team tests fold.
 template <int CAP, int HT = -1, bool FU = false>
 struct EnvSm {
   double x[CAP], y[CAP], h[CAP], cd[CAP];
@@ -676,7 +677,7 @@ __device__ __noinline__ void emit_obs(const Params& P, const EnvSm<CAP, HT, FU>&
                                          float* tile, float* __restrict__ gdst, int64_t w0, int wvalid, int rb,
                                          unsigned sel) {
   constexpr int EPW = Grp<G>::EPW;
-  const int A = P.A, D = P.D;
+  const int A = FU ? CAP / 2 : P.A, D = FU ? 10 + 17 * (CAP - 1) : P.D;
   const int wslot = (threadIdx.x & 31) / G;  // >= EPW only on dead lanes, which never build rows
   for (int a0 = 0; a0 < A; a0 += rb) {
     const int rows = min(rb, A - a0);
@@ -819,7 +820,7 @@ __global__ void __launch_bounds__(kThreads, 3) smax_step_kernel(const Params* __
   const int wvalid = int(max(int64_t(0), min64(EPW, lc.end - w0)));
   if (wvalid == 0) return;  // whole warp past the end (warp-uniform)
   const bool live = !g.dead && i < lc.end;
-  const int A = P.A;
+  const int A = FU ? CAP / 2 : P.A;
 
   int tg[UPL], sw[UPL];
   Key carry{0, 0, 0, 0};
@@ -1113,7 +1114,7 @@ void launch_step_g(const SmaxConfig& c, const Params* dP, const SmaxState& s, co
   bool marines = !c.random_types;
   for (int u = 0; u < c.na + c.ne && marines; ++u) marines = c.type[u] == 0;
   if (std::getenv("MARL_SMAX_GENERIC")) marines = false;
-  const bool full = c.na + c.ne == G * UPL && c.na == c.ne && !std::getenv("MARL_SMAX_GENERIC");
+  const bool full = c.na + c.ne == G * UPL && c.na == c.ne && !c.enemy_controlled && !std::getenv("MARL_SMAX_GENERIC");
   auto pick = [&](auto ht, auto fu) {
     return random ? smax_step_kernel<G, UPL, true, decltype(ht)::value, decltype(fu)::value>
                   : smax_step_kernel<G, UPL, false, decltype(ht)::value, decltype(fu)::value>;
