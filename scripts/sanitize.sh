@@ -10,9 +10,13 @@ from paper_2311_10090_b200.ppo import PpoTrainer, permutation
 prec = sys.argv[1]
 n, T = 512, 16
 cfg = {"n_envs": n, "n_rollout_steps": T, "total_timesteps": 2 * n * T}
-tr = PpoTrainer(m.VectorEnv(m.make_env("MPE_simple_spread_v3", {}), n), cfg, False, prec)
-r = tr.train(m.prng.key_from_seed(0))
-print("ppo", prec, r.metrics.as_array()[-1][:8])
+# MPE (Kx 32: two tiles in flight), SMAX 3m (Kx 96, two X buffers), 5m_vs_6m (Kx 192, one X buffer;
+# the policy reads observation rows through L2)
+for env_id, ecfg in [("MPE_simple_spread_v3", {}), ("SMAX_5m_vs_6m", {"ally_units": ["marine"] * 3,
+                     "enemy_units": ["marine"] * 3}), ("SMAX_5m_vs_6m", {})]:
+    tr = PpoTrainer(m.VectorEnv(m.make_env(env_id, ecfg), n), cfg, False, prec)
+    r = tr.train(m.prng.key_from_seed(0))
+    print("ppo", env_id, prec, r.metrics.as_array()[-1][:8])
 print("perm", permutation(m.prng.key_from_seed(1), 1000).sum().item())
 PY
 cat > /tmp/san_env.py <<'PY'
@@ -21,6 +25,7 @@ import paper_2311_10090_b200 as m
 from paper_2311_10090_b200 import prng as O
 for env_id, cfg, n in [("MPE_simple_speaker_listener_v4", {"continuous_actions": True}, 300),
                        ("SMAX_5m_vs_6m", {"ally_units": ["marine"]*3, "enemy_units": ["marine"]*3}, 33000),
+                       ("SMAX_2s3z", {}, 5000), ("SMAX_5m_vs_6m", {}, 5000),
                        ("overcooked_cramped_room_v0", {"max_steps": 3}, 33000)]:
     v = m.VectorEnv(env_id, n, config=cfg)
     v.reset(O.key_from_seed(1))
