@@ -37,4 +37,10 @@ timeout 900 $NCU --set full --clock-control none --import-source on -k regex:ppo
 timeout 900 $NCU --set full --clock-control none --import-source on -k regex:ppo_update_tc -s 20 -c 1 \
   -o gpurun_out/prof_${TAG}_ppo_update -f python bench.py --workload ppo --steps 1 --warmup 3 --no-cpu --no-e2e \
   > /dev/null 2>&1
+# summarise the step-kernel captures here and keep only what fits gpurun's 64 MiB return
+python scripts/ncu_summary.py ${TAG} smax3m mpe_large overcooked smax27m > /dev/null 2>&1
+mkdir -p gpurun_out/summary_${TAG}
+cp profiles/${TAG}_* profiles/ncu_traffic.json profiles/ncu_metrics.json gpurun_out/summary_${TAG}/ 2>/dev/null
+rm -f gpurun_out/prof_${TAG}_mpe_large.ncu-rep gpurun_out/prof_${TAG}_smax27m.ncu-rep gpurun_out/prof_${TAG}_overcooked.ncu-rep
+du -sh gpurun_out
 ls gpurun_out | grep ${TAG}
