@@ -194,7 +194,17 @@ __device__ __forceinline__ void separation_pass(const Params& P, EnvSm<CAP, HT, 
     while (row) {  // group-uniform
       bool hit[UPL];
       double hdx[UPL], hdy[UPL], hd[UPL];
-      const double xa = e.x[a], ya = e.y[a];
+      // a's position is read only by lanes that test a pair of the row, and
+      // every value read feeds the ballot below, so all reads of x[a], y[a]
+      // have completed before b's lane (past the ballot) writes them.
+      bool mine = false;
+#pragma unroll
+      for (int j = 0; j < UPL; ++j) mine |= (row >> (g.gl + G * j) & 1ull) != 0;
+      double xa = 0.0, ya = 0.0;
+      if (mine) {
+        xa = e.x[a];
+        ya = e.y[a];
+      }
 #pragma unroll
       for (int j = 0; j < UPL; ++j) {
         const int b = g.gl + G * j;
