@@ -12,8 +12,9 @@ n, T = 512, 16
 cfg = {"n_envs": n, "n_rollout_steps": T, "total_timesteps": 2 * n * T}
 # MPE (Kx 32: two tiles in flight), SMAX 3m (Kx 96, two X buffers), 5m_vs_6m (Kx 192, one X buffer;
 # the policy reads observation rows through L2)
-for env_id, ecfg in [("MPE_simple_spread_v3", {}), ("SMAX_5m_vs_6m", {"ally_units": ["marine"] * 3,
-                     "enemy_units": ["marine"] * 3}), ("SMAX_5m_vs_6m", {})]:
+envs = [("MPE_simple_spread_v3", {}), ("SMAX_5m_vs_6m", {"ally_units": ["marine"] * 3,
+         "enemy_units": ["marine"] * 3}), ("SMAX_5m_vs_6m", {})]
+for env_id, ecfg in envs[:1] if len(sys.argv) > 2 and sys.argv[2] == "mpe" else envs:
     tr = PpoTrainer(m.VectorEnv(m.make_env(env_id, ecfg), n), cfg, False, prec)
     r = tr.train(m.prng.key_from_seed(0))
     print("ppo", env_id, prec, r.metrics.as_array()[-1][:8])
@@ -40,8 +41,10 @@ for prec in fp32 bf16; do
   timeout 900 $CS --tool memcheck --leak-check no --error-exitcode 9 python /tmp/san_ppo.py $prec > gpurun_out/san_memcheck_ppo_$prec.log 2>&1
   echo "memcheck ppo $prec rc=$?"; grep -E "ERROR SUMMARY|Invalid|race" gpurun_out/san_memcheck_ppo_$prec.log | head -5
 done
-timeout 900 $CS --tool racecheck --error-exitcode 9 python /tmp/san_ppo.py fp32 > gpurun_out/san_racecheck_ppo.log 2>&1
+timeout 900 $CS --tool racecheck --error-exitcode 9 python /tmp/san_ppo.py fp32 mpe > gpurun_out/san_racecheck_ppo.log 2>&1
 echo "racecheck ppo fp32 rc=$?"; grep -E "ERROR SUMMARY|RACECHECK SUMMARY|hazard" gpurun_out/san_racecheck_ppo.log | head -5
+timeout 900 $CS --tool racecheck python scripts/race_smax.py > gpurun_out/san_racecheck_smax.log 2>&1
+echo "racecheck smax rc=$?"; grep -E "RACECHECK SUMMARY|Race reported" gpurun_out/san_racecheck_smax.log | sort | uniq -c | head -5
 fi
 timeout 900 $CS --tool memcheck --leak-check no --error-exitcode 9 python /tmp/san_env.py > gpurun_out/san_memcheck_env.log 2>&1
 echo "memcheck env rc=$?"; grep -E "ERROR SUMMARY|Invalid" gpurun_out/san_memcheck_env.log | head -5
