@@ -51,7 +51,7 @@ constexpr int kNorth = 0, kSouth = 1, kEast = 2, kWest = 3, kStop = 4, kAttackBa
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kTypes = 6;
-constexpr int kWarpStageBytes = 8 * 1024;  // observation staging budget per warp
+constexpr int kWarpStageBytes = 4 * 1024;  // observation staging budget per warp
 
 struct TypeStat {  // per unit type (smax.cpp:26-33), derived on the host
   double hmax, dmg, cdmax, spdt, rad, hi;  // spdt = speed * dt, hi = map - radius
@@ -814,7 +814,7 @@ __global__ void __launch_bounds__(kThreads) smax_reset_kernel(const Params* __re
 }
 
 template <int G, int UPL, bool RANDOM, int HT, bool FU>
-__global__ void __launch_bounds__(kThreads, 3) smax_step_kernel(const Params* __restrict__ gP, SmaxState st,
+__global__ void __launch_bounds__(kThreads, 4) smax_step_kernel(const Params* __restrict__ gP, SmaxState st,
                                                              LaunchCommon lc, Key step_key, Plan plan) {
   constexpr int EPW = Grp<G>::EPW, EPB = kWarps * EPW, CAP = G * UPL;
   extern __shared__ __align__(16) uint8_t smem[];
