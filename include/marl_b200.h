@@ -328,6 +328,10 @@ void marl_threefry2x32(uint32_t k0, uint32_t k1, uint32_t x0, uint32_t x1, uint3
 /* ---- diagnostics ------------------------------------------------------ */
 const char* marl_last_error(void);
 uint64_t marl_launch_count(void); /* kernels launched by this library */
+/* Test knob: cap the grid of every persistent (grid-stride / tile-loop) kernel
+ * at `ctas` CTAs (0 = no cap) so small inputs exercise the steady state of the
+ * loops; returns the previous cap.  No reference counterpart. */
+int marl_set_grid_cap(int ctas);
 const char* marl_version(void);
 
 #ifdef __cplusplus

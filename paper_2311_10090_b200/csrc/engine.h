@@ -418,4 +418,10 @@ void launch_validate_box(const float* actions, int64_t n, int A, const int32_t* 
 // Kernel launches issued by this library since load (evidence counter).
 extern unsigned long long g_launches;
 
+// Test knob (marl_set_grid_cap): upper bound on the grid of every persistent
+// (grid-stride / tile-loop) kernel, so small parity inputs drive each CTA or
+// warp through several iterations of its loop.  0 = no cap (the default).
+extern int g_grid_cap;
+inline int64_t cap_grid(int64_t g) { return g_grid_cap > 0 && g > g_grid_cap ? int64_t(g_grid_cap) : g; }
+
 }  // namespace marl_b200

@@ -538,7 +538,7 @@ void oc_launch_step_t(const OcConfig& c, const float* templ, const OcState& s, c
   const int64_t chunks = (lc.end - lc.begin + 31) / 32;
   const int64_t want = (chunks + warps - 1) / warps;
   const int64_t cap = int64_t(std::max(per_sm, 1)) * sms;
-  fn<<<unsigned(std::min(want, cap)), warps * 32, sm, lc.stream>>>(c, templ, s, lc, to_key(step_key), tma);
+  fn<<<unsigned(cap_grid(std::min(want, cap))), warps * 32, sm, lc.stream>>>(c, templ, s, lc, to_key(step_key), tma);
   ++g_launches;
 }
 

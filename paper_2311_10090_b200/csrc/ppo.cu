@@ -1104,7 +1104,7 @@ int ppo_branch_grid(int in, int W, int out, int64_t M) {
   }
   const int per_sm = std::max(1, int((228 * 1024) / (sm + 2048)));
   const int64_t tiles = (M + TR - 1) / TR;
-  return int(std::max<int64_t>(1, std::min<int64_t>(tiles, int64_t(sms) * std::min(per_sm, 2))));
+  return int(cap_grid(std::max<int64_t>(1, std::min<int64_t>(tiles, int64_t(sms) * std::min(per_sm, 2)))));
 }
 
 template <bool ACTOR>

@@ -638,6 +638,7 @@ void ppo_update_impl(marl_ppo* p, double row[12], int* diverged) {
   cuda_check(cudaMemsetAsync(p->flags, 0, 2 * sizeof(int), st), "cudaMemset");
   cuda_check(cudaMemsetAsync(p->metrics, 0, size_t(n_mb_total) * 8 * sizeof(double), st), "cudaMemset");
   tc_obs(p);
+  const int64_t adam_t0 = p->adam_t;
   int k = 0;
   for (int epoch = 0; epoch < c.update_epochs; ++epoch) {
     uint32_t pk[4];
@@ -667,6 +668,10 @@ void ppo_update_impl(marl_ppo* p, double row[12], int* diverged) {
     for (int j = 0; j < 7; ++j) sums[j] += m[size_t(q) * 8 + j];
     ++n_mb;
   }
+  // AdamState::t counts only the updates adam_update applied (nn.hpp:420-426):
+  // minibatch_apply advanced it for every launched minibatch, including those
+  // the device skipped after a DivergenceError
+  p->adam_t = adam_t0 + n_mb;
   if (flags[0]) {  // roll back to the last completed update (ppo.cpp:630-634)
     cuda_check(cudaMemcpyAsync(r->params, p->snapshot, size_t(p->P) * 4, cudaMemcpyDeviceToDevice, st), "cudaMemcpy");
   }
@@ -976,10 +981,13 @@ int marl_ppo_minibatch_grad(marl_ppo* p, const int32_t* d_idx, int64_t M, float*
     cuda_check(cudaMemcpyAsync(flags, p->flags, sizeof flags, cudaMemcpyDeviceToHost, st), "D2H");
     cuda_check(cudaStreamSynchronize(st), "cudaStreamSynchronize");
     if (flags[1]) raise(MARL_ERR_CONTRACT, "nn: ppo_row_loss: stored action not legal");
+    // with an all-reduce hook, minibatch_grad already folded the per-CTA rows
+    // into row 0 (and summed it over the ranks): read that row only
+    const int na = p->hook ? 1 : p->grid_a, nc = p->hook ? 1 : p->grid_c;
     double s[6] = {0, 0, 0, 0, 0, 0}, vt = 0.0;
-    for (int c = 0; c < p->grid_a; ++c)
+    for (int c = 0; c < na; ++c)
       for (int j = 0; j < 6; ++j) s[j] += sa[size_t(c) * 6 + j];
-    for (int c = 0; c < p->grid_c; ++c) vt += sc[size_t(c) * 6 + 1];
+    for (int c = 0; c < nc; ++c) vt += sc[size_t(c) * 6 + 1];
     const double tw = ms.total_w;
     if (tw > 0.0) {
       stats_out[0] = double(float((s[0] + p->cfg.vf_coef * vt - p->cfg.ent_coef * s[2]) / tw));
@@ -999,6 +1007,8 @@ int marl_ppo_minibatch_grad(marl_ppo* p, const int32_t* d_idx, int64_t M, float*
 int marl_ppo_set_allreduce(marl_ppo* p, marl_allreduce_fn fn, void* ctx) {
   return guarded([&] {
     if (!p) raise(MARL_ERR_CONTRACT, "marl_ppo_set_allreduce: NULL handle");
+    if (p->recurrent && fn)
+      raise(MARL_ERR_CONTRACT, "ppo: the data-parallel update covers feed-forward policies only (recurrent=true)");
     p->hook = fn;
     p->hook_ctx = ctx;
   });
@@ -1021,6 +1031,8 @@ int marl_ppo_set_nccl(marl_ppo* p, const uint8_t id[128], int rank, int world) {
   return guarded([&] {
     if (!p || !id) raise(MARL_ERR_CONTRACT, "marl_ppo_set_nccl: NULL argument");
     if (world < 1 || rank < 0 || rank >= world) raise(MARL_ERR_CONTRACT, "marl_ppo_set_nccl: bad rank / world");
+    if (p->recurrent)
+      raise(MARL_ERR_CONTRACT, "ppo: the data-parallel update covers feed-forward policies only (recurrent=true)");
     set_device(p->h);
     ncclUniqueId uid;
     std::memcpy(&uid, id, 128);

@@ -650,7 +650,7 @@ int ppo_tc_grid(int64_t M) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
   const int64_t tiles = (M + kRows - 1) / kRows;
-  return int(std::max<int64_t>(1, std::min<int64_t>(tiles, sms)));
+  return int(cap_grid(std::max<int64_t>(1, std::min<int64_t>(tiles, sms))));
 }
 
 void ppo_tc_pack(const PpoTcPack& p, cudaStream_t s) {

@@ -663,7 +663,7 @@ void rollout_policy_bf16(const PolicyNet& net, const PolicyNetBf16& nb, const Po
   if (const char* f = std::getenv("MARL_TC_FORCE_PER_SM")) per_sm = std::atoi(f);
   if (std::getenv("MARL_TC_DEBUG")) std::fprintf(stderr, "policy_tc: smem %zu per_sm %d\n", sm, per_sm);
   const int64_t tiles = (s.R + kTcRows - 1) / kTcRows;
-  const int64_t grid = std::min<int64_t>(tiles, int64_t(sms) * per_sm);
+  const int64_t grid = cap_grid(std::min<int64_t>(tiles, int64_t(sms) * per_sm));
   kern<<<unsigned(grid), kSplit * kTcRows, sm, st>>>(nb, net.in_dim, net.n_act, s, b);
   ++g_launches;
 }

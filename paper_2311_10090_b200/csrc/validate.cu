@@ -11,6 +11,7 @@
 namespace marl_b200 {
 
 unsigned long long g_launches = 0;
+int g_grid_cap = 0;
 
 namespace {
 __global__ void validate_kernel(const int32_t* __restrict__ actions, int64_t total, int A,

@@ -566,6 +566,11 @@ extern "C" {
 
 const char* marl_last_error(void) { return g_err.c_str(); }
 uint64_t marl_launch_count(void) { return g_launches; }
+int marl_set_grid_cap(int ctas) {
+  const int old = g_grid_cap;
+  g_grid_cap = ctas > 0 ? ctas : 0;
+  return old;
+}
 const char* marl_version(void) { return "marl-b200 0.1 (sm_100a)"; }
 
 int marl_registered_count(void) { return int(registered().size()); }
@@ -708,6 +713,7 @@ int marl_venv_step(marl_venv* h, const int32_t* d_actions) {
 
 int marl_venv_step_random(marl_venv* h, const uint32_t step_key[4]) {
   return guarded([&] {
+    if (!h || !step_key) raise(MARL_ERR_CONTRACT, "marl_venv_step_random: NULL argument");
     set_device(h);
     launch_step(h, true, step_key, nullptr);
   });
@@ -715,6 +721,7 @@ int marl_venv_step_random(marl_venv* h, const uint32_t step_key[4]) {
 
 int marl_venv_step_host(marl_venv* h, const int32_t* h_actions, const marl_host_step* out) {
   return guarded([&] {
+    if (!h || !h_actions) raise(MARL_ERR_CONTRACT, "marl_venv_step_host: NULL argument");
     set_device(h);
     require_state(h);
     const Env& e = *h->env;
@@ -740,6 +747,7 @@ int marl_venv_step_host(marl_venv* h, const int32_t* h_actions, const marl_host_
 
 int marl_venv_step_random_host(marl_venv* h, const uint32_t step_key[4], const marl_host_step* out) {
   return guarded([&] {
+    if (!h || !step_key) raise(MARL_ERR_CONTRACT, "marl_venv_step_random_host: NULL argument");
     set_device(h);
     require_state(h);
     if (out) {

@@ -1,0 +1,122 @@
+"""Steady state of the persistent kernels, at sizes the checkers can afford.
+
+The policy, PPO-update and fused Overcooked kernels loop over tiles / env
+chunks with one CTA (or a few) per SM; at the parity tests' sizes every CTA
+sees at most one tile, so the cross-tile paths (TMA prefetch of the next
+observation tile, double-buffered TMEM / mbarrier phases, gradient
+accumulation over a CTA's tiles, two tiles in flight) never ran under test.
+marl_set_grid_cap(k) caps those grids at k CTAs, so here each CTA walks tens
+of tiles:
+
+* policy_tc_kernel (bf16 tcgen05): the capped rollout equals the uncapped one
+  bit for bit (every row is computed by exactly one tile, whichever CTA runs
+  it) and agrees with the fp32 path at the first step;
+* ppo_update_tc_kernel (NS = 2 for MPE, NS = 1 for SMAX 3m) and the fp32
+  ppo_branch_tiled_kernel: one minibatch of >= 50k rows through 1-2 CTAs vs
+  the reference's ff_minibatch on the same buffer.
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+from _util import THREE_M
+
+pytestmark = pytest.mark.gpu
+
+
+def _need_ref():
+    if not O.ref_available():
+        pytest.skip("compiled reference (oracle/_ref) not built")
+
+
+class _Cap:
+    def __init__(self, k):
+        from paper_2311_10090_b200 import _native
+        self.L, self.k = _native.lib(), k
+
+    def __enter__(self):
+        self.old = self.L.marl_set_grid_cap(self.k)
+
+    def __exit__(self, *exc):
+        self.L.marl_set_grid_cap(self.old)
+
+
+def _collect(env_id, cfg, n, T, precision, key, a, c):
+    import paper_2311_10090_b200 as m
+    from paper_2311_10090_b200.rollout import IppoRollout
+    v = m.VectorEnv(m.make_env(env_id, cfg), n, device=0)
+    ro = IppoRollout(v, T, precision=precision)
+    ro.set_params(a, c)
+    ro.begin(key)
+    return {k: t.cpu().numpy().copy() for k, t in ro.collect().items()}
+
+
+@pytest.mark.parametrize("env_id,cfg,n", [("MPE_simple_spread_v3", {}, 4096), ("SMAX_5m_vs_6m", THREE_M, 2048)])
+def test_policy_tc_capped_grid_equals_full_grid(env_id, cfg, n):
+    _need_ref()
+    key = O.key_from_seed(17)
+    a, c = O.ref_ppo_init(env_id, cfg, O.fold_in(key, 10))
+    T = 6
+    full = _collect(env_id, cfg, n, T, "bf16", key, a, c)
+    for k in (1, 3):
+        with _Cap(k):
+            capped = _collect(env_id, cfg, n, T, "bf16", key, a, c)
+        for f, x in full.items():
+            assert np.array_equal(capped[f], x, equal_nan=True), (k, f)
+    f32 = _collect(env_id, cfg, n, T, "fp32", key, a, c)
+    assert np.array_equal(f32["obs"][0], full["obs"][0])
+    assert np.allclose(full["value"][0], f32["value"][0], rtol=0.05, atol=0.03)
+    assert (full["actions"][0] == f32["actions"][0]).mean() >= 0.97
+
+
+def _trainer(env_id, cfg, n_envs, T, precision):
+    import paper_2311_10090_b200 as m
+    from paper_2311_10090_b200.ppo import PpoTrainer
+    v = m.VectorEnv(m.make_env(env_id, cfg), n_envs, device=0)
+    pc = {"n_envs": n_envs, "n_rollout_steps": T, "total_timesteps": 4 * n_envs * T, "n_minibatches": 1}
+    return PpoTrainer(v, pc, False, precision)
+
+
+def _cos(a, b):
+    return float(np.dot(a, b) / (np.linalg.norm(a) * np.linalg.norm(b) + 1e-30))
+
+
+def _blocks(sp):
+    W, I, NA = sp.width, sp.in_dim, sp.n_actions
+    out, off = [], 0
+    for n in (W * I, W, W * W, W, NA * W, NA, W * I, W, W * W, W, W, 1):
+        out.append((off, off + n))
+        off += n
+    return out
+
+
+# MPE: in 18, Kx 32, two tiles in flight (NS = 2); SMAX 3m: in 95, Kx 96, NS = 1
+@pytest.mark.parametrize("env_id,cfg,n_envs", [("MPE_simple_spread_v3", {}, 1024), ("SMAX_5m_vs_6m", THREE_M, 1024)])
+@pytest.mark.parametrize("precision,cap", [("bf16", 1), ("bf16", 2), ("fp32", 2)])
+def test_update_kernel_steady_state_matches_ff_minibatch(env_id, cfg, n_envs, precision, cap):
+    _need_ref()
+    T = 24
+    with _Cap(cap):
+        tr = _trainer(env_id, cfg, n_envs, T, precision)
+        assert tr.tensor_core_update == (precision == "bf16")
+        tr.begin(O.key_from_seed(61))
+        tr.collect()
+        buf = {k: t.cpu().numpy() for k, t in tr.rollout._views.items()}
+        a, c = tr.params()
+        R = tr.rollout.R
+        M = 50_000
+        idx = np.random.default_rng(9).choice(T * R, size=M, replace=False).astype(np.int32)
+        g, st = tr.minibatch_grad(idx)
+    gr, sr = O.ref_ff_minibatch(env_id, cfg, a, c, buf, idx)
+    if precision == "bf16":
+        for lo, hi in _blocks(tr.spec):
+            x, y = g[lo:hi], gr[lo:hi]
+            if np.linalg.norm(y) < 1e-12:
+                continue
+            assert _cos(x, y) >= 0.995, (lo, hi, _cos(x, y))
+            assert abs(np.linalg.norm(x) / np.linalg.norm(y) - 1) < 0.03, (lo, hi)
+        assert np.allclose(st, sr, rtol=2e-2, atol=1e-4), (st, sr)
+    else:
+        tol = 2e-3 * np.abs(gr) + 1e-4 * np.abs(gr).max()
+        assert np.all(np.abs(g - gr) <= tol), np.abs(g - gr).max()
+        assert np.allclose(st, sr, rtol=1e-5, atol=1e-7), (st, sr)
