@@ -46,10 +46,19 @@ def _stale(src, obj, deps):
     return any(os.path.getmtime(p) > t for p in [src] + deps)
 
 
+def _obj_dir():
+    extra = os.environ.get("MARL_NVCC_EXTRA", "")
+    if not extra:
+        return OBJ
+    import hashlib  # development flags get their own objects (never mixed into a release build)
+    return OBJ + "_" + hashlib.sha1(extra.encode()).hexdigest()[:8]
+
+
 def _compile(src, verbose):
-    obj = os.path.join(OBJ, os.path.basename(src) + ".o")
+    obj = os.path.join(_obj_dir(), os.path.basename(src) + ".o")
     if src.endswith(".cu"):
-        cmd = [NVCC] + NVCC_FLAGS + (["-Xptxas", "-v"] if verbose else []) + ["-c", src, "-o", obj]
+        extra = os.environ.get("MARL_NVCC_EXTRA", "").split()  # development-only defines
+        cmd = [NVCC] + NVCC_FLAGS + extra + (["-Xptxas", "-v"] if verbose else []) + ["-c", src, "-o", obj]
     else:
         cmd = [os.environ.get("CXX", "g++")] + CXX_FLAGS + ["-c", src, "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
@@ -61,23 +70,27 @@ def _compile(src, verbose):
 def build(verbose: bool = False, force: bool = False) -> str:
     if not os.path.exists(NVCC):
         raise RuntimeError(f"nvcc not found at {NVCC}")
-    os.makedirs(OBJ, exist_ok=True)
+    os.makedirs(_obj_dir(), exist_ok=True)
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")) + glob.glob(os.path.join(CSRC, "*.cpp")))
     deps = _headers()
-    todo = [s for s in srcs if force or _stale(s, os.path.join(OBJ, os.path.basename(s) + ".o"), deps)]
+    todo = [s for s in srcs if force or _stale(s, os.path.join(_obj_dir(), os.path.basename(s) + ".o"), deps)]
     logs = []
     if todo:
         with cf.ThreadPoolExecutor(max_workers=min(8, len(todo))) as ex:
             for obj, log in ex.map(lambda s: _compile(s, verbose), todo):
                 logs.append(log)
-    objs = [os.path.join(OBJ, os.path.basename(s) + ".o") for s in srcs]
-    if todo or not os.path.exists(LIB) or any(os.path.getmtime(o) > os.path.getmtime(LIB) for o in objs):
+    objs = [os.path.join(_obj_dir(), os.path.basename(s) + ".o") for s in srcs]
+    stamp = LIB + ".objdir"
+    same_dir = os.path.exists(stamp) and open(stamp).read() == _obj_dir()
+    if todo or not same_dir or not os.path.exists(LIB) or any(os.path.getmtime(o) > os.path.getmtime(LIB) for o in objs):
         tmp = LIB + ".tmp"
         cmd = [NVCC] + ARCH + ["-shared", "-o", tmp] + objs + ["-lcudart_static", "-lrt", "-lpthread", "-ldl"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed: {' '.join(cmd)}\n{r.stdout}\n{r.stderr}")
         shutil.move(tmp, LIB)
+        with open(stamp, "w") as f:
+            f.write(_obj_dir())
     if verbose:
         for log in logs:
             sys.stderr.write(log)

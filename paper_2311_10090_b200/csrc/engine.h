@@ -100,6 +100,7 @@ struct SmaxConfig {
   int8_t type[kSmaxMaxUnits];     // per unit
   double stats[6][7];             // health damage cooldown speed sight range radius
   void* dev_params = nullptr;     // device copy of the derived constants (smax_prepare)
+  void* host_params = nullptr;    // host copy (passed by value to the one-thread-per-env kernel)
 };
 
 // Upload / free the derived per-unit constants for a config (once per handle).

@@ -40,41 +40,11 @@
 
 #include "common.cuh"
 #include "engine.h"
+#include "smax_params.cuh"
 
 namespace marl_b200 {
 namespace {
-
-constexpr double kDt = 1.0 / 16.0;  // smax.cpp:17
-constexpr int kTicks = 8;           // smax.cpp:18
-constexpr double kSepTol = 1e-6;    // smax.cpp:19
-constexpr int kNorth = 0, kSouth = 1, kEast = 2, kWest = 3, kStop = 4, kAttackBase = 5;
-constexpr int kThreads = 256;
-constexpr int kWarps = kThreads / 32;
-constexpr int kTypes = 6;
-constexpr int kWarpStageBytes = 4 * 1024;  // observation staging budget per warp
-
-struct TypeStat {  // per unit type (smax.cpp:26-33), derived on the host
-  double hmax, dmg, cdmax, spdt, rad, hi;  // spdt = speed * dt, hi = map - radius
-  Thresh sight;
-};
-struct PairStat {  // per (type a, type b)
-  Thresh reach;  // range(a) + radius(a) + radius(b), smax.cpp:497-501
-  Thresh rsum;   // radius(a) + radius(b), smax.cpp:551
-  Thresh otol;   // rsum - 1e-6: the max_overlap tolerance, smax.cpp:565,576
-};
-
-// Per-handle constants, staged into shared memory by every block (~3 KB).
-struct Params {
-  int na, ne, n, A, controlled, max_steps, D, n_pairs;
-  double map, jitter;
-  double sep_r2hi;  // max rsum.r2hi over the roster's type pairs: conservative overlap pre-check
-  int random_types;  // smacv2_*: per-episode random unit types and spawns (smax.cpp:169-181, 456-479)
-  int pad_;
-  int8_t type[kSmaxMaxUnits];
-  TypeStat ts[kTypes];
-  PairStat ps[kTypes][kTypes];
-};
-static_assert(sizeof(Params) % 16 == 0, "Params is staged with 16-byte copies");
+using namespace smax;
 
 // One env's unit state during a step (shared memory).
 // HT >= 0: every unit of the roster has type HT (fixed single-type rosters such
@@ -118,10 +88,6 @@ struct Grp {
   __device__ __forceinline__ int count(bool p) const { return __popc(__ballot_sync(mask, p) & mask); }
   __device__ __forceinline__ double bcast(double v, int src) const { return __shfl_sync(mask, v, base + src); }
 };
-
-__device__ __forceinline__ double dclamp(double v, double lo, double hi) {  // std::clamp
-  return (v < lo) ? lo : (hi < v) ? hi : v;
-}
 
 template <int CAP, int HT, bool FU>
 __device__ __forceinline__ bool in_range(const Params& P, const EnvSm<CAP, HT, FU>& e, int a, int b) {
@@ -338,13 +304,6 @@ __device__ __forceinline__ void separate(const Params& P, EnvSm<CAP, HT, FU>& e,
 }
 
 // ------------------------------------------------------------- unit logic
-// uniform1(key, lo, hi) (prng.cpp:169-178) through the out-of-line block.
-__device__ __forceinline__ double uniform_at_nl(const Key& k, double lo, double hi) {
-  double v = lo + to_unit(block_at_nl(k, 0)) * (hi - lo);
-  if (v >= hi) v = nextafter(hi, lo);
-  return v;
-}
-
 // Spawn of unit u: spawn_clusters / place_jittered (smax.cpp:448-454,481-492),
 // or spawn_smacv2 (smax.cpp:456-479) for the random-type scenarios; the
 // unit's type (e.T(u)) is already set.
@@ -421,15 +380,6 @@ __device__ __forceinline__ int random_legal(const Params& P, const EnvSm<CAP, HT
   if (pick < kAttackBase) return pick;
   for (pick -= kAttackBase; pick > 0; --pick) att &= att - 1;  // drop the lowest set bits
   return kAttackBase + __ffsll((long long)att) - 1;
-}
-
-// Is hypot(dxa, dya) < hypot(dxb, dyb)?  Decided from the squared lengths
-// outside a 2e-12 relative band (both hypots are within an ulp of the true
-// lengths), by the glibc-exact hypot inside it.
-__device__ __forceinline__ bool hypot_less(double dxa, double dya, double d2a, double dxb, double dyb, double d2b) {
-  if (d2a < d2b * (1.0 - 2e-12)) return true;
-  if (d2a > d2b * (1.0 + 2e-12)) return false;
-  return hypot_glibc(dxa, dya) < hypot_glibc(dxb, dyb);
 }
 
 // heuristic_action (smax.cpp:374-419) of unit u on the pre-step state.
@@ -644,15 +594,6 @@ template <int G, int UPL>
 __host__ __device__ inline size_t smem_bytes(int D, int rb) {
   constexpr int EPB = kWarps * Grp<G>::EPW, CAP = G * UPL;
   return a16(sizeof(Params)) + a16(EPB * sizeof(EnvSm<CAP>)) + kWarps * warp_tile_floats<G>(D, rb) * 4;
-}
-
-__device__ __forceinline__ void stage_params(Params* dst, const Params* __restrict__ src) {
-  const int words = int(sizeof(Params) / 16);
-  const int4* s = reinterpret_cast<const int4*>(src);
-  int4* d = reinterpret_cast<int4*>(dst);
-#pragma unroll 1
-  for (int q = threadIdx.x; q < words; q += blockDim.x) d[q] = __ldg(s + q);
-  __syncthreads();
 }
 
 // Copy nfloats from shared to global with one warp: 16-byte vectors when both
@@ -1039,50 +980,6 @@ __global__ void smax_world_state_kernel(const Params* __restrict__ gP, SmaxState
 }
 
 // ------------------------------------------------------------------ host
-Key to_key(KeyWords k) { return Key{k.w[0], k.w[1], k.w[2], k.w[3]}; }
-
-Params make_params(const SmaxConfig& c) {
-  Params P{};
-  P.na = c.na;
-  P.ne = c.ne;
-  P.n = c.na + c.ne;
-  P.A = c.na + (c.enemy_controlled ? c.ne : 0);
-  P.controlled = c.enemy_controlled;
-  P.max_steps = c.max_steps;
-  P.D = 10 + 17 * (P.n - 1);
-  P.n_pairs = P.n * (P.n - 1) / 2;
-  P.map = c.map;
-  P.jitter = c.jitter;
-  for (int u = 0; u < P.n; ++u) P.type[u] = c.type[u];
-  P.random_types = c.random_types;
-  for (int t = 0; t < kTypes; ++t) {
-    const double* st = c.stats[t];  // health damage cooldown speed sight range radius
-    TypeStat& T = P.ts[t];
-    T.hmax = st[0];
-    T.dmg = st[1];
-    T.cdmax = st[2];
-    T.spdt = st[3] * kDt;  // st.speed * kDt, smax.cpp:514
-    T.rad = st[6];
-    T.hi = c.map - st[6];  // map_ - radius, smax.cpp:515
-    T.sight = make_thresh(st[4]);
-  }
-  for (int a = 0; a < kTypes; ++a)
-    for (int b = 0; b < kTypes; ++b) {
-      PairStat& S = P.ps[a][b];
-      S.reach = make_thresh(c.stats[a][5] + c.stats[a][6] + c.stats[b][6]);
-      const double sum = c.stats[a][6] + c.stats[b][6];
-      S.rsum = make_thresh(sum);
-      S.otol = make_thresh(sum - kSepTol);
-    }
-  P.sep_r2hi = 0.0;
-  for (int a = 0; a < P.n; ++a)
-    for (int b = 0; b < P.n; ++b) P.sep_r2hi = std::max(P.sep_r2hi, P.ps[P.type[a]][P.type[b]].rsum.r2hi);
-  if (c.random_types)  // any type pair can meet
-    for (int ta = 0; ta < kTypes; ++ta)
-      for (int tb = 0; tb < kTypes; ++tb) P.sep_r2hi = std::max(P.sep_r2hi, P.ps[ta][tb].rsum.r2hi);
-  return P;
-}
-
 // Group shape for a roster of n units: lanes per env (the smallest listed G
 // >= n, so few lanes idle) and units per lane.
 int shape_id(const SmaxConfig& c) {
@@ -1158,11 +1055,14 @@ void smax_prepare(SmaxConfig& c) {
   cudaMalloc(&d, sizeof(Params));
   cudaMemcpy(d, &P, sizeof P, cudaMemcpyHostToDevice);
   c.dev_params = d;
+  c.host_params = new Params(P);
 }
 
 void smax_release(SmaxConfig& c) {
   if (c.dev_params) cudaFree(c.dev_params);
   c.dev_params = nullptr;
+  delete static_cast<Params*>(c.host_params);
+  c.host_params = nullptr;
 }
 
 void smax_launch_reset(const SmaxConfig& c, const SmaxState& s, const LaunchCommon& lc, KeyWords key,
@@ -1172,8 +1072,16 @@ void smax_launch_reset(const SmaxConfig& c, const SmaxState& s, const LaunchComm
   ++g_launches;
 }
 
+// smax_lane.cu: one thread per env for the small rosters (false: not covered)
+bool smax_lane_launch_step(const SmaxConfig& c, const SmaxState& s, const LaunchCommon& lc, bool random,
+                           KeyWords step_key);
+
 void smax_launch_step(const SmaxConfig& c, const SmaxState& s, const LaunchCommon& lc, bool random,
                       KeyWords step_key) {
+  if (smax_lane_launch_step(c, s, lc, random, step_key)) {
+    ++g_launches;
+    return;
+  }
   const Params* dP = static_cast<const Params*>(c.dev_params);
   MARL_SMAX_SHAPES(launch_step_g, c, dP, s, lc, random, to_key(step_key))
   ++g_launches;
