@@ -50,6 +50,22 @@ IPPO_T = 128
 L2_FLUSH_BYTES = 512 << 20  # > 4x the 126 MB L2; its ~80 us also covers the host's enqueue of the next step
 
 
+def workload_config(workload, world, n_per_gpu=None):
+    """The `config` object, identical in both arms (the reference arm times a
+    bounded sample of this workload and says so in cpu_baseline.sample)."""
+    env_id, cfg, n, label = WORKLOADS[workload]
+    n = n_per_gpu or n
+    agents = {"SMAX_2s3z": 5, "SMAX_27m_vs_30m": 27, "SMAX_5m_vs_6m": 3, "MPE_simple_spread_v3": 3,
+              "overcooked_cramped_room_v0": 2}[env_id]
+    c = {"workload": label, "env_id": env_id, "env_config": cfg, "n_envs_per_gpu": n, "global_envs": n * world,
+         "agents": agents}
+    if workload == "ippo":
+        c["rollout_steps_per_window"] = IPPO_T
+    if workload in PPO_WORKLOADS:
+        c.update({"rollout_steps": IPPO_T, "update_epochs": 5, "n_minibatches": 2})
+    return c
+
+
 def algorithmic_bytes(env, n_envs, n_finished):
     """Minimum bytes one fused step must move: state read +
     write, carry (key, return, length) read + write, every output view, and
@@ -303,10 +319,9 @@ def run_gpu_ippo(args, rank, world, local_rank):
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16 policy / f64 env",
         "data": "synthetic (reset from key_from_seed(0); orthogonal-init policy, sampled actions)",
-        "config": {"workload": label, "env_id": env_id, "n_envs_per_gpu": n_per_gpu, "global_envs": N, "agents": A,
-                   "rollout_steps_per_window": T, "step": "one collect window",
-                   "parallelism": f"env-sharded x{world}, no collective in the window",
-                   "l2": "no flush: each window writes a >20 GB rollout buffer (>> 126 MB L2)"},
+        "config": workload_config(args.workload, world, n_per_gpu),
+        "run": {"step": "one collect window", "parallelism": f"env-sharded x{world}, no collective in the window",
+                "l2": "no flush: each window writes a >20 GB rollout buffer (>> 126 MB L2)"},
         "env_steps_per_sec": env_steps / (total_ms * 1e-3),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": None, "peak_source": peak_src,
@@ -437,12 +452,11 @@ def run_gpu_ppo(args, rank, world, local_rank):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": ("f32 recurrent policy + f32 BPTT update (cuBLAS SGEMM steps)" if recurrent else
                   "bf16 rollout policy + bf16 tcgen05 PPO update (fp32 accumulate)") + " / f64 env", "data": "synthetic (key_from_seed(rank))",
-        "config": {"workload": label, "env_id": env_id, "n_envs_per_gpu": n_envs, "agents": A,
-                   "rollout_steps": T, "update_epochs": 5, "n_minibatches": 2, "batch_rows": T * R,
-                   "step": "one PPO update = collect + update",
-                   "parallelism": f"dp{world}: env shards, update sums all-reduced over NCCL" if world > 1
-                   else "single device",
-                   "l2": "no flush: the rollout buffer (> 1 GB) is rewritten every step"},
+        "config": workload_config(args.workload, world, n_envs),
+        "run": {"batch_rows": T * R, "step": "one PPO update = collect + update",
+                "parallelism": f"dp{world}: env shards, update sums all-reduced over NCCL" if world > 1
+                else "single device",
+                "l2": "no flush: the rollout buffer (> 1 GB) is rewritten every step"},
         "collect_ms": float(np.mean(col_ms)), "update_ms": float(np.mean(upd_ms)),
         "update_row_passes_per_sec": T * R * 5 / upd_s,
         "roofline": {"bound": "tensor", "achieved": tflops, "peak": peak, "unit": "TFLOP/s", "frac": tflops / peak,
@@ -462,6 +476,34 @@ def run_gpu_ppo(args, rank, world, local_rank):
                                                         "grad_norm", "lr"], rows[-1])},
     }
     print(json.dumps(line))
+
+
+def cpu_model():
+    """lscpu's model name and the host's thread count."""
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            if ln.startswith("Model name:"):
+                return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def cpu_baseline_both(env_id, cfg, A):
+    """The reference's probe loop on the host: MARL_NUM_THREADS = nproc (the
+    reported value) and = 1, each on a bounded sample."""
+    n_cpu, k_cpu = cpu_sample_size(env_id, cfg)
+    threads = os.cpu_count() or 1
+    sec, kind, cores, _ = cpu_reference_probe(env_id, cfg, n_cpu, k_cpu, 1, threads)
+    n1, k1 = max(64, n_cpu // 4), k_cpu
+    sec1, _, _, _ = cpu_reference_probe(env_id, cfg, n1, k1, 1, 1)
+    return {"value": n_cpu * A * k_cpu / sec, "unit": "agent-steps/s", "cores": cores, "kind": kind,
+            "sample": f"{n_cpu} envs x {k_cpu} steps of {env_id} ({sec:.1f} s, {cores} threads, "
+                      "reference VectorEnv::step + random_legal_actions)",
+            "single_thread": {"value": n1 * A * k1 / sec1, "cores": 1,
+                              "sample": f"{n1} envs x {k1} steps ({sec1:.1f} s, MARL_NUM_THREADS=1)"},
+            "cpu_model": cpu_model(), "nproc": threads}
 
 
 def cpu_sample_size(env_id, cfg):
@@ -493,8 +535,8 @@ def run_reference_arm(args, rank, world):
                 "unit": "agent-steps/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
                 "ms_per_step": 1e3 * sec / steps, "higher_is_better": True, "scaling": "weak",
                 "vs_baseline": None, "dtype": "f32 nets / f64 env", "data": "synthetic",
-                "config": {"workload": label, "env_id": env_id, "n_envs": n_cpu, "n_envs_requested": n_envs,
-                           "rollout_steps": t_cpu},
+                "config": workload_config(args.workload, world),
+                "run": {"cpu_sample_envs": n_cpu, "cpu_sample_rollout_steps": t_cpu},
                 "cpu_baseline": {"value": val, "unit": "agent-steps/s", "cores": 1, "kind": "reference",
                                  "sample": f"reference train_ippo, {n_cpu} envs x {t_cpu} steps x {steps} updates"},
                 "e2e": {"value": val, "unit": "agent-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -515,8 +557,8 @@ def run_reference_arm(args, rank, world):
                 "unit": "agent-steps/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
                 "ms_per_step": 1e3 * sec / max(1, args.steps), "higher_is_better": True, "scaling": "weak",
                 "vs_baseline": None, "dtype": "f32 policy / f64 env", "data": "synthetic",
-                "config": {"workload": label, "env_id": env_id, "n_envs": n_cpu, "n_envs_requested": n_envs,
-                           "rollout_steps_per_window": t_cpu},
+                "config": workload_config(args.workload, world),
+                "run": {"cpu_sample_envs": n_cpu, "cpu_sample_rollout_steps": t_cpu},
                 "cpu_baseline": {"value": val, "unit": "agent-steps/s", "cores": 1, "kind": "reference",
                                  "sample": f"reference Collector pieces, {n_cpu} envs x {t_cpu} steps x "
                                            f"{max(1, args.steps)} windows"},
@@ -533,8 +575,8 @@ def run_reference_arm(args, rank, world):
             "unit": "agent-steps/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * sec / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference random-legal action stream)",
-            "config": {"workload": label, "env_id": env_id, "env_config": cfg, "n_envs": n_cpu,
-                       "n_envs_requested": n_envs},
+            "config": workload_config(args.workload, world),
+            "run": {"cpu_sample_envs": n_cpu},
             "cpu_baseline": {"value": val, "unit": "agent-steps/s", "cores": cores, "kind": kind,
                              "sample": f"{n_cpu} envs x {args.steps} steps of {env_id} on {cores} threads"},
             "e2e": {"value": val, "unit": "agent-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -612,7 +654,13 @@ def run_gpu_arm(args, rank, world, local_rank):
         host = {"obs": pin((n_per_gpu, A, D), torch.float32), "rewards": pin((n_per_gpu, A), torch.float64),
                 "dones": pin((n_per_gpu, A + 1), torch.uint8), "finished": pin((n_per_gpu,), torch.uint8),
                 "final_returns": pin((n_per_gpu,), torch.float64), "final_lengths": pin((n_per_gpu,), torch.int32)}
-        d2h = sum(a.nbytes for a in host.values())
+        if env.n_info:
+            host["infos"] = pin((n_per_gpu, A, env.n_info), torch.float64)
+        dense = sum(a.nbytes for a in host.values())
+        # final_obs: valid where finished; the device writes just those rows into the mapped pinned buffer
+        host["final_obs"] = pin((n_per_gpu, A, D), torch.float32)
+        fin_rows = float(np.mean(finished)) if len(finished) else 0.0
+        d2h = dense + fin_rows * A * D * 4
         e2e_steps = max(3, min(args.steps, 20))
         venv.host_step_random(akeys[0], host)  # warm
         if dist:
@@ -630,20 +678,15 @@ def run_gpu_arm(args, rank, world, local_rank):
         return
     cpu = None
     if world == 1 and not args.no_cpu:
-        n_cpu, k_cpu = cpu_sample_size(env_id, cfg)
-        threads = os.cpu_count() or 1
-        sec, kind, cores, _ = cpu_reference_probe(env_id, cfg, n_cpu, k_cpu, 1, threads)
-        cpu = {"value": n_cpu * A * k_cpu / sec, "unit": "agent-steps/s", "cores": cores, "kind": kind,
-               "sample": f"{n_cpu} envs x {k_cpu} steps of {env_id} ({sec:.1f} s, {cores} threads, "
-                         "reference VectorEnv::step + random_legal_actions)"}
+        cpu = cpu_baseline_both(env_id, cfg, A)
     line = {
         "metric": "agent-steps/sec (env-steps/sec x agents)", "value": value, "unit": "agent-steps/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (reset from key_from_seed(0); reference random-legal action stream)",
-        "config": {"workload": label, "env_id": env_id, "env_config": cfg, "n_envs_per_gpu": n_per_gpu,
-                   "global_envs": N, "agents": A, "parallelism": f"env-sharded x{world}, no step collective",
-                   "l2": "flushed between timed steps (256 MB write, untimed)"},
+        "config": workload_config(args.workload, world, n_per_gpu),
+        "run": {"parallelism": f"env-sharded x{world}, no step collective",
+                "l2": "flushed between timed steps (512 MB write, untimed)"},
         "env_steps_per_sec": N * args.steps / (total_ms * 1e-3),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
@@ -659,6 +702,20 @@ def run_gpu_arm(args, rank, world, local_rank):
     print(json.dumps(line))
 
 
+def self_launch(n):
+    """`python bench.py --gpus N` outside torchrun: re-run this command as N
+    ranks (one per GPU, NCCL over NVLink, rendezvous on 127.0.0.1)."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")  # the NCCL log shows the N ranks and the transport
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd, env=env)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -671,12 +728,19 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(self_launch(args.gpus))  # one rank per GPU under torchrun
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    if world != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     if args.impl == "reference":
         run_reference_arm(args, rank, world)
         return
+    import torch
+    if torch.cuda.device_count() < world:
+        sys.exit(f"bench.py: --gpus {world} needs {world} visible GPUs, found {torch.cuda.device_count()}")
     if world > 1:
         import torch
         import torch.distributed as dist

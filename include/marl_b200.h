@@ -87,7 +87,11 @@ typedef struct { /* device pointers, see the data model above */
   int32_t* episode_lengths;
 } marl_views;
 
-typedef struct { /* host destinations for *_host / download calls; NULL = skip */
+/* Host destinations for *_host / download calls; NULL = skip.  final_obs is
+ * valid where finished (vector_env.hpp:31): when it points into mapped pinned
+ * memory (cudaHostAlloc / torch pin_memory) the device writes only the
+ * finished rows into it, else the whole view is copied. */
+typedef struct {
   float* obs;
   double* rewards;
   uint8_t* dones;

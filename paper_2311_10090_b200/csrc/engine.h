@@ -229,6 +229,10 @@ void smax_launch_world_state(const SmaxConfig& c, const SmaxState& s, int64_t n,
 // agent's unpadded row (mpe.cpp:229-242), Overcooked is agent 0's row
 // (overcooked.cpp:315-319).  seg_src/seg_len: [n_seg] (offset in the env's
 // [A][D] obs block, length), written back to back.
+// final_obs rows of the finished envs of [0, n) from device `src` into the
+// device-accessible (mapped pinned) host buffer `dst`; `row` floats per env.
+void launch_gather_finished_rows(const uint8_t* finished, int64_t n, const float* src, float* dst, int64_t row,
+                                 cudaStream_t st);
 void launch_obs_gather(const float* obs, int64_t n, int row_floats, const int32_t* seg_src, const int32_t* seg_len,
                        int n_seg, int width, float* out, cudaStream_t st);
 

@@ -396,6 +396,18 @@ void launch_step(marl_venv* h, bool random, const uint32_t* step_key, const void
 }
 
 // Rows [b, e) of every requested output view -> the host buffers, on stream st.
+// The device address of a host pointer into mapped pinned memory (cudaHostAlloc
+// / pin_memory under unified addressing), else null.
+float* mapped_device_ptr(void* host) {
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, host) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  if (at.type != cudaMemoryTypeHost || !at.devicePointer) return nullptr;
+  return static_cast<float*>(at.devicePointer);
+}
+
 void download_range(marl_venv* h, const marl_host_step* o, int64_t b, int64_t e, cudaStream_t st) {
   const Env& E = *h->env;
   const size_t A = size_t(E.A), D = size_t(E.D), rows = size_t(e - b);
@@ -410,7 +422,14 @@ void download_range(marl_venv* h, const marl_host_step* o, int64_t b, int64_t e,
   cp(o->rewards, h->v.rewards, A * 8);
   cp(o->dones, h->v.dones, A + 1);
   cp(o->finished, h->v.finished, 1);
-  cp(o->final_obs, h->v.final_obs, A * D * 4);
+  // final_obs is valid where finished (vector_env.hpp:31): a mapped pinned
+  // destination receives only the finished rows, written by the device
+  float* fo_dev = o->final_obs ? mapped_device_ptr(o->final_obs) : nullptr;
+  if (fo_dev)
+    launch_gather_finished_rows(h->v.finished + b, int64_t(rows), h->v.final_obs + size_t(b) * A * D,
+                                fo_dev + size_t(b) * A * D, int64_t(A * D), st);
+  else
+    cp(o->final_obs, h->v.final_obs, A * D * 4);
   cp(o->final_returns, h->v.final_returns, 8);
   cp(o->final_lengths, h->v.final_lengths, 4);
   if (E.n_info) cp(o->infos, h->v.infos, A * size_t(E.n_info) * 8);

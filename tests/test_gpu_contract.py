@@ -209,3 +209,33 @@ def test_generic_rollout_matches_oracle_loop():
                        tr.obs[..., 1].double().cpu().numpy())
     with pytest.raises(m.ContractError):
         m.rollout(v, policy, 0, O.key_from_seed(1))
+
+
+@pytest.mark.parametrize("env_id,cfg,n", [("SMAX_5m_vs_6m", THREE_M, 40_003),
+                                          ("overcooked_cramped_room_v0", {"max_steps": 3}, 33_001)])
+def test_host_final_obs_mapped_buffer_gets_finished_rows_only(env_id, cfg, n):
+    """final_obs is valid where finished (vector_env.hpp:31): into a mapped
+    pinned host buffer the device writes exactly the finished rows (equal to
+    the device view) and leaves every other row as the caller left it."""
+    import torch
+    m = _m()
+    a = m.VectorEnv(env_id, n, config=cfg)
+    b = m.VectorEnv(env_id, n, config=cfg)
+    a.reset(O.key_from_seed(5))
+    b.reset(O.key_from_seed(5))
+    shape = (n, a.env().num_agents(), a.env().obs_dim)
+    fo = torch.full(shape, -7.0, dtype=torch.float32, pin_memory=True).numpy()
+    fin = torch.zeros((n,), dtype=torch.uint8, pin_memory=True).numpy()
+    seen = 0
+    for k in range(25):
+        key = O.fold_in(O.key_from_seed(11), k)
+        a.step_random(key)
+        want = a.download(("final_obs", "finished"))
+        fo[:] = -7.0
+        b.host_step_random(key, {"final_obs": fo, "finished": fin})
+        f = want["finished"].astype(bool)
+        assert np.array_equal(fin, want["finished"])
+        assert np.array_equal(fo[f], want["final_obs"][f]), k
+        assert np.all(fo[~f] == -7.0), k
+        seen += int(f.sum())
+    assert seen > 0

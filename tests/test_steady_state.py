@@ -90,31 +90,57 @@ def _blocks(sp):
     return out
 
 
-# MPE: in 18, Kx 32, two tiles in flight (NS = 2); SMAX 3m: in 95, Kx 96, NS = 1
-@pytest.mark.parametrize("env_id,cfg,n_envs", [("MPE_simple_spread_v3", {}, 1024), ("SMAX_5m_vs_6m", THREE_M, 1024)])
-@pytest.mark.parametrize("precision,cap", [("bf16", 1), ("bf16", 2), ("fp32", 2)])
-def test_update_kernel_steady_state_matches_ff_minibatch(env_id, cfg, n_envs, precision, cap):
-    _need_ref()
-    T = 24
-    with _Cap(cap):
+def _grad(env_id, cfg, n_envs, T, precision, cap):
+    """One >= 50k-row minibatch gradient on a fresh trainer (grid capped to
+    `cap` CTAs, or uncapped for cap=0) plus what the reference needs."""
+    ctx = _Cap(cap) if cap else None
+    if ctx:
+        ctx.__enter__()
+    try:
         tr = _trainer(env_id, cfg, n_envs, T, precision)
         assert tr.tensor_core_update == (precision == "bf16")
         tr.begin(O.key_from_seed(61))
         tr.collect()
         buf = {k: t.cpu().numpy() for k, t in tr.rollout._views.items()}
         a, c = tr.params()
-        R = tr.rollout.R
-        M = 50_000
-        idx = np.random.default_rng(9).choice(T * R, size=M, replace=False).astype(np.int32)
+        idx = np.random.default_rng(9).choice(T * tr.rollout.R, size=50_000, replace=False).astype(np.int32)
         g, st = tr.minibatch_grad(idx)
+    finally:
+        if ctx:
+            ctx.__exit__()
+    return tr, buf, a, c, idx, g, st
+
+
+# MPE: in 18, Kx 32, two tiles in flight (NS = 2); SMAX 3m: in 95, Kx 96, NS = 1
+@pytest.mark.parametrize("env_id,cfg,n_envs", [("MPE_simple_spread_v3", {}, 1024), ("SMAX_5m_vs_6m", THREE_M, 1024)])
+@pytest.mark.parametrize("precision,cap", [("bf16", 1), ("bf16", 2), ("fp32", 2)])
+def test_update_kernel_steady_state_matches_ff_minibatch(env_id, cfg, n_envs, precision, cap):
+    """The steady-state property first: 1-2 CTAs walking hundreds of tiles
+    (cross-tile gradient accumulation in TMEM / registers, NS = 2 tiles in
+    flight) give the uncapped grid's gradient up to fp32 summation order.
+    Then both against the reference's ff_minibatch: fp32 within 2e-3
+    relative; bf16 per block cosine >= 0.995 and norm within 3 %, except the
+    one-element value-head bias, whose gradient is a mean of (v - v_target)
+    with heavy cancellation -- there bf16's ~0.3 % error on v is compared with
+    the scale of its sibling weight block (1 %)."""
+    _need_ref()
+    T = 24
+    tr, buf, a, c, idx, g, st = _grad(env_id, cfg, n_envs, T, precision, cap)
+    g0 = _grad(env_id, cfg, n_envs, T, precision, 0)[5]
+    for lo, hi in _blocks(tr.spec):
+        scale = np.linalg.norm(g0[lo:hi]) + 1e-30
+        assert np.abs(g[lo:hi] - g0[lo:hi]).max() <= 2e-4 * scale, (lo, hi)
     gr, sr = O.ref_ff_minibatch(env_id, cfg, a, c, buf, idx)
     if precision == "bf16":
+        prev = None
         for lo, hi in _blocks(tr.spec):
             x, y = g[lo:hi], gr[lo:hi]
-            if np.linalg.norm(y) < 1e-12:
-                continue
-            assert _cos(x, y) >= 0.995, (lo, hi, _cos(x, y))
-            assert abs(np.linalg.norm(x) / np.linalg.norm(y) - 1) < 0.03, (lo, hi)
+            if hi - lo == 1 and prev is not None:
+                assert abs(x[0] - y[0]) <= 0.03 * abs(y[0]) + 0.01 * np.linalg.norm(prev), (lo, hi, x, y)
+            elif np.linalg.norm(y) >= 1e-12:
+                assert _cos(x, y) >= 0.995, (lo, hi, _cos(x, y))
+                assert abs(np.linalg.norm(x) / np.linalg.norm(y) - 1) < 0.03, (lo, hi)
+            prev = y
         assert np.allclose(st, sr, rtol=2e-2, atol=1e-4), (st, sr)
     else:
         tol = 2e-3 * np.abs(gr) + 1e-4 * np.abs(gr).max()
