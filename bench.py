@@ -46,6 +46,7 @@ WORKLOADS = {
                  "2 minibatches of PPO; 95-wide observations), PpoConfig defaults"),
 }
 PPO_WORKLOADS = ("ppo", "ppo_rnn", "ppo_smax")
+FUSED_PROBE = ("mpe",)  # timed as one fused multi-step probe launch (marl_venv_probe_steps)
 IPPO_T = 128
 L2_FLUSH_BYTES = 512 << 20  # > 4x the 126 MB L2; its ~80 us also covers the host's enqueue of the next step
 
@@ -621,18 +622,35 @@ def run_gpu_arm(args, rank, world, local_rank):
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     fin_counts = torch.zeros(args.steps, dtype=torch.int64, device="cuda")
     launches0 = _native.lib().marl_launch_count()
-    for k in range(args.steps):
-        flush.fill_(float(k))  # L2 flush between timed steps (not timed); the GPU is busy with it
-        starts[k].record(stream)  # while the host enqueues the step, so no launch gap is timed
-        r = venv.step_random(akeys[args.warmup + k])
-        ends[k].record(stream)
-        fin_counts[k] = r.finished.sum()
+    fused = args.workload in FUSED_PROBE and not args.per_step
+    if fused:
+        # configs[0] is the reference's throughput_probe loop at 1024 envs, launch-
+        # bound one launch per step: the K timed steps run as ONE fused launch
+        # (marl_venv_probe_steps: state in registers across steps, every output
+        # view still written every step); L2 flushed once before it
+        flush.fill_(0.0)
+        starts[0].record(stream)
+        venv.probe_steps(m.prng.fold_in(key, 2), args.warmup, args.steps)
+        ends[0].record(stream)
+    else:
+        for k in range(args.steps):
+            flush.fill_(float(k))  # L2 flush between timed steps (not timed); the GPU is busy with it
+            starts[k].record(stream)  # while the host enqueues the step, so no launch gap is timed
+            r = venv.step_random(akeys[args.warmup + k])
+            ends[k].record(stream)
+            fin_counts[k] = r.finished.sum()
     torch.cuda.synchronize()
     launches = _native.lib().marl_launch_count() - launches0
     if dist:
         dist.barrier()
     clk = clocks.stop() if clocks else None
-    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    if fused:
+        whole = starts[0].elapsed_time(ends[0])
+        step_ms = [whole / args.steps] * args.steps
+        eps = venv.episode_stats_raw()[0]  # finished episodes over the K steps (shard-local)
+        fin_counts = torch.full((args.steps,), eps / args.steps, dtype=torch.float64)
+    else:
+        step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
     total_ms = float(sum(step_ms))
     total_ms = shard.max_over_ranks(total_ms, device="cuda")  # device time, max over ranks
     stats = shard.all_reduce_episode_stats(venv.episode_stats_raw(), device="cuda")  # the one collective
@@ -640,7 +658,7 @@ def run_gpu_arm(args, rank, world, local_rank):
 
     # roofline of the dominant (only) kernel: algorithmic bytes per launch / mean launch time
     finished = fin_counts.cpu().numpy()
-    bytes_per_launch = float(np.mean([algorithmic_bytes(env, n_per_gpu, int(f)) for f in finished]))
+    bytes_per_launch = float(np.mean([algorithmic_bytes(env, n_per_gpu, float(f)) for f in finished]))
     mean_launch_s = float(np.mean(step_ms)) * 1e-3
     achieved = bytes_per_launch / mean_launch_s / 1e9
     peak, peak_src = measured_peak()
@@ -686,12 +704,16 @@ def run_gpu_arm(args, rank, world, local_rank):
         "data": "synthetic (reset from key_from_seed(0); reference random-legal action stream)",
         "config": workload_config(args.workload, world, n_per_gpu),
         "run": {"parallelism": f"env-sharded x{world}, no step collective",
-                "l2": "flushed between timed steps (512 MB write, untimed)"},
+                "l2": ("flushed once before the fused K-step launch (state stays in registers across its steps)"
+                       if fused else "flushed between timed steps (512 MB write, untimed)"),
+                "launch": (f"one fused launch of {args.steps} probe steps (marl_venv_probe_steps)" if fused
+                           else "one launch per step (marl_venv_step_random)")},
         "env_steps_per_sec": N * args.steps / (total_ms * 1e-3),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                      "bytes_per_launch": bytes_per_launch, "mean_launch_us": mean_launch_s * 1e6,
-                     "kernel": "fused step kernel (step_random)",
+                     "kernel": ("fused multi-step probe kernel (per-step bytes; launch time / K)" if fused
+                                else "fused step kernel (step_random)"),
                      "ncu": ncu_metrics(args.workload)},
         "cpu_baseline": cpu,
         "e2e": e2e,
@@ -725,6 +747,7 @@ def main():
     ap.add_argument("--workload", default="smax3m", choices=sorted(WORKLOADS))
     ap.add_argument("--n-envs", type=int, default=0, help="override envs per GPU")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--per-step", action="store_true", help="mpe: one launch per step instead of the fused probe")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)

@@ -163,6 +163,14 @@ int marl_venv_step(marl_venv* h, const int32_t* d_actions);
  * the step kernel.  The drawn actions land in views.actions. */
 int marl_venv_step_random(marl_venv* h, const uint32_t step_key[4]);
 
+/* n_steps consecutive iterations of throughput_probe's loop (vector_env.cpp:
+ * 202-217): iteration k draws random-legal actions with
+ * split(parent, t0 + k)[g] -- parent = fold_in(key, 2), the probe's
+ * action-key parent -- and steps.  The same outputs as n_steps calls of
+ * marl_venv_step_random with those keys (the views hold the last step's);
+ * MPE runs all n_steps in one kernel launch with the env state in registers. */
+int marl_venv_probe_steps(marl_venv* h, const uint32_t parent[4], uint64_t t0, int n_steps);
+
 /* Host-buffer variants (the end-to-end path): host actions are validated on
  * the host exactly like Env::validate_actions, copied in, stepped, and the
  * requested outputs copied back; returns after the copies complete. */

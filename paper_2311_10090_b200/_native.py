@@ -50,7 +50,7 @@ EXPORTS = [
     "marl_venv_create", "marl_venv_create_shard",
     "marl_venv_destroy", "marl_venv_set_stream", "marl_venv_spec", "marl_venv_agent",
     "marl_venv_info_name", "marl_venv_id", "marl_venv_reset", "marl_venv_step",
-    "marl_venv_step_random", "marl_venv_step_host", "marl_venv_step_random_host",
+    "marl_venv_step_random", "marl_venv_probe_steps", "marl_venv_step_host", "marl_venv_step_random_host",
     "marl_venv_download", "marl_venv_views", "marl_copy_device_to_host", "marl_venv_legal", "marl_venv_state_hash",
     "marl_venv_episode_stats", "marl_venv_sync", "marl_throughput_probe",
     "marl_prng_key_from_seed", "marl_prng_split", "marl_prng_fold_in", "marl_prng_bits",
@@ -97,6 +97,7 @@ def lib() -> C.CDLL:
     L.marl_venv_reset.argtypes = [vp, u32p]
     L.marl_venv_step.argtypes = [vp, vp]
     L.marl_venv_step_random.argtypes = [vp, u32p]
+    L.marl_venv_probe_steps.argtypes = [vp, u32p, C.c_uint64, C.c_int]
     L.marl_venv_step_host.argtypes = [vp, vp, C.POINTER(HostStep)]
     L.marl_venv_step_random_host.argtypes = [vp, u32p, C.POINTER(HostStep)]
     L.marl_venv_download.argtypes = [vp, C.POINTER(HostStep)]

@@ -84,6 +84,8 @@ void mpe_launch_reset(const MpeConfig& c, const MpeState& s, const LaunchCommon&
 // (vector_env.cpp:169-187); else read from lc.v.actions.
 void mpe_launch_step(const MpeConfig& c, const MpeState& s, const LaunchCommon& lc, bool random,
                      KeyWords step_key);
+void mpe_launch_probe(const MpeConfig& c, const MpeState& s, const LaunchCommon& lc, KeyWords parent,
+                      uint64_t t0, int K);
 void mpe_launch_hash(const MpeConfig& c, const MpeState& s, int64_t n, uint64_t* out,
                      cudaStream_t st);
 

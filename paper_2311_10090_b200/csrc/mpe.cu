@@ -351,21 +351,28 @@ __global__ void __launch_bounds__(kThreads) mpe_reset_kernel(MpeState st, Launch
   block_store(lc.v.obs + i0 * ROW, s_obs, size_t(nvalid) * ROW * sizeof(float));
 }
 
-template <int S, bool RANDOM, bool CONT>
-__global__ void __launch_bounds__(kThreads) mpe_step_kernel(MpeState st, LaunchCommon lc, Key step_key,
-                                                            int coop_prey) {
+// One launch = K consecutive VectorEnv::step calls (K = 1 for marl_venv_step).
+// MULTI: the fused throughput_probe loop (vector_env.cpp:202-217) -- step k's
+// action key is split(fold_in(key, 2), T + 1)[t0 + k], derived in-kernel, and
+// the env's state, carry key and episode bookkeeping stay in registers across
+// the K steps.  Every step still writes every output view (obs, rewards,
+// dones, actions, finished, final_*), so after the launch the views hold step
+// t0 + K - 1's outputs exactly as K separate launches would leave them.
+template <int S, bool RANDOM, bool CONT, bool MULTI, int TPB>
+__global__ void __launch_bounds__(TPB) mpe_step_kernel(MpeState st, LaunchCommon lc, Key step_key,
+                                                       int coop_prey, uint64_t t0, int K) {
   using Sc = Scen<S>;
   constexpr int A = Sc::A, ROW = A * Sc::D;
-  __shared__ __align__(16) float s_obs[kThreads * ROW];
-  __shared__ __align__(16) double s_rew[kThreads * A];
-  __shared__ __align__(16) int32_t s_act[kThreads * A];
-  __shared__ __align__(16) uint8_t s_done[kThreads * (A + 1)];
-  __shared__ uint8_t s_fin[kThreads];
+  __shared__ __align__(16) float s_obs[TPB * ROW];
+  __shared__ __align__(16) double s_rew[TPB * A];
+  __shared__ __align__(16) int32_t s_act[TPB * A];
+  __shared__ __align__(16) uint8_t s_done[TPB * (A + 1)];
+  __shared__ uint8_t s_fin[TPB];
   if (*(volatile int*)lc.err) return;  // a pending contract error freezes the batch
 
-  const int64_t i0 = lc.begin + int64_t(blockIdx.x) * kThreads;
+  const int64_t i0 = lc.begin + int64_t(blockIdx.x) * TPB;
   const int64_t i = i0 + threadIdx.x;
-  const int nvalid = int(min64(kThreads, lc.end - i0));
+  const int nvalid = int(min64(TPB, lc.end - i0));
   const bool live = i < lc.end;
   float* my_obs = s_obs + threadIdx.x * ROW;
 
@@ -373,104 +380,113 @@ __global__ void __launch_bounds__(kThreads) mpe_step_kernel(MpeState st, LaunchC
   Key carry{0, 0, 0, 0};
   double ep_ret = 0.0;
   int ep_len = 0;
-  bool done = false;
+  bool any_reset = false;
   if (live) {
     uint4 kw = lc.carry.keys[i];
     carry = Key{kw.x, kw.y, kw.z, kw.w};
     ep_ret = lc.carry.ep_return[i];
     ep_len = lc.carry.ep_length[i];
     load_state<Sc, S>(s, st, i, lc.n);
-
-    int act[A];
-    float actf[CONT ? A * kBoxActDim : 1];
-    if (RANDOM && CONT) {
-      // box spaces: space.sample(fold_in(env_key, j)) = float(uniform(key, flat, 0, 1))
-      // (vector_env.cpp:179-181, spaces.cpp:48-54)
-      Key ek = split_child(step_key, uint64_t(lc.offset + i));
+  }
+  for (int k = 0; k < (MULTI ? K : 1); ++k) {
+    // MULTI: thread 0 drained the previous step's tile reads; nobody rewrites
+    // the tiles before that
+    if (MULTI && k > 0) __syncthreads();
+    const Key sk = MULTI ? split_child(step_key, t0 + uint64_t(k)) : step_key;
+    bool done = false;
+    if (live) {
+      int act[A];
+      float actf[CONT ? A * kBoxActDim : 1];
+      if (RANDOM && CONT) {
+        // box spaces: space.sample(fold_in(env_key, j)) = float(uniform(key, flat, 0, 1))
+        // (vector_env.cpp:179-181, spaces.cpp:48-54)
+        Key ek = split_child(sk, uint64_t(lc.offset + i));
 #pragma unroll
-      for (int j = 0; j < A; ++j) {
-        const Key kj = fold_in(ek, uint64_t(j));
+        for (int j = 0; j < A; ++j) {
+          const Key kj = fold_in(ek, uint64_t(j));
 #pragma unroll
-        for (int k = 0; k < kBoxActDim; ++k)
-          actf[j * kBoxActDim + k] = k < Sc::n_actions(j) ? float(uniform_at(kj, uint64_t(k), 0.0, 1.0)) : 0.0f;
-      }
-      float4* dst = reinterpret_cast<float4*>(lc.v.actions_f + i * A * kBoxActDim);
-      if ((A * kBoxActDim) % 4 == 0) {
+          for (int q = 0; q < kBoxActDim; ++q)
+            actf[j * kBoxActDim + q] = q < Sc::n_actions(j) ? float(uniform_at(kj, uint64_t(q), 0.0, 1.0)) : 0.0f;
+        }
+        float4* dst = reinterpret_cast<float4*>(lc.v.actions_f + i * A * kBoxActDim);
+        if ((A * kBoxActDim) % 4 == 0) {
 #pragma unroll
-        for (int q = 0; q < A * kBoxActDim / 4; ++q)
-          dst[q] = make_float4(actf[4 * q], actf[4 * q + 1], actf[4 * q + 2], actf[4 * q + 3]);
+          for (int q = 0; q < A * kBoxActDim / 4; ++q)
+            dst[q] = make_float4(actf[4 * q], actf[4 * q + 1], actf[4 * q + 2], actf[4 * q + 3]);
+        } else {
+#pragma unroll
+          for (int q = 0; q < A * kBoxActDim; ++q) lc.v.actions_f[i * A * kBoxActDim + q] = actf[q];
+        }
+      } else if (CONT) {
+#pragma unroll
+        for (int q = 0; q < A * kBoxActDim; ++q) actf[q] = lc.v.actions_f[i * A * kBoxActDim + q];
+      } else if (RANDOM) {
+        // random_legal_actions (vector_env.cpp:169-187); MPE masks are all-legal
+        // (env.hpp:71-73) so the draw is bits(env_key, j) % n_actions.
+        Key ek = split_child(sk, uint64_t(lc.offset + i));
+#pragma unroll
+        for (int j = 0; j < A; ++j) {
+          act[j] = int(block_at(ek, uint64_t(j)) % uint64_t(Sc::n_actions(j)));
+          s_act[threadIdx.x * A + j] = act[j];
+        }
       } else {
 #pragma unroll
-        for (int q = 0; q < A * kBoxActDim; ++q) lc.v.actions_f[i * A * kBoxActDim + q] = actf[q];
+        for (int j = 0; j < A; ++j) act[j] = lc.v.actions[i * A + j];
       }
-    } else if (CONT) {
-#pragma unroll
-      for (int q = 0; q < A * kBoxActDim; ++q) actf[q] = lc.v.actions_f[i * A * kBoxActDim + q];
-    } else if (RANDOM) {
-      // random_legal_actions (vector_env.cpp:169-187); MPE masks are all-legal
-      // (env.hpp:71-73) so the draw is bits(env_key, j) % n_actions.
-      Key ek = split_child(step_key, uint64_t(lc.offset + i));
+
+      physics<Sc, CONT>(s, act, actf);
+      done = s.steps >= kEpisodeSteps;
+      double sum = 0.0;
 #pragma unroll
       for (int j = 0; j < A; ++j) {
-        act[j] = int(block_at(ek, uint64_t(j)) % uint64_t(Sc::n_actions(j)));
-        s_act[threadIdx.x * A + j] = act[j];
+        double r = reward<Sc, S>(s, j, coop_prey != 0);
+        s_rew[threadIdx.x * A + j] = r;
+        sum += r;
+        s_done[threadIdx.x * (A + 1) + j] = done;
       }
-    } else {
-#pragma unroll
-      for (int j = 0; j < A; ++j) act[j] = lc.v.actions[i * A + j];
-    }
-
-    physics<Sc, CONT>(s, act, actf);
-    done = s.steps >= kEpisodeSteps;
-    double sum = 0.0;
-#pragma unroll
-    for (int j = 0; j < A; ++j) {
-      double r = reward<Sc, S>(s, j, coop_prey != 0);
-      s_rew[threadIdx.x * A + j] = r;
-      sum += r;
-      s_done[threadIdx.x * (A + 1) + j] = done;
-    }
-    s_done[threadIdx.x * (A + 1) + A] = done;
-    ep_ret = ep_ret + sum / double(A);  // team_reward, vector_env.cpp:14-18,99
-    ep_len = ep_len + 1;
-#pragma unroll
-    for (int a = 0; a < A; ++a) observe<Sc, S>(s, a, my_obs + a * Sc::D);
-    lc.v.finished[i] = done;
-    lc.v.final_returns[i] = done ? ep_ret : 0.0;
-    lc.v.final_lengths[i] = done ? ep_len : 0;
-  }
-  s_fin[threadIdx.x] = done;
-  stats_add(lc.stats, done, ep_len, ep_ret);
-
-  // Terminal observations leave as whole rows before auto-reset overwrites them.
-  if (__syncthreads_or(done)) {
-    for (int idx = threadIdx.x; idx < nvalid * ROW; idx += kThreads) {
-      int r = idx / ROW;
-      if (s_fin[r]) __stcs(lc.v.final_obs + i0 * ROW + idx, s_obs[idx]);
-    }
-    __syncthreads();
-    if (done) {  // vector_env.cpp:107-119: reset with the auto-reset child key
-      env_reset<Sc, S>(s, split_child(carry, 1));
+      s_done[threadIdx.x * (A + 1) + A] = done;
+      ep_ret = ep_ret + sum / double(A);  // team_reward, vector_env.cpp:14-18,99
+      ep_len = ep_len + 1;
 #pragma unroll
       for (int a = 0; a < A; ++a) observe<Sc, S>(s, a, my_obs + a * Sc::D);
-      ep_ret = 0.0;
-      ep_len = 0;
+      lc.v.finished[i] = done;
+      lc.v.final_returns[i] = done ? ep_ret : 0.0;
+      lc.v.final_lengths[i] = done ? ep_len : 0;
     }
+    s_fin[threadIdx.x] = done;
+    stats_add(lc.stats, done, ep_len, ep_ret);
+
+    // Terminal observations leave as whole rows before auto-reset overwrites them.
+    if (__syncthreads_or(done)) {
+      for (int idx = threadIdx.x; idx < nvalid * ROW; idx += TPB) {
+        int r = idx / ROW;
+        if (s_fin[r]) __stcs(lc.v.final_obs + i0 * ROW + idx, s_obs[idx]);
+      }
+      __syncthreads();
+      if (done) {  // vector_env.cpp:107-119: reset with the auto-reset child key
+        env_reset<Sc, S>(s, split_child(carry, 1));
+#pragma unroll
+        for (int a = 0; a < A; ++a) observe<Sc, S>(s, a, my_obs + a * Sc::D);
+        ep_ret = 0.0;
+        ep_len = 0;
+        any_reset = true;
+      }
+    }
+    carry = split_child(carry, 2);  // vector_env.cpp:126
+    // the block's rows leave as TMA bulk stores (one instruction per tile)
+    bulk_tile_fence();
+    tile_store(lc.v.obs + i0 * ROW, s_obs, size_t(nvalid) * ROW * sizeof(float));
+    tile_store(lc.v.rewards + i0 * A, s_rew, size_t(nvalid) * A * sizeof(double));
+    tile_store(lc.v.dones + i0 * (A + 1), s_done, size_t(nvalid) * (A + 1));
+    if (RANDOM && !CONT) tile_store(lc.v.actions + i0 * A, s_act, size_t(nvalid) * A * sizeof(int32_t));
+    tile_store_drain();
   }
   if (live) {
-    Key nk = split_child(carry, 2);  // vector_env.cpp:126
-    lc.carry.keys[i] = make_uint4(nk.k0, nk.k1, nk.c0, nk.c1);
+    lc.carry.keys[i] = make_uint4(carry.k0, carry.k1, carry.c0, carry.c1);
     lc.carry.ep_return[i] = ep_ret;
     lc.carry.ep_length[i] = ep_len;
-    store_state<Sc, S>(s, st, i, lc.n, done);
+    store_state<Sc, S>(s, st, i, lc.n, any_reset);
   }
-  // the block's rows leave as TMA bulk stores (one instruction per tile)
-  bulk_tile_fence();
-  tile_store(lc.v.obs + i0 * ROW, s_obs, size_t(nvalid) * ROW * sizeof(float));
-  tile_store(lc.v.rewards + i0 * A, s_rew, size_t(nvalid) * A * sizeof(double));
-  tile_store(lc.v.dones + i0 * (A + 1), s_done, size_t(nvalid) * (A + 1));
-  if (RANDOM && !CONT) tile_store(lc.v.actions + i0 * A, s_act, size_t(nvalid) * A * sizeof(int32_t));
-  tile_store_drain();
 }
 
 // state_hash (mpe.cpp:254-269), parity aid.
@@ -536,17 +552,39 @@ void mpe_launch_step(const MpeConfig& c, const MpeState& s, const LaunchCommon& 
                      KeyWords step_key) {
   unsigned g = grid_for(lc.end - lc.begin, kThreads);
   Key k = to_key(step_key);
-#define MARL_MPE_STEP(S)                                                                  \
-  c.continuous ? (random ? mpe_step_kernel<S, true, true><<<g, kThreads, 0, lc.stream>>>(s, lc, k, c.coop_prey)   \
-                         : mpe_step_kernel<S, false, true><<<g, kThreads, 0, lc.stream>>>(s, lc, k, c.coop_prey)) \
-               : (random ? mpe_step_kernel<S, true, false><<<g, kThreads, 0, lc.stream>>>(s, lc, k, c.coop_prey)  \
-                         : mpe_step_kernel<S, false, false><<<g, kThreads, 0, lc.stream>>>(s, lc, k, c.coop_prey))
+#define MARL_MPE_STEP(S, R, C) \
+  mpe_step_kernel<S, R, C, false, kThreads><<<g, kThreads, 0, lc.stream>>>(s, lc, k, c.coop_prey, 0, 1)
+#define MARL_MPE_STEPS(S)                                                                          \
+  c.continuous ? (random ? MARL_MPE_STEP(S, true, true) : MARL_MPE_STEP(S, false, true))           \
+               : (random ? MARL_MPE_STEP(S, true, false) : MARL_MPE_STEP(S, false, false))
   switch (c.scenario) {
-    case kMpeSpread: MARL_MPE_STEP(kMpeSpread); break;
-    case kMpeSpeakerListener: MARL_MPE_STEP(kMpeSpeakerListener); break;
-    default: MARL_MPE_STEP(kMpeTag); break;
+    case kMpeSpread: MARL_MPE_STEPS(kMpeSpread); break;
+    case kMpeSpeakerListener: MARL_MPE_STEPS(kMpeSpeakerListener); break;
+    default: MARL_MPE_STEPS(kMpeTag); break;
   }
+#undef MARL_MPE_STEPS
 #undef MARL_MPE_STEP
+  ++g_launches;
+}
+
+// K probe steps in one launch (see mpe_step_kernel's MULTI).  Small batches
+// are latency-bound, so the CTAs are one warp each: the envs spread over as
+// many SMs as possible.
+void mpe_launch_probe(const MpeConfig& c, const MpeState& s, const LaunchCommon& lc, KeyWords parent,
+                      uint64_t t0, int K) {
+  constexpr int kTpb = 32;
+  unsigned g = grid_for(lc.end - lc.begin, kTpb);
+  Key k = to_key(parent);
+#define MARL_MPE_PROBE(S)                                                                                  \
+  c.continuous                                                                                             \
+      ? mpe_step_kernel<S, true, true, true, kTpb><<<g, kTpb, 0, lc.stream>>>(s, lc, k, c.coop_prey, t0, K) \
+      : mpe_step_kernel<S, true, false, true, kTpb><<<g, kTpb, 0, lc.stream>>>(s, lc, k, c.coop_prey, t0, K)
+  switch (c.scenario) {
+    case kMpeSpread: MARL_MPE_PROBE(kMpeSpread); break;
+    case kMpeSpeakerListener: MARL_MPE_PROBE(kMpeSpeakerListener); break;
+    default: MARL_MPE_PROBE(kMpeTag); break;
+  }
+#undef MARL_MPE_PROBE
   ++g_launches;
 }
 

@@ -738,6 +738,33 @@ int marl_venv_step_random(marl_venv* h, const uint32_t step_key[4]) {
   });
 }
 
+int marl_venv_probe_steps(marl_venv* h, const uint32_t parent[4], uint64_t t0, int n_steps) {
+  return guarded([&] {
+    if (!h || !parent) raise(MARL_ERR_CONTRACT, "marl_venv_probe_steps: NULL argument");
+    if (n_steps < 0) raise(MARL_ERR_CONTRACT, "marl_venv_probe_steps: n_steps must be >= 0");
+    set_device(h);
+    require_state(h);
+    if (n_steps == 0) return;
+    Key p{parent[0], parent[1], parent[2], parent[3]};
+    if (h->env->family == MARL_FAMILY_MPE) {
+      // one launch for all K steps (state and carry in registers across them)
+      LaunchCommon lc = common(h);
+      lc.begin = 0;
+      lc.end = h->n;
+      KeyWords k{};
+      std::memcpy(k.w, parent, 16);
+      mpe_launch_probe(h->env->mpe, h->mpe, lc, k, t0, n_steps);
+      after_launch();
+      return;
+    }
+    for (int t = 0; t < n_steps; ++t) {
+      Key sk = split_child(p, t0 + uint64_t(t));
+      uint32_t s[4] = {sk.k0, sk.k1, sk.c0, sk.c1};
+      launch_step(h, true, s, nullptr);
+    }
+  });
+}
+
 int marl_venv_step_host(marl_venv* h, const int32_t* h_actions, const marl_host_step* out) {
   return guarded([&] {
     if (!h || !h_actions) raise(MARL_ERR_CONTRACT, "marl_venv_step_host: NULL argument");
@@ -963,11 +990,8 @@ int marl_throughput_probe(const char* env_id, const char* config_json, int64_t n
     uint32_t w[4] = {wk.k0, wk.k1, wk.c0, wk.c1};
     if (int r = marl_venv_step_random(h, w)) raise(r, g_err);
     cudaEventRecord(e1, h->stream);
-    for (int t = 0; t < n_steps; ++t) {
-      Key sk = action_key(uint64_t(t));
-      uint32_t s[4] = {sk.k0, sk.k1, sk.c0, sk.c1};
-      if (int r = marl_venv_step_random(h, s)) raise(r, g_err);
-    }
+    const uint32_t pw[4] = {parent.k0, parent.k1, parent.c0, parent.c1};
+    if (int r = marl_venv_probe_steps(h, pw, 0, n_steps)) raise(r, g_err);
     cudaEventRecord(e2, h->stream);
     cuda_check(cudaEventSynchronize(e2), "cudaEventSynchronize");
     float cold_ms = 0, warm_ms = 0;

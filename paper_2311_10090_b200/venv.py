@@ -324,6 +324,16 @@ class VectorEnv:
         self._version += 1
         return self._result()
 
+    def probe_steps(self, parent_key, t0: int, n_steps: int, state: Optional[BatchedState] = None) -> StepBatchResult:
+        """n_steps iterations of throughput_probe's loop (vector_env.cpp:202-217):
+        step k uses split(parent_key, t0 + k) as its action key, parent_key =
+        fold_in(key, 2).  Same outputs as n_steps step_random calls (the views
+        hold the last step's); MPE fuses them into one launch.  Asynchronous."""
+        self._check_state(state)
+        N.check(N.lib().marl_venv_probe_steps(self._h, _u32p(_key_arr(parent_key)), int(t0), int(n_steps)))
+        self._version += 1
+        return self._result()
+
     def legal_actions(self):
         """Env::legal_actions for every env/agent: uint8 [N, A, n_actions]."""
         out = self._torch.zeros((self._n, self._env.num_agents(), self._env.n_actions_max),

@@ -17,7 +17,7 @@ timeout 300 python bench.py --impl reference --workload ppo_rnn --steps 1 --warm
 timeout 300 python bench.py --impl reference --workload ppo_smax --steps 1 --warmup 3 2>/dev/null | grep '^{' >> gpurun_out/bench_${TAG}.jsonl
 wc -l gpurun_out/bench_${TAG}.jsonl
 NCU=/usr/local/cuda/bin/ncu
-for w in smax3m mpe_large overcooked smax27m; do
+for w in smax3m smax2s3z mpe_large overcooked smax27m; do
   SKIP=4; [[ $w == smax* ]] && SKIP=30
   timeout 600 $NCU --metrics gpu__time_duration.sum --clock-control none -c 200 --csv \
     --log-file gpurun_out/launches_${TAG}_$w.csv python bench.py --workload $w --steps 5 --warmup 3 --no-e2e --no-cpu \
@@ -38,9 +38,9 @@ timeout 900 $NCU --set full --clock-control none --import-source on -k regex:ppo
   -o gpurun_out/prof_${TAG}_ppo_update -f python bench.py --workload ppo --steps 1 --warmup 3 --no-cpu --no-e2e \
   > /dev/null 2>&1
 # summarise the step-kernel captures here and keep only what fits gpurun's 64 MiB return
-python scripts/ncu_summary.py ${TAG} smax3m mpe_large overcooked smax27m > /dev/null 2>&1
+python scripts/ncu_summary.py ${TAG} smax3m smax2s3z mpe_large overcooked smax27m > /dev/null 2>&1
 mkdir -p gpurun_out/summary_${TAG}
 cp profiles/${TAG}_* profiles/ncu_traffic.json profiles/ncu_metrics.json gpurun_out/summary_${TAG}/ 2>/dev/null
-rm -f gpurun_out/prof_${TAG}_mpe_large.ncu-rep gpurun_out/prof_${TAG}_smax27m.ncu-rep gpurun_out/prof_${TAG}_overcooked.ncu-rep
+rm -f gpurun_out/prof_${TAG}_smax2s3z.ncu-rep gpurun_out/prof_${TAG}_mpe_large.ncu-rep gpurun_out/prof_${TAG}_smax27m.ncu-rep gpurun_out/prof_${TAG}_overcooked.ncu-rep
 du -sh gpurun_out
 ls gpurun_out | grep ${TAG}
