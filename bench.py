@@ -607,9 +607,13 @@ def run_gpu_arm(args, rank, world, local_rank):
     akeys = m.prng.split(m.prng.fold_in(key, 2), args.steps + args.warmup + 2)  # vector_env.cpp:202
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device="cuda")
 
+    fused = args.workload in FUSED_PROBE and not args.per_step
     venv.reset(key)
     for t in range(args.warmup):
-        venv.step_random(akeys[t])
+        if fused:  # the probe kernel itself warms up (module load, caches)
+            venv.probe_steps(m.prng.fold_in(key, 2), t, 1)
+        else:
+            venv.step_random(akeys[t])
         flush.fill_(float(t))
     torch.cuda.synchronize()
     venv.episode_stats(clear=True)
@@ -622,7 +626,6 @@ def run_gpu_arm(args, rank, world, local_rank):
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     fin_counts = torch.zeros(args.steps, dtype=torch.int64, device="cuda")
     launches0 = _native.lib().marl_launch_count()
-    fused = args.workload in FUSED_PROBE and not args.per_step
     if fused:
         # configs[0] is the reference's throughput_probe loop at 1024 envs, launch-
         # bound one launch per step: the K timed steps run as ONE fused launch

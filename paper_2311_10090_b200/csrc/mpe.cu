@@ -181,22 +181,31 @@ __device__ __forceinline__ double bound_penalty(double x) {  // mpe.cpp:348-352
   return 10.0 < e ? 10.0 : e;
 }
 
-template <class Sc, int S>
-__device__ __forceinline__ double reward(const Local<Sc>& s, int i, bool coop_prey) {  // mpe.cpp:354-384
-  if (S == kMpeSpread) {
-    double rew = 0.0;
+// simple_spread's landmark-coverage term of reward() (mpe.cpp:357-365): the
+// same value for every agent, so it is evaluated once per step.
+template <class Sc>
+__device__ __forceinline__ double spread_cover(const Local<Sc>& s) {
+  double rew = 0.0;
 #pragma unroll
-    for (int j = 0; j < Sc::L; ++j) {
-      double best = 1e18;
+  for (int j = 0; j < Sc::L; ++j) {
+    double best = 1e18;
 #pragma unroll
-      for (int a = 0; a < Sc::A; ++a) {
-        double dx = s.pos[2 * a] - lm(s, j, 0);
-        double dy = s.pos[2 * a + 1] - lm(s, j, 1);
-        double d = sqrt(dx * dx + dy * dy);
-        best = d < best ? d : best;
-      }
-      rew -= best;
+    for (int a = 0; a < Sc::A; ++a) {
+      double dx = s.pos[2 * a] - lm(s, j, 0);
+      double dy = s.pos[2 * a + 1] - lm(s, j, 1);
+      double d = sqrt(dx * dx + dy * dy);
+      best = d < best ? d : best;
     }
+    rew -= best;
+  }
+  return rew;
+}
+
+// cover: spread_cover(s) for simple_spread (unused otherwise)
+template <class Sc, int S>
+__device__ __forceinline__ double reward(const Local<Sc>& s, int i, bool coop_prey, double cover) {  // mpe.cpp:354-384
+  if (S == kMpeSpread) {
+    double rew = cover;
 #pragma unroll
     for (int a = 0; a < Sc::A; ++a)
       if (a != i && collides(s, a, i)) rew -= 1.0;
@@ -351,28 +360,21 @@ __global__ void __launch_bounds__(kThreads) mpe_reset_kernel(MpeState st, Launch
   block_store(lc.v.obs + i0 * ROW, s_obs, size_t(nvalid) * ROW * sizeof(float));
 }
 
-// One launch = K consecutive VectorEnv::step calls (K = 1 for marl_venv_step).
-// MULTI: the fused throughput_probe loop (vector_env.cpp:202-217) -- step k's
-// action key is split(fold_in(key, 2), T + 1)[t0 + k], derived in-kernel, and
-// the env's state, carry key and episode bookkeeping stay in registers across
-// the K steps.  Every step still writes every output view (obs, rewards,
-// dones, actions, finished, final_*), so after the launch the views hold step
-// t0 + K - 1's outputs exactly as K separate launches would leave them.
-template <int S, bool RANDOM, bool CONT, bool MULTI, int TPB>
-__global__ void __launch_bounds__(TPB) mpe_step_kernel(MpeState st, LaunchCommon lc, Key step_key,
-                                                       int coop_prey, uint64_t t0, int K) {
+template <int S, bool RANDOM, bool CONT>
+__global__ void __launch_bounds__(kThreads) mpe_step_kernel(MpeState st, LaunchCommon lc, Key step_key,
+                                                            int coop_prey) {
   using Sc = Scen<S>;
   constexpr int A = Sc::A, ROW = A * Sc::D;
-  __shared__ __align__(16) float s_obs[TPB * ROW];
-  __shared__ __align__(16) double s_rew[TPB * A];
-  __shared__ __align__(16) int32_t s_act[TPB * A];
-  __shared__ __align__(16) uint8_t s_done[TPB * (A + 1)];
-  __shared__ uint8_t s_fin[TPB];
+  __shared__ __align__(16) float s_obs[kThreads * ROW];
+  __shared__ __align__(16) double s_rew[kThreads * A];
+  __shared__ __align__(16) int32_t s_act[kThreads * A];
+  __shared__ __align__(16) uint8_t s_done[kThreads * (A + 1)];
+  __shared__ uint8_t s_fin[kThreads];
   if (*(volatile int*)lc.err) return;  // a pending contract error freezes the batch
 
-  const int64_t i0 = lc.begin + int64_t(blockIdx.x) * TPB;
+  const int64_t i0 = lc.begin + int64_t(blockIdx.x) * kThreads;
   const int64_t i = i0 + threadIdx.x;
-  const int nvalid = int(min64(TPB, lc.end - i0));
+  const int nvalid = int(min64(kThreads, lc.end - i0));
   const bool live = i < lc.end;
   float* my_obs = s_obs + threadIdx.x * ROW;
 
@@ -380,112 +382,353 @@ __global__ void __launch_bounds__(TPB) mpe_step_kernel(MpeState st, LaunchCommon
   Key carry{0, 0, 0, 0};
   double ep_ret = 0.0;
   int ep_len = 0;
-  bool any_reset = false;
+  bool done = false;
   if (live) {
     uint4 kw = lc.carry.keys[i];
     carry = Key{kw.x, kw.y, kw.z, kw.w};
     ep_ret = lc.carry.ep_return[i];
     ep_len = lc.carry.ep_length[i];
     load_state<Sc, S>(s, st, i, lc.n);
-  }
-  for (int k = 0; k < (MULTI ? K : 1); ++k) {
-    // MULTI: thread 0 drained the previous step's tile reads; nobody rewrites
-    // the tiles before that
-    if (MULTI && k > 0) __syncthreads();
-    const Key sk = MULTI ? split_child(step_key, t0 + uint64_t(k)) : step_key;
-    bool done = false;
-    if (live) {
-      int act[A];
-      float actf[CONT ? A * kBoxActDim : 1];
-      if (RANDOM && CONT) {
-        // box spaces: space.sample(fold_in(env_key, j)) = float(uniform(key, flat, 0, 1))
-        // (vector_env.cpp:179-181, spaces.cpp:48-54)
-        Key ek = split_child(sk, uint64_t(lc.offset + i));
-#pragma unroll
-        for (int j = 0; j < A; ++j) {
-          const Key kj = fold_in(ek, uint64_t(j));
-#pragma unroll
-          for (int q = 0; q < kBoxActDim; ++q)
-            actf[j * kBoxActDim + q] = q < Sc::n_actions(j) ? float(uniform_at(kj, uint64_t(q), 0.0, 1.0)) : 0.0f;
-        }
-        float4* dst = reinterpret_cast<float4*>(lc.v.actions_f + i * A * kBoxActDim);
-        if ((A * kBoxActDim) % 4 == 0) {
-#pragma unroll
-          for (int q = 0; q < A * kBoxActDim / 4; ++q)
-            dst[q] = make_float4(actf[4 * q], actf[4 * q + 1], actf[4 * q + 2], actf[4 * q + 3]);
-        } else {
-#pragma unroll
-          for (int q = 0; q < A * kBoxActDim; ++q) lc.v.actions_f[i * A * kBoxActDim + q] = actf[q];
-        }
-      } else if (CONT) {
-#pragma unroll
-        for (int q = 0; q < A * kBoxActDim; ++q) actf[q] = lc.v.actions_f[i * A * kBoxActDim + q];
-      } else if (RANDOM) {
-        // random_legal_actions (vector_env.cpp:169-187); MPE masks are all-legal
-        // (env.hpp:71-73) so the draw is bits(env_key, j) % n_actions.
-        Key ek = split_child(sk, uint64_t(lc.offset + i));
-#pragma unroll
-        for (int j = 0; j < A; ++j) {
-          act[j] = int(block_at(ek, uint64_t(j)) % uint64_t(Sc::n_actions(j)));
-          s_act[threadIdx.x * A + j] = act[j];
-        }
-      } else {
-#pragma unroll
-        for (int j = 0; j < A; ++j) act[j] = lc.v.actions[i * A + j];
-      }
 
-      physics<Sc, CONT>(s, act, actf);
-      done = s.steps >= kEpisodeSteps;
-      double sum = 0.0;
+    int act[A];
+    float actf[CONT ? A * kBoxActDim : 1];
+    if (RANDOM && CONT) {
+      // box spaces: space.sample(fold_in(env_key, j)) = float(uniform(key, flat, 0, 1))
+      // (vector_env.cpp:179-181, spaces.cpp:48-54)
+      Key ek = split_child(step_key, uint64_t(lc.offset + i));
 #pragma unroll
       for (int j = 0; j < A; ++j) {
-        double r = reward<Sc, S>(s, j, coop_prey != 0);
-        s_rew[threadIdx.x * A + j] = r;
-        sum += r;
-        s_done[threadIdx.x * (A + 1) + j] = done;
+        const Key kj = fold_in(ek, uint64_t(j));
+#pragma unroll
+        for (int k = 0; k < kBoxActDim; ++k)
+          actf[j * kBoxActDim + k] = k < Sc::n_actions(j) ? float(uniform_at(kj, uint64_t(k), 0.0, 1.0)) : 0.0f;
       }
-      s_done[threadIdx.x * (A + 1) + A] = done;
-      ep_ret = ep_ret + sum / double(A);  // team_reward, vector_env.cpp:14-18,99
-      ep_len = ep_len + 1;
+      float4* dst = reinterpret_cast<float4*>(lc.v.actions_f + i * A * kBoxActDim);
+      if ((A * kBoxActDim) % 4 == 0) {
+#pragma unroll
+        for (int q = 0; q < A * kBoxActDim / 4; ++q)
+          dst[q] = make_float4(actf[4 * q], actf[4 * q + 1], actf[4 * q + 2], actf[4 * q + 3]);
+      } else {
+#pragma unroll
+        for (int q = 0; q < A * kBoxActDim; ++q) lc.v.actions_f[i * A * kBoxActDim + q] = actf[q];
+      }
+    } else if (CONT) {
+#pragma unroll
+      for (int q = 0; q < A * kBoxActDim; ++q) actf[q] = lc.v.actions_f[i * A * kBoxActDim + q];
+    } else if (RANDOM) {
+      // random_legal_actions (vector_env.cpp:169-187); MPE masks are all-legal
+      // (env.hpp:71-73) so the draw is bits(env_key, j) % n_actions.
+      Key ek = split_child(step_key, uint64_t(lc.offset + i));
+#pragma unroll
+      for (int j = 0; j < A; ++j) {
+        act[j] = int(block_at(ek, uint64_t(j)) % uint64_t(Sc::n_actions(j)));
+        s_act[threadIdx.x * A + j] = act[j];
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < A; ++j) act[j] = lc.v.actions[i * A + j];
+    }
+
+    physics<Sc, CONT>(s, act, actf);
+    done = s.steps >= kEpisodeSteps;
+    double sum = 0.0;
+    const double cover = S == kMpeSpread ? spread_cover(s) : 0.0;
+#pragma unroll
+    for (int j = 0; j < A; ++j) {
+      double r = reward<Sc, S>(s, j, coop_prey != 0, cover);
+      s_rew[threadIdx.x * A + j] = r;
+      sum += r;
+      s_done[threadIdx.x * (A + 1) + j] = done;
+    }
+    s_done[threadIdx.x * (A + 1) + A] = done;
+    ep_ret = ep_ret + sum / double(A);  // team_reward, vector_env.cpp:14-18,99
+    ep_len = ep_len + 1;
+#pragma unroll
+    for (int a = 0; a < A; ++a) observe<Sc, S>(s, a, my_obs + a * Sc::D);
+    lc.v.finished[i] = done;
+    lc.v.final_returns[i] = done ? ep_ret : 0.0;
+    lc.v.final_lengths[i] = done ? ep_len : 0;
+  }
+  s_fin[threadIdx.x] = done;
+  stats_add(lc.stats, done, ep_len, ep_ret);
+
+  // Terminal observations leave as whole rows before auto-reset overwrites them.
+  if (__syncthreads_or(done)) {
+    for (int idx = threadIdx.x; idx < nvalid * ROW; idx += kThreads) {
+      int r = idx / ROW;
+      if (s_fin[r]) __stcs(lc.v.final_obs + i0 * ROW + idx, s_obs[idx]);
+    }
+    __syncthreads();
+    if (done) {  // vector_env.cpp:107-119: reset with the auto-reset child key
+      env_reset<Sc, S>(s, split_child(carry, 1));
 #pragma unroll
       for (int a = 0; a < A; ++a) observe<Sc, S>(s, a, my_obs + a * Sc::D);
+      ep_ret = 0.0;
+      ep_len = 0;
+    }
+  }
+  if (live) {
+    Key nk = split_child(carry, 2);  // vector_env.cpp:126
+    lc.carry.keys[i] = make_uint4(nk.k0, nk.k1, nk.c0, nk.c1);
+    lc.carry.ep_return[i] = ep_ret;
+    lc.carry.ep_length[i] = ep_len;
+    store_state<Sc, S>(s, st, i, lc.n, done);
+  }
+  // the block's rows leave as TMA bulk stores (one instruction per tile)
+  bulk_tile_fence();
+  tile_store(lc.v.obs + i0 * ROW, s_obs, size_t(nvalid) * ROW * sizeof(float));
+  tile_store(lc.v.rewards + i0 * A, s_rew, size_t(nvalid) * A * sizeof(double));
+  tile_store(lc.v.dones + i0 * (A + 1), s_done, size_t(nvalid) * (A + 1));
+  if (RANDOM && !CONT) tile_store(lc.v.actions + i0 * A, s_act, size_t(nvalid) * A * sizeof(int32_t));
+  tile_store_drain();
+}
+
+// Named CTA barriers (ids 1..4; 0 is __syncthreads) between the two warps of
+// the probe kernel: a producer arrives, a consumer waits.
+__device__ __forceinline__ void nbar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ void nbar_arrive(int id, int n) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+// K consecutive iterations of throughput_probe's loop (vector_env.cpp:202-217)
+// in ONE launch: step k's action key is split(parent, t0 + k) (parent =
+// fold_in(key, 2)), derived in-kernel; the env's state, carry key and episode
+// bookkeeping stay on chip across the K steps.  Every step still writes every
+// output view (obs, rewards, dones, actions, finished, final_*), so after the
+// launch the views hold step t0 + K - 1's outputs exactly as K separate
+// mpe_step_kernel launches leave them.
+//
+// Small batches (configs[0]: 1024 envs) are latency-bound -- one env's step
+// is a dependent chain of Threefry blocks and fp64 sqrt / div / exp -- so the
+// step is split over a three-warp pipeline per 32 envs (one env per lane in
+// each warp), handing data on through double-buffered shared-memory slots
+// guarded by named barriers:
+//   KEY  warp, one step ahead: the action draw of random_legal_actions, the
+//        carry chain split(carry, 2) and, when the step ends an episode (MPE
+//        episodes are exactly 25 steps, so the key warp knows), the
+//        auto-reset state from split(carry, 1);
+//   SIM  warp: the only true recurrence, physics (mpe.cpp:137-214);
+//   POST warp, one step behind: rewards, dones, episode bookkeeping,
+//        statistics and every output row (terminal rows before the reset).
+// Rows leave straight from registers (no staging).
+template <int S, bool CONT>
+__global__ void __launch_bounds__(96) mpe_probe_kernel(MpeState st, LaunchCommon lc, Key parent, int coop_prey,
+                                                       uint64_t t0, int K) {
+  using Sc = Scen<S>;
+  constexpr int A = Sc::A, D = Sc::D, ROW = A * D, NAF = CONT ? A * kBoxActDim : 1, NP = 2 * Sc::E,
+                NV = 2 * Sc::A, NC = Sc::A * Sc::DC;
+  struct KeySlot {  // KEY -> SIM
+    float actf[NAF][32];
+    int32_t act[A][32];
+    double rpos[NP][32];
+    int32_t rgoal[32];
+    uint32_t done;  // bit lane: the step ends lane's episode
+  };
+  struct SimSlot {  // SIM -> POST: the post-physics state (+ the reset state when done)
+    double pos[NP][32], vel[NV][32], comm[NC][32], rpos[NP][32];
+    int32_t goal[32], rgoal[32];
+    uint32_t done;
+  };
+  __shared__ KeySlot kslot[2];
+  __shared__ SimSlot sslot[2];
+  if (*(volatile int*)lc.err) return;  // a pending contract error freezes the batch
+  const int lane = threadIdx.x & 31, role = threadIdx.x >> 5;  // 0 SIM, 1 KEY, 2 POST
+  const int64_t i = lc.begin + int64_t(blockIdx.x) * 32 + lane;
+  const bool live = i < lc.end;
+  // barrier ids: KEY->SIM full 1+b / empty 3+b, SIM->POST full 5+b / empty 7+b
+
+  if (role == 1) {  // ------------------------------------------------ KEY
+    Key carry{0, 0, 0, 0};
+    int steps = 0;
+    if (live) {
+      const uint4 kw = lc.carry.keys[i];
+      carry = Key{kw.x, kw.y, kw.z, kw.w};
+      steps = st.steps[i];
+    }
+    for (int k = 0; k < K; ++k) {
+      const int b = k & 1;
+      if (k >= 2) nbar_sync(3 + b, 64);  // SIM has consumed step k - 2's slot
+      KeySlot& sl = kslot[b];
+      bool done = false;
+      if (live) {
+        const Key ek = split_child(split_child(parent, t0 + uint64_t(k)), uint64_t(lc.offset + i));
+        if (CONT) {  // space.sample(fold_in(env_key, j)) (vector_env.cpp:179-181, spaces.cpp:48-54)
+#pragma unroll
+          for (int j = 0; j < A; ++j) {
+            const Key kj = fold_in(ek, uint64_t(j));
+#pragma unroll
+            for (int q = 0; q < kBoxActDim; ++q) {
+              const float v = q < Sc::n_actions(j) ? float(uniform_at(kj, uint64_t(q), 0.0, 1.0)) : 0.0f;
+              sl.actf[j * kBoxActDim + q][lane] = v;
+              lc.v.actions_f[i * A * kBoxActDim + j * kBoxActDim + q] = v;
+            }
+          }
+        } else {  // random_legal_actions with all-legal masks (vector_env.cpp:169-187, env.hpp:71-73)
+#pragma unroll
+          for (int j = 0; j < A; ++j) {
+            const int a = int(mod_small(block_at(ek, uint64_t(j)), uint32_t(Sc::n_actions(j))));
+            sl.act[j][lane] = a;
+            lc.v.actions[i * A + j] = a;
+          }
+        }
+        steps += 1;
+        done = steps >= kEpisodeSteps;
+        if (done) {  // env->reset(split(carry, 3)[1]) (vector_env.cpp:107-119)
+          Local<Sc> r;
+          env_reset<Sc, S>(r, split_child(carry, 1));
+#pragma unroll
+          for (int q = 0; q < NP; ++q) sl.rpos[q][lane] = r.pos[q];
+          sl.rgoal[lane] = r.goal;
+          steps = 0;
+        }
+        carry = split_child(carry, 2);  // vector_env.cpp:126
+      }
+      const unsigned dm = __ballot_sync(0xffffffffu, done);
+      if (lane == 0) sl.done = dm;
+      nbar_arrive(1 + b, 64);  // slot b holds step k
+    }
+    if (live) lc.carry.keys[i] = make_uint4(carry.k0, carry.k1, carry.c0, carry.c1);
+    return;
+  }
+
+  if (role == 0) {  // ------------------------------------------------ SIM
+    Local<Sc> s;
+    if (live) load_state<Sc, S>(s, st, i, lc.n);
+    bool any_reset = false;
+    for (int k = 0; k < K; ++k) {
+      const int b = k & 1;
+      nbar_sync(1 + b, 64);  // KEY's slot b holds step k
+      const KeySlot& kl = kslot[b];
+      int act[A];
+      float actf[NAF];
+      if (CONT) {
+#pragma unroll
+        for (int q = 0; q < NAF; ++q) actf[q] = kl.actf[q][lane];
+      } else {
+#pragma unroll
+        for (int j = 0; j < A; ++j) act[j] = kl.act[j][lane];
+      }
+      const unsigned dm = kl.done;
+      const bool done = (dm >> lane) & 1u;
+      double rpos[NP];
+      int rgoal = -1;
+      if (done) {
+#pragma unroll
+        for (int q = 0; q < NP; ++q) rpos[q] = kl.rpos[q][lane];
+        rgoal = kl.rgoal[lane];
+      }
+      if (k + 2 < K) nbar_arrive(3 + b, 64);  // KEY may refill slot b (step k + 2)
+      if (live) physics<Sc, CONT>(s, act, actf);
+      if (k >= 2) nbar_sync(7 + b, 64);  // POST has consumed step k - 2's slot
+      SimSlot& sl = sslot[b];
+      if (live) {
+#pragma unroll
+        for (int q = 0; q < NP; ++q) sl.pos[q][lane] = s.pos[q];
+#pragma unroll
+        for (int q = 0; q < NV; ++q) sl.vel[q][lane] = s.vel[q];
+#pragma unroll
+        for (int q = 0; q < NC; ++q) sl.comm[q][lane] = s.comm[q];
+        sl.goal[lane] = s.goal;
+        if (done) {
+#pragma unroll
+          for (int q = 0; q < NP; ++q) sl.rpos[q][lane] = rpos[q];
+          sl.rgoal[lane] = rgoal;
+        }
+      }
+      if (lane == 0) sl.done = dm;
+      nbar_arrive(5 + b, 64);  // slot b holds step k's state
+      if (live && done) {  // the auto-reset state (vector_env.cpp:107-119)
+#pragma unroll
+        for (int q = 0; q < NP; ++q) s.pos[q] = rpos[q];
+#pragma unroll
+        for (int q = 0; q < NV; ++q) s.vel[q] = 0.0;
+#pragma unroll
+        for (int q = 0; q < NC; ++q) s.comm[q] = 0.0;
+        s.steps = 0;
+        s.goal = rgoal;
+        any_reset = true;
+      }
+    }
+    if (live) store_state<Sc, S>(s, st, i, lc.n, any_reset);
+    return;
+  }
+
+  // ---------------------------------------------------------------- POST
+  double ep_ret = 0.0;
+  int ep_len = 0;
+  if (live) {
+    ep_ret = lc.carry.ep_return[i];
+    ep_len = lc.carry.ep_length[i];
+  }
+  static_assert(ROW % 2 == 0, "observation rows are stored as float2");
+  auto put_rows = [&](float* dst, const Local<Sc>& cs) {
+    float row[ROW];
+#pragma unroll
+    for (int a = 0; a < A; ++a) observe<Sc, S>(cs, a, row + a * D);
+    float2* d2 = reinterpret_cast<float2*>(dst + i * ROW);
+#pragma unroll
+    for (int q = 0; q < ROW / 2; ++q) d2[q] = make_float2(row[2 * q], row[2 * q + 1]);
+  };
+  for (int k = 0; k < K; ++k) {
+    const int b = k & 1;
+    nbar_sync(5 + b, 64);  // SIM's slot b holds step k's state
+    const SimSlot& sl = sslot[b];
+    const bool done = (sl.done >> lane) & 1u;
+    Local<Sc> s;
+    double rpos[NP];
+    int rgoal = -1;
+    if (live) {
+#pragma unroll
+      for (int q = 0; q < NP; ++q) s.pos[q] = sl.pos[q][lane];
+#pragma unroll
+      for (int q = 0; q < NV; ++q) s.vel[q] = sl.vel[q][lane];
+#pragma unroll
+      for (int q = 0; q < NC; ++q) s.comm[q] = sl.comm[q][lane];
+      s.goal = sl.goal[lane];
+      if (done) {
+#pragma unroll
+        for (int q = 0; q < NP; ++q) rpos[q] = sl.rpos[q][lane];
+        rgoal = sl.rgoal[lane];
+      }
+    }
+    if (k + 2 < K) nbar_arrive(7 + b, 64);  // SIM may refill slot b (step k + 2)
+    if (live) {
+      double sum = 0.0;
+      const double cover = S == kMpeSpread ? spread_cover(s) : 0.0;
+#pragma unroll
+      for (int j = 0; j < A; ++j) {
+        const double r = reward<Sc, S>(s, j, coop_prey != 0, cover);
+        lc.v.rewards[i * A + j] = r;
+        sum += r;
+        lc.v.dones[i * (A + 1) + j] = done;
+      }
+      lc.v.dones[i * (A + 1) + A] = done;
+      ep_ret = ep_ret + sum / double(A);  // team_reward, vector_env.cpp:14-18,99
+      ep_len = ep_len + 1;
       lc.v.finished[i] = done;
       lc.v.final_returns[i] = done ? ep_ret : 0.0;
       lc.v.final_lengths[i] = done ? ep_len : 0;
     }
-    s_fin[threadIdx.x] = done;
     stats_add(lc.stats, done, ep_len, ep_ret);
-
-    // Terminal observations leave as whole rows before auto-reset overwrites them.
-    if (__syncthreads_or(done)) {
-      for (int idx = threadIdx.x; idx < nvalid * ROW; idx += TPB) {
-        int r = idx / ROW;
-        if (s_fin[r]) __stcs(lc.v.final_obs + i0 * ROW + idx, s_obs[idx]);
-      }
-      __syncthreads();
-      if (done) {  // vector_env.cpp:107-119: reset with the auto-reset child key
-        env_reset<Sc, S>(s, split_child(carry, 1));
+    if (live) {
+      if (done) {  // terminal rows, then the reset state's rows
+        put_rows(lc.v.final_obs, s);
 #pragma unroll
-        for (int a = 0; a < A; ++a) observe<Sc, S>(s, a, my_obs + a * Sc::D);
+        for (int q = 0; q < NP; ++q) s.pos[q] = rpos[q];
+#pragma unroll
+        for (int q = 0; q < NV; ++q) s.vel[q] = 0.0;
+#pragma unroll
+        for (int q = 0; q < NC; ++q) s.comm[q] = 0.0;
+        s.goal = rgoal;
         ep_ret = 0.0;
         ep_len = 0;
-        any_reset = true;
       }
+      put_rows(lc.v.obs, s);
     }
-    carry = split_child(carry, 2);  // vector_env.cpp:126
-    // the block's rows leave as TMA bulk stores (one instruction per tile)
-    bulk_tile_fence();
-    tile_store(lc.v.obs + i0 * ROW, s_obs, size_t(nvalid) * ROW * sizeof(float));
-    tile_store(lc.v.rewards + i0 * A, s_rew, size_t(nvalid) * A * sizeof(double));
-    tile_store(lc.v.dones + i0 * (A + 1), s_done, size_t(nvalid) * (A + 1));
-    if (RANDOM && !CONT) tile_store(lc.v.actions + i0 * A, s_act, size_t(nvalid) * A * sizeof(int32_t));
-    tile_store_drain();
   }
   if (live) {
-    lc.carry.keys[i] = make_uint4(carry.k0, carry.k1, carry.c0, carry.c1);
     lc.carry.ep_return[i] = ep_ret;
     lc.carry.ep_length[i] = ep_len;
-    store_state<Sc, S>(s, st, i, lc.n, any_reset);
   }
 }
 
@@ -552,33 +795,28 @@ void mpe_launch_step(const MpeConfig& c, const MpeState& s, const LaunchCommon& 
                      KeyWords step_key) {
   unsigned g = grid_for(lc.end - lc.begin, kThreads);
   Key k = to_key(step_key);
-#define MARL_MPE_STEP(S, R, C) \
-  mpe_step_kernel<S, R, C, false, kThreads><<<g, kThreads, 0, lc.stream>>>(s, lc, k, c.coop_prey, 0, 1)
-#define MARL_MPE_STEPS(S)                                                                          \
-  c.continuous ? (random ? MARL_MPE_STEP(S, true, true) : MARL_MPE_STEP(S, false, true))           \
-               : (random ? MARL_MPE_STEP(S, true, false) : MARL_MPE_STEP(S, false, false))
+#define MARL_MPE_STEP(S)                                                                  \
+  c.continuous ? (random ? mpe_step_kernel<S, true, true><<<g, kThreads, 0, lc.stream>>>(s, lc, k, c.coop_prey)   \
+                         : mpe_step_kernel<S, false, true><<<g, kThreads, 0, lc.stream>>>(s, lc, k, c.coop_prey)) \
+               : (random ? mpe_step_kernel<S, true, false><<<g, kThreads, 0, lc.stream>>>(s, lc, k, c.coop_prey)  \
+                         : mpe_step_kernel<S, false, false><<<g, kThreads, 0, lc.stream>>>(s, lc, k, c.coop_prey))
   switch (c.scenario) {
-    case kMpeSpread: MARL_MPE_STEPS(kMpeSpread); break;
-    case kMpeSpeakerListener: MARL_MPE_STEPS(kMpeSpeakerListener); break;
-    default: MARL_MPE_STEPS(kMpeTag); break;
+    case kMpeSpread: MARL_MPE_STEP(kMpeSpread); break;
+    case kMpeSpeakerListener: MARL_MPE_STEP(kMpeSpeakerListener); break;
+    default: MARL_MPE_STEP(kMpeTag); break;
   }
-#undef MARL_MPE_STEPS
 #undef MARL_MPE_STEP
   ++g_launches;
 }
 
-// K probe steps in one launch (see mpe_step_kernel's MULTI).  Small batches
-// are latency-bound, so the CTAs are one warp each: the envs spread over as
-// many SMs as possible.
+// K probe steps in one launch (mpe_probe_kernel).
 void mpe_launch_probe(const MpeConfig& c, const MpeState& s, const LaunchCommon& lc, KeyWords parent,
                       uint64_t t0, int K) {
-  constexpr int kTpb = 32;
-  unsigned g = grid_for(lc.end - lc.begin, kTpb);
-  Key k = to_key(parent);
-#define MARL_MPE_PROBE(S)                                                                                  \
-  c.continuous                                                                                             \
-      ? mpe_step_kernel<S, true, true, true, kTpb><<<g, kTpb, 0, lc.stream>>>(s, lc, k, c.coop_prey, t0, K) \
-      : mpe_step_kernel<S, true, false, true, kTpb><<<g, kTpb, 0, lc.stream>>>(s, lc, k, c.coop_prey, t0, K)
+  const unsigned g = grid_for(lc.end - lc.begin, 32);
+  const Key k = to_key(parent);
+#define MARL_MPE_PROBE(S)                                                                        \
+  c.continuous ? mpe_probe_kernel<S, true><<<g, 96, 0, lc.stream>>>(s, lc, k, c.coop_prey, t0, K) \
+               : mpe_probe_kernel<S, false><<<g, 96, 0, lc.stream>>>(s, lc, k, c.coop_prey, t0, K)
   switch (c.scenario) {
     case kMpeSpread: MARL_MPE_PROBE(kMpeSpread); break;
     case kMpeSpeakerListener: MARL_MPE_PROBE(kMpeSpeakerListener); break;
