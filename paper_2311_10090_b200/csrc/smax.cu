@@ -126,6 +126,19 @@ struct PairIt {
 };
 
 // ---------------------------------------------------------------- separation
+// glibc hypot with the common case inline: finite operands whose ratio and
+// magnitudes need none of __hypot's rescaling go straight to its kernel (the
+// same operations hypot_glibc performs for them); the rest call it.  Inline
+// on the separation path: the out-of-line call spills the caller's live
+// registers around every push and every touching-pair test.
+__device__ __forceinline__ double hypot_fast(double x, double y) {
+  x = fabs(x);
+  y = fabs(y);
+  const double ax = x < y ? y : x, ay = x < y ? x : y;
+  if (ax <= 0x1p+511 && ay >= 0x1p-511 && ay > ax * 0x1p-54) return hypot_kernel(ax, ay);
+  return hypot_glibc(x, y);
+}
+
 __device__ __forceinline__ unsigned long long bits_above(int i) { return i >= 63 ? 0ull : ~0ull << (i + 1); }
 
 // Unit bitmask (bit u) of a per-unit predicate held by the owning lanes.
@@ -180,7 +193,7 @@ __device__ __forceinline__ void separation_pass(const Params& P, EnvSm<CAP, HT, 
         const double dx = e.x[b] - xa, dy = e.y[b] - ya;
         const Thresh& R = P.ps[ta][e.T(b)].rsum;
         if (dx * dx + dy * dy > R.r2hi) continue;  // hypot(dx,dy) > ra+rb: overlap <= 0
-        const double dd = hypot_glibc(dx, dy);
+        const double dd = hypot_fast(dx, dy);
         hit[j] = R.r - dd > 0.0;
         hdx[j] = dx;
         hdy[j] = dy;
@@ -263,7 +276,7 @@ __device__ __forceinline__ bool lane_pairs_overlap(const Params& P, const EnvSm<
     if (d2 > P.sep_r2hi) return false;  // farther than any radius sum
     const Thresh& R = P.ps[e.T(a)][e.T(b)].rsum;
     if (d2 > R.r2hi) return false;
-    return d2 < R.r2lo || R.r - hypot_glibc(dx, dy) > 0.0;
+    return d2 < R.r2lo || R.r - hypot_fast(dx, dy) > 0.0;
   });
 }
 
@@ -278,7 +291,7 @@ __device__ __forceinline__ bool lane_pairs_within_tol(const Params& P, const Env
     const double d2 = dx * dx + dy * dy;
     if (d2 > S.otol.r2hi) return false;      // surely sum - d <= tol
     if (d2 < S.otol.r2lo) return true;       // surely sum - d > tol
-    return !(S.rsum.r - hypot_glibc(dx, dy) <= kSepTol);
+    return !(S.rsum.r - hypot_fast(dx, dy) <= kSepTol);
   });
 }
 
