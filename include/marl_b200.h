@@ -337,6 +337,17 @@ void marl_prng_fold_in(const uint32_t key[4], uint64_t data, uint32_t out[4]);
 uint64_t marl_prng_bits(const uint32_t key[4], uint64_t index);
 void marl_threefry2x32(uint32_t k0, uint32_t k1, uint32_t x0, uint32_t x1, uint32_t out[2]);
 
+/* ---- tensor-core GEMM ---------------------------------------------------
+ * The recurrent policy's contractions (embed / GRU / post / head and their
+ * BPTT weight gradients; nn.hpp:42-70 matmul_nt / matmul_nn / matmul_tn over
+ * the RnnBranch of actor_critic.hpp:74-200), exposed for reuse and testing:
+ * C[M x N] = beta*C + A . B'^T, A(m, k) = A[m*sam + k*sak],
+ * B'(n, k) = B[n*sbn + k*sbk], C(m, n) = C[m*ldc + n]; fp32 in and out,
+ * fp32-accurate 3xTF32 on tcgen05, deterministic; device pointers, enqueued
+ * on `stream` (a cudaStream_t, NULL = default). */
+int marl_gemm_f32(int64_t M, int N, int64_t K, const float* A, int64_t sam, int64_t sak, const float* B, int64_t sbn,
+                  int64_t sbk, float* C, int64_t ldc, float beta, void* stream);
+
 /* ---- diagnostics ------------------------------------------------------ */
 const char* marl_last_error(void);
 uint64_t marl_launch_count(void); /* kernels launched by this library */

@@ -54,7 +54,7 @@ EXPORTS = [
     "marl_venv_download", "marl_venv_views", "marl_copy_device_to_host", "marl_venv_legal", "marl_venv_state_hash",
     "marl_venv_episode_stats", "marl_venv_sync", "marl_throughput_probe",
     "marl_prng_key_from_seed", "marl_prng_split", "marl_prng_fold_in", "marl_prng_bits",
-    "marl_threefry2x32", "marl_last_error", "marl_launch_count", "marl_set_grid_cap", "marl_version",
+    "marl_threefry2x32", "marl_gemm_f32", "marl_last_error", "marl_launch_count", "marl_set_grid_cap", "marl_version",
     "marl_venv_world_state_size", "marl_venv_world_state",
     "marl_rollout_policy_spec", "marl_rollout_create", "marl_rollout_set_params", "marl_rollout_begin",
     "marl_rollout_collect", "marl_rollout_get_views", "marl_rollout_destroy",
@@ -151,6 +151,8 @@ def lib() -> C.CDLL:
     L.marl_last_error.restype = C.c_char_p
     L.marl_launch_count.restype = C.c_uint64
     L.marl_set_grid_cap.argtypes = [C.c_int]
+    i64 = C.c_int64
+    L.marl_gemm_f32.argtypes = [i64, C.c_int, i64, vp, i64, i64, vp, i64, i64, vp, i64, C.c_float, vp]
     L.marl_version.restype = C.c_char_p
     _lib = L
     return L

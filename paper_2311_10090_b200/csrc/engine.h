@@ -425,6 +425,13 @@ void launch_validate_box(const float* actions, int64_t n, int A, const int32_t* 
 // Kernel launches issued by this library since load (evidence counter).
 extern unsigned long long g_launches;
 
+// gemm_tc.cu: C[M x N] = beta C + A . B'^T with A(m, k) = A[m*sam + k*sak] and
+// B'(n, k) = B[n*sbn + k*sbk] (fp32-accurate 3xTF32 on tcgen05); column sums
+// g[o] = beta g[o] + sum_k D[k*ldd + o] (fixed-order reduction).
+cudaError_t tc_gemm(cudaStream_t st, int64_t M, int N, int64_t K, const float* A, int64_t sam, int64_t sak,
+                    const float* B, int64_t sbn, int64_t sbk, float* C, int64_t ldc, float beta);
+cudaError_t tc_colsum(cudaStream_t st, int O, int64_t K, const float* D, int64_t ldd, float* g, float beta);
+
 // Test knob (marl_set_grid_cap): upper bound on the grid of every persistent
 // (grid-stride / tile-loop) kernel, so small parity inputs drive each CTA or
 // warp through several iterations of its loop.  0 = no cap (the default).

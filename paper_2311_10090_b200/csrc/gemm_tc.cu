@@ -1,0 +1,477 @@
+// fp32-accurate GEMMs on the 5th-generation tensor cores (3xTF32 on tcgen05)
+// for the recurrent policy's per-step and BPTT contractions (rollout_host.cpp,
+// ppo_host.cpp: the embed / GRU / post / head layers of the reference's
+// RnnBranch, actor_critic.hpp:74-200, nn.hpp:200-318, and their weight
+// gradients).  These are tall-skinny GEMMs -- rows x (18..1024) x (1..384) --
+// bound by HBM, so the tensor pipe has room for the split-precision scheme
+// that keeps them at fp32 accuracy:
+//     a = a_hi + a_lo   (a_hi = a with its low 13 mantissa bits cleared, an
+//                        exact tf32 value; a_lo = a - a_hi, exact in fp32)
+//     a.b ~= a_hi.b_hi + a_hi.b_lo + a_lo.b_hi      (fp32 accumulation in TMEM)
+// The dropped a_lo.b_lo term and the tf32 rounding of the lo parts are
+// ~2^-22 relative to each product: the same order as fp32 rounding.
+//
+// One kernel serves every operand layout: C[M x N] (+)= A[M x K] . B'[N x K]^T
+// with element strides A(m, k) = A[m*sam + k*sak], B'(n, k) = B[n*sbn + k*sbk],
+// so row-major, transposed and "sum over rows" (weight-gradient) forms are the
+// same code.  A CTA owns a 128-row M tile and an N tile of up to 256 columns
+// (one MMA per K step: tcgen05.mma.cta_group::1.kind::tf32, M = 128,
+// accumulators in TMEM).  K advances in chunks of 32: the raw fp32 chunks of
+// A and B' stream into a ring of NS shared-memory stages with cp.async (16-,
+// 8- or 4-byte copies by alignment, zero-filled outside the matrix), issued
+// NS - 1 chunks ahead so HBM latency stays hidden; the 128 threads then split
+// each landed chunk into the hi / lo images in the canonical no-swizzle
+// K-major layout (one or two tile sets, so the split of chunk c + 1 overlaps
+// the MMAs on chunk c), one elected thread issues the 3 x 4 MMAs and commits
+// them to the tile set's mbarrier, and the accumulator rows come back with
+// tcgen05.ld.  Long reductions (the weight
+// gradients sum over every (t, row)) split K across CTAs into per-split
+// partial tiles folded in a fixed order: results are deterministic.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <map>
+#include <mutex>
+
+#include "common.cuh"
+#include "engine.h"
+#include "tc.cuh"
+
+namespace marl_b200 {
+namespace {
+
+constexpr int kGemmM = 128;        // rows per CTA (UMMA M)
+constexpr int kGemmKC = 16;        // K elements per chunk (two MMA K steps of 8)
+constexpr int kGemmMaxN = 128;     // columns per CTA (UMMA N <= 256; 128 keeps three CTAs per SM)
+constexpr int kGemmThreads = 128;  // one TMEM lane (accumulator row) per thread
+constexpr int kRawPitch = kGemmKC + 4;  // raw K-contiguous rows, padded against bank conflicts
+constexpr uint32_t kGemmSmemMax = 227 * 1024 / 3 - 1024;  // three CTAs (three tiles in flight) per SM
+constexpr int kEpiPitch = 33;  // epilogue staging rows (32 columns + 1 against bank conflicts)
+
+// byte offset of element (r, k) in a K-major no-swizzle canonical [rows x kKC]
+// 4-byte tile: 8-row x 16-byte core matrices, K neighbours 128 B apart, 8-row
+// groups (kKC/4)*128 B apart
+__host__ __device__ __forceinline__ uint32_t canon4(int r, int k) {
+  return uint32_t((r >> 3) * ((kGemmKC / 4) * 128) + (k >> 2) * 128 + (r & 7) * 16 + (k & 3) * 4);
+}
+
+// kind::tf32 instruction descriptor: tf32 A/B (format 2), fp32 D, K-major, M x N
+__host__ __device__ constexpr uint32_t idesc_tf32(int M, int N) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | (uint32_t(N >> 3) << 17) | (uint32_t(M >> 4) << 24);
+}
+
+__device__ __forceinline__ void umma_tf32(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+
+// K-major operand descriptor of a canonical [rows x kKC] tile, K step k0 (multiple of 8)
+__device__ __forceinline__ uint64_t desc4(const void* tile, int k0) {
+  return desc_raw(smem_u32(tile) + uint32_t(k0 >> 2) * 128u, 128u, (kGemmKC / 4) * 128u);
+}
+
+// cp.async of SZ bytes (4, 8 or 16), zero-filled beyond src_bytes
+template <int SZ>
+__device__ __forceinline__ void cp_async(void* sdst, const void* gsrc, uint32_t src_bytes) {
+  if constexpr (SZ == 16)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(sdst)), "l"(gsrc), "r"(src_bytes)
+                 : "memory");
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;" ::"r"(smem_u32(sdst)), "l"(gsrc), "n"(SZ),
+                 "r"(src_bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// How an operand X(r, k) = X[r*sr + k*sk] is staged: K-contiguous (raw rows
+// [r][kRawPitch]) with copies of `vec` floats, or rows-contiguous (raw
+// [k][rows]) with copies of `vec` floats along r, or element by element.
+struct OpLayout {
+  const float* X;
+  int64_t sr, sk;
+  int kind;  // 0: K-contiguous, 1: rows-contiguous, 2: general (raw [r][kRawPitch])
+  int vec;   // floats per copy (1, 2, 4)
+};
+
+struct GemmArgs {
+  OpLayout a, b;
+  float* C;        // output (split == 1) ...
+  float* part;     // ... or [split][M][N] partial tiles (split > 1)
+  int64_t M, K, ldc;
+  int N, npad;     // columns; npad: MMA N of a tile (multiple of 16)
+  int ntile;       // columns per N tile
+  int split;       // K splits
+  int64_t kchunk;  // K elements per split (multiple of kGemmKC)
+  float beta;
+  uint32_t tmem_cols;
+  int ns, nt;      // raw stages, hi/lo tile sets
+  uint32_t a_raw, b_raw, a_tile, b_tile;  // bytes
+};
+
+__host__ __device__ inline uint32_t raw_bytes(int rows, int kind) {
+  return kind == 1 ? uint32_t(kGemmKC) * rows * 4 : uint32_t(rows) * kRawPitch * 4;
+}
+
+// Issue the cp.async copies of chunk [k0, k0 + KC) of rows [r0, r0 + rows)
+// (valid rows < rvalid, valid k < K) into a raw stage.
+template <int V>
+__device__ __forceinline__ void fetch_v(float* raw, const OpLayout& o, int64_t r0, int rows, int64_t rvalid, int64_t k0,
+                                        int64_t K) {
+  if (o.kind == 1) {  // raw[k][r], copies along r
+    const int per_k = rows / V;
+    for (int idx = threadIdx.x; idx < per_k * kGemmKC; idx += kGemmThreads) {
+      const int k = idx / per_k, r = (idx - k * per_k) * V;
+      const int64_t gk = k0 + k, gr = r0 + r;
+      int64_t nv = gk < K ? rvalid - gr : 0;
+      nv = nv < 0 ? 0 : nv > V ? V : nv;
+      const float* src = nv ? o.X + gr * o.sr + gk * o.sk : o.X;
+      cp_async<4 * V>(raw + k * rows + r, src, uint32_t(nv * 4));
+    }
+  } else {  // raw[r][k], copies along k (kind 0) or single elements (kind 2, V = 1)
+    const int per_r = kGemmKC / V;
+    for (int idx = threadIdx.x; idx < rows * per_r; idx += kGemmThreads) {
+      const int r = idx / per_r, k = (idx - r * per_r) * V;
+      const int64_t gk = k0 + k, gr = r0 + r;
+      int64_t nv = gr < rvalid ? K - gk : 0;
+      nv = nv < 0 ? 0 : nv > V ? V : nv;
+      const float* src = nv ? o.X + gr * o.sr + gk * o.sk : o.X;
+      cp_async<4 * V>(raw + r * kRawPitch + k, src, uint32_t(nv * 4));
+    }
+  }
+}
+__device__ __forceinline__ void fetch(float* raw, const OpLayout& o, int64_t r0, int rows, int64_t rvalid, int64_t k0,
+                                      int64_t K) {
+  if (o.vec == 4) fetch_v<4>(raw, o, r0, rows, rvalid, k0, K);
+  else if (o.vec == 2) fetch_v<2>(raw, o, r0, rows, rvalid, k0, K);
+  else fetch_v<1>(raw, o, r0, rows, rvalid, k0, K);
+}
+
+// hi / lo tf32 images of v: hi = v with the low 13 mantissa bits cleared
+// (exact in tf32), lo = v - hi (exact in fp32)
+__device__ __forceinline__ void split_tf32(float v, float& hi, float& lo) {
+  hi = __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
+  lo = v - hi;
+}
+
+// raw stage -> hi / lo canonical tiles (four K per thread step)
+__device__ __forceinline__ void convert(const float* raw, int kind, int rows, uint8_t* hi, uint8_t* lo) {
+  for (int idx = threadIdx.x; idx < rows * (kGemmKC / 4); idx += kGemmThreads) {
+    int r, k;
+    float4 v;
+    if (kind == 1) {  // raw[k][r]: consecutive threads take consecutive rows
+      r = idx % rows;
+      k = (idx / rows) * 4;
+      v = make_float4(raw[k * rows + r], raw[(k + 1) * rows + r], raw[(k + 2) * rows + r], raw[(k + 3) * rows + r]);
+    } else {
+      r = idx % rows;
+      k = (idx / rows) * 4;
+      v = *reinterpret_cast<const float4*>(raw + r * kRawPitch + k);
+    }
+    float4 h, l;
+    split_tf32(v.x, h.x, l.x);
+    split_tf32(v.y, h.y, l.y);
+    split_tf32(v.z, h.z, l.z);
+    split_tf32(v.w, h.w, l.w);
+    *reinterpret_cast<float4*>(hi + canon4(r, k)) = h;
+    *reinterpret_cast<float4*>(lo + canon4(r, k)) = l;
+  }
+}
+
+__global__ void __launch_bounds__(kGemmThreads, 3) gemm_tf32x3_kernel(GemmArgs g) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const int mt = blockIdx.x, nt = blockIdx.y, sp = blockIdx.z;
+  const int64_t m0 = int64_t(mt) * kGemmM;
+  const int n0 = nt * g.ntile;
+  const int nvalid = min(g.ntile, g.N - n0);
+  const int64_t kb = int64_t(sp) * g.kchunk, ke = min(g.K, kb + g.kchunk);
+  const int nch = int((ke - kb + kGemmKC - 1) / kGemmKC);
+  // smem: [tile sets: A hi, A lo, B hi, B lo] x nt, [raw stages: A, B] x ns, 2 barriers, TMEM slot
+  const uint32_t set_bytes = 2 * g.a_tile + 2 * g.b_tile, stage_bytes = g.a_raw + g.b_raw;
+  uint8_t* raw0 = smem + g.nt * set_bytes;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(raw0 + max(g.ns * stage_bytes, uint32_t(4 * 32 * kEpiPitch * 4)));
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 2);
+  const int warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) {
+    for (int q = 0; q < 2; ++q) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar + q)) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(g.tmem_cols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  OpLayout bo = g.b;
+  bo.X = g.b.X + int64_t(n0) * g.b.sr;
+  auto issue = [&](int c) {  // raw chunk c -> stage c % ns (one commit group per call)
+    if (c < nch) {
+      float* ra = reinterpret_cast<float*>(raw0 + (c % g.ns) * stage_bytes);
+      float* rb = reinterpret_cast<float*>(raw0 + (c % g.ns) * stage_bytes + g.a_raw);
+      const int64_t k0 = kb + int64_t(c) * kGemmKC;
+      fetch(ra, g.a, m0, kGemmM, g.M, k0, ke);
+      fetch(rb, bo, 0, g.npad, nvalid, k0, ke);
+    }
+    cp_async_commit();
+  };
+  for (int c = 0; c < g.ns - 1; ++c) issue(c);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t idesc = idesc_tf32(kGemmM, g.npad);
+
+  for (int c = 0; c < nch; ++c) {
+    issue(c + g.ns - 1);
+    // chunk c's copies (this thread's) have landed: at most ns - 1 newer groups pending
+    if (g.ns >= 3) cp_async_wait<2>();
+    else cp_async_wait<1>();
+    const int ts = g.nt == 2 ? (c & 1) : 0;
+    uint8_t* set = smem + ts * set_bytes;
+    uint8_t *ah = set, *al = set + g.a_tile, *bh = set + 2 * g.a_tile, *bl = set + 2 * g.a_tile + g.b_tile;
+    // the MMAs that last read this tile set (chunk c - nt) are done
+    if (c >= g.nt) mbar_wait(bar + ts, uint32_t((c - g.nt) / g.nt) & 1u);
+    __syncthreads();  // every thread's copies of chunk c are visible
+    const uint8_t* stg = raw0 + (c % g.ns) * stage_bytes;
+    convert(reinterpret_cast<const float*>(stg), g.a.kind, kGemmM, ah, al);
+    convert(reinterpret_cast<const float*>(stg + g.a_raw), g.b.kind, g.npad, bh, bl);
+    fence_proxy_async_smem();
+    __syncthreads();  // tiles complete; the raw stage may be refilled
+    if (threadIdx.x == 0) {
+      tc_fence_after();
+#pragma unroll
+      for (int kk = 0; kk < kGemmKC; kk += 8) {
+        const uint32_t acc0 = (c > 0 || kk > 0) ? 1u : 0u;
+        umma_tf32(tmem, desc4(ah, kk), desc4(bh, kk), idesc, acc0);
+        umma_tf32(tmem, desc4(ah, kk), desc4(bl, kk), idesc, 1u);
+        umma_tf32(tmem, desc4(al, kk), desc4(bh, kk), idesc, 1u);
+      }
+      umma_commit(bar + ts);
+    }
+  }
+  cp_async_wait<0>();
+  if (nch > 0) {
+    const int last = nch - 1, ts = g.nt == 2 ? (last & 1) : 0;
+    mbar_wait(bar + ts, uint32_t(last / g.nt) & 1u);
+  }
+  tc_fence_after();
+
+  // epilogue: thread r holds accumulator row r (TMEM lane r); each warp
+  // stages its 32 rows x 32 columns through shared memory (the raw stages are
+  // free now) and writes them back one row (128 B) per instruction
+  __syncthreads();
+  float* stg = reinterpret_cast<float*>(raw0) + warp * 32 * kEpiPitch;
+  const int lane = threadIdx.x & 31;
+  const uint32_t lane_base = uint32_t(warp * 32) << 16;
+  for (int c0 = 0; c0 < g.npad; c0 += 32) {
+    float v[32];
+    if (nch > 0) {
+      tmem_ld32(tmem + lane_base + uint32_t(c0), v);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] = 0.0f;
+    }
+#pragma unroll
+    for (int j = 0; j < 32; ++j) stg[lane * kEpiPitch + j] = v[j];
+    __syncwarp();
+    const int col = c0 + lane;
+    if (col < nvalid) {
+      for (int rr = 0; rr < 32; ++rr) {
+        const int64_t m = m0 + warp * 32 + rr;
+        if (m >= g.M) break;
+        const float x = stg[rr * kEpiPitch + lane];
+        if (g.split > 1) {
+          g.part[(int64_t(sp) * g.M + m) * g.N + n0 + col] = x;
+        } else {
+          float* d = g.C + m * g.ldc + n0 + col;
+          *d = g.beta != 0.0f ? *d + x : x;
+        }
+      }
+    }
+    __syncwarp();
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(g.tmem_cols) : "memory");
+}
+
+// C = beta C + sum over splits of the partial tiles, in split order
+__global__ void gemm_fold_kernel(const float* __restrict__ part, int split, int64_t M, int N, float* C, int64_t ldc,
+                                 float beta) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= M * N) return;
+  const int64_t m = i / N;
+  const int n = int(i - m * N);
+  float s = 0.0f;
+  for (int q = 0; q < split; ++q) s += part[int64_t(q) * M * N + i];
+  float* d = C + m * ldc + n;
+  *d = beta != 0.0f ? *d + s : s;
+}
+
+// g[o] = beta g[o] + sum_k D[k][o]: fixed-order partial sums over row blocks, then a fold
+constexpr int kColRows = 512;
+__global__ void colsum_part_kernel(const float* __restrict__ D, int64_t ldd, int O, int64_t K, float* __restrict__ part) {
+  const int o = blockIdx.y * blockDim.x + threadIdx.x;
+  if (o >= O) return;
+  const int64_t k0 = int64_t(blockIdx.x) * kColRows, k1 = min(K, k0 + kColRows);
+  float s = 0.0f;
+  for (int64_t k = k0; k < k1; ++k) s += __ldg(D + k * ldd + o);
+  part[int64_t(blockIdx.x) * O + o] = s;
+}
+__global__ void colsum_fold_kernel(const float* __restrict__ part, int nparts, int O, float* g, float beta) {
+  const int o = blockIdx.x * blockDim.x + threadIdx.x;
+  if (o >= O) return;
+  float s = 0.0f;
+  for (int q = 0; q < nparts; ++q) s += part[int64_t(q) * O + o];
+  g[o] = beta != 0.0f ? g[o] + s : s;
+}
+
+// split-K / column-sum partials: one scratch buffer per stream (grown on
+// demand; the stream's earlier kernels are drained before a buffer is freed)
+float* scratch(size_t floats, cudaStream_t st, cudaError_t* err) {
+  struct Buf {
+    float* p = nullptr;
+    size_t n = 0;
+  };
+  static std::map<cudaStream_t, Buf> bufs;
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lk(mu);
+  Buf& x = bufs[st];
+  if (x.n < floats) {
+    if (x.p) {
+      if ((*err = cudaStreamSynchronize(st)) != cudaSuccess) return nullptr;
+      cudaFree(x.p);
+      x.p = nullptr;
+      x.n = 0;
+    }
+    if ((*err = cudaMalloc(&x.p, floats * sizeof(float))) != cudaSuccess) {
+      x.p = nullptr;
+      return nullptr;
+    }
+    x.n = floats;
+  }
+  return x.p;
+}
+
+int sm_count() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return sms;
+}
+
+uint32_t pow2_cols(int n) {
+  uint32_t c = 32;
+  while (c < uint32_t(n)) c <<= 1;
+  return c;
+}
+
+OpLayout op_layout(const float* X, int64_t sr, int64_t sk, int rows_per_tile) {
+  OpLayout o{X, sr, sk, 2, 1};
+  const uintptr_t base = reinterpret_cast<uintptr_t>(X);
+  auto widest = [&](int64_t stride) {  // floats per copy keeping every copy aligned
+    for (int v : {4, 2}) {
+      if (stride % v == 0 && base % (4 * v) == 0) return v;
+    }
+    return 1;
+  };
+  if (sk == 1) {
+    o.kind = 0;
+    o.vec = widest(sr);
+  } else if (sr == 1) {
+    o.kind = 1;
+    o.vec = widest(sk);
+    while (o.vec > 1 && rows_per_tile % o.vec) o.vec >>= 1;
+  }
+  return o;
+}
+
+}  // namespace
+
+// C[M x N] = beta C + A . B'^T on the tensor cores (see the file comment).
+cudaError_t tc_gemm(cudaStream_t st, int64_t M, int N, int64_t K, const float* A, int64_t sam, int64_t sak,
+                    const float* B, int64_t sbn, int64_t sbk, float* C, int64_t ldc, float beta) {
+  if (M <= 0 || N <= 0) return cudaSuccess;
+  GemmArgs g{};
+  g.C = C;
+  g.M = M;
+  g.K = K;
+  g.ldc = ldc;
+  g.N = N;
+  g.beta = beta;
+  const int ntiles = (N + kGemmMaxN - 1) / kGemmMaxN;
+  g.ntile = ((N + ntiles - 1) / ntiles + 15) / 16 * 16;  // balanced N tiles, multiples of 16
+  g.npad = g.ntile;
+  g.tmem_cols = pow2_cols(g.npad);
+  g.a = op_layout(A, sam, sak, kGemmM);
+  g.b = op_layout(B, sbn, sbk, g.npad);
+  if (g.b.kind == 1 && ntiles > 1) {  // every N tile's base must keep the copy alignment
+    while (g.b.vec > 1 && (g.ntile % g.b.vec)) g.b.vec >>= 1;
+  }
+  g.a_raw = raw_bytes(kGemmM, g.a.kind);
+  g.b_raw = raw_bytes(g.npad, g.b.kind);
+  g.a_tile = kGemmM * kGemmKC * 4;
+  g.b_tile = uint32_t(g.npad) * kGemmKC * 4;
+  // as many raw stages (latency hiding) and tile sets (split / MMA overlap) as fit
+  g.ns = 3;
+  g.nt = 2;
+  auto bytes = [&] {  // the epilogue staging (4 warps x 32 x kEpiPitch floats) reuses the raw stages
+    const uint32_t raw = std::max<uint32_t>(g.ns * (g.a_raw + g.b_raw), 4 * 32 * kEpiPitch * 4);
+    return g.nt * (2 * g.a_tile + 2 * g.b_tile) + raw + 64;
+  };
+  while (bytes() > kGemmSmemMax && g.ns > 2) --g.ns;
+  if (bytes() > kGemmSmemMax) g.nt = 1;
+  while (bytes() > kGemmSmemMax && g.ns > 2) --g.ns;
+  const size_t smem = bytes();
+  const int64_t mtiles = (M + kGemmM - 1) / kGemmM;
+  // split K when the M x N tiles alone leave SMs idle and K is long
+  int split = 1;
+  const int64_t tiles = mtiles * ntiles;
+  if (tiles < sm_count() && K > 4 * kGemmKC) {
+    split = int(std::min<int64_t>(std::max<int64_t>(1, sm_count() / tiles), (K + 4 * kGemmKC - 1) / (4 * kGemmKC)));
+    split = std::max(1, std::min(split, 1024));
+  }
+  g.kchunk = std::max<int64_t>(kGemmKC, ((K + split - 1) / split + kGemmKC - 1) / kGemmKC * kGemmKC);
+  split = int(std::max<int64_t>(1, (K + g.kchunk - 1) / g.kchunk));
+  g.split = split;
+  if (split > 1) {
+    cudaError_t e = cudaSuccess;
+    g.part = scratch(size_t(split) * size_t(M) * size_t(N), st, &e);
+    if (!g.part) return e;
+  }
+  cudaFuncSetAttribute(gemm_tf32x3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  gemm_tf32x3_kernel<<<dim3(unsigned(mtiles), unsigned(ntiles), unsigned(split)), kGemmThreads, smem, st>>>(g);
+  ++g_launches;
+  if (split > 1) {
+    const int64_t total = M * N;
+    gemm_fold_kernel<<<unsigned((total + 255) / 256), 256, 0, st>>>(g.part, split, M, N, C, ldc, beta);
+    ++g_launches;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t tc_colsum(cudaStream_t st, int O, int64_t K, const float* D, int64_t ldd, float* g, float beta) {
+  if (O <= 0) return cudaSuccess;
+  const int nparts = int(std::max<int64_t>(1, (K + kColRows - 1) / kColRows));
+  cudaError_t e = cudaSuccess;
+  float* part = scratch(size_t(nparts) * size_t(O), st, &e);
+  if (!part) return e;
+  const int tx = std::min(128, (O + 31) / 32 * 32);
+  colsum_part_kernel<<<dim3(unsigned(nparts), unsigned((O + tx - 1) / tx)), tx, 0, st>>>(D, ldd, O, K, part);
+  colsum_fold_kernel<<<unsigned((O + 127) / 128), 128, 0, st>>>(part, nparts, O, g, beta);
+  g_launches += 2;
+  return cudaGetLastError();
+}
+
+}  // namespace marl_b200

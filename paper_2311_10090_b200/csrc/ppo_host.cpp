@@ -205,68 +205,25 @@ const Nccl& nccl() {
   return n;
 }
 
-// cuBLAS SGEMM / SGEMV for the recurrent update's per-step GEMMs (plain
-// library GEMMs), loaded at run time like NCCL (torch's copy when loaded).
-struct Blas {
-  void* lib = nullptr;
-  void* handle = nullptr;
-  int (*create)(void**) = nullptr;
-  int (*set_stream)(void*, cudaStream_t) = nullptr;
-  int (*sgemm)(void*, int, int, int, int, int, const float*, const float*, int, const float*, int, const float*,
-               float*, int) = nullptr;
-  int (*sgemv)(void*, int, int, int, const float*, const float*, int, const float*, int, const float*, float*,
-               int) = nullptr;
-};
-
-Blas& blas(cudaStream_t st) {
-  static Blas b = [] {
-    Blas x;
-    for (const char* name : {"libcublas.so.12", "libcublas.so"}) {
-      x.lib = dlopen(name, RTLD_NOW | RTLD_GLOBAL);
-      if (x.lib) break;
-    }
-    if (!x.lib) return x;
-    x.create = reinterpret_cast<decltype(x.create)>(dlsym(x.lib, "cublasCreate_v2"));
-    x.set_stream = reinterpret_cast<decltype(x.set_stream)>(dlsym(x.lib, "cublasSetStream_v2"));
-    x.sgemm = reinterpret_cast<decltype(x.sgemm)>(dlsym(x.lib, "cublasSgemm_v2"));
-    x.sgemv = reinterpret_cast<decltype(x.sgemv)>(dlsym(x.lib, "cublasSgemv_v2"));
-    if (x.create && x.create(&x.handle) != 0) x.handle = nullptr;
-    return x;
-  }();
-  if (!b.handle || !b.sgemm || !b.sgemv || !b.set_stream)
-    raise(MARL_ERR_CUDA, "cuBLAS (libcublas.so.12) is not loadable in this process");
-  b.set_stream(b.handle, st);
-  return b;
-}
-constexpr int kOpN = 0, kOpT = 1;
-
-// Row-major GEMMs on column-major cuBLAS.
-// C[M x N] = A[M x K] . B[N x K]^T (+ beta C)
+// The recurrent path's GEMMs: fp32-accurate 3xTF32 tcgen05 kernels (gemm_tc.cu).
+// Row-major C[M x N] = A[M x K] . B[N x K]^T (+ beta C)
 void gemm_nt(cudaStream_t st, int64_t M, int N, int K, const float* A, int lda, const float* B, int ldb, float* C,
              int ldc, float beta) {
-  const float one = 1.0f;
-  if (blas(st).sgemm(blas(st).handle, kOpT, kOpN, N, int(M), K, &one, B, ldb, A, lda, &beta, C, ldc) != 0)
-    raise(MARL_ERR_CUDA, "cublasSgemm failed");
+  cuda_check(tc_gemm(st, M, N, K, A, lda, 1, B, ldb, 1, C, ldc, beta), "tc_gemm");
 }
 // C[M x N] = A[M x K] . B[K x N] (+ beta C)
 void gemm_nn(cudaStream_t st, int64_t M, int N, int K, const float* A, int lda, const float* B, int ldb, float* C,
              int ldc, float beta) {
-  const float one = 1.0f;
-  if (blas(st).sgemm(blas(st).handle, kOpN, kOpN, N, int(M), K, &one, B, ldb, A, lda, &beta, C, ldc) != 0)
-    raise(MARL_ERR_CUDA, "cublasSgemm failed");
+  cuda_check(tc_gemm(st, M, N, K, A, lda, 1, B, 1, ldb, C, ldc, beta), "tc_gemm");
 }
 // G[O x I] = D[K x O]^T . X[K x I] (+ beta G): matmul_tn summed over all rows
 void gemm_tn(cudaStream_t st, int O, int I, int64_t K, const float* D, int ldd, const float* X, int ldx, float* G,
              float beta) {
-  const float one = 1.0f;
-  if (blas(st).sgemm(blas(st).handle, kOpN, kOpT, I, O, int(K), &one, X, ldx, D, ldd, &beta, G, I) != 0)
-    raise(MARL_ERR_CUDA, "cublasSgemm failed");
+  cuda_check(tc_gemm(st, O, I, K, D, 1, ldd, X, 1, ldx, G, I, beta), "tc_gemm");
 }
-// g[O] = sum_k D[k][o] (+ beta g): the bias gradients
-void colsum(cudaStream_t st, int O, int64_t K, const float* D, int ldd, const float* ones, float* g, float beta) {
-  const float one = 1.0f;
-  if (blas(st).sgemv(blas(st).handle, kOpN, O, int(K), &one, D, ldd, ones, 1, &beta, g, 1) != 0)
-    raise(MARL_ERR_CUDA, "cublasSgemv failed");
+// g[O] = sum_k D[k][o] (+ beta g): the bias gradients (fixed-order reduction)
+void colsum(cudaStream_t st, int O, int64_t K, const float* D, int ldd, const float* /*ones*/, float* g, float beta) {
+  cuda_check(tc_colsum(st, O, K, D, ldd, g, beta), "tc_colsum");
 }
 
 // the native hook: an in-place NCCL sum on the trainer's stream (no host sync)

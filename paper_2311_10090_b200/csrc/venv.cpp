@@ -592,6 +592,15 @@ int marl_set_grid_cap(int ctas) {
 }
 const char* marl_version(void) { return "marl-b200 0.1 (sm_100a)"; }
 
+int marl_gemm_f32(int64_t M, int N, int64_t K, const float* A, int64_t sam, int64_t sak, const float* B, int64_t sbn,
+                  int64_t sbk, float* C, int64_t ldc, float beta, void* stream) {
+  return guarded([&] {
+    if ((M > 0 && N > 0) && (!A || !B || !C)) raise(MARL_ERR_CONTRACT, "marl_gemm_f32: NULL operand");
+    if (M < 0 || N < 0 || K < 0 || N > 65535) raise(MARL_ERR_CONTRACT, "marl_gemm_f32: bad shape");
+    cuda_check(tc_gemm(static_cast<cudaStream_t>(stream), M, N, K, A, sam, sak, B, sbn, sbk, C, ldc, beta), "tc_gemm");
+  });
+}
+
 int marl_registered_count(void) { return int(registered().size()); }
 const char* marl_registered_env(int i) {
   return (i >= 0 && i < int(registered().size())) ? registered()[size_t(i)].c_str() : nullptr;
