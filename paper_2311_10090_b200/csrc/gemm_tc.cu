@@ -42,18 +42,22 @@ namespace marl_b200 {
 namespace {
 
 constexpr int kGemmM = 128;        // rows per CTA (UMMA M)
-constexpr int kGemmKC = 16;        // K elements per chunk (two MMA K steps of 8)
 constexpr int kGemmMaxN = 128;     // columns per CTA (UMMA N <= 256; 128 keeps three CTAs per SM)
 constexpr int kGemmThreads = 128;  // one TMEM lane (accumulator row) per thread
-constexpr int kRawPitch = kGemmKC + 4;  // raw K-contiguous rows, padded against bank conflicts
-constexpr uint32_t kGemmSmemMax = 227 * 1024 / 3 - 1024;  // three CTAs (three tiles in flight) per SM
+// Two configurations (K elements per chunk KC, CTAs per SM): grids of M x N
+// tiles run KC = 16 with three CTAs per SM; split-K grids (the weight
+// gradients, a few tiles over a very long K) run KC = 32 with one CTA per SM
+// and a deeper raw ring (four stages, two tile sets).
+template <int KC>
+__host__ __device__ constexpr int raw_pitch() { return KC + 4; }  // raw K-contiguous rows, padded against bank conflicts
 constexpr int kEpiPitch = 33;  // epilogue staging rows (32 columns + 1 against bank conflicts)
 
 // byte offset of element (r, k) in a K-major no-swizzle canonical [rows x kKC]
 // 4-byte tile: 8-row x 16-byte core matrices, K neighbours 128 B apart, 8-row
 // groups (kKC/4)*128 B apart
+template <int KC>
 __host__ __device__ __forceinline__ uint32_t canon4(int r, int k) {
-  return uint32_t((r >> 3) * ((kGemmKC / 4) * 128) + (k >> 2) * 128 + (r & 7) * 16 + (k & 3) * 4);
+  return uint32_t((r >> 3) * ((KC / 4) * 128) + (k >> 2) * 128 + (r & 7) * 16 + (k & 3) * 4);
 }
 
 // kind::tf32 instruction descriptor: tf32 A/B (format 2), fp32 D, K-major, M x N
@@ -70,8 +74,9 @@ __device__ __forceinline__ void umma_tf32(uint32_t d_tmem, uint64_t a, uint64_t 
 }
 
 // K-major operand descriptor of a canonical [rows x kKC] tile, K step k0 (multiple of 8)
+template <int KC>
 __device__ __forceinline__ uint64_t desc4(const void* tile, int k0) {
-  return desc_raw(smem_u32(tile) + uint32_t(k0 >> 2) * 128u, 128u, (kGemmKC / 4) * 128u);
+  return desc_raw(smem_u32(tile) + uint32_t(k0 >> 2) * 128u, 128u, (KC / 4) * 128u);
 }
 
 // cp.async of SZ bytes (4, 8 or 16), zero-filled beyond src_bytes
@@ -92,12 +97,12 @@ __device__ __forceinline__ void cp_async_wait() {
 }
 
 // How an operand X(r, k) = X[r*sr + k*sk] is staged: K-contiguous (raw rows
-// [r][kRawPitch]) with copies of `vec` floats, or rows-contiguous (raw
+// [r][KC + 4]) with copies of `vec` floats, or rows-contiguous (raw
 // [k][rows]) with copies of `vec` floats along r, or element by element.
 struct OpLayout {
   const float* X;
   int64_t sr, sk;
-  int kind;  // 0: K-contiguous, 1: rows-contiguous, 2: general (raw [r][kRawPitch])
+  int kind;  // 0: K-contiguous, 1: rows-contiguous, 2: general (raw [r][KC + 4])
   int vec;   // floats per copy (1, 2, 4)
 };
 
@@ -109,25 +114,25 @@ struct GemmArgs {
   int N, npad;     // columns; npad: MMA N of a tile (multiple of 16)
   int ntile;       // columns per N tile
   int split;       // K splits
-  int64_t kchunk;  // K elements per split (multiple of kGemmKC)
+  int64_t kchunk;  // K elements per split (multiple of the chunk KC)
   float beta;
   uint32_t tmem_cols;
   int ns, nt;      // raw stages, hi/lo tile sets
   uint32_t a_raw, b_raw, a_tile, b_tile;  // bytes
 };
 
-__host__ __device__ inline uint32_t raw_bytes(int rows, int kind) {
-  return kind == 1 ? uint32_t(kGemmKC) * rows * 4 : uint32_t(rows) * kRawPitch * 4;
+__host__ __device__ inline uint32_t raw_bytes(int rows, int kind, int KC) {
+  return kind == 1 ? uint32_t(KC) * rows * 4 : uint32_t(rows) * (KC + 4) * 4;
 }
 
 // Issue the cp.async copies of chunk [k0, k0 + KC) of rows [r0, r0 + rows)
 // (valid rows < rvalid, valid k < K) into a raw stage.
-template <int V>
+template <int KC, int V>
 __device__ __forceinline__ void fetch_v(float* raw, const OpLayout& o, int64_t r0, int rows, int64_t rvalid, int64_t k0,
                                         int64_t K) {
   if (o.kind == 1) {  // raw[k][r], copies along r
     const int per_k = rows / V;
-    for (int idx = threadIdx.x; idx < per_k * kGemmKC; idx += kGemmThreads) {
+    for (int idx = threadIdx.x; idx < per_k * KC; idx += kGemmThreads) {
       const int k = idx / per_k, r = (idx - k * per_k) * V;
       const int64_t gk = k0 + k, gr = r0 + r;
       int64_t nv = gk < K ? rvalid - gr : 0;
@@ -136,22 +141,23 @@ __device__ __forceinline__ void fetch_v(float* raw, const OpLayout& o, int64_t r
       cp_async<4 * V>(raw + k * rows + r, src, uint32_t(nv * 4));
     }
   } else {  // raw[r][k], copies along k (kind 0) or single elements (kind 2, V = 1)
-    const int per_r = kGemmKC / V;
+    const int per_r = KC / V;
     for (int idx = threadIdx.x; idx < rows * per_r; idx += kGemmThreads) {
       const int r = idx / per_r, k = (idx - r * per_r) * V;
       const int64_t gk = k0 + k, gr = r0 + r;
       int64_t nv = gr < rvalid ? K - gk : 0;
       nv = nv < 0 ? 0 : nv > V ? V : nv;
       const float* src = nv ? o.X + gr * o.sr + gk * o.sk : o.X;
-      cp_async<4 * V>(raw + r * kRawPitch + k, src, uint32_t(nv * 4));
+      cp_async<4 * V>(raw + r * raw_pitch<KC>() + k, src, uint32_t(nv * 4));
     }
   }
 }
+template <int KC>
 __device__ __forceinline__ void fetch(float* raw, const OpLayout& o, int64_t r0, int rows, int64_t rvalid, int64_t k0,
                                       int64_t K) {
-  if (o.vec == 4) fetch_v<4>(raw, o, r0, rows, rvalid, k0, K);
-  else if (o.vec == 2) fetch_v<2>(raw, o, r0, rows, rvalid, k0, K);
-  else fetch_v<1>(raw, o, r0, rows, rvalid, k0, K);
+  if (o.vec == 4) fetch_v<KC, 4>(raw, o, r0, rows, rvalid, k0, K);
+  else if (o.vec == 2) fetch_v<KC, 2>(raw, o, r0, rows, rvalid, k0, K);
+  else fetch_v<KC, 1>(raw, o, r0, rows, rvalid, k0, K);
 }
 
 // hi / lo tf32 images of v: hi = v with the low 13 mantissa bits cleared
@@ -162,8 +168,9 @@ __device__ __forceinline__ void split_tf32(float v, float& hi, float& lo) {
 }
 
 // raw stage -> hi / lo canonical tiles (four K per thread step)
+template <int KC>
 __device__ __forceinline__ void convert(const float* raw, int kind, int rows, uint8_t* hi, uint8_t* lo) {
-  for (int idx = threadIdx.x; idx < rows * (kGemmKC / 4); idx += kGemmThreads) {
+  for (int idx = threadIdx.x; idx < rows * (KC / 4); idx += kGemmThreads) {
     int r, k;
     float4 v;
     if (kind == 1) {  // raw[k][r]: consecutive threads take consecutive rows
@@ -173,26 +180,27 @@ __device__ __forceinline__ void convert(const float* raw, int kind, int rows, ui
     } else {
       r = idx % rows;
       k = (idx / rows) * 4;
-      v = *reinterpret_cast<const float4*>(raw + r * kRawPitch + k);
+      v = *reinterpret_cast<const float4*>(raw + r * raw_pitch<KC>() + k);
     }
     float4 h, l;
     split_tf32(v.x, h.x, l.x);
     split_tf32(v.y, h.y, l.y);
     split_tf32(v.z, h.z, l.z);
     split_tf32(v.w, h.w, l.w);
-    *reinterpret_cast<float4*>(hi + canon4(r, k)) = h;
-    *reinterpret_cast<float4*>(lo + canon4(r, k)) = l;
+    *reinterpret_cast<float4*>(hi + canon4<KC>(r, k)) = h;
+    *reinterpret_cast<float4*>(lo + canon4<KC>(r, k)) = l;
   }
 }
 
-__global__ void __launch_bounds__(kGemmThreads, 3) gemm_tf32x3_kernel(GemmArgs g) {
+template <int KC, int MINB>
+__global__ void __launch_bounds__(kGemmThreads, MINB) gemm_tf32x3_kernel(GemmArgs g) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const int mt = blockIdx.x, nt = blockIdx.y, sp = blockIdx.z;
   const int64_t m0 = int64_t(mt) * kGemmM;
   const int n0 = nt * g.ntile;
   const int nvalid = min(g.ntile, g.N - n0);
   const int64_t kb = int64_t(sp) * g.kchunk, ke = min(g.K, kb + g.kchunk);
-  const int nch = int((ke - kb + kGemmKC - 1) / kGemmKC);
+  const int nch = int((ke - kb + KC - 1) / KC);
   // smem: [tile sets: A hi, A lo, B hi, B lo] x nt, [raw stages: A, B] x ns, 2 barriers, TMEM slot
   const uint32_t set_bytes = 2 * g.a_tile + 2 * g.b_tile, stage_bytes = g.a_raw + g.b_raw;
   uint8_t* raw0 = smem + g.nt * set_bytes;
@@ -215,9 +223,9 @@ __global__ void __launch_bounds__(kGemmThreads, 3) gemm_tf32x3_kernel(GemmArgs g
     if (c < nch) {
       float* ra = reinterpret_cast<float*>(raw0 + (c % g.ns) * stage_bytes);
       float* rb = reinterpret_cast<float*>(raw0 + (c % g.ns) * stage_bytes + g.a_raw);
-      const int64_t k0 = kb + int64_t(c) * kGemmKC;
-      fetch(ra, g.a, m0, kGemmM, g.M, k0, ke);
-      fetch(rb, bo, 0, g.npad, nvalid, k0, ke);
+      const int64_t k0 = kb + int64_t(c) * KC;
+      fetch<KC>(ra, g.a, m0, kGemmM, g.M, k0, ke);
+      fetch<KC>(rb, bo, 0, g.npad, nvalid, k0, ke);
     }
     cp_async_commit();
   };
@@ -231,7 +239,8 @@ __global__ void __launch_bounds__(kGemmThreads, 3) gemm_tf32x3_kernel(GemmArgs g
   for (int c = 0; c < nch; ++c) {
     issue(c + g.ns - 1);
     // chunk c's copies (this thread's) have landed: at most ns - 1 newer groups pending
-    if (g.ns >= 3) cp_async_wait<2>();
+    if (g.ns >= 4) cp_async_wait<3>();
+    else if (g.ns == 3) cp_async_wait<2>();
     else cp_async_wait<1>();
     const int ts = g.nt == 2 ? (c & 1) : 0;
     uint8_t* set = smem + ts * set_bytes;
@@ -240,18 +249,18 @@ __global__ void __launch_bounds__(kGemmThreads, 3) gemm_tf32x3_kernel(GemmArgs g
     if (c >= g.nt) mbar_wait(bar + ts, uint32_t((c - g.nt) / g.nt) & 1u);
     __syncthreads();  // every thread's copies of chunk c are visible
     const uint8_t* stg = raw0 + (c % g.ns) * stage_bytes;
-    convert(reinterpret_cast<const float*>(stg), g.a.kind, kGemmM, ah, al);
-    convert(reinterpret_cast<const float*>(stg + g.a_raw), g.b.kind, g.npad, bh, bl);
+    convert<KC>(reinterpret_cast<const float*>(stg), g.a.kind, kGemmM, ah, al);
+    convert<KC>(reinterpret_cast<const float*>(stg + g.a_raw), g.b.kind, g.npad, bh, bl);
     fence_proxy_async_smem();
     __syncthreads();  // tiles complete; the raw stage may be refilled
     if (threadIdx.x == 0) {
       tc_fence_after();
 #pragma unroll
-      for (int kk = 0; kk < kGemmKC; kk += 8) {
+      for (int kk = 0; kk < KC; kk += 8) {
         const uint32_t acc0 = (c > 0 || kk > 0) ? 1u : 0u;
-        umma_tf32(tmem, desc4(ah, kk), desc4(bh, kk), idesc, acc0);
-        umma_tf32(tmem, desc4(ah, kk), desc4(bl, kk), idesc, 1u);
-        umma_tf32(tmem, desc4(al, kk), desc4(bh, kk), idesc, 1u);
+        umma_tf32(tmem, desc4<KC>(ah, kk), desc4<KC>(bh, kk), idesc, acc0);
+        umma_tf32(tmem, desc4<KC>(ah, kk), desc4<KC>(bl, kk), idesc, 1u);
+        umma_tf32(tmem, desc4<KC>(al, kk), desc4<KC>(bh, kk), idesc, 1u);
       }
       umma_commit(bar + ts);
     }
@@ -410,7 +419,11 @@ cudaError_t tc_gemm(cudaStream_t st, int64_t M, int N, int64_t K, const float* A
   g.ldc = ldc;
   g.N = N;
   g.beta = beta;
-  const int ntiles = (N + kGemmMaxN - 1) / kGemmMaxN;
+  // N tiles of up to 128 columns; a grid of fewer than two M x N tiles per SM
+  // takes 64-column tiles instead (twice the CTAs in flight)
+  const int64_t mt0 = (M + kGemmM - 1) / kGemmM;
+  const int maxn = (mt0 * ((N + kGemmMaxN - 1) / kGemmMaxN) < 2 * int64_t(sm_count()) && N > 64) ? 64 : kGemmMaxN;
+  const int ntiles = (N + maxn - 1) / maxn;
   g.ntile = ((N + ntiles - 1) / ntiles + 15) / 16 * 16;  // balanced N tiles, multiples of 16
   g.npad = g.ntile;
   g.tmem_cols = pow2_cols(g.npad);
@@ -419,30 +432,36 @@ cudaError_t tc_gemm(cudaStream_t st, int64_t M, int N, int64_t K, const float* A
   if (g.b.kind == 1 && ntiles > 1) {  // every N tile's base must keep the copy alignment
     while (g.b.vec > 1 && (g.ntile % g.b.vec)) g.b.vec >>= 1;
   }
-  g.a_raw = raw_bytes(kGemmM, g.a.kind);
-  g.b_raw = raw_bytes(g.npad, g.b.kind);
-  g.a_tile = kGemmM * kGemmKC * 4;
-  g.b_tile = uint32_t(g.npad) * kGemmKC * 4;
+  const int64_t mtiles = (M + kGemmM - 1) / kGemmM;
+  // split K when the M x N tiles alone leave SMs idle and K is long
+  int split = 1;
+  const int64_t tiles = mtiles * ntiles;
+  if (tiles < sm_count() && K > 128) {
+    split = int(std::min<int64_t>(std::max<int64_t>(1, sm_count() / tiles), (K + 127) / 128));
+    split = std::max(1, std::min(split, 1024));
+  }
+  // split-K grids (few tiles over a long K: the weight gradients) take the deep
+  // configuration; everything else keeps three CTAs per SM (measured: the deep
+  // ring on a 1.3-wave grid of 192 tiles is 1.7x slower than three CTAs per SM)
+  const bool deep = split > 1;
+  const int KC = deep ? 32 : 16;
+  const uint32_t budget = deep ? 227 * 1024 - 1024 : 227 * 1024 / 3 - 1024;
+  g.a_raw = raw_bytes(kGemmM, g.a.kind, KC);
+  g.b_raw = raw_bytes(g.npad, g.b.kind, KC);
+  g.a_tile = kGemmM * KC * 4;
+  g.b_tile = uint32_t(g.npad) * KC * 4;
   // as many raw stages (latency hiding) and tile sets (split / MMA overlap) as fit
-  g.ns = 3;
+  g.ns = deep ? 4 : 3;
   g.nt = 2;
   auto bytes = [&] {  // the epilogue staging (4 warps x 32 x kEpiPitch floats) reuses the raw stages
     const uint32_t raw = std::max<uint32_t>(g.ns * (g.a_raw + g.b_raw), 4 * 32 * kEpiPitch * 4);
     return g.nt * (2 * g.a_tile + 2 * g.b_tile) + raw + 64;
   };
-  while (bytes() > kGemmSmemMax && g.ns > 2) --g.ns;
-  if (bytes() > kGemmSmemMax) g.nt = 1;
-  while (bytes() > kGemmSmemMax && g.ns > 2) --g.ns;
+  while (bytes() > budget && g.ns > 2) --g.ns;
+  if (bytes() > budget) g.nt = 1;
+  while (bytes() > budget && g.ns > 2) --g.ns;
   const size_t smem = bytes();
-  const int64_t mtiles = (M + kGemmM - 1) / kGemmM;
-  // split K when the M x N tiles alone leave SMs idle and K is long
-  int split = 1;
-  const int64_t tiles = mtiles * ntiles;
-  if (tiles < sm_count() && K > 4 * kGemmKC) {
-    split = int(std::min<int64_t>(std::max<int64_t>(1, sm_count() / tiles), (K + 4 * kGemmKC - 1) / (4 * kGemmKC)));
-    split = std::max(1, std::min(split, 1024));
-  }
-  g.kchunk = std::max<int64_t>(kGemmKC, ((K + split - 1) / split + kGemmKC - 1) / kGemmKC * kGemmKC);
+  g.kchunk = std::max<int64_t>(KC, ((K + split - 1) / split + KC - 1) / KC * KC);
   split = int(std::max<int64_t>(1, (K + g.kchunk - 1) / g.kchunk));
   g.split = split;
   if (split > 1) {
@@ -450,8 +469,9 @@ cudaError_t tc_gemm(cudaStream_t st, int64_t M, int N, int64_t K, const float* A
     g.part = scratch(size_t(split) * size_t(M) * size_t(N), st, &e);
     if (!g.part) return e;
   }
-  cudaFuncSetAttribute(gemm_tf32x3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-  gemm_tf32x3_kernel<<<dim3(unsigned(mtiles), unsigned(ntiles), unsigned(split)), kGemmThreads, smem, st>>>(g);
+  auto kern = deep ? gemm_tf32x3_kernel<32, 1> : gemm_tf32x3_kernel<16, 3>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  kern<<<dim3(unsigned(mtiles), unsigned(ntiles), unsigned(split)), kGemmThreads, smem, st>>>(g);
   ++g_launches;
   if (split > 1) {
     const int64_t total = M * N;
