@@ -8,6 +8,8 @@ timeout 900 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu_${TAG}.log 
 for w in smax3m mpe mpe_large overcooked smax2s3z smax27m ippo; do
   timeout 600 python bench.py --workload $w --steps 30 --warmup 5 2>/dev/null | grep '^{' >> gpurun_out/bench_${TAG}.jsonl
 done
+timeout 600 python bench.py --workload smax27m --n-envs 16384 --steps 10 --warmup 3 2>/dev/null | grep '^{' >> gpurun_out/bench_${TAG}.jsonl
+timeout 600 python bench.py --workload mpe --per-step --steps 30 --warmup 5 --no-cpu 2>/dev/null | grep '^{' >> gpurun_out/bench_${TAG}.jsonl
 timeout 600 python bench.py --workload ppo --steps 10 --warmup 3 2>/dev/null | grep '^{' >> gpurun_out/bench_${TAG}.jsonl
 timeout 600 python bench.py --workload ppo_rnn --steps 3 --warmup 3 2>/dev/null | grep '^{' >> gpurun_out/bench_${TAG}.jsonl
 timeout 600 python bench.py --workload ppo_smax --steps 10 --warmup 3 2>/dev/null | grep '^{' >> gpurun_out/bench_${TAG}.jsonl
@@ -38,6 +40,10 @@ timeout 900 $NCU --set full --clock-control none --import-source on -k regex:ppo
   -o gpurun_out/prof_${TAG}_ppo_update -f python bench.py --workload ppo --steps 1 --warmup 3 --no-cpu --no-e2e \
   > /dev/null 2>&1
 # summarise the step-kernel captures here and keep only what fits gpurun's 64 MiB return
+timeout 600 /usr/local/cuda/bin/ncu --set full --clock-control none --import-source on -k regex:probe_kernel -s 5 -c 1 \
+  -o gpurun_out/prof_${TAG}_mpeprobe -f python bench.py --workload mpe --steps 1000 --warmup 5 --no-e2e --no-cpu > /dev/null 2>&1
+GSKIP=3000 bash scripts/prof_gemm.sh ${TAG} > /dev/null 2>&1
+LTAG=${TAG} SKIP=5000 CNT=6000 bash scripts/rnn_launches.sh > /dev/null 2>&1
 python scripts/ncu_summary.py ${TAG} smax3m smax2s3z mpe_large overcooked smax27m > /dev/null 2>&1
 mkdir -p gpurun_out/summary_${TAG}
 cp profiles/${TAG}_* profiles/ncu_traffic.json profiles/ncu_metrics.json gpurun_out/summary_${TAG}/ 2>/dev/null
