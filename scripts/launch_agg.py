@@ -13,7 +13,7 @@ for r in rows[hi + 1:]:
     if len(r) <= vi:
         continue
     v = float(r[vi].replace(',', ''))
-    v = {'nsecond': 1e-3, 'usecond': 1.0, 'msecond': 1e3}.get(r[ui], 1.0) * v
+    v = {'nsecond': 1e-3, 'ns': 1e-3, 'usecond': 1.0, 'us': 1.0, 'msecond': 1e3, 'ms': 1e3}.get(r[ui], 1.0) * v
     agg[r[ki].split('(')[0][-50:] + (" grid=" + r[gi] if gi is not None else "")].append(v)
 tot = sum(sum(v) for v in agg.values())
 for k, v in sorted(agg.items(), key=lambda x: -sum(x[1]))[:int(sys.argv[2]) if len(sys.argv) > 2 else 25]:
