@@ -125,12 +125,20 @@ __host__ __device__ inline uint32_t raw_bytes(int rows, int kind, int KC) {
   return kind == 1 ? uint32_t(KC) * rows * 4 : uint32_t(rows) * (KC + 4) * 4;
 }
 
+// Operand staging code (compile-time, one path per kernel instance so the
+// kernel stays small in the instruction cache): 0 K-contiguous with 16-byte
+// copies, 1 K-contiguous (or general strides) element by element, 2
+// rows-contiguous with 16-byte copies, 3 rows-contiguous element by element.
+__host__ __device__ constexpr int lay_kind(int L) { return L >= 2 ? 1 : 0; }
+__host__ __device__ constexpr int lay_vec(int L) { return (L == 0 || L == 2) ? 4 : 1; }
+
 // Issue the cp.async copies of chunk [k0, k0 + KC) of rows [r0, r0 + rows)
 // (valid rows < rvalid, valid k < K) into a raw stage.
-template <int KC, int V>
-__device__ __forceinline__ void fetch_v(float* raw, const OpLayout& o, int64_t r0, int rows, int64_t rvalid, int64_t k0,
-                                        int64_t K) {
-  if (o.kind == 1) {  // raw[k][r], copies along r
+template <int KC, int L>
+__device__ __forceinline__ void fetch(float* raw, const OpLayout& o, int64_t r0, int rows, int64_t rvalid, int64_t k0,
+                                      int64_t K) {
+  constexpr int V = lay_vec(L);
+  if constexpr (lay_kind(L) == 1) {  // raw[k][r], copies along r
     const int per_k = rows / V;
     for (int idx = threadIdx.x; idx < per_k * KC; idx += kGemmThreads) {
       const int k = idx / per_k, r = (idx - k * per_k) * V;
@@ -140,7 +148,7 @@ __device__ __forceinline__ void fetch_v(float* raw, const OpLayout& o, int64_t r
       const float* src = nv ? o.X + gr * o.sr + gk * o.sk : o.X;
       cp_async<4 * V>(raw + k * rows + r, src, uint32_t(nv * 4));
     }
-  } else {  // raw[r][k], copies along k (kind 0) or single elements (kind 2, V = 1)
+  } else {  // raw[r][k], copies along k
     const int per_r = KC / V;
     for (int idx = threadIdx.x; idx < rows * per_r; idx += kGemmThreads) {
       const int r = idx / per_r, k = (idx - r * per_r) * V;
@@ -152,13 +160,6 @@ __device__ __forceinline__ void fetch_v(float* raw, const OpLayout& o, int64_t r
     }
   }
 }
-template <int KC>
-__device__ __forceinline__ void fetch(float* raw, const OpLayout& o, int64_t r0, int rows, int64_t rvalid, int64_t k0,
-                                      int64_t K) {
-  if (o.vec == 4) fetch_v<KC, 4>(raw, o, r0, rows, rvalid, k0, K);
-  else if (o.vec == 2) fetch_v<KC, 2>(raw, o, r0, rows, rvalid, k0, K);
-  else fetch_v<KC, 1>(raw, o, r0, rows, rvalid, k0, K);
-}
 
 // hi / lo tf32 images of v: hi = v with the low 13 mantissa bits cleared
 // (exact in tf32), lo = v - hi (exact in fp32)
@@ -168,12 +169,12 @@ __device__ __forceinline__ void split_tf32(float v, float& hi, float& lo) {
 }
 
 // raw stage -> hi / lo canonical tiles (four K per thread step)
-template <int KC>
-__device__ __forceinline__ void convert(const float* raw, int kind, int rows, uint8_t* hi, uint8_t* lo) {
+template <int KC, int KIND>
+__device__ __forceinline__ void convert(const float* raw, int rows, uint8_t* hi, uint8_t* lo) {
   for (int idx = threadIdx.x; idx < rows * (KC / 4); idx += kGemmThreads) {
     int r, k;
     float4 v;
-    if (kind == 1) {  // raw[k][r]: consecutive threads take consecutive rows
+    if (KIND == 1) {  // raw[k][r]: consecutive threads take consecutive rows
       r = idx % rows;
       k = (idx / rows) * 4;
       v = make_float4(raw[k * rows + r], raw[(k + 1) * rows + r], raw[(k + 2) * rows + r], raw[(k + 3) * rows + r]);
@@ -192,7 +193,7 @@ __device__ __forceinline__ void convert(const float* raw, int kind, int rows, ui
   }
 }
 
-template <int KC, int MINB>
+template <int KC, int MINB, int AL, int BL>
 __global__ void __launch_bounds__(kGemmThreads, MINB) gemm_tf32x3_kernel(GemmArgs g) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const int mt = blockIdx.x, nt = blockIdx.y, sp = blockIdx.z;
@@ -224,8 +225,8 @@ __global__ void __launch_bounds__(kGemmThreads, MINB) gemm_tf32x3_kernel(GemmArg
       float* ra = reinterpret_cast<float*>(raw0 + (c % g.ns) * stage_bytes);
       float* rb = reinterpret_cast<float*>(raw0 + (c % g.ns) * stage_bytes + g.a_raw);
       const int64_t k0 = kb + int64_t(c) * KC;
-      fetch<KC>(ra, g.a, m0, kGemmM, g.M, k0, ke);
-      fetch<KC>(rb, bo, 0, g.npad, nvalid, k0, ke);
+      fetch<KC, AL>(ra, g.a, m0, kGemmM, g.M, k0, ke);
+      fetch<KC, BL>(rb, bo, 0, g.npad, nvalid, k0, ke);
     }
     cp_async_commit();
   };
@@ -249,8 +250,8 @@ __global__ void __launch_bounds__(kGemmThreads, MINB) gemm_tf32x3_kernel(GemmArg
     if (c >= g.nt) mbar_wait(bar + ts, uint32_t((c - g.nt) / g.nt) & 1u);
     __syncthreads();  // every thread's copies of chunk c are visible
     const uint8_t* stg = raw0 + (c % g.ns) * stage_bytes;
-    convert<KC>(reinterpret_cast<const float*>(stg), g.a.kind, kGemmM, ah, al);
-    convert<KC>(reinterpret_cast<const float*>(stg + g.a_raw), g.b.kind, g.npad, bh, bl);
+    convert<KC, lay_kind(AL)>(reinterpret_cast<const float*>(stg), kGemmM, ah, al);
+    convert<KC, lay_kind(BL)>(reinterpret_cast<const float*>(stg + g.a_raw), g.npad, bh, bl);
     fence_proxy_async_smem();
     __syncthreads();  // tiles complete; the raw stage may be refilled
     if (threadIdx.x == 0) {
@@ -408,6 +409,29 @@ OpLayout op_layout(const float* X, int64_t sr, int64_t sk, int rows_per_tile) {
 
 }  // namespace
 
+int lay_code(const OpLayout& o) { return o.kind == 1 ? (o.vec == 4 ? 2 : 3) : (o.kind == 0 && o.vec == 4 ? 0 : 1); }
+
+using GemmKernel = void (*)(GemmArgs);
+template <int KC, int MINB, int AL>
+GemmKernel pick_b(int bl) {
+  switch (bl) {
+    case 0: return gemm_tf32x3_kernel<KC, MINB, AL, 0>;
+    case 1: return gemm_tf32x3_kernel<KC, MINB, AL, 1>;
+    case 2: return gemm_tf32x3_kernel<KC, MINB, AL, 2>;
+    default: return gemm_tf32x3_kernel<KC, MINB, AL, 3>;
+  }
+}
+template <int KC, int MINB>
+GemmKernel pick_ab(int al, int bl) {
+  switch (al) {
+    case 0: return pick_b<KC, MINB, 0>(bl);
+    case 1: return pick_b<KC, MINB, 1>(bl);
+    case 2: return pick_b<KC, MINB, 2>(bl);
+    default: return pick_b<KC, MINB, 3>(bl);
+  }
+}
+GemmKernel pick_kernel(bool deep, int al, int bl) { return deep ? pick_ab<32, 1>(al, bl) : pick_ab<16, 3>(al, bl); }
+
 // C[M x N] = beta C + A . B'^T on the tensor cores (see the file comment).
 cudaError_t tc_gemm(cudaStream_t st, int64_t M, int N, int64_t K, const float* A, int64_t sam, int64_t sak,
                     const float* B, int64_t sbn, int64_t sbk, float* C, int64_t ldc, float beta) {
@@ -469,7 +493,7 @@ cudaError_t tc_gemm(cudaStream_t st, int64_t M, int N, int64_t K, const float* A
     g.part = scratch(size_t(split) * size_t(M) * size_t(N), st, &e);
     if (!g.part) return e;
   }
-  auto kern = deep ? gemm_tf32x3_kernel<32, 1> : gemm_tf32x3_kernel<16, 3>;
+  auto kern = pick_kernel(deep, lay_code(g.a), lay_code(g.b));
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   kern<<<dim3(unsigned(mtiles), unsigned(ntiles), unsigned(split)), kGemmThreads, smem, st>>>(g);
   ++g_launches;
