@@ -42,10 +42,11 @@ namespace marl_b200 {
 namespace {
 
 constexpr int kGemmM = 128;        // rows per CTA (UMMA M)
-constexpr int kGemmMaxN = 128;     // columns per CTA (UMMA N <= 256; 128 keeps three CTAs per SM)
-constexpr int kGemmThreads = 128;  // one TMEM lane (accumulator row) per thread
+constexpr int kGemmMaxN = 128;     // columns per CTA (UMMA N <= 256)
+constexpr int kGemmThreads = 256;  // two warps per TMEM lane quarter (accumulator rows 32q..32q+31)
+constexpr int kGemmWarps = kGemmThreads / 32;
 // Two configurations (K elements per chunk KC, CTAs per SM): grids of M x N
-// tiles run KC = 16 with three CTAs per SM; split-K grids (the weight
+// tiles run KC = 16 with two 256-thread CTAs per SM; split-K grids (the weight
 // gradients, a few tiles over a very long K) run KC = 32 with one CTA per SM
 // and a deeper raw ring (four stages, two tile sets).
 template <int KC>
@@ -205,7 +206,7 @@ __global__ void __launch_bounds__(kGemmThreads, MINB) gemm_tf32x3_kernel(GemmArg
   // smem: [tile sets: A hi, A lo, B hi, B lo] x nt, [raw stages: A, B] x ns, 2 barriers, TMEM slot
   const uint32_t set_bytes = 2 * g.a_tile + 2 * g.b_tile, stage_bytes = g.a_raw + g.b_raw;
   uint8_t* raw0 = smem + g.nt * set_bytes;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(raw0 + max(g.ns * stage_bytes, uint32_t(4 * 32 * kEpiPitch * 4)));
+  uint64_t* bar = reinterpret_cast<uint64_t*>(raw0 + max(g.ns * stage_bytes, uint32_t(kGemmWarps * 32 * kEpiPitch * 4)));
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 2);
   const int warp = threadIdx.x >> 5;
   if (threadIdx.x == 0) {
@@ -273,14 +274,15 @@ __global__ void __launch_bounds__(kGemmThreads, MINB) gemm_tf32x3_kernel(GemmArg
   }
   tc_fence_after();
 
-  // epilogue: thread r holds accumulator row r (TMEM lane r); each warp
-  // stages its 32 rows x 32 columns through shared memory (the raw stages are
-  // free now) and writes them back one row (128 B) per instruction
+  // epilogue: warp w reads accumulator rows 32 (w % 4) .. +31 (its TMEM lane
+  // quarter), every (kGemmWarps / 4)-th 32-column block; each block is staged
+  // through shared memory (the raw stages are free now) and written back one
+  // row (128 B) per instruction
   __syncthreads();
   float* stg = reinterpret_cast<float*>(raw0) + warp * 32 * kEpiPitch;
-  const int lane = threadIdx.x & 31;
-  const uint32_t lane_base = uint32_t(warp * 32) << 16;
-  for (int c0 = 0; c0 < g.npad; c0 += 32) {
+  const int lane = threadIdx.x & 31, quarter = warp & 3;
+  const uint32_t lane_base = uint32_t(quarter * 32) << 16;
+  for (int c0 = (warp >> 2) * 32; c0 < g.npad; c0 += 32 * (kGemmWarps / 4)) {
     float v[32];
     if (nch > 0) {
       tmem_ld32(tmem + lane_base + uint32_t(c0), v);
@@ -294,7 +296,7 @@ __global__ void __launch_bounds__(kGemmThreads, MINB) gemm_tf32x3_kernel(GemmArg
     const int col = c0 + lane;
     if (col < nvalid) {
       for (int rr = 0; rr < 32; ++rr) {
-        const int64_t m = m0 + warp * 32 + rr;
+        const int64_t m = m0 + quarter * 32 + rr;
         if (m >= g.M) break;
         const float x = stg[rr * kEpiPitch + lane];
         if (g.split > 1) {
@@ -430,7 +432,7 @@ GemmKernel pick_ab(int al, int bl) {
     default: return pick_b<KC, MINB, 3>(bl);
   }
 }
-GemmKernel pick_kernel(bool deep, int al, int bl) { return deep ? pick_ab<32, 1>(al, bl) : pick_ab<16, 3>(al, bl); }
+GemmKernel pick_kernel(bool deep, int al, int bl) { return deep ? pick_ab<32, 1>(al, bl) : pick_ab<16, 2>(al, bl); }
 
 // C[M x N] = beta C + A . B'^T on the tensor cores (see the file comment).
 cudaError_t tc_gemm(cudaStream_t st, int64_t M, int N, int64_t K, const float* A, int64_t sam, int64_t sak,
@@ -465,11 +467,11 @@ cudaError_t tc_gemm(cudaStream_t st, int64_t M, int N, int64_t K, const float* A
     split = std::max(1, std::min(split, 1024));
   }
   // split-K grids (few tiles over a long K: the weight gradients) take the deep
-  // configuration; everything else keeps three CTAs per SM (measured: the deep
-  // ring on a 1.3-wave grid of 192 tiles is 1.7x slower than three CTAs per SM)
+  // configuration; everything else keeps two CTAs per SM (measured: the deep
+  // ring on a 1.3-wave grid of 192 tiles is 1.7x slower than several CTAs per SM)
   const bool deep = split > 1;
   const int KC = deep ? 32 : 16;
-  const uint32_t budget = deep ? 227 * 1024 - 1024 : 227 * 1024 / 3 - 1024;
+  const uint32_t budget = deep ? 227 * 1024 - 1024 : 227 * 1024 / 2 - 1024;
   g.a_raw = raw_bytes(kGemmM, g.a.kind, KC);
   g.b_raw = raw_bytes(g.npad, g.b.kind, KC);
   g.a_tile = kGemmM * KC * 4;
@@ -478,7 +480,7 @@ cudaError_t tc_gemm(cudaStream_t st, int64_t M, int N, int64_t K, const float* A
   g.ns = deep ? 4 : 3;
   g.nt = 2;
   auto bytes = [&] {  // the epilogue staging (4 warps x 32 x kEpiPitch floats) reuses the raw stages
-    const uint32_t raw = std::max<uint32_t>(g.ns * (g.a_raw + g.b_raw), 4 * 32 * kEpiPitch * 4);
+    const uint32_t raw = std::max<uint32_t>(g.ns * (g.a_raw + g.b_raw), kGemmWarps * 32 * kEpiPitch * 4);
     return g.nt * (2 * g.a_tile + 2 * g.b_tile) + raw + 64;
   };
   while (bytes() > budget && g.ns > 2) --g.ns;
