@@ -112,7 +112,8 @@ struct GemmArgs {
   float* C;        // output (split == 1) ...
   float* part;     // ... or [split][M][N] partial tiles (split > 1)
   int64_t M, K, ldc;
-  int N, npad;     // columns; npad: MMA N of a tile (multiple of 16)
+  int N, npad;     // columns; npad: MMA N of a tile (a power of two >= 16)
+  int nlog;        // log2(npad)
   int ntile;       // columns per N tile
   int split;       // K splits
   int64_t kchunk;  // K elements per split (multiple of the chunk KC)
@@ -134,25 +135,27 @@ __host__ __device__ constexpr int lay_kind(int L) { return L >= 2 ? 1 : 0; }
 __host__ __device__ constexpr int lay_vec(int L) { return (L == 0 || L == 2) ? 4 : 1; }
 
 // Issue the cp.async copies of chunk [k0, k0 + KC) of rows [r0, r0 + rows)
-// (valid rows < rvalid, valid k < K) into a raw stage.
+// (valid rows < rvalid, valid k < K) into a raw stage.  rows = 1 << rlog, so
+// every index split is a shift or a mask.
 template <int KC, int L>
-__device__ __forceinline__ void fetch(float* raw, const OpLayout& o, int64_t r0, int rows, int64_t rvalid, int64_t k0,
+__device__ __forceinline__ void fetch(float* raw, const OpLayout& o, int64_t r0, int rlog, int64_t rvalid, int64_t k0,
                                       int64_t K) {
   constexpr int V = lay_vec(L);
+  const int rows = 1 << rlog;
   if constexpr (lay_kind(L) == 1) {  // raw[k][r], copies along r
-    const int per_k = rows / V;
-    for (int idx = threadIdx.x; idx < per_k * KC; idx += kGemmThreads) {
-      const int k = idx / per_k, r = (idx - k * per_k) * V;
+    const int plog = rlog - (V == 4 ? 2 : 0);  // log2(rows / V)
+    for (int idx = threadIdx.x; idx < (KC << plog); idx += kGemmThreads) {
+      const int k = idx >> plog, r = (idx & ((1 << plog) - 1)) * V;
       const int64_t gk = k0 + k, gr = r0 + r;
       int64_t nv = gk < K ? rvalid - gr : 0;
       nv = nv < 0 ? 0 : nv > V ? V : nv;
       const float* src = nv ? o.X + gr * o.sr + gk * o.sk : o.X;
-      cp_async<4 * V>(raw + k * rows + r, src, uint32_t(nv * 4));
+      cp_async<4 * V>(raw + (k << rlog) + r, src, uint32_t(nv * 4));
     }
   } else {  // raw[r][k], copies along k
-    const int per_r = KC / V;
+    constexpr int per_r = KC / V;
     for (int idx = threadIdx.x; idx < rows * per_r; idx += kGemmThreads) {
-      const int r = idx / per_r, k = (idx - r * per_r) * V;
+      const int r = idx / per_r, k = (idx % per_r) * V;
       const int64_t gk = k0 + k, gr = r0 + r;
       int64_t nv = gr < rvalid ? K - gk : 0;
       nv = nv < 0 ? 0 : nv > V ? V : nv;
@@ -171,17 +174,15 @@ __device__ __forceinline__ void split_tf32(float v, float& hi, float& lo) {
 
 // raw stage -> hi / lo canonical tiles (four K per thread step)
 template <int KC, int KIND>
-__device__ __forceinline__ void convert(const float* raw, int rows, uint8_t* hi, uint8_t* lo) {
+__device__ __forceinline__ void convert(const float* raw, int rlog, uint8_t* hi, uint8_t* lo) {
+  const int rows = 1 << rlog;
   for (int idx = threadIdx.x; idx < rows * (KC / 4); idx += kGemmThreads) {
-    int r, k;
+    const int r = idx & (rows - 1), k = (idx >> rlog) * 4;  // consecutive threads take consecutive rows
     float4 v;
-    if (KIND == 1) {  // raw[k][r]: consecutive threads take consecutive rows
-      r = idx % rows;
-      k = (idx / rows) * 4;
-      v = make_float4(raw[k * rows + r], raw[(k + 1) * rows + r], raw[(k + 2) * rows + r], raw[(k + 3) * rows + r]);
+    if (KIND == 1) {  // raw[k][r]
+      v = make_float4(raw[(k << rlog) + r], raw[((k + 1) << rlog) + r], raw[((k + 2) << rlog) + r],
+                      raw[((k + 3) << rlog) + r]);
     } else {
-      r = idx % rows;
-      k = (idx / rows) * 4;
       v = *reinterpret_cast<const float4*>(raw + r * raw_pitch<KC>() + k);
     }
     float4 h, l;
@@ -221,17 +222,20 @@ __global__ void __launch_bounds__(kGemmThreads, MINB) gemm_tf32x3_kernel(GemmArg
   }
   OpLayout bo = g.b;
   bo.X = g.b.X + int64_t(n0) * g.b.sr;
+  int wstage = 0;           // the stage the next issued chunk lands in
   auto issue = [&](int c) {  // raw chunk c -> stage c % ns (one commit group per call)
     if (c < nch) {
-      float* ra = reinterpret_cast<float*>(raw0 + (c % g.ns) * stage_bytes);
-      float* rb = reinterpret_cast<float*>(raw0 + (c % g.ns) * stage_bytes + g.a_raw);
+      float* ra = reinterpret_cast<float*>(raw0 + wstage * stage_bytes);
+      float* rb = reinterpret_cast<float*>(raw0 + wstage * stage_bytes + g.a_raw);
       const int64_t k0 = kb + int64_t(c) * KC;
-      fetch<KC, AL>(ra, g.a, m0, kGemmM, g.M, k0, ke);
-      fetch<KC, BL>(rb, bo, 0, g.npad, nvalid, k0, ke);
+      fetch<KC, AL>(ra, g.a, m0, 7, g.M, k0, ke);
+      fetch<KC, BL>(rb, bo, 0, g.nlog, nvalid, k0, ke);
     }
     cp_async_commit();
+    wstage = wstage + 1 == g.ns ? 0 : wstage + 1;
   };
   for (int c = 0; c < g.ns - 1; ++c) issue(c);
+  int rstage = 0;  // the stage chunk c is read from
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -241,18 +245,25 @@ __global__ void __launch_bounds__(kGemmThreads, MINB) gemm_tf32x3_kernel(GemmArg
   for (int c = 0; c < nch; ++c) {
     issue(c + g.ns - 1);
     // chunk c's copies (this thread's) have landed: at most ns - 1 newer groups pending
-    if (g.ns >= 4) cp_async_wait<3>();
-    else if (g.ns == 3) cp_async_wait<2>();
-    else cp_async_wait<1>();
+    switch (g.ns) {
+      case 8: cp_async_wait<7>(); break;
+      case 7: cp_async_wait<6>(); break;
+      case 6: cp_async_wait<5>(); break;
+      case 5: cp_async_wait<4>(); break;
+      case 4: cp_async_wait<3>(); break;
+      case 3: cp_async_wait<2>(); break;
+      default: cp_async_wait<1>(); break;
+    }
     const int ts = g.nt == 2 ? (c & 1) : 0;
     uint8_t* set = smem + ts * set_bytes;
     uint8_t *ah = set, *al = set + g.a_tile, *bh = set + 2 * g.a_tile, *bl = set + 2 * g.a_tile + g.b_tile;
     // the MMAs that last read this tile set (chunk c - nt) are done
     if (c >= g.nt) mbar_wait(bar + ts, uint32_t((c - g.nt) / g.nt) & 1u);
     __syncthreads();  // every thread's copies of chunk c are visible
-    const uint8_t* stg = raw0 + (c % g.ns) * stage_bytes;
-    convert<KC, lay_kind(AL)>(reinterpret_cast<const float*>(stg), kGemmM, ah, al);
-    convert<KC, lay_kind(BL)>(reinterpret_cast<const float*>(stg + g.a_raw), g.npad, bh, bl);
+    const uint8_t* stg = raw0 + rstage * stage_bytes;
+    rstage = rstage + 1 == g.ns ? 0 : rstage + 1;
+    convert<KC, lay_kind(AL)>(reinterpret_cast<const float*>(stg), 7, ah, al);
+    convert<KC, lay_kind(BL)>(reinterpret_cast<const float*>(stg + g.a_raw), g.nlog, bh, bl);
     fence_proxy_async_smem();
     __syncthreads();  // tiles complete; the raw stage may be refilled
     if (threadIdx.x == 0) {
@@ -451,7 +462,12 @@ cudaError_t tc_gemm(cudaStream_t st, int64_t M, int N, int64_t K, const float* A
   const int maxn = (mt0 * ((N + kGemmMaxN - 1) / kGemmMaxN) < 2 * int64_t(sm_count()) && N > 64) ? 64 : kGemmMaxN;
   const int ntiles = (N + maxn - 1) / maxn;
   g.ntile = ((N + ntiles - 1) / ntiles + 15) / 16 * 16;  // balanced N tiles, multiples of 16
-  g.npad = g.ntile;
+  g.npad = 16;
+  g.nlog = 4;
+  while (g.npad < g.ntile) {
+    g.npad <<= 1;
+    ++g.nlog;
+  }
   g.tmem_cols = pow2_cols(g.npad);
   g.a = op_layout(A, sam, sak, kGemmM);
   g.b = op_layout(B, sbn, sbk, g.npad);
@@ -477,7 +493,7 @@ cudaError_t tc_gemm(cudaStream_t st, int64_t M, int N, int64_t K, const float* A
   g.a_tile = kGemmM * KC * 4;
   g.b_tile = uint32_t(g.npad) * KC * 4;
   // as many raw stages (latency hiding) and tile sets (split / MMA overlap) as fit
-  g.ns = deep ? 4 : 3;
+  g.ns = 8;  // prefetch distance ns - 1 chunks: as deep as shared memory allows
   g.nt = 2;
   auto bytes = [&] {  // the epilogue staging (4 warps x 32 x kEpiPitch floats) reuses the raw stages
     const uint32_t raw = std::max<uint32_t>(g.ns * (g.a_raw + g.b_raw), kGemmWarps * 32 * kEpiPitch * 4);
