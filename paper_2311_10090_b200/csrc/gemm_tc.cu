@@ -306,16 +306,25 @@ __global__ void __launch_bounds__(kGemmThreads, MINB) gemm_tf32x3_kernel(GemmArg
     __syncwarp();
     const int col = c0 + lane;
     if (col < nvalid) {
-      for (int rr = 0; rr < 32; ++rr) {
-        const int64_t m = m0 + quarter * 32 + rr;
-        if (m >= g.M) break;
-        const float x = stg[rr * kEpiPitch + lane];
-        if (g.split > 1) {
-          g.part[(int64_t(sp) * g.M + m) * g.N + n0 + col] = x;
-        } else {
-          float* d = g.C + m * g.ldc + n0 + col;
-          *d = g.beta != 0.0f ? *d + x : x;
+      const int64_t mq = m0 + quarter * 32;
+      const int nr = int(min(int64_t(32), g.M - mq));
+      if (g.split > 1) {
+        float* dst = g.part + (int64_t(sp) * g.M + mq) * g.N + n0 + col;
+        for (int rr = 0; rr < nr; ++rr) dst[int64_t(rr) * g.N] = stg[rr * kEpiPitch + lane];
+      } else if (g.beta != 0.0f) {  // C += acc: eight independent loads in flight per batch
+        float* dst = g.C + mq * g.ldc + n0 + col;
+#pragma unroll 1
+        for (int r0 = 0; r0 < nr; r0 += 8) {
+          float old[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) old[q] = r0 + q < nr ? dst[int64_t(r0 + q) * g.ldc] : 0.0f;
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            if (r0 + q < nr) dst[int64_t(r0 + q) * g.ldc] = old[q] + stg[(r0 + q) * kEpiPitch + lane];
         }
+      } else {
+        float* dst = g.C + mq * g.ldc + n0 + col;
+        for (int rr = 0; rr < nr; ++rr) dst[int64_t(rr) * g.ldc] = stg[rr * kEpiPitch + lane];
       }
     }
     __syncwarp();
