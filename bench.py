@@ -451,7 +451,7 @@ def run_gpu_ppo(args, rank, world, local_rank):
         "metric": "agent-steps/sec (env-steps/sec x agents)", "value": value, "unit": "agent-steps/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": ("f32 recurrent policy + f32 BPTT update (cuBLAS SGEMM steps)" if recurrent else
+        "dtype": ("f32 recurrent policy + f32 BPTT update (3xTF32 tcgen05 GEMMs, fp32-accurate)" if recurrent else
                   "bf16 rollout policy + bf16 tcgen05 PPO update (fp32 accumulate)") + " / f64 env", "data": "synthetic (key_from_seed(rank))",
         "config": workload_config(args.workload, world, n_envs),
         "run": {"batch_rows": T * R, "step": "one PPO update = collect + update",
@@ -462,7 +462,7 @@ def run_gpu_ppo(args, rank, world, local_rank):
         "update_row_passes_per_sec": T * R * 5 / upd_s,
         "roofline": {"bound": "tensor", "achieved": tflops, "peak": peak, "unit": "TFLOP/s", "frac": tflops / peak,
                      "traffic": None, "peak_source": "MEASURED_PEAKS.json bf16_tflops (dense)",
-                     "kernel": ("recurrent PPO update (fp32 cuBLAS SGEMM per time step + gate kernels)" if recurrent
+                     "kernel": ("recurrent PPO update (3xTF32 tcgen05 GEMM per time step + gate kernels)" if recurrent
                                 else "PPO update phase (ppo_update_tc_kernel dominant: bf16 tcgen05 forward, input- "
                                      "and weight-gradient GEMMs, fp32 TMEM accumulation)"),
                      "flop_per_row_pass": fpr},

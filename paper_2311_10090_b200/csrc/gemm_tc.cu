@@ -30,6 +30,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstdint>
 #include <map>
 #include <mutex>
@@ -487,14 +488,17 @@ cudaError_t tc_gemm(cudaStream_t st, int64_t M, int N, int64_t K, const float* A
   // split K when the M x N tiles alone leave SMs idle and K is long
   int split = 1;
   const int64_t tiles = mtiles * ntiles;
+  const bool deep_env = getenv("MARL_GEMM_DEEP") != nullptr;  // A/B knob: split-K on the deep ring
   if (tiles < sm_count() && K > 128) {
-    split = int(std::min<int64_t>(std::max<int64_t>(1, sm_count() / tiles), (K + 127) / 128));
+    const char* ps = getenv("MARL_GEMM_SPLIT_PER_SM");
+    const int64_t per_sm = ps ? std::max(1, atoi(ps)) : deep_env ? 1 : 2;
+    split = int(std::min<int64_t>(std::max<int64_t>(1, per_sm * sm_count() / tiles), (K + 127) / 128));
     split = std::max(1, std::min(split, 1024));
   }
   // split-K grids (few tiles over a long K: the weight gradients) take the deep
   // configuration; everything else keeps two CTAs per SM (measured: the deep
   // ring on a 1.3-wave grid of 192 tiles is 1.7x slower than several CTAs per SM)
-  const bool deep = split > 1;
+  const bool deep = split > 1 && deep_env;
   const int KC = deep ? 32 : 16;
   const uint32_t budget = deep ? 227 * 1024 - 1024 : 227 * 1024 / 2 - 1024;
   g.a_raw = raw_bytes(kGemmM, g.a.kind, KC);

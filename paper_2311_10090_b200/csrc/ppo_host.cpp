@@ -1,7 +1,7 @@
 // The trainer of the C-ABI (marl_ppo_*, include/marl_b200.h): the reference's
 // train_ippo / train_mappo (proj/core/src/algo/ppo.cpp:518-651) around the
-// collector and the device update (ppo.cu, ppo_tc.cu, rnn.cu), with the
-// NCCL and cuBLAS libraries loaded at run time.
+// collector and the device update (ppo.cu, ppo_tc.cu, rnn.cu, gemm_tc.cu),
+// with the NCCL library loaded at run time.
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <nccl.h>
