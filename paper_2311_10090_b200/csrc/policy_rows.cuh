@@ -70,6 +70,41 @@ __device__ inline void sample_row_f32(double u, const float* logits, const uint8
   *logp = logits[pick] - mx - log_denom;
 }
 
+// sample_row_f32 with the loops bounded by a compile-time NMAX (>= n_act):
+// fully unrolled, the probabilities stay in registers.
+template <int NMAX>
+__device__ __forceinline__ void sample_row_n(double u, const float* logits, const uint8_t* legal, int n_act, int* action,
+                                             float* logp) {
+  bool lg[NMAX];
+  float mx = -INFINITY;
+#pragma unroll
+  for (int i = 0; i < NMAX; ++i) {
+    lg[i] = i < n_act && legal[i];
+    if (lg[i]) mx = fmaxf(mx, logits[i]);
+  }
+  float p[NMAX], denom = 0.0f;
+#pragma unroll
+  for (int i = 0; i < NMAX; ++i) {
+    p[i] = lg[i] ? expf(logits[i] - mx) : 0.0f;
+    denom += p[i];
+  }
+  const float log_denom = logf(denom), inv = 1.0f / denom;
+  double cum = 0.0;
+  int pick = -1;
+  bool done = false;
+  float lpick = 0.0f;
+#pragma unroll
+  for (int i = 0; i < NMAX; ++i) {
+    if (!lg[i] || done) continue;
+    pick = i;
+    lpick = logits[i];
+    cum += double(p[i] * inv);
+    done = u < cum;
+  }
+  *action = pick;
+  *logp = lpick - mx - log_denom;
+}
+
 // The fp32 path's per-row tail: sample, then the buffer writes.
 __device__ inline void sample_and_record(const PolicyStep& s, const RolloutBufs& b, int64_t r, const float* logits,
                                   int n_act, float value) {

@@ -294,12 +294,17 @@ __device__ __forceinline__ bool tile_obs_load(const PolicyStep& s, int64_t tile,
   return false;
 }
 
-// KXT = 32: the small-input instance (K, staging mode 3 compile-time); 0: any width
-template <int KXT>
-__global__ void __launch_bounds__(kSplit * kTcRows) policy_tc_kernel(PolicyNetBf16 nb, int in_dim, int n_act, PolicyStep s,
-                                                            RolloutBufs b) {
+// KXT = 32: the small-input instance (K, staging mode 3 compile-time); 0: any width.
+// SD / SA / SN > 0: the observation width, agent count and action count folded
+// to compile-time constants (MPE simple_spread: 18 / 3 / 5) -- the row build,
+// legal rows and sampling unroll into registers; 0: read from the step.
+template <int KXT, int SD = 0, int SA = 0, int SN = 0>
+__global__ void __launch_bounds__(kSplit * kTcRows) policy_tc_kernel(PolicyNetBf16 nb, int in_dim_rt, int n_act_rt,
+                                                                     PolicyStep s, RolloutBufs b) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  const TcLayout L = KXT ? tc_layout_mode(s.D, in_dim, n_act, 3) : tc_layout(s.D, in_dim, n_act);
+  const int D = SD ? SD : s.D, AA = SA ? SA : s.A, n_act = SN ? SN : n_act_rt;
+  const int in_dim = SD ? SD + (SA > 1 ? SA : 0) : in_dim_rt;
+  const TcLayout L = KXT ? tc_layout_mode(D, in_dim, n_act, 3) : tc_layout(D, in_dim, n_act);
   const int KX = KXT ? KXT : L.kx;
   const int NBUF = KXT ? 2 : L.nbuf;
   const bool HAS_OUT = KXT ? true : bool(L.has_out);
@@ -371,7 +376,6 @@ __global__ void __launch_bounds__(kSplit * kTcRows) policy_tc_kernel(PolicyNetBf
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const uint32_t lane_base = uint32_t((warp & 3) * 32) << 16;
-  const int D = s.D;
   const bool act_mode = !s.bootstrap;
   uint32_t phase = 0, in_phase[2] = {0, 0};
   bool in_flight[2] = {false, false};
@@ -401,8 +405,8 @@ __global__ void __launch_bounds__(kSplit * kTcRows) policy_tc_kernel(PolicyNetBf
     // ---- write_input / write_legal / agent_active (team.cpp:27-42): part q
     // builds K columns [KX q/kSplit, KX (q+1)/kSplit) of the row
     {
-      const int64_t e = r < 0x7fffffff ? int64_t(uint32_t(r) / uint32_t(s.A)) : r / s.A;
-      const int a = int(r - e * s.A);
+      const int64_t e = r < 0x7fffffff ? int64_t(uint32_t(r) / uint32_t(AA)) : r / AA;
+      const int a = int(r - e * AA);
       const int k0 = (KX / kSplit) * part;
       auto build = [&](auto load) {
 #pragma unroll 2
@@ -412,7 +416,7 @@ __global__ void __launch_bounds__(kSplit * kTcRows) policy_tc_kernel(PolicyNetBf
           for (int j = 0; j < 8; ++j) {
             const int k = k0 + kk + j;
             x[j] = (live && k < D) ? load(k) : 0.0f;
-            if (live && s.A > 1 && k == D + a) x[j] = 1.0f;
+            if (live && AA > 1 && k == D + a) x[j] = 1.0f;
           }
           if (live && act_mode && HAS_OUT) {
             float* o = obs_out + tid * in_dim;
@@ -430,7 +434,7 @@ __global__ void __launch_bounds__(kSplit * kTcRows) policy_tc_kernel(PolicyNetBf
         for (int j = 0; j < KXT / kSplit; ++j) {
           const int k = k0 + j;
           x[j] = (live && k < D) ? so[k] : 0.0f;
-          if (live && s.A > 1 && k == D + a) x[j] = 1.0f;
+          if (live && AA > 1 && k == D + a) x[j] = 1.0f;
         }
         if (live && act_mode) {
           float* o = obs_out + tid * in_dim;
@@ -456,7 +460,9 @@ __global__ void __launch_bounds__(kSplit * kTcRows) policy_tc_kernel(PolicyNetBf
             for (int q = 0; q < n_act; ++q) lg[q] = gl[q];
           } else {
             const int na = s.agent_actions[a];
-            for (int q = 0; q < n_act; ++q) lg[q] = q < na ? 1 : 0;
+#pragma unroll
+            for (int q = 0; q < (SN ? SN : 16); ++q)
+              if (q < n_act) lg[q] = q < na ? 1 : 0;
           }
           s_active[tid] = (s.family == 1) ? (lg[0] ? 1.0f : 0.0f) : 1.0f;
         }
@@ -472,9 +478,9 @@ __global__ void __launch_bounds__(kSplit * kTcRows) policy_tc_kernel(PolicyNetBf
         const int n = rows * in_dim;
         for (int q = threadIdx.x; q < n; q += blockDim.x) {
           const int rr = q / in_dim, k = q - rr * in_dim;
-          const int a = int((r0 + rr) % s.A);
+          const int a = int((r0 + rr) % AA);
           go[q] = k < D ? (NBUF > 0 ? tile_obs[rr * D + k] : __ldg(tile_obs + size_t(rr) * D + k))
-                        : ((s.A > 1 && k == D + a) ? 1.0f : 0.0f);
+                        : ((AA > 1 && k == D + a) ? 1.0f : 0.0f);
         }
       }
       if (!s.legal_ready) tile_put(b.legal + slot0 * n_act, s_legal, size_t(rows) * n_act);
@@ -565,7 +571,7 @@ __global__ void __launch_bounds__(kSplit * kTcRows) policy_tc_kernel(PolicyNetBf
         for (int j = 0; j < 16; ++j) logits[j] = hv[j] + s_bias[256 + j];
         int pick;
         float lp;
-        sample_row_f32(s_u[tid], logits, s_legal + tid * n_act, n_act, &pick, &lp);
+        sample_row_n<SN ? SN : 16>(s_u[tid], logits, s_legal + tid * n_act, n_act, &pick, &lp);
         b.actions[slot0 + tid] = pick;  // one element per thread: coalesced
         b.logp[slot0 + tid] = lp;
       }
@@ -645,7 +651,10 @@ void rollout_policy_bf16(const PolicyNet& net, const PolicyNetBf16& nb, const Po
   const size_t sm = tc_layout(s.D, net.in_dim, net.n_act).total;
   const TcLayout L = tc_layout(s.D, net.in_dim, net.n_act);
   const bool small = L.kx == 32 && L.nbuf == 2 && L.has_out;
-  auto kern = small ? policy_tc_kernel<32> : policy_tc_kernel<0>;
+  // MPE simple_spread (obs 18, 3 agents, 5 actions): the folded instance
+  const bool spread = small && s.D == 18 && s.A == 3 && net.n_act == 5 && net.in_dim == 21 &&
+                      !std::getenv("MARL_TC_GENERIC");
+  auto kern = small ? (spread ? policy_tc_kernel<32, 18, 3, 5> : policy_tc_kernel<32>) : policy_tc_kernel<0>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
   int per_sm = 1;
   cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
