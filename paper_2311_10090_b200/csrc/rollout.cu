@@ -435,6 +435,9 @@ __global__ void __launch_bounds__(kSplit * kTcRows) policy_tc_kernel(PolicyNetBf
           const int k = k0 + j;
           x[j] = (live && k < D) ? so[k] : 0.0f;
           if (live && AA > 1 && k == D + a) x[j] = 1.0f;
+          // folded instance: the last two K columns carry layer 1's bias (hi / lo
+          // bf16 halves in W1's image, pack_bf16_kernel) -- the MMA adds it
+          if (SD && live && k >= KXT - 2) x[j] = 1.0f;
         }
         if (live && act_mode) {
           float* o = obs_out + tid * in_dim;
@@ -512,7 +515,7 @@ __global__ void __launch_bounds__(kSplit * kTcRows) policy_tc_kernel(PolicyNetBf
       float v[32];
       tmem_ld32(tmem + lane_base + uint32_t(c), v);
 #pragma unroll
-      for (int i = 0; i < 32; ++i) v[i] = tanh_fast(v[i] + s_bias[c + i]);
+      for (int i = 0; i < 32; ++i) v[i] = tanh_fast(SD ? v[i] : v[i] + s_bias[c + i]);
       uint8_t* dsth = c < 64 ? ha : hc;
       put16(dsth, 64, tid, c & 63, v);
       put16(dsth, 64, tid, (c & 63) + 16, v + 16);
@@ -601,6 +604,11 @@ __global__ void pack_bf16_kernel(PolicyNet n, uint16_t* img, float* bias) {
     const int row = q / KX, k = q % KX;
     float v = 0.0f;
     if (k < in) v = row < 64 ? n.w1[row * in + k] : n.cw1[(row - 64) * in + k];
+    if (KX == 32 && in <= 30 && k >= 30) {  // layer-1 bias as hi / lo bf16 columns (read only by the folded
+      const float bb = row < 64 ? n.b1[row] : n.cb1[row - 64];  // instance, whose X carries 1 there)
+      const __nv_bfloat16 hi = __float2bfloat16_rn(bb);
+      v = k == 30 ? bb : bb - __bfloat162float(hi);
+    }
     a1[canon_off(row, k, KX) / 2] = bf(v);
   }
   for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < 64 * 64; q += gridDim.x * blockDim.x) {
