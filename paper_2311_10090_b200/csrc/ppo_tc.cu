@@ -189,7 +189,8 @@ __global__ void pack_rows_kernel(PpoTcPack p) {
 // NS tiles in flight: the phases of tile slots 0..NS-1 alternate, so one
 // slot's MMAs run under the other's epilogue; one thread issues every MMA in
 // a fixed order (the accumulation order is deterministic).
-template <int NS>
+// RELU: the torso activation folded (0 tanh, the PpoConfig default; 1 relu).
+template <int NS, int RELU>
 __global__ void __launch_bounds__(kThr, 1) ppo_update_tc_kernel(PpoTcArgs a) {
   constexpr uint32_t cG2 = tm_g2(NS), cG3 = tm_g3(NS), cGb = tm_gb(NS), cG1 = tm_g1(NS);
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -338,7 +339,7 @@ __global__ void __launch_bounds__(kThr, 1) ppo_update_tc_kernel(PpoTcArgs a) {
       float v[32];
       tmem_ld32(tmem + lane_base + cw + uint32_t(c), v);
 #pragma unroll
-      for (int i = 0; i < 32; ++i) v[i] = act_f(v[i] + b[c + i], a.relu);
+      for (int i = 0; i < 32; ++i) v[i] = act_f(v[i] + b[c + i], RELU);
       put16(dst, 128, row, c, v);
       put16(dst, 128, row, c + 16, v + 16);
     }
@@ -353,7 +354,7 @@ __global__ void __launch_bounds__(kThr, 1) ppo_update_tc_kernel(PpoTcArgs a) {
       get16(tile, 128, row, c, y);
       get16(tile, 128, row, c + 16, y + 16);
 #pragma unroll
-      for (int i = 0; i < 32; ++i) v[i] = act_d(v[i], y[i], a.relu);
+      for (int i = 0; i < 32; ++i) v[i] = act_d(v[i], y[i], RELU);
       put16(tile, 128, row, c, v);
       put16(tile, 128, row, c + 16, v + 16);
     }
@@ -664,7 +665,8 @@ void ppo_tc_pack(const PpoTcPack& p, cudaStream_t s) {
 void ppo_update_tc(const PpoTcArgs& a, int grid, cudaStream_t s) {
   const UpdLayout L = upd_layout(a.kx);
   const size_t sm = L.total;
-  auto kern = L.ns == 2 ? ppo_update_tc_kernel<2> : ppo_update_tc_kernel<1>;
+  auto kern = L.ns == 2 ? (a.relu ? ppo_update_tc_kernel<2, 1> : ppo_update_tc_kernel<2, 0>)
+                        : (a.relu ? ppo_update_tc_kernel<1, 1> : ppo_update_tc_kernel<1, 0>);
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
   kern<<<grid, kThr, sm, s>>>(a);
   ++g_launches;
