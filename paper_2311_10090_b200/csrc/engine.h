@@ -185,6 +185,7 @@ struct PolicyNet {
   const float *cw1, *cb1, *cw2, *cb2, *cw3, *cb3;
   int in_dim, n_act, width, relu;
   int critic_in;  // == in_dim (IPPO) or world_state_size (MAPPO, ppo.cpp:90-100)
+  int centralized;  // 1: the critic reads world_state rows (MAPPO)
 };
 
 // bf16 operand images for the tcgen05 path (K-major, no swizzle, UMMA
@@ -195,6 +196,7 @@ struct PolicyNetBf16 {
   const uint16_t* c2;   // [64 x 64]  critic W2
   const uint16_t* h3;   // [16 x 64]  actor head (rows 0..n_act-1), zero padded
   const uint16_t* hc3;  // [16 x 64]  critic head (row 0), zero padded
+  const uint16_t* c1;   // [64 x kc]  MAPPO critic W1 over world_state rows, K padded to kc = round16(critic_in); else null
   const float* bias;    // [64 b1a | 64 b1c | 64 b2a | 64 b2c | 16 b3a | 16 b3c]
 };
 
@@ -213,7 +215,7 @@ struct PolicyStep {
 };
 
 void rollout_policy_fp32(const PolicyNet& net, const PolicyStep& s, const RolloutBufs& b, cudaStream_t st);
-bool rollout_policy_bf16_supported(int in_dim, int n_act, int width);
+bool rollout_policy_bf16_supported(int in_dim, int n_act, int width, int critic_in = 0);  // critic_in > 0: MAPPO
 int rollout_tc_kx(int in_dim);  // K of the tcgen05 policy's layer 1: round16(in_dim), <= 192
 void rollout_policy_bf16(const PolicyNet& net, const PolicyNetBf16& nb, const PolicyStep& s, const RolloutBufs& b,
                          cudaStream_t st);

@@ -198,8 +198,9 @@ constexpr int kSplit = 2;            // threads per row (warps w, w+4, ... share
 // row widths (offsets in bytes from a 1024-aligned base).
 struct TcLayout {
   uint32_t w1, w2a, w2c, w3a, w3c, x, ha, hc, obs_in[2], obs_out, legal, resets, active, act, logp, value, u, bias,
-      bar, bar_in[2], tmem_slot, total;
+      bar, bar_in[2], tmem_slot, total, xc, wc1;
   int kx;       // K of layer 1: round16(in_dim)
+  int kc;       // MAPPO: K of the critic's layer 1, round16(critic_in) (its own X tile and W1 image); 0: IPPO
   int nbuf;     // staged observation tiles: 2 (next tile prefetched), 1 (prefetched after the row build), 0 (rows read from L2)
   int has_out;  // the buffer's input rows leave as one staged bulk store (else a coalesced cooperative store)
 };
@@ -211,9 +212,12 @@ __host__ __device__ inline uint32_t up(uint32_t v, uint32_t a) { return (v + a -
 __host__ __device__ inline int tc_kx(int in_dim) { return in_dim <= 32 ? 32 : (in_dim + 15) / 16 * 16; }
 
 // mode 3: two staged tiles + staged buffer rows; 2: two tiles; 1: one tile; 0: none
-__host__ __device__ inline TcLayout tc_layout_mode(int D, int in_dim, int n_act, int mode) {
+__host__ __device__ inline int tc_kc(int critic_in) { return critic_in > 0 ? (critic_in + 15) / 16 * 16 : 0; }
+
+__host__ __device__ inline TcLayout tc_layout_mode(int D, int in_dim, int n_act, int mode, int critic_in = 0) {
   TcLayout L{};
   L.kx = tc_kx(in_dim);
+  L.kc = tc_kc(critic_in);
   L.nbuf = mode >= 2 ? 2 : mode;
   L.has_out = mode == 3;
   uint32_t o = 0;
@@ -231,6 +235,8 @@ __host__ __device__ inline TcLayout tc_layout_mode(int D, int in_dim, int n_act,
   L.x = take(kTcRows * L.kx * 2, 128);
   L.ha = take(kTcRows * 64 * 2, 128);
   L.hc = take(kTcRows * 64 * 2, 128);
+  L.xc = L.kc ? take(uint32_t(kTcRows * L.kc * 2), 128) : 0;
+  L.wc1 = L.kc ? take(uint32_t(64 * L.kc * 2), 128) : 0;
   L.obs_in[0] = L.nbuf >= 1 ? take(uint32_t(kTcRows * D * 4), 16) : 0;
   L.obs_in[1] = L.nbuf >= 2 ? take(uint32_t(kTcRows * D * 4), 16) : L.obs_in[0];
   L.obs_out = L.has_out ? take(uint32_t(kTcRows * in_dim * 4), 16) : 0;
@@ -250,12 +256,12 @@ __host__ __device__ inline TcLayout tc_layout_mode(int D, int in_dim, int n_act,
   return L;
 }
 
-__host__ __device__ inline TcLayout tc_layout(int D, int in_dim, int n_act) {
+__host__ __device__ inline TcLayout tc_layout(int D, int in_dim, int n_act, int critic_in = 0) {
   for (int mode = 3; mode > 0; --mode) {
-    const TcLayout L = tc_layout_mode(D, in_dim, n_act, mode);
+    const TcLayout L = tc_layout_mode(D, in_dim, n_act, mode, critic_in);
     if (L.total <= kTcSmemMax) return L;
   }
-  return tc_layout_mode(D, in_dim, n_act, 0);
+  return tc_layout_mode(D, in_dim, n_act, 0, critic_in);
 }
 
 // Store a staged tile: one TMA bulk store when it qualifies, else a
@@ -298,13 +304,18 @@ __device__ __forceinline__ bool tile_obs_load(const PolicyStep& s, int64_t tile,
 // SD / SA / SN > 0: the observation width, agent count and action count folded
 // to compile-time constants (MPE simple_spread: 18 / 3 / 5) -- the row build,
 // legal rows and sampling unroll into registers; 0: read from the step.
-template <int KXT, int SD = 0, int SA = 0, int SN = 0>
+// CENT (generic instance only): MAPPO -- the critic's layer 1 reads the env's
+// world_state row (s.ws, critic_in wide) from its own X tile and W1 image.
+template <int KXT, int SD = 0, int SA = 0, int SN = 0, bool CENT = false>
 __global__ void __launch_bounds__(kSplit * kTcRows) policy_tc_kernel(PolicyNetBf16 nb, int in_dim_rt, int n_act_rt,
-                                                                     PolicyStep s, RolloutBufs b) {
+                                                                     PolicyStep s, RolloutBufs b, int critic_in) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   const int D = SD ? SD : s.D, AA = SA ? SA : s.A, n_act = SN ? SN : n_act_rt;
   const int in_dim = SD ? SD + (SA > 1 ? SA : 0) : in_dim_rt;
-  const TcLayout L = KXT ? tc_layout_mode(D, in_dim, n_act, 3) : tc_layout(D, in_dim, n_act);
+  const TcLayout L = KXT ? tc_layout_mode(D, in_dim, n_act, 3) : tc_layout(D, in_dim, n_act, CENT ? critic_in : 0);
+  const int KC = CENT ? L.kc : 0;
+  uint8_t* sxc = smem_raw + L.xc;
+  uint8_t* wc1 = smem_raw + L.wc1;
   const int KX = KXT ? KXT : L.kx;
   const int NBUF = KXT ? 2 : L.nbuf;
   const bool HAS_OUT = KXT ? true : bool(L.has_out);
@@ -369,6 +380,9 @@ __global__ void __launch_bounds__(kSplit * kTcRows) policy_tc_kernel(PolicyNetBf
       }
     }
     for (int q = threadIdx.x; q < 4 * 64 + 2 * 16; q += blockDim.x) s_bias[q] = __ldg(nb.bias + q);
+    if (CENT)
+      for (int q = threadIdx.x; q < 64 * KC * 2 / 16; q += blockDim.x)
+        reinterpret_cast<uint4*>(wc1)[q] = __ldg(reinterpret_cast<const uint4*>(nb.c1) + q);
   }
   fence_proxy_async_smem();
   tc_fence_before();
@@ -471,6 +485,23 @@ __global__ void __launch_bounds__(kSplit * kTcRows) policy_tc_kernel(PolicyNetBf
         }
       }
     }
+    if (CENT) {  // MAPPO critic rows: the env's world_state (ppo.cpp:341-346), part q builds K columns
+      // [KC q/kSplit, KC (q+1)/kSplit); the buffer keeps them in critic_in rows
+      const int64_t e = r < 0x7fffffff ? int64_t(uint32_t(r) / uint32_t(AA)) : r / AA;
+      const float* wsr = s.ws + size_t(e) * size_t(critic_in);
+      float* bc = b.critic_in + (slot0 + size_t(tid)) * size_t(critic_in);
+      const int kc0 = (KC / kSplit) * part;
+      for (int kk = 0; kk < KC / kSplit; kk += 8) {
+        float x[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int k = kc0 + kk + j;
+          x[j] = (live && k < critic_in) ? __ldg(wsr + k) : 0.0f;
+          if (live && act_mode && k < critic_in) bc[k] = x[j];
+        }
+        put8(sxc, KC, tid, kc0 + kk, x);
+      }
+    }
     fence_proxy_async_smem();
     __syncthreads();
     if (act_mode) {  // the input-side buffer rows leave while the MMAs run
@@ -499,8 +530,14 @@ __global__ void __launch_bounds__(kSplit * kTcRows) policy_tc_kernel(PolicyNetBf
     }
     if (threadIdx.x == 0) {
       tc_fence_after();
-      const uint32_t id = idesc_bf16(128, 128);
-      for (int k = 0; k < KX; k += 16) umma_bf16(tmem + 0, umma_desc(sx, KX, k), umma_desc(w1, KX, k), id, k > 0);
+      if (CENT) {  // actor rows 0-63 of W1 over X; the critic's W1 over the world_state tile
+        const uint32_t id = idesc_bf16(128, 64);
+        for (int k = 0; k < KX; k += 16) umma_bf16(tmem + 0, umma_desc(sx, KX, k), umma_desc(w1, KX, k), id, k > 0);
+        for (int k = 0; k < KC; k += 16) umma_bf16(tmem + 64, umma_desc(sxc, KC, k), umma_desc(wc1, KC, k), id, k > 0);
+      } else {
+        const uint32_t id = idesc_bf16(128, 128);
+        for (int k = 0; k < KX; k += 16) umma_bf16(tmem + 0, umma_desc(sx, KX, k), umma_desc(w1, KX, k), id, k > 0);
+      }
       umma_commit(bar);
     }
     // the row's sampling uniform (two Threefry blocks) is drawn by part 1
@@ -596,6 +633,7 @@ __global__ void pack_bf16_kernel(PolicyNet n, uint16_t* img, float* bias) {
   uint16_t* c2 = a2 + 64 * 64;
   uint16_t* h3 = c2 + 64 * 64;
   uint16_t* hc3 = h3 + 16 * 64;
+  uint16_t* c1 = hc3 + 16 * 64;  // MAPPO: the critic's W1 over world_state rows
   auto bf = [](float v) {
     const __nv_bfloat16 h = __float2bfloat16_rn(v);
     return *reinterpret_cast<const uint16_t*>(&h);
@@ -603,13 +641,20 @@ __global__ void pack_bf16_kernel(PolicyNet n, uint16_t* img, float* bias) {
   for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < 128 * KX; q += gridDim.x * blockDim.x) {
     const int row = q / KX, k = q % KX;
     float v = 0.0f;
-    if (k < in) v = row < 64 ? n.w1[row * in + k] : n.cw1[(row - 64) * in + k];
+    if (k < in && (row < 64 || !n.centralized)) v = row < 64 ? n.w1[row * in + k] : n.cw1[(row - 64) * in + k];
     if (KX == 32 && in <= 30 && k >= 30) {  // layer-1 bias as hi / lo bf16 columns (read only by the folded
       const float bb = row < 64 ? n.b1[row] : n.cb1[row - 64];  // instance, whose X carries 1 there)
       const __nv_bfloat16 hi = __float2bfloat16_rn(bb);
       v = k == 30 ? bb : bb - __bfloat162float(hi);
     }
     a1[canon_off(row, k, KX) / 2] = bf(v);
+  }
+  if (n.centralized) {
+    const int CI = n.critic_in, KC = tc_kc(CI);
+    for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < 64 * KC; q += gridDim.x * blockDim.x) {
+      const int row = q / KC, k = q % KC;
+      c1[canon_off(row, k, KC) / 2] = bf(k < CI ? n.cw1[row * CI + k] : 0.0f);
+    }
   }
   for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < 64 * 64; q += gridDim.x * blockDim.x) {
     const int row = q / 64, k = q % 64;
@@ -637,10 +682,10 @@ __global__ void pack_bf16_kernel(PolicyNet n, uint16_t* img, float* bias) {
 
 int rollout_tc_kx(int in_dim) { return tc_kx(in_dim); }
 
-bool rollout_policy_bf16_supported(int in_dim, int n_act, int width) {
+bool rollout_policy_bf16_supported(int in_dim, int n_act, int width, int critic_in) {
   // D <= in_dim: the layout without staged tiles bounds every mode
-  return in_dim >= 1 && tc_kx(in_dim) <= kTcMaxKx && n_act <= 16 && width == 64 &&
-         tc_layout_mode(in_dim, in_dim, n_act, 0).total <= kTcSmemMax;
+  return in_dim >= 1 && tc_kx(in_dim) <= kTcMaxKx && tc_kc(critic_in) <= kTcMaxKx && n_act <= 16 && width == 64 &&
+         tc_layout_mode(in_dim, in_dim, n_act, 0, critic_in).total <= kTcSmemMax;
 }
 
 void rollout_pack_bf16(const PolicyNet& net, uint16_t* images, float* bias, cudaStream_t st) {
@@ -656,13 +701,16 @@ void rollout_policy_bf16(const PolicyNet& net, const PolicyNetBf16& nb, const Po
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
-  const size_t sm = tc_layout(s.D, net.in_dim, net.n_act).total;
-  const TcLayout L = tc_layout(s.D, net.in_dim, net.n_act);
-  const bool small = L.kx == 32 && L.nbuf == 2 && L.has_out;
+  const bool cent = s.ws != nullptr;
+  const int ci = cent ? net.critic_in : 0;
+  const size_t sm = tc_layout(s.D, net.in_dim, net.n_act, ci).total;
+  const TcLayout L = tc_layout(s.D, net.in_dim, net.n_act, ci);
+  const bool small = !cent && L.kx == 32 && L.nbuf == 2 && L.has_out;
   // MPE simple_spread (obs 18, 3 agents, 5 actions): the folded instance
   const bool spread = small && s.D == 18 && s.A == 3 && net.n_act == 5 && net.in_dim == 21 &&
                       !std::getenv("MARL_TC_GENERIC");
-  auto kern = small ? (spread ? policy_tc_kernel<32, 18, 3, 5> : policy_tc_kernel<32>) : policy_tc_kernel<0>;
+  auto kern = small ? (spread ? policy_tc_kernel<32, 18, 3, 5> : policy_tc_kernel<32>)
+                    : (cent ? policy_tc_kernel<0, 0, 0, 0, true> : policy_tc_kernel<0>);
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
   int per_sm = 1;
   cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
@@ -681,7 +729,7 @@ void rollout_policy_bf16(const PolicyNet& net, const PolicyNetBf16& nb, const Po
   if (std::getenv("MARL_TC_DEBUG")) std::fprintf(stderr, "policy_tc: smem %zu per_sm %d\n", sm, per_sm);
   const int64_t tiles = (s.R + kTcRows - 1) / kTcRows;
   const int64_t grid = cap_grid(std::min<int64_t>(tiles, int64_t(sms) * per_sm));
-  kern<<<unsigned(grid), kSplit * kTcRows, sm, st>>>(nb, net.in_dim, net.n_act, s, b);
+  kern<<<unsigned(grid), kSplit * kTcRows, sm, st>>>(nb, net.in_dim, net.n_act, s, b, ci);
   ++g_launches;
 }
 

@@ -63,11 +63,11 @@ def test_policy_spec_matches_reference():
         assert W * in_dim + W + W * W + W + W + 1 == ref["n_critic"]
 
 
-def _gpu_collect(env_id, cfg, n, T, windows, shaping, precision, key, a, c):
+def _gpu_collect(env_id, cfg, n, T, windows, shaping, precision, key, a, c, centralized=False):
     import paper_2311_10090_b200 as m
     from paper_2311_10090_b200.rollout import IppoRollout
     v = m.VectorEnv(m.make_env(env_id, cfg), n, device=0)
-    ro = IppoRollout(v, T, precision=precision)
+    ro = IppoRollout(v, T, precision=precision, centralized=centralized)
     ro.set_params(a, c)
     ro.begin(key)
     for w in range(windows):
@@ -174,3 +174,48 @@ def test_mappo_rollout_matches_reference_collector(env_id, cfg, n, T):
     for f in ("value", "adv", "vtarg"):
         err = np.abs(got[f].astype(np.float64) - ref[f])
         assert np.all(err <= 2e-6 + 2e-5 * np.abs(ref[f])), (f, err.max())
+
+
+# MAPPO on the tensor cores: the critic's layer 1 reads world_state rows of
+# widths 54 (MPE spread), 109 (SMAX 3m) and 181 (2s3z) from its own X tile
+@pytest.mark.gpu
+@pytest.mark.parametrize("env_id,cfg,n", [("MPE_simple_spread_v3", {}, 700), ("SMAX_5m_vs_6m", THREE_M, 300),
+                                          ("SMAX_2s3z", {}, 131)])
+def test_bf16_mappo_rollout_agrees_with_fp32(env_id, cfg, n):
+    """centralized=True with precision bf16: the critic_in rows equal the
+    fp32 path's (and the reference's) exactly, values / log-probs within the
+    bf16 tolerances, >= 97% identical actions at step 0, a valid rollout."""
+    _need_ref()
+    key = O.key_from_seed(23)
+    a, c = O.ref_ppo_init(env_id, cfg, O.fold_in(key, 10), centralized=True)
+    T = 6
+    f32 = _gpu_collect(env_id, cfg, n, T, 1, 0.0, "fp32", key, a, c, centralized=True)
+    b16 = _gpu_collect(env_id, cfg, n, T, 1, 0.0, "bf16", key, a, c, centralized=True)
+    assert np.array_equal(f32["obs"][0], b16["obs"][0])
+    assert np.array_equal(f32["critic_in"][0], b16["critic_in"][0])
+    assert np.allclose(b16["value"][0], f32["value"][0], rtol=0.05, atol=0.03)
+    assert np.allclose(b16["logp"][0], f32["logp"][0], rtol=0.02, atol=0.02)
+    assert (b16["actions"][0] == f32["actions"][0]).mean() >= 0.97
+    act = b16["actions"]
+    assert np.take_along_axis(b16["legal"], act[..., None].astype(np.int64), -1).all()
+    assert np.array_equal(b16["vtarg"], b16["adv"] + b16["value"])
+    ref = O.ref_collect(env_id, cfg, n, 1, key, a, c, centralized=True)
+    if env_id.startswith("MPE"):
+        assert np.allclose(b16["critic_in"][0], ref["critic_in"][0], rtol=1e-5, atol=1e-6)
+    else:
+        assert np.array_equal(b16["critic_in"][0], ref["critic_in"][0])
+
+
+@pytest.mark.gpu
+def test_bf16_mappo_training_runs():
+    """train_mappo with the bf16 tcgen05 collector (the update stays on the
+    fp32 kernels for centralized critics): finite losses, counts as fp32."""
+    _need_ref()
+    import paper_2311_10090_b200 as m
+    from paper_2311_10090_b200.ppo import train_mappo
+    cfg = {"total_timesteps": 256 * 8 * 2, "n_envs": 256, "n_rollout_steps": 8}
+    key = O.key_from_seed(3)
+    r16 = train_mappo(m.make_env("MPE_simple_spread_v3", {}), cfg, key, precision="bf16").metrics.as_array()
+    r32 = train_mappo(m.make_env("MPE_simple_spread_v3", {}), cfg, key, precision="fp32").metrics.as_array()
+    assert np.isfinite(r16).all()
+    assert np.array_equal(r16[:, [0, 1, 3]], r32[:, [0, 1, 3]])
