@@ -510,7 +510,7 @@ def cpu_baseline_both(env_id, cfg, A):
 def cpu_sample_size(env_id, cfg):
     """(envs, steps) of a bounded CPU sample of the workload: ~10-30 s for the
     cpu_baseline leg; the envs cap also bounds one reference-arm step (~1 s)."""
-    return {"MPE_simple_spread_v3": (1024, 200), "SMAX_5m_vs_6m": (65536, 5), "SMAX_2s3z": (65536, 5),
+    return {"MPE_simple_spread_v3": (1024, 1000), "SMAX_5m_vs_6m": (65536, 40), "SMAX_2s3z": (65536, 5),
             "SMAX_27m_vs_30m": (4096, 4), "overcooked_cramped_room_v0": (65536, 5)}.get(env_id, (1024, 10))
 
 
