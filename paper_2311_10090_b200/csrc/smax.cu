@@ -302,8 +302,10 @@ template <int G, int UPL, int CAP, int HT, bool FU>
 __device__ __forceinline__ void separate(const Params& P, EnvSm<CAP, HT, FU>& e, const Grp<G>& g, const LanePairs<G>& lp,
                                          bool fixpoint) {
   unsigned long long alive = 0;
+  bool check = true;  // a pair over the tolerance overlaps: after a failed fixpoint test the next
+                      // pass is known not to be a no-op, so its pre-check is skipped
   for (int pass = 0; pass < (fixpoint ? 256 : 1); ++pass) {
-    if (!g.any(lane_pairs_overlap<G>(P, e, lp, g.gl))) break;
+    if (check && !g.any(lane_pairs_overlap<G>(P, e, lp, g.gl))) break;
     if (pass == 0) {  // health is constant during separation
       bool al[UPL];
 #pragma unroll
@@ -313,6 +315,9 @@ __device__ __forceinline__ void separate(const Params& P, EnvSm<CAP, HT, FU>& e,
     separation_pass<G, UPL>(P, e, g, alive);
     if (!fixpoint) break;
     if (g.all(lane_pairs_within_tol<G>(P, e, lp, g.gl))) break;
+#ifndef MARL_SEP_ALWAYS_CHECK  // A/B knob (development builds, MARL_NVCC_EXTRA)
+    check = false;
+#endif
   }
 }
 
