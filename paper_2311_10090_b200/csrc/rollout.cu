@@ -209,7 +209,11 @@ constexpr int kTcMaxKx = 192;
 
 __host__ __device__ inline uint32_t up(uint32_t v, uint32_t a) { return (v + a - 1) / a * a; }
 
-__host__ __device__ inline int tc_kx(int in_dim) { return in_dim <= 32 ? 32 : (in_dim + 15) / 16 * 16; }
+// K of layer 1: 32 for small rows, round16 up to kTcMaxKx, beyond that (the
+// wide-row kernel, K-chunked) round64 -- the W1 image is then chunk-major.
+__host__ __device__ inline int tc_kx(int in_dim) {
+  return in_dim <= 32 ? 32 : in_dim <= 192 ? (in_dim + 15) / 16 * 16 : (in_dim + 63) / 64 * 64;
+}
 
 // mode 3: two staged tiles + staged buffer rows; 2: two tiles; 1: one tile; 0: none
 __host__ __device__ inline int tc_kc(int critic_in) { return critic_in > 0 ? (critic_in + 15) / 16 * 16 : 0; }
@@ -625,6 +629,247 @@ __global__ void __launch_bounds__(kSplit * kTcRows) policy_tc_kernel(PolicyNetBf
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols) : "memory");
 }
 
+// ---------------------------------------------------------------- wide rows
+// IPPO inputs wider than kTcMaxKx (Overcooked: 520-wide observation rows):
+// layer 1 runs K-chunked.  W1's image is chunk-major ([KX/64][128 x 64]
+// canonical tiles); per 64-column chunk one TMA bulk load brings the W1 tile
+// (mbarrier expect-tx) while the 256 threads build the X chunk straight from
+// the observation rows in L2 (two threads per row, 32 columns each, the
+// buffer's input row written on the way), and one thread issues the chunk's
+// four MMAs into the same TMEM accumulators; W1 and X tiles are double
+// buffered across chunks (and tiles) and a buffer is refilled only after the
+// chunk two back has been committed.  Layers 2-3, sampling and the buffer
+// writes are the staged kernel's.
+struct WideLayout {
+  uint32_t wbuf[2], xbuf[2], w2a, w2c, w3a, w3c, ha, hc, legal, resets, active, bias, bar, bar_w[2], bar_c[2],
+      tmem_slot, total;
+};
+
+__host__ __device__ inline WideLayout wide_layout(int n_act) {
+  WideLayout L{};
+  uint32_t o = 0;
+  auto take = [&o](uint32_t bytes, uint32_t align) {
+    o = up(o, align);
+    const uint32_t at = o;
+    o += bytes;
+    return at;
+  };
+  for (int q = 0; q < 2; ++q) L.wbuf[q] = take(128 * 64 * 2, 1024);
+  for (int q = 0; q < 2; ++q) L.xbuf[q] = take(kTcRows * 64 * 2, 1024);
+  L.w2a = take(64 * 64 * 2, 128);
+  L.w2c = take(64 * 64 * 2, 128);
+  L.w3a = take(16 * 64 * 2, 128);
+  L.w3c = take(16 * 64 * 2, 128);
+  L.ha = take(kTcRows * 64 * 2, 128);
+  L.hc = take(kTcRows * 64 * 2, 128);
+  L.legal = take(uint32_t(kTcRows * n_act), 16);
+  L.resets = take(kTcRows, 16);
+  L.active = take(kTcRows * 4, 16);
+  L.bias = take((4 * 64 + 2 * 16) * 4, 16);
+  L.bar = take(8, 8);
+  for (int q = 0; q < 2; ++q) L.bar_w[q] = take(8, 8);
+  for (int q = 0; q < 2; ++q) L.bar_c[q] = take(8, 8);
+  L.tmem_slot = take(4, 4);
+  L.total = up(o, 128);
+  return L;
+}
+
+__global__ void __launch_bounds__(kSplit * kTcRows, 1) policy_tc_wide_kernel(PolicyNetBf16 nb, int in_dim, int n_act,
+                                                                            PolicyStep s, RolloutBufs b) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  const WideLayout L = wide_layout(n_act);
+  uint8_t* base = smem_raw;
+  uint8_t *w2a = base + L.w2a, *w2c = base + L.w2c, *w3a = base + L.w3a, *w3c = base + L.w3c, *ha = base + L.ha,
+          *hc = base + L.hc;
+  uint8_t* wbuf[2] = {base + L.wbuf[0], base + L.wbuf[1]};
+  uint8_t* xbuf[2] = {base + L.xbuf[0], base + L.xbuf[1]};
+  uint8_t* s_legal = base + L.legal;
+  uint8_t* s_resets = base + L.resets;
+  float* s_active = reinterpret_cast<float*>(base + L.active);
+  float* s_bias = reinterpret_cast<float*>(base + L.bias);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(base + L.bar);
+  uint64_t* bar_w[2] = {reinterpret_cast<uint64_t*>(base + L.bar_w[0]), reinterpret_cast<uint64_t*>(base + L.bar_w[1])};
+  uint64_t* bar_c[2] = {reinterpret_cast<uint64_t*>(base + L.bar_c[0]), reinterpret_cast<uint64_t*>(base + L.bar_c[1])};
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(base + L.tmem_slot);
+  const int tid = threadIdx.x & (kTcRows - 1), part = threadIdx.x >> 7, warp = threadIdx.x >> 5;
+  const int64_t n_tiles = (s.R + kTcRows - 1) / kTcRows;
+  const int D = s.D, AA = s.A, KX = tc_kx(in_dim), NC = KX / 64;
+
+  if (threadIdx.x == 0) {
+    for (uint64_t* m : {bar, bar_w[0], bar_w[1], bar_c[0], bar_c[1]})
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(m)) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(kTmemCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  {
+    const uint4* src[4] = {reinterpret_cast<const uint4*>(nb.a2), reinterpret_cast<const uint4*>(nb.c2),
+                           reinterpret_cast<const uint4*>(nb.h3), reinterpret_cast<const uint4*>(nb.hc3)};
+    uint4* dst[4] = {reinterpret_cast<uint4*>(w2a), reinterpret_cast<uint4*>(w2c), reinterpret_cast<uint4*>(w3a),
+                     reinterpret_cast<uint4*>(w3c)};
+    const int n16[4] = {64 * 64 * 2 / 16, 64 * 64 * 2 / 16, 16 * 64 * 2 / 16, 16 * 64 * 2 / 16};
+    for (int m = 0; m < 4; ++m)
+      for (int q = threadIdx.x; q < n16[m]; q += blockDim.x) dst[m][q] = __ldg(src[m] + q);
+    for (int q = threadIdx.x; q < 4 * 64 + 2 * 16; q += blockDim.x) s_bias[q] = __ldg(nb.bias + q);
+  }
+  fence_proxy_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t lane_base = uint32_t((warp & 3) * 32) << 16;
+  const bool act_mode = !s.bootstrap;
+  uint32_t phase = 0;
+  int64_t cc = 0;  // chunks issued by this CTA (buffer cc & 1, its (cc >> 1)-th use)
+
+  for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+    const int64_t r0 = tile * kTcRows, r = r0 + tid;
+    const int rows = int(min64(kTcRows, s.R - r0));
+    const bool live = tid < rows;
+    const size_t slot0 = size_t(s.t) * size_t(s.R) + size_t(r0);
+    const int64_t e = r < 0x7fffffff ? int64_t(uint32_t(r) / uint32_t(AA)) : r / AA;
+    const int a = int(r - e * AA);
+    const float* orow = s.env_obs + size_t(r) * size_t(D);
+    float* brow = b.obs + (slot0 + size_t(tid)) * size_t(in_dim);
+    if (live && act_mode && part == 0) {  // write_legal / agent_active (team.cpp:35-42)
+      s_resets[tid] = s.prev_finished ? s.prev_finished[e] : uint8_t(1);
+      uint8_t* lg = s_legal + tid * n_act;
+      if (s.legal_ready) {
+        const uint8_t* gl = b.legal + (slot0 + size_t(tid)) * n_act;
+        for (int q = 0; q < n_act; ++q) lg[q] = gl[q];
+      } else {
+        const int na = s.agent_actions[a];
+        for (int q = 0; q < n_act; ++q) lg[q] = q < na ? 1 : 0;
+      }
+      s_active[tid] = (s.family == 1) ? (lg[0] ? 1.0f : 0.0f) : 1.0f;
+    }
+    const double u_row = (part == 0 && live && act_mode) ? row_uniform(s, r) : 0.0;  // part 0 samples
+    // ---- layer 1, K-chunked
+    for (int c = 0; c < NC; ++c, ++cc) {
+      const int bs = int(cc & 1);
+      // the MMAs of chunk cc - 2 read this buffer pair
+      if (cc >= 2) mbar_wait(bar_c[bs], uint32_t((cc - 2) >> 1) & 1u);
+      if (threadIdx.x == 0)
+        bulk_load_g2s(wbuf[bs], nb.a1 + size_t(c) * (128 * 64), 128 * 64 * 2, bar_w[bs]);
+      const int k0 = 64 * c + 32 * part;
+      float x[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const int k = k0 + j;
+        x[j] = (live && k < D) ? __ldg(orow + k) : 0.0f;
+        if (live && AA > 1 && k == D + a) x[j] = 1.0f;
+      }
+      if (live && act_mode) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+          if (k0 + j < in_dim) brow[k0 + j] = x[j];
+      }
+#pragma unroll
+      for (int j = 0; j < 32; j += 8) put8(xbuf[bs], 64, tid, 32 * part + j, x + j);
+      fence_proxy_async_smem();
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        mbar_wait(bar_w[bs], uint32_t(cc >> 1) & 1u);
+        tc_fence_after();
+        const uint32_t id = idesc_bf16(128, 128);
+        for (int k = 0; k < 64; k += 16)
+          umma_bf16(tmem + 0, umma_desc(xbuf[bs], 64, k), umma_desc(wbuf[bs], 64, k), id, (c > 0 || k > 0) ? 1u : 0u);
+        umma_commit(bar_c[bs]);
+      }
+    }
+    if (act_mode) {  // legal rows (when the kernel built them), resets, active
+      fence_proxy_async_smem();
+      __syncthreads();
+      if (!s.legal_ready) tile_put(b.legal + slot0 * n_act, s_legal, size_t(rows) * n_act);
+      if (threadIdx.x == 0) bulk_commit();
+      if (live && part == 0) {
+        b.resets[slot0 + tid] = s_resets[tid];
+        b.active[slot0 + tid] = s_active[tid];
+      }
+    }
+    mbar_wait(bar_c[int((cc - 1) & 1)], uint32_t((cc - 1) >> 1) & 1u);  // the tile's last chunk: all of layer 1
+    tc_fence_after();
+    // ---- epilogue 1 / layer 2 / epilogue 2 / heads: as the staged kernel
+#pragma unroll 1
+    for (int cl = (128 / kSplit) * part; cl < (128 / kSplit) * (part + 1); cl += 32) {
+      float v[32];
+      tmem_ld32(tmem + lane_base + uint32_t(cl), v);
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] = tanh_fast(v[i] + s_bias[cl + i]);
+      uint8_t* dsth = cl < 64 ? ha : hc;
+      put16(dsth, 64, tid, cl & 63, v);
+      put16(dsth, 64, tid, (cl & 63) + 16, v + 16);
+    }
+    tc_fence_before();
+    fence_proxy_async_smem();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      tc_fence_after();
+      const uint32_t id = idesc_bf16(128, 64);
+      for (int k = 0; k < 64; k += 16) umma_bf16(tmem + 0, umma_desc(ha, 64, k), umma_desc(w2a, 64, k), id, k > 0);
+      for (int k = 0; k < 64; k += 16) umma_bf16(tmem + 64, umma_desc(hc, 64, k), umma_desc(w2c, 64, k), id, k > 0);
+      umma_commit(bar);
+    }
+    mbar_wait(bar, phase);
+    phase ^= 1;
+    tc_fence_after();
+#pragma unroll 1
+    for (int cl = (128 / kSplit) * part; cl < (128 / kSplit) * (part + 1); cl += 32) {
+      float v[32];
+      tmem_ld32(tmem + lane_base + uint32_t(cl), v);
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] = tanh_fast(v[i] + s_bias[128 + cl + i]);
+      uint8_t* dsth = cl < 64 ? ha : hc;
+      put16(dsth, 64, tid, cl & 63, v);
+      put16(dsth, 64, tid, (cl & 63) + 16, v + 16);
+    }
+    tc_fence_before();
+    fence_proxy_async_smem();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      tc_fence_after();
+      const uint32_t id = idesc_bf16(128, 16);
+      for (int k = 0; k < 64; k += 16) umma_bf16(tmem + 0, umma_desc(ha, 64, k), umma_desc(w3a, 64, k), id, k > 0);
+      for (int k = 0; k < 64; k += 16) umma_bf16(tmem + 16, umma_desc(hc, 64, k), umma_desc(w3c, 64, k), id, k > 0);
+      umma_commit(bar);
+    }
+    mbar_wait(bar, phase);
+    phase ^= 1;
+    tc_fence_after();
+    {
+      float hv[16];
+      tmem_ld16(tmem + lane_base + uint32_t(16 * part), hv);
+      tc_fence_before();
+      if (part == 1) {
+        const float value = hv[0] + s_bias[256 + 16];
+        if (live) {
+          if (act_mode) b.value[slot0 + tid] = value;
+          else b.last_value[r] = value;
+        }
+      } else if (act_mode && live) {
+        float logits[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) logits[j] = hv[j] + s_bias[256 + j];
+        int pick;
+        float lp;
+        sample_row_n<16>(u_row, logits, s_legal + tid * n_act, n_act, &pick, &lp);
+        b.actions[slot0 + tid] = pick;
+        b.logp[slot0 + tid] = lp;
+      }
+    }
+    if (threadIdx.x == 0) bulk_wait_read<0>();  // the legal tile has been read out before it is rebuilt
+    __syncthreads();  // TMEM columns and hidden tiles are reused by the next tile
+  }
+  if (threadIdx.x == 0) bulk_wait<0>();
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols) : "memory");
+}
+
 // fp32 parameters -> canonical bf16 operand images + bias block.
 __global__ void pack_bf16_kernel(PolicyNet n, uint16_t* img, float* bias) {
   const int in = n.in_dim, NA = n.n_act, KX = tc_kx(in);
@@ -647,7 +892,10 @@ __global__ void pack_bf16_kernel(PolicyNet n, uint16_t* img, float* bias) {
       const __nv_bfloat16 hi = __float2bfloat16_rn(bb);
       v = k == 30 ? bb : bb - __bfloat162float(hi);
     }
-    a1[canon_off(row, k, KX) / 2] = bf(v);
+    if (KX > kTcMaxKx)  // wide rows: [chunk of 64 K][128 rows x 64] canonical tiles
+      a1[(k / 64) * (128 * 64) + canon_off(row, k % 64, 64) / 2] = bf(v);
+    else
+      a1[canon_off(row, k, KX) / 2] = bf(v);
   }
   if (n.centralized) {
     const int CI = n.critic_in, KC = tc_kc(CI);
@@ -683,6 +931,8 @@ __global__ void pack_bf16_kernel(PolicyNet n, uint16_t* img, float* bias) {
 int rollout_tc_kx(int in_dim) { return tc_kx(in_dim); }
 
 bool rollout_policy_bf16_supported(int in_dim, int n_act, int width, int critic_in) {
+  if (in_dim > kTcMaxKx)  // wide rows: the K-chunked kernel (IPPO critics)
+    return critic_in == 0 && n_act <= 16 && width == 64 && wide_layout(n_act).total <= kTcSmemMax;
   // D <= in_dim: the layout without staged tiles bounds every mode
   return in_dim >= 1 && tc_kx(in_dim) <= kTcMaxKx && tc_kc(critic_in) <= kTcMaxKx && n_act <= 16 && width == 64 &&
          tc_layout_mode(in_dim, in_dim, n_act, 0, critic_in).total <= kTcSmemMax;
@@ -700,6 +950,15 @@ void rollout_policy_bf16(const PolicyNet& net, const PolicyNetBf16& nb, const Po
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  if (net.in_dim > kTcMaxKx) {  // wide rows: K-chunked layer 1, one CTA per SM
+    const size_t smw = wide_layout(net.n_act).total;
+    cudaFuncSetAttribute(policy_tc_wide_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smw));
+    const int64_t tiles = (s.R + kTcRows - 1) / kTcRows;
+    const int64_t grid = cap_grid(std::min<int64_t>(tiles, int64_t(sms)));
+    policy_tc_wide_kernel<<<unsigned(grid), kSplit * kTcRows, smw, st>>>(nb, net.in_dim, net.n_act, s, b);
+    ++g_launches;
+    return;
   }
   const bool cent = s.ws != nullptr;
   const int ci = cent ? net.critic_in : 0;

@@ -100,7 +100,10 @@ def test_fp32_rollout_matches_reference_collector(env_id, cfg, n, T, windows, sh
 # buffer rows, two tiles, one tile or none) and layer-1 K of 32 .. 192
 @pytest.mark.gpu
 @pytest.mark.parametrize("env_id,cfg,n", [("MPE_simple_spread_v3", {}, 512), ("SMAX_5m_vs_6m", THREE_M, 300),
-                                          ("SMAX_2s3z", {}, 131), ("SMAX_5m_vs_6m", {}, 77)])
+                                          ("SMAX_2s3z", {}, 131), ("SMAX_5m_vs_6m", {}, 77),
+                                          # wide rows (K-chunked layer 1): Overcooked's 520 + 2 columns
+                                          ("overcooked_cramped_room_v0", {"max_steps": 20}, 300),
+                                          ("overcooked_coordination_ring_v0", {"max_steps": 20}, 97)])
 def test_bf16_tensor_core_rollout_agrees_with_fp32(env_id, cfg, n):
     from paper_2311_10090_b200._native import lib
     _need_ref()
