@@ -1,7 +1,7 @@
 """Benchmark of the batched env-step hot path (BASELINE.json metric:
 agent-steps/s at 1/2/4/8 B200 vs the CPU reference; % of HBM roofline).
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload smax3m|mpe|overcooked|smax2s3z|smax27m]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload smax3m|mpe|mpe_large|overcooked|smax2s3z|smax27m|ippo|ippo_oc|ppo|ppo_smax|ppo_rnn]
   python bench.py --impl reference ...     # the reference's own CPU path, host cores
 
 A "step" is one fused VectorEnv step over the whole synthetic batch with the
@@ -37,6 +37,8 @@ WORKLOADS = {
     # configs[4]: one "step" is one Collector::collect window of IPPO_T env steps
     "ippo": ("MPE_simple_spread_v3", {}, 1 << 20, "IPPO rollout on MPE simple_spread, 2^20 envs x 128 steps, "
              "bf16 actor+critic on tcgen05, configs[4]"),
+    "ippo_oc": ("overcooked_cramped_room_v0", {}, 1 << 16, "IPPO rollout on Overcooked cramped_room, 2^16 envs x "
+                "128 steps, bf16 tcgen05 wide-row policy (520 + 2 input columns, K-chunked layer 1)"),
     # one "step" is one train_ippo update (collect + update_epochs x n_minibatches)
     "ppo": ("MPE_simple_spread_v3", {}, 1 << 16, "IPPO training update on MPE simple_spread (collect 128 steps + "
             "5 epochs x 2 minibatches of PPO), PpoConfig defaults"),
@@ -46,6 +48,7 @@ WORKLOADS = {
                  "2 minibatches of PPO; 95-wide observations), PpoConfig defaults"),
 }
 PPO_WORKLOADS = ("ppo", "ppo_rnn", "ppo_smax")
+IPPO_WORKLOADS = ("ippo", "ippo_oc")
 FUSED_PROBE = ("mpe",)  # timed as one fused multi-step probe launch (marl_venv_probe_steps)
 IPPO_T = 128
 L2_FLUSH_BYTES = 512 << 20  # > 4x the 126 MB L2; its ~80 us also covers the host's enqueue of the next step
@@ -60,7 +63,7 @@ def workload_config(workload, world, n_per_gpu=None):
               "overcooked_cramped_room_v0": 2}[env_id]
     c = {"workload": label, "env_id": env_id, "env_config": cfg, "n_envs_per_gpu": n, "global_envs": n * world,
          "agents": agents}
-    if workload == "ippo":
+    if workload in IPPO_WORKLOADS:
         c["rollout_steps_per_window"] = IPPO_T
     if workload in PPO_WORKLOADS:
         c.update({"rollout_steps": IPPO_T, "update_epochs": 5, "n_minibatches": 2})
@@ -287,7 +290,9 @@ def run_gpu_ippo(args, rank, world, local_rank):
     bpe = ippo_bytes_per_env_step(env, ro.spec.in_dim, ro.spec.n_actions)
     achieved = n_per_gpu * T * bpe / mean_win_s / 1e9
     peak, peak_src = measured_peak()
-    flop_row = 2 * (128 * 32 + 2 * 64 * 64 + 2 * 16 * 64)  # MMA FLOPs per row as issued (padded operands)
+    in_ = ro.spec.in_dim
+    kx = 32 if in_ <= 32 else ((in_ + 15) // 16 * 16 if in_ <= 192 else (in_ + 63) // 64 * 64)
+    flop_row = 2 * (128 * kx + 2 * 64 * 64 + 2 * 16 * 64)  # MMA FLOPs per row as issued (padded operands)
     tflops = n_per_gpu * A * (T + 1) * flop_row / mean_win_s / 1e12
 
     # end to end through the public API: parameters H2D from pinned memory,
@@ -543,7 +548,7 @@ def run_reference_arm(args, rank, world):
                 "e2e": {"value": val, "unit": "agent-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(line))
         return
-    if args.workload == "ippo":  # one step = one collect window of a bounded env sample
+    if args.workload in IPPO_WORKLOADS:  # one step = one collect window of a bounded env sample
         sys.path.insert(0, os.path.join(ROOT, "oracle"))
         import oracle as O
         n_cpu, t_cpu = 256, IPPO_T
@@ -552,7 +557,7 @@ def run_reference_arm(args, rank, world):
         t0 = time.perf_counter()
         O.ref_collect(env_id, cfg, n_cpu, t_cpu, O.key_from_seed(0), ka, kc, n_windows=max(1, args.steps))
         sec = time.perf_counter() - t0
-        A = 3
+        A = workload_config(args.workload, 1)["agents"]
         val = n_cpu * A * t_cpu * max(1, args.steps) / sec
         line = {"impl": "reference", "metric": "agent-steps/sec (env-steps/sec x agents)", "value": val,
                 "unit": "agent-steps/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -773,7 +778,7 @@ def main():
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl")
     try:
-        if args.workload == "ippo":
+        if args.workload in IPPO_WORKLOADS:
             run_gpu_ippo(args, rank, world, local_rank)
         elif args.workload in PPO_WORKLOADS:
             run_gpu_ppo(args, rank, world, local_rank)

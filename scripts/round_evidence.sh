@@ -5,7 +5,7 @@ TAG=${1:-r01}
 mkdir -p gpurun_out
 timeout 900 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu_${TAG}.log 2>&1; tail -2 gpurun_out/pytest_gpu_${TAG}.log
 : > gpurun_out/bench_${TAG}.jsonl
-for w in smax3m mpe mpe_large overcooked smax2s3z smax27m ippo; do
+for w in smax3m mpe mpe_large overcooked smax2s3z smax27m ippo ippo_oc; do
   timeout 600 python bench.py --workload $w --steps 30 --warmup 5 2>/dev/null | grep '^{' >> gpurun_out/bench_${TAG}.jsonl
 done
 timeout 600 python bench.py --workload smax27m --n-envs 16384 --steps 10 --warmup 3 2>/dev/null | grep '^{' >> gpurun_out/bench_${TAG}.jsonl
@@ -14,6 +14,7 @@ timeout 600 python bench.py --workload ppo --steps 10 --warmup 3 2>/dev/null | g
 timeout 600 python bench.py --workload ppo_rnn --steps 3 --warmup 3 2>/dev/null | grep '^{' >> gpurun_out/bench_${TAG}.jsonl
 timeout 600 python bench.py --workload ppo_smax --steps 10 --warmup 3 2>/dev/null | grep '^{' >> gpurun_out/bench_${TAG}.jsonl
 timeout 300 python bench.py --impl reference --workload smax3m --steps 3 --warmup 1 2>/dev/null | grep '^{' >> gpurun_out/bench_${TAG}.jsonl
+timeout 300 python bench.py --impl reference --workload ippo_oc --steps 1 --warmup 1 2>/dev/null | grep '^{' >> gpurun_out/bench_${TAG}.jsonl
 timeout 300 python bench.py --impl reference --workload ppo --steps 2 --warmup 3 2>/dev/null | grep '^{' >> gpurun_out/bench_${TAG}.jsonl
 timeout 300 python bench.py --impl reference --workload ppo_rnn --steps 1 --warmup 3 2>/dev/null | grep '^{' >> gpurun_out/bench_${TAG}.jsonl
 timeout 300 python bench.py --impl reference --workload ppo_smax --steps 1 --warmup 3 2>/dev/null | grep '^{' >> gpurun_out/bench_${TAG}.jsonl
