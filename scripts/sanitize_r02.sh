@@ -42,6 +42,18 @@ if what in ("smax", "all"):
             v.step_random(O.fold_in(key, t))
         v.sync()
         print("smax", env_id, v.episode_stats())
+if what in ("policy", "all"):  # tcgen05 rollout policies: wide rows (Overcooked), MAPPO critics, folded MPE
+    from paper_2311_10090_b200.rollout import IppoRollout, orthogonal_init
+    for env_id, cent in [("overcooked_cramped_room_v0", False), ("MPE_simple_spread_v3", True),
+                         ("MPE_simple_spread_v3", False)]:
+        v = m.VectorEnv(env_id, 300)
+        ro = IppoRollout(v, 4, precision="bf16", centralized=cent)
+        a, c = orthogonal_init(0, ro.spec)
+        ro.set_params(a, c)
+        ro.begin(O.key_from_seed(1))
+        out = ro.collect()
+        torch.cuda.synchronize()
+        print("policy", env_id, cent, float(out["value"].sum()))
 if what in ("rnn", "all"):
     from paper_2311_10090_b200.ppo import PpoTrainer
     n, T = 256, 8
@@ -50,11 +62,11 @@ if what in ("rnn", "all"):
     r = tr.train(O.key_from_seed(0))
     print("rnn", r.metrics.as_array()[-1][:8])
 PY
-for what in probe gemm smax rnn; do
+for what in probe gemm smax rnn policy; do
   timeout 900 $CS --tool memcheck --leak-check no --error-exitcode 9 python /tmp/san_r02.py $what > gpurun_out/san_r02_memcheck_$what.log 2>&1
   echo "memcheck $what rc=$?"; grep -E "ERROR SUMMARY" gpurun_out/san_r02_memcheck_$what.log | head -2
 done
-for what in probe gemm; do
+for what in probe gemm policy; do
   timeout 900 $CS --tool racecheck --error-exitcode 9 python /tmp/san_r02.py $what > gpurun_out/san_r02_racecheck_$what.log 2>&1
   echo "racecheck $what rc=$?"; grep -E "RACECHECK SUMMARY|ERROR SUMMARY|hazard" gpurun_out/san_r02_racecheck_$what.log | head -3
   timeout 900 $CS --tool synccheck --error-exitcode 9 python /tmp/san_r02.py $what > gpurun_out/san_r02_synccheck_$what.log 2>&1
