@@ -1,7 +1,7 @@
 """Benchmark of the batched env-step hot path (BASELINE.json metric:
 agent-steps/s at 1/2/4/8 B200 vs the CPU reference; % of HBM roofline).
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload smax3m|mpe|mpe_large|overcooked|smax2s3z|smax27m|ippo|ippo_oc|ppo|ppo_smax|ppo_rnn]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload smax3m|mpe|mpe_large|overcooked|smax2s3z|smax27m|ippo|ippo_oc|ppo|ppo_smax|ppo_oc|ppo_rnn]
   python bench.py --impl reference ...     # the reference's own CPU path, host cores
 
 A "step" is one fused VectorEnv step over the whole synthetic batch with the
@@ -46,8 +46,11 @@ WORKLOADS = {
                 "(collect 128 steps + 5 epochs x 2 minibatches, BPTT), PpoConfig defaults + recurrent"),
     "ppo_smax": ("SMAX_5m_vs_6m", THREE_M, 1 << 14, "IPPO training update on SMAX 3m (collect 128 steps + 5 epochs x "
                  "2 minibatches of PPO; 95-wide observations), PpoConfig defaults"),
+    "ppo_oc": ("overcooked_cramped_room_v0", {}, 1 << 14, "IPPO training update on Overcooked cramped_room (collect "
+               "128 steps + 5 epochs x 2 minibatches of PPO; 520 + 2 wide observations, fp32-accurate GEMM-chain "
+               "update), PpoConfig defaults"),
 }
-PPO_WORKLOADS = ("ppo", "ppo_rnn", "ppo_smax")
+PPO_WORKLOADS = ("ppo", "ppo_rnn", "ppo_smax", "ppo_oc")
 IPPO_WORKLOADS = ("ippo", "ippo_oc")
 FUSED_PROBE = ("mpe",)  # timed as one fused multi-step probe launch (marl_venv_probe_steps)
 IPPO_T = 128
@@ -457,7 +460,9 @@ def run_gpu_ppo(args, rank, world, local_rank):
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": ("f32 recurrent policy + f32 BPTT update (3xTF32 tcgen05 GEMMs, fp32-accurate)" if recurrent else
-                  "bf16 rollout policy + bf16 tcgen05 PPO update (fp32 accumulate)") + " / f64 env", "data": "synthetic (key_from_seed(rank))",
+                  "bf16 rollout policy + bf16 tcgen05 PPO update (fp32 accumulate)" if tr.tensor_core_update else
+                  "bf16 rollout policy + f32 PPO update (3xTF32 tcgen05 GEMM chain, fp32-accurate)")
+        + " / f64 env", "data": "synthetic (key_from_seed(rank))",
         "config": workload_config(args.workload, world, n_envs),
         "run": {"batch_rows": T * R, "step": "one PPO update = collect + update",
                 "parallelism": f"dp{world}: env shards, update sums all-reduced over NCCL" if world > 1
@@ -469,7 +474,9 @@ def run_gpu_ppo(args, rank, world, local_rank):
                      "traffic": None, "peak_source": "MEASURED_PEAKS.json bf16_tflops (dense)",
                      "kernel": ("recurrent PPO update (3xTF32 tcgen05 GEMM per time step + gate kernels)" if recurrent
                                 else "PPO update phase (ppo_update_tc_kernel dominant: bf16 tcgen05 forward, input- "
-                                     "and weight-gradient GEMMs, fp32 TMEM accumulation)"),
+                                     "and weight-gradient GEMMs, fp32 TMEM accumulation)" if tr.tensor_core_update
+                                else "PPO update phase (wide rows: 3xTF32 tcgen05 GEMM chain, layer-1 product and "
+                                     "weight gradient dominant; 3 tf32 MMAs per product, counted once)"),
                      "flop_per_row_pass": fpr},
         "cpu_baseline": cpu,
         "e2e": {"value": world * n_envs * A * T * e2e_steps / sec, "unit": "agent-steps/s", "h2d_bytes_per_step": 0,

@@ -413,6 +413,25 @@ void ppo_branch_geometry(int in, int W, int out, int* TR, int* staged, size_t* s
 int ppo_branch_grid(int in, int W, int out, int64_t M);
 void ppo_branch(PpoBranchArgs a, bool actor, int grid, cudaStream_t s);
 void ppo_grad_reduce(const float* part, int nparts, int P, float* grad, cudaStream_t s);
+// out[m][0..in) = x[idx[m]][0..in), rows of out `ldo` floats apart (ff_minibatch's gather)
+void ppo_gather_rows(const float* x, const int32_t* idx, int64_t M, int in, float* out, int ldo, cudaStream_t s);
+// The wide-input fp32 update (ppo_wide.cu, ppo_host.cpp minibatch_grad_wide).
+struct WideStage {
+  const float *pa, *pc;  // the branches' parameters (nn::pack order)
+  int64_t Pa, Pc;
+  float *qa, *qc;  // their 16-byte aligned copies
+  int W, in_a, in_c, ldx;
+  float* w1s;   // [2W][ldx] stacked layer-1 matrices (null: not stacked)
+  float* bias;  // [4W] b1a | b1c | b2a | b2c
+};
+void wide_stage(const WideStage& s, cudaStream_t st);
+// y[m][c] = act(y[m][c] + b[c]) over [M][N]
+void wide_bias_act(float* y, int64_t M, int N, const float* b, int relu, cudaStream_t st);
+// d *= act'(h) in place (h null: unchanged), then column sums of d: columns
+// c < split to dst0[c], the rest to dst1[c - split]; part: wide_part_floats(M, N)
+void wide_grad_colsum(float* d, const float* h, int64_t M, int N, int relu, float* part, int split, float* dst0,
+                      float* dst1, cudaStream_t st);
+int64_t wide_part_floats(int64_t M, int N);
 void ppo_clip_adam(const PpoApplyArgs& a, cudaStream_t s);
 
 // ------------------------------------------------------------ common

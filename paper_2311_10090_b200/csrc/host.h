@@ -289,6 +289,18 @@ struct marl_ppo {
   int64_t rnn_chunk = 0;  // rows per BPTT chunk (caches sized for it)
   int rnn_blocks = 0;     // loss partial blocks of the last minibatch
   float *rnn_h = nullptr, *rnn_gx = nullptr, *rnn_gh = nullptr, *rnn_dh = nullptr, *rnn_ones = nullptr;
+  // wide-input fp32 update (ff_minibatch as a GEMM chain, minibatch_grad_wide):
+  // per branch the gathered rows, both hidden layers and the head's output and
+  // gradient, one [M][W] pair for the backward's layer gradients
+  bool wide = false;
+  float* wx[2] = {nullptr, nullptr};  // [M][ldx]: the actor's rows, the critic's (== wx[0] for IPPO)
+  int wldx[2] = {0, 0};
+  // [M][2W], actor columns then critic columns: hidden layers and their gradients
+  float *wh1 = nullptr, *wh2 = nullptr, *wd1 = nullptr, *wd2 = nullptr;
+  float *wy[2] = {nullptr, nullptr}, *wdy[2] = {nullptr, nullptr};  // head outputs / gradients [M][out]
+  float *wq[2] = {nullptr, nullptr};  // aligned parameter copies
+  float *w1s = nullptr, *wbias = nullptr, *wg1 = nullptr;  // stacked W1 [2W][ldx], biases [4W], dW1 [2W][in]
+  float* wpart = nullptr;  // column-sum partials
   ~marl_ppo();
 };
 

@@ -1153,6 +1153,36 @@ void ppo_branch(PpoBranchArgs a, bool actor, int grid, cudaStream_t s) {
     launch_branch<false>(a, grid, sm, s);
 }
 
+// one warp per row: 8-byte copies when every row start allows them (522-column
+// Overcooked rows are 8-byte aligned), 4-byte copies otherwise
+template <int V>
+__global__ void gather_rows_kernel(const float* __restrict__ x, const int32_t* __restrict__ idx, int64_t M, int in,
+                                   float* __restrict__ out, int ldo) {
+  const int64_t m = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  if (m >= M) return;
+  const int lane = threadIdx.x & 31;
+  const float* src = x + size_t(__ldg(idx + m)) * size_t(in);
+  float* dst = out + size_t(m) * size_t(ldo);
+  if constexpr (V == 2) {
+    for (int i = lane; i < in / 2; i += 32)
+      reinterpret_cast<float2*>(dst)[i] = __ldg(reinterpret_cast<const float2*>(src) + i);
+  } else {
+    for (int i = lane; i < in; i += 32) dst[i] = __ldg(src + i);
+  }
+}
+
+void ppo_gather_rows(const float* x, const int32_t* idx, int64_t M, int in, float* out, int ldo, cudaStream_t s) {
+  if (M <= 0) return;
+  const unsigned blocks = unsigned((M * 32 + 255) / 256);
+  const bool v2 = in % 2 == 0 && ldo % 2 == 0 && reinterpret_cast<uintptr_t>(x) % 8 == 0 &&
+                  reinterpret_cast<uintptr_t>(out) % 8 == 0;
+  if (v2)
+    gather_rows_kernel<2><<<blocks, 256, 0, s>>>(x, idx, M, in, out, ldo);
+  else
+    gather_rows_kernel<1><<<blocks, 256, 0, s>>>(x, idx, M, in, out, ldo);
+  ++g_launches;
+}
+
 void ppo_grad_reduce(const float* part, int nparts, int P, float* grad, cudaStream_t s) {
   grad_reduce_kernel<<<blocks_for(P, 256), 256, 0, s>>>(part, nparts, P, grad);
   ++g_launches;

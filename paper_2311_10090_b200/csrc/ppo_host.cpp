@@ -283,6 +283,110 @@ PpoBranchArgs branch_args(marl_ppo* p, bool actor, const int32_t* idx, int64_t M
   return a;
 }
 
+// Inputs at least this wide (Overcooked's 522 columns, MAPPO world_state rows
+// of Overcooked / 27m) run the fp32 update as a GEMM chain: the per-row
+// CUDA-core kernel spends most of its time on layer 1's dot products there.
+constexpr int kPpoWideIn = 256;
+
+// ff_minibatch (ppo.cpp:409-441) as a GEMM chain on the fp32-accurate 3xTF32
+// tensor-core kernels (gemm_tc.cu): per branch gather the rows, dense_forward
+// + act_inplace per layer (nn.hpp:108-115, 136-138), ppo_row_loss over the
+// minibatch (rnn_loss: the same per-row loss the recurrent path uses), then the
+// backward layer by layer with g.w = dy^T x and g.b = sum dy over all rows
+// (nn.hpp:124-126) straight into p->grad in nn::pack order.
+void minibatch_grad_wide(marl_ppo* p, const int32_t* idx, int64_t M) {
+  marl_rollout* r = p->ro;
+  cudaStream_t st = p->h->stream;
+  const int W = r->width, W2 = 2 * W, relu = r->relu;
+  const bool stack = !r->centralized;  // IPPO: both branches read the same rows
+  const int in[2] = {r->in_dim, r->critic_in}, out[2] = {r->n_act, 1};
+  p->rnn_blocks = rnn_loss_blocks(M);
+  WideStage sg{};
+  sg.pa = r->params;
+  sg.pc = r->params + r->n_actor;
+  sg.Pa = p->Pa;
+  sg.Pc = p->Pc;
+  sg.qa = p->wq[0];
+  sg.qc = p->wq[1];
+  sg.W = W;
+  sg.in_a = in[0];
+  sg.in_c = in[1];
+  sg.ldx = p->wldx[0];
+  sg.w1s = stack ? p->w1s : nullptr;
+  sg.bias = p->wbias;
+  wide_stage(sg, st);
+  struct Ff {  // one branch's layers in nn::pack order (aligned copy / gradient)
+    float *w1, *b1, *w2, *b2, *w3, *b3;
+  };
+  auto ff = [&](float* q, int br) {
+    Ff f;
+    f.w1 = q;
+    f.b1 = f.w1 + size_t(W) * in[br];
+    f.w2 = f.b1 + W;
+    f.b2 = f.w2 + W * W;
+    f.w3 = f.b2 + W;
+    f.b3 = f.w3 + out[br] * W;
+    return f;
+  };
+  const Ff q[2] = {ff(p->wq[0], 0), ff(p->wq[1], 1)};
+  const Ff g[2] = {ff(p->grad, 0), ff(p->grad + p->Pa, 1)};
+  float *h1 = p->wh1, *h2 = p->wh2, *d1 = p->wd1, *d2 = p->wd2;
+  if (M > 0) {  // forward with cache, both branches
+    for (int br = 0; br < (stack ? 1 : 2); ++br)
+      ppo_gather_rows(br == 0 ? r->b.obs : r->b.critic_in, idx, M, in[br], p->wx[br], p->wldx[br], st);
+    if (stack) {
+      gemm_nt(st, M, W2, in[0], p->wx[0], p->wldx[0], p->w1s, p->wldx[0], h1, W2, 0.0f);
+    } else {
+      for (int br = 0; br < 2; ++br)
+        gemm_nt(st, M, W, in[br], p->wx[br], p->wldx[br], q[br].w1, in[br], h1 + br * W, W2, 0.0f);
+    }
+    wide_bias_act(h1, M, W2, p->wbias, relu, st);
+    for (int br = 0; br < 2; ++br) gemm_nt(st, M, W, W, h1 + br * W, W2, q[br].w2, W, h2 + br * W, W2, 0.0f);
+    wide_bias_act(h2, M, W2, p->wbias + W2, relu, st);
+    for (int br = 0; br < 2; ++br) {
+      gemm_nt(st, M, out[br], W, h2 + br * W, W2, q[br].w3, W, p->wy[br], out[br], 0.0f);
+      rnn_bias_act(p->wy[br], M, out[br], q[br].b3, false, relu, st);
+    }
+  }
+  RnnSeqArgs la{};  // ppo_row_loss reads both branches' head outputs
+  la.n_act = r->n_act;
+  la.ca.y = p->wy[0];
+  la.ca.dy = p->wdy[0];
+  la.cc.y = p->wy[1];
+  la.cc.dy = p->wdy[1];
+  rnn_loss(la, idx, M, r->b, p->mbst, p->cfg.clip_eps, p->cfg.ent_coef, p->cfg.vf_coef, p->spart_a, p->spart_c,
+           p->flags + 1, st);
+  // backward: head, layer 2, layer 1; g.w = dy^T x over all rows, g.b = sum dy
+  for (int br = 0; br < 2; ++br) {
+    const float* dy = p->wdy[br];
+    wide_grad_colsum(p->wdy[br], nullptr, M, out[br], relu, p->wpart, out[br], g[br].b3, nullptr, st);
+    if (M == 0) continue;
+    gemm_tn(st, out[br], W, M, dy, out[br], h2 + br * W, W2, g[br].w3, 0.0f);
+    gemm_nn(st, M, W, out[br], dy, out[br], q[br].w3, W, d2 + br * W, W2, 0.0f);
+  }
+  wide_grad_colsum(d2, h2, M, W2, relu, p->wpart, W, g[0].b2, g[1].b2, st);
+  for (int br = 0; br < 2 && M > 0; ++br) {
+    gemm_tn(st, W, W, M, d2 + br * W, W2, h1 + br * W, W2, g[br].w2, 0.0f);
+    gemm_nn(st, M, W, W, d2 + br * W, W2, q[br].w2, W, d1 + br * W, W2, 0.0f);
+  }
+  wide_grad_colsum(d1, h1, M, W2, relu, p->wpart, W, g[0].b1, g[1].b1, st);
+  if (M == 0) {
+    for (int br = 0; br < 2; ++br)
+      for (float* w : {g[br].w1, g[br].w2, g[br].w3})
+        cuda_check(cudaMemsetAsync(w, 0, size_t(W) * size_t(w == g[br].w1 ? in[br] : w == g[br].w2 ? W : out[br]) * 4, st),
+                   "cudaMemsetAsync");
+  } else if (stack) {  // one dW1 product for both branches, then each branch's rows into place
+    gemm_tn(st, W2, in[0], M, d1, W2, p->wx[0], p->wldx[0], p->wg1, 0.0f);
+    for (int br = 0; br < 2; ++br)
+      cuda_check(cudaMemcpyAsync(g[br].w1, p->wg1 + size_t(br) * W * in[0], size_t(W) * in[0] * 4,
+                                 cudaMemcpyDeviceToDevice, st),
+                 "cudaMemcpyAsync");
+  } else {
+    for (int br = 0; br < 2; ++br)
+      gemm_tn(st, W, in[br], M, d1 + br * W, W2, p->wx[br], p->wldx[br], g[br].w1, 0.0f);
+  }
+}
+
 // ff_minibatch's gradient (ppo.cpp:409-441) into p->grad (actor | critic).
 // global: idx are slots of the GLOBAL rollout (t*R_global + r); a sharded
 // trainer keeps the ones it owns and all-reduces the sums.
@@ -325,16 +429,20 @@ void minibatch_grad(marl_ppo* p, const int32_t* idx, int64_t M, bool global = fa
     a.ent_coef = p->cfg.ent_coef;
     a.vf_coef = p->cfg.vf_coef;
     ppo_update_tc(a, p->grid_a, st);
+  } else if (p->wide) {
+    minibatch_grad_wide(p, idx, M);
   } else {
     ppo_branch(branch_args(p, true, idx, M), true, p->grid_a, st);
     ppo_branch(branch_args(p, false, idx, M), false, p->grid_c, st);
   }
-  ppo_grad_reduce(p->gpart_a, p->grid_a, p->Pa, p->grad, st);
-  ppo_grad_reduce(p->gpart_c, p->grid_c, p->Pc, p->grad + p->Pa, st);
+  if (!p->wide) {
+    ppo_grad_reduce(p->gpart_a, p->grid_a, p->Pa, p->grad, st);
+    ppo_grad_reduce(p->gpart_c, p->grid_c, p->Pc, p->grad + p->Pa, st);
+  }
   after_launch();
   if (p->hook) {  // the data-parallel exchange: gradient and loss sums over the ranks
-    ppo_stats_fold(p->spart_a, p->grid_a, st);
-    ppo_stats_fold(p->spart_c, p->grid_c, st);
+    ppo_stats_fold(p->spart_a, p->wide ? p->rnn_blocks : p->grid_a, st);
+    ppo_stats_fold(p->spart_c, p->wide ? p->rnn_blocks : p->grid_c, st);
     after_launch();
     allreduce(p, p->grad, p->P, MARL_DTYPE_F32);
     allreduce(p, p->spart_a, 6, MARL_DTYPE_F64);
@@ -518,8 +626,9 @@ void minibatch_apply(marl_ppo* p, double lr_u, double* metrics_slot) {
   a.P = p->P;
   a.actor_stats = p->spart_a;
   a.critic_stats = p->spart_c;
-  a.n_actor_parts = p->hook ? 1 : (p->recurrent ? p->rnn_blocks : p->grid_a);  // folded + all-reduced into row 0
-  a.n_critic_parts = p->hook ? 1 : (p->recurrent ? p->rnn_blocks : p->grid_c);
+  const bool by_rows = p->recurrent || p->wide;  // loss partials of rnn_loss's blocks
+  a.n_actor_parts = p->hook ? 1 : (by_rows ? p->rnn_blocks : p->grid_a);  // folded + all-reduced into row 0
+  a.n_critic_parts = p->hook ? 1 : (by_rows ? p->rnn_blocks : p->grid_c);
   a.st = p->mbst;
   a.vf_coef = p->cfg.vf_coef;
   a.ent_coef = p->cfg.ent_coef;
@@ -716,6 +825,9 @@ int marl_ppo_create(marl_venv* h, const char* ppo_config_json, int centralized, 
       p->grid_a = p->grid_c = int(std::min<int64_t>(int64_t(1) << 30, rnn_loss_blocks(rnn_Kc) * nchunks));
     } else if (p->tc) {
       p->grid_a = p->grid_c = ppo_tc_grid(p->per);
+    } else if (std::max(r->in_dim, r->critic_in) >= kPpoWideIn && !std::getenv("MARL_PPO_ROW_KERNEL")) {
+      p->wide = true;  // MARL_PPO_ROW_KERNEL=1 keeps the per-row kernels (A/B knob)
+      p->grid_a = p->grid_c = rnn_loss_blocks(p->per);
     } else {
       p->grid_a = ppo_branch_grid(r->in_dim, r->width, r->n_act, p->per);
       p->grid_c = ppo_branch_grid(r->critic_in, r->width, 1, p->per);
@@ -729,8 +841,27 @@ int marl_ppo_create(marl_venv* h, const char* ppo_config_json, int centralized, 
     ar.add(&p->snapshot, size_t(p->P));
     // per-CTA gradient partials of the feed-forward kernels (the recurrent path
     // accumulates straight into the gradient)
-    ar.add(&p->gpart_a, p->recurrent ? 1 : size_t(p->grid_a) * size_t(p->Pa));
-    ar.add(&p->gpart_c, p->recurrent ? 1 : size_t(p->grid_c) * size_t(p->Pc));
+    const bool no_parts = p->recurrent || p->wide;
+    ar.add(&p->gpart_a, no_parts ? 1 : size_t(p->grid_a) * size_t(p->Pa));
+    ar.add(&p->gpart_c, no_parts ? 1 : size_t(p->grid_c) * size_t(p->Pc));
+    if (p->wide) {
+      const size_t M = size_t(p->per), W = size_t(r->width);
+      for (int br = 0; br < 2; ++br) {
+        const int in = br == 0 ? r->in_dim : r->critic_in;
+        p->wldx[br] = (in + 3) / 4 * 4;  // 16-byte rows: four-float copies in the GEMMs' staging
+        if (br == 0 || centralized) ar.add(&p->wx[br], M * size_t(p->wldx[br]));
+        ar.add(&p->wy[br], M * size_t(br == 0 ? r->n_act : 1));
+        ar.add(&p->wdy[br], M * size_t(br == 0 ? r->n_act : 1));
+        ar.add(&p->wq[br], size_t(br == 0 ? p->Pa : p->Pc));
+      }
+      for (float** q : {&p->wh1, &p->wh2, &p->wd1, &p->wd2}) ar.add(q, M * 2 * W);
+      if (!centralized) {
+        ar.add(&p->w1s, 2 * W * size_t(p->wldx[0]));
+        ar.add(&p->wg1, 2 * W * size_t(r->in_dim));
+      }
+      ar.add(&p->wbias, 4 * W);
+      ar.add(&p->wpart, size_t(wide_part_floats(p->per, 2 * r->width)));
+    }
     ar.add(&p->spart_a, size_t(p->grid_a) * 6);
     ar.add(&p->spart_c, size_t(p->grid_c) * 6);
     ar.add(&p->adv_part, size_t(std::max(nb, ppo_stat_blocks(rnn_K))) * 2);
@@ -775,6 +906,7 @@ int marl_ppo_create(marl_venv* h, const char* ppo_config_json, int centralized, 
       ar.add(&p->cmp_scratch, p->cmp_scratch_bytes);
     }
     ar.commit();
+    if (p->wide && !centralized) p->wx[1] = p->wx[0];  // IPPO: the critic reads the actor's rows
     if (p->recurrent) {
       std::vector<float> ones(size_t(rnn_Kc), 1.0f);
       cuda_check(cudaMemcpy(p->rnn_ones, ones.data(), ones.size() * 4, cudaMemcpyHostToDevice), "cudaMemcpy");

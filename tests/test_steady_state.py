@@ -112,9 +112,11 @@ def _grad(env_id, cfg, n_envs, T, precision, cap):
     return tr, buf, a, c, idx, g, st
 
 
-# MPE: in 18, Kx 32, two tiles in flight (NS = 2); SMAX 3m: in 95, Kx 96, NS = 1
-@pytest.mark.parametrize("env_id,cfg,n_envs", [("MPE_simple_spread_v3", {}, 1024), ("SMAX_5m_vs_6m", THREE_M, 1024)])
-@pytest.mark.parametrize("precision,cap", [("bf16", 1), ("bf16", 2), ("fp32", 2)])
+# MPE: in 18, Kx 32, two tiles in flight (NS = 2); SMAX 3m: in 95, Kx 96, NS = 1;
+# Overcooked (in 522, fp32 only): layer 1 as tensor-core GEMMs around the branch kernel
+@pytest.mark.parametrize("env_id,cfg,n_envs,precision,cap", [
+    (e, c, n, p, k) for e, c, n in (("MPE_simple_spread_v3", {}, 1024), ("SMAX_5m_vs_6m", THREE_M, 1024))
+    for p, k in (("bf16", 1), ("bf16", 2), ("fp32", 2))] + [("overcooked_cramped_room_v0", {}, 1100, "fp32", 2)])
 def test_update_kernel_steady_state_matches_ff_minibatch(env_id, cfg, n_envs, precision, cap):
     """The steady-state property first: 1-2 CTAs walking hundreds of tiles
     (cross-tile gradient accumulation in TMEM / registers, NS = 2 tiles in
