@@ -194,10 +194,10 @@ struct PolicyNetBf16 {
   const uint16_t* a1;   // [128 x kx] : actor W1 rows 0..63, critic W1 rows 64..127, K padded to kx = round16(in)
   const uint16_t* a2;   // [64 x 64]  actor W2
   const uint16_t* c2;   // [64 x 64]  critic W2
-  const uint16_t* h3;   // [16 x 64]  actor head (rows 0..n_act-1), zero padded
+  const uint16_t* h3;   // [64 x 64]  actor head (rows 0..n_act-1), zero padded (narrow kernels read rows 0..15)
   const uint16_t* hc3;  // [16 x 64]  critic head (row 0), zero padded
   const uint16_t* c1;   // [64 x kc]  MAPPO critic W1 over world_state rows, K padded to kc = round16(critic_in); else null
-  const float* bias;    // [64 b1a | 64 b1c | 64 b2a | 64 b2c | 16 b3a | 16 b3c]
+  const float* bias;    // [64 b1a | 64 b1c | 64 b2a | 64 b2c | 16 b3a | 16 b3c | 64 b3a (heads up to 64)]
 };
 
 struct PolicyStep {

@@ -72,6 +72,34 @@ __device__ inline void sample_row_f32(double u, const float* logits, const uint8
 
 // sample_row_f32 with the loops bounded by a compile-time NMAX (>= n_act):
 // fully unrolled, the probabilities stay in registers.
+// sample_row_n for heads of up to 64 actions without the per-action
+// probability array (the exponentials are recomputed: same values, same order)
+__device__ __forceinline__ void sample_row_wide(double u, const float* logits, const uint8_t* legal, int n_act,
+                                                int* action, float* logp) {
+  float mx = -INFINITY;
+#pragma unroll
+  for (int i = 0; i < 64; ++i)
+    if (i < n_act && legal[i]) mx = fmaxf(mx, logits[i]);
+  float denom = 0.0f;
+#pragma unroll
+  for (int i = 0; i < 64; ++i) denom += (i < n_act && legal[i]) ? expf(logits[i] - mx) : 0.0f;
+  const float log_denom = logf(denom), inv = 1.0f / denom;
+  double cum = 0.0;
+  int pick = -1;
+  bool done = false;
+  float lpick = 0.0f;
+#pragma unroll
+  for (int i = 0; i < 64; ++i) {
+    if (!(i < n_act && legal[i]) || done) continue;
+    pick = i;
+    lpick = logits[i];
+    cum += double(expf(logits[i] - mx) * inv);
+    done = u < cum;
+  }
+  *action = pick;
+  *logp = lpick - mx - log_denom;
+}
+
 template <int NMAX>
 __device__ __forceinline__ void sample_row_n(double u, const float* logits, const uint8_t* legal, int n_act, int* action,
                                              float* logp) {

@@ -658,14 +658,14 @@ __host__ __device__ inline WideLayout wide_layout(int n_act) {
   for (int q = 0; q < 2; ++q) L.xbuf[q] = take(kTcRows * 64 * 2, 1024);
   L.w2a = take(64 * 64 * 2, 128);
   L.w2c = take(64 * 64 * 2, 128);
-  L.w3a = take(16 * 64 * 2, 128);
+  L.w3a = take(64 * 64 * 2, 128);  // actor head: up to 64 actions
   L.w3c = take(16 * 64 * 2, 128);
   L.ha = take(kTcRows * 64 * 2, 128);
   L.hc = take(kTcRows * 64 * 2, 128);
   L.legal = take(uint32_t(kTcRows * n_act), 16);
   L.resets = take(kTcRows, 16);
   L.active = take(kTcRows * 4, 16);
-  L.bias = take((4 * 64 + 2 * 16) * 4, 16);
+  L.bias = take((4 * 64 + 2 * 16 + 64) * 4, 16);
   L.bar = take(8, 8);
   for (int q = 0; q < 2; ++q) L.bar_w[q] = take(8, 8);
   for (int q = 0; q < 2; ++q) L.bar_c[q] = take(8, 8);
@@ -694,6 +694,7 @@ __global__ void __launch_bounds__(kSplit * kTcRows, 1) policy_tc_wide_kernel(Pol
   const int tid = threadIdx.x & (kTcRows - 1), part = threadIdx.x >> 7, warp = threadIdx.x >> 5;
   const int64_t n_tiles = (s.R + kTcRows - 1) / kTcRows;
   const int D = s.D, AA = s.A, KX = tc_kx(in_dim), NC = KX / 64;
+  const int hn = n_act <= 16 ? 16 : (n_act + 15) / 16 * 16;  // actor head MMA N
 
   if (threadIdx.x == 0) {
     for (uint64_t* m : {bar, bar_w[0], bar_w[1], bar_c[0], bar_c[1]})
@@ -711,10 +712,10 @@ __global__ void __launch_bounds__(kSplit * kTcRows, 1) policy_tc_wide_kernel(Pol
                            reinterpret_cast<const uint4*>(nb.h3), reinterpret_cast<const uint4*>(nb.hc3)};
     uint4* dst[4] = {reinterpret_cast<uint4*>(w2a), reinterpret_cast<uint4*>(w2c), reinterpret_cast<uint4*>(w3a),
                      reinterpret_cast<uint4*>(w3c)};
-    const int n16[4] = {64 * 64 * 2 / 16, 64 * 64 * 2 / 16, 16 * 64 * 2 / 16, 16 * 64 * 2 / 16};
+    const int n16[4] = {64 * 64 * 2 / 16, 64 * 64 * 2 / 16, 64 * 64 * 2 / 16, 16 * 64 * 2 / 16};
     for (int m = 0; m < 4; ++m)
       for (int q = threadIdx.x; q < n16[m]; q += blockDim.x) dst[m][q] = __ldg(src[m] + q);
-    for (int q = threadIdx.x; q < 4 * 64 + 2 * 16; q += blockDim.x) s_bias[q] = __ldg(nb.bias + q);
+    for (int q = threadIdx.x; q < 4 * 64 + 2 * 16 + 64; q += blockDim.x) s_bias[q] = __ldg(nb.bias + q);
   }
   fence_proxy_async_smem();
   tc_fence_before();
@@ -830,33 +831,51 @@ __global__ void __launch_bounds__(kSplit * kTcRows, 1) policy_tc_wide_kernel(Pol
     tc_fence_before();
     fence_proxy_async_smem();
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == 0) {  // actor head: TMEM columns 0..hn-1; critic head: 64..79
       tc_fence_after();
-      const uint32_t id = idesc_bf16(128, 16);
+      const uint32_t id = idesc_bf16(128, hn);
       for (int k = 0; k < 64; k += 16) umma_bf16(tmem + 0, umma_desc(ha, 64, k), umma_desc(w3a, 64, k), id, k > 0);
-      for (int k = 0; k < 64; k += 16) umma_bf16(tmem + 16, umma_desc(hc, 64, k), umma_desc(w3c, 64, k), id, k > 0);
+      const uint32_t idc = idesc_bf16(128, 16);
+      for (int k = 0; k < 64; k += 16) umma_bf16(tmem + 64, umma_desc(hc, 64, k), umma_desc(w3c, 64, k), idc, k > 0);
       umma_commit(bar);
     }
     mbar_wait(bar, phase);
     phase ^= 1;
     tc_fence_after();
-    {
+    if (part == 1) {
       float hv[16];
-      tmem_ld16(tmem + lane_base + uint32_t(16 * part), hv);
+      tmem_ld16(tmem + lane_base + 64u, hv);
       tc_fence_before();
-      if (part == 1) {
-        const float value = hv[0] + s_bias[256 + 16];
-        if (live) {
-          if (act_mode) b.value[slot0 + tid] = value;
-          else b.last_value[r] = value;
-        }
-      } else if (act_mode && live) {
+      const float value = hv[0] + s_bias[256 + 16];
+      if (live) {
+        if (act_mode) b.value[slot0 + tid] = value;
+        else b.last_value[r] = value;
+      }
+    } else if (hn == 16) {
+      float hv[16];
+      tmem_ld16(tmem + lane_base, hv);
+      tc_fence_before();
+      if (act_mode && live) {
         float logits[16];
 #pragma unroll
         for (int j = 0; j < 16; ++j) logits[j] = hv[j] + s_bias[256 + j];
         int pick;
         float lp;
         sample_row_n<16>(u_row, logits, s_legal + tid * n_act, n_act, &pick, &lp);
+        b.actions[slot0 + tid] = pick;
+        b.logp[slot0 + tid] = lp;
+      }
+    } else {  // up to 64 actions (SMAX 27m_vs_30m: 35)
+      float logits[64];
+      tmem_ld32(tmem + lane_base, logits);
+      tmem_ld32(tmem + lane_base + 32u, logits + 32);
+      tc_fence_before();
+      if (act_mode && live) {
+#pragma unroll
+        for (int j = 0; j < 64; ++j) logits[j] += s_bias[288 + j];
+        int pick;
+        float lp;
+        sample_row_wide(u_row, logits, s_legal + tid * n_act, n_act, &pick, &lp);
         b.actions[slot0 + tid] = pick;
         b.logp[slot0 + tid] = lp;
       }
@@ -877,7 +896,7 @@ __global__ void pack_bf16_kernel(PolicyNet n, uint16_t* img, float* bias) {
   uint16_t* a2 = a1 + 128 * KX;
   uint16_t* c2 = a2 + 64 * 64;
   uint16_t* h3 = c2 + 64 * 64;
-  uint16_t* hc3 = h3 + 16 * 64;
+  uint16_t* hc3 = h3 + 64 * 64;
   uint16_t* c1 = hc3 + 16 * 64;  // MAPPO: the critic's W1 over world_state rows
   auto bf = [](float v) {
     const __nv_bfloat16 h = __float2bfloat16_rn(v);
@@ -909,16 +928,17 @@ __global__ void pack_bf16_kernel(PolicyNet n, uint16_t* img, float* bias) {
     a2[canon_off(row, k, 64) / 2] = bf(n.w2[row * 64 + k]);
     c2[canon_off(row, k, 64) / 2] = bf(n.cw2[row * 64 + k]);
   }
-  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < 16 * 64; q += gridDim.x * blockDim.x) {
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < 64 * 64; q += gridDim.x * blockDim.x) {
     const int row = q / 64, k = q % 64;
     h3[canon_off(row, k, 64) / 2] = bf(row < NA ? n.w3[row * 64 + k] : 0.0f);
-    hc3[canon_off(row, k, 64) / 2] = bf(row == 0 ? n.cw3[k] : 0.0f);
+    if (row < 16) hc3[canon_off(row, k, 64) / 2] = bf(row == 0 ? n.cw3[k] : 0.0f);
   }
   for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < 64; q += gridDim.x * blockDim.x) {
     bias[q] = n.b1[q];
     bias[64 + q] = n.cb1[q];
     bias[128 + q] = n.b2[q];
     bias[192 + q] = n.cb2[q];
+    bias[288 + q] = q < NA ? n.b3[q] : 0.0f;
     if (q < 16) {
       bias[256 + q] = q < NA ? n.b3[q] : 0.0f;
       bias[272 + q] = q == 0 ? n.cb3[0] : 0.0f;
@@ -932,7 +952,7 @@ int rollout_tc_kx(int in_dim) { return tc_kx(in_dim); }
 
 bool rollout_policy_bf16_supported(int in_dim, int n_act, int width, int critic_in) {
   if (in_dim > kTcMaxKx)  // wide rows: the K-chunked kernel (IPPO critics)
-    return critic_in == 0 && n_act <= 16 && width == 64 && wide_layout(n_act).total <= kTcSmemMax;
+    return critic_in == 0 && n_act <= 64 && width == 64 && wide_layout(n_act).total <= kTcSmemMax;
   // D <= in_dim: the layout without staged tiles bounds every mode
   return in_dim >= 1 && tc_kx(in_dim) <= kTcMaxKx && tc_kc(critic_in) <= kTcMaxKx && n_act <= 16 && width == 64 &&
          tc_layout_mode(in_dim, in_dim, n_act, 0, critic_in).total <= kTcSmemMax;

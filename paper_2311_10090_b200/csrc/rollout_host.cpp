@@ -56,7 +56,7 @@ PolicyNetBf16 net_bf16_of(const marl_rollout* r) {
   n.a2 = n.a1 + 128 * rollout_tc_kx(r->in_dim);
   n.c2 = n.a2 + 64 * 64;
   n.h3 = n.c2 + 64 * 64;
-  n.hc3 = n.h3 + 16 * 64;
+  n.hc3 = n.h3 + 64 * 64;
   n.c1 = r->centralized ? n.hc3 + 16 * 64 : nullptr;
   n.bias = r->bias;
   return n;
@@ -179,7 +179,7 @@ marl_rollout* rollout_create_impl(marl_venv* h, int T, int width, int n_layers, 
     if (ps.in_dim > 1024 || ps.n_actions > 64) raise(MARL_ERR_SCHEMA, "rollout: input wider than 1024 or > 64 actions");
     if (precision == 1 && !rollout_policy_bf16_supported(ps.in_dim, ps.n_actions, width, centralized ? ps.critic_in : 0))
       raise(MARL_ERR_SCHEMA, "rollout: the tcgen05 bf16 policy needs in_dim (and the MAPPO critic's world_state) <= "
-                             "192, n_actions <= 16, fc_width == 64");
+                             "192 and n_actions <= 16 (wider IPPO rows: <= 1024 with n_actions <= 64), fc_width == 64");
     if (precision != 0 && precision != 1) raise(MARL_ERR_SCHEMA, "rollout: precision must be 0 (fp32) or 1 (bf16)");
     set_device(h);
     auto r = std::make_unique<marl_rollout>();
@@ -219,9 +219,9 @@ marl_rollout* rollout_create_impl(marl_venv* h, int T, int width, int n_layers, 
       ar.add(&r->ws, size_t(h->n) * size_t(r->critic_in));
     }
     ar.add(&r->params, size_t(r->n_actor + r->n_critic));
-    ar.add(&r->images, size_t(128 * rollout_tc_kx(ps.in_dim) + 2 * 64 * 64 + 2 * 16 * 64 +
+    ar.add(&r->images, size_t(128 * rollout_tc_kx(ps.in_dim) + 2 * 64 * 64 + 64 * 64 + 16 * 64 +
                               (centralized ? 64 * ((ps.critic_in + 15) / 16 * 16) : 0)));
-    ar.add(&r->bias, size_t(4 * 64 + 2 * 16));
+    ar.add(&r->bias, size_t(4 * 64 + 2 * 16 + 64));
     ar.add(&r->agent_actions, size_t(e.A));
     if (hidden > 0) {
       r->recurrent = 1;

@@ -773,7 +773,7 @@ __global__ void __launch_bounds__(kThreads) smax_reset_kernel(const Params* __re
 }
 
 template <int G, int UPL, bool RANDOM, int HT, bool FU>
-__global__ void __launch_bounds__(kThreads, 4) smax_step_kernel(const Params* __restrict__ gP, SmaxState st,
+__global__ void __launch_bounds__(kThreads, 4 * 256 / kThreads) smax_step_kernel(const Params* __restrict__ gP, SmaxState st,
                                                              LaunchCommon lc, Key step_key, Plan plan) {
   constexpr int EPW = Grp<G>::EPW, EPB = kWarps * EPW, CAP = G * UPL;
   extern __shared__ __align__(16) uint8_t smem[];

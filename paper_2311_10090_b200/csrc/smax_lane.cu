@@ -38,7 +38,10 @@ namespace marl_b200 {
 namespace {
 using namespace smax;
 
-constexpr int kLT = 128;  // threads (= envs) per block
+#ifndef MARL_LANE_LT
+#define MARL_LANE_LT 32  // one warp per block: 2048 blocks over 148 SMs balance to within 1 % (128: 13 %)
+#endif
+constexpr int kLT = MARL_LANE_LT;  // threads (= envs) per block
 constexpr int kLW = kLT / 32;
 
 constexpr int a16i(int b) { return (b + 15) & ~15; }
@@ -576,7 +579,7 @@ __device__ __forceinline__ const double* reset_draws(const Params& P, uint8_t* s
 }
 
 template <class R, bool RANDOM>
-__global__ void __launch_bounds__(kLT, R::kMinBlocks) smax_lane_step_kernel(const __grid_constant__ Params P, SmaxState st,
+__global__ void __launch_bounds__(kLT, R::kMinBlocks * 128 / kLT) smax_lane_step_kernel(const __grid_constant__ Params P, SmaxState st,
                                                                LaunchCommon lc, Key step_key) {
   extern __shared__ __align__(16) uint8_t smem[];
   if (*(volatile int*)lc.err) return;  // a pending contract error freezes the batch

@@ -14,7 +14,10 @@ constexpr double kDt = 1.0 / 16.0;  // smax.cpp:17
 constexpr int kTicks = 8;           // smax.cpp:18
 constexpr double kSepTol = 1e-6;    // smax.cpp:19
 constexpr int kNorth = 0, kSouth = 1, kEast = 2, kWest = 3, kStop = 4, kAttackBase = 5;
-constexpr int kThreads = 256;
+#ifndef MARL_SMAX_THREADS
+#define MARL_SMAX_THREADS 256
+#endif
+constexpr int kThreads = MARL_SMAX_THREADS;
 constexpr int kWarps = kThreads / 32;
 constexpr int kTypes = 6;
 constexpr int kWarpStageBytes = 4 * 1024;  // observation staging budget per warp

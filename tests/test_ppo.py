@@ -32,7 +32,8 @@ def _need_ref():
         pytest.skip("oracle/_ref not built")
 
 
-ENVS = [("MPE_simple_spread_v3", {}), ("SMAX_5m_vs_6m", THREE_M), ("overcooked_cramped_room_v0", {})]
+ENVS = [("MPE_simple_spread_v3", {}), ("SMAX_5m_vs_6m", THREE_M), ("overcooked_cramped_room_v0", {}),
+        ("SMAX_27m_vs_30m", {"max_steps": 20})]
 
 
 # ------------------------------------------------------------------ CPU tests
@@ -127,7 +128,9 @@ def _close(got, ref, rel=2e-3, absf=1e-4):
 @pytest.mark.parametrize("centralized", [False, True])
 def test_minibatch_gradient_matches_ff_minibatch(env_id, cfg, centralized):
     _need_ref()
-    n_envs, T = (16, 24) if not env_id.startswith("overcooked") else (4, 24)
+    if centralized and env_id == "SMAX_27m_vs_30m":
+        pytest.skip("27m_vs_30m's world_state is wider than the collector's 1024-column critic input")
+    n_envs, T = (16, 24) if env_id.startswith(("MPE", "SMAX_5m")) else (4, 24)
     tr = _trainer(env_id, cfg, n_envs, T, centralized)
     key = O.key_from_seed(21)
     tr.begin(key)

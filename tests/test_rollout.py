@@ -103,7 +103,9 @@ def test_fp32_rollout_matches_reference_collector(env_id, cfg, n, T, windows, sh
                                           ("SMAX_2s3z", {}, 131), ("SMAX_5m_vs_6m", {}, 77),
                                           # wide rows (K-chunked layer 1): Overcooked's 520 + 2 columns
                                           ("overcooked_cramped_room_v0", {"max_steps": 20}, 300),
-                                          ("overcooked_coordination_ring_v0", {"max_steps": 20}, 97)])
+                                          ("overcooked_coordination_ring_v0", {"max_steps": 20}, 97),
+                                          # 989 columns, 35 actions (head N = 48)
+                                          ("SMAX_27m_vs_30m", {"max_steps": 20}, 40)])
 def test_bf16_tensor_core_rollout_agrees_with_fp32(env_id, cfg, n):
     from paper_2311_10090_b200._native import lib
     _need_ref()

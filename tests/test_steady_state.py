@@ -52,7 +52,8 @@ def _collect(env_id, cfg, n, T, precision, key, a, c):
 
 
 @pytest.mark.parametrize("env_id,cfg,n", [("MPE_simple_spread_v3", {}, 4096), ("SMAX_5m_vs_6m", THREE_M, 2048),
-                                          ("overcooked_cramped_room_v0", {"max_steps": 10}, 1024)])
+                                          ("overcooked_cramped_room_v0", {"max_steps": 10}, 1024),
+                                          ("SMAX_27m_vs_30m", {"max_steps": 10}, 64)])
 def test_policy_tc_capped_grid_equals_full_grid(env_id, cfg, n):
     _need_ref()
     key = O.key_from_seed(17)
