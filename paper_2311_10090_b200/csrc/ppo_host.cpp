@@ -1072,7 +1072,9 @@ int marl_ppo_minibatch_grad(marl_ppo* p, const int32_t* d_idx, int64_t M, float*
     if (flags[1]) raise(MARL_ERR_CONTRACT, "nn: ppo_row_loss: stored action not legal");
     // with an all-reduce hook, minibatch_grad already folded the per-CTA rows
     // into row 0 (and summed it over the ranks): read that row only
-    const int na = p->hook ? 1 : p->grid_a, nc = p->hook ? 1 : p->grid_c;
+    // (the wide path's loss rows are rnn_loss's blocks of this minibatch)
+    const int na = p->hook ? 1 : p->wide ? p->rnn_blocks : p->grid_a;
+    const int nc = p->hook ? 1 : p->wide ? p->rnn_blocks : p->grid_c;
     double s[6] = {0, 0, 0, 0, 0, 0}, vt = 0.0;
     for (int c = 0; c < na; ++c)
       for (int j = 0; j < 6; ++j) s[j] += sa[size_t(c) * 6 + j];

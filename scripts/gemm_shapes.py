@@ -33,7 +33,7 @@ def case(name, Mm, N, K, A, sam, sak, B, sbn, sbk, ref):
     us = timeit(lambda: L.marl_gemm_f32(Mm, N, K, p(A), sam, sak, p(B), sbn, sbk, p(Cc), N, 0.0, None))
     ub = timeit(ref)
     gb = 4 * (Mm * K + N * K + Mm * N) / 1e9
-    print(f"{name:44s} tc {us:8.1f} us ({gb / us * 1e3:6.0f} GB/s)   cuBLAS sgemm {ub:8.1f} us")
+    print(f"{name:44s} tc {us:8.1f} us ({gb * 1e6 / us:6.0f} GB/s)   cuBLAS sgemm {ub:8.1f} us")
 
 
 W, I, ld = 64, 522, 524

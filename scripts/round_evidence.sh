@@ -13,11 +13,14 @@ timeout 600 python bench.py --workload mpe --per-step --steps 30 --warmup 5 --no
 timeout 600 python bench.py --workload ppo --steps 10 --warmup 3 2>/dev/null | grep '^{' >> gpurun_out/bench_${TAG}.jsonl
 timeout 600 python bench.py --workload ppo_rnn --steps 3 --warmup 3 2>/dev/null | grep '^{' >> gpurun_out/bench_${TAG}.jsonl
 timeout 600 python bench.py --workload ppo_smax --steps 10 --warmup 3 2>/dev/null | grep '^{' >> gpurun_out/bench_${TAG}.jsonl
+timeout 600 python bench.py --workload ppo_oc --steps 5 --warmup 3 2>/dev/null | grep '^{' >> gpurun_out/bench_${TAG}.jsonl
 timeout 300 python bench.py --impl reference --workload smax3m --steps 3 --warmup 1 2>/dev/null | grep '^{' >> gpurun_out/bench_${TAG}.jsonl
 timeout 300 python bench.py --impl reference --workload ippo_oc --steps 1 --warmup 1 2>/dev/null | grep '^{' >> gpurun_out/bench_${TAG}.jsonl
 timeout 300 python bench.py --impl reference --workload ppo --steps 2 --warmup 3 2>/dev/null | grep '^{' >> gpurun_out/bench_${TAG}.jsonl
 timeout 300 python bench.py --impl reference --workload ppo_rnn --steps 1 --warmup 3 2>/dev/null | grep '^{' >> gpurun_out/bench_${TAG}.jsonl
 timeout 300 python bench.py --impl reference --workload ppo_smax --steps 1 --warmup 3 2>/dev/null | grep '^{' >> gpurun_out/bench_${TAG}.jsonl
+timeout 300 python bench.py --impl reference --workload ppo_oc --steps 1 --warmup 3 2>/dev/null | grep '^{' >> gpurun_out/bench_${TAG}.jsonl
+timeout 600 python scripts/ippo_oc_time.py 4096 SMAX_27m_vs_30m > gpurun_out/ippo27m_${TAG}.txt 2>&1
 wc -l gpurun_out/bench_${TAG}.jsonl
 NCU=/usr/local/cuda/bin/ncu
 for w in smax3m smax2s3z mpe_large overcooked smax27m; do
@@ -44,6 +47,15 @@ timeout 900 $NCU --set full --clock-control none --import-source on -k regex:ppo
 timeout 600 /usr/local/cuda/bin/ncu --set full --clock-control none --import-source on -k regex:probe_kernel -s 5 -c 1 \
   -o gpurun_out/prof_${TAG}_mpeprobe -f python bench.py --workload mpe --steps 1000 --warmup 5 --no-e2e --no-cpu > /dev/null 2>&1
 GSKIP=3000 bash scripts/prof_gemm.sh ${TAG} > /dev/null 2>&1
+# the wide-input update: launch list of one Overcooked PPO step, full captures of its two layer-1 GEMMs
+timeout 600 $NCU --metrics gpu__time_duration.sum --clock-control none -c 8000 --csv \
+  --log-file gpurun_out/launches_${TAG}_ppo_oc.csv python scripts/ppo_oc_time.py 4096 > /dev/null 2>&1
+timeout 600 $NCU --set full --clock-control none --import-source on -k regex:gemm_tf32x3 -s 0 -c 1 \
+  -o gpurun_out/prof_${TAG}_gemm_z1 -f python scripts/gemm_shapes.py 262144 > /dev/null 2>&1
+timeout 600 $NCU --set full --clock-control none --import-source on -k regex:gemm_tf32x3 -s 21 -c 1 \
+  -o gpurun_out/prof_${TAG}_gemm_dw1 -f python scripts/gemm_shapes.py 262144 > /dev/null 2>&1
+timeout 600 $NCU --set full --clock-control none --import-source on -k regex:policy_tc_wide -s 10 -c 1 \
+  -o gpurun_out/prof_${TAG}_wide27m -f python scripts/ippo_oc_time.py 1024 SMAX_27m_vs_30m > /dev/null 2>&1
 LTAG=${TAG} SKIP=5000 CNT=6000 bash scripts/rnn_launches.sh > /dev/null 2>&1
 python scripts/ncu_summary.py ${TAG} smax3m smax2s3z mpe_large overcooked smax27m > /dev/null 2>&1
 mkdir -p gpurun_out/summary_${TAG}

@@ -139,13 +139,17 @@ def test_minibatch_gradient_matches_ff_minibatch(env_id, cfg, centralized):
     a, c = tr.params()
     R = tr.rollout.R
     rng = np.random.default_rng(3)
-    for M in (1, 37, T * R // 2):
+    for M in (T * R // 2, 1, 37):  # largest first: a smaller minibatch must not read its stale loss rows
         idx = rng.choice(T * R, size=M, replace=False).astype(np.int32)
         g, st = tr.minibatch_grad(idx)
         gr, sr = O.ref_ff_minibatch(env_id, cfg, a, c, buf, idx, centralized=centralized)
         ok, err = _close(g, gr)
         assert ok, (M, err)
-        assert np.allclose(st, sr, rtol=1e-5, atol=1e-7), (M, st, sr)
+        # the per-row kernels evaluate the forward in the reference's order (stats within 1e-5); wide
+        # inputs run it as 3xTF32 GEMMs (fp32-accurate, another summation order), so a row whose value
+        # sits near its target moves the value loss by more: the gradient's 2e-3 bar there
+        rtol = 2e-3 if max(tr.spec.in_dim, tr.spec.critic_in) >= 256 else 1e-5
+        assert np.allclose(st, sr, rtol=rtol, atol=1e-7), (M, st, sr)
 
 
 @pytest.mark.gpu
