@@ -645,7 +645,13 @@ cudaError_t tc_gemm(cudaStream_t st, int64_t M, int N, int64_t K, const float* A
   // N tiles of up to 128 columns; a grid of fewer than two M x N tiles per SM
   // takes 64-column tiles instead (twice the CTAs in flight)
   const int64_t mt0 = (M + kGemmM - 1) / kGemmM;
-  const int maxn = (mt0 * ((N + kGemmMaxN - 1) / kGemmMaxN) < 2 * int64_t(sm_count()) && N > 64) ? 64 : kGemmMaxN;
+  // -- unless K is long enough to split: then the split supplies the CTAs and
+  // wider tiles re-stage the A operand fewer times (MARL_GEMM_SPLITN64=1: off)
+  const bool splits = mt0 * ((N + kGemmMaxN - 1) / kGemmMaxN) < int64_t(sm_count()) && K >= 64 * 128 &&
+                      !getenv("MARL_GEMM_SPLITN64");
+  const int maxn = (mt0 * ((N + kGemmMaxN - 1) / kGemmMaxN) < 2 * int64_t(sm_count()) && N > 64 && !splits)
+                       ? 64
+                       : kGemmMaxN;
   const int ntiles = (N + maxn - 1) / maxn;
   g.ntile = ((N + ntiles - 1) / ntiles + 15) / 16 * 16;  // balanced N tiles, multiples of 16
   g.npad = 16;
