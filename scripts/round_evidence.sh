@@ -60,6 +60,13 @@ LTAG=${TAG} SKIP=5000 CNT=6000 bash scripts/rnn_launches.sh > /dev/null 2>&1
 python scripts/ncu_summary.py ${TAG} smax3m smax2s3z mpe_large overcooked smax27m > /dev/null 2>&1
 mkdir -p gpurun_out/summary_${TAG}
 cp profiles/${TAG}_* profiles/ncu_traffic.json profiles/ncu_metrics.json gpurun_out/summary_${TAG}/ 2>/dev/null
-rm -f gpurun_out/prof_${TAG}_smax2s3z.ncu-rep gpurun_out/prof_${TAG}_mpe_large.ncu-rep gpurun_out/prof_${TAG}_smax27m.ncu-rep gpurun_out/prof_${TAG}_overcooked.ncu-rep
+# a markdown brief of every capture, then keep only three reports (gpurun returns <= 64 MiB)
+for r in gpurun_out/prof_${TAG}_*.ncu-rep; do
+  b=$(basename $r .ncu-rep); python scripts/ncu_brief.py $r ${b#prof_${TAG}_} > gpurun_out/summary_${TAG}/brief_${b}.md 2>&1
+done
+python scripts/ncu_srcsum.py gpurun_out/prof_${TAG}_smax3m.ncu-rep 65536 45 > gpurun_out/summary_${TAG}/srcsum_smax3m.txt 2>&1
+for r in gpurun_out/prof_${TAG}_*.ncu-rep; do
+  case $r in *_smax3m.ncu-rep|*_gemm_dw1.ncu-rep|*_wide27m.ncu-rep) ;; *) rm -f $r ;; esac
+done
 du -sh gpurun_out
 ls gpurun_out | grep ${TAG}
