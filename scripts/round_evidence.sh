@@ -50,9 +50,9 @@ GSKIP=3000 bash scripts/prof_gemm.sh ${TAG} > /dev/null 2>&1
 # the wide-input update: launch list of one Overcooked PPO step, full captures of its two layer-1 GEMMs
 timeout 600 $NCU --metrics gpu__time_duration.sum --clock-control none -c 8000 --csv \
   --log-file gpurun_out/launches_${TAG}_ppo_oc.csv python scripts/ppo_oc_time.py 4096 > /dev/null 2>&1
-timeout 600 $NCU --set full --clock-control none --import-source on -k regex:gemm_tf32x3 -s 0 -c 1 \
+timeout 600 $NCU --set full --clock-control none --import-source on -k regex:gemm_ws_kernel -s 0 -c 1 \
   -o gpurun_out/prof_${TAG}_gemm_z1 -f python scripts/gemm_shapes.py 262144 > /dev/null 2>&1
-timeout 600 $NCU --set full --clock-control none --import-source on -k regex:gemm_tf32x3 -s 21 -c 1 \
+timeout 600 $NCU --set full --clock-control none --import-source on -k regex:gemm_ws_kernel -s 21 -c 1 \
   -o gpurun_out/prof_${TAG}_gemm_dw1 -f python scripts/gemm_shapes.py 262144 > /dev/null 2>&1
 timeout 600 $NCU --set full --clock-control none --import-source on -k regex:policy_tc_wide -s 10 -c 1 \
   -o gpurun_out/prof_${TAG}_wide27m -f python scripts/ippo_oc_time.py 1024 SMAX_27m_vs_30m > /dev/null 2>&1
