@@ -142,7 +142,7 @@ __host__ __device__ constexpr int lay_vec(int L) { return (L == 0 || L == 2) ? 4
 // Issue the cp.async copies of chunk [k0, k0 + KC) of rows [r0, r0 + rows)
 // (valid rows < rvalid, valid k < K) into a raw stage.  rows = 1 << rlog, so
 // every index split is a shift or a mask.
-template <int KC, int L>
+template <int KC, int L, bool DIRECT = false>
 __device__ __forceinline__ void fetch(float* raw, const OpLayout& o, int64_t r0, int rlog, int64_t rvalid, int64_t k0,
                                       int64_t K, int tid = threadIdx.x, int nth = kGemmThreads) {
   constexpr int V = lay_vec(L);
@@ -165,7 +165,8 @@ __device__ __forceinline__ void fetch(float* raw, const OpLayout& o, int64_t r0,
       int64_t nv = gr < rvalid ? K - gk : 0;
       nv = nv < 0 ? 0 : nv > V ? V : nv;
       const float* src = nv ? o.X + gr * o.sr + gk * o.sk : o.X;
-      cp_async<4 * V>(raw + r * raw_pitch<KC>() + k, src, uint32_t(nv * 4));
+      float* dst = DIRECT ? raw + canon4<KC>(r, k) / 4 : raw + r * raw_pitch<KC>() + k;  // DIRECT: V == 4
+      cp_async<4 * V>(dst, src, uint32_t(nv * 4));
     }
   }
 }
@@ -178,13 +179,23 @@ __device__ __forceinline__ void split_tf32(float v, float& hi, float& lo) {
 }
 
 // raw stage -> hi / lo canonical tiles (four K per thread step)
-template <int KC, int KIND>
+template <int KC, int KIND, bool DIRECT = false>
 __device__ __forceinline__ void convert(const float* raw, int rlog, uint8_t* hi, uint8_t* lo, int tid = threadIdx.x,
                                         int nth = kGemmThreads) {
   const int rows = 1 << rlog;
   for (int idx = tid; idx < rows * (KC / 4); idx += nth) {
     const int r = idx & (rows - 1), k = (idx >> rlog) * 4;  // consecutive threads take consecutive rows
     float4 v;
+    if constexpr (DIRECT) {  // the raw stage is the canonical image: it serves as hi, only lo is written
+      v = *reinterpret_cast<const float4*>(reinterpret_cast<const uint8_t*>(raw) + canon4<KC>(r, k));
+      float4 h, l;
+      split_tf32(v.x, h.x, l.x);
+      split_tf32(v.y, h.y, l.y);
+      split_tf32(v.z, h.z, l.z);
+      split_tf32(v.w, h.w, l.w);
+      *reinterpret_cast<float4*>(lo + canon4<KC>(r, k)) = l;
+      continue;
+    }
     if (KIND == 1) {  // raw[k][r]
       v = make_float4(raw[(k << rlog) + r], raw[((k + 1) << rlog) + r], raw[((k + 2) << rlog) + r],
                       raw[((k + 3) << rlog) + r]);
@@ -354,6 +365,14 @@ constexpr int kWsThreads = kGemmThreads + 32;
 #define MARL_WS_SPLIT 128
 #endif
 constexpr int kWsSplit = MARL_WS_SPLIT, kWsProd = kGemmThreads - kWsSplit;  // splitter / producer threads
+// MARL_WS_DIRECT=1: K-contiguous 16-byte operands feed the MMA straight from
+// the raw stage as the hi image (correct: kind::tf32 ignores the low 13
+// mantissa bits, test_gemm_tc passes) but slower (Z1 334 -> 365 us: the raw
+// stage is held until the MMAs complete, so the ring runs shallower)
+#ifndef MARL_WS_DIRECT
+#define MARL_WS_DIRECT 0
+#endif
+constexpr bool kWsDirect = MARL_WS_DIRECT;
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
@@ -363,6 +382,10 @@ __device__ __forceinline__ void cp_async_arrive(uint64_t* bar) {
 
 template <int KC, int MINB, int AL, int BL>
 __global__ void __launch_bounds__(kWsThreads, MINB) gemm_ws_kernel(GemmArgs g) {
+  // (kWsDirect) K-contiguous 16-byte operands land in the raw stage in canonical
+  // layout and feed the MMA as the hi image directly; the stage then lives until
+  // the chunk's MMAs complete
+  constexpr bool DA = kWsDirect && AL == 0, DB = kWsDirect && BL == 0, DIRECT = DA || DB;
   extern __shared__ __align__(1024) uint8_t smem[];
   const int mt = blockIdx.x, nt = blockIdx.y, sp = blockIdx.z;
   const int64_t m0 = int64_t(mt) * kGemmM;
@@ -382,7 +405,8 @@ __global__ void __launch_bounds__(kWsThreads, MINB) gemm_ws_kernel(GemmArgs g) {
   if (threadIdx.x == 0) {
     for (int q = 0; q < 8; ++q) {
       asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(full + q)), "n"(kWsProd) : "memory");
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(empty + q)), "n"(kWsSplit) : "memory");
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(empty + q)), "n"(DIRECT ? 1 : kWsSplit)
+                   : "memory");
     }
     for (int q = 0; q < 2; ++q) {
       asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(tfull + q)), "n"(kWsSplit) : "memory");
@@ -411,8 +435,8 @@ __global__ void __launch_bounds__(kWsThreads, MINB) gemm_ws_kernel(GemmArgs g) {
       float* ra = reinterpret_cast<float*>(raw0 + st * stage_bytes);
       float* rb = reinterpret_cast<float*>(raw0 + st * stage_bytes + g.a_raw);
       const int64_t k0 = kb + int64_t(c) * KC;
-      fetch<KC, AL>(ra, g.a, m0, 7, g.M, k0, ke, tid, kWsProd);
-      fetch<KC, BL>(rb, bo, 0, g.nlog, nvalid, k0, ke, tid, kWsProd);
+      fetch<KC, AL, DA>(ra, g.a, m0, 7, g.M, k0, ke, tid, kWsProd);
+      fetch<KC, BL, DB>(rb, bo, 0, g.nlog, nvalid, k0, ke, tid, kWsProd);
       cp_async_arrive(full + st);
     }
     cp_async_wait<0>();
@@ -425,20 +449,22 @@ __global__ void __launch_bounds__(kWsThreads, MINB) gemm_ws_kernel(GemmArgs g) {
       uint8_t* set = smem + ts * set_bytes;
       uint8_t *ah = set, *al = set + g.a_tile, *bh = set + 2 * g.a_tile, *bl = set + 2 * g.a_tile + g.b_tile;
       const uint8_t* stg = raw0 + st * stage_bytes;
-      convert<KC, lay_kind(AL)>(reinterpret_cast<const float*>(stg), 7, ah, al, tid, kWsSplit);
-      convert<KC, lay_kind(BL)>(reinterpret_cast<const float*>(stg + g.a_raw), g.nlog, bh, bl, tid, kWsSplit);
-      mbar_arrive(empty + st);
+      convert<KC, lay_kind(AL), DA>(reinterpret_cast<const float*>(stg), 7, ah, al, tid, kWsSplit);
+      convert<KC, lay_kind(BL), DB>(reinterpret_cast<const float*>(stg + g.a_raw), g.nlog, bh, bl, tid, kWsSplit);
+      if (!DIRECT) mbar_arrive(empty + st);
       fence_proxy_async_smem();
       mbar_arrive(tfull + ts);
     }
   } else if (threadIdx.x == 256) {  // the MMA issuer
     const uint32_t idesc = idesc_tf32(kGemmM, g.npad);
     for (int c = 0; c < nch; ++c) {
-      const int ts = g.nt == 2 ? (c & 1) : 0;
+      const int ts = g.nt == 2 ? (c & 1) : 0, st = c % g.ns;
       mbar_wait(tfull + ts, uint32_t(c / g.nt) & 1u);
       tc_fence_after();
       uint8_t* set = smem + ts * set_bytes;
       uint8_t *ah = set, *al = set + g.a_tile, *bh = set + 2 * g.a_tile, *bl = set + 2 * g.a_tile + g.b_tile;
+      if (DA) ah = raw0 + st * stage_bytes;
+      if (DB) bh = raw0 + st * stage_bytes + g.a_raw;
 #pragma unroll
       for (int kk = 0; kk < KC; kk += 8) {
         const uint32_t acc0 = (c > 0 || kk > 0) ? 1u : 0u;
@@ -447,6 +473,7 @@ __global__ void __launch_bounds__(kWsThreads, MINB) gemm_ws_kernel(GemmArgs g) {
         umma_tf32(tmem, desc4<KC>(al, kk), desc4<KC>(bh, kk), idesc, 1u);
       }
       umma_commit(tfree + ts);
+      if (DIRECT) umma_commit(empty + st);  // the stage held this chunk's hi images
     }
   }
   if (nch > 0 && warp < 8) {  // the last chunk's MMAs (and so all of them) are done
