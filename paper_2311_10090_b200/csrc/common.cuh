@@ -7,6 +7,8 @@
 #include <cmath>
 #include <cstdint>
 #include <cuda_runtime.h>
+#include <mutex>
+#include <unordered_set>
 
 #define MARL_HD __host__ __device__ __forceinline__
 #ifdef __CUDACC__
@@ -286,5 +288,27 @@ __device__ __forceinline__ void tile_store_drain() {
   if (threadIdx.x == 0) bulk_wait_read<0>();
 }
 #endif
+
+// Let `fn` use the device's whole opt-in shared memory per block.  Launches
+// pass their own dynamic size; setting the attribute to ONE value (the
+// maximum) instead of each launch's size keeps concurrent host threads from
+// racing on it (one thread's smaller value failing another's launch with
+// "too many resources requested").  Done once per kernel.
+inline void smem_optin(const void* fn) {
+  static std::mutex mu;
+  static std::unordered_set<const void*> done;
+  std::lock_guard<std::mutex> lk(mu);
+  if (!done.insert(fn).second) return;
+  int dev = 0, optin = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  cudaFuncAttributes fa{};
+  cudaFuncGetAttributes(&fa, fn);
+  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - int(fa.sharedSizeBytes));
+}
+template <class F>
+inline void smem_optin(F* fn) {
+  smem_optin(reinterpret_cast<const void*>(fn));
+}
 
 }  // namespace marl_b200

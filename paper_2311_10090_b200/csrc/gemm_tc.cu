@@ -738,7 +738,7 @@ cudaError_t tc_gemm(cudaStream_t st, int64_t M, int N, int64_t K, const float* A
     if (!g.part) return e;
   }
   auto kern = pick_kernel(deep, ws, lay_code(g.a), lay_code(g.b));
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  smem_optin(kern);
   kern<<<dim3(unsigned(mtiles), unsigned(ntiles), unsigned(split)), ws ? kWsThreads : kGemmThreads, smem, st>>>(g);
   ++g_launches;
   if (split > 1) {

@@ -504,7 +504,7 @@ size_t oc_smem_bytes(const OcConfig& c) { return 4 * tmpl_floats(kPlanes * c.h *
 void oc_launch_reset_t(const OcConfig& c, const float* templ, const OcState& s, const LaunchCommon& lc,
                        KeyWords key, KeyWords carry_parent) {
   size_t sm = oc_smem_bytes(c);
-  cudaFuncSetAttribute(oc_reset_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+  smem_optin(oc_reset_kernel);
   unsigned g = unsigned((lc.n + kThreads - 1) / kThreads);
   oc_reset_kernel<<<g, kThreads, sm, lc.stream>>>(c, templ, s, lc, to_key(key), to_key(carry_parent));
   ++g_launches;
@@ -532,7 +532,7 @@ void oc_launch_step_t(const OcConfig& c, const float* templ, const OcState& s, c
     sm = oc_smem_bytes(c);
   }
   auto fn = random ? oc_step_kernel<true> : oc_step_kernel<false>;
-  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+  smem_optin(fn);
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, warps * 32, sm);
   const int64_t chunks = (lc.end - lc.begin + 31) / 32;

@@ -1111,7 +1111,7 @@ template <bool ACTOR>
 static void launch_branch(PpoBranchArgs a, int grid, size_t sm, cudaStream_t s) {
   const int P = a.W * a.in + a.W + a.W * a.W + a.W + a.out * a.W + a.out;
   auto go = [&](auto kern) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+    smem_optin(kern);
     kern<<<grid, kThreads, sm, s>>>(a);
   };
   if (P <= kThreads * 24)
@@ -1128,7 +1128,7 @@ bool ppo_tiled_ok(int in, int W, int out) { return in <= kTIn && W == kTW && out
 template <bool ACTOR, int NOP>
 static void launch_tiled(const PpoBranchArgs& a, int grid, cudaStream_t s) {
   const size_t sm = sizeof(TiledSmem<NOP>);
-  cudaFuncSetAttribute(ppo_branch_tiled_kernel<ACTOR, NOP>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+  smem_optin(ppo_branch_tiled_kernel<ACTOR, NOP>);
   ppo_branch_tiled_kernel<ACTOR, NOP><<<grid, kThreads, sm, s>>>(a);
   ++g_launches;
 }

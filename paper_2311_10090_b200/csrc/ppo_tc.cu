@@ -667,7 +667,7 @@ void ppo_update_tc(const PpoTcArgs& a, int grid, cudaStream_t s) {
   const size_t sm = L.total;
   auto kern = L.ns == 2 ? (a.relu ? ppo_update_tc_kernel<2, 1> : ppo_update_tc_kernel<2, 0>)
                         : (a.relu ? ppo_update_tc_kernel<1, 1> : ppo_update_tc_kernel<1, 0>);
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+  smem_optin(kern);
   kern<<<grid, kThr, sm, s>>>(a);
   ++g_launches;
 }

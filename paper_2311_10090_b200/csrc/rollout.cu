@@ -159,7 +159,7 @@ void rollout_policy_fp32(const PolicyNet& net, const PolicyStep& s, const Rollou
   size_t sm = size_t(net_floats(net.in_dim, net.critic_in, net.width, net.n_act)) * sizeof(float);
   const int staged = sm <= size_t(160) * 1024;
   if (!staged) sm = 0;
-  cudaFuncSetAttribute(policy_fp32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+  smem_optin(policy_fp32_kernel);
   policy_fp32_kernel<<<unsigned((s.R + 127) / 128), 128, sm, st>>>(net, s, b, staged);
   ++g_launches;
 }
@@ -973,7 +973,7 @@ void rollout_policy_bf16(const PolicyNet& net, const PolicyNetBf16& nb, const Po
   }
   if (net.in_dim > kTcMaxKx) {  // wide rows: K-chunked layer 1, one CTA per SM
     const size_t smw = wide_layout(net.n_act).total;
-    cudaFuncSetAttribute(policy_tc_wide_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smw));
+    smem_optin(policy_tc_wide_kernel);
     const int64_t tiles = (s.R + kTcRows - 1) / kTcRows;
     const int64_t grid = cap_grid(std::min<int64_t>(tiles, int64_t(sms)));
     policy_tc_wide_kernel<<<unsigned(grid), kSplit * kTcRows, smw, st>>>(nb, net.in_dim, net.n_act, s, b);
@@ -990,7 +990,7 @@ void rollout_policy_bf16(const PolicyNet& net, const PolicyNetBf16& nb, const Po
                       !std::getenv("MARL_TC_GENERIC");
   auto kern = small ? (spread ? policy_tc_kernel<32, 18, 3, 5> : policy_tc_kernel<32>)
                     : (cent ? policy_tc_kernel<0, 0, 0, 0, true> : policy_tc_kernel<0>);
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+  smem_optin(kern);
   int per_sm = 1;
   cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   static int smem_sm = 0;

@@ -1025,7 +1025,7 @@ void launch_reset_g(const SmaxConfig& c, const Params* dP, const SmaxState& s, c
   size_t sm;
   Plan plan = make_plan<G, UPL>(c, &sm);
   auto fn = smax_reset_kernel<G, UPL>;
-  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+  smem_optin(fn);
   constexpr int EPB = kWarps * Grp<G>::EPW;
   fn<<<unsigned((lc.n + EPB - 1) / EPB), kThreads, sm, lc.stream>>>(dP, s, lc, k, cp, plan);
 }
@@ -1048,7 +1048,7 @@ void launch_step_g(const SmaxConfig& c, const Params* dP, const SmaxState& s, co
   using AnyType = std::integral_constant<int, -1>;
   auto fn = marines ? (full ? pick(Marine{}, std::true_type{}) : pick(Marine{}, std::false_type{}))
                     : (full ? pick(AnyType{}, std::true_type{}) : pick(AnyType{}, std::false_type{}));
-  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+  smem_optin(fn);
   constexpr int EPB = kWarps * Grp<G>::EPW;
   fn<<<unsigned((lc.end - lc.begin + EPB - 1) / EPB), kThreads, sm, lc.stream>>>(dP, s, lc, k, plan);
 }

@@ -737,7 +737,7 @@ template <class R>
 bool launch(const Params& P, const SmaxState& s, const LaunchCommon& lc, bool random, Key k) {
   const size_t sm = size_t(kLW) * R::kWarpBytes;
   auto fn = random ? smax_lane_step_kernel<R, true> : smax_lane_step_kernel<R, false>;
-  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+  smem_optin(fn);
   fn<<<unsigned((lc.end - lc.begin + kLT - 1) / kLT), kLT, sm, lc.stream>>>(P, s, lc, k);
   return true;
 }

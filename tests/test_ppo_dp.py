@@ -112,6 +112,60 @@ def test_two_rank_update_matches_single_device(env_id, cfg, n, T, precision):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("precision", ["fp32", "bf16"])
+def test_two_rank_wide_gradient_matches_single_device(precision):
+    """The wide-input update (Overcooked, 3xTF32 GEMM chain) under the
+    data-parallel hook: each rank's gradient over its own rows of a global
+    minibatch, summed by the hook, equals the single device's gradient over
+    the whole minibatch (fp32 summation-order bar), and so do the loss sums.
+    (Whole training trajectories are not compared here: Adam's first step moves
+    every parameter by +-lr whatever its gradient's size, so entries that
+    cancel to ~0 take the sign of their summation-order noise.)"""
+    import paper_2311_10090_b200 as m
+    from paper_2311_10090_b200 import dist as D
+    env = m.make_env("overcooked_cramped_room_v0", {"max_steps": 40})
+    n, T = 16, 32
+    key = O.key_from_seed(12)
+    single = _trainer(m.VectorEnv(env, n, device=0), n, T, precision)
+    pair = _PairSum()
+    ranks = [_trainer(D.make_sharded(env, n, r, 2, device=0), n, T, precision) for r in range(2)]
+    for r, tr in enumerate(ranks):
+        tr.set_allreduce(pair.hook(r))
+    for tr in [single] + ranks:
+        assert not tr.tensor_core_update
+    single.begin(key)
+    single.collect()
+    R, Rl = single.rollout.R, ranks[0].rollout.R
+    assert ranks[1].rollout.R == Rl and 2 * Rl == R
+    idx = np.random.default_rng(5).choice(T * R, size=T * R // 2, replace=False).astype(np.int32)
+    t, row = idx // R, idx % R
+    local = [(t * Rl + (row - r * Rl))[(row >= r * Rl) & (row < (r + 1) * Rl)].astype(np.int32) for r in range(2)]
+    assert all(len(x) > 0 for x in local)
+    g1, s1 = single.minibatch_grad(idx)
+    out, err = [None, None], []
+
+    def run(r):  # the ranks' collect all-reduces episode counts: both ranks run concurrently
+        try:
+            ranks[r].begin(key)
+            ranks[r].collect()
+            out[r] = ranks[r].minibatch_grad(local[r])
+        except Exception as e:
+            err.append(e)
+            pair.barrier.abort()
+
+    th = [threading.Thread(target=run, args=(r,)) for r in range(2)]
+    for x in th:
+        x.start()
+    for x in th:
+        x.join(300)
+    assert not err, err
+    (ga, sa), (gb, sb) = out
+    assert np.array_equal(ga, gb) and np.array_equal(sa, sb)
+    assert _close(ga, g1, 2e-3), np.abs(ga - g1).max()
+    assert np.allclose(sa, s1, rtol=2e-3, atol=1e-7), (sa, s1)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
 def test_nccl_world_of_one_is_identity(precision):
     import paper_2311_10090_b200 as m
     from paper_2311_10090_b200.ppo import nccl_unique_id
