@@ -292,11 +292,19 @@ struct RnnStepArgs {
   float* h;          // [M][H] running hidden
   float* x;          // cache x_t     [M][in]
   float *hprev, *z, *r, *c, *ah, *hn;  // caches at step t [M][H]
+  float* hnext;       // gates: also write step t+1's h_prev (apply_reset at t+1) here; null: no
+  const float* dhp;   // gru_bwd: the post layer's dh share of step t (carry > 0)
+  int carry;          // gru_bwd: 0 g = dhs; 1 g = dhp; 2 g = (reset at t+1 ? 0 : dhs) + dhp
   struct {
     const float *bzx, *brx, *bnx, *bzh, *brh, *bnh;
   } w;
 };
 void rnn_step_gather(const RnnStepArgs& a, cudaStream_t s);
+// x[t][i][:] = src[t][rows[i]][:] for every t < T at once (the non-recurrent part of sq_gather)
+void rnn_seq_x_gather(const int32_t* rows, int64_t Mc, int T, int64_t R, int in, const float* src, float* x,
+                      cudaStream_t s);
+// dst = (copy ? 0 : dst) + src over n floats
+void rnn_add(float* dst, const float* src, int64_t n, bool copy, cudaStream_t s);
 // GEMM-structured acting step of the collector (many rows)
 void rnn_policy_rows(const PolicyStep& s, const RolloutBufs& b, int in, int CI, int NA, int H, float* xa, float* xc,
                      float* ha, float* hc, float* hc_peek, cudaStream_t st);

@@ -476,7 +476,40 @@ void rnn_chunk_forward(marl_ppo* p, int branch, const int32_t* rows, int64_t Mc)
   a.w.bzh = w.bias6 + 3 * H;
   a.w.brh = w.bias6 + 4 * H;
   a.w.bnh = w.bias6 + 5 * H;
-  for (int t = 0; t < r->T; ++t) {
+  const int T = r->T;
+  const int64_t Kc = int64_t(T) * Mc;
+  if (!p->rnn_stepwise) {
+    // everything but the recurrence runs once over all T x Mc (t, row) pairs: the
+    // x gather, embed, the GRU's input path gx = e.[Wz;Wr;Wn]^T, then after the
+    // sequence the post and head layers (row results identical to per-step GEMMs)
+    rnn_seq_x_gather(rows, Mc, T, r->R, in, a.src, c.x, st);
+    gemm_nt(st, Kc, F, in, c.x, in, w.we, in, c.e, F, 0.0f);
+    rnn_bias_act(c.e, Kc, F, w.be, true, r->relu, st);
+    float* gx = c.daz;  // [Kc][3H] inside the backward's [Kc][4H] buffer, unused until then
+    gemm_nt(st, Kc, 3 * H, F, c.e, F, w.wx, F, gx, 3 * H, 0.0f);
+    a.in = 0;  // sq_gather: h_prev only, and only at t = 0 (the gates write the next step's)
+    for (int t = 0; t < T; ++t) {
+      const size_t k0 = size_t(t) * size_t(Mc);
+      a.t = t;
+      a.hprev = c.h + k0 * H;
+      a.z = c.z + k0 * H;
+      a.r = c.r + k0 * H;
+      a.c = c.c + k0 * H;
+      a.ah = c.ah + k0 * H;
+      a.hn = c.hn + k0 * H;
+      a.hnext = t + 1 < T ? c.h + (k0 + Mc) * H : nullptr;
+      if (t == 0) rnn_step_gather(a, st);
+      gemm_nt(st, Mc, 3 * H, H, a.hprev, H, w.uh, H, p->rnn_gh, 3 * H, 0.0f);
+      rnn_gates(a, gx + k0 * 3 * H, p->rnn_gh, st);
+    }
+    gemm_nt(st, Kc, F, H, c.hn, H, w.wp, H, c.p, F, 0.0f);
+    rnn_bias_act(c.p, Kc, F, w.bp, true, r->relu, st);
+    gemm_nt(st, Kc, out, F, c.p, F, w.wh, F, c.y, out, 0.0f);
+    rnn_bias_act(c.y, Kc, out, w.bh, false, r->relu, st);
+    after_launch();
+    return;
+  }
+  for (int t = 0; t < T; ++t) {  // MARL_RNN_STEPWISE=1: every layer per time step (A/B knob)
     const size_t k0 = size_t(t) * size_t(Mc);
     a.t = t;
     a.x = c.x + k0 * in;
@@ -522,7 +555,37 @@ void rnn_chunk_backward(marl_ppo* p, int branch, const int32_t* rows, int64_t Mc
   a.resets = r->b.resets;
   float* dh = p->rnn_dh;
   float* d4 = c.daz;  // [Kc][4H] = daz | dar | dac | dah
-  for (int t = T - 1; t >= 0; --t) {
+  if (!p->rnn_stepwise) {
+    // head and post over all (t, row) first: dzp = (dy . Wh) * act'(p), the
+    // post layer's share of each step's dh = dzp . Wp; then the recurrence
+    // (gru_backward and the U paths) per step; then the embed path over all
+    // [Kc][H] aliased onto the front of d4 = [Kc][4H]: step t reads its rows
+    // [t Mc H, (t+1) Mc H) before writing d4's [4 t Mc H, 4 (t+1) Mc H), and the
+    // rows of the earlier steps t' < t it still needs lie below t Mc H
+    float* dhp = d4;
+    gemm_nn(st, Kc, F, out, c.dy, out, w.wh, F, c.dzp, F, 0.0f);
+    rnn_act_grad(c.dzp, c.p, Kc * F, r->relu, st);
+    gemm_nn(st, Kc, H, F, c.dzp, F, w.wp, H, dhp, H, 0.0f);
+    for (int t = T - 1; t >= 0; --t) {
+      const size_t k0 = size_t(t) * size_t(Mc);
+      a.t = t;
+      a.hprev = c.h + k0 * H;
+      a.z = c.z + k0 * H;
+      a.r = c.r + k0 * H;
+      a.c = c.c + k0 * H;
+      a.ah = c.ah + k0 * H;
+      a.dhp = dhp + k0 * H;  // gru_bwd folds in the post share and the previous step's cut
+      a.carry = t == T - 1 ? 1 : 2;
+      float* d4t = d4 + k0 * 4 * H;
+      rnn_gru_bwd(a, dh, d4t, dh, st);
+      gemm_nn(st, Mc, H, 2 * H, d4t, 4 * H, w.uh, H, dh, H, 1.0f);
+      gemm_nn(st, Mc, H, H, d4t + 3 * H, 4 * H, w.uh + 2 * H * H, H, dh, H, 1.0f);
+    }
+    a.carry = 0;
+    gemm_nn(st, Kc, F, 3 * H, d4, 4 * H, w.wx, F, c.dze, F, 0.0f);
+    rnn_act_grad(c.dze, c.e, Kc * F, r->relu, st);
+  }
+  for (int t = T - 1; t >= 0 && p->rnn_stepwise; --t) {
     const size_t k0 = size_t(t) * size_t(Mc);
     a.t = t;
     a.hprev = c.h + k0 * H;
@@ -886,6 +949,7 @@ int marl_ppo_create(marl_venv* h, const char* ppo_config_json, int centralized, 
       ar.add(&p->rnn_gx, Mc * 3 * H);
       ar.add(&p->rnn_gh, Mc * 3 * H);
       ar.add(&p->rnn_ones, size_t(rnn_Kc));
+      p->rnn_stepwise = std::getenv("MARL_RNN_STEPWISE") != nullptr;
     }
     ar.add(&p->metrics, size_t(c.update_epochs) * size_t(c.n_minibatches) * 8);
     ar.add(&p->mbst, 1);

@@ -293,7 +293,11 @@ __global__ void gru_gate_kernel(RnnStepArgs a, const float* __restrict__ gx, con
   a.c[q] = cand;
   a.ah[q] = ah;
   a.hn[q] = hn;
-  a.h[q] = hn;
+  if (a.hnext) {  // the next step's sq_gather (h part), fused
+    a.hnext[q] = a.resets[size_t(a.t + 1) * size_t(a.R) + size_t(a.rows[i])] ? 0.0f : hn;
+  } else {
+    a.h[q] = hn;
+  }
 }
 
 __global__ void act_grad_kernel(float* __restrict__ g, const float* __restrict__ y, int64_t n, int relu) {
@@ -309,7 +313,16 @@ __global__ void gru_bwd_kernel(RnnStepArgs a, const float* __restrict__ dhs, flo
   if (q >= a.M * H) return;
   const int64_t i = q / H;
   const int c = int(q - i * H);
-  const float g = dhs[q], z = a.z[q], r = a.r[q], cd = a.c[q];
+  float g;
+  if (a.carry == 0) {
+    g = dhs[q];
+  } else if (a.carry == 1) {
+    g = a.dhp[q];
+  } else {  // the previous step's cut (no gradient across its episode boundary), then + the post layer's share
+    const float d = a.resets[size_t(a.t + 1) * size_t(a.R) + size_t(a.rows[i])] ? 0.0f : dhs[q];
+    g = __fadd_rn(d, a.dhp[q]);
+  }
+  const float z = a.z[q], r = a.r[q], cd = a.c[q];
   const float dz = __fmul_rn(g, __fsub_rn(a.hprev[q], cd));
   const float dc = __fmul_rn(g, __fsub_rn(1.0f, z));
   const float ac = __fmul_rn(dc, __fsub_rn(1.0f, __fmul_rn(cd, cd)));
@@ -406,6 +419,26 @@ RnnWPtrs rnn_weights(const float* p, int in, int F, int H, int out) {
   return RnnWPtrs{w.we, w.be, w.wz, w.uz, w.bzx, w.wp, w.bp, w.wh, w.bh};
 }
 
+__global__ void seq_x_gather_kernel(const int32_t* __restrict__ rows, int64_t Mc, int T, int64_t R, int in,
+                                    const float* __restrict__ src, float* __restrict__ x) {
+  const int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (q >= int64_t(T) * Mc * in) return;
+  const int64_t k = q / in, j = q - k * in, t = k / Mc, i = k - t * Mc;
+  x[q] = __ldg(src + (size_t(t) * size_t(R) + size_t(__ldg(rows + i))) * size_t(in) + j);
+}
+__global__ void add_kernel(float* __restrict__ dst, const float* __restrict__ src, int64_t n, int copy) {
+  const int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (q < n) dst[q] = copy ? src[q] : __fadd_rn(dst[q], src[q]);
+}
+void rnn_seq_x_gather(const int32_t* rows, int64_t Mc, int T, int64_t R, int in, const float* src, float* x,
+                      cudaStream_t s) {
+  seq_x_gather_kernel<<<nb(int64_t(T) * Mc * in), 256, 0, s>>>(rows, Mc, T, R, in, src, x);
+  ++g_launches;
+}
+void rnn_add(float* dst, const float* src, int64_t n, bool copy, cudaStream_t s) {
+  add_kernel<<<nb(n), 256, 0, s>>>(dst, src, n, copy ? 1 : 0);
+  ++g_launches;
+}
 void rnn_step_gather(const RnnStepArgs& a, cudaStream_t s) {
   sq_gather_kernel<<<nb(a.M * std::max(a.in, a.H)), 256, 0, s>>>(a);
   ++g_launches;
