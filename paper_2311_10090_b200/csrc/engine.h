@@ -303,8 +303,6 @@ void rnn_step_gather(const RnnStepArgs& a, cudaStream_t s);
 // x[t][i][:] = src[t][rows[i]][:] for every t < T at once (the non-recurrent part of sq_gather)
 void rnn_seq_x_gather(const int32_t* rows, int64_t Mc, int T, int64_t R, int in, const float* src, float* x,
                       cudaStream_t s);
-// dst = (copy ? 0 : dst) + src over n floats
-void rnn_add(float* dst, const float* src, int64_t n, bool copy, cudaStream_t s);
 // GEMM-structured acting step of the collector (many rows)
 void rnn_policy_rows(const PolicyStep& s, const RolloutBufs& b, int in, int CI, int NA, int H, float* xa, float* xc,
                      float* ha, float* hc, float* hc_peek, cudaStream_t st);
@@ -315,7 +313,6 @@ void rnn_bias_act(float* y, int64_t M, int N, const float* b, bool act, int relu
 void rnn_gates(const RnnStepArgs& a, const float* gx, const float* gh, cudaStream_t s);
 void rnn_act_grad(float* g, const float* y, int64_t n, int relu, cudaStream_t s);
 void rnn_gru_bwd(const RnnStepArgs& a, const float* dhs, float* d4, float* dh, cudaStream_t s);
-void rnn_cut(const RnnStepArgs& a, float* dh, cudaStream_t s);
 
 // flat[k = t*M + i] = t*R + rows[i] (the loss rows of rnn_minibatch, ppo.cpp:472-477)
 void rnn_flat_slots(const int32_t* rows, int64_t M, int T, int64_t R, int32_t* flat, cudaStream_t st);

@@ -289,7 +289,6 @@ struct marl_ppo {
   int64_t rnn_chunk = 0;  // rows per BPTT chunk (caches sized for it)
   int rnn_blocks = 0;     // loss partial blocks of the last minibatch
   float *rnn_h = nullptr, *rnn_gx = nullptr, *rnn_gh = nullptr, *rnn_dh = nullptr, *rnn_ones = nullptr;
-  bool rnn_stepwise = false;   // MARL_RNN_STEPWISE=1: every layer per time step (A/B knob)
   // wide-input fp32 update (ff_minibatch as a GEMM chain, minibatch_grad_wide):
   // per branch the gathered rows, both hidden layers and the head's output and
   // gradient, one [M][W] pair for the backward's layer gradients

@@ -460,10 +460,12 @@ void rnn_chunk_forward(marl_ppo* p, int branch, const int32_t* rows, int64_t Mc)
   const RnnCache& c = branch == 0 ? p->rca : p->rcc;
   const int in = branch == 0 ? r->in_dim : r->critic_in, out = branch == 0 ? r->n_act : 1, F = r->F, H = r->H;
   const RnnWPtrs w = rnn_weights(branch == 0 ? r->params : r->params + r->n_actor, in, F, H, out);
+  const int T = r->T;
+  const int64_t Kc = int64_t(T) * Mc;
   RnnStepArgs a{};
   a.M = Mc;
   a.R = r->R;
-  a.in = in;
+  a.in = 0;  // sq_gather: h_prev only (x is gathered for all steps at once)
   a.H = H;
   a.rows = rows;
   a.resets = r->b.resets;
@@ -476,68 +478,42 @@ void rnn_chunk_forward(marl_ppo* p, int branch, const int32_t* rows, int64_t Mc)
   a.w.bzh = w.bias6 + 3 * H;
   a.w.brh = w.bias6 + 4 * H;
   a.w.bnh = w.bias6 + 5 * H;
-  const int T = r->T;
-  const int64_t Kc = int64_t(T) * Mc;
-  if (!p->rnn_stepwise) {
-    // everything but the recurrence runs once over all T x Mc (t, row) pairs: the
-    // x gather, embed, the GRU's input path gx = e.[Wz;Wr;Wn]^T, then after the
-    // sequence the post and head layers (row results identical to per-step GEMMs)
-    rnn_seq_x_gather(rows, Mc, T, r->R, in, a.src, c.x, st);
-    gemm_nt(st, Kc, F, in, c.x, in, w.we, in, c.e, F, 0.0f);
-    rnn_bias_act(c.e, Kc, F, w.be, true, r->relu, st);
-    float* gx = c.daz;  // [Kc][3H] inside the backward's [Kc][4H] buffer, unused until then
-    gemm_nt(st, Kc, 3 * H, F, c.e, F, w.wx, F, gx, 3 * H, 0.0f);
-    a.in = 0;  // sq_gather: h_prev only, and only at t = 0 (the gates write the next step's)
-    for (int t = 0; t < T; ++t) {
-      const size_t k0 = size_t(t) * size_t(Mc);
-      a.t = t;
-      a.hprev = c.h + k0 * H;
-      a.z = c.z + k0 * H;
-      a.r = c.r + k0 * H;
-      a.c = c.c + k0 * H;
-      a.ah = c.ah + k0 * H;
-      a.hn = c.hn + k0 * H;
-      a.hnext = t + 1 < T ? c.h + (k0 + Mc) * H : nullptr;
-      if (t == 0) rnn_step_gather(a, st);
-      gemm_nt(st, Mc, 3 * H, H, a.hprev, H, w.uh, H, p->rnn_gh, 3 * H, 0.0f);
-      rnn_gates(a, gx + k0 * 3 * H, p->rnn_gh, st);
-    }
-    gemm_nt(st, Kc, F, H, c.hn, H, w.wp, H, c.p, F, 0.0f);
-    rnn_bias_act(c.p, Kc, F, w.bp, true, r->relu, st);
-    gemm_nt(st, Kc, out, F, c.p, F, w.wh, F, c.y, out, 0.0f);
-    rnn_bias_act(c.y, Kc, out, w.bh, false, r->relu, st);
-    after_launch();
-    return;
-  }
-  for (int t = 0; t < T; ++t) {  // MARL_RNN_STEPWISE=1: every layer per time step (A/B knob)
+  // everything but the recurrence runs once over all T x Mc (t, row) pairs (a
+  // row's result does not depend on how many rows share its GEMM): the x
+  // gather, embed, the GRU's input path gx = e.[Wz;Wr;Wn]^T ...
+  rnn_seq_x_gather(rows, Mc, T, r->R, in, a.src, c.x, st);
+  gemm_nt(st, Kc, F, in, c.x, in, w.we, in, c.e, F, 0.0f);
+  rnn_bias_act(c.e, Kc, F, w.be, true, r->relu, st);
+  float* gx = c.daz;  // [Kc][3H] inside the backward's [Kc][4H] buffer, unused until then
+  gemm_nt(st, Kc, 3 * H, F, c.e, F, w.wx, F, gx, 3 * H, 0.0f);
+  // ... the recurrence per step: gh = h_prev.[Uz;Ur;Un]^T and the gates, which
+  // also write the next step's h_prev (apply_reset at t+1) ...
+  for (int t = 0; t < T; ++t) {
     const size_t k0 = size_t(t) * size_t(Mc);
     a.t = t;
-    a.x = c.x + k0 * in;
     a.hprev = c.h + k0 * H;
     a.z = c.z + k0 * H;
     a.r = c.r + k0 * H;
     a.c = c.c + k0 * H;
     a.ah = c.ah + k0 * H;
     a.hn = c.hn + k0 * H;
-    rnn_step_gather(a, st);
-    float* e = c.e + k0 * F;
-    gemm_nt(st, Mc, F, in, a.x, in, w.we, in, e, F, 0.0f);
-    rnn_bias_act(e, Mc, F, w.be, true, r->relu, st);
-    gemm_nt(st, Mc, 3 * H, F, e, F, w.wx, F, p->rnn_gx, 3 * H, 0.0f);
+    a.hnext = t + 1 < T ? c.h + (k0 + Mc) * H : nullptr;
+    if (t == 0) rnn_step_gather(a, st);
     gemm_nt(st, Mc, 3 * H, H, a.hprev, H, w.uh, H, p->rnn_gh, 3 * H, 0.0f);
-    rnn_gates(a, p->rnn_gx, p->rnn_gh, st);
-    float* pp = c.p + k0 * F;
-    gemm_nt(st, Mc, F, H, a.hn, H, w.wp, H, pp, F, 0.0f);
-    rnn_bias_act(pp, Mc, F, w.bp, true, r->relu, st);
-    float* y = c.y + k0 * out;
-    gemm_nt(st, Mc, out, F, pp, F, w.wh, F, y, out, 0.0f);
-    rnn_bias_act(y, Mc, out, w.bh, false, r->relu, st);
+    rnn_gates(a, gx + k0 * 3 * H, p->rnn_gh, st);
   }
+  // ... then post and head over all pairs
+  gemm_nt(st, Kc, F, H, c.hn, H, w.wp, H, c.p, F, 0.0f);
+  rnn_bias_act(c.p, Kc, F, w.bp, true, r->relu, st);
+  gemm_nt(st, Kc, out, F, c.p, F, w.wh, F, c.y, out, 0.0f);
+  rnn_bias_act(c.y, Kc, out, w.bh, false, r->relu, st);
   after_launch();
 }
 
 // rnn_seq_backward (actor_critic.hpp:164-196) of one branch over a chunk, then
 // its weight gradients (matmul_tn over every (t, row)) into G in pack order.
+// D4 = [daz | dar | dah | dac] per (t, row): the hidden path [Uz;Ur;Un] reads
+// columns 0..3H-1 as one operand, the input path [Wz;Wr;Wn] reads 0..2H-1 and dac.
 void rnn_chunk_backward(marl_ppo* p, int branch, const int32_t* rows, int64_t Mc, float* G, bool accumulate) {
   marl_rollout* r = p->ro;
   cudaStream_t st = p->h->stream;
@@ -554,38 +530,18 @@ void rnn_chunk_backward(marl_ppo* p, int branch, const int32_t* rows, int64_t Mc
   a.rows = rows;
   a.resets = r->b.resets;
   float* dh = p->rnn_dh;
-  float* d4 = c.daz;  // [Kc][4H] = daz | dar | dac | dah
-  if (!p->rnn_stepwise) {
-    // head and post over all (t, row) first: dzp = (dy . Wh) * act'(p), the
-    // post layer's share of each step's dh = dzp . Wp; then the recurrence
-    // (gru_backward and the U paths) per step; then the embed path over all
-    // [Kc][H] aliased onto the front of d4 = [Kc][4H]: step t reads its rows
-    // [t Mc H, (t+1) Mc H) before writing d4's [4 t Mc H, 4 (t+1) Mc H), and the
-    // rows of the earlier steps t' < t it still needs lie below t Mc H
-    float* dhp = d4;
-    gemm_nn(st, Kc, F, out, c.dy, out, w.wh, F, c.dzp, F, 0.0f);
-    rnn_act_grad(c.dzp, c.p, Kc * F, r->relu, st);
-    gemm_nn(st, Kc, H, F, c.dzp, F, w.wp, H, dhp, H, 0.0f);
-    for (int t = T - 1; t >= 0; --t) {
-      const size_t k0 = size_t(t) * size_t(Mc);
-      a.t = t;
-      a.hprev = c.h + k0 * H;
-      a.z = c.z + k0 * H;
-      a.r = c.r + k0 * H;
-      a.c = c.c + k0 * H;
-      a.ah = c.ah + k0 * H;
-      a.dhp = dhp + k0 * H;  // gru_bwd folds in the post share and the previous step's cut
-      a.carry = t == T - 1 ? 1 : 2;
-      float* d4t = d4 + k0 * 4 * H;
-      rnn_gru_bwd(a, dh, d4t, dh, st);
-      gemm_nn(st, Mc, H, 2 * H, d4t, 4 * H, w.uh, H, dh, H, 1.0f);
-      gemm_nn(st, Mc, H, H, d4t + 3 * H, 4 * H, w.uh + 2 * H * H, H, dh, H, 1.0f);
-    }
-    a.carry = 0;
-    gemm_nn(st, Kc, F, 3 * H, d4, 4 * H, w.wx, F, c.dze, F, 0.0f);
-    rnn_act_grad(c.dze, c.e, Kc * F, r->relu, st);
-  }
-  for (int t = T - 1; t >= 0 && p->rnn_stepwise; --t) {
+  float* d4 = c.daz;
+  // head and post over all (t, row) first: dzp = (dy . Wh) * act'(p) and the
+  // post layer's share of each step's dh, dzp . Wp -- [Kc][H] aliased onto the
+  // front of d4: step t reads its rows [t Mc H, (t+1) Mc H) before writing d4's
+  // [4 t Mc H, 4 (t+1) Mc H), and the earlier steps' rows it still needs lie below
+  float* dhp = d4;
+  gemm_nn(st, Kc, F, out, c.dy, out, w.wh, F, c.dzp, F, 0.0f);
+  rnn_act_grad(c.dzp, c.p, Kc * F, r->relu, st);
+  gemm_nn(st, Kc, H, F, c.dzp, F, w.wp, H, dhp, H, 0.0f);
+  // the recurrence per step: gru_backward (folding in the post share and the
+  // previous step's episode cut), then dh_prev += [daz|dar|dah] . [Uz;Ur;Un]
+  for (int t = T - 1; t >= 0; --t) {
     const size_t k0 = size_t(t) * size_t(Mc);
     a.t = t;
     a.hprev = c.h + k0 * H;
@@ -593,39 +549,34 @@ void rnn_chunk_backward(marl_ppo* p, int branch, const int32_t* rows, int64_t Mc
     a.r = c.r + k0 * H;
     a.c = c.c + k0 * H;
     a.ah = c.ah + k0 * H;
-    // head and post: dzp = (dy . Wh) * act'(p); dh_step = dzp . Wp + dh
-    float* dzp = c.dzp + k0 * F;
-    gemm_nn(st, Mc, F, out, c.dy + k0 * out, out, w.wh, F, dzp, F, 0.0f);
-    rnn_act_grad(dzp, c.p + k0 * F, Mc * F, r->relu, st);
-    gemm_nn(st, Mc, H, F, dzp, F, w.wp, H, dh, H, t == T - 1 ? 0.0f : 1.0f);
-    // gru_backward: gates, carry dh = g*z, then dx and the gate paths of dh
+    a.dhp = dhp + k0 * H;
+    a.carry = t == T - 1 ? 1 : 2;
     float* d4t = d4 + k0 * 4 * H;
     rnn_gru_bwd(a, dh, d4t, dh, st);
-    float* dze = c.dze + k0 * F;
-    gemm_nn(st, Mc, F, 3 * H, d4t, 4 * H, w.wx, F, dze, F, 0.0f);
-    rnn_act_grad(dze, c.e + k0 * F, Mc * F, r->relu, st);
-    gemm_nn(st, Mc, H, 2 * H, d4t, 4 * H, w.uh, H, dh, H, 1.0f);
-    gemm_nn(st, Mc, H, H, d4t + 3 * H, 4 * H, w.uh + 2 * H * H, H, dh, H, 1.0f);
-    rnn_cut(a, dh, st);
+    gemm_nn(st, Mc, H, 3 * H, d4t, 4 * H, w.uh, H, dh, H, 1.0f);
   }
+  // the embed path over all pairs: dze = ([daz|dar] . [Wz;Wr] + dac . Wn) * act'(e)
+  gemm_nn(st, Kc, F, 2 * H, d4, 4 * H, w.wx, F, c.dze, F, 0.0f);
+  gemm_nn(st, Kc, F, H, d4 + 3 * H, 4 * H, w.wx + size_t(2) * H * F, F, c.dze, F, 1.0f);
+  rnn_act_grad(c.dze, c.e, Kc * F, r->relu, st);
   const float beta = accumulate ? 1.0f : 0.0f;
   const float* ones = p->rnn_ones;
   gemm_tn(st, F, in, Kc, c.dze, F, c.x, in, G, beta);  // embed
   G += size_t(F) * in;
   colsum(st, F, Kc, c.dze, F, ones, G, beta);
   G += F;
-  gemm_tn(st, 3 * H, F, Kc, d4, 4 * H, c.e, F, G, beta);  // wz, wr, wn
-  G += size_t(3) * H * F;
-  gemm_tn(st, 2 * H, H, Kc, d4, 4 * H, c.h, H, G, beta);  // uz, ur
-  G += size_t(2) * H * H;
-  gemm_tn(st, H, H, Kc, d4 + 3 * H, 4 * H, c.h, H, G, beta);  // un
-  G += size_t(H) * H;
-  colsum(st, 3 * H, Kc, d4, 4 * H, ones, G, beta);  // bzx, brx, bnx
-  G += 3 * H;
-  colsum(st, 2 * H, Kc, d4, 4 * H, ones, G, beta);  // bzh, brh
+  gemm_tn(st, 2 * H, F, Kc, d4, 4 * H, c.e, F, G, beta);  // wz, wr
+  G += size_t(2) * H * F;
+  gemm_tn(st, H, F, Kc, d4 + 3 * H, 4 * H, c.e, F, G, beta);  // wn
+  G += size_t(H) * F;
+  gemm_tn(st, 3 * H, H, Kc, d4, 4 * H, c.h, H, G, beta);  // uz, ur, un
+  G += size_t(3) * H * H;
+  colsum(st, 2 * H, Kc, d4, 4 * H, ones, G, beta);  // bzx, brx
   G += 2 * H;
-  colsum(st, H, Kc, d4 + 3 * H, 4 * H, ones, G, beta);  // bnh
+  colsum(st, H, Kc, d4 + 3 * H, 4 * H, ones, G, beta);  // bnx
   G += H;
+  colsum(st, 3 * H, Kc, d4, 4 * H, ones, G, beta);  // bzh, brh, bnh
+  G += 3 * H;
   gemm_tn(st, F, H, Kc, c.dzp, F, c.hn, H, G, beta);  // post
   G += size_t(F) * H;
   colsum(st, F, Kc, c.dzp, F, ones, G, beta);
@@ -949,7 +900,6 @@ int marl_ppo_create(marl_venv* h, const char* ppo_config_json, int centralized, 
       ar.add(&p->rnn_gx, Mc * 3 * H);
       ar.add(&p->rnn_gh, Mc * 3 * H);
       ar.add(&p->rnn_ones, size_t(rnn_Kc));
-      p->rnn_stepwise = std::getenv("MARL_RNN_STEPWISE") != nullptr;
     }
     ar.add(&p->metrics, size_t(c.update_epochs) * size_t(c.n_minibatches) * 8);
     ar.add(&p->mbst, 1);

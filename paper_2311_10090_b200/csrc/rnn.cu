@@ -327,18 +327,11 @@ __global__ void gru_bwd_kernel(RnnStepArgs a, const float* __restrict__ dhs, flo
   const float dc = __fmul_rn(g, __fsub_rn(1.0f, z));
   const float ac = __fmul_rn(dc, __fsub_rn(1.0f, __fmul_rn(cd, cd)));
   float* o = d4 + i * 4 * H;
-  o[2 * H + c] = ac;
-  o[3 * H + c] = __fmul_rn(ac, r);
+  o[3 * H + c] = ac;                  // dac
+  o[2 * H + c] = __fmul_rn(ac, r);    // dah
   o[H + c] = __fmul_rn(__fmul_rn(__fmul_rn(ac, a.ah[q]), r), __fsub_rn(1.0f, r));
   o[c] = __fmul_rn(__fmul_rn(dz, z), __fsub_rn(1.0f, z));
   dh[q] = __fmul_rn(g, z);
-}
-
-__global__ void cut_kernel(RnnStepArgs a, float* __restrict__ dh) {  // no gradient across episode cuts
-  const int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (q >= a.M * a.H) return;
-  const int64_t i = q / a.H;
-  if (a.resets[size_t(a.t) * size_t(a.R) + size_t(a.rows[i])]) dh[q] = 0.0f;
 }
 
 unsigned nb(int64_t n) { return unsigned(std::max<int64_t>((n + 255) / 256, 1)); }
@@ -426,17 +419,9 @@ __global__ void seq_x_gather_kernel(const int32_t* __restrict__ rows, int64_t Mc
   const int64_t k = q / in, j = q - k * in, t = k / Mc, i = k - t * Mc;
   x[q] = __ldg(src + (size_t(t) * size_t(R) + size_t(__ldg(rows + i))) * size_t(in) + j);
 }
-__global__ void add_kernel(float* __restrict__ dst, const float* __restrict__ src, int64_t n, int copy) {
-  const int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (q < n) dst[q] = copy ? src[q] : __fadd_rn(dst[q], src[q]);
-}
 void rnn_seq_x_gather(const int32_t* rows, int64_t Mc, int T, int64_t R, int in, const float* src, float* x,
                       cudaStream_t s) {
   seq_x_gather_kernel<<<nb(int64_t(T) * Mc * in), 256, 0, s>>>(rows, Mc, T, R, in, src, x);
-  ++g_launches;
-}
-void rnn_add(float* dst, const float* src, int64_t n, bool copy, cudaStream_t s) {
-  add_kernel<<<nb(n), 256, 0, s>>>(dst, src, n, copy ? 1 : 0);
   ++g_launches;
 }
 void rnn_step_gather(const RnnStepArgs& a, cudaStream_t s) {
@@ -457,10 +442,6 @@ void rnn_act_grad(float* g, const float* y, int64_t n, int relu, cudaStream_t s)
 }
 void rnn_gru_bwd(const RnnStepArgs& a, const float* dhs, float* d4, float* dh, cudaStream_t s) {
   gru_bwd_kernel<<<nb(a.M * a.H), 256, 0, s>>>(a, dhs, d4, dh);
-  ++g_launches;
-}
-void rnn_cut(const RnnStepArgs& a, float* dh, cudaStream_t s) {
-  cut_kernel<<<nb(a.M * a.H), 256, 0, s>>>(a, dh);
   ++g_launches;
 }
 
