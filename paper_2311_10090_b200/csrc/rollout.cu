@@ -641,9 +641,41 @@ __global__ void __launch_bounds__(kSplit * kTcRows) policy_tc_kernel(PolicyNetBf
 // chunk two back has been committed.  Layers 2-3, sampling and the buffer
 // writes are the staged kernel's.
 struct WideLayout {
-  uint32_t wbuf[2], xbuf[2], w2a, w2c, w3a, w3c, ha, hc, legal, resets, active, bias, bar, bar_w[2], bar_c[2],
-      tmem_slot, total;
+  uint32_t wbuf[2], xbuf[2], ostage[2], w2a, w2c, w3a, w3c, ha, hc, legal, resets, active, bias, bar, bar_w[2],
+      bar_c[2], tmem_slot, total;
 };
+constexpr int kOsPitch = 72;  // fp32 observation staging rows: the 16-byte-aligned 68-float superset of 64 columns, + 4
+
+// cp.async of SZ bytes (4, 8 or 16), zero-filled beyond src_bytes
+template <int SZ>
+__device__ __forceinline__ void cpa(void* sdst, const void* gsrc, uint32_t src_bytes) {
+  if constexpr (SZ == 16)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(sdst)), "l"(gsrc), "r"(src_bytes)
+                 : "memory");
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;" ::"r"(smem_u32(sdst)), "l"(gsrc), "n"(SZ),
+                 "r"(src_bytes)
+                 : "memory");
+}
+
+// The [128 rows x 64 columns] fp32 observation block of chunk c of the tile at
+// rb into a staging buffer with 16-byte copies whatever D's alignment: row i's
+// columns start at float e = (rb + i) D + 64c, and the 17 copies cover the
+// aligned superset [e & ~3, (e & ~3) + 68), so the row's data sits at offset
+// e & 3 of its staging row (columns past D belong to the next row: the builder
+// masks them).  Copies past the end of the observations (or of R) read nothing
+// (zero-filled).  One commit group per call, possibly empty.
+__device__ __forceinline__ void stage_obs(float* dst, const float* obs, int64_t R, int D, int64_t rb, int c) {
+  const int nrows = int(rb < R ? min64(kTcRows, R - rb) : 0);
+  const int64_t total = R * int64_t(D);
+  for (int idx = threadIdx.x; idx < kTcRows * 17; idx += kSplit * kTcRows) {
+    const int row = idx / 17, g = idx - row * 17;
+    const int64_t e4 = ((rb + row) * int64_t(D) + 64 * c) & ~int64_t(3), q = e4 + 4 * g;
+    int64_t nv = row < nrows ? total - q : 0;
+    nv = nv < 0 ? 0 : nv > 4 ? 4 : nv;
+    cpa<16>(dst + row * kOsPitch + 4 * g, nv ? obs + q : obs, uint32_t(nv * 4));
+  }
+}
 
 __host__ __device__ inline WideLayout wide_layout(int n_act) {
   WideLayout L{};
@@ -656,6 +688,7 @@ __host__ __device__ inline WideLayout wide_layout(int n_act) {
   };
   for (int q = 0; q < 2; ++q) L.wbuf[q] = take(128 * 64 * 2, 1024);
   for (int q = 0; q < 2; ++q) L.xbuf[q] = take(kTcRows * 64 * 2, 1024);
+  for (int q = 0; q < 2; ++q) L.ostage[q] = take(kTcRows * kOsPitch * 4, 16);
   L.w2a = take(64 * 64 * 2, 128);
   L.w2c = take(64 * 64 * 2, 128);
   L.w3a = take(64 * 64 * 2, 128);  // actor head: up to 64 actions
@@ -683,6 +716,7 @@ __global__ void __launch_bounds__(kSplit * kTcRows, 1) policy_tc_wide_kernel(Pol
           *hc = base + L.hc;
   uint8_t* wbuf[2] = {base + L.wbuf[0], base + L.wbuf[1]};
   uint8_t* xbuf[2] = {base + L.xbuf[0], base + L.xbuf[1]};
+  float* ostage[2] = {reinterpret_cast<float*>(base + L.ostage[0]), reinterpret_cast<float*>(base + L.ostage[1])};
   uint8_t* s_legal = base + L.legal;
   uint8_t* s_resets = base + L.resets;
   float* s_active = reinterpret_cast<float*>(base + L.active);
@@ -691,7 +725,8 @@ __global__ void __launch_bounds__(kSplit * kTcRows, 1) policy_tc_wide_kernel(Pol
   uint64_t* bar_w[2] = {reinterpret_cast<uint64_t*>(base + L.bar_w[0]), reinterpret_cast<uint64_t*>(base + L.bar_w[1])};
   uint64_t* bar_c[2] = {reinterpret_cast<uint64_t*>(base + L.bar_c[0]), reinterpret_cast<uint64_t*>(base + L.bar_c[1])};
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(base + L.tmem_slot);
-  const int tid = threadIdx.x & (kTcRows - 1), part = threadIdx.x >> 7, warp = threadIdx.x >> 5;
+  const int tid = threadIdx.x & (kTcRows - 1), part = threadIdx.x >> 7, warp = threadIdx.x >> 5,
+            lane = threadIdx.x & 31;
   const int64_t n_tiles = (s.R + kTcRows - 1) / kTcRows;
   const int D = s.D, AA = s.A, KX = tc_kx(in_dim), NC = KX / 64;
   const int hn = n_act <= 16 ? 16 : (n_act + 15) / 16 * 16;  // actor head MMA N
@@ -726,6 +761,13 @@ __global__ void __launch_bounds__(kSplit * kTcRows, 1) policy_tc_wide_kernel(Pol
   const bool act_mode = !s.bootstrap;
   uint32_t phase = 0;
   int64_t cc = 0;  // chunks issued by this CTA (buffer cc & 1, its (cc >> 1)-th use)
+  // the observation block of chunk cc + 1 streams into staging buffer (cc + 1) & 1
+  // while chunk cc is built (cp.async, 16-byte copies)
+  auto prefetch = [&](int64_t tl, int c, int q) {
+    stage_obs(ostage[q], s.env_obs, s.R, D, tl * kTcRows, c);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  prefetch(blockIdx.x, 0, 0);
 
   for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
     const int64_t r0 = tile * kTcRows, r = r0 + tid;
@@ -734,8 +776,6 @@ __global__ void __launch_bounds__(kSplit * kTcRows, 1) policy_tc_wide_kernel(Pol
     const size_t slot0 = size_t(s.t) * size_t(s.R) + size_t(r0);
     const int64_t e = r < 0x7fffffff ? int64_t(uint32_t(r) / uint32_t(AA)) : r / AA;
     const int a = int(r - e * AA);
-    const float* orow = s.env_obs + size_t(r) * size_t(D);
-    float* brow = b.obs + (slot0 + size_t(tid)) * size_t(in_dim);
     if (live && act_mode && part == 0) {  // write_legal / agent_active (team.cpp:35-42)
       s_resets[tid] = s.prev_finished ? s.prev_finished[e] : uint8_t(1);
       uint8_t* lg = s_legal + tid * n_act;
@@ -752,25 +792,48 @@ __global__ void __launch_bounds__(kSplit * kTcRows, 1) policy_tc_wide_kernel(Pol
     // ---- layer 1, K-chunked
     for (int c = 0; c < NC; ++c, ++cc) {
       const int bs = int(cc & 1);
+      // the next chunk's observation block (this tile's, else the next tile's first)
+      if (c + 1 < NC)
+        prefetch(tile, c + 1, bs ^ 1);
+      else
+        prefetch(tile + gridDim.x, 0, bs ^ 1);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");  // this chunk's block has landed (own copies)
+      __syncthreads();                                       // (everyone's)
       // the MMAs of chunk cc - 2 read this buffer pair
       if (cc >= 2) mbar_wait(bar_c[bs], uint32_t((cc - 2) >> 1) & 1u);
       if (threadIdx.x == 0)
         bulk_load_g2s(wbuf[bs], nb.a1 + size_t(c) * (128 * 64), 128 * 64 * 2, bar_w[bs]);
-      const int k0 = 64 * c + 32 * part;
-      float x[32];
+      // the chunk's [128 rows x 64 columns] X block, built warp-cooperatively: a
+      // warp instruction covers 8 rows x 32 columns (4 lanes x 8 columns per row),
+      // so the observation loads and buffer-row stores are 32-byte segments and
+      // each lane's bf16 octet is one conflict-free 16-byte canonical store
+      for (int it = warp; it < 2 * (kTcRows / 8); it += kSplit * kTcRows / 32) {
+        const int rr = (it >> 1) * 8 + (lane >> 2), k = 64 * c + 32 * (it & 1) + 8 * (lane & 3);
+        const bool lv = rr < rows;
+        float x[8];
+        const float* sv = ostage[bs] + rr * kOsPitch + int(((r0 + rr) * int64_t(D) + 64 * c) & 3) + (k - 64 * c);
+        if (k + 8 <= D) {
 #pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        const int k = k0 + j;
-        x[j] = (live && k < D) ? __ldg(orow + k) : 0.0f;
-        if (live && AA > 1 && k == D + a) x[j] = 1.0f;
+          for (int j = 0; j < 8; ++j) x[j] = sv[j];  // zero for rows beyond R
+        } else {  // past the observation: zeros, then the agent one-hot (TeamLayout::write_input)
+          const int ar = lv && AA > 1 ? int((r0 + rr) % AA) : -1;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) x[j] = k + j < D ? sv[j] : (k + j == D + ar ? 1.0f : 0.0f);
+        }
+        if (lv && act_mode) {
+          float* br = b.obs + (slot0 + size_t(rr)) * size_t(in_dim);
+          if (k + 8 <= in_dim && (in_dim & 1) == 0) {
+            float2* b2 = reinterpret_cast<float2*>(br + k);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) b2[j] = make_float2(x[2 * j], x[2 * j + 1]);
+          } else {
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              if (k + j < in_dim) br[k + j] = x[j];
+          }
+        }
+        put8(xbuf[bs], 64, rr, k - 64 * c, x);
       }
-      if (live && act_mode) {
-#pragma unroll
-        for (int j = 0; j < 32; ++j)
-          if (k0 + j < in_dim) brow[k0 + j] = x[j];
-      }
-#pragma unroll
-      for (int j = 0; j < 32; j += 8) put8(xbuf[bs], 64, tid, 32 * part + j, x + j);
       fence_proxy_async_smem();
       __syncthreads();
       if (threadIdx.x == 0) {
@@ -883,6 +946,7 @@ __global__ void __launch_bounds__(kSplit * kTcRows, 1) policy_tc_wide_kernel(Pol
     if (threadIdx.x == 0) bulk_wait_read<0>();  // the legal tile has been read out before it is rebuilt
     __syncthreads();  // TMEM columns and hidden tiles are reused by the next tile
   }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");  // the last (empty) prefetch
   if (threadIdx.x == 0) bulk_wait<0>();
   __syncthreads();
   if (warp == 0)
