@@ -38,7 +38,7 @@ WORKLOADS = {
     "ippo": ("MPE_simple_spread_v3", {}, 1 << 20, "IPPO rollout on MPE simple_spread, 2^20 envs x 128 steps, "
              "bf16 actor+critic on tcgen05, configs[4]"),
     "ippo_oc": ("overcooked_cramped_room_v0", {}, 1 << 16, "IPPO rollout on Overcooked cramped_room, 2^16 envs x "
-                "128 steps, bf16 tcgen05 wide-row policy (520 + 2 input columns, K-chunked layer 1)"),
+                "128 steps, bf16 tcgen05 wide-row policy (541 + 2 input columns, K-chunked layer 1)"),
     # one "step" is one train_ippo update (collect + update_epochs x n_minibatches)
     "ppo": ("MPE_simple_spread_v3", {}, 1 << 16, "IPPO training update on MPE simple_spread (collect 128 steps + "
             "5 epochs x 2 minibatches of PPO), PpoConfig defaults"),
@@ -47,7 +47,7 @@ WORKLOADS = {
     "ppo_smax": ("SMAX_5m_vs_6m", THREE_M, 1 << 14, "IPPO training update on SMAX 3m (collect 128 steps + 5 epochs x "
                  "2 minibatches of PPO; 95-wide observations), PpoConfig defaults"),
     "ppo_oc": ("overcooked_cramped_room_v0", {}, 1 << 14, "IPPO training update on Overcooked cramped_room (collect "
-               "128 steps + 5 epochs x 2 minibatches of PPO; 520 + 2 wide observations, fp32-accurate GEMM-chain "
+               "128 steps + 5 epochs x 2 minibatches of PPO; 541 + 2 wide observations, fp32-accurate GEMM-chain "
                "update), PpoConfig defaults"),
 }
 PPO_WORKLOADS = ("ppo", "ppo_rnn", "ppo_smax", "ppo_oc")

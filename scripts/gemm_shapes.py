@@ -36,13 +36,13 @@ def case(name, Mm, N, K, A, sam, sak, B, sbn, sbk, ref):
     print(f"{name:44s} tc {us:8.1f} us ({gb * 1e6 / us:6.0f} GB/s)   cuBLAS sgemm {ub:8.1f} us")
 
 
-W, I, ld = 64, 522, 524
+W, I, ld = 64, 543, 544
 X = torch.randn(M, ld, device="cuda")
 Xv = X[:, :I]
 W1s = torch.randn(2 * W, ld, device="cuda")
-case(f"Z1 stacked  {M}x128x522", M, 2 * W, I, X, ld, 1, W1s, ld, 1, lambda: Xv @ W1s[:, :I].t())
+case(f"Z1 stacked  {M}x128x543", M, 2 * W, I, X, ld, 1, W1s, ld, 1, lambda: Xv @ W1s[:, :I].t())
 D1 = torch.randn(M, 2 * W, device="cuda")
-case(f"dW1 stacked 128x522x{M}", 2 * W, I, M, D1, 1, 2 * W, X, 1, ld, lambda: D1.t() @ Xv)
+case(f"dW1 stacked 128x543x{M}", 2 * W, I, M, D1, 1, 2 * W, X, 1, ld, lambda: D1.t() @ Xv)
 H1 = torch.randn(M, 2 * W, device="cuda")
 W2 = torch.randn(W, W, device="cuda")
 case(f"Z2 {M}x64x64 (lda 128)", M, W, W, H1, 2 * W, 1, W2, W, 1, lambda: H1[:, :W] @ W2.t())
