@@ -745,10 +745,19 @@ bool launch(const Params& P, const SmaxState& s, const LaunchCommon& lc, bool ra
 }  // namespace
 
 // One-thread-per-env instances for the small rosters; false -> the caller
-// uses the lane-group kernel (smax.cu).  MARL_SMAX_GROUP=1 forces the latter.
+// uses the lane-group kernel (smax.cu).  MARL_SMAX_GROUP=1 forces the latter,
+// MARL_SMAX_LANE=1 the former.
 bool smax_lane_launch_step(const SmaxConfig& c, const SmaxState& s, const LaunchCommon& lc, bool random,
                            KeyWords step_key) {
   if (std::getenv("MARL_SMAX_GROUP")) return false;
+  // small batches: one thread per env leaves most warp slots empty (16 384 envs:
+  // 3.5 warps per SM) and the lane-group kernel, G lanes per env, is faster --
+  // 3m at 16 384 envs 0.125 vs 0.141 ms, at 32 768 0.193 vs 0.151 ms; 2s3z at
+  // 32 768 0.78 vs 0.83 ms, at 49 152 1.12 vs 0.88 ms (same-box runs).
+  // MARL_SMAX_LANE=1 forces this kernel at any size (the parity tests).
+  static const char* lane_min_env = std::getenv("MARL_SMAX_LANE_MIN");
+  const int64_t lane_min = lane_min_env ? std::atoll(lane_min_env) : (c.na + c.ne <= 6 ? 24576 : 40960);
+  if (lc.end - lc.begin < lane_min && !std::getenv("MARL_SMAX_LANE")) return false;
   const Params& dP = *static_cast<const Params*>(c.host_params);
   const Key k = to_key(step_key);
   bool marines = !c.random_types;

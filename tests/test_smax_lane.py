@@ -1,6 +1,8 @@
 """The one-thread-per-env SMAX step (smax_lane.cu: 3m, 5m_vs_6m, 2s3z,
 smacv2_5_units) against the lane-group kernel (smax.cu, forced with
-MARL_SMAX_GROUP=1) and against the oracle at the bench shape.
+MARL_SMAX_GROUP=1; the lane kernel forced with MARL_SMAX_LANE=1, since by
+default it only takes batches of >= 24 576 envs) and against the oracle at the
+bench shape.
 
 Both kernels are separately parity-tested against the oracle at small sizes
 (test_gpu_parity.py runs whichever kernel the roster selects); here they must
@@ -28,8 +30,10 @@ def _run(env_id, cfg, n, T, group, monkeypatch, explicit=False):
     import paper_2311_10090_b200 as m
     if group:
         monkeypatch.setenv("MARL_SMAX_GROUP", "1")
-    else:
+        monkeypatch.delenv("MARL_SMAX_LANE", raising=False)
+    else:  # the lane kernel at any size (by default it takes batches of >= 24 576 envs)
         monkeypatch.delenv("MARL_SMAX_GROUP", raising=False)
+        monkeypatch.setenv("MARL_SMAX_LANE", "1")
     v = m.VectorEnv(m.make_env(env_id, cfg), n, device=0)
     n_info = 3
     key, ak = probe_keys(71, T)
