@@ -477,7 +477,11 @@ def run_gpu_ppo(args, rank, world, local_rank):
                                      "and weight-gradient GEMMs, fp32 TMEM accumulation)" if tr.tensor_core_update
                                 else "PPO update phase (wide rows: 3xTF32 tcgen05 GEMM chain, layer-1 product and "
                                      "weight gradient dominant; 3 tf32 MMAs per product, counted once)"),
-                     "flop_per_row_pass": fpr},
+                     "flop_per_row_pass": fpr,
+                     # fp32-accurate paths: tf32 MMAs run at half the bf16 rate and 3xTF32 issues three per
+                     # product, so bf16 peak / 6 is their tensor ceiling (a derived figure, stated beside frac)
+                     "frac_vs_3xtf32_ceiling": (tflops / (peak / 6.0)) if (recurrent or not tr.tensor_core_update)
+                     else None},
         "cpu_baseline": cpu,
         "e2e": {"value": world * n_envs * A * T * e2e_steps / sec, "unit": "agent-steps/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": int(a.nbytes + c.nbytes + 12 * 8), "steps": e2e_steps,
