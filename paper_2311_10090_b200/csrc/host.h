@@ -214,6 +214,7 @@ struct marl_rollout {
   Arena arena;
   RolloutBufs b{};
   float* params = nullptr;     // packed actor | critic (fp32, nn::pack order)
+  float* critic_al = nullptr;  // recurrent: a 16-byte-aligned copy of the critic's parameters (rnn_critic_params)
   uint16_t* images = nullptr;  // bf16 UMMA operand images (tcgen05 path)
   float* bias = nullptr;
   int32_t* agent_actions = nullptr;
@@ -230,6 +231,17 @@ struct marl_rollout {
 };
 
 namespace mhost {
+// The recurrent critic's parameters for the 3xTF32 GEMMs: params + n_actor
+// when that is 16-byte aligned, else a fresh aligned copy (the GEMMs' staging
+// falls back to 4-byte copies on a misaligned weight operand: 25-30 % slower)
+inline const float* rnn_critic_params(marl_rollout* r, cudaStream_t st) {
+  const float* c = r->params + r->n_actor;
+  if (reinterpret_cast<uintptr_t>(c) % 16 == 0 || !r->critic_al) return c;
+  cuda_check(cudaMemcpyAsync(r->critic_al, c, size_t(r->n_critic) * 4, cudaMemcpyDeviceToDevice, st),
+             "cudaMemcpyAsync (aligned critic)");
+  return r->critic_al;
+}
+
 struct PpoCfg {  // PpoConfig (ppo.hpp:30-55) with its defaults
   int64_t total_timesteps = 1000000;
   int n_envs = 16, n_rollout_steps = 128;
@@ -292,6 +304,7 @@ struct marl_ppo {
   // wide-input fp32 update (ff_minibatch as a GEMM chain, minibatch_grad_wide):
   // per branch the gathered rows, both hidden layers and the head's output and
   // gradient, one [M][W] pair for the backward's layer gradients
+  const float* rnn_critic_w = nullptr;  // the critic's (aligned) parameters for this minibatch
   bool wide = false;
   float* wx[2] = {nullptr, nullptr};  // [M][ldx]: the actor's rows, the critic's (== wx[0] for IPPO)
   int wldx[2] = {0, 0};

@@ -459,7 +459,7 @@ void rnn_chunk_forward(marl_ppo* p, int branch, const int32_t* rows, int64_t Mc)
   cudaStream_t st = p->h->stream;
   const RnnCache& c = branch == 0 ? p->rca : p->rcc;
   const int in = branch == 0 ? r->in_dim : r->critic_in, out = branch == 0 ? r->n_act : 1, F = r->F, H = r->H;
-  const RnnWPtrs w = rnn_weights(branch == 0 ? r->params : r->params + r->n_actor, in, F, H, out);
+  const RnnWPtrs w = rnn_weights(branch == 0 ? r->params : p->rnn_critic_w, in, F, H, out);
   const int T = r->T;
   const int64_t Kc = int64_t(T) * Mc;
   RnnStepArgs a{};
@@ -519,7 +519,7 @@ void rnn_chunk_backward(marl_ppo* p, int branch, const int32_t* rows, int64_t Mc
   cudaStream_t st = p->h->stream;
   const RnnCache& c = branch == 0 ? p->rca : p->rcc;
   const int in = branch == 0 ? r->in_dim : r->critic_in, out = branch == 0 ? r->n_act : 1, F = r->F, H = r->H;
-  const RnnWPtrs w = rnn_weights(branch == 0 ? r->params : r->params + r->n_actor, in, F, H, out);
+  const RnnWPtrs w = rnn_weights(branch == 0 ? r->params : p->rnn_critic_w, in, F, H, out);
   const int T = r->T;
   const int64_t Kc = int64_t(T) * Mc;
   RnnStepArgs a{};
@@ -598,6 +598,7 @@ void minibatch_grad_rnn(marl_ppo* p, const int32_t* rows, int64_t M) {
   // advantage statistics over the whole minibatch's [t][i] rows
   rnn_flat_slots(rows, M, T, r->R, p->rnn_flat, st);
   ppo_adv_stats(r->b, p->rnn_flat, K, p->adv_part, p->adv_part2, p->adv_g, p->mbst, st, {});
+  p->rnn_critic_w = rnn_critic_params(r, st);  // the parameters are fixed within the minibatch
   // then the rows in chunks whose BPTT caches fit the budget; gradients and
   // per-block loss sums accumulate over the chunks
   const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(M, p->rnn_chunk));

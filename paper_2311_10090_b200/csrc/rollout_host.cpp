@@ -67,12 +67,13 @@ PolicyNetBf16 net_bf16_of(const marl_rollout* r) {
 // per-row kernel up to the GEMMs' summation order.
 void rnn_collect_gemm(marl_rollout* r, const PolicyStep& s) {
   cudaStream_t st = r->h->stream;
+  const float* critic = rnn_critic_params(r, st);
   const int64_t R = r->R;
   const int in = r->in_dim, CI = r->critic_in, NA = r->n_act, F = r->F, H = r->H;
   rnn_policy_rows(s, r->b, in, CI, NA, H, r->s_xa, r->s_xc, r->h_actor, r->h_critic, r->s_hpeek, st);
   for (int branch = (s.bootstrap ? 1 : 0); branch < 2; ++branch) {
     const int bin = branch == 0 ? in : CI, out = branch == 0 ? NA : 1;
-    const RnnWPtrs w = rnn_weights(branch == 0 ? r->params : r->params + r->n_actor, bin, F, H, out);
+    const RnnWPtrs w = rnn_weights(branch == 0 ? r->params : critic, bin, F, H, out);
     float* h = branch == 0 ? r->h_actor : (s.bootstrap ? r->s_hpeek : r->h_critic);
     const float* x = branch == 0 ? r->s_xa : r->s_xc;
     float* y = branch == 0 ? r->s_ya : r->s_yc;
@@ -229,6 +230,7 @@ marl_rollout* rollout_create_impl(marl_venv* h, int T, int width, int n_layers, 
       r->H = hidden;
       for (float** q : {&r->h_actor, &r->h_critic, &r->h0_actor, &r->h0_critic})
         ar.add(q, size_t(r->R) * size_t(hidden));
+      ar.add(&r->critic_al, size_t(r->n_critic));
       const char* mode = std::getenv("MARL_RNN_COLLECT");
       r->rnn_gemm = mode ? std::string(mode) == "gemm" : r->R >= 4096;
       if (r->rnn_gemm) {
