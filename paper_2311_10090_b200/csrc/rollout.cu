@@ -665,10 +665,10 @@ __device__ __forceinline__ void cpa(void* sdst, const void* gsrc, uint32_t src_b
 // e & 3 of its staging row (columns past D belong to the next row: the builder
 // masks them).  Copies past the end of the observations (or of R) read nothing
 // (zero-filled).  One commit group per call, possibly empty.
-__device__ __forceinline__ void stage_obs(float* dst, const float* obs, int64_t R, int D, int64_t rb, int c) {
+__device__ __forceinline__ void stage_obs(float* dst, const float* obs, int64_t R, int D, int64_t rb, int c, int nth) {
   const int nrows = int(rb < R ? min64(kTcRows, R - rb) : 0);
   const int64_t total = R * int64_t(D);
-  for (int idx = threadIdx.x; idx < kTcRows * 17; idx += kSplit * kTcRows) {
+  for (int idx = threadIdx.x; idx < kTcRows * 17; idx += nth) {
     const int row = idx / 17, g = idx - row * 17;
     const int64_t e4 = ((rb + row) * int64_t(D) + 64 * c) & ~int64_t(3), q = e4 + 4 * g;
     int64_t nv = row < nrows ? total - q : 0;
@@ -707,7 +707,11 @@ __host__ __device__ inline WideLayout wide_layout(int n_act) {
   return L;
 }
 
-__global__ void __launch_bounds__(kSplit * kTcRows, 1) policy_tc_wide_kernel(PolicyNetBf16 nb, int in_dim, int n_act,
+#ifndef MARL_WIDE_SPLIT
+#define MARL_WIDE_SPLIT 4
+#endif
+constexpr int kSplitW = MARL_WIDE_SPLIT;  // wide kernel: threads per row (more warps for the X build's memory traffic)
+__global__ void __launch_bounds__(kSplitW * kTcRows, 1) policy_tc_wide_kernel(PolicyNetBf16 nb, int in_dim, int n_act,
                                                                             PolicyStep s, RolloutBufs b) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   const WideLayout L = wide_layout(n_act);
@@ -764,7 +768,7 @@ __global__ void __launch_bounds__(kSplit * kTcRows, 1) policy_tc_wide_kernel(Pol
   // the observation block of chunk cc + 1 streams into staging buffer (cc + 1) & 1
   // while chunk cc is built (cp.async, 16-byte copies)
   auto prefetch = [&](int64_t tl, int c, int q) {
-    stage_obs(ostage[q], s.env_obs, s.R, D, tl * kTcRows, c);
+    stage_obs(ostage[q], s.env_obs, s.R, D, tl * kTcRows, c, kSplitW * kTcRows);
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
   prefetch(blockIdx.x, 0, 0);
@@ -807,7 +811,7 @@ __global__ void __launch_bounds__(kSplit * kTcRows, 1) policy_tc_wide_kernel(Pol
       // warp instruction covers 8 rows x 32 columns (4 lanes x 8 columns per row),
       // so the observation loads and buffer-row stores are 32-byte segments and
       // each lane's bf16 octet is one conflict-free 16-byte canonical store
-      for (int it = warp; it < 2 * (kTcRows / 8); it += kSplit * kTcRows / 32) {
+      for (int it = warp; it < 2 * (kTcRows / 8); it += kSplitW * kTcRows / 32) {
         const int rr = (it >> 1) * 8 + (lane >> 2), k = 64 * c + 32 * (it & 1) + 8 * (lane & 3);
         const bool lv = rr < rows;
         float x[8];
@@ -859,7 +863,7 @@ __global__ void __launch_bounds__(kSplit * kTcRows, 1) policy_tc_wide_kernel(Pol
     tc_fence_after();
     // ---- epilogue 1 / layer 2 / epilogue 2 / heads: as the staged kernel
 #pragma unroll 1
-    for (int cl = (128 / kSplit) * part; cl < (128 / kSplit) * (part + 1); cl += 32) {
+    for (int cl = (128 / kSplitW) * part; cl < (128 / kSplitW) * (part + 1); cl += 32) {
       float v[32];
       tmem_ld32(tmem + lane_base + uint32_t(cl), v);
 #pragma unroll
@@ -882,7 +886,7 @@ __global__ void __launch_bounds__(kSplit * kTcRows, 1) policy_tc_wide_kernel(Pol
     phase ^= 1;
     tc_fence_after();
 #pragma unroll 1
-    for (int cl = (128 / kSplit) * part; cl < (128 / kSplit) * (part + 1); cl += 32) {
+    for (int cl = (128 / kSplitW) * part; cl < (128 / kSplitW) * (part + 1); cl += 32) {
       float v[32];
       tmem_ld32(tmem + lane_base + uint32_t(cl), v);
 #pragma unroll
@@ -914,7 +918,7 @@ __global__ void __launch_bounds__(kSplit * kTcRows, 1) policy_tc_wide_kernel(Pol
         if (act_mode) b.value[slot0 + tid] = value;
         else b.last_value[r] = value;
       }
-    } else if (hn == 16) {
+    } else if (part == 0 && hn == 16) {
       float hv[16];
       tmem_ld16(tmem + lane_base, hv);
       tc_fence_before();
@@ -928,7 +932,7 @@ __global__ void __launch_bounds__(kSplit * kTcRows, 1) policy_tc_wide_kernel(Pol
         b.actions[slot0 + tid] = pick;
         b.logp[slot0 + tid] = lp;
       }
-    } else {  // up to 64 actions (SMAX 27m_vs_30m: 35)
+    } else if (part == 0) {  // up to 64 actions (SMAX 27m_vs_30m: 35)
       float logits[64];
       tmem_ld32(tmem + lane_base, logits);
       tmem_ld32(tmem + lane_base + 32u, logits + 32);
@@ -1040,7 +1044,7 @@ void rollout_policy_bf16(const PolicyNet& net, const PolicyNetBf16& nb, const Po
     smem_optin(policy_tc_wide_kernel);
     const int64_t tiles = (s.R + kTcRows - 1) / kTcRows;
     const int64_t grid = cap_grid(std::min<int64_t>(tiles, int64_t(sms)));
-    policy_tc_wide_kernel<<<unsigned(grid), kSplit * kTcRows, smw, st>>>(nb, net.in_dim, net.n_act, s, b);
+    policy_tc_wide_kernel<<<unsigned(grid), kSplitW * kTcRows, smw, st>>>(nb, net.in_dim, net.n_act, s, b);
     ++g_launches;
     return;
   }
