@@ -408,7 +408,7 @@ int ppo_stat_blocks(int64_t M);
 // rec (optional): read adv / active from the tcgen05 step's packed records
 void ppo_adv_stats(const RolloutBufs& b, const int32_t* idx, int64_t M, double* part, double* part2, double* g,
                    PpoMbStats* st, cudaStream_t s, const std::function<void(double*, int)>& allreduce,
-                   const PpoRowRec* rec = nullptr);
+                   const PpoRowRec* rec = nullptr, float2* gath = nullptr);
 // sharded update: the global minibatch slots this shard owns, as local slots (order kept), count -> d_count
 size_t ppo_compact_scratch_bytes(int64_t M);
 void ppo_shard_compact(const int32_t* idx, int64_t M, int64_t Rg, int64_t row0, int64_t Rl, int32_t* tmp,

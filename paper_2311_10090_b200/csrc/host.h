@@ -304,6 +304,7 @@ struct marl_ppo {
   // wide-input fp32 update (ff_minibatch as a GEMM chain, minibatch_grad_wide):
   // per branch the gathered rows, both hidden layers and the head's output and
   // gradient, one [M][W] pair for the backward's layer gradients
+  float2* adv_gath = nullptr;  // [per] the minibatch's gathered (adv, active): the variance pass reads them in order
   const float* rnn_critic_w = nullptr;  // the critic's (aligned) parameters for this minibatch
   bool wide = false;
   float* wx[2] = {nullptr, nullptr};  // [M][ldx]: the actor's rows, the critic's (== wx[0] for IPPO)

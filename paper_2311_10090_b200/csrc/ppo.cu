@@ -115,13 +115,16 @@ __device__ double block_sum(double v, double* sh) {
 // adv / active of slot r at [r * stride] (stride 1: the rollout buffer; 8: the
 // tcgen05 step's packed 32-byte records, one sector per row)
 __global__ void adv_sum_kernel(const float* __restrict__ adv, const float* __restrict__ active, int stride,
-                               const int32_t* __restrict__ idx, int64_t M, double* __restrict__ part) {
+                               const int32_t* __restrict__ idx, int64_t M, double* __restrict__ part,
+                               float2* __restrict__ gath) {
   __shared__ double sh[32];
   double s = 0.0, n = 0.0;
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < M; i += int64_t(gridDim.x) * blockDim.x) {
     const int64_t r = int64_t(idx[i]) * stride;
-    const double w = double(active[r]);
-    s += w * double(adv[r]);
+    const float a = adv[r], w32 = active[r];
+    if (gath) gath[i] = make_float2(a, w32);  // the variance pass reads these contiguously
+    const double w = double(w32);
+    s += w * double(a);
     n += w;
   }
   s = block_sum(s, sh);
@@ -155,14 +158,21 @@ __global__ void __launch_bounds__(kFoldThreads) adv_fold_kernel(const double* __
 // (all-reduced) mean of g
 __global__ void adv_var_kernel(const float* __restrict__ adv, const float* __restrict__ active, int stride,
                                const int32_t* __restrict__ idx, int64_t M, const double* __restrict__ g,
-                               double* __restrict__ part2) {
+                               double* __restrict__ part2, const float2* __restrict__ gath) {
   __shared__ double sh[32];
   const double mean = g[1] > 0.0 ? g[0] / g[1] : 0.0;
   double v = 0.0;
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < M; i += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t r = int64_t(idx[i]) * stride;
-    const double d = double(adv[r]) - mean;
-    v += double(active[r]) * d * d;
+    float a, w;
+    if (gath) {
+      const float2 q = gath[i];
+      a = q.x, w = q.y;
+    } else {
+      const int64_t r = int64_t(idx[i]) * stride;
+      a = adv[r], w = active[r];
+    }
+    const double d = double(a) - mean;
+    v += double(w) * d * d;
   }
   v = block_sum(v, sh);
   if (threadIdx.x == 0) part2[blockIdx.x] = v;
@@ -1031,15 +1041,15 @@ int ppo_stat_blocks(int64_t M) { return int(std::min<int64_t>(std::max<int64_t>(
 
 void ppo_adv_stats(const RolloutBufs& b, const int32_t* idx, int64_t M, double* part, double* part2, double* g,
                    PpoMbStats* st, cudaStream_t s, const std::function<void(double*, int)>& allreduce,
-                   const PpoRowRec* rec) {
+                   const PpoRowRec* rec, float2* gath) {
   const int nb = ppo_stat_blocks(M);
   const float* adv = rec ? &rec->adv : b.adv;
   const float* active = rec ? &rec->active : b.active;
   const int stride = rec ? int(sizeof(PpoRowRec) / sizeof(float)) : 1;
-  adv_sum_kernel<<<nb, kRedThreads, 0, s>>>(adv, active, stride, idx, M, part);
+  adv_sum_kernel<<<nb, kRedThreads, 0, s>>>(adv, active, stride, idx, M, part, gath);
   adv_fold_kernel<<<1, kFoldThreads, 0, s>>>(part, nb, g);
   if (allreduce) allreduce(g, 2);
-  adv_var_kernel<<<nb, kRedThreads, 0, s>>>(adv, active, stride, idx, M, g, part2);
+  adv_var_kernel<<<nb, kRedThreads, 0, s>>>(adv, active, stride, idx, M, g, part2, gath);
   adv_fold2_kernel<<<1, kFoldThreads, 0, s>>>(part2, nb, g);
   if (allreduce) allreduce(g + 2, 1);
   adv_final_kernel<<<1, 32, 0, s>>>(g, st);

@@ -405,7 +405,7 @@ void minibatch_grad(marl_ppo* p, const int32_t* idx, int64_t M, bool global = fa
   std::function<void(double*, int)> red;
   if (p->hook) red = [p](double* g, int n) { allreduce(p, g, n, MARL_DTYPE_F64); };
   ppo_adv_stats(p->ro->b, idx, M, p->adv_part, p->adv_part2, p->adv_g, p->mbst, st, red,
-                p->tc ? p->rows_rec : nullptr);
+                p->tc ? p->rows_rec : nullptr, p->adv_gath);
   if (p->tc) {
     const marl_rollout* r = p->ro;
     PpoTcArgs a{};
@@ -597,7 +597,8 @@ void minibatch_grad_rnn(marl_ppo* p, const int32_t* rows, int64_t M) {
   const int64_t K = int64_t(T) * M;
   // advantage statistics over the whole minibatch's [t][i] rows
   rnn_flat_slots(rows, M, T, r->R, p->rnn_flat, st);
-  ppo_adv_stats(r->b, p->rnn_flat, K, p->adv_part, p->adv_part2, p->adv_g, p->mbst, st, {});
+  ppo_adv_stats(r->b, p->rnn_flat, K, p->adv_part, p->adv_part2, p->adv_g, p->mbst, st, {}, nullptr,
+                p->adv_gath);
   p->rnn_critic_w = rnn_critic_params(r, st);  // the parameters are fixed within the minibatch
   // then the rows in chunks whose BPTT caches fit the budget; gradients and
   // per-block loss sums accumulate over the chunks
@@ -881,6 +882,7 @@ int marl_ppo_create(marl_venv* h, const char* ppo_config_json, int centralized, 
     ar.add(&p->spart_c, size_t(p->grid_c) * 6);
     ar.add(&p->adv_part, size_t(std::max(nb, ppo_stat_blocks(rnn_K))) * 2);
     ar.add(&p->adv_part2, size_t(std::max(nb, ppo_stat_blocks(rnn_K))));
+    ar.add(&p->adv_gath, size_t(std::max<int64_t>(p->per, rnn_K)));  // the minibatch's (adv, active) pairs
     if (p->recurrent) {
       ar.add(&p->rnn_flat, size_t(rnn_K + rnn_Kc));  // the minibatch's slots, then one chunk's
       const int F = r->F, H = r->H;
