@@ -54,6 +54,22 @@ if what in ("policy", "all"):  # tcgen05 rollout policies: wide rows (Overcooked
         out = ro.collect()
         torch.cuda.synchronize()
         print("policy", env_id, cent, float(out["value"].sum()))
+if what in ("wide", "all"):  # the wide-input GEMM-chain update (Overcooked, fp32) and the 35-action wide policy (27m)
+    from paper_2311_10090_b200.ppo import PpoTrainer
+    from paper_2311_10090_b200.rollout import IppoRollout, orthogonal_init
+    n, T = 64, 8
+    cfg = {"n_envs": n, "n_rollout_steps": T, "total_timesteps": n * T}
+    tr = PpoTrainer(m.VectorEnv(m.make_env("overcooked_cramped_room_v0", {}), n), cfg, False, "fp32")
+    r = tr.train(O.key_from_seed(0))
+    print("wide update", r.metrics.as_array()[-1][:8])
+    v = m.VectorEnv("SMAX_27m_vs_30m", 12)
+    ro = IppoRollout(v, 3, precision="bf16")
+    a, c = orthogonal_init(0, ro.spec)
+    ro.set_params(a, c)
+    ro.begin(O.key_from_seed(1))
+    out = ro.collect()
+    torch.cuda.synchronize()
+    print("wide policy 27m", float(out["value"].sum()))
 if what in ("rnn", "all"):
     from paper_2311_10090_b200.ppo import PpoTrainer
     n, T = 256, 8
@@ -62,13 +78,14 @@ if what in ("rnn", "all"):
     r = tr.train(O.key_from_seed(0))
     print("rnn", r.metrics.as_array()[-1][:8])
 PY
-for what in probe gemm smax rnn policy; do
-  timeout 900 $CS --tool memcheck --leak-check no --error-exitcode 9 python /tmp/san_r02.py $what > gpurun_out/san_r02_memcheck_$what.log 2>&1
-  echo "memcheck $what rc=$?"; grep -E "ERROR SUMMARY" gpurun_out/san_r02_memcheck_$what.log | head -2
+TAG=${TAG:-r02}
+for what in ${MEMCHECK:-probe gemm smax rnn policy wide}; do
+  timeout 900 $CS --tool memcheck --leak-check no --error-exitcode 9 python /tmp/san_r02.py $what > gpurun_out/san_${TAG}_memcheck_$what.log 2>&1
+  echo "memcheck $what rc=$?"; grep -E "ERROR SUMMARY" gpurun_out/san_${TAG}_memcheck_$what.log | head -2
 done
-for what in probe gemm policy; do
-  timeout 900 $CS --tool racecheck --error-exitcode 9 python /tmp/san_r02.py $what > gpurun_out/san_r02_racecheck_$what.log 2>&1
-  echo "racecheck $what rc=$?"; grep -E "RACECHECK SUMMARY|ERROR SUMMARY|hazard" gpurun_out/san_r02_racecheck_$what.log | head -3
-  timeout 900 $CS --tool synccheck --error-exitcode 9 python /tmp/san_r02.py $what > gpurun_out/san_r02_synccheck_$what.log 2>&1
-  echo "synccheck $what rc=$?"; grep -E "ERROR SUMMARY" gpurun_out/san_r02_synccheck_$what.log | head -2
+for what in ${RACECHECK:-probe gemm policy wide}; do
+  timeout 900 $CS --tool racecheck --error-exitcode 9 python /tmp/san_r02.py $what > gpurun_out/san_${TAG}_racecheck_$what.log 2>&1
+  echo "racecheck $what rc=$?"; grep -E "RACECHECK SUMMARY|ERROR SUMMARY|hazard" gpurun_out/san_${TAG}_racecheck_$what.log | head -3
+  timeout 900 $CS --tool synccheck --error-exitcode 9 python /tmp/san_r02.py $what > gpurun_out/san_${TAG}_synccheck_$what.log 2>&1
+  echo "synccheck $what rc=$?"; grep -E "ERROR SUMMARY" gpurun_out/san_${TAG}_synccheck_$what.log | head -2
 done
