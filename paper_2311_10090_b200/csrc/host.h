@@ -344,7 +344,7 @@ void run_policy(marl_rollout* r, int t, bool bootstrap, int64_t seq_base);
 marl_rollout* rollout_create_impl(marl_venv* h, int T, int width, int n_layers, int relu, int centralized,
                                   int precision, int hidden);
 
-// ppo_host.cpp: row-major SGEMM / SGEMV helpers over cuBLAS
+// ppo_host.cpp: row-major GEMM helpers over the 3xTF32 tcgen05 kernel (gemm_tc.cu)
 void gemm_nt(cudaStream_t st, int64_t M, int N, int K, const float* A, int lda, const float* B, int ldb, float* C,
              int ldc, float beta);
 void gemm_nn(cudaStream_t st, int64_t M, int N, int K, const float* A, int lda, const float* B, int ldb, float* C,
