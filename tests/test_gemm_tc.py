@@ -71,3 +71,20 @@ def test_gemm_tn_split_k_deterministic(O, I, K):
     _gemm(O, I, K, D, 1, O, X, 1, I, G2, I, 0.0)
     assert torch.equal(G1, G2)
     _check(G1.cpu().numpy(), D.cpu().double().numpy().T, X.cpu().double().numpy().T, 0, 0.0)
+
+
+@pytest.mark.parametrize("O,I,ldx,K", [(128, 543, 544, 100_000), (64, 300, 300, 70_000)])
+def test_gemm_tn_split_k_wide_tiles(O, I, ldx, K):
+    """The wide update's dW1 = dZ1^T . X shape: a long K split across CTAs
+    with 128-column N tiles (several of them, the last ragged) over a padded
+    row pitch -- deterministic and within the fp32 bar."""
+    import torch
+    g = torch.Generator(device="cpu").manual_seed(O + I)
+    D = torch.randn(K, O, generator=g).cuda()
+    X = torch.randn(K, ldx, generator=g).cuda()
+    G1 = torch.zeros(O, I).cuda()
+    G2 = torch.zeros(O, I).cuda()
+    _gemm(O, I, K, D, 1, O, X, 1, ldx, G1, I, 0.0)
+    _gemm(O, I, K, D, 1, O, X, 1, ldx, G2, I, 0.0)
+    assert torch.equal(G1, G2)
+    _check(G1.cpu().numpy(), D.cpu().double().numpy().T, X[:, :I].cpu().double().numpy().T, 0, 0.0)
